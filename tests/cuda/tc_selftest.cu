@@ -1,0 +1,416 @@
+// Standalone numerics + timing check for the tcgen05 implicit-GEMM kernel.
+// Build: nvcc -std=c++17 -O2 -gencode arch=compute_100a,code=sm_100a
+//        -I paper_2101_07344_b200/csrc/kernels tests/cuda/tc_selftest.cu
+//        paper_2101_07344_b200/csrc/kernels/tc_conv.cu -o tc_selftest
+// Compares against an fp64 CPU restatement of the same convolution.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "tc_conv.cuh"
+
+using namespace lcb;
+
+#define CK(x)                                                                            \
+  do {                                                                                   \
+    cudaError_t e = (x);                                                                 \
+    if (e != cudaSuccess) {                                                              \
+      printf("CUDA error %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__);     \
+      exit(2);                                                                           \
+    }                                                                                    \
+  } while (0)
+
+static uint64_t g_state = 88172645463325252ull;
+static double urand() {
+  g_state ^= g_state << 13;
+  g_state ^= g_state >> 7;
+  g_state ^= g_state << 17;
+  return (g_state >> 11) * (1.0 / 9007199254740992.0);
+}
+
+static float bf16_round(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
+
+struct Planes {
+  std::vector<__nv_bfloat16> hi, lo;
+  std::vector<double> exact;  // value the planes represent (hi+lo or hi)
+};
+
+static Planes make_planes(const std::vector<float>& v, bool x3) {
+  Planes p;
+  p.hi.resize(v.size());
+  p.lo.resize(v.size());
+  p.exact.resize(v.size());
+  for (size_t i = 0; i < v.size(); ++i) {
+    const float h = bf16_round(v[i]);
+    const float l = bf16_round(v[i] - h);
+    p.hi[i] = __float2bfloat16_rn(h);
+    p.lo[i] = __float2bfloat16_rn(l);
+    p.exact[i] = x3 ? static_cast<double>(v[i]) : static_cast<double>(h);
+  }
+  return p;
+}
+
+template <typename T>
+static T* dev_copy(const std::vector<T>& h) {
+  T* d = nullptr;
+  CK(cudaMalloc(&d, h.size() * sizeof(T) + 256));
+  CK(cudaMemcpy(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return d;
+}
+
+static int g_sms = 148;
+static int g_fail = 0;
+
+static void report(const char* name, double max_rel, double tol) {
+  const bool ok = max_rel <= tol;
+  if (!ok) g_fail++;
+  printf("%-48s max_rel=%.3e tol=%.1e %s\n", name, max_rel, tol, ok ? "PASS" : "FAIL");
+}
+
+// Conv test: input NHWC [N,H,W,C], 3x3 (or 1x1) stride s, pad k/2; output [N,Ho,Wo,Cout].
+static void conv_test(const char* name, int N, int H, int W, int C, int Cout, int k, int stride, bool x3,
+                      bool use_res, bool relu, bool use_surv, int BNforce = 0) {
+  const int pad = k / 2;
+  const int Ho = (H + 2 * pad - k) / stride + 1, Wo = (W + 2 * pad - k) / stride + 1;
+  std::vector<float> x(static_cast<size_t>(N) * H * W * C), wt(static_cast<size_t>(Cout) * k * k * C);
+  for (auto& v : x) v = static_cast<float>(urand() * 2 - 1);
+  for (auto& v : wt) v = static_cast<float>((urand() * 2 - 1) * 0.1);
+  std::vector<float> scale(Cout), shift(Cout);
+  for (int i = 0; i < Cout; ++i) {
+    scale[i] = static_cast<float>(0.5 + urand());
+    shift[i] = static_cast<float>(urand() - 0.5);
+  }
+  std::vector<float> res(static_cast<size_t>(N) * Ho * Wo * Cout);
+  for (auto& v : res) v = static_cast<float>(urand() - 0.5);
+
+  // Phase split for stride 2: P = 4 phase images of [N, Hp, Wp, C].
+  int P = 1, Hs = H, Ws = W;
+  std::vector<float> src = x;
+  if (stride == 2) {
+    P = 4;
+    Hs = (H + 1) / 2;
+    Ws = (W + 1) / 2;
+    src.assign(static_cast<size_t>(4) * N * Hs * Ws * C, 0.f);
+    for (int ph = 0; ph < 2; ++ph)
+      for (int pw = 0; pw < 2; ++pw)
+        for (int n = 0; n < N; ++n)
+          for (int i = 0; i < Hs; ++i)
+            for (int j = 0; j < Ws; ++j) {
+              const int h = 2 * i + ph, w = 2 * j + pw;
+              if (h >= H || w >= W) continue;
+              for (int c = 0; c < C; ++c)
+                src[((((size_t)(ph * 2 + pw) * N + n) * Hs + i) * Ws + j) * C + c] =
+                    x[(((size_t)n * H + h) * W + w) * C + c];
+            }
+  }
+  Planes ps = make_planes(src, x3), pw_ = make_planes(wt, x3), pr = make_planes(res, x3);
+  // CPU reference on the planes' exact values.
+  Planes px = make_planes(x, x3);
+  std::vector<double> ref(static_cast<size_t>(N) * Ho * Wo * Cout);
+  for (int n = 0; n < N; ++n)
+    for (int oh = 0; oh < Ho; ++oh)
+      for (int ow = 0; ow < Wo; ++ow)
+        for (int co = 0; co < Cout; ++co) {
+          double acc = 0;
+          for (int r = 0; r < k; ++r)
+            for (int s = 0; s < k; ++s) {
+              const int ih = oh * stride + r - pad, iw = ow * stride + s - pad;
+              if (ih < 0 || ih >= H || iw < 0 || iw >= W) continue;
+              const double* xr = &px.exact[(((size_t)n * H + ih) * W + iw) * C];
+              const double* wr = &pw_.exact[((size_t)co * k * k + r * k + s) * C];
+              for (int c = 0; c < C; ++c) acc += xr[c] * wr[c];
+            }
+          double v = acc * scale[co] + shift[co];
+          const size_t oi = (((size_t)n * Ho + oh) * Wo + ow) * Cout + co;
+          if (use_res) v += pr.exact[oi];
+          if (relu) v = v > 0 ? v : 0;
+          ref[oi] = v;
+        }
+
+  auto* dA_hi = dev_copy(ps.hi);
+  auto* dA_lo = dev_copy(ps.lo);
+  auto* dW_hi = dev_copy(pw_.hi);
+  auto* dW_lo = dev_copy(pw_.lo);
+  auto* dR_hi = dev_copy(pr.hi);
+  auto* dR_lo = dev_copy(pr.lo);
+  auto* dScale = dev_copy(scale);
+  auto* dShift = dev_copy(shift);
+  __nv_bfloat16 *dO_hi, *dO_lo;
+  const size_t on = static_cast<size_t>(N) * Ho * Wo * Cout;
+  CK(cudaMalloc(&dO_hi, on * 2));
+  CK(cudaMalloc(&dO_lo, on * 2));
+  CK(cudaMemset(dO_hi, 0, on * 2));
+  CK(cudaMemset(dO_lo, 0, on * 2));
+
+  // Survivors: every other image in reverse order when requested.
+  std::vector<int> surv;
+  for (int n = N - 1; n >= 0; n -= (use_surv ? 2 : 1)) surv.push_back(n);
+  if (!use_surv) {
+    surv.clear();
+    for (int n = 0; n < N; ++n) surv.push_back(n);
+  }
+  int* dSurv = dev_copy(surv);
+  std::vector<int> cnt = {static_cast<int>(surv.size())};
+  int* dCnt = dev_copy(cnt);
+
+  TcConvParams p;
+  memset(&p, 0, sizeof(p));
+  // Box geometry.
+  int hb, wb, ipt;
+  const int pix = Ho * Wo;
+  if (pix >= 128) {
+    wb = Wo >= 128 ? 128 : Wo;
+    // round wb up to a power of two for partial widths
+    int w2 = 1;
+    while (w2 < wb) w2 <<= 1;
+    wb = w2 > 128 ? 128 : w2;
+    hb = 128 / wb;
+    ipt = 1;
+  } else {
+    int w2 = 1;
+    while (w2 < Wo) w2 <<= 1;
+    int h2 = 1;
+    while (h2 < Ho) h2 <<= 1;
+    wb = w2;
+    hb = h2;
+    ipt = 128 / (hb * wb);
+  }
+  p.plain = 0;
+  p.Ho = Ho;
+  p.Wo = Wo;
+  p.hb = hb;
+  p.wb = wb;
+  p.ipt = ipt;
+  p.tiles_h = (Ho + hb - 1) / hb;
+  p.tiles_w = (Wo + wb - 1) / wb;
+  p.C = C;
+  p.ntaps = k * k;
+  p.segs = x3 ? 3 : 1;
+  p.Cout = Cout;
+  p.ksplit = 1;
+  p.surv = dSurv;
+  p.count = dCnt;
+  p.count_static = static_cast<int>(surv.size());
+  p.mode = 0;
+  p.scale = dScale;
+  p.shift = dShift;
+  p.res_hi = use_res ? dR_hi : nullptr;
+  p.res_lo = use_res && x3 ? dR_lo : nullptr;
+  p.relu = relu;
+  p.out_hi = dO_hi;
+  p.out_lo = x3 ? dO_lo : nullptr;
+  for (int r = 0; r < k; ++r)
+    for (int s = 0; s < k; ++s) {
+      const int t = r * k + s;
+      if (stride == 1) {
+        p.tap_phase[t] = 0;
+        p.tap_dh[t] = static_cast<signed char>(r - pad);
+        p.tap_dw[t] = static_cast<signed char>(s - pad);
+      } else {
+        // input row 2*oh + r - pad = 2*(oh + dh) + phase_h
+        const int oh_off = r - pad;  // in [-pad, k-1-pad]
+        const int ph = ((oh_off % 2) + 2) % 2, dh = (oh_off - ph) / 2;
+        const int ow_off = s - pad;
+        const int pw2 = ((ow_off % 2) + 2) % 2, dw = (ow_off - pw2) / 2;
+        p.tap_phase[t] = static_cast<signed char>(ph * 2 + pw2);
+        p.tap_dh[t] = static_cast<signed char>(dh);
+        p.tap_dw[t] = static_cast<signed char>(dw);
+      }
+    }
+  const int BN = BNforce ? BNforce : tc_conv_pick_bn(Cout);
+  bool ok = encode_act_map(&p.tmA[0], dA_hi, C, Ws, Hs, N, P, wb, hb) &&
+            encode_act_map(&p.tmA[1], dA_lo, C, Ws, Hs, N, P, wb, hb) &&
+            encode_weight_map(&p.tmB[0], dW_hi, k * k * C, Cout, BN) &&
+            encode_weight_map(&p.tmB[1], dW_lo, k * k * C, Cout, BN);
+  if (!ok) {
+    printf("%s: tensor map encode failed\n", name);
+    g_fail++;
+    return;
+  }
+  CK(tc_conv_launch(p, BN, g_sms, 0));
+  CK(cudaDeviceSynchronize());
+  std::vector<__nv_bfloat16> oh(on), ol(on);
+  CK(cudaMemcpy(oh.data(), dO_hi, on * 2, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(ol.data(), dO_lo, on * 2, cudaMemcpyDeviceToHost));
+  double max_rel = 0;
+  std::vector<char> is_surv(N, 0);
+  for (int n : surv) is_surv[n] = 1;
+  long bad_unwritten = 0;
+  for (int n = 0; n < N; ++n)
+    for (size_t i = 0; i < static_cast<size_t>(Ho) * Wo * Cout; ++i) {
+      const size_t oi = static_cast<size_t>(n) * Ho * Wo * Cout + i;
+      double got = __bfloat162float(oh[oi]) + (x3 ? __bfloat162float(ol[oi]) : 0.0);
+      if (!is_surv[n]) {
+        if (got != 0.0) bad_unwritten++;
+        continue;
+      }
+      const double d = fabs(got - ref[oi]) / std::max(1.0, fabs(ref[oi]));
+      if (d > max_rel) max_rel = d;
+    }
+  char label[160];
+  snprintf(label, sizeof label, "%s BN=%d hb=%d wb=%d ipt=%d", name, BN, hb, wb, ipt);
+  // bf16 output rounding dominates in plain mode (2^-8); x3 keeps hi+lo (~2^-16).
+  report(label, max_rel + (bad_unwritten ? 1.0 : 0.0), x3 ? 2e-4 : 1.2e-2);
+  cudaFree(dA_hi);
+  cudaFree(dA_lo);
+  cudaFree(dW_hi);
+  cudaFree(dW_lo);
+  cudaFree(dR_hi);
+  cudaFree(dR_lo);
+  cudaFree(dO_hi);
+  cudaFree(dO_lo);
+  cudaFree(dScale);
+  cudaFree(dShift);
+  cudaFree(dSurv);
+  cudaFree(dCnt);
+}
+
+// Plain GEMM rows x K times [Cout, K]^T with split-K fp32 partials.
+static void gemm_test(const char* name, int M, int K, int Cout, bool x3, int ksplit) {
+  std::vector<float> a(static_cast<size_t>(M) * K), b(static_cast<size_t>(Cout) * K);
+  for (auto& v : a) v = static_cast<float>(urand() * 2 - 1);
+  for (auto& v : b) v = static_cast<float>((urand() * 2 - 1) * 0.05);
+  Planes pa = make_planes(a, x3), pb = make_planes(b, x3);
+  auto* dA_hi = dev_copy(pa.hi);
+  auto* dA_lo = dev_copy(pa.lo);
+  auto* dB_hi = dev_copy(pb.hi);
+  auto* dB_lo = dev_copy(pb.lo);
+  float* dOut;
+  CK(cudaMalloc(&dOut, static_cast<size_t>(ksplit) * M * Cout * 4));
+  std::vector<int> cnt = {M};
+  int* dCnt = dev_copy(cnt);
+  TcConvParams p;
+  memset(&p, 0, sizeof(p));
+  p.plain = 1;
+  p.Ho = 1;
+  p.Wo = M;
+  p.hb = 1;
+  p.wb = 128;
+  p.ipt = 1;
+  p.tiles_h = 1;
+  p.C = K;
+  p.ntaps = 1;
+  p.segs = x3 ? 3 : 1;
+  p.Cout = Cout;
+  p.ksplit = ksplit;
+  p.count = dCnt;
+  p.count_static = M;
+  p.mode = 1;
+  p.rows_total = M;
+  p.out_f32 = dOut;
+  const int BN = tc_conv_pick_bn(Cout);
+  bool ok = encode_act_map(&p.tmA[0], dA_hi, K, M, 1, 1, 1, 128, 1) &&
+            encode_act_map(&p.tmA[1], dA_lo, K, M, 1, 1, 1, 128, 1) &&
+            encode_weight_map(&p.tmB[0], dB_hi, K, Cout, BN) && encode_weight_map(&p.tmB[1], dB_lo, K, Cout, BN);
+  if (!ok) {
+    printf("%s: encode failed\n", name);
+    g_fail++;
+    return;
+  }
+  CK(tc_conv_launch(p, BN, g_sms, 0));
+  CK(cudaDeviceSynchronize());
+  std::vector<float> out(static_cast<size_t>(ksplit) * M * Cout);
+  CK(cudaMemcpy(out.data(), dOut, out.size() * 4, cudaMemcpyDeviceToHost));
+  double max_rel = 0;
+  for (int m = 0; m < M; ++m)
+    for (int n = 0; n < Cout; ++n) {
+      double ref = 0, scale = 0;
+      for (int k = 0; k < K; ++k) {
+        ref += pa.exact[(size_t)m * K + k] * pb.exact[(size_t)n * K + k];
+        scale += fabs(pa.exact[(size_t)m * K + k] * pb.exact[(size_t)n * K + k]);
+      }
+      double got = 0;
+      for (int s = 0; s < ksplit; ++s) got += out[((size_t)s * M + m) * Cout + n];
+      const double d = fabs(got - ref) / std::max(1e-3, scale);
+      if (d > max_rel) max_rel = d;
+    }
+  char label[160];
+  snprintf(label, sizeof label, "%s M=%d K=%d N=%d ks=%d BN=%d", name, M, K, Cout, ksplit, BN);
+  report(label, max_rel, x3 ? 1e-5 : 1e-5);
+  cudaFree(dA_hi);
+  cudaFree(dA_lo);
+  cudaFree(dB_hi);
+  cudaFree(dB_lo);
+  cudaFree(dOut);
+  cudaFree(dCnt);
+}
+
+static void perf_test(int M, int K, int Cout) {
+  __nv_bfloat16 *dA, *dB;
+  float* dOut;
+  CK(cudaMalloc(&dA, (size_t)M * K * 2));
+  CK(cudaMalloc(&dB, (size_t)Cout * K * 2));
+  CK(cudaMalloc(&dOut, (size_t)M * Cout * 4));
+  CK(cudaMemset(dA, 0, (size_t)M * K * 2));
+  CK(cudaMemset(dB, 0, (size_t)Cout * K * 2));
+  TcConvParams p;
+  memset(&p, 0, sizeof(p));
+  p.plain = 1;
+  p.Ho = 1;
+  p.Wo = M;
+  p.hb = 1;
+  p.wb = 128;
+  p.ipt = 1;
+  p.tiles_h = 1;
+  p.C = K;
+  p.ntaps = 1;
+  p.segs = 1;
+  p.Cout = Cout;
+  p.ksplit = 1;
+  p.count_static = M;
+  p.mode = 1;
+  p.rows_total = M;
+  p.out_f32 = dOut;
+  const int BN = 256;
+  encode_act_map(&p.tmA[0], dA, K, M, 1, 1, 1, 128, 1);
+  encode_weight_map(&p.tmB[0], dB, K, Cout, BN);
+  for (int i = 0; i < 3; ++i) CK(tc_conv_launch(p, BN, g_sms, 0));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  const int iters = 20;
+  for (int i = 0; i < iters; ++i) tc_conv_launch(p, BN, g_sms, 0);
+  cudaEventRecord(e1);
+  CK(cudaEventSynchronize(e1));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  ms /= iters;
+  const double tf = 2.0 * M * K * Cout / (ms * 1e-3) / 1e12;
+  printf("perf plain bf16 GEMM %dx%dx%d BN=%d: %.3f ms  %.1f TFLOP/s\n", M, K, Cout, BN, ms, tf);
+  cudaFree(dA);
+  cudaFree(dB);
+  cudaFree(dOut);
+}
+
+int main(int argc, char** argv) {
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, 0));
+  g_sms = prop.multiProcessorCount;
+  printf("device %s, %d SMs\n", prop.name, g_sms);
+  gemm_test("gemm bf16", 300, 192, 128, false, 1);
+  gemm_test("gemm x3", 300, 192, 128, true, 1);
+  gemm_test("gemm x3 splitk", 256, 4096, 256, true, 8);
+  gemm_test("gemm bf16 N64", 130, 128, 64, false, 1);
+  conv_test("conv3x3 s1 32x32 x3", 2, 32, 32, 64, 64, 3, 1, true, true, true, false);
+  conv_test("conv3x3 s1 32x32 bf16", 2, 32, 32, 64, 128, 3, 1, false, false, true, false);
+  conv_test("conv3x3 s1 16x16 x3 surv", 5, 16, 16, 128, 128, 3, 1, true, true, true, true);
+  conv_test("conv3x3 s1 8x8 x3 surv", 7, 8, 8, 64, 256, 3, 1, true, false, true, true, 256);
+  conv_test("conv3x3 s1 4x4 x3 surv", 19, 4, 4, 128, 512, 3, 1, true, true, true, true);
+  conv_test("conv3x3 s2 32->16 x3", 3, 32, 32, 64, 128, 3, 2, true, false, true, false);
+  conv_test("conv1x1 s2 16->8 x3", 5, 16, 16, 128, 256, 1, 2, true, false, false, true);
+  conv_test("conv3x3 s1 7x7 x3", 5, 7, 7, 64, 128, 3, 1, true, true, true, false);
+  conv_test("conv3x3 s1 14x14 bf16", 3, 14, 14, 64, 64, 3, 1, false, true, true, false);
+  conv_test("conv1x1 s1 56x56 x3", 2, 56, 56, 64, 256, 1, 1, true, true, false, false);
+  if (argc > 1 && strcmp(argv[1], "--perf") == 0) {
+    perf_test(8192, 8192, 8192);
+    perf_test(16384, 4096, 4096);
+  }
+  printf("%s (%d failures)\n", g_fail ? "SELFTEST FAILED" : "SELFTEST OK", g_fail);
+  return g_fail ? 1 : 0;
+}
