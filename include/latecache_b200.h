@@ -1,0 +1,166 @@
+/* latecache-b200: C-ABI boundary of the B200-native learned-cache serve path.
+ *
+ * The reference (latecache, /root/reference/proj) exposes this path only as a
+ * C++ library API in namespace latecache. Each entry point
+ * below replaces one reference interface; the cited file:line is the
+ * function it stands in for. Plain pointers and sizes only; all handles are
+ * opaque. Every function returns LC_OK or an error code, with a message in
+ * lc_last_error() (thread-local). Codes map 1:1 onto the reference's
+ * exception types: LC_ERR_INVALID_ARGUMENT = std::invalid_argument,
+ * LC_ERR_RUNTIME = std::runtime_error (malformed artifacts),
+ * LC_ERR_INFEASIBLE_PLAN = the invalid_argument simulate_model throws for a
+ * plan that fails check_constraints (serving.cpp:23-29), LC_ERR_CUDA = device
+ * failure. There is no CPU fallback: engine calls fail with LC_ERR_CUDA when
+ * no sm_100 device is present.
+ */
+#ifndef LATECACHE_B200_H
+#define LATECACHE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define LC_API __attribute__((visibility("default")))
+#else
+#define LC_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#pragma GCC visibility push(default)
+#endif
+
+#define LC_OK 0
+#define LC_ERR_INVALID_ARGUMENT 1
+#define LC_ERR_RUNTIME 2
+#define LC_ERR_INFEASIBLE_PLAN 3
+#define LC_ERR_CUDA 4
+
+/* Precision tiers of the tensor-core contractions. */
+#define LC_PREC_BF16X3 0 /* hi/lo bf16 split, fp32-class: the parity tier */
+#define LC_PREC_BF16 1   /* plain bf16 operands, fp32 accumulate */
+
+/* lc_serve_* flags */
+#define LC_SERVE_SHADOW 1u   /* no compaction: every request runs full depth (base_pred for all) */
+#define LC_SERVE_NO_GRAPH 2u /* launch kernels directly instead of replaying the CUDA graph */
+
+typedef struct lc_model lc_model;     /* latecache::BaseModel   (base_model.hpp:31-39) */
+typedef struct lc_variant lc_variant; /* latecache::CacheVariant (cache.hpp:57-64) */
+typedef struct lc_engine lc_engine;   /* latecache::Deployment   (serving.hpp:61-69), resident on one GPU */
+
+const char* lc_last_error(void);
+const char* lc_version(void);
+void lc_free(void* p); /* frees strings returned by the *_save functions */
+
+/* ------------------------------------------------------------ base models */
+/* make_base_model (base_model.cpp:30-54) */
+int lc_model_make_mlp(int input_dim, int num_classes, const int* widths, int n_widths, int blocks, uint64_t seed,
+                      lc_model** out);
+/* load_base_model (base_model.cpp:156-175), "latecache-model v1" text */
+int lc_model_load(const char* text, size_t len, lc_model** out);
+/* save_base_model (base_model.cpp:143-154) */
+int lc_model_save(const lc_model* m, char** text, size_t* len);
+/* CNN families of BASELINE.json (no reference counterpart): "resnet18_cifar",
+ * "resnet50", "resnet152", "vgg16_cifar"; synthetic weights from `seed`. */
+int lc_model_make_cnn(const char* arch, int num_classes, uint64_t seed, lc_model** out);
+int lc_model_info(const lc_model* m, int* blocks, int* classes, long long* input_dim);
+/* Tap geometry of block `layer` (1-based), NCHW: dim = C*H*W (mlp: C = width, H = W = 1). */
+int lc_model_tap(const lc_model* m, int layer, int* C, int* H, int* W);
+/* Base multiply-accumulates per request up to and including `block` (0 = none, blocks = full). */
+long long lc_model_macs(const lc_model* m, int block);
+void lc_model_free(lc_model* m);
+
+/* CNN op list (for the CPU oracle's restatement of the same network). */
+typedef struct {
+  int kind; /* 0 stem conv, 1 conv, 2 max-pool, 3 GAP + FC head */
+  int in, out, res; /* activation slots (-1 = network input / none) */
+  int C, H, W, Cout, k, stride, pad, relu, tap;
+  const double* w; /* conv OIHW [Cout][C][k][k]; head [classes][C] */
+  long long w_len;
+  const double* scale; /* folded batch-norm, per Cout (conv) */
+  const double* shift; /* folded batch-norm shift (conv) / head bias */
+} lc_cnn_op_desc;
+int lc_model_cnn_ops(const lc_model* m, int* n_ops, int* n_slots);
+int lc_model_cnn_op(const lc_model* m, int i, lc_cnn_op_desc* out);
+
+/* ------------------------------------------------------------ cache variants */
+/* build_variant (cache.cpp:104-140); arch = "FC(h)" | "Pool(w)" | "Conv(k,s)" (ArchSpec::parse, cache.cpp:80-97) */
+int lc_variant_build(int layer, int variant_idx, const char* arch, long long tap_dim, int num_classes, uint64_t seed,
+                     lc_variant** out);
+/* load_variant / save_variant (cache.cpp:464-489 / :452-462), "latecache-variant v1" text */
+int lc_variant_load(const char* text, size_t len, lc_variant** out);
+int lc_variant_save(const lc_variant* v, char** text, size_t* len);
+/* CacheVariant::delta (cache.hpp:63) */
+int lc_variant_set_delta(lc_variant* v, double delta);
+int lc_variant_info(const lc_variant* v, int* layer, int* variant_idx, double* delta, char* arch, int arch_len);
+/* predictor_macs + selector_macs (cache.cpp:307-308) */
+long long lc_variant_macs(const lc_variant* v);
+/* Layer `idx` of the predictor (which = 0) or selector (which = 1): kind as
+ * network.hpp:14 (0 FC, 1 ReLU, 2 AvgPool, 3 Conv1d, 4 Softmax) and borrowed
+ * weight pointers (valid while the variant lives). Returns LC_ERR_INVALID_ARGUMENT past the end. */
+int lc_variant_layer(const lc_variant* v, int which, int idx, int* kind, int* in_dim, int* out_dim, int* pool_window,
+                     int* kernel, int* stride, const double** w, long long* w_len, const double** b, long long* b_len);
+/* force_selector (test_serving.cpp:123-129) generalised: selector output weights *= gain, final bias = bias. */
+int lc_variant_set_selector_out(lc_variant* v, double gain, double bias);
+void lc_variant_free(lc_variant* v);
+
+/* ------------------------------------------------------------ plan checks */
+/* load_metrics + load_plan + check_constraints (cache.cpp:424-450, composer.cpp:330-365, :128-160).
+ * profile_ms[blocks]. *feasible = 1/0; *report (nullable, free with lc_free) = violations, one per line.
+ * Plan-file choices are written to chosen_layers/chosen_variants (capacity cap, count in *n_chosen). */
+int lc_plan_check(const char* metrics_text, const char* plan_text, const double* profile_ms, int blocks,
+                  double accuracy_threshold, double memory_budget_mb, int* feasible, int* chosen_layers,
+                  int* chosen_variants, int cap, int* n_chosen, char** report);
+
+/* ------------------------------------------------------------ workload / summary */
+/* gen_workload (serving.cpp:61-91) over per-sample labels of the test split. */
+int lc_gen_workload(int num_classes, double zipf_alpha, double rotation_period_min, double requests_per_sec,
+                    double duration_min, uint64_t seed, const int* labels, long long n_labels, int dataset_classes,
+                    long long* n_out, long long* sample_idx, int* true_class, double* time_min, long long cap);
+/* Nearest-rank percentile (serving.cpp:361-365). */
+double lc_nearest_rank(const double* v, long long n, double q);
+
+/* ------------------------------------------------------------ engine */
+/* Deployment on `device`: the base model plus the plan's chosen variants
+ * (any order; probed in ascending layer; at most one per layer, as
+ * make_plan, composer.cpp:65-89). Weights are copied to HBM. */
+int lc_engine_create(int device, const lc_model* m, const lc_variant* const* variants, int n_variants, int precision,
+                     int max_batch, lc_engine** out);
+int lc_engine_destroy(lc_engine* e);
+int lc_engine_set_delta(lc_engine* e, int layer, double delta);
+int lc_engine_set_selector_out(lc_engine* e, int layer, double gain, double bias);
+/* Device input buffer [max_batch][input_dim] fp32 (images: NCHW). */
+int lc_engine_input(lc_engine* e, float** device_ptr);
+
+/* simulate_model -> serve_one (serving.cpp:97-158) for one batch of B requests,
+ * end to end from HOST buffers: inputs [B][input_dim] fp32 in; per request
+ * exit_layer (0 = miss, served by the base model), served label, base label
+ * (-1 where compaction skipped the full pass), selector probability per
+ * probed layer probs [blocks][B] (NaN = not probed), device-timed latency
+ * (ms from batch start to the request's exit). Output pointers are nullable. */
+int lc_serve_batch(lc_engine* e, const float* inputs, int B, unsigned flags, int* exit_layer, int* served,
+                   int* base_pred, float* probs, double* latency_ms);
+/* Same, input already in lc_engine_input(); enqueued asynchronously. */
+int lc_serve_device(lc_engine* e, int B, unsigned flags);
+int lc_engine_sync(lc_engine* e);
+int lc_engine_results(lc_engine* e, int B, int* exit_layer, int* served, int* base_pred, float* probs,
+                      double* latency_ms);
+/* Surviving requests after each block: counts[0..blocks] (counts[0] = B). */
+int lc_engine_counts(lc_engine* e, int* counts);
+
+/* lookup (cache.cpp:259-265) batched: taps [B][tap_dim] fp32 NCHW-flat (host);
+ * hit[B], label = argmax(pr) [B], prob = selector probability [B],
+ * pr [B][classes], logits [B][classes] (nullable). */
+int lc_lookup_batch(lc_engine* e, int layer, const float* taps, int B, int* hit, int* label, float* prob, float* pr,
+                    float* logits);
+
+/* Device time of `iters` graph replays of a B-request batch (CUDA events on the engine stream). */
+int lc_engine_time(lc_engine* e, int B, unsigned flags, int iters, double* ms_per_batch);
+/* Kernel launches per batch of the given kind (-1 all, 1 tensor-core, 2 lookup, 3 exit/compaction). */
+int lc_engine_kernel_count(lc_engine* e, unsigned flags, int kind);
+
+#ifdef __cplusplus
+#pragma GCC visibility pop
+}
+#endif
+#endif

@@ -181,6 +181,16 @@ int ref_variant_force_selector(void* vp, double bias) {
   return 0;
 }
 
+// Selector output layer *= gain, final bias = bias (calibrated synthetic
+// deployments; mirrors lc_variant_set_selector_out in the product).
+int ref_variant_set_selector_out(void* vp, double gain, double bias) {
+  CacheVariant& v = *static_cast<CacheVariant*>(vp);
+  LayerWeights& lw = v.selector.weights.back();
+  for (double& w : lw.w.data) w *= gain;
+  lw.b.data.back() = bias;
+  return 0;
+}
+
 // Selector logit, the input to sigmoid in lookup (cache.cpp:262).
 int ref_selector_logit(void* vp, const double* tap, int D, double* logit) {
   return guard([&] {

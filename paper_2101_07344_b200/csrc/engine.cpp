@@ -1,0 +1,922 @@
+// Device engine implementation (see engine.hpp).
+#include "engine.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <string>
+
+namespace lcb {
+
+namespace {
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaFailure(std::string(what) + ": " + cudaGetErrorString(e));
+}
+void require(bool ok, const std::string& msg) {
+  if (!ok) throw std::invalid_argument(msg);
+}
+int round_up(long long v, int m) { return static_cast<int>((v + m - 1) / m * m); }
+
+// A tile covers 128 output pixels: ipt images x (hb x wb) boxes. Boxes are a
+// multiple of 8 rows so every box starts 1024-byte aligned in shared memory
+// (the 128-byte swizzle atom).
+void choose_box(int Ho, int Wo, int& hb, int& wb, int& ipt) {
+  int w2 = 1;
+  while (w2 < Wo) w2 <<= 1;
+  int h2 = 1;
+  while (h2 < Ho) h2 <<= 1;
+  if (w2 > 128) w2 = 128;
+  if (h2 * w2 <= 128) {
+    hb = h2;
+    wb = w2;
+    while (hb * wb < 8) wb <<= 1;
+    ipt = 128 / (hb * wb);
+  } else {
+    wb = w2;
+    hb = 128 / wb;
+    ipt = 1;
+  }
+}
+
+void split_planes(const std::vector<float>& v, std::vector<__nv_bfloat16>& hi, std::vector<__nv_bfloat16>& lo) {
+  hi.resize(v.size());
+  lo.resize(v.size());
+  for (size_t i = 0; i < v.size(); ++i) {
+    const __nv_bfloat16 h = __float2bfloat16_rn(v[i]);
+    hi[i] = h;
+    lo[i] = __float2bfloat16_rn(v[i] - __bfloat162float(h));
+  }
+}
+
+std::vector<float> to_f32(const std::vector<double>& v) { return std::vector<float>(v.begin(), v.end()); }
+
+}  // namespace
+
+struct DevCache {
+  int layer = 0, family = 0, classes = 0;
+  long long D = 0;
+  // pool
+  int width = 0, win = 1;
+  // conv
+  int kernel = 0, stride = 0, out_dim = 0, chunk_elems = 0, nchunks = 0;
+  float* w1 = nullptr;
+  float b1c = 0.0f;
+  // fc
+  int h = 0, hp = 0, ks = 1, Dk = 0;
+  Planes W1;
+  float* b1 = nullptr;
+  Planes gather;
+  // shared
+  float* W2 = nullptr;
+  float* b2 = nullptr;
+  float* Ws1 = nullptr;
+  float* bs1 = nullptr;
+  float* ws2 = nullptr;
+  float bs2 = 0.0f;
+  double delta = 0.5;
+  // scratch / outputs (row-indexed)
+  float* feats = nullptr;
+  int* hit = nullptr;
+  int* label = nullptr;
+  float* prob = nullptr;
+  float* pr_out = nullptr;
+  float* logits_out = nullptr;
+  // lookup-only step list
+  std::vector<Step> lookup_steps;
+};
+
+// ------------------------------------------------------------------ memory
+void* Engine::dalloc(size_t bytes) {
+  void* p = nullptr;
+  ck(cudaMalloc(&p, bytes < 256 ? 256 : bytes), "cudaMalloc");
+  allocs_.push_back(p);
+  return p;
+}
+Planes Engine::alloc_planes(size_t elems) {
+  Planes p;
+  p.elems = elems;
+  p.hi = static_cast<__nv_bfloat16*>(dalloc(elems * 2));
+  ck(cudaMemsetAsync(p.hi, 0, elems * 2, stream_), "memset");
+  if (prec_ == kPrecX3) {
+    p.lo = static_cast<__nv_bfloat16*>(dalloc(elems * 2));
+    ck(cudaMemsetAsync(p.lo, 0, elems * 2, stream_), "memset");
+  }
+  return p;
+}
+Planes Engine::upload_planes(const std::vector<float>& v) {
+  Planes p = alloc_planes(v.size());
+  std::vector<__nv_bfloat16> hi, lo;
+  split_planes(v, hi, lo);
+  ck(cudaMemcpy(p.hi, hi.data(), v.size() * 2, cudaMemcpyHostToDevice), "upload");
+  if (p.lo) ck(cudaMemcpy(p.lo, lo.data(), v.size() * 2, cudaMemcpyHostToDevice), "upload");
+  return p;
+}
+float* Engine::upload_f32(const std::vector<float>& v) {
+  float* p = static_cast<float*>(dalloc(v.size() * sizeof(float)));
+  ck(cudaMemcpy(p, v.data(), v.size() * sizeof(float), cudaMemcpyHostToDevice), "upload");
+  return p;
+}
+
+// ------------------------------------------------------------------ build
+Engine::Engine(int device, const BaseModel& model, std::vector<CacheVariant> variants, Precision prec, int max_batch)
+    : device_(device), prec_(prec), max_batch_(max_batch), model_(model), variants_(std::move(variants)) {
+  require(max_batch > 0, "engine: max_batch must be positive");
+  require(model_.num_blocks > 0, "engine: empty base model");
+  int ndev = 0;
+  ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+  require(device >= 0 && device < ndev, "engine: device index out of range");
+  ck(cudaSetDevice(device), "cudaSetDevice");
+  cudaDeviceProp prop;
+  ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+  require(prop.major == 10, "engine: requires an sm_100 (B200) device");
+  num_sms_ = prop.multiProcessorCount;
+  ck(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+  ck(cudaEventCreate(&ev0_), "event");
+  ck(cudaEventCreate(&ev1_), "event");
+
+  // make_plan semantics (composer.cpp:65-89): probe order = ascending layer,
+  // at most one variant per layer.
+  std::stable_sort(variants_.begin(), variants_.end(),
+                   [](const CacheVariant& a, const CacheVariant& b) { return a.layer < b.layer; });
+  for (size_t k = 1; k < variants_.size(); ++k)
+    require(variants_[k - 1].layer != variants_[k].layer,
+            "plan: more than one variant at layer " + std::to_string(variants_[k].layer));
+  cache_of_layer_.assign(static_cast<size_t>(model_.num_blocks) + 1, -1);
+  for (size_t k = 0; k < variants_.size(); ++k) {
+    const CacheVariant& v = variants_[k];
+    require(v.layer >= 1 && v.layer <= model_.num_blocks,
+            "simulate: variant layer " + std::to_string(v.layer) + " outside the model");
+    require(v.predictor.input_dim() == model_.tap_dim(v.layer),
+            "forward: input dim " + std::to_string(model_.tap_dim(v.layer)) + " != expected " +
+                std::to_string(v.predictor.input_dim()));
+    require(v.predictor.output_dim() == model_.num_classes && v.selector.input_dim() == model_.num_classes,
+            "engine: variant class count does not match the base model");
+    cache_of_layer_[static_cast<size_t>(v.layer)] = static_cast<int>(k);
+  }
+  build_weights();
+  ck(cudaStreamSynchronize(stream_), "build");
+}
+
+Engine::~Engine() {
+  if (stream_) cudaStreamSynchronize(stream_);
+  for (auto& g : graph_)
+    if (g) cudaGraphExecDestroy(g);
+  for (void* p : allocs_) cudaFree(p);
+  if (h_batch_) cudaFreeHost(h_batch_);
+  if (ev0_) cudaEventDestroy(ev0_);
+  if (ev1_) cudaEventDestroy(ev1_);
+  if (stream_) cudaStreamDestroy(stream_);
+}
+
+void Engine::build_weights() {
+  const int L = model_.num_blocks;
+  const int B = max_batch_;
+  // batch state
+  d_x_ = static_cast<float*>(dalloc(static_cast<size_t>(B) * model_.input_dim() * sizeof(float)));
+  d_batch_ = static_cast<int*>(dalloc(sizeof(int)));
+  ck(cudaMallocHost(&h_batch_, sizeof(int)), "cudaMallocHost");
+  d_ids_ = static_cast<int*>(dalloc(static_cast<size_t>(L + 1) * B * sizeof(int)));
+  d_src_ = static_cast<int*>(dalloc(static_cast<size_t>(L + 1) * B * sizeof(int)));
+  d_counts_ = static_cast<int*>(dalloc(static_cast<size_t>(L + 2) * sizeof(int)));
+  d_exit_ = static_cast<int*>(dalloc(static_cast<size_t>(B) * sizeof(int)));
+  d_served_ = static_cast<int*>(dalloc(static_cast<size_t>(B) * sizeof(int)));
+  d_base_ = static_cast<int*>(dalloc(static_cast<size_t>(B) * sizeof(int)));
+  d_exit_ns_ = static_cast<unsigned long long*>(dalloc(static_cast<size_t>(B) * 8));
+  d_t0_ = static_cast<unsigned long long*>(dalloc(8));
+  d_probs_ = static_cast<float*>(dalloc(static_cast<size_t>(L) * B * sizeof(float)));
+  d_lk_count_ = static_cast<int*>(dalloc(sizeof(int)));
+
+  // ---------------- base model
+  long long max_tap_storage = 0;
+  if (model_.family == "mlp") {
+    const Network& net = model_.net;
+    for (int b = 0; b < L; ++b) {
+      const LayerSpec& s = net.layers[static_cast<size_t>(2 * b)];
+      DevFC f;
+      f.in = s.in_dim;
+      f.out = s.out_dim;
+      f.inp = round_up(s.in_dim, 64);
+      f.outp = round_up(s.out_dim, 64);
+      std::vector<float> w(static_cast<size_t>(f.outp) * f.inp, 0.0f), bias(static_cast<size_t>(f.outp), 0.0f);
+      const LayerWeights& lw = net.weights[static_cast<size_t>(2 * b)];
+      for (int o = 0; o < f.out; ++o) {
+        for (int i = 0; i < f.in; ++i)
+          w[static_cast<size_t>(o) * f.inp + i] = static_cast<float>(lw.w[static_cast<size_t>(o) * f.in + i]);
+        bias[static_cast<size_t>(o)] = static_cast<float>(lw.b[static_cast<size_t>(o)]);
+      }
+      f.w = upload_planes(w);
+      f.b = upload_f32(bias);
+      mlp_fc_.push_back(f);
+      mlp_act_.push_back(alloc_planes(static_cast<size_t>(B) * f.outp));
+      mlp_cin_.push_back(alloc_planes(static_cast<size_t>(B) * f.outp));
+      max_tap_storage = std::max<long long>(max_tap_storage, f.outp);
+    }
+    mlp_in_ = alloc_planes(static_cast<size_t>(B) * mlp_fc_[0].inp);
+    const LayerWeights& hw = net.weights[static_cast<size_t>(2 * L)];
+    head_w_ = upload_f32(to_f32(hw.w));
+    head_b_ = upload_f32(to_f32(hw.b));
+  } else {
+    cnn_w_.resize(model_.ops.size());
+    std::vector<long long> slot_elems(static_cast<size_t>(model_.nslots), 0);
+    long long phase_elems = 0, im2col_elems = 0;
+    for (size_t i = 0; i < model_.ops.size(); ++i) {
+      const CnnOp& o = model_.ops[i];
+      if (o.kind == CnnOpKind::Stem || o.kind == CnnOpKind::Conv) {
+        DevConv dc;
+        const int K = o.k * o.k * o.C;
+        dc.Kp = o.kind == CnnOpKind::Stem ? round_up(K, 64) : K;
+        require(o.kind == CnnOpKind::Stem || o.C % 64 == 0, "engine: conv input channels must be a multiple of 64");
+        std::vector<float> w(static_cast<size_t>(o.Cout) * dc.Kp, 0.0f);
+        for (int co = 0; co < o.Cout; ++co)
+          for (int c = 0; c < o.C; ++c)
+            for (int r = 0; r < o.k; ++r)
+              for (int s = 0; s < o.k; ++s)
+                w[static_cast<size_t>(co) * dc.Kp + (r * o.k + s) * o.C + c] =
+                    static_cast<float>(o.w[((static_cast<size_t>(co) * o.C + c) * o.k + r) * o.k + s]);
+        dc.w = upload_planes(w);
+        dc.scale = upload_f32(to_f32(o.scale));
+        dc.shift = upload_f32(to_f32(o.shift));
+        cnn_w_[i] = dc;
+        slot_elems[static_cast<size_t>(o.out)] = static_cast<long long>(B) * o.Ho() * o.Wo() * o.Cout;
+        if (o.kind == CnnOpKind::Stem)
+          im2col_elems = std::max(im2col_elems, static_cast<long long>(B) * o.Ho() * o.Wo() * dc.Kp);
+        if (o.stride == 2)
+          phase_elems = std::max(phase_elems, 4LL * B * ((o.H + 1) / 2) * ((o.W + 1) / 2) * o.C);
+      } else if (o.kind == CnnOpKind::MaxPool) {
+        slot_elems[static_cast<size_t>(o.out)] = static_cast<long long>(B) * o.Ho() * o.Wo() * o.C;
+      } else if (o.kind == CnnOpKind::Head) {
+        head_w_ = upload_f32(to_f32(o.w));
+        head_b_ = upload_f32(to_f32(o.shift));
+      }
+    }
+    // Liveness-based slot -> buffer assignment.
+    std::vector<int> last_use(static_cast<size_t>(model_.nslots), -1);
+    for (size_t i = 0; i < model_.ops.size(); ++i) {
+      const CnnOp& o = model_.ops[i];
+      if (o.in >= 0) last_use[static_cast<size_t>(o.in)] = static_cast<int>(i);
+      if (o.res >= 0) last_use[static_cast<size_t>(o.res)] = static_cast<int>(i);
+    }
+    slot_buf_.assign(static_cast<size_t>(model_.nslots), Planes{});
+    std::multimap<long long, Planes> free_pool;
+    for (size_t i = 0; i < model_.ops.size(); ++i) {
+      const CnnOp& o = model_.ops[i];
+      if (o.kind != CnnOpKind::Head) {
+        const long long need = slot_elems[static_cast<size_t>(o.out)];
+        auto it = free_pool.find(need);
+        if (it != free_pool.end()) {
+          slot_buf_[static_cast<size_t>(o.out)] = it->second;
+          free_pool.erase(it);
+        } else {
+          slot_buf_[static_cast<size_t>(o.out)] = alloc_planes(static_cast<size_t>(need));
+        }
+      }
+      for (int s = 0; s < model_.nslots; ++s)
+        if (last_use[static_cast<size_t>(s)] == static_cast<int>(i) && slot_buf_[static_cast<size_t>(s)].hi)
+          free_pool.emplace(slot_elems[static_cast<size_t>(s)], slot_buf_[static_cast<size_t>(s)]);
+    }
+    if (phase_elems) phase_buf_ = alloc_planes(static_cast<size_t>(phase_elems));
+    if (im2col_elems) im2col_buf_ = alloc_planes(static_cast<size_t>(im2col_elems));
+    for (const TapInfo& t : model_.taps) max_tap_storage = std::max(max_tap_storage, t.dim());
+  }
+
+  // ---------------- caches
+  for (const CacheVariant& v : variants_) {
+    auto c = std::make_unique<DevCache>();
+    c->layer = v.layer;
+    c->classes = model_.num_classes;
+    c->D = model_.tap_dim(v.layer);
+    c->delta = v.delta;
+    const TapInfo ti = model_.taps[static_cast<size_t>(v.layer - 1)];
+    const bool mlp = model_.family == "mlp";
+    const long long row_stride = mlp ? mlp_fc_[static_cast<size_t>(v.layer - 1)].outp : c->D;
+    const auto& P = v.predictor.layers;
+    const auto& PW = v.predictor.weights;
+    const int C = c->classes;
+    if (P.size() == 2 && P[0].kind == LayerKind::Pool && P[1].kind == LayerKind::FC) {
+      c->family = 1;
+      c->win = P[0].pool_window;
+      c->width = P[0].out_dim;
+      c->W2 = upload_f32(to_f32(PW[1].w));
+      c->b2 = upload_f32(to_f32(PW[1].b));
+      c->feats = static_cast<float*>(dalloc(static_cast<size_t>(B) * c->width * sizeof(float)));
+    } else if (P.size() == 3 && P[0].kind == LayerKind::Conv1d && P[1].kind == LayerKind::ReLU &&
+               P[2].kind == LayerKind::FC) {
+      c->family = 2;
+      c->kernel = P[0].kernel;
+      c->stride = P[0].stride;
+      c->out_dim = P[0].out_dim;
+      c->w1 = upload_f32(to_f32(PW[0].w));
+      c->b1c = static_cast<float>(PW[0].b[0]);
+      c->W2 = upload_f32(to_f32(PW[2].w));
+      c->b2 = upload_f32(to_f32(PW[2].b));
+      // chunk = whole channels, <= ~24K floats of shared memory
+      if (ti.H * ti.W == 1) {
+        c->chunk_elems = static_cast<int>(std::min<long long>(c->D, 8192));
+      } else {
+        const int HW = ti.H * ti.W;
+        int cb = std::max(1, 24576 / HW);
+        cb = std::min(cb, ti.C);
+        c->chunk_elems = cb * HW;
+      }
+      c->nchunks = static_cast<int>((c->D + c->chunk_elems - 1) / c->chunk_elems);
+      c->feats = static_cast<float*>(dalloc(static_cast<size_t>(B) * c->nchunks * C * sizeof(float)));
+    } else if (P.size() == 3 && P[0].kind == LayerKind::FC && P[1].kind == LayerKind::ReLU &&
+               P[2].kind == LayerKind::FC) {
+      c->family = 0;
+      c->h = P[0].out_dim;
+      c->hp = round_up(c->h, 64);
+      c->Dk = static_cast<int>(round_up(row_stride, 64));
+      std::vector<float> w(static_cast<size_t>(c->hp) * c->Dk, 0.0f);
+      const int HW = ti.H * ti.W, Ct = ti.C;
+      for (int j = 0; j < c->h; ++j)
+        for (long long f = 0; f < c->D; ++f) {
+          const long long off = mlp ? f : (f % HW) * Ct + f / HW;  // NCHW-flat -> storage order
+          w[static_cast<size_t>(j) * c->Dk + static_cast<size_t>(off)] =
+              static_cast<float>(PW[0].w[static_cast<size_t>(j) * c->D + static_cast<size_t>(f)]);
+        }
+      c->W1 = upload_planes(w);
+      c->b1 = upload_f32(to_f32(PW[0].b));
+      c->W2 = upload_f32(to_f32(PW[2].w));
+      c->b2 = upload_f32(to_f32(PW[2].b));
+      const int tiles_mn = ((B + 127) / 128) * (c->hp / tc_conv_pick_bn(c->hp));
+      const int nk = (c->Dk / 64) * (prec_ == kPrecX3 ? 3 : 1);
+      c->ks = std::max(1, std::min(nk, num_sms_ / std::max(1, tiles_mn)));
+      c->feats = static_cast<float*>(dalloc(static_cast<size_t>(c->ks) * B * c->hp * sizeof(float)));
+      if (!mlp) c->gather = alloc_planes(static_cast<size_t>(B) * c->Dk);
+    } else {
+      throw std::invalid_argument("engine: unsupported predictor architecture at layer " + std::to_string(v.layer));
+    }
+    const auto& S = v.selector.layers;
+    require(S.size() == 3 && S[0].kind == LayerKind::FC && S[0].out_dim == 16 && S[1].kind == LayerKind::ReLU &&
+                S[2].kind == LayerKind::FC && S[2].out_dim == 1,
+            "engine: selector must be FC(C,16)+ReLU+FC(16,1) (cache.cpp:135-137)");
+    c->Ws1 = upload_f32(to_f32(v.selector.weights[0].w));
+    c->bs1 = upload_f32(to_f32(v.selector.weights[0].b));
+    c->ws2 = upload_f32(to_f32(v.selector.weights[2].w));
+    c->bs2 = static_cast<float>(v.selector.weights[2].b[0]);
+    c->hit = static_cast<int*>(dalloc(static_cast<size_t>(B) * sizeof(int)));
+    c->label = static_cast<int*>(dalloc(static_cast<size_t>(B) * sizeof(int)));
+    c->prob = static_cast<float*>(dalloc(static_cast<size_t>(B) * sizeof(float)));
+    c->pr_out = static_cast<float*>(dalloc(static_cast<size_t>(B) * C * sizeof(float)));
+    c->logits_out = static_cast<float*>(dalloc(static_cast<size_t>(B) * C * sizeof(float)));
+    caches_.push_back(std::move(c));
+  }
+  lk_tap_ = alloc_planes(static_cast<size_t>(B) * round_up(max_tap_storage, 64));
+}
+
+// ------------------------------------------------------------------ lookups
+void Engine::add_lookup_steps(std::vector<Step>& steps, DevCache& c, const TapView& tap, int max_rows,
+                              bool stage_gather) {
+  DevCache* cp = &c;
+  if (c.family == 1) {
+    steps.push_back({[cp, tap, max_rows](cudaStream_t s) {
+                       launch_pool_bins(tap, max_rows, cp->win, cp->width, cp->feats, s);
+                     },
+                     2});
+  } else if (c.family == 2) {
+    steps.push_back({[cp, tap, max_rows](cudaStream_t s) {
+                       launch_conv1d_partials(tap, max_rows, cp->D, cp->kernel, cp->stride, cp->out_dim, cp->w1,
+                                              cp->b1c, cp->W2, cp->classes, cp->chunk_elems, cp->nchunks, cp->feats,
+                                              s);
+                     },
+                     2});
+  } else {
+    // FC(h): hidden = W1 . tap as a split-K tensor-core GEMM over the rows.
+    const __nv_bfloat16* a_hi = tap.hi;
+    const __nv_bfloat16* a_lo = tap.lo;
+    if (stage_gather) {
+      const long long row_elems = tap.row_stride;
+      Planes g = c.gather;
+      const int* idx = tap.data_idx;
+      const int* cnt = tap.count;
+      steps.push_back({[g, tap, row_elems, idx, cnt, max_rows](cudaStream_t s) {
+                         launch_gather_rows(tap.hi, tap.lo, g.hi, g.lo, row_elems, idx, cnt, max_rows, s);
+                       },
+                       3});
+      a_hi = g.hi;
+      a_lo = g.lo;
+    }
+    auto prm = std::make_shared<TcConvParams>();
+    std::memset(prm.get(), 0, sizeof(TcConvParams));
+    const int BN = tc_conv_pick_bn(c.hp);
+    const bool x3 = prec_ == kPrecX3;
+    bool ok = encode_act_map(&prm->tmA[0], a_hi, c.Dk, max_rows, 1, 1, 1, 128, 1) &&
+              encode_weight_map(&prm->tmB[0], c.W1.hi, c.Dk, c.hp, BN);
+    if (x3)
+      ok = ok && encode_act_map(&prm->tmA[1], a_lo, c.Dk, max_rows, 1, 1, 1, 128, 1) &&
+           encode_weight_map(&prm->tmB[1], c.W1.lo, c.Dk, c.hp, BN);
+    if (!ok) throw CudaFailure("engine: TMA descriptor encode failed (FC cache)");
+    prm->plain = 1;
+    prm->Ho = 1;
+    prm->Wo = max_rows;
+    prm->hb = 1;
+    prm->wb = 128;
+    prm->ipt = 1;
+    prm->tiles_h = 1;
+    prm->C = c.Dk;
+    prm->ntaps = 1;
+    prm->segs = x3 ? 3 : 1;
+    prm->Cout = c.hp;
+    prm->ksplit = c.ks;
+    prm->count = tap.count;
+    prm->count_static = max_rows;
+    prm->mode = 1;
+    prm->rows_total = max_rows;
+    prm->out_f32 = c.feats;
+    const int sms = num_sms_;
+    steps.push_back({[prm, BN, sms](cudaStream_t s) { ck(tc_conv_launch(*prm, BN, sms, s), "tc_conv (fc cache)"); }, 1});
+  }
+  const int rows_total = max_rows;
+  steps.push_back({[cp, tap, max_rows, rows_total](cudaStream_t s) {
+                     CacheHeadParams p;
+                     p.family = cp->family;
+                     p.classes = cp->classes;
+                     p.feat = cp->family == 1 ? cp->width : (cp->family == 0 ? cp->h : cp->nchunks);
+                     p.feats = cp->feats;
+                     p.ks = cp->ks;
+                     p.hp = cp->hp;
+                     p.rows_total = rows_total;
+                     p.b1 = cp->b1;
+                     p.W2 = cp->W2;
+                     p.b2 = cp->b2;
+                     p.Ws1 = cp->Ws1;
+                     p.bs1 = cp->bs1;
+                     p.ws2 = cp->ws2;
+                     p.bs2 = cp->bs2;
+                     p.delta = cp->delta;
+                     p.count = tap.count;
+                     p.prob = cp->prob;
+                     p.hit = cp->hit;
+                     p.label = cp->label;
+                     p.pr_out = cp->pr_out;
+                     p.logits_out = cp->logits_out;
+                     launch_cache_head(p, max_rows, s);
+                   },
+                   2});
+}
+
+// ------------------------------------------------------------------ MLP serve
+void Engine::build_mlp_steps(std::vector<Step>& steps, bool shadow) {
+  const int B = max_batch_, L = model_.num_blocks;
+  const bool x3 = prec_ == kPrecX3;
+  int* ids = d_ids_;
+  int* src = d_src_;
+  int* counts = d_counts_;
+  steps.push_back({[this, L](cudaStream_t s) {
+                     launch_init_batch(d_batch_, max_batch_, d_ids_, d_counts_, nullptr, 0, d_exit_, d_served_, d_base_,
+                                       d_exit_ns_, d_probs_, L, s);
+                     launch_stamp_start(d_t0_, s);
+                   },
+                   0, 2});
+  const int in_dim = static_cast<int>(model_.input_dim());
+  {
+    Planes in = mlp_in_;
+    const int inp = mlp_fc_[0].inp;
+    steps.push_back({[this, in, in_dim, inp, counts, B](cudaStream_t s) {
+                       launch_split_rows(d_x_, in_dim, inp, nullptr, counts, B, in.hi, in.lo, s);
+                     },
+                     0});
+  }
+  Planes cur = mlp_in_;
+  int* cur_ids = ids;
+  int* cur_count = counts;
+  for (int b = 0; b < L; ++b) {
+    const DevFC& f = mlp_fc_[static_cast<size_t>(b)];
+    Planes act = mlp_act_[static_cast<size_t>(b)];
+    auto prm = std::make_shared<TcConvParams>();
+    std::memset(prm.get(), 0, sizeof(TcConvParams));
+    const int BN = tc_conv_pick_bn(f.outp);
+    bool ok = encode_act_map(&prm->tmA[0], cur.hi, f.inp, B, 1, 1, 1, 128, 1) &&
+              encode_weight_map(&prm->tmB[0], f.w.hi, f.inp, f.outp, BN);
+    if (x3)
+      ok = ok && encode_act_map(&prm->tmA[1], cur.lo, f.inp, B, 1, 1, 1, 128, 1) &&
+           encode_weight_map(&prm->tmB[1], f.w.lo, f.inp, f.outp, BN);
+    if (!ok) throw CudaFailure("engine: TMA descriptor encode failed (mlp)");
+    prm->plain = 1;
+    prm->Ho = 1;
+    prm->Wo = B;
+    prm->hb = 1;
+    prm->wb = 128;
+    prm->ipt = 1;
+    prm->tiles_h = 1;
+    prm->C = f.inp;
+    prm->ntaps = 1;
+    prm->segs = x3 ? 3 : 1;
+    prm->Cout = f.outp;
+    prm->ksplit = 1;
+    prm->count = cur_count;
+    prm->count_static = B;
+    prm->mode = 0;
+    prm->shift = f.b;
+    prm->relu = 1;
+    prm->out_hi = act.hi;
+    prm->out_lo = act.lo;
+    const int sms = num_sms_;
+    steps.push_back({[prm, BN, sms](cudaStream_t s) { ck(tc_conv_launch(*prm, BN, sms, s), "tc_conv (mlp)"); }, 1});
+    const int layer = b + 1;
+    const int ci = cache_of_layer_[static_cast<size_t>(layer)];
+    if (ci >= 0) {
+      DevCache& c = *caches_[static_cast<size_t>(ci)];
+      TapView tap;
+      tap.hi = act.hi;
+      tap.lo = act.lo;
+      tap.row_stride = f.outp;
+      tap.C = f.out;
+      tap.HW = 1;
+      tap.data_idx = nullptr;
+      tap.count = cur_count;
+      add_lookup_steps(steps, c, tap, B, false);
+      int* ids_out = ids + static_cast<size_t>(layer) * B;
+      int* src_out = src + static_cast<size_t>(layer) * B;
+      int* cnt_out = counts + layer;
+      DevCache* cp = &c;
+      float* probs_out = d_probs_ + static_cast<size_t>(layer - 1) * B;
+      steps.push_back({[this, cp, layer, cur_count, cur_ids, ids_out, src_out, cnt_out, probs_out, shadow](cudaStream_t s) {
+                         launch_exit_compact(layer, cur_count, cur_ids, cp->hit, cp->label, cp->prob, d_exit_,
+                                             d_served_, d_exit_ns_, probs_out, ids_out, src_out, cnt_out, shadow ? 1 : 0,
+                                             s);
+                       },
+                       3});
+      if (!shadow) {
+        Planes dst = mlp_cin_[static_cast<size_t>(b)];
+        const long long row_elems = f.outp;
+        steps.push_back({[act, dst, row_elems, src_out, cnt_out, B](cudaStream_t s) {
+                           launch_gather_rows(act.hi, act.lo, dst.hi, dst.lo, row_elems, src_out, cnt_out, B, s);
+                         },
+                         3});
+        cur = dst;
+      } else {
+        cur = act;
+      }
+      cur_ids = ids_out;
+      cur_count = cnt_out;
+    } else {
+      cur = act;
+    }
+  }
+  const DevFC& last = mlp_fc_.back();
+  const int classes = model_.num_classes;
+  steps.push_back({[this, cur, last, classes, cur_ids, cur_count, B](cudaStream_t s) {
+                     launch_mlp_head(cur.hi, cur.lo, last.outp, last.out, head_w_, head_b_, classes, cur_ids,
+                                     cur_count, B, d_base_, nullptr, d_exit_, d_served_, d_exit_ns_, s);
+                   },
+                   0});
+}
+
+// ------------------------------------------------------------------ CNN serve
+void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow) {
+  const int B = max_batch_, L = model_.num_blocks;
+  const bool x3 = prec_ == kPrecX3;
+  int* ids = d_ids_;
+  int* counts = d_counts_;
+  int stem_mult = 1;
+  for (const CnnOp& o : model_.ops)
+    if (o.kind == CnnOpKind::Stem) stem_mult = o.Ho() * o.Wo();
+  int* stem_rows = counts + L + 1;
+  steps.push_back({[this, L, stem_rows, stem_mult](cudaStream_t s) {
+                     launch_init_batch(d_batch_, max_batch_, d_ids_, d_counts_, stem_rows, stem_mult, d_exit_, d_served_,
+                                       d_base_, d_exit_ns_, d_probs_, L, s);
+                     launch_stamp_start(d_t0_, s);
+                   },
+                   0, 2});
+  int* cur_ids = ids;
+  int* cur_count = counts;
+  const int sms = num_sms_;
+  for (size_t i = 0; i < model_.ops.size(); ++i) {
+    const CnnOp& o = model_.ops[i];
+    if (o.kind == CnnOpKind::Stem) {
+      const DevConv& dc = cnn_w_[i];
+      Planes col = im2col_buf_;
+      Planes out = slot_buf_[static_cast<size_t>(o.out)];
+      const int Ho = o.Ho(), Wo = o.Wo();
+      steps.push_back({[this, o, Ho, Wo, dc, col, counts, B](cudaStream_t s) {
+                         launch_stem_im2col(d_x_, counts, B, o.C, o.H, o.W, o.k, o.stride, o.pad, Ho, Wo, dc.Kp, col.hi,
+                                            col.lo, s);
+                       },
+                       0});
+      auto prm = std::make_shared<TcConvParams>();
+      std::memset(prm.get(), 0, sizeof(TcConvParams));
+      const int rows = B * Ho * Wo;
+      const int BN = tc_conv_pick_bn(o.Cout);
+      bool ok = encode_act_map(&prm->tmA[0], col.hi, dc.Kp, rows, 1, 1, 1, 128, 1) &&
+                encode_weight_map(&prm->tmB[0], dc.w.hi, dc.Kp, o.Cout, BN);
+      if (x3)
+        ok = ok && encode_act_map(&prm->tmA[1], col.lo, dc.Kp, rows, 1, 1, 1, 128, 1) &&
+             encode_weight_map(&prm->tmB[1], dc.w.lo, dc.Kp, o.Cout, BN);
+      if (!ok) throw CudaFailure("engine: TMA descriptor encode failed (stem)");
+      prm->plain = 1;
+      prm->Ho = 1;
+      prm->Wo = rows;
+      prm->hb = 1;
+      prm->wb = 128;
+      prm->ipt = 1;
+      prm->tiles_h = 1;
+      prm->C = dc.Kp;
+      prm->ntaps = 1;
+      prm->segs = x3 ? 3 : 1;
+      prm->Cout = o.Cout;
+      prm->ksplit = 1;
+      prm->count = stem_rows;
+      prm->count_static = rows;
+      prm->mode = 0;
+      prm->scale = dc.scale;
+      prm->shift = dc.shift;
+      prm->relu = o.relu ? 1 : 0;
+      prm->out_hi = out.hi;
+      prm->out_lo = out.lo;
+      steps.push_back({[prm, BN, sms](cudaStream_t s) { ck(tc_conv_launch(*prm, BN, sms, s), "tc_conv (stem)"); }, 1});
+    } else if (o.kind == CnnOpKind::MaxPool) {
+      Planes in = slot_buf_[static_cast<size_t>(o.in)], out = slot_buf_[static_cast<size_t>(o.out)];
+      const int Ho = o.Ho(), Wo = o.Wo();
+      steps.push_back({[o, in, out, Ho, Wo, cur_ids, cur_count, B](cudaStream_t s) {
+                         launch_maxpool(in.hi, in.lo, o.H, o.W, o.C, o.k, o.stride, o.pad, Ho, Wo, cur_ids, cur_count,
+                                        B, out.hi, out.lo, s);
+                       },
+                       0});
+    } else if (o.kind == CnnOpKind::Conv) {
+      const DevConv& dc = cnn_w_[i];
+      Planes in = slot_buf_[static_cast<size_t>(o.in)], out = slot_buf_[static_cast<size_t>(o.out)];
+      Planes src = in;
+      int P = 1, Hs = o.H, Ws = o.W;
+      if (o.stride == 2) {
+        Hs = (o.H + 1) / 2;
+        Ws = (o.W + 1) / 2;
+        P = 4;
+        Planes ph = phase_buf_;
+        steps.push_back({[o, in, ph, Hs, Ws, cur_ids, cur_count, B](cudaStream_t s) {
+                           launch_phase_split(in.hi, in.lo, o.H, o.W, o.C, B, Hs, Ws, cur_ids, cur_count, B, ph.hi,
+                                              ph.lo, s);
+                         },
+                         0});
+        src = ph;
+      } else {
+        require(o.stride == 1, "engine: only stride 1 and 2 convolutions are supported");
+      }
+      const int Ho = o.Ho(), Wo = o.Wo();
+      int hb, wb, ipt;
+      choose_box(Ho, Wo, hb, wb, ipt);
+      auto prm = std::make_shared<TcConvParams>();
+      std::memset(prm.get(), 0, sizeof(TcConvParams));
+      const int BN = tc_conv_pick_bn(o.Cout);
+      bool ok = encode_act_map(&prm->tmA[0], src.hi, o.C, Ws, Hs, B, P, wb, hb) &&
+                encode_weight_map(&prm->tmB[0], dc.w.hi, dc.Kp, o.Cout, BN);
+      if (x3)
+        ok = ok && encode_act_map(&prm->tmA[1], src.lo, o.C, Ws, Hs, B, P, wb, hb) &&
+             encode_weight_map(&prm->tmB[1], dc.w.lo, dc.Kp, o.Cout, BN);
+      if (!ok) throw CudaFailure("engine: TMA descriptor encode failed (conv)");
+      prm->plain = 0;
+      prm->Ho = Ho;
+      prm->Wo = Wo;
+      prm->hb = hb;
+      prm->wb = wb;
+      prm->ipt = ipt;
+      prm->tiles_h = (Ho + hb - 1) / hb;
+      prm->tiles_w = (Wo + wb - 1) / wb;
+      prm->C = o.C;
+      prm->ntaps = o.k * o.k;
+      prm->segs = x3 ? 3 : 1;
+      prm->Cout = o.Cout;
+      prm->ksplit = 1;
+      prm->surv = cur_ids;
+      prm->count = cur_count;
+      prm->count_static = B;
+      prm->mode = 0;
+      prm->scale = dc.scale;
+      prm->shift = dc.shift;
+      if (o.res >= 0) {
+        prm->res_hi = slot_buf_[static_cast<size_t>(o.res)].hi;
+        prm->res_lo = slot_buf_[static_cast<size_t>(o.res)].lo;
+      }
+      prm->relu = o.relu ? 1 : 0;
+      prm->out_hi = out.hi;
+      prm->out_lo = out.lo;
+      for (int r = 0; r < o.k; ++r)
+        for (int sx = 0; sx < o.k; ++sx) {
+          const int t = r * o.k + sx;
+          if (o.stride == 1) {
+            prm->tap_phase[t] = 0;
+            prm->tap_dh[t] = static_cast<signed char>(r - o.pad);
+            prm->tap_dw[t] = static_cast<signed char>(sx - o.pad);
+          } else {
+            const int oh = r - o.pad, ow = sx - o.pad;
+            const int ph = ((oh % 2) + 2) % 2, pw = ((ow % 2) + 2) % 2;
+            prm->tap_phase[t] = static_cast<signed char>(ph * 2 + pw);
+            prm->tap_dh[t] = static_cast<signed char>((oh - ph) / 2);
+            prm->tap_dw[t] = static_cast<signed char>((ow - pw) / 2);
+          }
+        }
+      steps.push_back({[prm, BN, sms](cudaStream_t s) { ck(tc_conv_launch(*prm, BN, sms, s), "tc_conv (conv)"); }, 1});
+    } else if (o.kind == CnnOpKind::Head) {
+      Planes in = slot_buf_[static_cast<size_t>(o.in)];
+      const int classes = model_.num_classes, C = o.C, HW = o.H * o.W;
+      steps.push_back({[this, in, C, HW, classes, cur_ids, cur_count, B](cudaStream_t s) {
+                         launch_cnn_head(in.hi, in.lo, C, HW, head_w_, head_b_, classes, cur_ids, cur_count, B,
+                                         d_base_, nullptr, d_exit_, d_served_, d_exit_ns_, s);
+                       },
+                       0});
+    }
+    if (o.tap >= 0) {
+      const int layer = o.tap + 1;
+      const int ci = cache_of_layer_[static_cast<size_t>(layer)];
+      if (ci >= 0) {
+        DevCache& c = *caches_[static_cast<size_t>(ci)];
+        const TapInfo& ti = model_.taps[static_cast<size_t>(o.tap)];
+        Planes tb = slot_buf_[static_cast<size_t>(o.out)];
+        TapView tap;
+        tap.hi = tb.hi;
+        tap.lo = tb.lo;
+        tap.row_stride = ti.dim();
+        tap.C = ti.C;
+        tap.HW = ti.H * ti.W;
+        tap.data_idx = cur_ids;
+        tap.count = cur_count;
+        add_lookup_steps(steps, c, tap, B, true);
+        int* ids_out = ids + static_cast<size_t>(layer) * B;
+        int* cnt_out = counts + layer;
+        DevCache* cp = &c;
+        float* probs_out = d_probs_ + static_cast<size_t>(layer - 1) * B;
+        steps.push_back({[this, cp, layer, cur_count, cur_ids, ids_out, cnt_out, probs_out, shadow](cudaStream_t s) {
+                           launch_exit_compact(layer, cur_count, cur_ids, cp->hit, cp->label, cp->prob, d_exit_,
+                                               d_served_, d_exit_ns_, probs_out, ids_out, nullptr, cnt_out,
+                                               shadow ? 1 : 0, s);
+                         },
+                         3});
+        cur_ids = ids_out;
+        cur_count = cnt_out;
+      }
+    }
+  }
+}
+
+std::vector<Step>& Engine::steps_for(bool shadow) {
+  std::vector<Step>& st = shadow ? steps_shadow_ : steps_compact_;
+  bool& built = shadow ? built_shadow_ : built_compact_;
+  if (!built) {
+    st.clear();
+    if (model_.family == "mlp") build_mlp_steps(st, shadow);
+    else build_cnn_steps(st, shadow);
+    built = true;
+  }
+  return st;
+}
+
+int Engine::num_steps(bool shadow) const { return static_cast<int>((shadow ? steps_shadow_ : steps_compact_).size()); }
+
+int Engine::count_kernels(bool shadow, int kind) {
+  const auto& st = steps_for(shadow);
+  int n = 0;
+  for (const Step& s : st)
+    if (kind < 0 || s.kind == kind) n += s.launches;
+  return n;
+}
+
+void Engine::serve(int B, bool shadow, bool use_graph) {
+  require(B > 0 && B <= max_batch_, "serve: batch size " + std::to_string(B) + " outside [1, max_batch]");
+  ck(cudaSetDevice(device_), "cudaSetDevice");
+  *h_batch_ = B;
+  ck(cudaMemcpyAsync(d_batch_, h_batch_, sizeof(int), cudaMemcpyHostToDevice, stream_), "batch size");
+  std::vector<Step>& st = steps_for(shadow);
+  if (!use_graph) {
+    for (Step& s : st) s.run(stream_);
+    ck(cudaGetLastError(), "serve");
+    return;
+  }
+  cudaGraphExec_t& ge = graph_[shadow ? 1 : 0];
+  if (!ge) {
+    cudaGraph_t g;
+    ck(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "capture");
+    for (Step& s : st) s.run(stream_);
+    ck(cudaStreamEndCapture(stream_, &g), "capture end");
+    ck(cudaGraphInstantiate(&ge, g, 0), "graph instantiate");
+    cudaGraphDestroy(g);
+  }
+  ck(cudaGraphLaunch(ge, stream_), "graph launch");
+}
+
+void Engine::serve_host(const float* x, int B, bool shadow, bool use_graph) {
+  require(B > 0 && B <= max_batch_, "serve: batch size " + std::to_string(B) + " outside [1, max_batch]");
+  ck(cudaSetDevice(device_), "cudaSetDevice");
+  ck(cudaMemcpyAsync(d_x_, x, static_cast<size_t>(B) * model_.input_dim() * sizeof(float), cudaMemcpyHostToDevice,
+                     stream_),
+     "input upload");
+  serve(B, shadow, use_graph);
+}
+
+void Engine::synchronize() { ck(cudaStreamSynchronize(stream_), "synchronize"); }
+
+void Engine::copy_results(int B, int* exit_layer, int* served, int* base, float* probs_LB, double* latency_ms) {
+  ck(cudaSetDevice(device_), "cudaSetDevice");
+  if (exit_layer) ck(cudaMemcpyAsync(exit_layer, d_exit_, B * sizeof(int), cudaMemcpyDeviceToHost, stream_), "d2h");
+  if (served) ck(cudaMemcpyAsync(served, d_served_, B * sizeof(int), cudaMemcpyDeviceToHost, stream_), "d2h");
+  if (base) ck(cudaMemcpyAsync(base, d_base_, B * sizeof(int), cudaMemcpyDeviceToHost, stream_), "d2h");
+  if (probs_LB)
+    for (int l = 0; l < model_.num_blocks; ++l)
+      ck(cudaMemcpyAsync(probs_LB + static_cast<size_t>(l) * B, d_probs_ + static_cast<size_t>(l) * max_batch_,
+                         B * sizeof(float), cudaMemcpyDeviceToHost, stream_),
+         "d2h");
+  std::vector<unsigned long long> ns;
+  unsigned long long t0 = 0;
+  if (latency_ms) {
+    ns.resize(static_cast<size_t>(B));
+    ck(cudaMemcpyAsync(ns.data(), d_exit_ns_, B * 8, cudaMemcpyDeviceToHost, stream_), "d2h");
+    ck(cudaMemcpyAsync(&t0, d_t0_, 8, cudaMemcpyDeviceToHost, stream_), "d2h");
+  }
+  ck(cudaStreamSynchronize(stream_), "d2h sync");
+  if (latency_ms)
+    for (int i = 0; i < B; ++i) latency_ms[i] = static_cast<double>(ns[static_cast<size_t>(i)] - t0) * 1e-6;
+}
+
+void Engine::lookup(int layer, const float* taps_dev, int B, int* hit, int* label, float* prob, float* pr,
+                    float* logits) {
+  require(layer >= 1 && layer <= model_.num_blocks, "lookup: layer out of range");
+  const int ci = cache_of_layer_[static_cast<size_t>(layer)];
+  require(ci >= 0, "lookup: no cache attached at layer " + std::to_string(layer));
+  require(B > 0 && B <= max_batch_, "lookup: batch outside [1, max_batch]");
+  ck(cudaSetDevice(device_), "cudaSetDevice");
+  DevCache& c = *caches_[static_cast<size_t>(ci)];
+  const TapInfo& ti = model_.taps[static_cast<size_t>(layer - 1)];
+  const bool mlp = model_.family == "mlp";
+  const long long row_stride = mlp ? mlp_fc_[static_cast<size_t>(layer - 1)].outp : ti.dim();
+  if (c.lookup_steps.empty()) {
+    TapView tap;
+    tap.hi = lk_tap_.hi;
+    tap.lo = lk_tap_.lo;
+    tap.row_stride = row_stride;
+    tap.C = mlp ? ti.C : ti.C;
+    tap.HW = mlp ? 1 : ti.H * ti.W;
+    tap.data_idx = nullptr;
+    tap.count = d_lk_count_;
+    add_lookup_steps(c.lookup_steps, c, tap, max_batch_, false);
+  }
+  *h_batch_ = B;
+  ck(cudaMemcpyAsync(d_lk_count_, h_batch_, sizeof(int), cudaMemcpyHostToDevice, stream_), "count");
+  launch_split_taps_nchw(taps_dev, ti.C, mlp ? 1 : ti.H * ti.W, B, row_stride, lk_tap_.hi, lk_tap_.lo, stream_);
+  for (Step& s : c.lookup_steps) s.run(stream_);
+  ck(cudaGetLastError(), "lookup");
+  const int C = model_.num_classes;
+  if (hit) ck(cudaMemcpyAsync(hit, c.hit, B * sizeof(int), cudaMemcpyDeviceToHost, stream_), "d2h");
+  if (label) ck(cudaMemcpyAsync(label, c.label, B * sizeof(int), cudaMemcpyDeviceToHost, stream_), "d2h");
+  if (prob) ck(cudaMemcpyAsync(prob, c.prob, B * sizeof(float), cudaMemcpyDeviceToHost, stream_), "d2h");
+  if (pr) ck(cudaMemcpyAsync(pr, c.pr_out, static_cast<size_t>(B) * C * sizeof(float), cudaMemcpyDeviceToHost, stream_), "d2h");
+  if (logits)
+    ck(cudaMemcpyAsync(logits, c.logits_out, static_cast<size_t>(B) * C * sizeof(float), cudaMemcpyDeviceToHost, stream_),
+       "d2h");
+  ck(cudaStreamSynchronize(stream_), "lookup sync");
+}
+
+void Engine::set_delta(int layer, double delta) {
+  require(layer >= 1 && layer <= model_.num_blocks, "set_delta: layer out of range");
+  const int ci = cache_of_layer_[static_cast<size_t>(layer)];
+  require(ci >= 0, "set_delta: no cache attached at layer " + std::to_string(layer));
+  caches_[static_cast<size_t>(ci)]->delta = delta;
+  variants_[static_cast<size_t>(ci)].delta = delta;
+  // Graphs bake kernel parameters: re-capture on next serve.
+  for (auto& g : graph_)
+    if (g) {
+      cudaGraphExecDestroy(g);
+      g = nullptr;
+    }
+}
+
+double Engine::delta(int layer) const {
+  const int ci = cache_of_layer_.at(static_cast<size_t>(layer));
+  if (ci < 0) throw std::invalid_argument("delta: no cache attached at layer " + std::to_string(layer));
+  return caches_[static_cast<size_t>(ci)]->delta;
+}
+
+// Rescale the selector's output layer (FC(16,1)) and set its bias; used to
+// calibrate synthetic deployments to a target exit profile (the analogue of
+// the reference tests' force_selector, test_serving.cpp:123-129).
+void Engine::set_selector_out(int layer, double gain, double bias) {
+  const int ci = cache_of_layer_.at(static_cast<size_t>(layer));
+  require(ci >= 0, "set_selector_out: no cache attached at layer " + std::to_string(layer));
+  CacheVariant& v = variants_[static_cast<size_t>(ci)];
+  for (double& w : v.selector.weights[2].w) w *= gain;
+  v.selector.weights[2].b[0] = bias;
+  DevCache& c = *caches_[static_cast<size_t>(ci)];
+  const std::vector<float> w = to_f32(v.selector.weights[2].w);
+  ck(cudaMemcpy(c.ws2, w.data(), w.size() * sizeof(float), cudaMemcpyHostToDevice), "selector upload");
+  c.bs2 = static_cast<float>(bias);
+  for (auto& g : graph_)
+    if (g) {
+      cudaGraphExecDestroy(g);
+      g = nullptr;
+    }
+  c.lookup_steps.clear();
+}
+
+double Engine::time_serve_ms(int B, bool shadow, int iters) {
+  serve(B, shadow, true);  // capture outside the timed region
+  ck(cudaStreamSynchronize(stream_), "sync");
+  ck(cudaEventRecord(ev0_, stream_), "event");
+  for (int i = 0; i < iters; ++i) serve(B, shadow, true);
+  ck(cudaEventRecord(ev1_, stream_), "event");
+  ck(cudaEventSynchronize(ev1_), "event sync");
+  float ms = 0.0f;
+  ck(cudaEventElapsedTime(&ms, ev0_, ev1_), "elapsed");
+  return ms / iters;
+}
+
+}  // namespace lcb

@@ -1,0 +1,153 @@
+// Device engine: a Deployment (reference serving.hpp:61-69) resident on one
+// B200. Holds the base model and the plan's chosen cache variants in HBM and
+// runs the batched serve path — the B200 form of simulate_model ->
+// serve_one (serving.cpp:97-158): base forward block by block, the cache
+// lookup at every chosen layer, first-hit exit and stream compaction so
+// deeper layers only run on the surviving requests.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <functional>
+#include <memory>
+#include <vector>
+
+#include "host/lcb_host.hpp"
+#include "kernels/serve_kernels.cuh"
+#include "kernels/tc_conv.cuh"
+
+namespace lcb {
+
+enum Precision { kPrecX3 = 0, kPrecBF16 = 1 };
+
+struct Planes {
+  __nv_bfloat16* hi = nullptr;
+  __nv_bfloat16* lo = nullptr;
+  size_t elems = 0;
+};
+
+struct DevCache;  // per chosen layer
+struct Step {
+  std::function<void(cudaStream_t)> run;
+  int kind = 0;      // 0 = other, 1 = tensor-core contraction, 2 = lookup, 3 = exit/compaction
+  int launches = 1;  // kernel launches this step enqueues
+};
+
+class Engine {
+ public:
+  Engine(int device, const BaseModel& model, std::vector<CacheVariant> variants, Precision prec, int max_batch);
+  ~Engine();
+  Engine(const Engine&) = delete;
+  Engine& operator=(const Engine&) = delete;
+
+  // ----- serve
+  float* input_buffer() { return d_x_; }  // [max_batch][input_dim] fp32 (device)
+  long long input_dim() const { return model_.input_dim(); }
+  // Enqueue a batch already in input_buffer(). shadow: no compaction (every
+  // request runs full depth; base_pred for all; first hit recorded).
+  void serve(int B, bool shadow, bool use_graph);
+  void serve_host(const float* x, int B, bool shadow, bool use_graph);
+  void synchronize();
+  // Results (device pointers, indexed by request id).
+  const int* exit_layer() const { return d_exit_; }
+  const int* served() const { return d_served_; }
+  const int* base_pred() const { return d_base_; }
+  const unsigned long long* exit_ns() const { return d_exit_ns_; }
+  const unsigned long long* start_ns() const { return d_t0_; }
+  const float* probs() const { return d_probs_; }  // [blocks][max_batch]
+  const int* layer_counts() const { return d_counts_; }  // [blocks + 1]
+  void copy_results(int B, int* exit_layer, int* served, int* base, float* probs_LB, double* latency_ms);
+
+  // ----- lookup only (reference lookup() on caller-provided NCHW-flat taps)
+  void lookup(int layer, const float* taps_dev, int B, int* hit, int* label, float* prob, float* pr, float* logits);
+
+  void set_delta(int layer, double delta);
+  double delta(int layer) const;
+  void set_selector_out(int layer, double gain, double bias);
+
+  // ----- introspection
+  int device() const { return device_; }
+  int max_batch() const { return max_batch_; }
+  int blocks() const { return model_.num_blocks; }
+  int classes() const { return model_.num_classes; }
+  const BaseModel& model() const { return model_; }
+  cudaStream_t stream() const { return stream_; }
+  int num_steps(bool shadow) const;
+  int count_kernels(bool shadow, int kind);
+  // Time `iters` serve() calls (graph replay) with CUDA events on the engine stream.
+  double time_serve_ms(int B, bool shadow, int iters);
+
+ private:
+  void build_weights();
+  void build_mlp_steps(std::vector<Step>& steps, bool shadow);
+  void build_cnn_steps(std::vector<Step>& steps, bool shadow);
+  void add_lookup_steps(std::vector<Step>& steps, DevCache& c, const TapView& tap, int max_rows, bool stage_gather);
+  std::vector<Step>& steps_for(bool shadow);
+  void* dalloc(size_t bytes);
+  Planes alloc_planes(size_t elems);
+  Planes upload_planes(const std::vector<float>& v);
+  float* upload_f32(const std::vector<float>& v);
+
+  int device_;
+  int num_sms_ = 148;
+  Precision prec_;
+  int max_batch_;
+  BaseModel model_;
+  std::vector<CacheVariant> variants_;
+  std::vector<std::unique_ptr<DevCache>> caches_;  // by chosen order
+  std::vector<int> cache_of_layer_;                // layer -> index or -1
+  cudaStream_t stream_ = nullptr;
+  std::vector<void*> allocs_;
+
+  // batch state
+  float* d_x_ = nullptr;
+  int* d_batch_ = nullptr;
+  int* h_batch_ = nullptr;  // pinned
+  int* d_ids_ = nullptr;    // [blocks + 1][max_batch]
+  int* d_src_ = nullptr;    // [blocks + 1][max_batch]
+  int* d_counts_ = nullptr; // [blocks + 1] (+1 stem rows)
+  int* d_exit_ = nullptr;
+  int* d_served_ = nullptr;
+  int* d_base_ = nullptr;
+  unsigned long long* d_exit_ns_ = nullptr;
+  unsigned long long* d_t0_ = nullptr;
+  float* d_probs_ = nullptr;
+
+  // MLP weights: per block FC (padded) + head
+  struct DevFC {
+    int in = 0, out = 0, inp = 0, outp = 0;
+    Planes w;
+    float* b = nullptr;
+  };
+  std::vector<DevFC> mlp_fc_;
+  std::vector<Planes> mlp_act_;   // [blocks] outputs (taps), [max_batch][outp]
+  std::vector<Planes> mlp_cin_;   // [blocks] compacted inputs of block b+1
+  Planes mlp_in_;
+  float* head_w_ = nullptr;
+  float* head_b_ = nullptr;
+
+  // CNN weights/buffers
+  struct DevConv {
+    Planes w;  // [Cout][k*k*C] (stem: [64][Kp])
+    float* scale = nullptr;
+    float* shift = nullptr;
+    int Kp = 0;
+  };
+  std::vector<DevConv> cnn_w_;    // by op index
+  std::vector<Planes> slot_buf_;  // by slot
+  Planes phase_buf_;
+  Planes im2col_buf_;
+
+  std::vector<Step> steps_compact_, steps_shadow_;
+  bool built_compact_ = false, built_shadow_ = false;
+  cudaGraphExec_t graph_[2] = {nullptr, nullptr};
+  cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
+
+  // lookup-only scratch
+  Planes lk_tap_;
+  int* d_lk_count_ = nullptr;
+  friend struct DevCache;
+};
+
+}  // namespace lcb

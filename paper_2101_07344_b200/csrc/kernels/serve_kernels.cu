@@ -1,0 +1,761 @@
+// Serve-path kernels (see serve_kernels.cuh). All cache-head arithmetic is
+// fp32 with deterministic (fixed-order) reductions; only the activations are
+// bf16 hi (+lo) planes.
+#include "serve_kernels.cuh"
+
+#include <cfloat>
+
+namespace lcb {
+
+namespace {
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ float ld_tap(const TapView& t, long long off) {
+  float v = __bfloat162float(t.hi[off]);
+  if (t.lo) v += __bfloat162float(t.lo[off]);
+  return v;
+}
+
+// 8 consecutive channels (16 bytes per plane) -> 8 floats.
+__device__ __forceinline__ void ld_tap8(const TapView& t, long long off, float (&v)[8]) {
+  const uint4 h = *reinterpret_cast<const uint4*>(t.hi + off);
+  const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&h);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 f = __bfloat1622float2(h2[e]);
+    v[2 * e] = f.x;
+    v[2 * e + 1] = f.y;
+  }
+  if (t.lo) {
+    const uint4 l = *reinterpret_cast<const uint4*>(t.lo + off);
+    const __nv_bfloat162* l2 = reinterpret_cast<const __nv_bfloat162*>(&l);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __bfloat1622float2(l2[e]);
+      v[2 * e] += f.x;
+      v[2 * e + 1] += f.y;
+    }
+  }
+}
+
+__device__ __forceinline__ void split_store(float v, __nv_bfloat16* hi, __nv_bfloat16* lo, long long off) {
+  const __nv_bfloat16 h = __float2bfloat16_rn(v);
+  hi[off] = h;
+  if (lo) lo[off] = __float2bfloat16_rn(v - __bfloat162float(h));
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Block-wide sum with a fixed reduction tree (deterministic). blockDim <= 1024.
+__device__ float block_sum(float v, float* scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) scratch[warp] = v;
+  __syncthreads();
+  float t = 0.0f;
+  if (warp == 0) {
+    t = lane < nw ? scratch[lane] : 0.0f;
+    t = warp_sum(t);
+    if (lane == 0) scratch[0] = t;
+  }
+  __syncthreads();
+  const float r = scratch[0];
+  __syncthreads();
+  return r;
+}
+__device__ float block_max(float v, float* scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  v = warp_max(v);
+  __syncthreads();
+  if (lane == 0) scratch[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    float t = lane < nw ? scratch[lane] : -FLT_MAX;
+    t = warp_max(t);
+    if (lane == 0) scratch[0] = t;
+  }
+  __syncthreads();
+  const float r = scratch[0];
+  __syncthreads();
+  return r;
+}
+
+// ------------------------------------------------------------------ pooling
+// Reference AvgPool (network.cpp:130-138) over the NCHW-flat tap: bin o is
+// the mean of flat elements [o*win, (o+1)*win).
+// Case A: win divides HW -> bins are channel strips; each thread owns whole
+// strips of 8 channels and streams them (16-byte loads).
+__global__ void pool_strips_kernel(TapView t, int win, int width, float inv, float* bins) {
+  const int r = blockIdx.x;
+  if (r >= *t.count) return;
+  const long long n = t.data_idx ? t.data_idx[r] : r;
+  const int cs = blockIdx.y * 64;
+  const int g = threadIdx.x & 7, q = threadIdx.x >> 3;
+  const int spc = t.HW / win;
+  const int per = (spc + 31) / 32;
+  const long long base = n * t.row_stride + cs + g * 8;
+  for (int wi = q * per; wi < (q + 1) * per && wi < spc; ++wi) {
+    float s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int p = wi * win; p < (wi + 1) * win; ++p) {
+      float v[8];
+      ld_tap8(t, base + static_cast<long long>(p) * t.C, v);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) s[e] += v[e];
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) bins[static_cast<long long>(r) * width + static_cast<long long>(cs + g * 8 + e) * spc + wi] = s[e] * inv;
+  }
+}
+
+// Case B: win = gch * HW (gch divides 64): per-channel totals over 32 pixel
+// ranges, combined in a fixed order, then gch channels per bin.
+__global__ void pool_channels_kernel(TapView t, int gch, int width, float inv, float* bins) {
+  __shared__ float part[32][65];
+  __shared__ float tot[64];
+  const int r = blockIdx.x;
+  if (r >= *t.count) return;
+  const long long n = t.data_idx ? t.data_idx[r] : r;
+  const int cs = blockIdx.y * 64;
+  const int g = threadIdx.x & 7, q = threadIdx.x >> 3;
+  const int R = (t.HW + 31) / 32;
+  const long long base = n * t.row_stride + cs + g * 8;
+  float s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int p = q * R; p < (q + 1) * R && p < t.HW; ++p) {
+    float v[8];
+    ld_tap8(t, base + static_cast<long long>(p) * t.C, v);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) s[e] += v[e];
+  }
+#pragma unroll
+  for (int e = 0; e < 8; ++e) part[q][g * 8 + e] = s[e];
+  __syncthreads();
+  if (threadIdx.x < 64) {
+    float a = 0.0f;
+    for (int k = 0; k < 32; ++k) a += part[k][threadIdx.x];
+    tot[threadIdx.x] = a;
+  }
+  __syncthreads();
+  const int nb = 64 / gch;
+  if (threadIdx.x < nb) {
+    float a = 0.0f;
+    for (int k = 0; k < gch; ++k) a += tot[threadIdx.x * gch + k];
+    bins[static_cast<long long>(r) * width + cs / gch + threadIdx.x] = a * inv;
+  }
+}
+
+// Generic: one thread per bin, sequential over its flat window.
+__global__ void pool_generic_kernel(TapView t, int win, int width, float inv, float* bins) {
+  const int r = blockIdx.x;
+  if (r >= *t.count) return;
+  const long long n = t.data_idx ? t.data_idx[r] : r;
+  for (int o = blockIdx.y * blockDim.x + threadIdx.x; o < width; o += gridDim.y * blockDim.x) {
+    float s = 0.0f;
+    for (long long f = static_cast<long long>(o) * win; f < static_cast<long long>(o + 1) * win; ++f) {
+      const long long off = (f % t.HW) * t.C + f / t.HW;
+      s += ld_tap(t, n * t.row_stride + off);
+    }
+    bins[static_cast<long long>(r) * width + o] = s * inv;
+  }
+}
+
+// ------------------------------------------------------------------ conv1d
+// Reference Conv(k,s) predictor (cache.cpp:126-131): y[o] = relu(b1 +
+// sum_t w1[t] x[o*s+t]) over the flat tap, then logits = W2 y + b2. Each CTA
+// stages a chunk of the flat tap (plus a k-1 halo) in shared memory and
+// emits per-chunk partial logits (summed in a fixed order by the head).
+__global__ void conv1d_partials_kernel(TapView t, long long D, int kernel, int stride, int out_dim, const float* w1,
+                                       float b1, const float* W2, int classes, int chunk_elems, int nchunks,
+                                       float* partials) {
+  extern __shared__ float xs[];
+  __shared__ float red[32];
+  const int r = blockIdx.x;
+  if (r >= *t.count) return;
+  const long long n = t.data_idx ? t.data_idx[r] : r;
+  const int chunk = blockIdx.y;
+  const long long f0 = static_cast<long long>(chunk) * chunk_elems;
+  const long long f1 = f0 + chunk_elems < D ? f0 + chunk_elems : D;
+  const long long fe = f1 + kernel - 1 < D ? f1 + kernel - 1 : D;
+  const long long len = fe - f0;
+  const long long rowb = n * t.row_stride;
+  if (t.HW == 1) {
+    for (long long i = threadIdx.x; i < len; i += blockDim.x) xs[i] = ld_tap(t, rowb + f0 + i);
+  } else {
+    // chunk_elems is a whole number of channels: walk (pixel, channel) with
+    // the channel fastest so consecutive threads read consecutive addresses.
+    const long long c0 = f0 / t.HW;
+    const long long cb = (f1 - f0 + t.HW - 1) / t.HW;
+    const long long body = cb * t.HW;
+    for (long long i = threadIdx.x; i < body; i += blockDim.x) {
+      const long long cl = i % cb, p = i / cb;
+      const long long f = (c0 + cl) * t.HW + p;
+      if (f < f1) xs[f - f0] = ld_tap(t, rowb + p * t.C + c0 + cl);
+    }
+    for (long long f = f1 + threadIdx.x; f < fe; f += blockDim.x) {
+      xs[f - f0] = ld_tap(t, rowb + (f % t.HW) * t.C + f / t.HW);
+    }
+  }
+  __syncthreads();
+  const long long ob = (f0 + stride - 1) / stride;
+  long long oe = (f1 + stride - 1) / stride;
+  if (oe > out_dim) oe = out_dim;
+  for (int k0 = 0; k0 < classes; k0 += 16) {
+    float acc[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) acc[k] = 0.0f;
+    for (long long o = ob + threadIdx.x; o < oe; o += blockDim.x) {
+      float y = b1;
+      const long long xb = o * stride - f0;
+      for (int tt = 0; tt < kernel; ++tt) y += w1[tt] * xs[xb + tt];
+      y = y > 0.0f ? y : 0.0f;
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+        if (k0 + k < classes) acc[k] += W2[static_cast<long long>(k0 + k) * out_dim + o] * y;
+    }
+    for (int k = 0; k < 16 && k0 + k < classes; ++k) {
+      const float s = block_sum(acc[k], red);
+      if (threadIdx.x == 0) partials[(static_cast<long long>(r) * nchunks + chunk) * classes + k0 + k] = s;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ head
+// Reference lookup (cache.cpp:259-265): pr = softmax(pred(tap)),
+// p = sigmoid(sel(pr)), hit = p >= delta (inclusive); label = argmax(pr).
+__global__ void cache_head_kernel(CacheHeadParams p) {
+  extern __shared__ float sm[];
+  __shared__ float red[32];
+  __shared__ float hsel[16];
+  __shared__ int best_idx_s[4];
+  __shared__ float best_val_s[4];
+  const int r = blockIdx.x;
+  if (r >= *p.count) return;
+  const int C = p.classes;
+  float* logits = sm;        // [C]
+  float* feat = sm + C;      // [feat]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+
+  if (p.family == 2) {
+    for (int k = tid; k < C; k += blockDim.x) {
+      float a = p.b2[k];
+      for (int c = 0; c < p.feat; ++c) a += p.feats[(static_cast<long long>(r) * p.feat + c) * C + k];
+      logits[k] = a;
+    }
+  } else {
+    if (p.family == 1) {
+      for (int o = tid; o < p.feat; o += blockDim.x) feat[o] = p.feats[static_cast<long long>(r) * p.feat + o];
+    } else {
+      for (int j = tid; j < p.feat; j += blockDim.x) {
+        float a = p.b1[j];
+        for (int s = 0; s < p.ks; ++s) a += p.feats[(static_cast<long long>(s) * p.rows_total + r) * p.hp + j];
+        feat[j] = a > 0.0f ? a : 0.0f;
+      }
+    }
+    __syncthreads();
+    for (int k = warp; k < C; k += nw) {
+      const float* wr = p.W2 + static_cast<long long>(k) * p.feat;
+      float a = 0.0f;
+      for (int o = lane; o < p.feat; o += 32) a += wr[o] * feat[o];
+      a = warp_sum(a);
+      if (lane == 0) logits[k] = a + p.b2[k];
+    }
+  }
+  __syncthreads();
+  // softmax (losses.cpp:35-46)
+  float m = -FLT_MAX;
+  for (int k = tid; k < C; k += blockDim.x) m = fmaxf(m, logits[k]);
+  m = block_max(m, red);
+  float part = 0.0f;
+  for (int k = tid; k < C; k += blockDim.x) part += expf(logits[k] - m);
+  const float sum = block_sum(part, red);
+  float* pr = feat;  // reuse
+  __syncthreads();
+  for (int k = tid; k < C; k += blockDim.x) pr[k] = expf(logits[k] - m) / sum;
+  __syncthreads();
+  // selector FC(C,16) + ReLU
+  for (int j = warp; j < 16; j += nw) {
+    const float* wr = p.Ws1 + j * C;
+    float a = 0.0f;
+    for (int k = lane; k < C; k += 32) a += wr[k] * pr[k];
+    a = warp_sum(a);
+    if (lane == 0) {
+      a += p.bs1[j];
+      hsel[j] = a > 0.0f ? a : 0.0f;
+    }
+  }
+  // argmax(pr), lowest index on ties (tensor.hpp:57-63)
+  float bv = -FLT_MAX;
+  int bi = 0x7fffffff;
+  for (int k = tid; k < C; k += blockDim.x) {
+    if (pr[k] > bv) {
+      bv = pr[k];
+      bi = k;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > bv || (ov == bv && oi < bi)) {
+      bv = ov;
+      bi = oi;
+    }
+  }
+  if (lane == 0) {
+    best_val_s[warp] = bv;
+    best_idx_s[warp] = bi;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    float v = best_val_s[0];
+    int i = best_idx_s[0];
+    for (int w = 1; w < nw; ++w)
+      if (best_val_s[w] > v || (best_val_s[w] == v && best_idx_s[w] < i)) {
+        v = best_val_s[w];
+        i = best_idx_s[w];
+      }
+    float z = p.bs2;
+    for (int j = 0; j < 16; ++j) z += p.ws2[j] * hsel[j];
+    float q;
+    if (z >= 0.0f) {
+      q = 1.0f / (1.0f + expf(-z));
+    } else {
+      const float e = expf(z);
+      q = e / (1.0f + e);
+    }
+    p.prob[r] = q;
+    p.hit[r] = static_cast<double>(q) >= p.delta ? 1 : 0;
+    p.label[r] = i;
+  }
+  if (p.pr_out)
+    for (int k = tid; k < C; k += blockDim.x) p.pr_out[static_cast<long long>(r) * C + k] = pr[k];
+  if (p.logits_out)
+    for (int k = tid; k < C; k += blockDim.x) p.logits_out[static_cast<long long>(r) * C + k] = logits[k];
+}
+
+// ------------------------------------------------------------------ exit
+__global__ void exit_compact_kernel(int layer, const int* count_in, const int* ids_in, const int* hit, const int* label,
+                                    const float* prob, int* exit_layer, int* served, unsigned long long* exit_ns,
+                                    float* probs_out, int* ids_out, int* src_rows_out, int* count_out, int shadow) {
+  __shared__ int warp_tot[32];
+  __shared__ int base_s;
+  const int n = *count_in;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) base_s = 0;
+  __syncthreads();
+  const unsigned long long now = globaltimer();
+  for (int c0 = 0; c0 < n; c0 += blockDim.x) {
+    const int r = c0 + tid;
+    const bool valid = r < n;
+    const bool h = valid && hit[r];
+    const int id = valid ? ids_in[r] : -1;
+    if (valid) {
+      if (probs_out) probs_out[id] = prob[r];
+      if (h && exit_layer[id] == 0) {
+        exit_layer[id] = layer;
+        served[id] = label[r];
+        exit_ns[id] = now;
+      }
+    }
+    const bool keep = valid && (shadow || !h);
+    const unsigned mask = __ballot_sync(0xffffffffu, keep);
+    const int pos_in_warp = __popc(mask & ((1u << lane) - 1u));
+    if (lane == 0) warp_tot[warp] = __popc(mask);
+    __syncthreads();
+    if (warp == 0) {
+      const int nw = blockDim.x >> 5;
+      int v = lane < nw ? warp_tot[lane] : 0;
+      // inclusive scan
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += u;
+      }
+      if (lane < nw) warp_tot[lane] = v;  // inclusive prefix
+    }
+    __syncthreads();
+    const int warp_off = warp == 0 ? 0 : warp_tot[warp - 1];
+    const int base = base_s;
+    if (keep) {
+      ids_out[base + warp_off + pos_in_warp] = id;
+      if (src_rows_out) src_rows_out[base + warp_off + pos_in_warp] = r;
+    }
+    __syncthreads();
+    if (tid == 0) base_s = base + warp_tot[(blockDim.x >> 5) - 1];
+    __syncthreads();
+  }
+  if (tid == 0) *count_out = base_s;
+}
+
+__global__ void gather_rows_kernel(const __nv_bfloat16* src_hi, const __nv_bfloat16* src_lo, __nv_bfloat16* dst_hi,
+                                   __nv_bfloat16* dst_lo, long long row_elems, const int* src_rows, const int* count) {
+  const int j = blockIdx.x;
+  if (j >= *count) return;
+  const long long s = src_rows[j];
+  const uint4* sh = reinterpret_cast<const uint4*>(src_hi + s * row_elems);
+  uint4* dh = reinterpret_cast<uint4*>(dst_hi + static_cast<long long>(j) * row_elems);
+  const long long nv = row_elems / 8;
+  for (long long i = blockIdx.y * blockDim.x + threadIdx.x; i < nv; i += gridDim.y * blockDim.x) dh[i] = sh[i];
+  if (src_lo) {
+    const uint4* sl = reinterpret_cast<const uint4*>(src_lo + s * row_elems);
+    uint4* dl = reinterpret_cast<uint4*>(dst_lo + static_cast<long long>(j) * row_elems);
+    for (long long i = blockIdx.y * blockDim.x + threadIdx.x; i < nv; i += gridDim.y * blockDim.x) dl[i] = sl[i];
+  }
+}
+
+__global__ void split_rows_kernel(const float* x, int in_dim, int dp, const int* ids, const int* count,
+                                  __nv_bfloat16* hi, __nv_bfloat16* lo) {
+  const int j = blockIdx.x;
+  if (j >= *count) return;
+  const long long src = ids ? ids[j] : j;
+  for (int i = threadIdx.x; i < dp; i += blockDim.x) {
+    const float v = i < in_dim ? x[src * in_dim + i] : 0.0f;
+    split_store(v, hi, lo, static_cast<long long>(j) * dp + i);
+  }
+}
+
+__global__ void split_taps_nchw_kernel(const float* x, int C, int HW, long long row_stride, __nv_bfloat16* hi,
+                                       __nv_bfloat16* lo) {
+  const int r = blockIdx.x;
+  const long long D = static_cast<long long>(C) * HW;
+  for (long long i = blockIdx.y * blockDim.x + threadIdx.x; i < row_stride; i += gridDim.y * blockDim.x) {
+    // storage index i = p*C + c  <-  flat f = c*HW + p
+    float v = 0.0f;
+    if (i < D) {
+      const long long p = i / C, c = i % C;
+      v = x[r * D + c * HW + p];
+    }
+    split_store(v, hi, lo, r * row_stride + i);
+  }
+}
+
+// Base head (base_model.cpp:48-49): logits -> softmax -> argmax (serving.cpp:108).
+template <bool kGap>
+__global__ void base_head_kernel(const __nv_bfloat16* hi, const __nv_bfloat16* lo, long long row_stride, int C, int HW,
+                                 const float* W, const float* b, int classes, const int* ids, const int* count,
+                                 int* base_pred, float* logits_out, int* exit_layer, int* served,
+                                 unsigned long long* exit_ns) {
+  extern __shared__ float sm[];
+  __shared__ float red[32];
+  __shared__ int bi_s[32];
+  __shared__ float bv_s[32];
+  const int r = blockIdx.x;
+  if (r >= *count) return;
+  const int id = ids[r];
+  const long long n = kGap ? id : r;
+  float* feat = sm;          // [C]
+  float* logits = sm + C;    // [classes]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  TapView t;
+  t.hi = hi;
+  t.lo = lo;
+  for (int c = tid; c < C; c += blockDim.x) {
+    if (kGap) {
+      float a = 0.0f;
+      for (int q = 0; q < HW; ++q) a += ld_tap(t, n * row_stride + static_cast<long long>(q) * C + c);
+      feat[c] = a * (1.0f / HW);
+    } else {
+      feat[c] = ld_tap(t, n * row_stride + c);
+    }
+  }
+  __syncthreads();
+  for (int k = warp; k < classes; k += nw) {
+    const float* wr = W + static_cast<long long>(k) * C;
+    float a = 0.0f;
+    for (int c = lane; c < C; c += 32) a += wr[c] * feat[c];
+    a = warp_sum(a);
+    if (lane == 0) logits[k] = a + b[k];
+  }
+  __syncthreads();
+  float m = -FLT_MAX;
+  for (int k = tid; k < classes; k += blockDim.x) m = fmaxf(m, logits[k]);
+  m = block_max(m, red);
+  float part = 0.0f;
+  for (int k = tid; k < classes; k += blockDim.x) part += expf(logits[k] - m);
+  const float sum = block_sum(part, red);
+  float bv = -FLT_MAX;
+  int bi = 0x7fffffff;
+  for (int k = tid; k < classes; k += blockDim.x) {
+    const float pk = expf(logits[k] - m) / sum;
+    if (pk > bv) {
+      bv = pk;
+      bi = k;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > bv || (ov == bv && oi < bi)) {
+      bv = ov;
+      bi = oi;
+    }
+  }
+  if (lane == 0) {
+    bv_s[warp] = bv;
+    bi_s[warp] = bi;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    float v = bv_s[0];
+    int i = bi_s[0];
+    for (int w = 1; w < nw; ++w)
+      if (bv_s[w] > v || (bv_s[w] == v && bi_s[w] < i)) {
+        v = bv_s[w];
+        i = bi_s[w];
+      }
+    base_pred[id] = i;
+    if (exit_layer[id] == 0) {
+      served[id] = i;
+      exit_ns[id] = globaltimer();
+    }
+  }
+  if (logits_out)
+    for (int k = tid; k < classes; k += blockDim.x) logits_out[static_cast<long long>(id) * classes + k] = logits[k];
+}
+
+__global__ void stem_im2col_kernel(const float* x, const int* count, int C, int H, int W, int k, int stride, int pad,
+                                   int Ho, int Wo, int Kp, __nv_bfloat16* hi, __nv_bfloat16* lo) {
+  const long long total = static_cast<long long>(*count) * Ho * Wo * Kp;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int kk = static_cast<int>(i % Kp);
+    const long long m = i / Kp;
+    const int ow = static_cast<int>(m % Wo);
+    const int oh = static_cast<int>((m / Wo) % Ho);
+    const long long n = m / (static_cast<long long>(Wo) * Ho);
+    float v = 0.0f;
+    if (kk < k * k * C) {
+      const int c = kk % C, rs = kk / C, s = rs % k, r = rs / k;
+      const int ih = oh * stride + r - pad, iw = ow * stride + s - pad;
+      if (ih >= 0 && ih < H && iw >= 0 && iw < W) v = x[((n * C + c) * H + ih) * W + iw];
+    }
+    split_store(v, hi, lo, i);
+  }
+}
+
+__global__ void phase_split_kernel(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int H, int W, int C, int N,
+                                   int Hs, int Ws, const int* ids, const int* count, __nv_bfloat16* ohi,
+                                   __nv_bfloat16* olo) {
+  const int j = blockIdx.x;
+  if (j >= *count) return;
+  const long long n = ids[j];
+  const int cv = C / 8;
+  const long long per = 4LL * Hs * Ws * cv;
+  for (long long i = blockIdx.y * blockDim.x + threadIdx.x; i < per; i += gridDim.y * blockDim.x) {
+    const int c8 = static_cast<int>(i % cv);
+    long long rest = i / cv;
+    const int jj = static_cast<int>(rest % Ws);
+    rest /= Ws;
+    const int ii = static_cast<int>(rest % Hs);
+    const int ph = static_cast<int>(rest / Hs);
+    const int h = 2 * ii + (ph >> 1), w = 2 * jj + (ph & 1);
+    const long long dst = ((((static_cast<long long>(ph) * N + n) * Hs + ii) * Ws + jj) * C) + c8 * 8;
+    uint4 vh = make_uint4(0, 0, 0, 0), vl = make_uint4(0, 0, 0, 0);
+    if (h < H && w < W) {
+      const long long src = ((n * H + h) * W + w) * C + c8 * 8;
+      vh = *reinterpret_cast<const uint4*>(hi + src);
+      if (lo) vl = *reinterpret_cast<const uint4*>(lo + src);
+    }
+    *reinterpret_cast<uint4*>(ohi + dst) = vh;
+    if (olo) *reinterpret_cast<uint4*>(olo + dst) = vl;
+  }
+}
+
+__global__ void maxpool_kernel(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int H, int W, int C, int k, int stride,
+                               int pad, int Ho, int Wo, const int* ids, const int* count, __nv_bfloat16* ohi,
+                               __nv_bfloat16* olo) {
+  const int j = blockIdx.x;
+  if (j >= *count) return;
+  const long long n = ids[j];
+  const long long per = static_cast<long long>(Ho) * Wo * C;
+  for (long long i = blockIdx.y * blockDim.x + threadIdx.x; i < per; i += gridDim.y * blockDim.x) {
+    const int c = static_cast<int>(i % C);
+    const int ow = static_cast<int>((i / C) % Wo);
+    const int oh = static_cast<int>(i / (static_cast<long long>(C) * Wo));
+    float best = -FLT_MAX;
+    __nv_bfloat16 bh = __float2bfloat16_rn(0.0f), bl = __float2bfloat16_rn(0.0f);
+    for (int r = 0; r < k; ++r)
+      for (int s = 0; s < k; ++s) {
+        const int ih = oh * stride + r - pad, iw = ow * stride + s - pad;
+        if (ih < 0 || ih >= H || iw < 0 || iw >= W) continue;
+        const long long src = ((n * H + ih) * W + iw) * C + c;
+        const __nv_bfloat16 vh = hi[src];
+        const __nv_bfloat16 vl = lo ? lo[src] : __float2bfloat16_rn(0.0f);
+        const float v = __bfloat162float(vh) + __bfloat162float(vl);
+        if (v > best) {
+          best = v;
+          bh = vh;
+          bl = vl;
+        }
+      }
+    const long long dst = ((n * Ho + oh) * Wo + ow) * C + c;
+    ohi[dst] = bh;
+    if (olo) olo[dst] = bl;
+  }
+}
+
+__global__ void stamp_kernel(unsigned long long* t0) { *t0 = globaltimer(); }
+
+__global__ void init_batch_kernel(const int* batch, int max_batch, int* ids0, int* count0, int* rows_out, int rows_mult,
+                                  int* exit_layer, int* served, int* base_pred, unsigned long long* exit_ns,
+                                  float* probs, int L) {
+  const int B = *batch;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < max_batch; i += gridDim.x * blockDim.x) {
+    ids0[i] = i;
+    exit_layer[i] = 0;
+    served[i] = -1;
+    base_pred[i] = -1;
+    exit_ns[i] = 0;
+    for (int l = 0; l < L; ++l) probs[static_cast<long long>(l) * max_batch + i] = __int_as_float(0x7fc00000);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *count0 = B;
+    if (rows_out) *rows_out = B * rows_mult;
+  }
+}
+
+}  // namespace
+
+void launch_pool_bins(const TapView& tap, int max_rows, int win, int width, float* bins, cudaStream_t s) {
+  const float inv = static_cast<float>(1.0 / win);
+  if (max_rows <= 0) return;
+  if (tap.HW > 1 && tap.C % 64 == 0 && win <= tap.HW && tap.HW % win == 0 && tap.HW / win >= 32) {
+    pool_strips_kernel<<<dim3(max_rows, tap.C / 64), 256, 0, s>>>(tap, win, width, inv, bins);
+  } else if (tap.HW > 1 && tap.C % 64 == 0 && win % tap.HW == 0 && 64 % (win / tap.HW) == 0) {
+    pool_channels_kernel<<<dim3(max_rows, tap.C / 64), 256, 0, s>>>(tap, win / tap.HW, width, inv, bins);
+  } else {
+    const int gy = (width + 255) / 256 < 64 ? (width + 255) / 256 : 64;
+    pool_generic_kernel<<<dim3(max_rows, gy), 256, 0, s>>>(tap, win, width, inv, bins);
+  }
+}
+
+void launch_conv1d_partials(const TapView& tap, int max_rows, long long D, int kernel, int stride, int out_dim,
+                            const float* w1, float b1, const float* W2, int classes, int chunk_elems, int nchunks,
+                            float* partials, cudaStream_t s) {
+  if (max_rows <= 0) return;
+  const size_t smem = static_cast<size_t>(chunk_elems + kernel) * sizeof(float);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(conv1d_partials_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  conv1d_partials_kernel<<<dim3(max_rows, nchunks), 256, smem, s>>>(tap, D, kernel, stride, out_dim, w1, b1, W2,
+                                                                    classes, chunk_elems, nchunks, partials);
+}
+
+void launch_cache_head(const CacheHeadParams& p, int max_rows, cudaStream_t s) {
+  if (max_rows <= 0) return;
+  const int feat_len = p.family == 2 ? p.classes : (p.feat > p.classes ? p.feat : p.classes);
+  const size_t smem = static_cast<size_t>(p.classes + feat_len) * sizeof(float);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(cache_head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  cache_head_kernel<<<max_rows, 128, smem, s>>>(p);
+}
+
+void launch_exit_compact(int layer, const int* count_in, const int* ids_in, const int* hit, const int* label,
+                         const float* prob, int* exit_layer, int* served, unsigned long long* exit_ns, float* probs_out,
+                         int* ids_out, int* src_rows_out, int* count_out, int shadow, cudaStream_t s) {
+  exit_compact_kernel<<<1, 1024, 0, s>>>(layer, count_in, ids_in, hit, label, prob, exit_layer, served, exit_ns,
+                                         probs_out, ids_out, src_rows_out, count_out, shadow);
+}
+
+void launch_gather_rows(const __nv_bfloat16* src_hi, const __nv_bfloat16* src_lo, __nv_bfloat16* dst_hi,
+                        __nv_bfloat16* dst_lo, long long row_elems, const int* src_rows, const int* count, int max_rows,
+                        cudaStream_t s) {
+  if (max_rows <= 0) return;
+  const long long nv = row_elems / 8;
+  int gy = static_cast<int>((nv + 255) / 256);
+  if (gy > 64) gy = 64;
+  gather_rows_kernel<<<dim3(max_rows, gy), 256, 0, s>>>(src_hi, src_lo, dst_hi, dst_lo, row_elems, src_rows, count);
+}
+
+void launch_split_rows(const float* x, int in_dim, int dp, const int* ids, const int* count, int max_rows,
+                       __nv_bfloat16* hi, __nv_bfloat16* lo, cudaStream_t s) {
+  if (max_rows <= 0) return;
+  split_rows_kernel<<<max_rows, 256, 0, s>>>(x, in_dim, dp, ids, count, hi, lo);
+}
+
+void launch_split_taps_nchw(const float* x, int C, int HW, int rows, long long row_stride, __nv_bfloat16* hi,
+                            __nv_bfloat16* lo, cudaStream_t s) {
+  if (rows <= 0) return;
+  int gy = static_cast<int>((row_stride + 255) / 256);
+  if (gy > 128) gy = 128;
+  split_taps_nchw_kernel<<<dim3(rows, gy), 256, 0, s>>>(x, C, HW, row_stride, hi, lo);
+}
+
+void launch_mlp_head(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int dp, int dim, const float* W, const float* b,
+                     int classes, const int* ids, const int* count, int max_rows, int* base_pred, float* logits_out,
+                     int* exit_layer, int* served, unsigned long long* exit_ns, cudaStream_t s) {
+  if (max_rows <= 0) return;
+  const size_t smem = static_cast<size_t>(dim + classes) * sizeof(float);
+  base_head_kernel<false><<<max_rows, 128, smem, s>>>(hi, lo, dp, dim, 1, W, b, classes, ids, count, base_pred,
+                                                      logits_out, exit_layer, served, exit_ns);
+}
+
+void launch_cnn_head(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int C, int HW, const float* W, const float* b,
+                     int classes, const int* ids, const int* count, int max_rows, int* base_pred, float* logits_out,
+                     int* exit_layer, int* served, unsigned long long* exit_ns, cudaStream_t s) {
+  if (max_rows <= 0) return;
+  const size_t smem = static_cast<size_t>(C + classes) * sizeof(float);
+  base_head_kernel<true><<<max_rows, 256, smem, s>>>(hi, lo, static_cast<long long>(C) * HW, C, HW, W, b, classes, ids,
+                                                     count, base_pred, logits_out, exit_layer, served, exit_ns);
+}
+
+void launch_stem_im2col(const float* x, const int* count, int max_n, int C, int H, int W, int k, int stride, int pad,
+                        int Ho, int Wo, int Kp, __nv_bfloat16* hi, __nv_bfloat16* lo, cudaStream_t s) {
+  const long long total = static_cast<long long>(max_n) * Ho * Wo * Kp;
+  long long blocks = (total + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  if (blocks < 1) blocks = 1;
+  stem_im2col_kernel<<<static_cast<int>(blocks), 256, 0, s>>>(x, count, C, H, W, k, stride, pad, Ho, Wo, Kp, hi, lo);
+}
+
+void launch_phase_split(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int H, int W, int C, int N, int Hs, int Ws,
+                        const int* ids, const int* count, int max_rows, __nv_bfloat16* ohi, __nv_bfloat16* olo,
+                        cudaStream_t s) {
+  if (max_rows <= 0) return;
+  const long long per = 4LL * Hs * Ws * (C / 8);
+  int gy = static_cast<int>((per + 255) / 256);
+  if (gy > 64) gy = 64;
+  phase_split_kernel<<<dim3(max_rows, gy), 256, 0, s>>>(hi, lo, H, W, C, N, Hs, Ws, ids, count, ohi, olo);
+}
+
+void launch_maxpool(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int H, int W, int C, int k, int stride, int pad,
+                    int Ho, int Wo, const int* ids, const int* count, int max_rows, __nv_bfloat16* ohi,
+                    __nv_bfloat16* olo, cudaStream_t s) {
+  if (max_rows <= 0) return;
+  const long long per = static_cast<long long>(Ho) * Wo * C;
+  int gy = static_cast<int>((per + 255) / 256);
+  if (gy > 128) gy = 128;
+  maxpool_kernel<<<dim3(max_rows, gy), 256, 0, s>>>(hi, lo, H, W, C, k, stride, pad, Ho, Wo, ids, count, ohi, olo);
+}
+
+void launch_stamp_start(unsigned long long* t0, cudaStream_t s) { stamp_kernel<<<1, 1, 0, s>>>(t0); }
+
+void launch_init_batch(const int* batch, int max_batch, int* ids0, int* count0, int* rows_out, int rows_mult,
+                       int* exit_layer, int* served, int* base_pred, unsigned long long* exit_ns, float* probs, int L,
+                       cudaStream_t s) {
+  const int blocks = (max_batch + 255) / 256 > 0 ? (max_batch + 255) / 256 : 1;
+  init_batch_kernel<<<blocks, 256, 0, s>>>(batch, max_batch, ids0, count0, rows_out, rows_mult, exit_layer, served,
+                                           base_pred, exit_ns, probs, L);
+}
+
+}  // namespace lcb

@@ -1,0 +1,112 @@
+// Serve-path kernels other than the tensor-core contractions: the learned-cache
+// lookup heads (reference lookup(), cache.cpp:259-265), the first-hit exit
+// and stream compaction (serve_one, serving.cpp:112-121), and the CNN glue
+// (stem im2col, stride-2 phase split, max-pool, GAP+FC head).
+//
+// Tap addressing: every tap is an activation stored hi (+lo) bf16 with
+// `row_stride` elements per request and, inside a row, NHWC order (C
+// innermost). The reference's caches see the NCHW-flattened vector, so flat
+// index f maps to storage offset (f % HW) * C + f / HW (for MLP taps HW == 1,
+// which is the identity).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace lcb {
+
+struct TapView {
+  const __nv_bfloat16* hi;
+  const __nv_bfloat16* lo;  // nullable (bf16 tier)
+  long long row_stride;     // elements per request row
+  int C, HW;                // channels, pixels (MLP: C = dim, HW = 1)
+  const int* data_idx;      // row r -> storage row (nullable = r)
+  const int* count;         // rows in this layer
+};
+
+// Per-row cache head inputs (one of three predictor families).
+struct CacheHeadParams {
+  int family;              // 0 = FC(h), 1 = Pool(width), 2 = Conv(k,s)
+  int classes;
+  int feat;                // pool: width; fc: hidden h; conv: number of chunks
+  const float* feats;      // pool: bins [rows][feat]; fc: partials [ks][rows_total][hp]; conv: partials [rows][chunks][classes]
+  int ks;                  // fc split-K factor
+  int hp;                  // fc padded hidden stride
+  long long rows_total;    // fc partial row stride
+  const float* b1;         // fc: hidden bias [h]
+  const float* W2;         // pool: [classes][width]; fc: [classes][h]
+  const float* b2;         // [classes]
+  const float* Ws1;        // selector FC(C,16): [16][classes]
+  const float* bs1;        // [16]
+  const float* ws2;        // FC(16,1): [16]
+  float bs2;
+  double delta;
+  const int* count;
+  // outputs (row-indexed)
+  float* prob;             // [rows] selector probability
+  int* hit;                // [rows]
+  int* label;              // [rows] argmax(pr)
+  float* pr_out;           // nullable [rows][classes]
+  float* logits_out;       // nullable [rows][classes]
+};
+
+void launch_pool_bins(const TapView& tap, int max_rows, int win, int width, float* bins, cudaStream_t s);
+void launch_conv1d_partials(const TapView& tap, int max_rows, long long D, int kernel, int stride, int out_dim,
+                            const float* w1, float b1, const float* W2, int classes, int chunk_elems, int nchunks,
+                            float* partials, cudaStream_t s);
+void launch_cache_head(const CacheHeadParams& p, int max_rows, cudaStream_t s);
+
+// First-hit exit + stable stream compaction (single CTA, warp ballot +
+// block prefix sum). Rows with hit leave; `ids_in[r]` is the original request
+// id of row r. Writes ids_out/src_rows_out (kept rows in order) and count_out.
+// shadow != 0: every row stays (probing continues) but only the first hit of
+// each request is recorded.
+void launch_exit_compact(int layer, const int* count_in, const int* ids_in, const int* hit, const int* label,
+                         const float* prob, int* exit_layer, int* served, unsigned long long* exit_ns,
+                         float* probs_out /*[B] for this layer*/, int* ids_out, int* src_rows_out, int* count_out,
+                         int shadow, cudaStream_t s);
+
+// Copies rows src_rows[j] of src into row j of dst (hi and lo planes).
+void launch_gather_rows(const __nv_bfloat16* src_hi, const __nv_bfloat16* src_lo, __nv_bfloat16* dst_hi,
+                        __nv_bfloat16* dst_lo, long long row_elems, const int* src_rows, const int* count,
+                        int max_rows, cudaStream_t s);
+
+// fp32 rows [rows][in_dim] (row stride in_dim) -> hi/lo bf16 [rows][dp],
+// zero padded; row j comes from src row ids[j] (nullable = j).
+void launch_split_rows(const float* x, int in_dim, int dp, const int* ids, const int* count, int max_rows,
+                       __nv_bfloat16* hi, __nv_bfloat16* lo, cudaStream_t s);
+// fp32 NCHW-flat taps -> hi/lo NHWC storage (lookup-only entry point).
+void launch_split_taps_nchw(const float* x, int C, int HW, int rows, long long row_stride, __nv_bfloat16* hi,
+                            __nv_bfloat16* lo, cudaStream_t s);
+
+// MLP head: logits = W [classes][dim] . act + b, softmax, argmax -> base_pred.
+void launch_mlp_head(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int dp, int dim, const float* W, const float* b,
+                     int classes, const int* ids, const int* count, int max_rows, int* base_pred, float* logits_out,
+                     int* exit_layer, int* served, unsigned long long* exit_ns, cudaStream_t s);
+// CNN head: GAP over HW then FC [classes][C] + b, softmax, argmax.
+void launch_cnn_head(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int C, int HW, const float* W, const float* b,
+                     int classes, const int* ids, const int* count, int max_rows, int* base_pred, float* logits_out,
+                     int* exit_layer, int* served, unsigned long long* exit_ns, cudaStream_t s);
+
+// Stem: NCHW fp32 images -> im2col rows [(n*Ho+oh)*Wo+ow][Kp] hi/lo with K
+// order (r, s, c), zero padded to Kp.
+void launch_stem_im2col(const float* x, const int* count, int max_n, int C, int H, int W, int k, int stride, int pad,
+                        int Ho, int Wo, int Kp, __nv_bfloat16* hi, __nv_bfloat16* lo, cudaStream_t s);
+// Stride-2 phase split of survivors: [N,H,W,C] -> [4][N][Hs][Ws][C].
+void launch_phase_split(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int H, int W, int C, int N, int Hs, int Ws,
+                        const int* ids, const int* count, int max_rows, __nv_bfloat16* ohi, __nv_bfloat16* olo,
+                        cudaStream_t s);
+void launch_maxpool(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int H, int W, int C, int k, int stride, int pad,
+                    int Ho, int Wo, const int* ids, const int* count, int max_rows, __nv_bfloat16* ohi,
+                    __nv_bfloat16* olo, cudaStream_t s);
+
+void launch_stamp_start(unsigned long long* t0, cudaStream_t s);
+// Batch prologue: B = *batch; ids0 = identity, count0 = B, rows_out = B *
+// rows_mult (stem GEMM rows, nullable), outputs reset, probs [L][max_batch] = NaN.
+void launch_init_batch(const int* batch, int max_batch, int* ids0, int* count0, int* rows_out, int rows_mult,
+                       int* exit_layer, int* served, int* base_pred, unsigned long long* exit_ns, float* probs, int L,
+                       cudaStream_t s);
+
+}  // namespace lcb
