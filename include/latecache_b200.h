@@ -131,6 +131,9 @@ int lc_engine_set_delta(lc_engine* e, int layer, double delta);
 int lc_engine_set_selector_out(lc_engine* e, int layer, double gain, double bias);
 /* Device input buffer [max_batch][input_dim] fp32 (images: NCHW). */
 int lc_engine_input(lc_engine* e, float** device_ptr);
+/* Copy B requests' inputs into that buffer (on the engine stream, synchronous);
+ * src is a device pointer when on_device != 0, else host memory. */
+int lc_engine_stage_input(lc_engine* e, const float* src, int B, int on_device);
 
 /* simulate_model -> serve_one (serving.cpp:97-158) for one batch of B requests,
  * end to end from HOST buffers: inputs [B][input_dim] fp32 in; per request
@@ -156,8 +159,15 @@ int lc_lookup_batch(lc_engine* e, int layer, const float* taps, int B, int* hit,
 
 /* Device time of `iters` graph replays of a B-request batch (CUDA events on the engine stream). */
 int lc_engine_time(lc_engine* e, int B, unsigned flags, int iters, double* ms_per_batch);
+/* One batch from lc_engine_input(), CUDA events around it on the engine stream; synchronous. */
+int lc_serve_timed(lc_engine* e, int B, unsigned flags, double* ms);
 /* Kernel launches per batch of the given kind (-1 all, 1 tensor-core, 2 lookup, 3 exit/compaction). */
 int lc_engine_kernel_count(lc_engine* e, unsigned flags, int kind);
+/* One batch with CUDA events around every step (no graph): per step its kind,
+ * device ms, algorithmic FLOPs and bytes (per-unit figure x surviving units).
+ * Writes at most `cap` entries; *n = number of steps. */
+int lc_engine_profile(lc_engine* e, int B, unsigned flags, int cap, int* n, int* kinds, double* ms, double* flops,
+                      double* bytes);
 
 #ifdef __cplusplus
 #pragma GCC visibility pop

@@ -89,6 +89,9 @@ def _load() -> C.CDLL:
         "lc_lookup_batch": (I, [P, I, pF, I, pI, pI, pF, pF, pF]),
         "lc_engine_time": (I, [P, I, C.c_uint, I, pD]),
         "lc_engine_kernel_count": (I, [P, C.c_uint, I]),
+        "lc_engine_profile": (I, [P, I, C.c_uint, I, pI, pI, pD, pD, pD]),
+        "lc_serve_timed": (I, [P, I, C.c_uint, pD]),
+        "lc_engine_stage_input": (I, [P, P, I, I]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -128,5 +131,5 @@ EXPORTED_SYMBOLS = [
     "lc_plan_check", "lc_gen_workload", "lc_nearest_rank", "lc_engine_create", "lc_engine_destroy",
     "lc_engine_set_delta", "lc_engine_set_selector_out", "lc_engine_input", "lc_serve_batch", "lc_serve_device",
     "lc_engine_sync", "lc_engine_results", "lc_engine_counts", "lc_lookup_batch", "lc_engine_time",
-    "lc_engine_kernel_count",
+    "lc_engine_kernel_count", "lc_engine_profile", "lc_serve_timed", "lc_engine_stage_input",
 ]

@@ -321,12 +321,22 @@ class Deployment:
         check(lib.lc_serve_batch(self._h, _fptr(x), B, flags, _iptr(el), _iptr(sv), _iptr(bp), _fptr(pr), _dptr(lat)))
         return ServeResult(el, sv, bp, pr, lat)
 
+    def stage_input_device(self, src_ptr: int, B: int) -> None:
+        """Copy B inputs from device memory (raw pointer) into the engine's input buffer."""
+        check(lib.lc_engine_stage_input(self._h, C.c_void_p(src_ptr), B, 1))
+
     def serve_device(self, B: int, shadow: bool = False, graph: bool = True) -> None:
         flags = (LC_SERVE_SHADOW if shadow else 0) | (0 if graph else LC_SERVE_NO_GRAPH)
         check(lib.lc_serve_device(self._h, B, flags))
 
     def sync(self) -> None:
         check(lib.lc_engine_sync(self._h))
+
+    def serve_timed(self, B: int, shadow: bool = False) -> float:
+        """One batch from the device input buffer; device ms (CUDA events on the engine stream)."""
+        ms = C.c_double()
+        check(lib.lc_serve_timed(self._h, B, LC_SERVE_SHADOW if shadow else 0, C.byref(ms)))
+        return ms.value
 
     def results(self, B: int) -> ServeResult:
         el = np.zeros(B, np.int32)
@@ -362,6 +372,20 @@ class Deployment:
 
     def kernel_count(self, shadow: bool = False, kind: int = -1) -> int:
         return int(lib.lc_engine_kernel_count(self._h, LC_SERVE_SHADOW if shadow else 0, kind))
+
+    def profile(self, B: int, shadow: bool = False) -> Dict[str, np.ndarray]:
+        """Per-step device ms + algorithmic FLOPs/bytes of one batch (no graph).
+        kind: 0 other, 1 tensor-core contraction, 2 lookup, 3 exit/compaction."""
+        cap = 4096
+        n = C.c_int()
+        kinds = np.zeros(cap, np.int32)
+        ms = np.zeros(cap)
+        fl = np.zeros(cap)
+        by = np.zeros(cap)
+        check(lib.lc_engine_profile(self._h, B, LC_SERVE_SHADOW if shadow else 0, cap, C.byref(n), _iptr(kinds),
+                                    _dptr(ms), _dptr(fl), _dptr(by)))
+        k = n.value
+        return {"kind": kinds[:k], "ms": ms[:k], "flops": fl[:k], "bytes": by[:k]}
 
 
 @dataclass

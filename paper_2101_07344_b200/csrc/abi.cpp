@@ -390,6 +390,20 @@ int lc_engine_input(lc_engine* e, float** device_ptr) {
   });
 }
 
+int lc_engine_stage_input(lc_engine* e, const float* src, int B, int on_device) {
+  return guard([&] {
+    need(src, "src");
+    lcb::Engine& en = eng(e);
+    if (B <= 0 || B > en.max_batch()) throw std::invalid_argument("stage_input: batch outside [1, max_batch]");
+    const size_t bytes = static_cast<size_t>(B) * static_cast<size_t>(en.input_dim()) * sizeof(float);
+    if (cudaSetDevice(en.device()) != cudaSuccess ||
+        cudaMemcpyAsync(en.input_buffer(), src, bytes, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                        en.stream()) != cudaSuccess ||
+        cudaStreamSynchronize(en.stream()) != cudaSuccess)
+      throw lcb::CudaFailure("stage_input: copy failed");
+  });
+}
+
 int lc_serve_batch(lc_engine* e, const float* inputs, int B, unsigned flags, int* exit_layer, int* served,
                    int* base_pred, float* probs, double* latency_ms) {
   return guard([&] {
@@ -454,9 +468,30 @@ int lc_engine_time(lc_engine* e, int B, unsigned flags, int iters, double* ms_pe
   });
 }
 
+int lc_serve_timed(lc_engine* e, int B, unsigned flags, double* ms) {
+  return guard([&] {
+    need(ms, "ms");
+    *ms = eng(e).serve_timed(B, (flags & LC_SERVE_SHADOW) != 0);
+  });
+}
+
 int lc_engine_kernel_count(lc_engine* e, unsigned flags, int kind) {
   if (!e || !e->e) return -1;
   return e->e->count_kernels((flags & LC_SERVE_SHADOW) != 0, kind);
+}
+
+int lc_engine_profile(lc_engine* e, int B, unsigned flags, int cap, int* n, int* kinds, double* ms, double* flops,
+                      double* bytes) {
+  return guard([&] {
+    const auto prof = eng(e).profile(B, (flags & LC_SERVE_SHADOW) != 0);
+    if (n) *n = static_cast<int>(prof.size());
+    for (size_t i = 0; i < prof.size() && static_cast<int>(i) < cap; ++i) {
+      if (kinds) kinds[i] = prof[i].kind;
+      if (ms) ms[i] = prof[i].ms;
+      if (flops) flops[i] = prof[i].flops;
+      if (bytes) bytes[i] = prof[i].bytes;
+    }
+  });
 }
 
 }  // extern "C"

@@ -370,18 +370,23 @@ void Engine::build_weights() {
 void Engine::add_lookup_steps(std::vector<Step>& steps, DevCache& c, const TapView& tap, int max_rows,
                               bool stage_gather) {
   DevCache* cp = &c;
+  const long long L2 = model_.num_blocks + 2;
+  const int cidx = (tap.count >= d_counts_ && tap.count < d_counts_ + L2) ? static_cast<int>(tap.count - d_counts_) : -1;
+  const double eb = prec_ == kPrecX3 ? 4.0 : 2.0;  // bytes per activation element (hi + lo planes)
+  const double tap_bytes = static_cast<double>(c.D) * eb;
   if (c.family == 1) {
     steps.push_back({[cp, tap, max_rows](cudaStream_t s) {
                        launch_pool_bins(tap, max_rows, cp->win, cp->width, cp->feats, s);
                      },
-                     2});
+                     2, 1, cidx, 0.0, tap_bytes + 4.0 * c.width});
   } else if (c.family == 2) {
     steps.push_back({[cp, tap, max_rows](cudaStream_t s) {
                        launch_conv1d_partials(tap, max_rows, cp->D, cp->kernel, cp->stride, cp->out_dim, cp->w1,
                                               cp->b1c, cp->W2, cp->classes, cp->chunk_elems, cp->nchunks, cp->feats,
                                               s);
                      },
-                     2});
+                     2, 1, cidx, 2.0 * (static_cast<double>(c.out_dim) * c.kernel + static_cast<double>(c.out_dim) * c.classes),
+                     tap_bytes});
   } else {
     // FC(h): hidden = W1 . tap as a split-K tensor-core GEMM over the rows.
     const __nv_bfloat16* a_hi = tap.hi;
@@ -394,7 +399,7 @@ void Engine::add_lookup_steps(std::vector<Step>& steps, DevCache& c, const TapVi
       steps.push_back({[g, tap, row_elems, idx, cnt, max_rows](cudaStream_t s) {
                          launch_gather_rows(tap.hi, tap.lo, g.hi, g.lo, row_elems, idx, cnt, max_rows, s);
                        },
-                       3});
+                       3, 1, cidx, 0.0, 2.0 * tap_bytes});
       a_hi = g.hi;
       a_lo = g.lo;
     }
@@ -426,7 +431,8 @@ void Engine::add_lookup_steps(std::vector<Step>& steps, DevCache& c, const TapVi
     prm->rows_total = max_rows;
     prm->out_f32 = c.feats;
     const int sms = num_sms_;
-    steps.push_back({[prm, BN, sms](cudaStream_t s) { ck(tc_conv_launch(*prm, BN, sms, s), "tc_conv (fc cache)"); }, 1});
+    steps.push_back({[prm, BN, sms](cudaStream_t s) { ck(tc_conv_launch(*prm, BN, sms, s), "tc_conv (fc cache)"); }, 1,
+                     1, cidx, 2.0 * static_cast<double>(c.D) * c.h, tap_bytes});
   }
   const int rows_total = max_rows;
   steps.push_back({[cp, tap, max_rows, rows_total](cudaStream_t s) {
@@ -454,7 +460,7 @@ void Engine::add_lookup_steps(std::vector<Step>& steps, DevCache& c, const TapVi
                      p.logits_out = cp->logits_out;
                      launch_cache_head(p, max_rows, s);
                    },
-                   2});
+                   2, 1, cidx, 0.0, 0.0});
 }
 
 // ------------------------------------------------------------------ MLP serve
@@ -514,7 +520,9 @@ void Engine::build_mlp_steps(std::vector<Step>& steps, bool shadow) {
     prm->out_hi = act.hi;
     prm->out_lo = act.lo;
     const int sms = num_sms_;
-    steps.push_back({[prm, BN, sms](cudaStream_t s) { ck(tc_conv_launch(*prm, BN, sms, s), "tc_conv (mlp)"); }, 1});
+    steps.push_back({[prm, BN, sms](cudaStream_t s) { ck(tc_conv_launch(*prm, BN, sms, s), "tc_conv (mlp)"); }, 1, 1,
+                     static_cast<int>(cur_count - d_counts_), 2.0 * f.in * f.out,
+                     (x3 ? 4.0 : 2.0) * (static_cast<double>(f.inp) + f.outp)});
     const int layer = b + 1;
     const int ci = cache_of_layer_[static_cast<size_t>(layer)];
     if (ci >= 0) {
@@ -626,7 +634,9 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow) {
       prm->relu = o.relu ? 1 : 0;
       prm->out_hi = out.hi;
       prm->out_lo = out.lo;
-      steps.push_back({[prm, BN, sms](cudaStream_t s) { ck(tc_conv_launch(*prm, BN, sms, s), "tc_conv (stem)"); }, 1});
+      steps.push_back({[prm, BN, sms](cudaStream_t s) { ck(tc_conv_launch(*prm, BN, sms, s), "tc_conv (stem)"); }, 1,
+                       1, 0, 2.0 * Ho * Wo * o.Cout * o.k * o.k * o.C,
+                       (x3 ? 4.0 : 2.0) * Ho * Wo * (static_cast<double>(dc.Kp) + o.Cout)});
     } else if (o.kind == CnnOpKind::MaxPool) {
       Planes in = slot_buf_[static_cast<size_t>(o.in)], out = slot_buf_[static_cast<size_t>(o.out)];
       const int Ho = o.Ho(), Wo = o.Wo();
@@ -707,7 +717,11 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow) {
             prm->tap_dw[t] = static_cast<signed char>((ow - pw) / 2);
           }
         }
-      steps.push_back({[prm, BN, sms](cudaStream_t s) { ck(tc_conv_launch(*prm, BN, sms, s), "tc_conv (conv)"); }, 1});
+      steps.push_back({[prm, BN, sms](cudaStream_t s) { ck(tc_conv_launch(*prm, BN, sms, s), "tc_conv (conv)"); }, 1,
+                       1, static_cast<int>(cur_count - d_counts_),
+                       2.0 * Ho * Wo * o.Cout * static_cast<double>(o.C) * o.k * o.k,
+                       (x3 ? 4.0 : 2.0) * (static_cast<double>(o.H) * o.W * o.C +
+                                           static_cast<double>(Ho) * Wo * o.Cout * (o.res >= 0 ? 2 : 1))});
     } else if (o.kind == CnnOpKind::Head) {
       Planes in = slot_buf_[static_cast<size_t>(o.in)];
       const int classes = model_.num_classes, C = o.C, HW = o.H * o.W;
@@ -905,6 +919,44 @@ void Engine::set_selector_out(int layer, double gain, double bias) {
       g = nullptr;
     }
   c.lookup_steps.clear();
+}
+
+std::vector<StepProfile> Engine::profile(int B, bool shadow) {
+  require(B > 0 && B <= max_batch_, "profile: batch outside [1, max_batch]");
+  ck(cudaSetDevice(device_), "cudaSetDevice");
+  *h_batch_ = B;
+  ck(cudaMemcpyAsync(d_batch_, h_batch_, sizeof(int), cudaMemcpyHostToDevice, stream_), "batch size");
+  std::vector<Step>& st = steps_for(shadow);
+  std::vector<cudaEvent_t> ev(st.size() + 1);
+  for (auto& e : ev) ck(cudaEventCreate(&e), "event");
+  ck(cudaEventRecord(ev[0], stream_), "event");
+  for (size_t i = 0; i < st.size(); ++i) {
+    st[i].run(stream_);
+    ck(cudaEventRecord(ev[i + 1], stream_), "event");
+  }
+  ck(cudaStreamSynchronize(stream_), "profile sync");
+  std::vector<int> counts(static_cast<size_t>(model_.num_blocks) + 2);
+  ck(cudaMemcpy(counts.data(), d_counts_, counts.size() * sizeof(int), cudaMemcpyDeviceToHost), "counts");
+  std::vector<StepProfile> out;
+  for (size_t i = 0; i < st.size(); ++i) {
+    float ms = 0.0f;
+    ck(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]), "elapsed");
+    const double units = st[i].count_idx >= 0 ? counts[static_cast<size_t>(st[i].count_idx)] : 0.0;
+    out.push_back({st[i].kind, ms, st[i].flops_per_unit * units, st[i].bytes_per_unit * units});
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  return out;
+}
+
+double Engine::serve_timed(int B, bool shadow) {
+  steps_for(shadow);
+  ck(cudaEventRecord(ev0_, stream_), "event");
+  serve(B, shadow, true);
+  ck(cudaEventRecord(ev1_, stream_), "event");
+  ck(cudaEventSynchronize(ev1_), "event sync");
+  float ms = 0.0f;
+  ck(cudaEventElapsedTime(&ms, ev0_, ev1_), "elapsed");
+  return ms;
 }
 
 double Engine::time_serve_ms(int B, bool shadow, int iters) {

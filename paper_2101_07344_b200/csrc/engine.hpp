@@ -32,6 +32,16 @@ struct Step {
   std::function<void(cudaStream_t)> run;
   int kind = 0;      // 0 = other, 1 = tensor-core contraction, 2 = lookup, 3 = exit/compaction
   int launches = 1;  // kernel launches this step enqueues
+  // Algorithmic work = per-unit figure x units processed, where units =
+  // counts[count_idx] after the batch (surviving requests; -1 = none).
+  int count_idx = -1;
+  double flops_per_unit = 0.0;
+  double bytes_per_unit = 0.0;
+};
+
+struct StepProfile {
+  int kind;
+  double ms, flops, bytes;
 };
 
 class Engine {
@@ -77,6 +87,11 @@ class Engine {
   int count_kernels(bool shadow, int kind);
   // Time `iters` serve() calls (graph replay) with CUDA events on the engine stream.
   double time_serve_ms(int B, bool shadow, int iters);
+  // One batch (graph replay), CUDA events on the engine stream around it; synchronous.
+  double serve_timed(int B, bool shadow);
+  // One batch with CUDA events around every step (no graph) and the
+  // algorithmic work each step did.
+  std::vector<StepProfile> profile(int B, bool shadow);
 
  private:
   void build_weights();

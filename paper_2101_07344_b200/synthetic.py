@@ -62,6 +62,34 @@ def calibrate_biases(z: Dict[int, np.ndarray], fractions: Dict[int, float], delt
     return biases
 
 
+def selector_logits_from_probs(p: np.ndarray) -> np.ndarray:
+    q = np.clip(np.asarray(p, np.float64), 1e-7, 1 - 1e-7)
+    return np.log(q) - np.log1p(-q)
+
+
+def calibrate_variants(model, variants, calib_x: np.ndarray, full_fraction: float, delta: float = 0.5,
+                       precision: str = "bf16x3", device: int = 0):
+    """Set each variant's selector gain/bias (host objects, in place) so the
+    calibration batch follows exit_profile(); returns the fractions used.
+    Uses one shadow-mode pass on the GPU to read every layer's selector output."""
+    from .api import Deployment
+    for v in variants:
+        v.delta = delta
+    B = calib_x.shape[0]
+    dep = Deployment(model, variants, precision=precision, max_batch=B, device=device)
+    res = dep.serve(calib_x, shadow=True)
+    dep.close()
+    layers = sorted(v.layer for v in variants)
+    z = {l: selector_logits_from_probs(res.probs[l - 1]) for l in layers}
+    # selectors start with zero final bias (make_network), so z is linear in the gain
+    gains = gains_for(z)
+    fr = exit_profile(layers, full_fraction)
+    biases = calibrate_biases({l: z[l] * gains[l] for l in layers}, fr, delta)
+    for v in variants:
+        v.set_selector_out(gains[v.layer], biases[v.layer])
+    return fr
+
+
 def mlp_inputs(B: int, dim: int, seed: int) -> np.ndarray:
     """Uniform [-1.5, 1.5) inputs (test_util.hpp:73-77 random_vec)."""
     return np.random.default_rng(seed).uniform(-1.5, 1.5, size=(B, dim))

@@ -1,0 +1,318 @@
+"""Parity tests proper (need a B200): the CUDA serve path through the C-ABI
+against the CPU oracle, which tests/test_oracle.py pins bit-exactly to the
+compiled reference and its golden fixtures.
+
+Contract (north_star / SURVEY §8c), written here as code:
+  * selector probabilities / logits / pr within 1e-3 relative
+    (close_rel: |a-b| <= tol * max(1, |a|, |b|), test_util.hpp:19-22);
+  * exit layer and served label bit-exact, except requests whose oracle
+    selector probability lies within BAND = 1e-4 of delta at any probed layer
+    (reported separately) and label near-ties (top-2 gap < 1e-4);
+  * base prediction bit-exact where computed (shadow mode: all requests).
+Precision tier under test: bf16x3 (fp32-class). The bf16 tier is reported
+as an agreement rate with its own, looser bound.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from tests.helpers import GOLDEN, have_gpu, requires_ref
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not have_gpu(), reason="needs a B200")]
+
+import paper_2101_07344_b200 as lcb  # noqa: E402
+from paper_2101_07344_b200.synthetic import (C1_MENU, C1_WIDTHS, calibrate_variants, image_inputs,  # noqa: E402
+                                             mlp_inputs)
+
+O = pytest.importorskip("oracle.oracle")
+
+TOL = 1e-3
+BAND = 1e-4
+GAP = 1e-4
+
+
+def close_rel(a, b, tol=TOL):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return np.abs(a - b) <= tol * np.maximum(1.0, np.maximum(np.abs(a), np.abs(b)))
+
+
+def in_band(probs_o, exit_o, deltas):
+    """probs_o [B][L] oracle probs (NaN = unprobed); a request is in band if any
+    probed layer up to its oracle exit has |p - delta| < BAND."""
+    B, L = probs_o.shape
+    band = np.zeros(B, bool)
+    for i in range(B):
+        last = exit_o[i] if exit_o[i] > 0 else L
+        for l in range(1, last + 1):
+            p = probs_o[i, l - 1]
+            if not np.isnan(p) and abs(p - deltas.get(l, 0.5)) < BAND:
+                band[i] = True
+    return band
+
+
+def compare_serve(res, exit_o, served_o, base_o, probs_o, deltas, shadow, label_gap=None):
+    band = in_band(probs_o, exit_o, deltas)
+    ok = ~band
+    if label_gap is not None:
+        ok &= ~label_gap
+    assert np.array_equal(res.exit_layer[ok], exit_o[ok]), (
+        f"exit mismatch on {np.sum(res.exit_layer[ok] != exit_o[ok])} of {ok.sum()} requests")
+    assert np.array_equal(res.served[ok], served_o[ok])
+    if shadow:
+        assert np.array_equal(res.base_pred[ok], base_o[ok])
+    else:
+        miss = ok & (exit_o == 0)
+        assert np.array_equal(res.base_pred[miss], base_o[miss])
+    # probabilities at every layer the reference probes (ascending, up to the exit)
+    L = probs_o.shape[1]
+    last = np.where(exit_o > 0, exit_o, L)
+    probed = ~np.isnan(probs_o) & (np.arange(1, L + 1)[None, :] <= last[:, None])
+    gp = res.probs.T  # [B][L]
+    assert np.all(close_rel(gp[probed & ok[:, None]], probs_o[probed & ok[:, None]]))
+    return int(band.sum())
+
+
+# ------------------------------------------------------------------ MLP tier (reference family)
+def _load_trained():
+    d = os.path.join(GOLDEN, "trained")
+    model_txt = open(os.path.join(d, "model.txt")).read()
+    vtxt = []
+    k = 0
+    while os.path.exists(os.path.join(d, f"variant_{k}.txt")):
+        vtxt.append(open(os.path.join(d, f"variant_{k}.txt")).read())
+        k += 1
+    test = [l.split() for l in open(os.path.join(d, "dataset.txt")).read().split("\n") if l.startswith("test ")]
+    X = np.array([[float(v) for v in t[2:]] for t in test])
+    reqs = [tuple(map(int, l.split())) for l in open(os.path.join(d, "requests.txt")).read().split("\n") if l]
+    traces = [l.split() for l in open(os.path.join(d, "traces.txt")).read().split("\n")[1:]
+              if l and not l.startswith("#")]
+    return model_txt, vtxt, X, reqs, traces
+
+
+@pytest.mark.parametrize("shadow", [True, False])
+def test_golden_trained_deployment(shadow):
+    """The reference's own trained deployment + traces (tests/golden/trained)."""
+    model_txt, vtxt, X, reqs, traces = _load_trained()
+    m = lcb.load_base_model(model_txt)
+    vs = [lcb.load_variant(t) for t in vtxt]
+    dep = lcb.Deployment(m, vs, precision="bf16x3", max_batch=4096)
+    idx = np.array([s for _, s in reqs])
+    res = dep.serve(X[idx], shadow=shadow)
+    exit_ref = np.array([int(t[5]) for t in traces])
+    served_ref = np.array([int(t[4]) for t in traces])
+    base_ref = np.array([int(t[3]) for t in traces])
+    model = O.parse_model(model_txt)
+    caches = []
+    for t in vtxt:
+        meta = O.parse_variant(t)
+        caches.append((meta["layer"], meta["predictor"], meta["selector"], meta["delta"]))
+    el, sv, bp, probs = O.oracle_serve_mlp(model, caches, X[idx])
+    assert np.array_equal(el, exit_ref) and np.array_equal(sv, served_ref)
+    deltas = {c[0]: c[3] for c in caches}
+    nb = compare_serve(res, exit_ref, served_ref, base_ref, probs, deltas, shadow)
+    assert nb <= 0.01 * len(idx)
+
+
+@pytest.mark.parametrize("delta", [0.9, 0.99, 0.999])
+def test_trained_deployment_threshold_sweep(delta):
+    """Same deployment with raised thresholds so requests exit at every layer
+    (the C4 confidence-threshold sweep on the reference family)."""
+    model_txt, vtxt, X, reqs, _ = _load_trained()
+    m = lcb.load_base_model(model_txt)
+    vs = [lcb.load_variant(t) for t in vtxt]
+    for v in vs:
+        v.delta = delta
+    dep = lcb.Deployment(m, vs, precision="bf16x3", max_batch=1024)
+    x = X[:1024] if len(X) >= 1024 else X
+    res = dep.serve(x, shadow=False)
+    model = O.parse_model(model_txt)
+    caches = []
+    for t in vtxt:
+        meta = O.parse_variant(t)
+        caches.append((meta["layer"], meta["predictor"], meta["selector"], delta))
+    el, sv, bp, probs = O.oracle_serve_mlp(model, caches, x)
+    compare_serve(res, el, sv, bp, probs, {c[0]: delta for c in caches}, shadow=False)
+    # the compacted run agrees with the shadow run on every decision
+    sh = dep.serve(x, shadow=True)
+    assert np.array_equal(sh.exit_layer, res.exit_layer) and np.array_equal(sh.served, res.served)
+
+
+def test_golden_c1_config():
+    """C1 reference config (3072-input block MLP, ResNet-18 stage widths, a
+    cache after every block from all three families)."""
+    spec = json.load(open(os.path.join(GOLDEN, "c1", "c1.json")))
+    m = lcb.make_base_model(spec["input_dim"], spec["classes"], spec["widths"], spec["blocks"], spec["model_seed"])
+    vs = []
+    for l in range(spec["blocks"]):
+        v = lcb.build_variant(l + 1, l, spec["menu"][l], m.tap_dim(l + 1), spec["classes"], spec["cache_seed"])
+        v.set_selector_out(spec["gains"][str(l + 1)], spec["biases"][str(l + 1)])
+        v.delta = spec["delta"]
+        vs.append(v)
+    x = mlp_inputs(spec["n"], spec["input_dim"], spec["input_seed"])
+    probs_o = np.array(spec["probs"])
+    exit_o, served_o, base_o = (np.array(spec[k]) for k in ("exit_layer", "served", "base"))
+    deltas = {l + 1: spec["delta"] for l in range(spec["blocks"])}
+    for shadow in (True, False):
+        dep = lcb.Deployment(m, vs, precision="bf16x3", max_batch=128)
+        res = dep.serve(x, shadow=shadow)
+        compare_serve(res, exit_o, served_o, base_o, probs_o, deltas, shadow)
+        dep.close()
+
+
+@pytest.mark.parametrize("arch", ["FC(1024)", "FC(32)", "Pool(16)", "Pool(8192)", "Conv(3,1)", "Conv(5,2)"])
+def test_lookup_mlp_taps(arch):
+    m = lcb.make_base_model(64, 10, [96], 2, 5)
+    v = lcb.build_variant(2, 0, arch, 96, 10, 11)
+    v.set_selector_out(30.0, 0.0)
+    dep = lcb.Deployment(m, [v], max_batch=64)
+    taps = np.random.default_rng(1).uniform(-1.5, 1.5, (64, 96))
+    got = dep.lookup(2, taps)
+    pred, sel, d = O.variant_layers_from_product(v)
+    pn, sn = O.OracleNet(pred), O.OracleNet(sel)
+    for i in range(64):
+        hit, p, pr, lg = O.oracle_lookup(pn, sn, d, taps[i])
+        assert close_rel(got["prob"][i], p)
+        assert np.all(close_rel(got["pr"][i], pr)) and np.all(close_rel(got["logits"][i], lg))
+        if abs(p - d) >= BAND:
+            assert bool(got["hit"][i]) == hit
+        top = np.sort(pr)[::-1]
+        if top[0] - top[1] >= GAP:
+            assert got["label"][i] == O.argmax(pr)
+
+
+def test_inclusive_threshold_on_gpu():
+    # test_cache.cpp:218-227 on the device: zeroed selector -> prob exactly 0.5
+    m = lcb.make_base_model(4, 3, [4], 1, 1)
+    v = lcb.build_variant(1, 0, "FC(8)", 4, 3, 9)
+    v.set_selector_out(0.0, 0.0)
+    dep = lcb.Deployment(m, [v], max_batch=4)
+    tap = np.array([[0.3, -0.1, 0.2, 0.0]])
+    r = dep.lookup(1, tap)
+    assert r["prob"][0] == 0.5 and r["hit"][0] == 1
+    dep.set_delta(1, 0.5000000001)
+    assert dep.lookup(1, tap)["hit"][0] == 0
+
+
+def test_errors_are_reference_typed():
+    m = lcb.make_base_model(16, 10, [64], 3, 1)
+    v1 = lcb.build_variant(2, 0, "Pool(16)", 64, 10, 1)
+    v2 = lcb.build_variant(2, 1, "FC(32)", 64, 10, 1)
+    with pytest.raises(ValueError, match="more than one variant at layer 2"):
+        lcb.Deployment(m, [v1, v2], max_batch=8)
+    bad = lcb.build_variant(2, 0, "Pool(16)", 32, 10, 1)  # wrong tap dim
+    with pytest.raises(ValueError):
+        lcb.Deployment(m, [bad], max_batch=8)
+    dep = lcb.Deployment(m, [v1], max_batch=8)
+    with pytest.raises(ValueError):
+        dep.serve(np.zeros((9, 16), np.float32))
+    with pytest.raises(ValueError):
+        dep.lookup(1, np.zeros((2, 64)))  # no cache at layer 1
+
+
+def test_graph_and_direct_launch_identical():
+    spec = json.load(open(os.path.join(GOLDEN, "c1", "c1.json")))
+    m = lcb.make_base_model(3072, 10, C1_WIDTHS, 8, spec["model_seed"])
+    vs = []
+    for l in range(8):
+        v = lcb.build_variant(l + 1, l, C1_MENU[l], m.tap_dim(l + 1), 10, spec["cache_seed"])
+        v.set_selector_out(spec["gains"][str(l + 1)], spec["biases"][str(l + 1)])
+        vs.append(v)
+    dep = lcb.Deployment(m, vs, max_batch=128)
+    x = mlp_inputs(128, 3072, 3)
+    a = dep.serve(x, graph=True)
+    b = dep.serve(x, graph=False)
+    c = dep.serve(x, graph=True)
+    for r in (b, c):
+        assert np.array_equal(a.exit_layer, r.exit_layer) and np.array_equal(a.served, r.served)
+        assert np.array_equal(a.probs, r.probs, equal_nan=True)
+
+
+# ------------------------------------------------------------------ CNN tier
+def _cnn_deployment(arch, classes, seed, B, precision="bf16x3", cache="Pool", full_fraction=0.2):
+    m = lcb.make_cnn_model(arch, classes, seed)
+    vs = []
+    for l in range(1, m.num_blocks + 1):
+        C, H, W = m.tap(l)
+        a = f"Pool({C})" if cache == "Pool" else cache
+        vs.append(lcb.build_variant(l, 0, a, m.tap_dim(l), classes, seed + l))
+    side = 32 if arch.endswith("cifar") else 224
+    calib = image_inputs(B, 3, side, side, seed=seed + 100)
+    calibrate_variants(m, vs, calib, full_fraction, precision=precision)
+    return m, vs
+
+
+def _oracle_cnn(m, vs, x, threads=8):
+    ops = m.cnn_ops()
+    taps, logits = O.oracle_cnn_forward(ops, m.nslots, x, m.num_blocks, m.tap_dims, m.num_classes, threads=threads)
+    B = x.shape[0]
+    L = m.num_blocks
+    nets = {}
+    for v in vs:
+        pred, sel, d = O.variant_layers_from_product(v)
+        nets[v.layer] = (O.OracleNet(pred), O.OracleNet(sel), d)
+    exit_o = np.zeros(B, int)
+    served = np.zeros(B, int)
+    base = np.array([O.argmax(O.softmax(logits[i])) for i in range(B)])
+    probs = np.full((B, L), np.nan)
+    gaps = np.zeros(B, bool)
+    for i in range(B):
+        top = np.sort(O.softmax(logits[i]))[::-1]
+        gaps[i] |= top[0] - top[1] < GAP
+        served[i] = base[i]
+        for l in sorted(nets):
+            pn, sn, d = nets[l]
+            hit, p, pr, _ = O.oracle_lookup(pn, sn, d, taps[l - 1][i])
+            probs[i, l - 1] = p
+            if hit:
+                exit_o[i] = l
+                served[i] = O.argmax(pr)
+                t2 = np.sort(pr)[::-1]
+                gaps[i] |= t2[0] - t2[1] < GAP
+                break
+    return exit_o, served, base, probs, gaps, taps, logits
+
+
+@pytest.mark.parametrize("shadow", [True, False])
+def test_resnet18_cifar_serve_vs_oracle(shadow):
+    m, vs = _cnn_deployment("resnet18_cifar", 10, 21, 64)
+    x = image_inputs(24, 3, 32, 32, seed=5)
+    dep = lcb.Deployment(m, vs, precision="bf16x3", max_batch=32)
+    res = dep.serve(x, shadow=shadow)
+    exit_o, served_o, base_o, probs_o, gaps, _, _ = _oracle_cnn(m, vs, x)
+    deltas = {v.layer: v.delta for v in vs}
+    compare_serve(res, exit_o, served_o, base_o, probs_o, deltas, shadow, label_gap=gaps)
+    assert len(set(exit_o.tolist())) >= 3  # exits spread over several layers
+
+
+def test_resnet18_cnn_lookups_on_oracle_taps():
+    """Cache heads of every family on real CNN taps (NCHW-flat from the fp64
+    oracle), through the engine's lookup entry point."""
+    m = lcb.make_cnn_model("resnet18_cifar", 10, 4)
+    x = image_inputs(4, 3, 32, 32, seed=9)
+    taps, _ = O.oracle_cnn_forward(m.cnn_ops(), m.nslots, x, m.num_blocks, m.tap_dims, 10, threads=4)
+    for layer, arch in [(1, "Pool(64)"), (1, "Pool(8192)"), (2, "Pool(4096)"), (5, "Pool(256)"), (7, "Conv(3,1)"),
+                        (8, "Conv(5,2)"), (8, "FC(256)"), (8, "Pool(8192)")]:
+        v = lcb.build_variant(layer, 0, arch, m.tap_dim(layer), 10, 17)
+        v.set_selector_out(20.0, 0.0)
+        dep = lcb.Deployment(m, [v], max_batch=4)
+        got = dep.lookup(layer, taps[layer - 1])
+        pred, sel, d = O.variant_layers_from_product(v)
+        pn, sn = O.OracleNet(pred), O.OracleNet(sel)
+        for i in range(4):
+            _, p, pr, lg = O.oracle_lookup(pn, sn, d, taps[layer - 1][i])
+            assert close_rel(got["prob"][i], p), (layer, arch)
+            assert np.all(close_rel(got["logits"][i], lg)), (layer, arch)
+        dep.close()
+
+
+def test_resnet18_bf16_tier_agreement():
+    m, vs = _cnn_deployment("resnet18_cifar", 10, 21, 64, precision="bf16")
+    x = image_inputs(32, 3, 32, 32, seed=6)
+    d3 = lcb.Deployment(m, vs, precision="bf16x3", max_batch=32)
+    d1 = lcb.Deployment(m, vs, precision="bf16", max_batch=32)
+    a, b = d3.serve(x, shadow=True), d1.serve(x, shadow=True)
+    agree = np.mean((a.exit_layer == b.exit_layer) & (a.served == b.served))
+    assert agree >= 0.8, agree
