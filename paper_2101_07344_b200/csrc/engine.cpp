@@ -187,6 +187,9 @@ void Engine::build_weights() {
   d_t0_ = static_cast<unsigned long long*>(dalloc(8));
   d_probs_ = static_cast<float*>(dalloc(static_cast<size_t>(L) * B * sizeof(float)));
   d_lk_count_ = static_cast<int*>(dalloc(sizeof(int)));
+  ws_ = static_cast<float*>(dalloc(tc_conv_ws_floats(256, num_sms_) * sizeof(float)));
+  ws_counters_ = static_cast<int*>(dalloc(2 * static_cast<size_t>(num_sms_) * sizeof(int)));
+  ck(cudaMemset(ws_counters_, 0, 2 * static_cast<size_t>(num_sms_) * sizeof(int)), "memset");
 
   // ---------------- base model
   long long max_tap_storage = 0;
@@ -220,7 +223,7 @@ void Engine::build_weights() {
   } else {
     cnn_w_.resize(model_.ops.size());
     std::vector<long long> slot_elems(static_cast<size_t>(model_.nslots), 0);
-    long long phase_elems = 0, im2col_elems = 0;
+    long long im2col_elems = 0;
     for (size_t i = 0; i < model_.ops.size(); ++i) {
       const CnnOp& o = model_.ops[i];
       if (o.kind == CnnOpKind::Stem || o.kind == CnnOpKind::Conv) {
@@ -242,8 +245,6 @@ void Engine::build_weights() {
         slot_elems[static_cast<size_t>(o.out)] = static_cast<long long>(B) * o.Ho() * o.Wo() * o.Cout;
         if (o.kind == CnnOpKind::Stem)
           im2col_elems = std::max(im2col_elems, static_cast<long long>(B) * o.Ho() * o.Wo() * dc.Kp);
-        if (o.stride == 2)
-          phase_elems = std::max(phase_elems, 4LL * B * ((o.H + 1) / 2) * ((o.W + 1) / 2) * o.C);
       } else if (o.kind == CnnOpKind::MaxPool) {
         slot_elems[static_cast<size_t>(o.out)] = static_cast<long long>(B) * o.Ho() * o.Wo() * o.C;
       } else if (o.kind == CnnOpKind::Head) {
@@ -276,7 +277,6 @@ void Engine::build_weights() {
         if (last_use[static_cast<size_t>(s)] == static_cast<int>(i) && slot_buf_[static_cast<size_t>(s)].hi)
           free_pool.emplace(slot_elems[static_cast<size_t>(s)], slot_buf_[static_cast<size_t>(s)]);
     }
-    if (phase_elems) phase_buf_ = alloc_planes(static_cast<size_t>(phase_elems));
     if (im2col_elems) im2col_buf_ = alloc_planes(static_cast<size_t>(im2col_elems));
     for (const TapInfo& t : model_.taps) max_tap_storage = std::max(max_tap_storage, t.dim());
   }
@@ -340,8 +340,8 @@ void Engine::build_weights() {
       c->b1 = upload_f32(to_f32(PW[0].b));
       c->W2 = upload_f32(to_f32(PW[2].w));
       c->b2 = upload_f32(to_f32(PW[2].b));
-      const int tiles_mn = ((B + 127) / 128) * (c->hp / tc_conv_pick_bn(c->hp));
-      const int nk = (c->Dk / 64) * (prec_ == kPrecX3 ? 3 : 1);
+      const int tiles_mn = ((B + 127) / 128) * (c->hp / tc_conv_pick_bn(c->hp, prec_ == kPrecX3 ? 3 : 1));
+      const int nk = c->Dk / 64;  // K-steps (one 64-channel slice each; bf16x3 segments share a step)
       c->ks = std::max(1, std::min(nk, num_sms_ / std::max(1, tiles_mn)));
       c->feats = static_cast<float*>(dalloc(static_cast<size_t>(c->ks) * B * c->hp * sizeof(float)));
       if (!mlp) c->gather = alloc_planes(static_cast<size_t>(B) * c->Dk);
@@ -405,7 +405,7 @@ void Engine::add_lookup_steps(std::vector<Step>& steps, DevCache& c, const TapVi
     }
     auto prm = std::make_shared<TcConvParams>();
     std::memset(prm.get(), 0, sizeof(TcConvParams));
-    const int BN = tc_conv_pick_bn(c.hp);
+    const int BN = tc_conv_pick_bn(c.hp, prec_ == kPrecX3 ? 3 : 1);
     const bool x3 = prec_ == kPrecX3;
     bool ok = encode_act_map(&prm->tmA[0], a_hi, c.Dk, max_rows, 1, 1, 1, 128, 1) &&
               encode_weight_map(&prm->tmB[0], c.W1.hi, c.Dk, c.hp, BN);
@@ -493,7 +493,7 @@ void Engine::build_mlp_steps(std::vector<Step>& steps, bool shadow) {
     Planes act = mlp_act_[static_cast<size_t>(b)];
     auto prm = std::make_shared<TcConvParams>();
     std::memset(prm.get(), 0, sizeof(TcConvParams));
-    const int BN = tc_conv_pick_bn(f.outp);
+    const int BN = tc_conv_pick_bn(f.outp, x3 ? 3 : 1);
     bool ok = encode_act_map(&prm->tmA[0], cur.hi, f.inp, B, 1, 1, 1, 128, 1) &&
               encode_weight_map(&prm->tmB[0], f.w.hi, f.inp, f.outp, BN);
     if (x3)
@@ -512,6 +512,9 @@ void Engine::build_mlp_steps(std::vector<Step>& steps, bool shadow) {
     prm->segs = x3 ? 3 : 1;
     prm->Cout = f.outp;
     prm->ksplit = 1;
+    prm->ks_max = 32;
+    prm->ws = ws_;
+    prm->ws_counters = ws_counters_;
     prm->count = cur_count;
     prm->count_static = B;
     prm->mode = 0;
@@ -607,7 +610,7 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow) {
       auto prm = std::make_shared<TcConvParams>();
       std::memset(prm.get(), 0, sizeof(TcConvParams));
       const int rows = B * Ho * Wo;
-      const int BN = tc_conv_pick_bn(o.Cout);
+      const int BN = tc_conv_pick_bn(o.Cout, x3 ? 3 : 1);
       bool ok = encode_act_map(&prm->tmA[0], col.hi, dc.Kp, rows, 1, 1, 1, 128, 1) &&
                 encode_weight_map(&prm->tmB[0], dc.w.hi, dc.Kp, o.Cout, BN);
       if (x3)
@@ -648,32 +651,18 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow) {
     } else if (o.kind == CnnOpKind::Conv) {
       const DevConv& dc = cnn_w_[i];
       Planes in = slot_buf_[static_cast<size_t>(o.in)], out = slot_buf_[static_cast<size_t>(o.out)];
-      Planes src = in;
-      int P = 1, Hs = o.H, Ws = o.W;
-      if (o.stride == 2) {
-        Hs = (o.H + 1) / 2;
-        Ws = (o.W + 1) / 2;
-        P = 4;
-        Planes ph = phase_buf_;
-        steps.push_back({[o, in, ph, Hs, Ws, cur_ids, cur_count, B](cudaStream_t s) {
-                           launch_phase_split(in.hi, in.lo, o.H, o.W, o.C, B, Hs, Ws, cur_ids, cur_count, B, ph.hi,
-                                              ph.lo, s);
-                         },
-                         0});
-        src = ph;
-      } else {
-        require(o.stride == 1, "engine: only stride 1 and 2 convolutions are supported");
-      }
+      // Stride 2 reads the NHWC input directly through TMA traversal strides.
+      require(o.stride == 1 || o.stride == 2, "engine: only stride 1 and 2 convolutions are supported");
       const int Ho = o.Ho(), Wo = o.Wo();
       int hb, wb, ipt;
       choose_box(Ho, Wo, hb, wb, ipt);
       auto prm = std::make_shared<TcConvParams>();
       std::memset(prm.get(), 0, sizeof(TcConvParams));
-      const int BN = tc_conv_pick_bn(o.Cout);
-      bool ok = encode_act_map(&prm->tmA[0], src.hi, o.C, Ws, Hs, B, P, wb, hb) &&
+      const int BN = tc_conv_pick_bn(o.Cout, x3 ? 3 : 1);
+      bool ok = encode_act_map(&prm->tmA[0], in.hi, o.C, o.W, o.H, B, 1, wb, hb, o.stride) &&
                 encode_weight_map(&prm->tmB[0], dc.w.hi, dc.Kp, o.Cout, BN);
       if (x3)
-        ok = ok && encode_act_map(&prm->tmA[1], src.lo, o.C, Ws, Hs, B, P, wb, hb) &&
+        ok = ok && encode_act_map(&prm->tmA[1], in.lo, o.C, o.W, o.H, B, 1, wb, hb, o.stride) &&
              encode_weight_map(&prm->tmB[1], dc.w.lo, dc.Kp, o.Cout, BN);
       if (!ok) throw CudaFailure("engine: TMA descriptor encode failed (conv)");
       prm->plain = 0;
@@ -684,11 +673,15 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow) {
       prm->ipt = ipt;
       prm->tiles_h = (Ho + hb - 1) / hb;
       prm->tiles_w = (Wo + wb - 1) / wb;
+      prm->conv_stride = o.stride;
       prm->C = o.C;
       prm->ntaps = o.k * o.k;
       prm->segs = x3 ? 3 : 1;
       prm->Cout = o.Cout;
       prm->ksplit = 1;
+      prm->ks_max = 32;
+      prm->ws = ws_;
+      prm->ws_counters = ws_counters_;
       prm->surv = cur_ids;
       prm->count = cur_count;
       prm->count_static = B;
@@ -705,17 +698,9 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow) {
       for (int r = 0; r < o.k; ++r)
         for (int sx = 0; sx < o.k; ++sx) {
           const int t = r * o.k + sx;
-          if (o.stride == 1) {
-            prm->tap_phase[t] = 0;
-            prm->tap_dh[t] = static_cast<signed char>(r - o.pad);
-            prm->tap_dw[t] = static_cast<signed char>(sx - o.pad);
-          } else {
-            const int oh = r - o.pad, ow = sx - o.pad;
-            const int ph = ((oh % 2) + 2) % 2, pw = ((ow % 2) + 2) % 2;
-            prm->tap_phase[t] = static_cast<signed char>(ph * 2 + pw);
-            prm->tap_dh[t] = static_cast<signed char>((oh - ph) / 2);
-            prm->tap_dw[t] = static_cast<signed char>((ow - pw) / 2);
-          }
+          prm->tap_phase[t] = 0;
+          prm->tap_dh[t] = static_cast<signed char>(r - o.pad);
+          prm->tap_dw[t] = static_cast<signed char>(sx - o.pad);
         }
       steps.push_back({[prm, BN, sms](cudaStream_t s) { ck(tc_conv_launch(*prm, BN, sms, s), "tc_conv (conv)"); }, 1,
                        1, static_cast<int>(cur_count - d_counts_),

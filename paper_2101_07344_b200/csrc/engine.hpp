@@ -151,7 +151,8 @@ class Engine {
   };
   std::vector<DevConv> cnn_w_;    // by op index
   std::vector<Planes> slot_buf_;  // by slot
-  Planes phase_buf_;
+  float* ws_ = nullptr;        // split-K workspace shared by all contractions (stream-ordered)
+  int* ws_counters_ = nullptr;
   Planes im2col_buf_;
 
   std::vector<Step> steps_compact_, steps_shadow_;

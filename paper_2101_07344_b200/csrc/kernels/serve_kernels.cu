@@ -347,6 +347,86 @@ __global__ void cache_head_kernel(CacheHeadParams p) {
     for (int k = tid; k < C; k += blockDim.x) p.logits_out[static_cast<long long>(r) * C + k] = logits[k];
 }
 
+// Warp-per-row form of the same head for classes <= 32 (no block barriers):
+// lane k owns class k; features are streamed lane-strided.
+__global__ void cache_head_warp_kernel(CacheHeadParams p) {
+  extern __shared__ float smw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (r >= *p.count) return;
+  const int C = p.classes;
+  float logit = -FLT_MAX;
+  if (p.family == 2) {
+    if (lane < C) {
+      float a = p.b2[lane];
+      for (int c = 0; c < p.feat; ++c) a += p.feats[(static_cast<long long>(r) * p.feat + c) * C + lane];
+      logit = a;
+    }
+  } else {
+    float* feat = smw + warp * p.feat;
+    if (p.family == 1) {
+      for (int o = lane; o < p.feat; o += 32) feat[o] = p.feats[static_cast<long long>(r) * p.feat + o];
+    } else {
+      for (int j = lane; j < p.feat; j += 32) {
+        float a = p.b1[j];
+        for (int s = 0; s < p.ks; ++s) a += p.feats[(static_cast<long long>(s) * p.rows_total + r) * p.hp + j];
+        feat[j] = a > 0.0f ? a : 0.0f;
+      }
+    }
+    __syncwarp();
+    for (int k = 0; k < C; ++k) {
+      const float* wr = p.W2 + static_cast<long long>(k) * p.feat;
+      float a = 0.0f;
+      for (int o = lane; o < p.feat; o += 32) a += wr[o] * feat[o];
+      a = warp_sum(a);
+      if (lane == k) logit = a + p.b2[k];
+    }
+  }
+  const float m = warp_max(lane < C ? logit : -FLT_MAX);
+  const float e = lane < C ? expf(logit - m) : 0.0f;
+  const float sum = warp_sum(e);
+  const float pr = lane < C ? e / sum : 0.0f;
+  // selector FC(C,16) + ReLU: lane j < 16 owns hidden unit j
+  float h = 0.0f;
+  {
+    float a = lane < 16 ? p.bs1[lane] : 0.0f;
+    for (int k = 0; k < C; ++k) {
+      const float pk = __shfl_sync(0xffffffffu, pr, k);
+      if (lane < 16) a += p.Ws1[lane * C + k] * pk;
+    }
+    h = (lane < 16 && a > 0.0f) ? a : 0.0f;
+  }
+  const float z = warp_sum(lane < 16 ? p.ws2[lane] * h : 0.0f) + p.bs2;
+  // argmax(pr), lowest index on ties
+  float bv = lane < C ? pr : -FLT_MAX;
+  int bi = lane < C ? lane : 0x7fffffff;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > bv || (ov == bv && oi < bi)) {
+      bv = ov;
+      bi = oi;
+    }
+  }
+  if (lane == 0) {
+    float q;
+    if (z >= 0.0f) {
+      q = 1.0f / (1.0f + expf(-z));
+    } else {
+      const float ez = expf(z);
+      q = ez / (1.0f + ez);
+    }
+    p.prob[r] = q;
+    p.hit[r] = static_cast<double>(q) >= p.delta ? 1 : 0;
+    p.label[r] = bi;
+  }
+  if (lane < C) {
+    if (p.pr_out) p.pr_out[static_cast<long long>(r) * C + lane] = pr;
+    if (p.logits_out) p.logits_out[static_cast<long long>(r) * C + lane] = logit;
+  }
+}
+
 // ------------------------------------------------------------------ exit
 __global__ void exit_compact_kernel(int layer, const int* count_in, const int* ids_in, const int* hit, const int* label,
                                     const float* prob, int* exit_layer, int* served, unsigned long long* exit_ns,
@@ -528,23 +608,45 @@ __global__ void base_head_kernel(const __nv_bfloat16* hi, const __nv_bfloat16* l
     for (int k = tid; k < classes; k += blockDim.x) logits_out[static_cast<long long>(id) * classes + k] = logits[k];
 }
 
+// One thread per (output pixel, 8 consecutive K entries): 16-byte stores.
 __global__ void stem_im2col_kernel(const float* x, const int* count, int C, int H, int W, int k, int stride, int pad,
                                    int Ho, int Wo, int Kp, __nv_bfloat16* hi, __nv_bfloat16* lo) {
-  const long long total = static_cast<long long>(*count) * Ho * Wo * Kp;
+  const int kg = Kp / 8;
+  const int pix = Ho * Wo;
+  const long long total = static_cast<long long>(*count) * pix * kg;
+  const int K = k * k * C;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int kk = static_cast<int>(i % Kp);
-    const long long m = i / Kp;
-    const int ow = static_cast<int>(m % Wo);
-    const int oh = static_cast<int>((m / Wo) % Ho);
-    const long long n = m / (static_cast<long long>(Wo) * Ho);
-    float v = 0.0f;
-    if (kk < k * k * C) {
-      const int c = kk % C, rs = kk / C, s = rs % k, r = rs / k;
-      const int ih = oh * stride + r - pad, iw = ow * stride + s - pad;
-      if (ih >= 0 && ih < H && iw >= 0 && iw < W) v = x[((n * C + c) * H + ih) * W + iw];
+    const int g8 = static_cast<int>(i % kg);
+    const long long m = i / kg;
+    const int n = static_cast<int>(m / pix);
+    const int rem = static_cast<int>(m - static_cast<long long>(n) * pix);
+    const int oh = rem / Wo, ow = rem - (rem / Wo) * Wo;
+    const float* xn = x + static_cast<long long>(n) * C * H * W;
+    float v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int kk = g8 * 8 + e;
+      float val = 0.0f;
+      if (kk < K) {
+        const int c = kk % C, rs = kk / C, s2 = rs % k, r = rs / k;
+        const int ih = oh * stride + r - pad, iw = ow * stride + s2 - pad;
+        if (ih >= 0 && ih < H && iw >= 0 && iw < W) val = xn[(c * H + ih) * W + iw];
+      }
+      v[e] = val;
     }
-    split_store(v, hi, lo, i);
+    uint4 h4, l4;
+    __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&h4);
+    __nv_bfloat162* l2 = reinterpret_cast<__nv_bfloat162*>(&l4);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const __nv_bfloat162 hh = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+      h2[e] = hh;
+      const float2 hf = __bfloat1622float2(hh);
+      l2[e] = __floats2bfloat162_rn(v[2 * e] - hf.x, v[2 * e + 1] - hf.y);
+    }
+    reinterpret_cast<uint4*>(hi)[i] = h4;
+    if (lo) reinterpret_cast<uint4*>(lo)[i] = l4;
   }
 }
 
@@ -660,6 +762,17 @@ void launch_conv1d_partials(const TapView& tap, int max_rows, long long D, int k
 
 void launch_cache_head(const CacheHeadParams& p, int max_rows, cudaStream_t s) {
   if (max_rows <= 0) return;
+  if (p.classes <= 32 && (p.family == 2 || p.feat <= 4096)) {
+    const int warps = 4;
+    const size_t smem = p.family == 2 ? 0 : static_cast<size_t>(warps) * p.feat * sizeof(float);
+    static bool wattr = false;
+    if (!wattr) {
+      cudaFuncSetAttribute(cache_head_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      wattr = true;
+    }
+    cache_head_warp_kernel<<<(max_rows + warps - 1) / warps, 32 * warps, smem, s>>>(p);
+    return;
+  }
   const int feat_len = p.family == 2 ? p.classes : (p.feat > p.classes ? p.feat : p.classes);
   const size_t smem = static_cast<size_t>(p.classes + feat_len) * sizeof(float);
   static bool attr = false;
@@ -721,7 +834,7 @@ void launch_cnn_head(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int C, in
 
 void launch_stem_im2col(const float* x, const int* count, int max_n, int C, int H, int W, int k, int stride, int pad,
                         int Ho, int Wo, int Kp, __nv_bfloat16* hi, __nv_bfloat16* lo, cudaStream_t s) {
-  const long long total = static_cast<long long>(max_n) * Ho * Wo * Kp;
+  const long long total = static_cast<long long>(max_n) * Ho * Wo * (Kp / 8);
   long long blocks = (total + 255) / 256;
   if (blocks > 148 * 32) blocks = 148 * 32;
   if (blocks < 1) blocks = 1;

@@ -5,11 +5,9 @@
 //   warp 1      : MMA issuer (lane 0)
 //   warps 2..5  : epilogue, one TMEM lane quadrant (warp % 4) each
 // Pipelines: smem ring full/empty (TMA <-> MMA), TMEM double buffer
-// tfull/tempty (MMA <-> epilogue).
+// tfull/tempty (MMA <-> epilogue), split-K tile counters (CTA <-> CTA).
 #include "sm100_prims.cuh"
 #include "tc_conv.cuh"
-
-#include <cstdio>
 
 namespace lcb {
 
@@ -18,16 +16,20 @@ namespace {
 constexpr int kBM = 128;
 constexpr int kABytes = kBM * 128;  // 128 rows x 64 bf16
 
-template <int BN>
+template <int BN, bool X3>
 struct TcCfg {
+  static constexpr int kPlanes = X3 ? 2 : 1;
   static constexpr int kBBytes = BN * 128;
-  static constexpr int kStages = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
-  static constexpr int kSmem = kStages * (kABytes + kBBytes) + 1024 /*bars*/ + 1024 /*align*/;
+  static constexpr int kStageBytes = kPlanes * (kABytes + kBBytes);
+  static constexpr int kStagesRaw = (200 * 1024) / kStageBytes;
+  static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
+  static constexpr int kSmem = kStages * kStageBytes + 1024 /*bars*/ + 1024 /*align*/;
   static constexpr uint32_t kTmemCols = 2 * BN;
+  static_assert(kStages >= 2, "pipeline needs at least two stages");
 };
 
 struct TileGeom {
-  int count, n_groups, tiles_w, tiles_img, tiles_n, total, nk;
+  int count, n_groups, tiles_w, tiles_img, tiles_n, tiles_mn, ks, total, nk;
 };
 
 __device__ __forceinline__ TileGeom tile_geom(const TcConvParams& p, int BN) {
@@ -42,46 +44,141 @@ __device__ __forceinline__ TileGeom tile_geom(const TcConvParams& p, int BN) {
   }
   g.tiles_img = p.tiles_h * g.tiles_w;
   g.tiles_n = p.Cout / BN;
-  g.total = g.n_groups * g.tiles_img * g.tiles_n * p.ksplit;
-  g.nk = p.ntaps * (p.C / 64) * p.segs;
+  g.tiles_mn = g.n_groups * g.tiles_img * g.tiles_n;
+  g.nk = p.ntaps * (p.C / 64);
+  if (p.mode == 1) {
+    g.ks = p.ksplit;
+  } else if (p.ks_max > 1 && g.tiles_mn > 0) {
+    // Fill the grid as the surviving-request count shrinks.
+    int ks = (static_cast<int>(gridDim.x) + g.tiles_mn - 1) / g.tiles_mn;
+    ks = ks > p.ks_max ? p.ks_max : ks;
+    ks = ks > g.nk ? g.nk : ks;
+    g.ks = ks < 1 ? 1 : ks;
+  } else {
+    g.ks = 1;
+  }
+  g.total = g.tiles_mn * g.ks;
   return g;
 }
 
 struct Tile {
-  int tn, ks, grp, h0, w0, s_begin, s_end;
+  int tn, ks, tile_mn, grp, h0, w0, s_begin, s_end;
 };
 
 __device__ __forceinline__ Tile decode_tile(int t, const TcConvParams& p, const TileGeom& g) {
   Tile x;
-  x.ks = t % p.ksplit;
-  t /= p.ksplit;
+  x.ks = t % g.ks;
+  t /= g.ks;
+  x.tile_mn = t;
   x.tn = t % g.tiles_n;
   const int tm = t / g.tiles_n;
   x.grp = tm / g.tiles_img;
   const int r = tm % g.tiles_img;
   x.h0 = (r / g.tiles_w) * p.hb;
   x.w0 = (r % g.tiles_w) * p.wb;
-  x.s_begin = static_cast<int>((static_cast<long long>(g.nk) * x.ks) / p.ksplit);
-  x.s_end = static_cast<int>((static_cast<long long>(g.nk) * (x.ks + 1)) / p.ksplit);
+  x.s_begin = static_cast<int>((static_cast<long long>(g.nk) * x.ks) / g.ks);
+  x.s_end = static_cast<int>((static_cast<long long>(g.nk) * (x.ks + 1)) / g.ks);
   return x;
 }
 
 __device__ __forceinline__ int image_of(const TcConvParams& p, int idx) { return p.surv ? p.surv[idx] : idx; }
 
-template <int BN>
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+// scale/shift, residual, ReLU, hi/lo split and NHWC store of 16 channels.
+__device__ __forceinline__ void epilogue_store(const TcConvParams& p, float (&v)[16], size_t off, int co) {
+  if (p.scale) {
+    const float4* sc = reinterpret_cast<const float4*>(p.scale + co);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float4 s4 = __ldg(sc + q);
+      v[4 * q] *= s4.x;
+      v[4 * q + 1] *= s4.y;
+      v[4 * q + 2] *= s4.z;
+      v[4 * q + 3] *= s4.w;
+    }
+  }
+  if (p.shift) {
+    const float4* sh = reinterpret_cast<const float4*>(p.shift + co);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float4 s4 = __ldg(sh + q);
+      v[4 * q] += s4.x;
+      v[4 * q + 1] += s4.y;
+      v[4 * q + 2] += s4.z;
+      v[4 * q + 3] += s4.w;
+    }
+  }
+  if (p.res_hi) {
+    const uint4* rh = reinterpret_cast<const uint4*>(p.res_hi + off);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const uint4 u = rh[q];
+      const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __bfloat1622float2(b2[e]);
+        v[8 * q + 2 * e] += f.x;
+        v[8 * q + 2 * e + 1] += f.y;
+      }
+    }
+    if (p.res_lo) {
+      const uint4* rl = reinterpret_cast<const uint4*>(p.res_lo + off);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const uint4 u = rl[q];
+        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __bfloat1622float2(b2[e]);
+          v[8 * q + 2 * e] += f.x;
+          v[8 * q + 2 * e + 1] += f.y;
+        }
+      }
+    }
+  }
+  if (p.relu) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = v[i] > 0.0f ? v[i] : 0.0f;
+  }
+  uint4 hi[2], lo[2];
+  __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(hi);
+  __nv_bfloat162* l2 = reinterpret_cast<__nv_bfloat162*>(lo);
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const __nv_bfloat162 hh = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+    h2[e] = hh;
+    const float2 hf = __bfloat1622float2(hh);
+    l2[e] = __floats2bfloat162_rn(v[2 * e] - hf.x, v[2 * e + 1] - hf.y);
+  }
+  uint4* oh = reinterpret_cast<uint4*>(p.out_hi + off);
+  oh[0] = hi[0];
+  oh[1] = hi[1];
+  if (p.out_lo) {
+    uint4* ol = reinterpret_cast<uint4*>(p.out_lo + off);
+    ol[0] = lo[0];
+    ol[1] = lo[1];
+  }
+}
+
+template <int BN, bool X3>
 __global__ void __launch_bounds__(192, 1) tc_conv_kernel(const __grid_constant__ TcConvParams p) {
-  using Cfg = TcCfg<BN>;
+  using Cfg = TcCfg<BN, X3>;
   constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + S * kABytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + S * Cfg::kBBytes);
+  // stage s: [A_hi][A_lo?][B_hi][B_lo?]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
+  volatile int* s_last = reinterpret_cast<volatile int*>(tmem_holder + 1);
   const uint32_t full0 = smem_u32(bars);
   const uint32_t empty0 = smem_u32(bars + S);
   const uint32_t tfull0 = smem_u32(bars + 2 * S);
   const uint32_t tempty0 = smem_u32(bars + 2 * S + 2);
+  auto stage_a = [&](int s, int plane) { return smem + s * Cfg::kStageBytes + plane * kABytes; };
+  auto stage_b = [&](int s, int plane) {
+    return smem + s * Cfg::kStageBytes + Cfg::kPlanes * kABytes + plane * Cfg::kBBytes;
+  };
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -98,7 +195,7 @@ __global__ void __launch_bounds__(192, 1) tc_conv_kernel(const __grid_constant__
     fence_mbar_init();
     tma_prefetch_desc(&p.tmA[0]);
     tma_prefetch_desc(&p.tmB[0]);
-    if (p.segs > 1) {
+    if (X3) {
       tma_prefetch_desc(&p.tmA[1]);
       tma_prefetch_desc(&p.tmB[1]);
     }
@@ -111,6 +208,7 @@ __global__ void __launch_bounds__(192, 1) tc_conv_kernel(const __grid_constant__
 
   const TileGeom g = tile_geom(p, BN);
   const int cchunks = p.C / 64;
+  const int cs = p.conv_stride > 0 ? p.conv_stride : 1;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -120,32 +218,33 @@ __global__ void __launch_bounds__(192, 1) tc_conv_kernel(const __grid_constant__
       const int box_bytes = p.hb * p.wb * 128;
       for (int t = blockIdx.x; t < g.total; t += gridDim.x) {
         const Tile x = decode_tile(t, p, g);
-        int imgs[8];
+        int imgs[16];
+        const int ipt = p.plain ? 1 : p.ipt;
         if (p.plain) {
           imgs[0] = 0;
         } else {
-          for (int j = 0; j < p.ipt; ++j) {
-            int idx = x.grp * p.ipt + j;
+          for (int j = 0; j < ipt; ++j) {
+            int idx = x.grp * ipt + j;
             if (idx >= g.count) idx = g.count - 1;  // rows discarded by the epilogue
             imgs[j] = image_of(p, idx);
           }
         }
-        const int ipt = p.plain ? 1 : p.ipt;
+        int cc = x.s_begin % cchunks, tap = x.s_begin / cchunks;
         for (int s = x.s_begin; s < x.s_end; ++s) {
           mbar_wait(empty0 + 8 * stage, phase ^ 1);
           const uint32_t fb = full0 + 8 * stage;
-          mbar_expect_tx(fb, kABytes + Cfg::kBBytes);
-          const int seg = s % p.segs;
-          const int cc = (s / p.segs) % cchunks;
-          const int tap = s / (p.segs * cchunks);
-          const CUtensorMap* am = (seg == 2) ? &p.tmA[1] : &p.tmA[0];
-          const CUtensorMap* bm = (seg == 1) ? &p.tmB[1] : &p.tmB[0];
-          const uint32_t a_dst = smem_u32(sA + stage * kABytes);
-          const int dh = p.tap_dh[tap], dw = p.tap_dw[tap], ph = p.tap_phase[tap];
-          for (int j = 0; j < ipt; ++j) {
-            tma_load_5d(a_dst + j * box_bytes, am, fb, cc * 64, x.w0 + dw, x.h0 + dh, imgs[j], ph);
+          mbar_expect_tx(fb, Cfg::kStageBytes);
+          const int wc = x.w0 * cs + p.tap_dw[tap], hc = x.h0 * cs + p.tap_dh[tap], ph = p.tap_phase[tap];
+#pragma unroll 1
+          for (int pl = 0; pl < Cfg::kPlanes; ++pl) {
+            const uint32_t a_dst = smem_u32(stage_a(stage, pl));
+            for (int j = 0; j < ipt; ++j) tma_load_5d(a_dst + j * box_bytes, &p.tmA[pl], fb, cc * 64, wc, hc, imgs[j], ph);
+            tma_load_2d(smem_u32(stage_b(stage, pl)), &p.tmB[pl], fb, tap * p.C + cc * 64, x.tn * BN);
           }
-          tma_load_2d(smem_u32(sB + stage * Cfg::kBBytes), bm, fb, tap * p.C + cc * 64, x.tn * BN);
+          if (++cc == cchunks) {
+            cc = 0;
+            ++tap;
+          }
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
@@ -169,12 +268,16 @@ __global__ void __launch_bounds__(192, 1) tc_conv_kernel(const __grid_constant__
         for (int s = x.s_begin; s < x.s_end; ++s) {
           mbar_wait(full0 + 8 * stage, phase);
           tc_fence_after();
-          const uint32_t a_base = smem_u32(sA + stage * kABytes);
-          const uint32_t b_base = smem_u32(sB + stage * Cfg::kBBytes);
+          const uint32_t ah = smem_u32(stage_a(stage, 0)), bh = smem_u32(stage_b(stage, 0));
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            umma_bf16(d_tmem, umma_desc_sw128(a_base + 32 * k), umma_desc_sw128(b_base + 32 * k), idesc,
-                      (s > x.s_begin || k > 0) ? 1u : 0u);
+            const uint32_t first = (s > x.s_begin || k > 0) ? 1u : 0u;
+            umma_bf16(d_tmem, umma_desc_sw128(ah + 32 * k), umma_desc_sw128(bh + 32 * k), idesc, first);
+            if (X3) {
+              const uint32_t al = smem_u32(stage_a(stage, 1)), bl = smem_u32(stage_b(stage, 1));
+              umma_bf16(d_tmem, umma_desc_sw128(ah + 32 * k), umma_desc_sw128(bl + 32 * k), idesc, 1u);
+              umma_bf16(d_tmem, umma_desc_sw128(al + 32 * k), umma_desc_sw128(bh + 32 * k), idesc, 1u);
+            }
           }
           umma_commit(empty0 + 8 * stage);
           if (++stage == S) {
@@ -196,7 +299,6 @@ __global__ void __launch_bounds__(192, 1) tc_conv_kernel(const __grid_constant__
     const int rows_per_img = p.hb * p.wb;
     for (int t = blockIdx.x; t < g.total; t += gridDim.x) {
       const Tile x = decode_tile(t, p, g);
-      // Which output position does this accumulator row hold?
       bool valid;
       size_t obase;  // element offset of (n, h, w, 0) / row start
       int grow = 0;
@@ -214,13 +316,20 @@ __global__ void __launch_bounds__(192, 1) tc_conv_kernel(const __grid_constant__
         const int n = valid ? image_of(p, idx) : 0;
         obase = ((static_cast<size_t>(n) * p.Ho + h) * p.Wo + w) * p.Cout;
       }
+      const bool split = p.mode == 0 && g.ks > 1;
+      float* wsrow = split ? p.ws + (static_cast<size_t>(x.tile_mn) * g.ks * kBM + row) * BN : nullptr;
       mbar_wait(tfull0 + 8 * acc, acc_phase);
       tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * BN;
 #pragma unroll 1
+      const bool empty_k = x.s_end <= x.s_begin;  // no MMA wrote this accumulator
       for (int c16 = 0; c16 < BN / 16; ++c16) {
         float v[16];
         tmem_ld16(t_row + c16 * 16, v);
+        if (empty_k) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = 0.0f;
+        }
         if (!valid) continue;
         const int co = x.tn * BN + c16 * 16;
         if (p.mode == 1) {
@@ -228,80 +337,12 @@ __global__ void __launch_bounds__(192, 1) tc_conv_kernel(const __grid_constant__
               p.out_f32 + (static_cast<size_t>(x.ks) * p.rows_total + grow) * p.Cout + co);
 #pragma unroll
           for (int q = 0; q < 4; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-          continue;
-        }
-        if (p.scale) {
-          const float4* sc = reinterpret_cast<const float4*>(p.scale + co);
+        } else if (split) {
+          float4* dst = reinterpret_cast<float4*>(wsrow + static_cast<size_t>(x.ks) * kBM * BN + c16 * 16);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float4 s4 = __ldg(sc + q);
-            v[4 * q] *= s4.x;
-            v[4 * q + 1] *= s4.y;
-            v[4 * q + 2] *= s4.z;
-            v[4 * q + 3] *= s4.w;
-          }
-        }
-        if (p.shift) {
-          const float4* sh = reinterpret_cast<const float4*>(p.shift + co);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float4 s4 = __ldg(sh + q);
-            v[4 * q] += s4.x;
-            v[4 * q + 1] += s4.y;
-            v[4 * q + 2] += s4.z;
-            v[4 * q + 3] += s4.w;
-          }
-        }
-        const size_t off = obase + co;
-        if (p.res_hi) {
-          const uint4* rh = reinterpret_cast<const uint4*>(p.res_hi + off);
-#pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            const uint4 u = rh[q];
-            const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 f = __bfloat1622float2(b2[e]);
-              v[8 * q + 2 * e] += f.x;
-              v[8 * q + 2 * e + 1] += f.y;
-            }
-          }
-          if (p.res_lo) {
-            const uint4* rl = reinterpret_cast<const uint4*>(p.res_lo + off);
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-              const uint4 u = rl[q];
-              const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float2 f = __bfloat1622float2(b2[e]);
-                v[8 * q + 2 * e] += f.x;
-                v[8 * q + 2 * e + 1] += f.y;
-              }
-            }
-          }
-        }
-        if (p.relu) {
-#pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = v[i] > 0.0f ? v[i] : 0.0f;
-        }
-        uint4 hi[2], lo[2];
-        __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(hi);
-        __nv_bfloat162* l2 = reinterpret_cast<__nv_bfloat162*>(lo);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const __nv_bfloat162 hh = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
-          h2[e] = hh;
-          const float2 hf = __bfloat1622float2(hh);
-          l2[e] = __floats2bfloat162_rn(v[2 * e] - hf.x, v[2 * e + 1] - hf.y);
-        }
-        uint4* oh = reinterpret_cast<uint4*>(p.out_hi + off);
-        oh[0] = hi[0];
-        oh[1] = hi[1];
-        if (p.out_lo) {
-          uint4* ol = reinterpret_cast<uint4*>(p.out_lo + off);
-          ol[0] = lo[0];
-          ol[1] = lo[1];
+          for (int q = 0; q < 4; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        } else {
+          epilogue_store(p, v, obase + co, co);
         }
       }
       tc_fence_before();
@@ -309,6 +350,41 @@ __global__ void __launch_bounds__(192, 1) tc_conv_kernel(const __grid_constant__
       if (lane == 0) mbar_arrive(tempty0 + 8 * acc);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
+      if (split) {
+        // Last CTA to finish this output tile sums the partials (fixed order) and stores.
+        __threadfence();
+        epi_bar();
+        if (warp == 2 && lane == 0) {
+          const int old = atomicAdd(p.ws_counters + x.tile_mn, 1);
+          *s_last = (old == g.ks - 1) ? 1 : 0;
+        }
+        epi_bar();
+        if (*s_last) {
+          __threadfence();
+          if (valid) {
+#pragma unroll 1
+            for (int c16 = 0; c16 < BN / 16; ++c16) {
+              float v[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) v[i] = 0.0f;
+              for (int k = 0; k < g.ks; ++k) {
+                const float4* src = reinterpret_cast<const float4*>(wsrow + static_cast<size_t>(k) * kBM * BN + c16 * 16);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  const float4 f = __ldcg(src + q);
+                  v[4 * q] += f.x;
+                  v[4 * q + 1] += f.y;
+                  v[4 * q + 2] += f.z;
+                  v[4 * q + 3] += f.w;
+                }
+              }
+              const int co = x.tn * BN + c16 * 16;
+              epilogue_store(p, v, obase + co, co);
+            }
+          }
+          if (warp == 2 && lane == 0) p.ws_counters[x.tile_mn] = 0;
+        }
+      }
     }
   }
   __syncthreads();
@@ -335,25 +411,27 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-template <int BN>
-cudaError_t launch_bn(const TcConvParams& p, int num_sms, cudaStream_t stream) {
-  using Cfg = TcCfg<BN>;
+template <int BN, bool X3>
+cudaError_t launch_cfg(const TcConvParams& p, int num_sms, cudaStream_t stream) {
+  using Cfg = TcCfg<BN, X3>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(tc_conv_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
+    cudaError_t e =
+        cudaFuncSetAttribute(tc_conv_kernel<BN, X3>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  int tiles = tc_conv_max_tiles(p, BN);
+  long long tiles = tc_conv_max_tiles(p, BN);
+  if (p.mode == 0 && p.ks_max > 1) tiles *= p.ks_max;
   if (tiles <= 0) return cudaSuccess;
-  const int grid = tiles < num_sms ? tiles : num_sms;
-  tc_conv_kernel<BN><<<grid, 192, Cfg::kSmem, stream>>>(p);
+  const int grid = tiles < num_sms ? static_cast<int>(tiles) : num_sms;
+  tc_conv_kernel<BN, X3><<<grid, 192, Cfg::kSmem, stream>>>(p);
   return cudaGetLastError();
 }
 
 }  // namespace
 
-bool encode_act_map(CUtensorMap* map, const void* base, int C, int W, int H, int N, int P, int wb, int hb) {
+bool encode_act_map(CUtensorMap* map, const void* base, int C, int W, int H, int N, int P, int wb, int hb, int stride) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[5] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H),
@@ -363,8 +441,10 @@ bool encode_act_map(CUtensorMap* map, const void* base, int C, int W, int H, int
   strides[1] = strides[0] * W;
   strides[2] = strides[1] * H;
   strides[3] = strides[2] * N;
-  cuuint32_t box[5] = {64, static_cast<cuuint32_t>(wb), static_cast<cuuint32_t>(hb), 1, 1};
-  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  const cuuint32_t st = static_cast<cuuint32_t>(stride < 1 ? 1 : stride);
+  // With traversal stride st, TMA loads boxDim/st elements: box = wanted * st.
+  cuuint32_t box[5] = {64, static_cast<cuuint32_t>(wb) * st, static_cast<cuuint32_t>(hb) * st, 1, 1};
+  cuuint32_t estr[5] = {1, st, st, 1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -384,8 +464,8 @@ bool encode_weight_map(CUtensorMap* map, const void* base, int K, int Cout, int 
   return r == CUDA_SUCCESS;
 }
 
-int tc_conv_pick_bn(int Cout) {
-  if (Cout % 256 == 0 && Cout >= 512) return 256;
+int tc_conv_pick_bn(int Cout, int segs) {
+  if (segs == 1 && Cout % 256 == 0 && Cout >= 512) return 256;
   if (Cout % 128 == 0) return 128;
   return 64;
 }
@@ -400,18 +480,21 @@ int tc_conv_max_tiles(const TcConvParams& p, int BN) {
     n_groups = (count + p.ipt - 1) / p.ipt;
     tiles_w = p.tiles_w;
   }
-  const long long total = n_groups * p.tiles_h * tiles_w * (p.Cout / BN) * p.ksplit;
+  const long long total = n_groups * p.tiles_h * tiles_w * (p.Cout / BN) * (p.mode == 1 ? p.ksplit : 1);
   return total > 0x7fffffff ? 0x7fffffff : static_cast<int>(total);
 }
 
+size_t tc_conv_ws_floats(int BN, int max_ctas) { return 2ull * static_cast<size_t>(max_ctas) * kBM * BN; }
+
 cudaError_t tc_conv_launch(const TcConvParams& p, int BN, int num_sms, cudaStream_t stream) {
+  const bool x3 = p.segs == 3;
   switch (BN) {
     case 64:
-      return launch_bn<64>(p, num_sms, stream);
+      return x3 ? launch_cfg<64, true>(p, num_sms, stream) : launch_cfg<64, false>(p, num_sms, stream);
     case 128:
-      return launch_bn<128>(p, num_sms, stream);
+      return x3 ? launch_cfg<128, true>(p, num_sms, stream) : launch_cfg<128, false>(p, num_sms, stream);
     case 256:
-      return launch_bn<256>(p, num_sms, stream);
+      return x3 ? cudaErrorInvalidValue : launch_cfg<256, false>(p, num_sms, stream);
     default:
       return cudaErrorInvalidValue;
   }

@@ -1,6 +1,6 @@
 // Persistent tcgen05 implicit-GEMM kernel: base-model convolutions (NHWC,
-// 3x3/1x1, stride via phase split), dense FC layers (plain GEMM mode) and the
-// FC(h) cache predictor GEMMs (split-K fp32 partials).
+// any k x k, stride 1 or 2 through TMA traversal strides), dense FC layers
+// (plain GEMM mode) and the FC(h) cache predictor GEMMs (split-K fp32 partials).
 //
 // A operand: activations as a 5-D TMA tensor (C, W, H, N, P) in bf16, C
 // innermost; each K-step loads one 64-channel slice of one filter tap for the
@@ -9,9 +9,14 @@
 // Accumulators live in TMEM (double-buffered, 2*BN columns).
 //
 // Precision: segs == 1 -> plain bf16 x bf16 -> fp32. segs == 3 -> "bf16x3":
-// every operand is stored as hi + lo bf16 planes and the kernel accumulates
-// hi*hi + hi*lo + lo*hi, which is fp32-class (~2^-16 relative per product);
-// this is the parity tier the reference oracle is compared against.
+// every operand is stored as hi + lo bf16 planes; one pipeline stage carries
+// A_hi, A_lo, B_hi, B_lo and the MMA warp accumulates hi*hi + hi*lo + lo*hi
+// (fp32-class, ~2^-16 relative per product) — the parity tier.
+//
+// Split-K (mode 0, ks_max > 1): the split factor is chosen ON DEVICE from the
+// surviving-request count so the grid stays full as requests exit; partial
+// tiles go to an fp32 workspace and the last CTA of each tile (atomic
+// counter) sums them in a fixed order and runs the epilogue (deterministic).
 #pragma once
 
 #include <cstdint>
@@ -28,17 +33,21 @@ struct TcConvParams {
   CUtensorMap tmB[2];  // weight planes hi, lo (2-D: K, Cout)
   int plain;           // 1: plain GEMM over rows (A = [rows, K], count = rows)
   int Ho, Wo;          // output spatial dims
-  int hb, wb, ipt;     // A box geometry: ipt images x hb x wb = 128 rows
+  int hb, wb, ipt;     // output tile geometry: ipt images x hb x wb = 128 rows
   int tiles_h, tiles_w;
+  int conv_stride;     // input coordinate = output * conv_stride + tap offset
   int C;               // input channels per tap (multiple of 64)
   int ntaps;
-  int segs;            // 1 or 3
+  int segs;            // 1 (bf16) or 3 (bf16x3)
   int Cout;            // output channels (multiple of BN)
-  int ksplit;          // split-K factor (mode 1 only)
+  int ksplit;          // mode 1: static split-K factor
+  int ks_max;          // mode 0: dynamic split-K upper bound (1 = off)
+  float* ws;           // mode 0 split-K workspace (fp32 partial tiles)
+  int* ws_counters;    // per output tile arrival counters (zeroed; reset by the last CTA)
   const int* surv;     // survivor image list (nullptr = identity)
   const int* count;    // device-side image/row count (nullptr -> count_static)
   int count_static;
-  int mode;            // 0: bf16 NHWC out (+lo), 1: fp32 partials [ksplit][rows_total][Cout]
+  int mode;            // 0: NHWC out (+lo), 1: fp32 partials [ksplit][rows_total][Cout]
   int rows_total;      // mode 1 row stride
   const float* scale;  // per-Cout multiplier (nullable = 1)
   const float* shift;  // per-Cout bias (nullable = 0)
@@ -54,11 +63,14 @@ struct TcConvParams {
 };
 
 // Host helpers (tc_conv.cu).
-bool encode_act_map(CUtensorMap* map, const void* base, int C, int W, int H, int N, int P, int wb, int hb);
+bool encode_act_map(CUtensorMap* map, const void* base, int C, int W, int H, int N, int P, int wb, int hb,
+                    int stride = 1);
 bool encode_weight_map(CUtensorMap* map, const void* base, int K, int Cout, int BN);
-int tc_conv_pick_bn(int Cout);
+int tc_conv_pick_bn(int Cout, int segs = 1);
 // Upper bound on the tile count at count_static (used to size the grid).
 int tc_conv_max_tiles(const TcConvParams& p, int BN);
+// Workspace floats needed for mode-0 split-K with `max_ctas` CTAs.
+size_t tc_conv_ws_floats(int BN, int max_ctas);
 cudaError_t tc_conv_launch(const TcConvParams& p, int BN, int num_sms, cudaStream_t stream);
 
 }  // namespace lcb

@@ -74,7 +74,7 @@ static void report(const char* name, double max_rel, double tol) {
 
 // Conv test: input NHWC [N,H,W,C], 3x3 (or 1x1) stride s, pad k/2; output [N,Ho,Wo,Cout].
 static void conv_test(const char* name, int N, int H, int W, int C, int Cout, int k, int stride, bool x3,
-                      bool use_res, bool relu, bool use_surv, int BNforce = 0) {
+                      bool use_res, bool relu, bool use_surv, int BNforce = 0, int ks_max = 1) {
   const int pad = k / 2;
   const int Ho = (H + 2 * pad - k) / stride + 1, Wo = (W + 2 * pad - k) / stride + 1;
   std::vector<float> x(static_cast<size_t>(N) * H * W * C), wt(static_cast<size_t>(Cout) * k * k * C);
@@ -88,26 +88,9 @@ static void conv_test(const char* name, int N, int H, int W, int C, int Cout, in
   std::vector<float> res(static_cast<size_t>(N) * Ho * Wo * Cout);
   for (auto& v : res) v = static_cast<float>(urand() - 0.5);
 
-  // Phase split for stride 2: P = 4 phase images of [N, Hp, Wp, C].
+  // Stride 2 uses TMA traversal strides on the original NHWC tensor.
   int P = 1, Hs = H, Ws = W;
   std::vector<float> src = x;
-  if (stride == 2) {
-    P = 4;
-    Hs = (H + 1) / 2;
-    Ws = (W + 1) / 2;
-    src.assign(static_cast<size_t>(4) * N * Hs * Ws * C, 0.f);
-    for (int ph = 0; ph < 2; ++ph)
-      for (int pw = 0; pw < 2; ++pw)
-        for (int n = 0; n < N; ++n)
-          for (int i = 0; i < Hs; ++i)
-            for (int j = 0; j < Ws; ++j) {
-              const int h = 2 * i + ph, w = 2 * j + pw;
-              if (h >= H || w >= W) continue;
-              for (int c = 0; c < C; ++c)
-                src[((((size_t)(ph * 2 + pw) * N + n) * Hs + i) * Ws + j) * C + c] =
-                    x[(((size_t)n * H + h) * W + w) * C + c];
-            }
-  }
   Planes ps = make_planes(src, x3), pw_ = make_planes(wt, x3), pr = make_planes(res, x3);
   // CPU reference on the planes' exact values.
   Planes px = make_planes(x, x3);
@@ -188,8 +171,19 @@ static void conv_test(const char* name, int N, int H, int W, int C, int Cout, in
   p.ipt = ipt;
   p.tiles_h = (Ho + hb - 1) / hb;
   p.tiles_w = (Wo + wb - 1) / wb;
+  p.conv_stride = stride;
   p.C = C;
   p.ntaps = k * k;
+  p.ks_max = ks_max;
+  float* dWs = nullptr;
+  int* dCtr = nullptr;
+  if (ks_max > 1) {
+    CK(cudaMalloc(&dWs, tc_conv_ws_floats(256, g_sms) * 4));
+    CK(cudaMalloc(&dCtr, 4 * g_sms * 4));
+    CK(cudaMemset(dCtr, 0, 4 * g_sms * 4));
+  }
+  p.ws = dWs;
+  p.ws_counters = dCtr;
   p.segs = x3 ? 3 : 1;
   p.Cout = Cout;
   p.ksplit = 1;
@@ -207,24 +201,13 @@ static void conv_test(const char* name, int N, int H, int W, int C, int Cout, in
   for (int r = 0; r < k; ++r)
     for (int s = 0; s < k; ++s) {
       const int t = r * k + s;
-      if (stride == 1) {
-        p.tap_phase[t] = 0;
-        p.tap_dh[t] = static_cast<signed char>(r - pad);
-        p.tap_dw[t] = static_cast<signed char>(s - pad);
-      } else {
-        // input row 2*oh + r - pad = 2*(oh + dh) + phase_h
-        const int oh_off = r - pad;  // in [-pad, k-1-pad]
-        const int ph = ((oh_off % 2) + 2) % 2, dh = (oh_off - ph) / 2;
-        const int ow_off = s - pad;
-        const int pw2 = ((ow_off % 2) + 2) % 2, dw = (ow_off - pw2) / 2;
-        p.tap_phase[t] = static_cast<signed char>(ph * 2 + pw2);
-        p.tap_dh[t] = static_cast<signed char>(dh);
-        p.tap_dw[t] = static_cast<signed char>(dw);
-      }
+      p.tap_phase[t] = 0;
+      p.tap_dh[t] = static_cast<signed char>(r - pad);
+      p.tap_dw[t] = static_cast<signed char>(s - pad);
     }
-  const int BN = BNforce ? BNforce : tc_conv_pick_bn(Cout);
-  bool ok = encode_act_map(&p.tmA[0], dA_hi, C, Ws, Hs, N, P, wb, hb) &&
-            encode_act_map(&p.tmA[1], dA_lo, C, Ws, Hs, N, P, wb, hb) &&
+  const int BN = BNforce ? BNforce : tc_conv_pick_bn(Cout, x3 ? 3 : 1);
+  bool ok = encode_act_map(&p.tmA[0], dA_hi, C, Ws, Hs, N, P, wb, hb, stride) &&
+            encode_act_map(&p.tmA[1], dA_lo, C, Ws, Hs, N, P, wb, hb, stride) &&
             encode_weight_map(&p.tmB[0], dW_hi, k * k * C, Cout, BN) &&
             encode_weight_map(&p.tmB[1], dW_lo, k * k * C, Cout, BN);
   if (!ok) {
@@ -253,7 +236,7 @@ static void conv_test(const char* name, int N, int H, int W, int C, int Cout, in
       if (d > max_rel) max_rel = d;
     }
   char label[160];
-  snprintf(label, sizeof label, "%s BN=%d hb=%d wb=%d ipt=%d", name, BN, hb, wb, ipt);
+  snprintf(label, sizeof label, "%s BN=%d hb=%d wb=%d ipt=%d ks=%d", name, BN, hb, wb, ipt, ks_max);
   // bf16 output rounding dominates in plain mode (2^-8); x3 keeps hi+lo (~2^-16).
   report(label, max_rel + (bad_unwritten ? 1.0 : 0.0), x3 ? 2e-4 : 1.2e-2);
   cudaFree(dA_hi);
@@ -268,6 +251,9 @@ static void conv_test(const char* name, int N, int H, int W, int C, int Cout, in
   cudaFree(dShift);
   cudaFree(dSurv);
   cudaFree(dCnt);
+  if (dWs) cudaFree(dWs);
+  if (dCtr) cudaFree(dCtr);
+  // split-K must leave every tile counter at zero for the next launch
 }
 
 // Plain GEMM rows x K times [Cout, K]^T with split-K fp32 partials.
@@ -303,7 +289,7 @@ static void gemm_test(const char* name, int M, int K, int Cout, bool x3, int ksp
   p.mode = 1;
   p.rows_total = M;
   p.out_f32 = dOut;
-  const int BN = tc_conv_pick_bn(Cout);
+  const int BN = tc_conv_pick_bn(Cout, x3 ? 3 : 1);
   bool ok = encode_act_map(&p.tmA[0], dA_hi, K, M, 1, 1, 1, 128, 1) &&
             encode_act_map(&p.tmA[1], dA_lo, K, M, 1, 1, 1, 128, 1) &&
             encode_weight_map(&p.tmB[0], dB_hi, K, Cout, BN) && encode_weight_map(&p.tmB[1], dB_lo, K, Cout, BN);
@@ -397,16 +383,24 @@ int main(int argc, char** argv) {
   gemm_test("gemm x3", 300, 192, 128, true, 1);
   gemm_test("gemm x3 splitk", 256, 4096, 256, true, 8);
   gemm_test("gemm bf16 N64", 130, 128, 64, false, 1);
+  gemm_test("gemm bf16 N512", 200, 256, 512, false, 2);
   conv_test("conv3x3 s1 32x32 x3", 2, 32, 32, 64, 64, 3, 1, true, true, true, false);
   conv_test("conv3x3 s1 32x32 bf16", 2, 32, 32, 64, 128, 3, 1, false, false, true, false);
   conv_test("conv3x3 s1 16x16 x3 surv", 5, 16, 16, 128, 128, 3, 1, true, true, true, true);
-  conv_test("conv3x3 s1 8x8 x3 surv", 7, 8, 8, 64, 256, 3, 1, true, false, true, true, 256);
+  conv_test("conv3x3 s1 8x8 x3 surv", 7, 8, 8, 64, 256, 3, 1, true, false, true, true);
+  conv_test("conv3x3 s1 8x8 bf16 BN256", 7, 8, 8, 64, 512, 3, 1, false, true, true, true, 256);
   conv_test("conv3x3 s1 4x4 x3 surv", 19, 4, 4, 128, 512, 3, 1, true, true, true, true);
   conv_test("conv3x3 s2 32->16 x3", 3, 32, 32, 64, 128, 3, 2, true, false, true, false);
+  conv_test("conv3x3 s2 16->8 bf16 surv", 5, 16, 16, 128, 256, 3, 2, false, true, true, true);
   conv_test("conv1x1 s2 16->8 x3", 5, 16, 16, 128, 256, 1, 2, true, false, false, true);
   conv_test("conv3x3 s1 7x7 x3", 5, 7, 7, 64, 128, 3, 1, true, true, true, false);
   conv_test("conv3x3 s1 14x14 bf16", 3, 14, 14, 64, 64, 3, 1, false, true, true, false);
   conv_test("conv1x1 s1 56x56 x3", 2, 56, 56, 64, 256, 1, 1, true, true, false, false);
+  conv_test("conv3x3 s2 56->28 x3", 2, 56, 56, 64, 128, 3, 2, true, false, true, false);
+  conv_test("conv3x3 s1 4x4 x3 splitK", 19, 4, 4, 128, 512, 3, 1, true, true, true, true, 0, 16);
+  conv_test("conv3x3 s1 8x8 bf16 splitK", 9, 8, 8, 256, 256, 3, 1, false, true, true, true, 0, 8);
+  conv_test("conv3x3 s1 4x4 x3 splitK again", 19, 4, 4, 128, 512, 3, 1, true, true, true, true, 0, 16);
+  conv_test("conv1x1 s2 8->4 bf16 splitK", 6, 8, 8, 256, 512, 1, 2, false, false, false, true, 256, 4);
   if (argc > 1 && strcmp(argv[1], "--perf") == 0) {
     perf_test(8192, 8192, 8192);
     perf_test(16384, 4096, 4096);
