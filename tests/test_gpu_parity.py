@@ -332,3 +332,15 @@ def test_repeated_serves_bit_identical():
             if shadow:
                 assert np.array_equal(r.probs, ref.probs, equal_nan=True)
                 assert np.array_equal(r.base_pred, ref.base_pred)
+
+
+def test_cpp_dropin_against_reference_library():
+    """tests/cpp/test_dropin.cpp: the unmodified reference library and the
+    B200 façade (include/latecache_b200.hpp) in one C++ binary."""
+    import subprocess
+    from tests.helpers import ROOT
+    exe = os.path.join(ROOT, "oracle", "_ref", "test_dropin")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/test_dropin not built (make -C oracle dropin)")
+    r = subprocess.run([exe, os.path.join(GOLDEN, "trained")], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "DROPIN OK" in r.stdout, r.stdout + r.stderr
