@@ -3,8 +3,10 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <string>
 
 namespace lcb {
@@ -52,6 +54,26 @@ void split_planes(const std::vector<float>& v, std::vector<__nv_bfloat16>& hi, s
 
 std::vector<float> to_f32(const std::vector<double>& v) { return std::vector<float>(v.begin(), v.end()); }
 
+// One stream per device shared by every engine on it: launches of different
+// engines never run concurrently, which the split-K reduction in tc_conv
+// relies on (all CTAs of a launch co-resident), and graph capture on that
+// stream is serialised by the device lock.
+struct DevStream {
+  std::recursive_mutex mu;
+  cudaStream_t stream = nullptr;
+};
+DevStream& dev_stream(int device) {
+  static std::mutex m;
+  static std::map<int, std::unique_ptr<DevStream>> streams;
+  std::lock_guard<std::mutex> g(m);
+  auto& p = streams[device];
+  if (!p) {
+    p = std::make_unique<DevStream>();
+    ck(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+  }
+  return *p;
+}
+
 }  // namespace
 
 struct DevCache {
@@ -83,6 +105,10 @@ struct DevCache {
   float* prob = nullptr;
   float* pr_out = nullptr;
   float* logits_out = nullptr;
+  float* fc_scratch = nullptr;
+  // fused GAP partials written by the tap conv's epilogue (Pool(C) caches)
+  float* gap = nullptr;
+  int gap_segs = 0;
   // lookup-only step list
   std::vector<Step> lookup_steps;
 };
@@ -132,7 +158,7 @@ Engine::Engine(int device, const BaseModel& model, std::vector<CacheVariant> var
   ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
   require(prop.major == 10, "engine: requires an sm_100 (B200) device");
   num_sms_ = prop.multiProcessorCount;
-  ck(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+  stream_ = dev_stream(device).stream;
   ck(cudaEventCreate(&ev0_), "event");
   ck(cudaEventCreate(&ev1_), "event");
 
@@ -155,6 +181,8 @@ Engine::Engine(int device, const BaseModel& model, std::vector<CacheVariant> var
             "engine: variant class count does not match the base model");
     cache_of_layer_[static_cast<size_t>(v.layer)] = static_cast<int>(k);
   }
+  const char* nf = std::getenv("LCB_NO_GAP_FUSION");
+  gap_fusion_ = !(nf && nf[0] == '1');
   build_weights();
   ck(cudaStreamSynchronize(stream_), "build");
 }
@@ -167,7 +195,6 @@ Engine::~Engine() {
   if (h_batch_) cudaFreeHost(h_batch_);
   if (ev0_) cudaEventDestroy(ev0_);
   if (ev1_) cudaEventDestroy(ev1_);
-  if (stream_) cudaStreamDestroy(stream_);
 }
 
 void Engine::build_weights() {
@@ -361,6 +388,10 @@ void Engine::build_weights() {
     c->prob = static_cast<float*>(dalloc(static_cast<size_t>(B) * sizeof(float)));
     c->pr_out = static_cast<float*>(dalloc(static_cast<size_t>(B) * C * sizeof(float)));
     c->logits_out = static_cast<float*>(dalloc(static_cast<size_t>(B) * C * sizeof(float)));
+    if (C > 32 && c->family != 2) {
+      const int feat = c->family == 1 ? c->width : c->h;
+      c->fc_scratch = static_cast<float*>(dalloc(static_cast<size_t>(rows_fc_splits(feat)) * B * C * sizeof(float)));
+    }
     caches_.push_back(std::move(c));
   }
   lk_tap_ = alloc_planes(static_cast<size_t>(B) * round_up(max_tap_storage, 64));
@@ -368,13 +399,19 @@ void Engine::build_weights() {
 
 // ------------------------------------------------------------------ lookups
 void Engine::add_lookup_steps(std::vector<Step>& steps, DevCache& c, const TapView& tap, int max_rows,
-                              bool stage_gather) {
+                              bool stage_gather, bool fused_gap) {
   DevCache* cp = &c;
   const long long L2 = model_.num_blocks + 2;
   const int cidx = (tap.count >= d_counts_ && tap.count < d_counts_ + L2) ? static_cast<int>(tap.count - d_counts_) : -1;
   const double eb = prec_ == kPrecX3 ? 4.0 : 2.0;  // bytes per activation element (hi + lo planes)
   const double tap_bytes = static_cast<double>(c.D) * eb;
-  if (c.family == 1) {
+  if (c.family == 1 && fused_gap && c.gap) {
+    steps.push_back({[cp, tap, max_rows](cudaStream_t s) {
+                       launch_gap_bins(cp->gap, cp->gap_segs, tap.C, tap.HW, tap.data_idx, tap.count, max_rows,
+                                       cp->feats, s);
+                     },
+                     2, 1, cidx, 0.0, 4.0 * c.gap_segs * c.width + 4.0 * c.width});
+  } else if (c.family == 1) {
     steps.push_back({[cp, tap, max_rows](cudaStream_t s) {
                        launch_pool_bins(tap, max_rows, cp->win, cp->width, cp->feats, s);
                      },
@@ -436,7 +473,7 @@ void Engine::add_lookup_steps(std::vector<Step>& steps, DevCache& c, const TapVi
   }
   const int rows_total = max_rows;
   steps.push_back({[cp, tap, max_rows, rows_total](cudaStream_t s) {
-                     CacheHeadParams p;
+                     CacheHeadParams p{};
                      p.family = cp->family;
                      p.classes = cp->classes;
                      p.feat = cp->family == 1 ? cp->width : (cp->family == 0 ? cp->h : cp->nchunks);
@@ -458,9 +495,10 @@ void Engine::add_lookup_steps(std::vector<Step>& steps, DevCache& c, const TapVi
                      p.label = cp->label;
                      p.pr_out = cp->pr_out;
                      p.logits_out = cp->logits_out;
+                     p.fc_scratch = cp->fc_scratch;
                      launch_cache_head(p, max_rows, s);
                    },
-                   2, 1, cidx, 0.0, 0.0});
+                   2, (c.classes > 32 && c.family != 2) ? 2 : 1, cidx, 0.0, 0.0});
 }
 
 // ------------------------------------------------------------------ MLP serve
@@ -695,6 +733,22 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow) {
       prm->relu = o.relu ? 1 : 0;
       prm->out_hi = out.hi;
       prm->out_lo = out.lo;
+      if (o.tap >= 0 && gap_fusion_) {
+        // Pool(C) cache on this conv's output: GAP partials from the epilogue.
+        const int ci = cache_of_layer_[static_cast<size_t>(o.tap + 1)];
+        if (ci >= 0) {
+          DevCache& c = *caches_[static_cast<size_t>(ci)];
+          if (c.family == 1 && c.win == Ho * Wo && c.width == o.Cout) {
+            const int segs = tc_conv_gap_segs(prm->tiles_h, prm->tiles_w, hb, wb);
+            if (!c.gap) {
+              c.gap = static_cast<float*>(dalloc(static_cast<size_t>(B) * segs * o.Cout * sizeof(float)));
+              c.gap_segs = segs;
+            }
+            prm->gap_out = c.gap;
+            prm->gap_segs = segs;
+          }
+        }
+      }
       for (int r = 0; r < o.k; ++r)
         for (int sx = 0; sx < o.k; ++sx) {
           const int t = r * o.k + sx;
@@ -710,11 +764,13 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow) {
     } else if (o.kind == CnnOpKind::Head) {
       Planes in = slot_buf_[static_cast<size_t>(o.in)];
       const int classes = model_.num_classes, C = o.C, HW = o.H * o.W;
-      steps.push_back({[this, in, C, HW, classes, cur_ids, cur_count, B](cudaStream_t s) {
+      float* fs = static_cast<float*>(dalloc(static_cast<size_t>(B) * C * sizeof(float)));
+      float* ls = static_cast<float*>(dalloc(static_cast<size_t>(rows_fc_splits(C)) * B * classes * sizeof(float)));
+      steps.push_back({[this, in, C, HW, classes, cur_ids, cur_count, B, fs, ls](cudaStream_t s) {
                          launch_cnn_head(in.hi, in.lo, C, HW, head_w_, head_b_, classes, cur_ids, cur_count, B,
-                                         d_base_, nullptr, d_exit_, d_served_, d_exit_ns_, s);
+                                         d_base_, nullptr, d_exit_, d_served_, d_exit_ns_, fs, ls, s);
                        },
-                       0});
+                       0, classes > 32 ? 3 : 1});
     }
     if (o.tap >= 0) {
       const int layer = o.tap + 1;
@@ -731,7 +787,7 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow) {
         tap.HW = ti.H * ti.W;
         tap.data_idx = cur_ids;
         tap.count = cur_count;
-        add_lookup_steps(steps, c, tap, B, true);
+        add_lookup_steps(steps, c, tap, B, true, c.gap != nullptr);
         int* ids_out = ids + static_cast<size_t>(layer) * B;
         int* cnt_out = counts + layer;
         DevCache* cp = &c;
@@ -772,6 +828,7 @@ int Engine::count_kernels(bool shadow, int kind) {
 }
 
 void Engine::serve(int B, bool shadow, bool use_graph) {
+  std::lock_guard<std::recursive_mutex> dev_lock(dev_stream(device_).mu);
   require(B > 0 && B <= max_batch_, "serve: batch size " + std::to_string(B) + " outside [1, max_batch]");
   ck(cudaSetDevice(device_), "cudaSetDevice");
   *h_batch_ = B;
@@ -795,6 +852,7 @@ void Engine::serve(int B, bool shadow, bool use_graph) {
 }
 
 void Engine::serve_host(const float* x, int B, bool shadow, bool use_graph) {
+  std::lock_guard<std::recursive_mutex> dev_lock(dev_stream(device_).mu);
   require(B > 0 && B <= max_batch_, "serve: batch size " + std::to_string(B) + " outside [1, max_batch]");
   ck(cudaSetDevice(device_), "cudaSetDevice");
   ck(cudaMemcpyAsync(d_x_, x, static_cast<size_t>(B) * model_.input_dim() * sizeof(float), cudaMemcpyHostToDevice,
@@ -806,6 +864,7 @@ void Engine::serve_host(const float* x, int B, bool shadow, bool use_graph) {
 void Engine::synchronize() { ck(cudaStreamSynchronize(stream_), "synchronize"); }
 
 void Engine::copy_results(int B, int* exit_layer, int* served, int* base, float* probs_LB, double* latency_ms) {
+  std::lock_guard<std::recursive_mutex> dev_lock(dev_stream(device_).mu);
   ck(cudaSetDevice(device_), "cudaSetDevice");
   if (exit_layer) ck(cudaMemcpyAsync(exit_layer, d_exit_, B * sizeof(int), cudaMemcpyDeviceToHost, stream_), "d2h");
   if (served) ck(cudaMemcpyAsync(served, d_served_, B * sizeof(int), cudaMemcpyDeviceToHost, stream_), "d2h");
@@ -829,6 +888,7 @@ void Engine::copy_results(int B, int* exit_layer, int* served, int* base, float*
 
 void Engine::lookup(int layer, const float* taps_dev, int B, int* hit, int* label, float* prob, float* pr,
                     float* logits) {
+  std::lock_guard<std::recursive_mutex> dev_lock(dev_stream(device_).mu);
   require(layer >= 1 && layer <= model_.num_blocks, "lookup: layer out of range");
   const int ci = cache_of_layer_[static_cast<size_t>(layer)];
   require(ci >= 0, "lookup: no cache attached at layer " + std::to_string(layer));
@@ -907,6 +967,7 @@ void Engine::set_selector_out(int layer, double gain, double bias) {
 }
 
 std::vector<StepProfile> Engine::profile(int B, bool shadow) {
+  std::lock_guard<std::recursive_mutex> dev_lock(dev_stream(device_).mu);
   require(B > 0 && B <= max_batch_, "profile: batch outside [1, max_batch]");
   ck(cudaSetDevice(device_), "cudaSetDevice");
   *h_batch_ = B;
@@ -934,6 +995,7 @@ std::vector<StepProfile> Engine::profile(int B, bool shadow) {
 }
 
 double Engine::serve_timed(int B, bool shadow) {
+  std::lock_guard<std::recursive_mutex> dev_lock(dev_stream(device_).mu);
   steps_for(shadow);
   ck(cudaEventRecord(ev0_, stream_), "event");
   serve(B, shadow, true);
@@ -945,6 +1007,7 @@ double Engine::serve_timed(int B, bool shadow) {
 }
 
 double Engine::time_serve_ms(int B, bool shadow, int iters) {
+  std::lock_guard<std::recursive_mutex> dev_lock(dev_stream(device_).mu);
   serve(B, shadow, true);  // capture outside the timed region
   ck(cudaStreamSynchronize(stream_), "sync");
   ck(cudaEventRecord(ev0_, stream_), "event");

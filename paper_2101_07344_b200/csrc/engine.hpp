@@ -97,7 +97,8 @@ class Engine {
   void build_weights();
   void build_mlp_steps(std::vector<Step>& steps, bool shadow);
   void build_cnn_steps(std::vector<Step>& steps, bool shadow);
-  void add_lookup_steps(std::vector<Step>& steps, DevCache& c, const TapView& tap, int max_rows, bool stage_gather);
+  void add_lookup_steps(std::vector<Step>& steps, DevCache& c, const TapView& tap, int max_rows, bool stage_gather,
+                        bool fused_gap = false);
   std::vector<Step>& steps_for(bool shadow);
   void* dalloc(size_t bytes);
   Planes alloc_planes(size_t elems);
@@ -153,6 +154,7 @@ class Engine {
   std::vector<Planes> slot_buf_;  // by slot
   float* ws_ = nullptr;        // split-K workspace shared by all contractions (stream-ordered)
   int* ws_counters_ = nullptr;
+  bool gap_fusion_ = true;  // LCB_NO_GAP_FUSION=1 disables the fused Pool(C) partials
   Planes im2col_buf_;
 
   std::vector<Step> steps_compact_, steps_shadow_;

@@ -158,6 +158,21 @@ __global__ void pool_channels_kernel(TapView t, int gch, int width, float inv, f
   }
 }
 
+// Fused-GAP bins: bin c = (sum over the tap conv's segment partials, fixed
+// order) x 1/HW; the partials were written by tc_conv's epilogue.
+__global__ void gap_bins_kernel(const float* gap, int segs, int C, float inv, const int* data_idx, const int* count,
+                                float* bins) {
+  const int r = blockIdx.x;
+  if (r >= *count) return;
+  const long long n = data_idx ? data_idx[r] : r;
+  const float* src = gap + n * segs * C;
+  for (int c = blockIdx.y * blockDim.x + threadIdx.x; c < C; c += gridDim.y * blockDim.x) {
+    float a = 0.0f;
+    for (int sg = 0; sg < segs; ++sg) a += src[static_cast<long long>(sg) * C + c];
+    bins[static_cast<long long>(r) * C + c] = a * inv;
+  }
+}
+
 // Generic: one thread per bin, sequential over its flat window.
 __global__ void pool_generic_kernel(TapView t, int win, int width, float inv, float* bins) {
   const int r = blockIdx.x;
@@ -233,6 +248,103 @@ __global__ void conv1d_partials_kernel(TapView t, long long D, int kernel, int s
   }
 }
 
+// ------------------------------------------------------------------ batched FC
+// part[z][r][k] = sum_{o in K-slice z} A(r, o) * W[k][o] over the surviving
+// rows: the reference FC (network.cpp:116-126) as a split-K batched GEMM; the
+// consumer adds b[k] + sum_z part[z][r][k] in ascending z (fixed order). A is
+// a dense fp32 [rows][feat] matrix (kMode 0) or the FC(h) cache hidden layer
+// relu(b1[o] + sum_s partials[s][r][o]) (kMode 1, split-K partials of the
+// tensor-core GEMM). Every 16-row tile reads its W slice once instead of
+// once per row: the logits GEMM of heads with many classes (ImageNet).
+constexpr int kFcBM = 16, kFcBN = 64, kFcBK = 32;
+
+template <int kMode>
+__global__ void __launch_bounds__(256) rows_fc_kernel(const float* A, long long lda, int ks, long long part_stride,
+                                                      const float* b1, int feat, int kslice, const float* W,
+                                                      int classes, const int* count, long long max_rows, float* out) {
+  __shared__ float As[kFcBM][kFcBK + 1];
+  __shared__ float Ws[kFcBN][kFcBK + 1];
+  const int n = *count;
+  const int r0 = blockIdx.y * kFcBM, k0 = blockIdx.x * kFcBN;
+  if (r0 >= n) return;
+  const int z = blockIdx.z;
+  const int oz0 = z * kslice, oz1 = oz0 + kslice < feat ? oz0 + kslice : feat;
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+  float acc[2][2] = {{0.0f, 0.0f}, {0.0f, 0.0f}};
+  for (int o0 = oz0; o0 < oz1; o0 += kFcBK) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int idx = tid + i * 256, rr = idx >> 5, oo = idx & 31;
+      const int r = r0 + rr, o = o0 + oo;
+      float v = 0.0f;
+      if (r < n && o < oz1) {
+        if (kMode == 0) {
+          v = A[static_cast<long long>(r) * lda + o];
+        } else {
+          float a = b1[o];
+          for (int s = 0; s < ks; ++s) a += A[static_cast<long long>(s) * part_stride + static_cast<long long>(r) * lda + o];
+          v = a > 0.0f ? a : 0.0f;
+        }
+      }
+      As[rr][oo] = v;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int idx = tid + i * 256, kk = idx >> 5, oo = idx & 31;
+      const int k = k0 + kk, o = o0 + oo;
+      Ws[kk][oo] = (k < classes && o < oz1) ? W[static_cast<long long>(k) * feat + o] : 0.0f;
+    }
+    __syncthreads();
+    const int olim = oz1 - o0 < kFcBK ? oz1 - o0 : kFcBK;
+    for (int o = 0; o < olim; ++o) {
+      const float a0 = As[2 * ty][o], a1 = As[2 * ty + 1][o];
+      const float w0 = Ws[tx][o], w1 = Ws[tx + 32][o];
+      acc[0][0] += a0 * w0;
+      acc[0][1] += a0 * w1;
+      acc[1][0] += a1 * w0;
+      acc[1][1] += a1 * w1;
+    }
+    __syncthreads();
+  }
+  float* outz = out + static_cast<long long>(z) * max_rows * classes;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int r = r0 + 2 * ty + i;
+    if (r >= n) continue;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int k = k0 + tx + 32 * j;
+      if (k < classes) outz[static_cast<long long>(r) * classes + k] = acc[i][j];
+    }
+  }
+}
+
+__device__ __forceinline__ float fc_logit(const float* part, int nz, long long zstride, const float* b, int r,
+                                          int classes, int k) {
+  float a = b[k];
+  for (int z = 0; z < nz; ++z) a += part[z * zstride + static_cast<long long>(r) * classes + k];
+  return a;
+}
+
+// Global average pool of the surviving images' final activations (NHWC,
+// image ids[r]) -> feats [rows][C]; per channel a sequential pixel sum, then
+// x (1/HW) as the base head's GAP.
+__global__ void gap_rows_kernel(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int C, int HW, const int* ids,
+                                const int* count, float* feats) {
+  const int r = blockIdx.x;
+  if (r >= *count) return;
+  const long long n = ids[r];
+  TapView t;
+  t.hi = hi;
+  t.lo = lo;
+  const float inv = 1.0f / HW;
+  for (int c = blockIdx.y * blockDim.x + threadIdx.x; c < C; c += gridDim.y * blockDim.x) {
+    float a = 0.0f;
+    for (int q = 0; q < HW; ++q) a += ld_tap(t, (n * HW + q) * C + c);
+    feats[static_cast<long long>(r) * C + c] = a * inv;
+  }
+}
+
 // ------------------------------------------------------------------ head
 // Reference lookup (cache.cpp:259-265): pr = softmax(pred(tap)),
 // p = sigmoid(sel(pr)), hit = p >= delta (inclusive); label = argmax(pr).
@@ -249,7 +361,9 @@ __global__ void cache_head_kernel(CacheHeadParams p) {
   float* feat = sm + C;      // [feat]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
 
-  if (p.family == 2) {
+  if (p.pre_logits) {
+    for (int k = tid; k < C; k += blockDim.x) logits[k] = fc_logit(p.pre_logits, p.pre_nz, p.pre_zstride, p.b2, r, C, k);
+  } else if (p.family == 2) {
     for (int k = tid; k < C; k += blockDim.x) {
       float a = p.b2[k];
       for (int c = 0; c < p.feat; ++c) a += p.feats[(static_cast<long long>(r) * p.feat + c) * C + k];
@@ -528,7 +642,8 @@ template <bool kGap>
 __global__ void base_head_kernel(const __nv_bfloat16* hi, const __nv_bfloat16* lo, long long row_stride, int C, int HW,
                                  const float* W, const float* b, int classes, const int* ids, const int* count,
                                  int* base_pred, float* logits_out, int* exit_layer, int* served,
-                                 unsigned long long* exit_ns) {
+                                 unsigned long long* exit_ns, const float* pre_logits, int pre_nz,
+                                 long long pre_zstride) {
   extern __shared__ float sm[];
   __shared__ float red[32];
   __shared__ int bi_s[32];
@@ -543,7 +658,10 @@ __global__ void base_head_kernel(const __nv_bfloat16* hi, const __nv_bfloat16* l
   TapView t;
   t.hi = hi;
   t.lo = lo;
-  for (int c = tid; c < C; c += blockDim.x) {
+  if (pre_logits) {
+    for (int k = tid; k < classes; k += blockDim.x) logits[k] = fc_logit(pre_logits, pre_nz, pre_zstride, b, r, classes, k);
+  }
+  for (int c = tid; c < C && !pre_logits; c += blockDim.x) {
     if (kGap) {
       float a = 0.0f;
       for (int q = 0; q < HW; ++q) a += ld_tap(t, n * row_stride + static_cast<long long>(q) * C + c);
@@ -553,7 +671,7 @@ __global__ void base_head_kernel(const __nv_bfloat16* hi, const __nv_bfloat16* l
     }
   }
   __syncthreads();
-  for (int k = warp; k < classes; k += nw) {
+  for (int k = warp; k < classes && !pre_logits; k += nw) {
     const float* wr = W + static_cast<long long>(k) * C;
     float a = 0.0f;
     for (int c = lane; c < C; c += 32) a += wr[c] * feat[c];
@@ -681,33 +799,48 @@ __global__ void phase_split_kernel(const __nv_bfloat16* hi, const __nv_bfloat16*
 __global__ void maxpool_kernel(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int H, int W, int C, int k, int stride,
                                int pad, int Ho, int Wo, const int* ids, const int* count, __nv_bfloat16* ohi,
                                __nv_bfloat16* olo) {
+  // One thread per (output pixel, 8 channels): 16-byte loads/stores; per
+  // channel the first maximum in (r, s) order wins (hi and lo move together).
   const int j = blockIdx.x;
   if (j >= *count) return;
   const long long n = ids[j];
-  const long long per = static_cast<long long>(Ho) * Wo * C;
+  const int c8n = C / 8;
+  const long long per = static_cast<long long>(Ho) * Wo * c8n;
   for (long long i = blockIdx.y * blockDim.x + threadIdx.x; i < per; i += gridDim.y * blockDim.x) {
-    const int c = static_cast<int>(i % C);
-    const int ow = static_cast<int>((i / C) % Wo);
-    const int oh = static_cast<int>(i / (static_cast<long long>(C) * Wo));
-    float best = -FLT_MAX;
-    __nv_bfloat16 bh = __float2bfloat16_rn(0.0f), bl = __float2bfloat16_rn(0.0f);
-    for (int r = 0; r < k; ++r)
-      for (int s = 0; s < k; ++s) {
-        const int ih = oh * stride + r - pad, iw = ow * stride + s - pad;
-        if (ih < 0 || ih >= H || iw < 0 || iw >= W) continue;
-        const long long src = ((n * H + ih) * W + iw) * C + c;
-        const __nv_bfloat16 vh = hi[src];
-        const __nv_bfloat16 vl = lo ? lo[src] : __float2bfloat16_rn(0.0f);
-        const float v = __bfloat162float(vh) + __bfloat162float(vl);
-        if (v > best) {
-          best = v;
-          bh = vh;
-          bl = vl;
+    const int c8 = static_cast<int>(i % c8n);
+    const long long pix = i / c8n;
+    const int ow = static_cast<int>(pix % Wo), oh = static_cast<int>(pix / Wo);
+    float best[8];
+    uint4 bh = make_uint4(0, 0, 0, 0), bl = make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) best[e] = -FLT_MAX;
+    for (int r = 0; r < k; ++r) {
+      const int ih = oh * stride + r - pad;
+      if (ih < 0 || ih >= H) continue;
+      for (int s2 = 0; s2 < k; ++s2) {
+        const int iw = ow * stride + s2 - pad;
+        if (iw < 0 || iw >= W) continue;
+        const long long src = ((n * H + ih) * W + iw) * C + c8 * 8;
+        const uint4 vh = *reinterpret_cast<const uint4*>(hi + src);
+        const uint4 vl = lo ? *reinterpret_cast<const uint4*>(lo + src) : make_uint4(0, 0, 0, 0);
+        const __nv_bfloat16* h8 = reinterpret_cast<const __nv_bfloat16*>(&vh);
+        const __nv_bfloat16* l8 = reinterpret_cast<const __nv_bfloat16*>(&vl);
+        __nv_bfloat16* bh8 = reinterpret_cast<__nv_bfloat16*>(&bh);
+        __nv_bfloat16* bl8 = reinterpret_cast<__nv_bfloat16*>(&bl);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float v = __bfloat162float(h8[e]) + __bfloat162float(l8[e]);
+          if (v > best[e]) {
+            best[e] = v;
+            bh8[e] = h8[e];
+            bl8[e] = l8[e];
+          }
         }
       }
-    const long long dst = ((n * Ho + oh) * Wo + ow) * C + c;
-    ohi[dst] = bh;
-    if (olo) olo[dst] = bl;
+    }
+    const long long dst = ((n * Ho + oh) * Wo + ow) * C + c8 * 8;
+    *reinterpret_cast<uint4*>(ohi + dst) = bh;
+    if (olo) *reinterpret_cast<uint4*>(olo + dst) = bl;
   }
 }
 
@@ -746,6 +879,13 @@ void launch_pool_bins(const TapView& tap, int max_rows, int win, int width, floa
   }
 }
 
+void launch_gap_bins(const float* gap, int segs, int C, int HW, const int* data_idx, const int* count, int max_rows,
+                     float* bins, cudaStream_t s) {
+  if (max_rows <= 0) return;
+  const float inv = static_cast<float>(1.0 / HW);
+  gap_bins_kernel<<<dim3(max_rows, (C + 255) / 256), 256, 0, s>>>(gap, segs, C, inv, data_idx, count, bins);
+}
+
 void launch_conv1d_partials(const TapView& tap, int max_rows, long long D, int kernel, int stride, int out_dim,
                             const float* w1, float b1, const float* W2, int classes, int chunk_elems, int nchunks,
                             float* partials, cudaStream_t s) {
@@ -760,9 +900,35 @@ void launch_conv1d_partials(const TapView& tap, int max_rows, long long D, int k
                                                                     classes, chunk_elems, nchunks, partials);
 }
 
-void launch_cache_head(const CacheHeadParams& p, int max_rows, cudaStream_t s) {
+int rows_fc_splits(int feat) { return (feat + kRowsFcSlice - 1) / kRowsFcSlice; }
+
+void launch_rows_fc(const float* A, long long lda, int ks, long long part_stride, const float* b1, int feat,
+                    const float* W, int classes, const int* count, int max_rows, float* out, cudaStream_t s) {
   if (max_rows <= 0) return;
-  if (p.classes <= 32 && (p.family == 2 || p.feat <= 4096)) {
+  const dim3 grid((classes + kFcBN - 1) / kFcBN, (max_rows + kFcBM - 1) / kFcBM, rows_fc_splits(feat));
+  if (ks > 0)
+    rows_fc_kernel<1><<<grid, 256, 0, s>>>(A, lda, ks, part_stride, b1, feat, kRowsFcSlice, W, classes, count,
+                                           max_rows, out);
+  else
+    rows_fc_kernel<0><<<grid, 256, 0, s>>>(A, lda, 0, 0, nullptr, feat, kRowsFcSlice, W, classes, count, max_rows,
+                                           out);
+}
+
+void launch_cache_head(const CacheHeadParams& p_in, int max_rows, cudaStream_t s) {
+  if (max_rows <= 0) return;
+  CacheHeadParams p = p_in;
+  if (p.classes > 32 && p.family != 2 && p.fc_scratch) {
+    // Many classes: one batched split-K logits GEMM, then the per-row head.
+    if (p.family == 1)
+      launch_rows_fc(p.feats, p.feat, 0, 0, nullptr, p.feat, p.W2, p.classes, p.count, max_rows, p.fc_scratch, s);
+    else
+      launch_rows_fc(p.feats, p.hp, p.ks, p.rows_total * p.hp, p.b1, p.feat, p.W2, p.classes, p.count, max_rows,
+                     p.fc_scratch, s);
+    p.pre_logits = p.fc_scratch;
+    p.pre_nz = rows_fc_splits(p.feat);
+    p.pre_zstride = static_cast<long long>(max_rows) * p.classes;
+  }
+  if (!p.pre_logits && p.classes <= 32 && (p.family == 2 || p.feat <= 4096)) {
     const int warps = 4;
     const size_t smem = p.family == 2 ? 0 : static_cast<size_t>(warps) * p.feat * sizeof(float);
     static bool wattr = false;
@@ -773,7 +939,7 @@ void launch_cache_head(const CacheHeadParams& p, int max_rows, cudaStream_t s) {
     cache_head_warp_kernel<<<(max_rows + warps - 1) / warps, 32 * warps, smem, s>>>(p);
     return;
   }
-  const int feat_len = p.family == 2 ? p.classes : (p.feat > p.classes ? p.feat : p.classes);
+  const int feat_len = (p.family == 2 || p.pre_logits) ? p.classes : (p.feat > p.classes ? p.feat : p.classes);
   const size_t smem = static_cast<size_t>(p.classes + feat_len) * sizeof(float);
   static bool attr = false;
   if (!attr) {
@@ -820,16 +986,26 @@ void launch_mlp_head(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int dp, i
   if (max_rows <= 0) return;
   const size_t smem = static_cast<size_t>(dim + classes) * sizeof(float);
   base_head_kernel<false><<<max_rows, 128, smem, s>>>(hi, lo, dp, dim, 1, W, b, classes, ids, count, base_pred,
-                                                      logits_out, exit_layer, served, exit_ns);
+                                                      logits_out, exit_layer, served, exit_ns, nullptr, 0, 0);
 }
 
 void launch_cnn_head(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int C, int HW, const float* W, const float* b,
                      int classes, const int* ids, const int* count, int max_rows, int* base_pred, float* logits_out,
-                     int* exit_layer, int* served, unsigned long long* exit_ns, cudaStream_t s) {
+                     int* exit_layer, int* served, unsigned long long* exit_ns, float* feats_scratch,
+                     float* logits_scratch, cudaStream_t s) {
   if (max_rows <= 0) return;
+  const float* pre = nullptr;
+  if (classes > 32 && feats_scratch && logits_scratch) {
+    // Many classes: GAP rows, one batched logits GEMM, then the per-row softmax/argmax.
+    int gy = (C + 255) / 256;
+    gap_rows_kernel<<<dim3(max_rows, gy), 256, 0, s>>>(hi, lo, C, HW, ids, count, feats_scratch);
+    launch_rows_fc(feats_scratch, C, 0, 0, nullptr, C, W, classes, count, max_rows, logits_scratch, s);
+    pre = logits_scratch;
+  }
   const size_t smem = static_cast<size_t>(C + classes) * sizeof(float);
   base_head_kernel<true><<<max_rows, 256, smem, s>>>(hi, lo, static_cast<long long>(C) * HW, C, HW, W, b, classes, ids,
-                                                     count, base_pred, logits_out, exit_layer, served, exit_ns);
+                                                     count, base_pred, logits_out, exit_layer, served, exit_ns, pre,
+                                                     rows_fc_splits(C), static_cast<long long>(max_rows) * classes);
 }
 
 void launch_stem_im2col(const float* x, const int* count, int max_n, int C, int H, int W, int k, int stride, int pad,
@@ -855,7 +1031,7 @@ void launch_maxpool(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int H, int
                     int Ho, int Wo, const int* ids, const int* count, int max_rows, __nv_bfloat16* ohi,
                     __nv_bfloat16* olo, cudaStream_t s) {
   if (max_rows <= 0) return;
-  const long long per = static_cast<long long>(Ho) * Wo * C;
+  const long long per = static_cast<long long>(Ho) * Wo * (C / 8);
   int gy = static_cast<int>((per + 255) / 256);
   if (gy > 128) gy = 128;
   maxpool_kernel<<<dim3(max_rows, gy), 256, 0, s>>>(hi, lo, H, W, C, k, stride, pad, Ho, Wo, ids, count, ohi, olo);

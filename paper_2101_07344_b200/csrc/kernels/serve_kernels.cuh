@@ -50,13 +50,30 @@ struct CacheHeadParams {
   int* label;              // [rows] argmax(pr)
   float* pr_out;           // nullable [rows][classes]
   float* logits_out;       // nullable [rows][classes]
+  float* fc_scratch;       // nullable: [rows_fc_splits(feat)][max_rows][classes]; enables the
+                           // batched logits GEMM for classes > 32
+  // set by launch_cache_head: split-K logit partials (logit = b2 + sum_z part[z])
+  const float* pre_logits;
+  int pre_nz;
+  long long pre_zstride;
 };
 
+constexpr int kRowsFcSlice = 256;  // K-slice of the batched logits GEMM
+int rows_fc_splits(int feat);
+
 void launch_pool_bins(const TapView& tap, int max_rows, int win, int width, float* bins, cudaStream_t s);
+// Pool(C) bins from tc_conv's fused GAP partials gap[image][segs][C].
+void launch_gap_bins(const float* gap, int segs, int C, int HW, const int* data_idx, const int* count, int max_rows,
+                     float* bins, cudaStream_t s);
 void launch_conv1d_partials(const TapView& tap, int max_rows, long long D, int kernel, int stride, int out_dim,
                             const float* w1, float b1, const float* W2, int classes, int chunk_elems, int nchunks,
                             float* partials, cudaStream_t s);
 void launch_cache_head(const CacheHeadParams& p, int max_rows, cudaStream_t s);
+// out[z][r][k] = sum_{o in slice z} A(r,o) W[k][o] for r < *count, z < rows_fc_splits(feat)
+// (slices of kRowsFcSlice, ascending o inside a slice; out z-stride = max_rows*classes).
+// ks == 0: A dense [rows][lda]; ks > 0: A(r,o) = relu(b1[o] + sum_s A[s*part_stride + r*lda + o]).
+void launch_rows_fc(const float* A, long long lda, int ks, long long part_stride, const float* b1, int feat,
+                    const float* W, int classes, const int* count, int max_rows, float* out, cudaStream_t s);
 
 // First-hit exit + stable stream compaction (single CTA, warp ballot +
 // block prefix sum). Rows with hit leave; `ids_in[r]` is the original request
@@ -86,9 +103,12 @@ void launch_mlp_head(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int dp, i
                      int classes, const int* ids, const int* count, int max_rows, int* base_pred, float* logits_out,
                      int* exit_layer, int* served, unsigned long long* exit_ns, cudaStream_t s);
 // CNN head: GAP over HW then FC [classes][C] + b, softmax, argmax.
+// feats_scratch [max_rows][C] / logits_scratch [rows_fc_splits(C)][max_rows][classes] (nullable)
+// enable the batched path (GAP rows + logits GEMM) used for classes > 32.
 void launch_cnn_head(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int C, int HW, const float* W, const float* b,
                      int classes, const int* ids, const int* count, int max_rows, int* base_pred, float* logits_out,
-                     int* exit_layer, int* served, unsigned long long* exit_ns, cudaStream_t s);
+                     int* exit_layer, int* served, unsigned long long* exit_ns, float* feats_scratch,
+                     float* logits_scratch, cudaStream_t s);
 
 // Stem: NCHW fp32 images -> im2col rows [(n*Ho+oh)*Wo+ow][Kp] hi/lo with K
 // order (r, s, c), zero padded to Kp.

@@ -1,9 +1,10 @@
 // tcgen05 / TMA / TMEM implicit-GEMM kernel. See tc_conv.cuh for the contract.
 //
-// Warp roles (192 threads, one CTA per SM, persistent over tiles):
+// Warp roles (320 threads, one CTA per SM, persistent over tiles):
 //   warp 0      : TMA producer (lane 0) + TMEM allocator (whole warp)
 //   warp 1      : MMA issuer (lane 0)
-//   warps 2..5  : epilogue, one TMEM lane quadrant (warp % 4) each
+//   warps 2..9  : epilogue; warp w reads TMEM lane quadrant w % 4 and owns
+//                 column half (w - 2) / 4 of the tile (two warps per quadrant)
 // Pipelines: smem ring full/empty (TMA <-> MMA), TMEM double buffer
 // tfull/tempty (MMA <-> epilogue), split-K tile counters (CTA <-> CTA).
 #include "sm100_prims.cuh"
@@ -49,8 +50,10 @@ __device__ __forceinline__ TileGeom tile_geom(const TcConvParams& p, int BN) {
   if (p.mode == 1) {
     g.ks = p.ksplit;
   } else if (p.ks_max > 1 && g.tiles_mn > 0) {
-    // Fill the grid as the surviving-request count shrinks.
-    int ks = (static_cast<int>(gridDim.x) + g.tiles_mn - 1) / g.tiles_mn;
+    // Fill the grid as the surviving-request count shrinks. Floor, so that
+    // tiles_mn * ks <= gridDim.x: every CTA owns at most one unit of a split
+    // tile and all units of a tile are co-resident (the reduction waits on them).
+    int ks = static_cast<int>(gridDim.x) / g.tiles_mn;
     ks = ks > p.ks_max ? p.ks_max : ks;
     ks = ks > g.nk ? g.nk : ks;
     g.ks = ks < 1 ? 1 : ks;
@@ -83,10 +86,53 @@ __device__ __forceinline__ Tile decode_tile(int t, const TcConvParams& p, const 
 
 __device__ __forceinline__ int image_of(const TcConvParams& p, int idx) { return p.surv ? p.surv[idx] : idx; }
 
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+constexpr int kEpiWarps = 8;
+constexpr int kEpiThreads = kEpiWarps * 32;
+constexpr int kThreads = 64 + kEpiThreads;
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
-// scale/shift, residual, ReLU, hi/lo split and NHWC store of 16 channels.
-__device__ __forceinline__ void epilogue_store(const TcConvParams& p, float (&v)[16], size_t off, int co) {
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ unsigned long long clk() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+  return t;
+}
+
+// Trace slot (debug instrumentation): CTA < kTraceCtas, unit < kTraceUnits.
+constexpr int kTraceCtas = 8, kTraceUnits = 32;
+__device__ __forceinline__ void trace_put(const TcConvParams& p, int unit, int field) {
+  if (p.trace && blockIdx.x < kTraceCtas && unit < kTraceUnits)
+    p.trace[(blockIdx.x * kTraceUnits + unit) * 8 + field] = clk();
+}
+
+// Output element offset of tile row `row` (NHWC (n, h, w, 0) or plain row start).
+__device__ __forceinline__ bool out_row(const TcConvParams& p, const TileGeom& g, const Tile& x, int row, size_t& obase) {
+  if (p.plain) {
+    const int grow = x.w0 + row;
+    obase = static_cast<size_t>(grow) * p.Cout;
+    return grow < g.count;
+  }
+  const int rows_per_img = p.hb * p.wb;
+  const int j = row / rows_per_img;
+  const int pix = row % rows_per_img;
+  const int h = x.h0 + pix / p.wb;
+  const int w = x.w0 + pix % p.wb;
+  const int idx = x.grp * p.ipt + j;
+  const bool valid = (idx < g.count) && (h < p.Ho) && (w < p.Wo);
+  const int n = valid ? (p.surv ? p.surv[idx] : idx) : 0;
+  obase = ((static_cast<size_t>(n) * p.Ho + h) * p.Wo + w) * p.Cout;
+  return valid;
+}
+
+// scale/shift, residual (prefetched 16-byte chunks), ReLU, hi/lo split and
+// NHWC store of 16 channels.
+__device__ __forceinline__ void epilogue_store(const TcConvParams& p, float (&v)[16], size_t off, int co,
+                                               const uint4* rh, const uint4* rl) {
   if (p.scale) {
     const float4* sc = reinterpret_cast<const float4*>(p.scale + co);
 #pragma unroll
@@ -109,12 +155,10 @@ __device__ __forceinline__ void epilogue_store(const TcConvParams& p, float (&v)
       v[4 * q + 3] += s4.w;
     }
   }
-  if (p.res_hi) {
-    const uint4* rh = reinterpret_cast<const uint4*>(p.res_hi + off);
+  if (rh) {
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
-      const uint4 u = rh[q];
-      const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+      const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&rh[q]);
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const float2 f = __bfloat1622float2(b2[e]);
@@ -122,12 +166,10 @@ __device__ __forceinline__ void epilogue_store(const TcConvParams& p, float (&v)
         v[8 * q + 2 * e + 1] += f.y;
       }
     }
-    if (p.res_lo) {
-      const uint4* rl = reinterpret_cast<const uint4*>(p.res_lo + off);
+    if (rl) {
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
-        const uint4 u = rl[q];
-        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&rl[q]);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const float2 f = __bfloat1622float2(b2[e]);
@@ -161,8 +203,97 @@ __device__ __forceinline__ void epilogue_store(const TcConvParams& p, float (&v)
   }
 }
 
+// Same, loading the residual itself (split-K reduction path).
+__device__ __forceinline__ void epilogue_store_ld(const TcConvParams& p, float (&v)[16], size_t off, int co) {
+  uint4 rh[2], rl[2];
+  if (p.res_hi) {
+    rh[0] = reinterpret_cast<const uint4*>(p.res_hi + off)[0];
+    rh[1] = reinterpret_cast<const uint4*>(p.res_hi + off)[1];
+    if (p.res_lo) {
+      rl[0] = reinterpret_cast<const uint4*>(p.res_lo + off)[0];
+      rl[1] = reinterpret_cast<const uint4*>(p.res_lo + off)[1];
+    }
+  }
+  epilogue_store(p, v, off, co, p.res_hi ? rh : nullptr, p.res_lo ? rl : nullptr);
+}
+
+// Fused global-average-pool partials of the tap this conv produces (the
+// learned cache's Pool(C) = GAP predictor input, cache.cpp:104-140 with
+// window H*W): the 32 lanes of a warp hold 32 consecutive tile rows (pixels)
+// of one 16-channel chunk. A segmented reduce-scatter over the lane bits
+// inside an image's run of rows (segments of min(rows_per_img, 32) rows)
+// halves the live values at each xor step (16 -> 8 -> 4 -> 2 -> 1 values,
+// 15-16 shuffles instead of 80, fixed order), leaving each lane with the
+// segment sum of channel(s) selected by its lane bits; those lanes write the
+// sums to gap_out[n][segment][Cout]. Every segment slot of every present
+// image is written each launch (rows outside the image contribute 0), so the
+// head sums all gap_segs slots.
+template <int kO, int kN>
+__device__ __forceinline__ void rs_step(float (&v)[16], int lane) {
+  // keep the lower half of the kN live values if the lane bit is 0, else the upper half
+  const bool up = (lane & kO) != 0;
+#pragma unroll
+  for (int e = 0; e < kN / 2; ++e) {
+    const float send = up ? v[e] : v[e + kN / 2];
+    const float keep = up ? v[e + kN / 2] : v[e];
+    v[e] = keep + __shfl_xor_sync(0xffffffffu, send, kO);
+  }
+}
+
+template <int kSeg>
+__device__ __forceinline__ void gap_segment_t(const TcConvParams& p, const TileGeom& g, const Tile& x, int row,
+                                              int lane, float (&v)[16], int co) {
+  // Halving steps over the segment's lane bits (high to low); value e of a
+  // lane is then channel chbase + e.
+  int chbase = 0;
+  bool writer = true;
+  constexpr int kLive = kSeg == 8 ? 2 : 1;
+  if (kSeg == 32) {
+    rs_step<16, 16>(v, lane);
+    rs_step<8, 8>(v, lane);
+    rs_step<4, 4>(v, lane);
+    rs_step<2, 2>(v, lane);
+    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+    chbase = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+    writer = (lane & 1) == 0;
+  } else if (kSeg == 16) {
+    rs_step<8, 16>(v, lane);
+    rs_step<4, 8>(v, lane);
+    rs_step<2, 4>(v, lane);
+    rs_step<1, 2>(v, lane);
+    chbase = ((lane >> 3) & 1) * 8 + ((lane >> 2) & 1) * 4 + ((lane >> 1) & 1) * 2 + (lane & 1);
+  } else {
+    rs_step<4, 16>(v, lane);
+    rs_step<2, 8>(v, lane);
+    rs_step<1, 4>(v, lane);
+    chbase = ((lane >> 2) & 1) * 8 + ((lane >> 1) & 1) * 4 + (lane & 1) * 2;
+  }
+  const int rpi = p.hb * p.wb;
+  const int seg_first = row & ~(kSeg - 1);  // first row of this lane's segment
+  const int j = seg_first / rpi;
+  const int idx = x.grp * p.ipt + j;
+  if (writer && idx < g.count) {
+    const int n = p.surv ? p.surv[idx] : idx;
+    const int pix = seg_first % rpi;
+    const int per_tile = rpi > 32 ? rpi / 32 : 1;
+    const int tile_r = (x.h0 / p.hb) * p.tiles_w + x.w0 / p.wb;
+    const int sg = tile_r * per_tile + pix / 32;
+    float* dst = p.gap_out + (static_cast<size_t>(n) * p.gap_segs + sg) * p.Cout + co + chbase;
+#pragma unroll
+    for (int e = 0; e < kLive; ++e) dst[e] = v[e];
+  }
+}
+
+__device__ __forceinline__ void gap_segment(const TcConvParams& p, const TileGeom& g, const Tile& x, int row,
+                                            int lane, float (&v)[16], int co) {
+  const int rpi = p.hb * p.wb;  // power of two >= 8 (engine choose_box)
+  if (rpi >= 32) gap_segment_t<32>(p, g, x, row, lane, v, co);
+  else if (rpi == 16) gap_segment_t<16>(p, g, x, row, lane, v, co);
+  else gap_segment_t<8>(p, g, x, row, lane, v, co);
+}
+
 template <int BN, bool X3>
-__global__ void __launch_bounds__(192, 1) tc_conv_kernel(const __grid_constant__ TcConvParams p) {
+__global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_constant__ TcConvParams p) {
   using Cfg = TcCfg<BN, X3>;
   constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
@@ -170,7 +301,6 @@ __global__ void __launch_bounds__(192, 1) tc_conv_kernel(const __grid_constant__
   // stage s: [A_hi][A_lo?][B_hi][B_lo?]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
-  volatile int* s_last = reinterpret_cast<volatile int*>(tmem_holder + 1);
   const uint32_t full0 = smem_u32(bars);
   const uint32_t empty0 = smem_u32(bars + S);
   const uint32_t tfull0 = smem_u32(bars + 2 * S);
@@ -190,7 +320,7 @@ __global__ void __launch_bounds__(192, 1) tc_conv_kernel(const __grid_constant__
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(tfull0 + 8 * i, 1);
-      mbar_init(tempty0 + 8 * i, 4);
+      mbar_init(tempty0 + 8 * i, kEpiWarps);
     }
     fence_mbar_init();
     tma_prefetch_desc(&p.tmA[0]);
@@ -216,8 +346,10 @@ __global__ void __launch_bounds__(192, 1) tc_conv_kernel(const __grid_constant__
       int stage = 0;
       uint32_t phase = 0;
       const int box_bytes = p.hb * p.wb * 128;
-      for (int t = blockIdx.x; t < g.total; t += gridDim.x) {
+      int unit = 0;
+      for (int t = blockIdx.x; t < g.total; t += gridDim.x, ++unit) {
         const Tile x = decode_tile(t, p, g);
+        trace_put(p, unit, 0);
         int imgs[16];
         const int ipt = p.plain ? 1 : p.ipt;
         if (p.plain) {
@@ -250,6 +382,7 @@ __global__ void __launch_bounds__(192, 1) tc_conv_kernel(const __grid_constant__
             phase ^= 1;
           }
         }
+        trace_put(p, unit, 1);
       }
     }
   } else if (warp == 1) {
@@ -260,10 +393,12 @@ __global__ void __launch_bounds__(192, 1) tc_conv_kernel(const __grid_constant__
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = blockIdx.x; t < g.total; t += gridDim.x) {
+      int unit = 0;
+      for (int t = blockIdx.x; t < g.total; t += gridDim.x, ++unit) {
         const Tile x = decode_tile(t, p, g);
         mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1);
         tc_fence_after();
+        trace_put(p, unit, 2);
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int s = x.s_begin; s < x.s_end; ++s) {
           mbar_wait(full0 + 8 * stage, phase);
@@ -286,63 +421,89 @@ __global__ void __launch_bounds__(192, 1) tc_conv_kernel(const __grid_constant__
           }
         }
         umma_commit(tfull0 + 8 * acc);
+        trace_put(p, unit, 3);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
     }
   } else {
     // ------------------------------------------------ epilogue
+    constexpr int kCols = BN / 2;          // columns per epilogue warp
+    constexpr int kChunks = kCols / 8;     // 16-byte residual chunks per row
     const int quad = warp & 3;
+    const int half = (warp - 2) >> 2;
     const int row = quad * 32 + lane;
+    const int etid = threadIdx.x - 64;  // 0..255
+    const int col0 = half * kCols;
     int acc = 0;
     uint32_t acc_phase = 0;
-    const int rows_per_img = p.hb * p.wb;
-    for (int t = blockIdx.x; t < g.total; t += gridDim.x) {
+    int unit = 0;
+    for (int t = blockIdx.x; t < g.total; t += gridDim.x, ++unit) {
       const Tile x = decode_tile(t, p, g);
-      bool valid;
-      size_t obase;  // element offset of (n, h, w, 0) / row start
-      int grow = 0;
-      if (p.plain) {
-        grow = x.w0 + row;
-        valid = grow < g.count;
-        obase = static_cast<size_t>(grow) * p.Cout;
-      } else {
-        const int j = row / rows_per_img;
-        const int pix = row % rows_per_img;
-        const int h = x.h0 + pix / p.wb;
-        const int w = x.w0 + pix % p.wb;
-        const int idx = x.grp * p.ipt + j;
-        valid = (idx < g.count) && (h < p.Ho) && (w < p.Wo);
-        const int n = valid ? image_of(p, idx) : 0;
-        obase = ((static_cast<size_t>(n) * p.Ho + h) * p.Wo + w) * p.Cout;
-      }
+      size_t obase;
+      const bool valid = out_row(p, g, x, row, obase);
+      const int grow = x.w0 + row;
       const bool split = p.mode == 0 && g.ks > 1;
-      float* wsrow = split ? p.ws + (static_cast<size_t>(x.tile_mn) * g.ks * kBM + row) * BN : nullptr;
+      // Residual of this row's columns, fetched before the accumulator is
+      // ready so its latency overlaps the tile's MMAs.
+      uint4 rh[kChunks], rl[X3 ? kChunks : 1];
+      const bool use_res = p.mode == 0 && !split && valid && p.res_hi;
+      if (use_res) {
+        const uint4* src = reinterpret_cast<const uint4*>(p.res_hi + obase + x.tn * BN + col0);
+#pragma unroll
+        for (int i = 0; i < kChunks; ++i) rh[i] = src[i];
+        if (X3 && p.res_lo) {
+          const uint4* srl = reinterpret_cast<const uint4*>(p.res_lo + obase + x.tn * BN + col0);
+#pragma unroll
+          for (int i = 0; i < (X3 ? kChunks : 1); ++i) rl[i] = srl[i];
+        }
+      }
       mbar_wait(tfull0 + 8 * acc, acc_phase);
       tc_fence_after();
-      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * BN;
-#pragma unroll 1
+      if (etid == 0) trace_put(p, unit, 4);
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * BN + col0;
       const bool empty_k = x.s_end <= x.s_begin;  // no MMA wrote this accumulator
-      for (int c16 = 0; c16 < BN / 16; ++c16) {
-        float v[16];
-        tmem_ld16(t_row + c16 * 16, v);
-        if (empty_k) {
+      // split-K partial tile layout: [tile_mn][ks][BN/16][128 rows][16] (64 B per row chunk)
+      float* wsp = split ? p.ws + (static_cast<size_t>(x.tile_mn) * g.ks + x.ks) * kBM * BN : nullptr;
 #pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = 0.0f;
-        }
-        if (!valid) continue;
-        const int co = x.tn * BN + c16 * 16;
-        if (p.mode == 1) {
-          float4* dst = reinterpret_cast<float4*>(
-              p.out_f32 + (static_cast<size_t>(x.ks) * p.rows_total + grow) * p.Cout + co);
+      for (int c32 = 0; c32 < kCols / 32 || (kCols < 32 && c32 == 0); ++c32) {
+        constexpr int kSub = kCols < 32 ? kCols / 16 : 2;
+        float v[kSub][16];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-        } else if (split) {
-          float4* dst = reinterpret_cast<float4*>(wsrow + static_cast<size_t>(x.ks) * kBM * BN + c16 * 16);
+        for (int u = 0; u < kSub; ++u) tmem_ld16_nowait(t_row + c32 * 32 + u * 16, v[u]);
+        tmem_ld_wait();
 #pragma unroll
-          for (int q = 0; q < 4; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-        } else {
-          epilogue_store(p, v, obase + co, co);
+        for (int u = 0; u < kSub; ++u) {
+          if (empty_k) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[u][i] = 0.0f;
+          }
+          const int c16 = (col0 >> 4) + c32 * 2 + u;  // 16-column chunk index in the tile
+          const int co = x.tn * BN + c16 * 16;
+          if (split) {
+            float4* dst = reinterpret_cast<float4*>(wsp + (static_cast<size_t>(c16) * kBM + row) * 16);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              dst[q] = make_float4(v[u][4 * q], v[u][4 * q + 1], v[u][4 * q + 2], v[u][4 * q + 3]);
+          } else if (p.mode == 1) {
+            if (valid) {
+              float4* dst = reinterpret_cast<float4*>(
+                  p.out_f32 + (static_cast<size_t>(x.ks) * p.rows_total + grow) * p.Cout + co);
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                dst[q] = make_float4(v[u][4 * q], v[u][4 * q + 1], v[u][4 * q + 2], v[u][4 * q + 3]);
+            }
+          } else {
+            if (valid) {
+              const int ci = (c32 * 2 + u) * 2;  // residual chunk index within this warp's columns
+              epilogue_store(p, v[u], obase + co, co, use_res ? &rh[ci] : nullptr,
+                             (use_res && X3 && p.res_lo) ? &rl[X3 ? ci : 0] : nullptr);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) v[u][i] = 0.0f;
+            }
+            if (p.gap_out) gap_segment(p, g, x, row, lane, v[u], co);  // warp-uniform call
+          }
         }
       }
       tc_fence_before();
@@ -351,40 +512,60 @@ __global__ void __launch_bounds__(192, 1) tc_conv_kernel(const __grid_constant__
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
       if (split) {
-        // Last CTA to finish this output tile sums the partials (fixed order) and stores.
+        // All ks CTAs of this tile are resident (one unit per CTA, single
+        // round): publish the partial, wait for the others, then each CTA
+        // reduces 1/ks of the tile in a fixed k order and runs the epilogue.
+        int* arr = p.ws_counters + 2 * x.tile_mn;
+        int* dep = arr + 1;
         __threadfence();
         epi_bar();
-        if (warp == 2 && lane == 0) {
-          const int old = atomicAdd(p.ws_counters + x.tile_mn, 1);
-          *s_last = (old == g.ks - 1) ? 1 : 0;
+        if (etid == 0) {
+          atomicAdd(arr, 1);
+          while (ld_acquire(arr) < g.ks) __nanosleep(64);
         }
         epi_bar();
-        if (*s_last) {
-          __threadfence();
-          if (valid) {
-#pragma unroll 1
-            for (int c16 = 0; c16 < BN / 16; ++c16) {
-              float v[16];
+        // Warp units of (16-column chunk, 32-row quarter), so the lanes of a
+        // warp hold 32 consecutive rows (segment-aligned for the GAP partials).
+        const int nu = (BN / 16) * (kBM / 32);
+        const int u0 = static_cast<int>((static_cast<long long>(nu) * x.ks) / g.ks);
+        const int u1 = static_cast<int>((static_cast<long long>(nu) * (x.ks + 1)) / g.ks);
+        const float* tile_ws = p.ws + static_cast<size_t>(x.tile_mn) * g.ks * kBM * BN;
+        for (int uu = u0 + (etid >> 5); uu < u1; uu += kEpiWarps) {
+          const int c16 = uu / (kBM / 32), r = (uu % (kBM / 32)) * 32 + lane;
+          float v[16];
 #pragma unroll
-              for (int i = 0; i < 16; ++i) v[i] = 0.0f;
-              for (int k = 0; k < g.ks; ++k) {
-                const float4* src = reinterpret_cast<const float4*>(wsrow + static_cast<size_t>(k) * kBM * BN + c16 * 16);
+          for (int i = 0; i < 16; ++i) v[i] = 0.0f;
+          for (int k = 0; k < g.ks; ++k) {
+            const float4* src = reinterpret_cast<const float4*>(tile_ws + static_cast<size_t>(k) * kBM * BN +
+                                                                (static_cast<size_t>(c16) * kBM + r) * 16);
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                  const float4 f = __ldcg(src + q);
-                  v[4 * q] += f.x;
-                  v[4 * q + 1] += f.y;
-                  v[4 * q + 2] += f.z;
-                  v[4 * q + 3] += f.w;
-                }
-              }
-              const int co = x.tn * BN + c16 * 16;
-              epilogue_store(p, v, obase + co, co);
+            for (int u = 0; u < 4; ++u) {
+              const float4 f = __ldcg(src + u);
+              v[4 * u] += f.x;
+              v[4 * u + 1] += f.y;
+              v[4 * u + 2] += f.z;
+              v[4 * u + 3] += f.w;
             }
           }
-          if (warp == 2 && lane == 0) p.ws_counters[x.tile_mn] = 0;
+          size_t ob;
+          const int co = x.tn * BN + c16 * 16;
+          if (out_row(p, g, x, r, ob)) {
+            epilogue_store_ld(p, v, ob + co, co);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = 0.0f;
+          }
+          if (p.gap_out) gap_segment(p, g, x, r, lane, v, co);
+        }
+        epi_bar();
+        if (etid == 0) {
+          if (atomicAdd(dep, 1) == g.ks - 1) {
+            *arr = 0;
+            *dep = 0;
+          }
         }
       }
+      if (etid == 0) trace_put(p, unit, 5);
     }
   }
   __syncthreads();
@@ -425,7 +606,7 @@ cudaError_t launch_cfg(const TcConvParams& p, int num_sms, cudaStream_t stream) 
   if (p.mode == 0 && p.ks_max > 1) tiles *= p.ks_max;
   if (tiles <= 0) return cudaSuccess;
   const int grid = tiles < num_sms ? static_cast<int>(tiles) : num_sms;
-  tc_conv_kernel<BN, X3><<<grid, 192, Cfg::kSmem, stream>>>(p);
+  tc_conv_kernel<BN, X3><<<grid, kThreads, Cfg::kSmem, stream>>>(p);
   return cudaGetLastError();
 }
 

@@ -14,9 +14,14 @@
 // (fp32-class, ~2^-16 relative per product) — the parity tier.
 //
 // Split-K (mode 0, ks_max > 1): the split factor is chosen ON DEVICE from the
-// surviving-request count so the grid stays full as requests exit; partial
-// tiles go to an fp32 workspace and the last CTA of each tile (atomic
-// counter) sums them in a fixed order and runs the epilogue (deterministic).
+// surviving-request count so the grid stays full as requests exit
+// (ks = floor(grid / tiles), so every split unit runs in the single resident
+// wave). Partial tiles go to an fp32 workspace; the ks CTAs of a tile meet at
+// a per-tile arrival counter and each reduces 1/ks of the tile in a fixed k
+// order before running the epilogue on it (deterministic, parallel). The
+// wait requires all CTAs of a launch to be co-resident: one CTA per SM,
+// grid <= SM count, and launches on one device must not run concurrently
+// (the engine uses one stream per device).
 #pragma once
 
 #include <cstdint>
@@ -57,6 +62,9 @@ struct TcConvParams {
   __nv_bfloat16* out_hi;
   __nv_bfloat16* out_lo;
   float* out_f32;
+  float* gap_out;      // nullable: fused GAP partials [image][gap_segs][Cout] (NHWC conv mode only)
+  int gap_segs;        // segments per image = tiles_h * tiles_w * max(1, hb*wb/32)
+  unsigned long long* trace;  // nullable debug: clock64 stamps [8 CTAs][32 units][8]
   signed char tap_phase[kMaxTaps];
   signed char tap_dh[kMaxTaps];
   signed char tap_dw[kMaxTaps];
@@ -67,6 +75,10 @@ bool encode_act_map(CUtensorMap* map, const void* base, int C, int W, int H, int
                     int stride = 1);
 bool encode_weight_map(CUtensorMap* map, const void* base, int K, int Cout, int BN);
 int tc_conv_pick_bn(int Cout, int segs = 1);
+// Segments per image of the fused GAP partials for a conv tile geometry.
+inline int tc_conv_gap_segs(int tiles_h, int tiles_w, int hb, int wb) {
+  return tiles_h * tiles_w * (hb * wb > 32 ? hb * wb / 32 : 1);
+}
 // Upper bound on the tile count at count_static (used to size the grid).
 int tc_conv_max_tiles(const TcConvParams& p, int BN);
 // Workspace floats needed for mode-0 split-K with `max_ctas` CTAs.

@@ -374,6 +374,165 @@ static void perf_test(int M, int K, int Cout) {
   cudaFree(dOut);
 }
 
+// Same box rule as the engine (engine.cpp choose_box).
+static void choose_box(int Ho, int Wo, int& hb, int& wb, int& ipt) {
+  int w2 = 1;
+  while (w2 < Wo) w2 <<= 1;
+  int h2 = 1;
+  while (h2 < Ho) h2 <<= 1;
+  if (w2 > 128) w2 = 128;
+  if (h2 * w2 <= 128) {
+    hb = h2;
+    wb = w2;
+    while (hb * wb < 8) wb <<= 1;
+    ipt = 128 / (hb * wb);
+  } else {
+    wb = w2;
+    hb = 128 / wb;
+    ipt = 1;
+  }
+}
+
+// Timing of one conv layer shape (no CPU check): `nsurv` of N images survive.
+static void perf_conv(const char* name, int N, int nsurv, int H, int W, int C, int Cout, int k, int stride, bool x3,
+                      bool use_res, int ks_max, bool trace) {
+  const int pad = k / 2;
+  const int Ho = (H + 2 * pad - k) / stride + 1, Wo = (W + 2 * pad - k) / stride + 1;
+  const size_t xn = (size_t)N * H * W * C, wn = (size_t)Cout * k * k * C, on = (size_t)N * Ho * Wo * Cout;
+  __nv_bfloat16 *a_hi, *a_lo, *w_hi, *w_lo, *o_hi, *o_lo, *r_hi, *r_lo;
+  CK(cudaMalloc(&a_hi, xn * 2));
+  CK(cudaMalloc(&a_lo, xn * 2));
+  CK(cudaMalloc(&w_hi, wn * 2));
+  CK(cudaMalloc(&w_lo, wn * 2));
+  CK(cudaMalloc(&o_hi, on * 2));
+  CK(cudaMalloc(&o_lo, on * 2));
+  CK(cudaMalloc(&r_hi, on * 2));
+  CK(cudaMalloc(&r_lo, on * 2));
+  CK(cudaMemset(a_hi, 0, xn * 2));
+  CK(cudaMemset(a_lo, 0, xn * 2));
+  CK(cudaMemset(w_hi, 0, wn * 2));
+  CK(cudaMemset(w_lo, 0, wn * 2));
+  CK(cudaMemset(r_hi, 0, on * 2));
+  CK(cudaMemset(r_lo, 0, on * 2));
+  std::vector<float> sc(Cout, 1.0f), sh(Cout, 0.0f);
+  float* dScale = dev_copy(sc);
+  float* dShift = dev_copy(sh);
+  std::vector<int> surv;
+  for (int i = 0; i < nsurv; ++i) surv.push_back((int)((long long)i * N / nsurv));
+  int* dSurv = dev_copy(surv);
+  std::vector<int> cnt = {nsurv};
+  int* dCnt = dev_copy(cnt);
+  float* dWs;
+  int* dCtr;
+  CK(cudaMalloc(&dWs, tc_conv_ws_floats(256, g_sms) * 4));
+  CK(cudaMalloc(&dCtr, 4 * g_sms * 4));
+  CK(cudaMemset(dCtr, 0, 4 * g_sms * 4));
+  unsigned long long* dTrace;
+  CK(cudaMalloc(&dTrace, 8 * 32 * 8 * 8));
+  CK(cudaMemset(dTrace, 0, 8 * 32 * 8 * 8));
+  TcConvParams p;
+  memset(&p, 0, sizeof(p));
+  int hb, wb, ipt;
+  choose_box(Ho, Wo, hb, wb, ipt);
+  p.plain = 0;
+  p.Ho = Ho;
+  p.Wo = Wo;
+  p.hb = hb;
+  p.wb = wb;
+  p.ipt = ipt;
+  p.tiles_h = (Ho + hb - 1) / hb;
+  p.tiles_w = (Wo + wb - 1) / wb;
+  p.conv_stride = stride;
+  p.C = C;
+  p.ntaps = k * k;
+  p.segs = x3 ? 3 : 1;
+  p.Cout = Cout;
+  p.ksplit = 1;
+  p.ks_max = ks_max;
+  p.ws = dWs;
+  p.ws_counters = dCtr;
+  p.surv = dSurv;
+  p.count = dCnt;
+  p.count_static = N;
+  p.mode = 0;
+  p.scale = dScale;
+  p.shift = dShift;
+  p.res_hi = use_res ? r_hi : nullptr;
+  p.res_lo = use_res && x3 ? r_lo : nullptr;
+  p.relu = 1;
+  p.out_hi = o_hi;
+  p.out_lo = x3 ? o_lo : nullptr;
+  for (int r = 0; r < k; ++r)
+    for (int s2 = 0; s2 < k; ++s2) {
+      const int t = r * k + s2;
+      p.tap_dh[t] = static_cast<signed char>(r - pad);
+      p.tap_dw[t] = static_cast<signed char>(s2 - pad);
+    }
+  const int BN = tc_conv_pick_bn(Cout, x3 ? 3 : 1);
+  bool ok = encode_act_map(&p.tmA[0], a_hi, C, W, H, N, 1, wb, hb, stride) &&
+            encode_act_map(&p.tmA[1], a_lo, C, W, H, N, 1, wb, hb, stride) &&
+            encode_weight_map(&p.tmB[0], w_hi, k * k * C, Cout, BN) &&
+            encode_weight_map(&p.tmB[1], w_lo, k * k * C, Cout, BN);
+  if (!ok) {
+    printf("%s: encode failed\n", name);
+    return;
+  }
+  for (int i = 0; i < 3; ++i) CK(tc_conv_launch(p, BN, g_sms, 0));
+  CK(cudaDeviceSynchronize());
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int iters = 20;
+  cudaEventRecord(e0);
+  for (int i = 0; i < iters; ++i) tc_conv_launch(p, BN, g_sms, 0);
+  cudaEventRecord(e1);
+  CK(cudaEventSynchronize(e1));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  ms /= iters;
+  const double flops = 2.0 * nsurv * Ho * Wo * Cout * (double)C * k * k;
+  const double tf = flops / (ms * 1e-3) / 1e12;
+  printf("perf %-26s N=%3d/%3d %3dx%-3d C=%4d->%4d k=%d s=%d %s: %8.1f us  %7.1f TFLOP/s alg  (%5.1f%% tensor of 1590)\n",
+         name, nsurv, N, H, W, C, Cout, k, stride, x3 ? "x3 " : "b16", ms * 1e3, tf, 100.0 * tf * (x3 ? 3 : 1) / 1590.0);
+  if (trace) {
+    p.trace = dTrace;
+    CK(tc_conv_launch(p, BN, g_sms, 0));
+    CK(cudaDeviceSynchronize());
+    std::vector<unsigned long long> tr(8 * 32 * 8);
+    CK(cudaMemcpy(tr.data(), dTrace, tr.size() * 8, cudaMemcpyDeviceToHost));
+    for (int cta = 0; cta < 2; ++cta) {
+      const unsigned long long t0 = tr[(cta * 32) * 8 + 0];
+      printf("  trace CTA %d (cycles from first TMA issue): unit: tma0 tmaN | mma0 mmaN | epi0 epiN\n", cta);
+      for (int u = 0; u < 32; ++u) {
+        const unsigned long long* q = &tr[(cta * 32 + u) * 8];
+        if (!q[0] && !q[4]) break;
+        auto rel = [&](unsigned long long v) { return v ? (long long)(v - t0) : -1LL; };
+        printf("   %2d: %8lld %8lld | %8lld %8lld | %8lld %8lld\n", u, rel(q[0]), rel(q[1]), rel(q[2]), rel(q[3]),
+               rel(q[4]), rel(q[5]));
+      }
+    }
+  }
+  cudaFree(a_hi); cudaFree(a_lo); cudaFree(w_hi); cudaFree(w_lo); cudaFree(o_hi); cudaFree(o_lo);
+  cudaFree(r_hi); cudaFree(r_lo); cudaFree(dScale); cudaFree(dShift); cudaFree(dSurv); cudaFree(dCnt);
+  cudaFree(dWs); cudaFree(dCtr); cudaFree(dTrace);
+}
+
+static void perf_layers(bool trace) {
+  // ResNet-18 CIFAR shapes at the survivor counts of a compacted step.
+  perf_conv("r18 b1 conv 64", 256, 256, 32, 32, 64, 64, 3, 1, true, true, 32, trace);
+  perf_conv("r18 b1 conv 64 bf16", 256, 256, 32, 32, 64, 64, 3, 1, false, true, 32, false);
+  perf_conv("r18 b3 conv1 s2", 256, 159, 32, 32, 64, 128, 3, 2, true, false, 32, false);
+  perf_conv("r18 b3 conv2", 256, 159, 16, 16, 128, 128, 3, 1, true, true, 32, false);
+  perf_conv("r18 b5 conv2", 256, 98, 8, 8, 256, 256, 3, 1, true, true, 32, trace);
+  perf_conv("r18 b8 conv2", 256, 16, 4, 4, 512, 512, 3, 1, true, true, 32, trace);
+  perf_conv("r18 b8 conv2 full", 256, 256, 4, 4, 512, 512, 3, 1, true, true, 32, false);
+  // ResNet-50 ImageNet layer1/layer4 shapes (batch 128).
+  perf_conv("r50 l1 1x1 64->64", 128, 128, 56, 56, 64, 64, 1, 1, true, false, 32, false);
+  perf_conv("r50 l1 3x3 64", 128, 128, 56, 56, 64, 64, 3, 1, true, false, 32, trace);
+  perf_conv("r50 l1 1x1 64->256 res", 128, 128, 56, 56, 64, 256, 1, 1, true, true, 32, trace);
+  perf_conv("r50 l4 3x3 512", 128, 15, 7, 7, 512, 512, 3, 1, true, false, 32, false);
+}
+
 int main(int argc, char** argv) {
   cudaDeviceProp prop;
   CK(cudaGetDeviceProperties(&prop, 0));
@@ -401,6 +560,10 @@ int main(int argc, char** argv) {
   conv_test("conv3x3 s1 8x8 bf16 splitK", 9, 8, 8, 256, 256, 3, 1, false, true, true, true, 0, 8);
   conv_test("conv3x3 s1 4x4 x3 splitK again", 19, 4, 4, 128, 512, 3, 1, true, true, true, true, 0, 16);
   conv_test("conv1x1 s2 8->4 bf16 splitK", 6, 8, 8, 256, 512, 1, 2, false, false, false, true, 256, 4);
+  if (argc > 1 && strcmp(argv[1], "--layers") == 0) {
+    perf_layers(argc > 2 && strcmp(argv[2], "--trace") == 0);
+    return 0;
+  }
   if (argc > 1 && strcmp(argv[1], "--perf") == 0) {
     perf_test(8192, 8192, 8192);
     perf_test(16384, 4096, 4096);

@@ -287,6 +287,40 @@ def test_resnet18_cifar_serve_vs_oracle(shadow):
     assert len(set(exit_o.tolist())) >= 3  # exits spread over several layers
 
 
+def test_fused_gap_matches_unfused_pool(monkeypatch):
+    """Pool(C) caches read GAP partials written by the tap conv's epilogue;
+    the unfused path (LCB_NO_GAP_FUSION=1) pools the stored tap instead. Both
+    must agree on every decision and to fp32 rounding on the probabilities."""
+    m, vs = _cnn_deployment("resnet18_cifar", 10, 21, 64)
+    x = image_inputs(32, 3, 32, 32, seed=8)
+    fused = lcb.Deployment(m, vs, precision="bf16x3", max_batch=32)
+    monkeypatch.setenv("LCB_NO_GAP_FUSION", "1")
+    plain = lcb.Deployment(m, vs, precision="bf16x3", max_batch=32)
+    for shadow in (True, False):
+        a, b = fused.serve(x, shadow=shadow), plain.serve(x, shadow=shadow)
+        assert np.array_equal(a.exit_layer, b.exit_layer) and np.array_equal(a.served, b.served)
+        both = ~np.isnan(a.probs) & ~np.isnan(b.probs)
+        assert np.array_equal(np.isnan(a.probs), np.isnan(b.probs))
+        assert np.all(np.abs(a.probs[both] - b.probs[both]) <= 1e-5)
+    fused.close()
+    plain.close()
+
+
+def test_resnet50_serve_vs_oracle():
+    """ImageNet shape (224x224, 1000 classes, 16 bottleneck blocks): stem,
+    max-pool, 1x1/3x3/strided convs, fused GAP partials, split-K deep layers
+    and the batched 1000-class logits GEMM, against the fp64 restatement."""
+    m, vs = _cnn_deployment("resnet50", 1000, 31, 8, full_fraction=0.3)
+    x = image_inputs(6, 3, 224, 224, seed=12)
+    dep = lcb.Deployment(m, vs, precision="bf16x3", max_batch=8)
+    exit_o, served_o, base_o, probs_o, gaps, _, _ = _oracle_cnn(m, vs, x, threads=os.cpu_count() or 8)
+    deltas = {v.layer: v.delta for v in vs}
+    for shadow in (True, False):
+        res = dep.serve(x, shadow=shadow)
+        compare_serve(res, exit_o, served_o, base_o, probs_o, deltas, shadow, label_gap=gaps)
+    dep.close()
+
+
 def test_resnet18_cnn_lookups_on_oracle_taps():
     """Cache heads of every family on real CNN taps (NCHW-flat from the fp64
     oracle), through the engine's lookup entry point."""
