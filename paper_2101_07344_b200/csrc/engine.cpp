@@ -183,6 +183,10 @@ Engine::Engine(int device, const BaseModel& model, std::vector<CacheVariant> var
   }
   const char* nf = std::getenv("LCB_NO_GAP_FUSION");
   gap_fusion_ = !(nf && nf[0] == '1');
+  const char* nr = std::getenv("LCB_NO_MMA_RESIDUAL");
+  mma_residual_ = !(nr && nr[0] == '1');
+  const char* nt = std::getenv("LCB_NO_TMA_STORE");
+  tma_store_ = !(nt && nt[0] == '1');
   build_weights();
   ck(cudaStreamSynchronize(stream_), "build");
 }
@@ -248,30 +252,50 @@ void Engine::build_weights() {
     head_w_ = upload_f32(to_f32(hw.w));
     head_b_ = upload_f32(to_f32(hw.b));
   } else {
+    {
+      std::vector<__nv_bfloat16> eye(256 * 256, __float2bfloat16_rn(0.0f));
+      for (int i = 0; i < 256; ++i) eye[static_cast<size_t>(i) * 256 + i] = __float2bfloat16_rn(1.0f);
+      identity_ = static_cast<__nv_bfloat16*>(dalloc(eye.size() * 2));
+      ck(cudaMemcpy(identity_, eye.data(), eye.size() * 2, cudaMemcpyHostToDevice), "identity upload");
+    }
     cnn_w_.resize(model_.ops.size());
     std::vector<long long> slot_elems(static_cast<size_t>(model_.nslots), 0);
     long long im2col_elems = 0;
     for (size_t i = 0; i < model_.ops.size(); ++i) {
       const CnnOp& o = model_.ops[i];
-      if (o.kind == CnnOpKind::Stem || o.kind == CnnOpKind::Conv) {
+      if (o.kind == CnnOpKind::Stem) {
+        require(o.Cout == 64 && (o.stride == 1 || o.stride == 2) && o.C * o.stride * o.stride <= 16,
+                "engine: stem must be C_in*stride^2 <= 16 -> 64 channels, stride 1 or 2");
+        DevConv dc;
+        const StemGeom g = stem_geom(o.H, o.W, o.k, o.stride, o.pad);
+        std::vector<float> w(static_cast<size_t>(g.kk) * g.kk * 2 * 64 * 8);
+        stem_weights(o.w.data(), o.Cout, o.C, o.k, o.stride, g, w.data());
+        dc.w = upload_planes(w);
+        dc.scale = upload_f32(to_f32(o.scale));
+        dc.shift = upload_f32(to_f32(o.shift));
+        cnn_w_[i] = dc;
+        slot_elems[static_cast<size_t>(o.out)] = static_cast<long long>(B) * o.Ho() * o.Wo() * o.Cout;
+        im2col_elems = std::max(im2col_elems, static_cast<long long>(B) * 2 * g.Hx * g.Wx * 8);
+      } else if (o.kind == CnnOpKind::Conv) {
         DevConv dc;
         const int K = o.k * o.k * o.C;
-        dc.Kp = o.kind == CnnOpKind::Stem ? round_up(K, 64) : K;
-        require(o.kind == CnnOpKind::Stem || o.C % 64 == 0, "engine: conv input channels must be a multiple of 64");
+        dc.Kp = K;
+        require(o.C % 64 == 0, "engine: conv input channels must be a multiple of 64");
+        // folded batch-norm scale goes into the weights (W * scale), so the
+        // epilogue only adds the shift (and a residual add can ride the MMA)
         std::vector<float> w(static_cast<size_t>(o.Cout) * dc.Kp, 0.0f);
         for (int co = 0; co < o.Cout; ++co)
           for (int c = 0; c < o.C; ++c)
             for (int r = 0; r < o.k; ++r)
               for (int s = 0; s < o.k; ++s)
                 w[static_cast<size_t>(co) * dc.Kp + (r * o.k + s) * o.C + c] =
-                    static_cast<float>(o.w[((static_cast<size_t>(co) * o.C + c) * o.k + r) * o.k + s]);
+                    static_cast<float>(o.w[((static_cast<size_t>(co) * o.C + c) * o.k + r) * o.k + s] *
+                                       o.scale[static_cast<size_t>(co)]);
         dc.w = upload_planes(w);
-        dc.scale = upload_f32(to_f32(o.scale));
+        dc.scale = nullptr;
         dc.shift = upload_f32(to_f32(o.shift));
         cnn_w_[i] = dc;
         slot_elems[static_cast<size_t>(o.out)] = static_cast<long long>(B) * o.Ho() * o.Wo() * o.Cout;
-        if (o.kind == CnnOpKind::Stem)
-          im2col_elems = std::max(im2col_elems, static_cast<long long>(B) * o.Ho() * o.Wo() * dc.Kp);
       } else if (o.kind == CnnOpKind::MaxPool) {
         slot_elems[static_cast<size_t>(o.out)] = static_cast<long long>(B) * o.Ho() * o.Wo() * o.C;
       } else if (o.kind == CnnOpKind::Head) {
@@ -560,6 +584,9 @@ void Engine::build_mlp_steps(std::vector<Step>& steps, bool shadow) {
     prm->relu = 1;
     prm->out_hi = act.hi;
     prm->out_lo = act.lo;
+    if (tma_store_)
+      prm->tma_store = encode_out_map_2d(&prm->tmO[0], act.hi, f.outp, B) &&
+                       (!x3 || encode_out_map_2d(&prm->tmO[1], act.lo, f.outp, B));
     const int sms = num_sms_;
     steps.push_back({[prm, BN, sms](cudaStream_t s) { ck(tc_conv_launch(*prm, BN, sms, s), "tc_conv (mlp)"); }, 1, 1,
                      static_cast<int>(cur_count - d_counts_), 2.0 * f.in * f.out,
@@ -636,48 +663,36 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow) {
   for (size_t i = 0; i < model_.ops.size(); ++i) {
     const CnnOp& o = model_.ops[i];
     if (o.kind == CnnOpKind::Stem) {
+      // Space-to-depth rewrite of the images, then the slab-fed tcgen05 stem.
       const DevConv& dc = cnn_w_[i];
-      Planes col = im2col_buf_;
+      Planes X = im2col_buf_;
       Planes out = slot_buf_[static_cast<size_t>(o.out)];
-      const int Ho = o.Ho(), Wo = o.Wo();
-      steps.push_back({[this, o, Ho, Wo, dc, col, counts, B](cudaStream_t s) {
-                         launch_stem_im2col(d_x_, counts, B, o.C, o.H, o.W, o.k, o.stride, o.pad, Ho, Wo, dc.Kp, col.hi,
-                                            col.lo, s);
+      const StemGeom g = stem_geom(o.H, o.W, o.k, o.stride, o.pad);
+      steps.push_back({[this, o, g, X, counts, B](cudaStream_t s) {
+                         launch_stem_s2d(d_x_, counts, B, o.C, o.H, o.W, o.stride, o.pad, g, X.hi, X.lo, s);
                        },
                        0});
-      auto prm = std::make_shared<TcConvParams>();
-      std::memset(prm.get(), 0, sizeof(TcConvParams));
-      const int rows = B * Ho * Wo;
-      const int BN = tc_conv_pick_bn(o.Cout, x3 ? 3 : 1);
-      bool ok = encode_act_map(&prm->tmA[0], col.hi, dc.Kp, rows, 1, 1, 1, 128, 1) &&
-                encode_weight_map(&prm->tmB[0], dc.w.hi, dc.Kp, o.Cout, BN);
-      if (x3)
-        ok = ok && encode_act_map(&prm->tmA[1], col.lo, dc.Kp, rows, 1, 1, 1, 128, 1) &&
-             encode_weight_map(&prm->tmB[1], dc.w.lo, dc.Kp, o.Cout, BN);
-      if (!ok) throw CudaFailure("engine: TMA descriptor encode failed (stem)");
-      prm->plain = 1;
-      prm->Ho = 1;
-      prm->Wo = rows;
-      prm->hb = 1;
-      prm->wb = 128;
-      prm->ipt = 1;
-      prm->tiles_h = 1;
-      prm->C = dc.Kp;
-      prm->ntaps = 1;
-      prm->segs = x3 ? 3 : 1;
-      prm->Cout = o.Cout;
-      prm->ksplit = 1;
-      prm->count = stem_rows;
-      prm->count_static = rows;
-      prm->mode = 0;
-      prm->scale = dc.scale;
-      prm->shift = dc.shift;
-      prm->relu = o.relu ? 1 : 0;
-      prm->out_hi = out.hi;
-      prm->out_lo = out.lo;
-      steps.push_back({[prm, BN, sms](cudaStream_t s) { ck(tc_conv_launch(*prm, BN, sms, s), "tc_conv (stem)"); }, 1,
-                       1, 0, 2.0 * Ho * Wo * o.Cout * o.k * o.k * o.C,
-                       (x3 ? 4.0 : 2.0) * Ho * Wo * (static_cast<double>(dc.Kp) + o.Cout)});
+      StemParams sp{};
+      sp.x_hi = X.hi;
+      sp.x_lo = x3 ? X.lo : nullptr;
+      sp.w_hi = dc.w.hi;
+      sp.w_lo = x3 ? dc.w.lo : nullptr;
+      sp.Hx = g.Hx;
+      sp.Wx = g.Wx;
+      sp.Ho = g.Ho;
+      sp.Wo = g.Wo;
+      sp.kk = g.kk;
+      sp.tiles_per_img = (g.Ho * g.Wx + 127) / 128;
+      sp.count = counts;
+      sp.count_static = B;
+      sp.scale = dc.scale;
+      sp.shift = dc.shift;
+      sp.relu = o.relu ? 1 : 0;
+      sp.out_hi = out.hi;
+      sp.out_lo = x3 ? out.lo : nullptr;
+      steps.push_back({[sp, sms](cudaStream_t s) { ck(tc_stem_launch(sp, sms, s), "tc_stem"); }, 1, 1, 0,
+                       2.0 * g.Ho * g.Wo * o.Cout * o.k * o.k * o.C,
+                       (x3 ? 4.0 : 2.0) * (32.0 * g.Hx * g.Wx / 2.0 + static_cast<double>(g.Ho) * g.Wo * o.Cout)});
     } else if (o.kind == CnnOpKind::MaxPool) {
       Planes in = slot_buf_[static_cast<size_t>(o.in)], out = slot_buf_[static_cast<size_t>(o.out)];
       const int Ho = o.Ho(), Wo = o.Wo();
@@ -727,12 +742,28 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow) {
       prm->scale = dc.scale;
       prm->shift = dc.shift;
       if (o.res >= 0) {
-        prm->res_hi = slot_buf_[static_cast<size_t>(o.res)].hi;
-        prm->res_lo = slot_buf_[static_cast<size_t>(o.res)].lo;
+        const Planes& rb = slot_buf_[static_cast<size_t>(o.res)];
+        if (mma_residual_) {
+          // residual add on the tensor core: BN/64 extra K-steps (residual x identity)
+          bool rok = encode_act_map(&prm->tmR[0], rb.hi, o.Cout, Wo, Ho, B, 1, wb, hb, 1) &&
+                     (!x3 || encode_act_map(&prm->tmR[1], rb.lo, o.Cout, Wo, Ho, B, 1, wb, hb, 1)) &&
+                     encode_weight_map(&prm->tmE, identity_, 256, 256, BN);
+          if (!rok) throw CudaFailure("engine: TMA descriptor encode failed (residual)");
+          prm->nres = BN / 64;
+        } else {
+          prm->res_hi = rb.hi;
+          prm->res_lo = rb.lo;
+        }
       }
       prm->relu = o.relu ? 1 : 0;
       prm->out_hi = out.hi;
       prm->out_lo = out.lo;
+      if (tma_store_) {
+        int bw, bh;
+        tc_conv_store_box(hb, wb, bw, bh);
+        prm->tma_store = encode_out_map(&prm->tmO[0], out.hi, o.Cout, Wo, Ho, B, bw, bh) &&
+                         (!x3 || encode_out_map(&prm->tmO[1], out.lo, o.Cout, Wo, Ho, B, bw, bh));
+      }
       if (o.tap >= 0 && gap_fusion_) {
         // Pool(C) cache on this conv's output: GAP partials from the epilogue.
         const int ci = cache_of_layer_[static_cast<size_t>(o.tap + 1)];

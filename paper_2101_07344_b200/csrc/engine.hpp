@@ -16,6 +16,7 @@
 #include "host/lcb_host.hpp"
 #include "kernels/serve_kernels.cuh"
 #include "kernels/tc_conv.cuh"
+#include "kernels/tc_stem.cuh"
 
 namespace lcb {
 
@@ -155,6 +156,9 @@ class Engine {
   float* ws_ = nullptr;        // split-K workspace shared by all contractions (stream-ordered)
   int* ws_counters_ = nullptr;
   bool gap_fusion_ = true;  // LCB_NO_GAP_FUSION=1 disables the fused Pool(C) partials
+  bool tma_store_ = true;
+  bool mma_residual_ = true;  // LCB_NO_MMA_RESIDUAL=1: residual added in the epilogue instead of by identity K-steps
+  __nv_bfloat16* identity_ = nullptr;   // LCB_NO_TMA_STORE=1: direct st.global epilogue instead of TMA stores
   Planes im2col_buf_;
 
   std::vector<Step> steps_compact_, steps_shadow_;

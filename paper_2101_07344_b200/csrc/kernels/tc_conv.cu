@@ -22,9 +22,10 @@ struct TcCfg {
   static constexpr int kPlanes = X3 ? 2 : 1;
   static constexpr int kBBytes = BN * 128;
   static constexpr int kStageBytes = kPlanes * (kABytes + kBBytes);
-  static constexpr int kStagesRaw = (200 * 1024) / kStageBytes;
+  static constexpr int kStagesRaw = (192 * 1024) / kStageBytes;
   static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
-  static constexpr int kSmem = kStages * kStageBytes + 1024 /*bars*/ + 1024 /*align*/;
+  static constexpr int kEpiStage = 8 * 4096;  // per epilogue warp: 32 rows x 64 B x 2 planes (TMA store staging)
+  static constexpr int kSmem = kStages * kStageBytes + kEpiStage + 1024 /*bars*/ + 1024 /*align*/;
   static constexpr uint32_t kTmemCols = 2 * BN;
   static_assert(kStages >= 2, "pipeline needs at least two stages");
 };
@@ -46,7 +47,7 @@ __device__ __forceinline__ TileGeom tile_geom(const TcConvParams& p, int BN) {
   g.tiles_img = p.tiles_h * g.tiles_w;
   g.tiles_n = p.Cout / BN;
   g.tiles_mn = g.n_groups * g.tiles_img * g.tiles_n;
-  g.nk = p.ntaps * (p.C / 64);
+  g.nk = p.ntaps * (p.C / 64) + p.nres;
   if (p.mode == 1) {
     g.ks = p.ksplit;
   } else if (p.ks_max > 1 && g.tiles_mn > 0) {
@@ -131,8 +132,8 @@ __device__ __forceinline__ bool out_row(const TcConvParams& p, const TileGeom& g
 
 // scale/shift, residual (prefetched 16-byte chunks), ReLU, hi/lo split and
 // NHWC store of 16 channels.
-__device__ __forceinline__ void epilogue_store(const TcConvParams& p, float (&v)[16], size_t off, int co,
-                                               const uint4* rh, const uint4* rl) {
+__device__ __forceinline__ void epilogue_math(const TcConvParams& p, float (&v)[16], int co, const uint4* rh,
+                                              const uint4* rl) {
   if (p.scale) {
     const float4* sc = reinterpret_cast<const float4*>(p.scale + co);
 #pragma unroll
@@ -183,6 +184,23 @@ __device__ __forceinline__ void epilogue_store(const TcConvParams& p, float (&v)
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = v[i] > 0.0f ? v[i] : 0.0f;
   }
+}
+
+__device__ __forceinline__ void split16(const float (&v)[16], uint4 (&hi)[2], uint4 (&lo)[2]) {
+  __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(hi);
+  __nv_bfloat162* l2 = reinterpret_cast<__nv_bfloat162*>(lo);
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const __nv_bfloat162 hh = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+    h2[e] = hh;
+    const float2 hf = __bfloat1622float2(hh);
+    l2[e] = __floats2bfloat162_rn(v[2 * e] - hf.x, v[2 * e + 1] - hf.y);
+  }
+}
+
+__device__ __forceinline__ void epilogue_store(const TcConvParams& p, float (&v)[16], size_t off, int co,
+                                               const uint4* rh, const uint4* rl) {
+  epilogue_math(p, v, co, rh, rl);
   uint4 hi[2], lo[2];
   __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(hi);
   __nv_bfloat162* l2 = reinterpret_cast<__nv_bfloat162*>(lo);
@@ -299,12 +317,14 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   // stage s: [A_hi][A_lo?][B_hi][B_lo?]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes + Cfg::kEpiStage);
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
   const uint32_t full0 = smem_u32(bars);
   const uint32_t empty0 = smem_u32(bars + S);
   const uint32_t tfull0 = smem_u32(bars + 2 * S);
   const uint32_t tempty0 = smem_u32(bars + 2 * S + 2);
+  // per epilogue warp TMA-store staging (after the pipeline stages; bars follow)
+  uint8_t* epi_stage = smem + S * Cfg::kStageBytes;
   auto stage_a = [&](int s, int plane) { return smem + s * Cfg::kStageBytes + plane * kABytes; };
   auto stage_b = [&](int s, int plane) {
     return smem + s * Cfg::kStageBytes + Cfg::kPlanes * kABytes + plane * Cfg::kBBytes;
@@ -328,6 +348,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
     if (X3) {
       tma_prefetch_desc(&p.tmA[1]);
       tma_prefetch_desc(&p.tmB[1]);
+    }
+    if (p.nres) {
+      tma_prefetch_desc(&p.tmR[0]);
+      if (X3) tma_prefetch_desc(&p.tmR[1]);
+      tma_prefetch_desc(&p.tmE);
     }
   }
   if (warp == 0) tmem_alloc(smem_u32(tmem_holder), Cfg::kTmemCols);
@@ -361,17 +386,31 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
             imgs[j] = image_of(p, idx);
           }
         }
+        const int nk_conv = p.ntaps * cchunks;
         int cc = x.s_begin % cchunks, tap = x.s_begin / cchunks;
         for (int s = x.s_begin; s < x.s_end; ++s) {
           mbar_wait(empty0 + 8 * stage, phase ^ 1);
           const uint32_t fb = full0 + 8 * stage;
           mbar_expect_tx(fb, Cfg::kStageBytes);
+          if (s >= nk_conv) {
+            // residual K-step: A = residual channels [tn*BN + j*64, +64) at the
+            // output pixels, B = identity slice (the residual add on the tensor core)
+            const int j = s - nk_conv;
+#pragma unroll 1
+            for (int pl = 0; pl < Cfg::kPlanes; ++pl) {
+              const uint32_t a_dst = smem_u32(stage_a(stage, pl));
+              for (int jj = 0; jj < ipt; ++jj)
+                tma_load_5d(a_dst + jj * box_bytes, &p.tmR[pl], fb, x.tn * BN + j * 64, x.w0, x.h0, imgs[jj], 0);
+              tma_load_2d(smem_u32(stage_b(stage, pl)), &p.tmE, fb, j * 64, 0);
+            }
+          } else {
           const int wc = x.w0 * cs + p.tap_dw[tap], hc = x.h0 * cs + p.tap_dh[tap], ph = p.tap_phase[tap];
 #pragma unroll 1
           for (int pl = 0; pl < Cfg::kPlanes; ++pl) {
             const uint32_t a_dst = smem_u32(stage_a(stage, pl));
             for (int j = 0; j < ipt; ++j) tma_load_5d(a_dst + j * box_bytes, &p.tmA[pl], fb, cc * 64, wc, hc, imgs[j], ph);
             tma_load_2d(smem_u32(stage_b(stage, pl)), &p.tmB[pl], fb, tap * p.C + cc * 64, x.tn * BN);
+          }
           }
           if (++cc == cchunks) {
             cc = 0;
@@ -400,17 +439,20 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
         tc_fence_after();
         trace_put(p, unit, 2);
         const uint32_t d_tmem = tmem_base + acc * BN;
+        const int nk_conv = p.ntaps * (p.C / 64);
         for (int s = x.s_begin; s < x.s_end; ++s) {
           mbar_wait(full0 + 8 * stage, phase);
           tc_fence_after();
           const uint32_t ah = smem_u32(stage_a(stage, 0)), bh = smem_u32(stage_b(stage, 0));
+          const bool res_step = s >= nk_conv;
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const uint32_t first = (s > x.s_begin || k > 0) ? 1u : 0u;
             umma_bf16(d_tmem, umma_desc_sw128(ah + 32 * k), umma_desc_sw128(bh + 32 * k), idesc, first);
             if (X3) {
               const uint32_t al = smem_u32(stage_a(stage, 1)), bl = smem_u32(stage_b(stage, 1));
-              umma_bf16(d_tmem, umma_desc_sw128(ah + 32 * k), umma_desc_sw128(bl + 32 * k), idesc, 1u);
+              if (!res_step)  // identity has no lo plane
+                umma_bf16(d_tmem, umma_desc_sw128(ah + 32 * k), umma_desc_sw128(bl + 32 * k), idesc, 1u);
               umma_bf16(d_tmem, umma_desc_sw128(al + 32 * k), umma_desc_sw128(bh + 32 * k), idesc, 1u);
             }
           }
@@ -435,6 +477,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
     const int row = quad * 32 + lane;
     const int etid = threadIdx.x - 64;  // 0..255
     const int col0 = half * kCols;
+    const uint32_t wstage = smem_u32(epi_stage + (warp - 2) * 4096);
+    uint32_t tslot = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     int unit = 0;
@@ -444,6 +488,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
       const bool valid = out_row(p, g, x, row, obase);
       const int grow = x.w0 + row;
       const bool split = p.mode == 0 && g.ks > 1;
+      const bool tstore = p.tma_store && p.mode == 0 && !split;
       // Residual of this row's columns, fetched before the accumulator is
       // ready so its latency overlaps the tile's MMAs.
       uint4 rh[kChunks], rl[X3 ? kChunks : 1];
@@ -493,6 +538,14 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
               for (int q = 0; q < 4; ++q)
                 dst[q] = make_float4(v[u][4 * q], v[u][4 * q + 1], v[u][4 * q + 2], v[u][4 * q + 3]);
             }
+          } else if (tstore) {
+            const int ci = (c32 * 2 + u) * 2;
+            epilogue_math(p, v[u], co, use_res ? &rh[ci] : nullptr,
+                          (use_res && X3 && p.res_lo) ? &rl[X3 ? ci : 0] : nullptr);
+            if (!valid) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) v[u][i] = 0.0f;
+            }
           } else {
             if (valid) {
               const int ci = (c32 * 2 + u) * 2;  // residual chunk index within this warp's columns
@@ -503,6 +556,57 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
               for (int i = 0; i < 16; ++i) v[u][i] = 0.0f;
             }
             if (p.gap_out) gap_segment(p, g, x, row, lane, v[u], co);  // warp-uniform call
+          }
+        }
+        if (tstore) {
+          // this warp's 32 rows x 32 columns, one plane at a time through two
+          // 2 KB staging slots (64-byte swizzle) -> TMA stores (bulk groups);
+          // a slot is rewritten once its previous store has been read.
+#pragma unroll
+          for (int pl = 0; pl < (X3 ? 2 : 1); ++pl) {
+            if (pl == 1 && !p.out_lo) break;
+            const uint32_t slot = wstage + (tslot & 1) * 2048;
+            ++tslot;
+            if (lane == 0) bulk_wait_read1();
+            __syncwarp();
+#pragma unroll
+            for (int u = 0; u < kSub; ++u) {
+              uint4 hi[2], lo[2];
+              split16(v[u], hi, lo);
+#pragma unroll
+              for (int hq = 0; hq < 2; ++hq) {
+                const uint32_t off = static_cast<uint32_t>(lane * 64 + (((u * 2 + hq) ^ ((lane >> 1) & 3)) * 16));
+                st_shared_v4(slot + off, pl == 0 ? hi[hq] : lo[hq]);
+              }
+            }
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              const int c0 = x.tn * BN + col0 + c32 * 32;
+              const int row0 = quad * 32;
+              const CUtensorMap* om = &p.tmO[pl];
+              if (p.plain) {
+                tma_store_2d(om, slot, c0, x.w0 + row0);
+              } else {
+                const int rpi = p.hb * p.wb;
+                const int nimg = rpi >= 32 ? 1 : 32 / rpi;
+                for (int jj = 0; jj < nimg; ++jj) {
+                  const int r0 = row0 + jj * (rpi >= 32 ? 0 : rpi);
+                  const int idx = x.grp * p.ipt + r0 / rpi;
+                  if (idx >= g.count) continue;
+                  const int n = p.surv ? p.surv[idx] : idx;
+                  const int pix = r0 % rpi;
+                  tma_store_5d(om, slot + static_cast<uint32_t>((r0 - row0) * 64), c0, x.w0 + pix % p.wb,
+                               x.h0 + pix / p.wb, n, 0);
+                }
+              }
+              bulk_commit();
+            }
+          }
+          if (p.gap_out) {
+#pragma unroll
+            for (int u = 0; u < kSub; ++u)
+              gap_segment(p, g, x, row, lane, v[u], x.tn * BN + col0 + c32 * 32 + u * 16);  // after staging: destroys v
           }
         }
       }
@@ -567,6 +671,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
       }
       if (etid == 0) trace_put(p, unit, 5);
     }
+    if (lane == 0) bulk_wait0();
   }
   __syncthreads();
   if (warp == 0) {
@@ -643,6 +748,52 @@ bool encode_weight_map(CUtensorMap* map, const void* base, int K, int Cout, int 
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
+}
+
+bool encode_out_map(CUtensorMap* map, const void* base, int Cout, int Wo, int Ho, int N, int bw, int bh) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[5] = {static_cast<cuuint64_t>(Cout), static_cast<cuuint64_t>(Wo), static_cast<cuuint64_t>(Ho),
+                        static_cast<cuuint64_t>(N), 1};
+  cuuint64_t strides[4];
+  strides[0] = static_cast<cuuint64_t>(Cout) * 2;
+  strides[1] = strides[0] * Wo;
+  strides[2] = strides[1] * Ho;
+  strides[3] = strides[2] * N;
+  cuuint32_t box[5] = {32, static_cast<cuuint32_t>(bw), static_cast<cuuint32_t>(bh), 1, 1};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+bool encode_out_map_2d(CUtensorMap* map, const void* base, int Cout, int rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(Cout), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(Cout) * 2};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+void tc_conv_store_box(int hb, int wb, int& bw, int& bh) {
+  // the 32 consecutive tile rows of one epilogue warp as a (w, h) box of one image
+  const int rpi = hb * wb;
+  if (rpi <= 32) {
+    bw = wb;
+    bh = hb;
+  } else if (wb >= 32) {
+    bw = 32;
+    bh = 1;
+  } else {
+    bw = wb;
+    bh = 32 / wb;
+  }
 }
 
 int tc_conv_pick_bn(int Cout, int segs) {

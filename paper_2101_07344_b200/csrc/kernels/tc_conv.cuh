@@ -36,6 +36,11 @@ constexpr int kMaxTaps = 64;
 struct TcConvParams {
   CUtensorMap tmA[2];  // activation planes hi, lo (5-D: C, W, H, N, P)
   CUtensorMap tmB[2];  // weight planes hi, lo (2-D: K, Cout)
+  CUtensorMap tmO[2];  // output planes for TMA stores (tma_store = 1): 5-D NHWC or 2-D rows, box 32 channels
+  CUtensorMap tmR[2];  // residual planes as an A operand (nres > 0): 5-D NHWC at the output resolution
+  CUtensorMap tmE;     // identity matrix [256][256] bf16 as the B operand of the residual K-steps
+  int nres;            // residual K-steps per tile (BN/64): out = conv + residual computed by the MMA
+  int tma_store;       // 1: epilogue stages tiles in shared memory and TMA-stores them (mode 0, no split)
   int plain;           // 1: plain GEMM over rows (A = [rows, K], count = rows)
   int Ho, Wo;          // output spatial dims
   int hb, wb, ipt;     // output tile geometry: ipt images x hb x wb = 128 rows
@@ -75,6 +80,11 @@ bool encode_act_map(CUtensorMap* map, const void* base, int C, int W, int H, int
                     int stride = 1);
 bool encode_weight_map(CUtensorMap* map, const void* base, int K, int Cout, int BN);
 int tc_conv_pick_bn(int Cout, int segs = 1);
+// Output maps for the TMA-store epilogue (64-byte swizzle, 32-channel boxes).
+bool encode_out_map(CUtensorMap* map, const void* base, int Cout, int Wo, int Ho, int N, int bw, int bh);
+bool encode_out_map_2d(CUtensorMap* map, const void* base, int Cout, int rows);
+// (w, h) box of one epilogue warp's 32 tile rows for a tile box hb x wb.
+void tc_conv_store_box(int hb, int wb, int& bw, int& bh);
 // Segments per image of the fused GAP partials for a conv tile geometry.
 inline int tc_conv_gap_segs(int tiles_h, int tiles_w, int hb, int wb) {
   return tiles_h * tiles_w * (hb * wb > 32 ? hb * wb / 32 : 1);

@@ -1,0 +1,348 @@
+// tcgen05 stem convolution over the space-to-depth image X (see tc_stem.cuh).
+//
+// Warp roles (192 threads, one persistent CTA per SM):
+//   warp 0     : producer (lane 0): resident weights once, then one X slab per
+//                tile (bulk copies, 2 groups x planes) into a ring of stages
+//   warp 1     : MMA issuer (lane 0): k'^2 taps x {1, 3} MMAs (M128 N64 K16)
+//   warps 2..5 : epilogue (TMEM lane quadrant warp % 4): folded BN, ReLU,
+//                hi/lo split, NHWC store of the valid anchors
+#include "sm100_prims.cuh"
+#include "tc_stem.cuh"
+
+namespace lcb {
+
+namespace {
+
+constexpr int kBM = 128;
+constexpr int kCout = 64;
+constexpr int kTapBytes = 2 * kCout * 16;  // [2 groups][64 rows][16 B]
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
+// No-swizzle K-major descriptor: core matrix = 8 rows x 16 B (rows 16 B
+// apart); lbo = byte distance between the two K-adjacent core matrices
+// (channel groups), sbo = byte distance between 8-row groups (128 B).
+__device__ __forceinline__ uint64_t desc_kmajor_none(uint32_t saddr, uint32_t lbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>(128 >> 4) << 32;
+  d |= static_cast<uint64_t>(1) << 46;  // sm_100 descriptor version; layout type 0 = no swizzle
+  return d;
+}
+
+struct StemSmem {
+  int planes, taps, npix_alloc, stages;
+  uint32_t w_bytes, stage_bytes, group_bytes, plane_bytes;
+};
+
+__host__ __device__ inline StemSmem stem_smem(int x3, int kk, int Wx) {
+  StemSmem s;
+  s.planes = x3 ? 2 : 1;
+  s.taps = kk * kk;
+  const int npix = kBM + (kk - 1) * (Wx + 1);
+  s.npix_alloc = (npix + 7) / 8 * 8;
+  s.group_bytes = static_cast<uint32_t>(s.npix_alloc) * 16;
+  s.plane_bytes = 2 * s.group_bytes;
+  s.stage_bytes = s.planes * s.plane_bytes;
+  s.w_bytes = static_cast<uint32_t>(s.planes * s.taps * kTapBytes);
+  int st = static_cast<int>((200u * 1024u - s.w_bytes) / s.stage_bytes);
+  s.stages = st > 8 ? 8 : st;
+  return s;
+}
+
+template <bool X3>
+__global__ void __launch_bounds__(192, 1) tc_stem_kernel(const __grid_constant__ StemParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const StemSmem L = stem_smem(X3 ? 1 : 0, p.kk, p.Wx);
+  const int S = L.stages;
+  uint8_t* wsm = smem;
+  uint8_t* slabs = smem + L.w_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(slabs + S * L.stage_bytes);
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * 8 + 5);
+  const uint32_t full0 = smem_u32(bars);
+  const uint32_t empty0 = smem_u32(bars + 8);
+  const uint32_t tfull0 = smem_u32(bars + 16);
+  const uint32_t tempty0 = smem_u32(bars + 18);
+  const uint32_t wbar = smem_u32(bars + 20);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(full0 + 8 * i, 1);
+      mbar_init(empty0 + 8 * i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(tfull0 + 8 * i, 1);
+      mbar_init(tempty0 + 8 * i, 4);
+    }
+    mbar_init(wbar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc(smem_u32(tmem_holder), 2 * kCout);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  const int count = *p.count;
+  const int total = count * p.tiles_per_img;
+  const int HWx = p.Hx * p.Wx;
+  const int npix = kBM + (p.kk - 1) * (p.Wx + 1);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------ producer
+      const uint32_t wplane = static_cast<uint32_t>(L.taps * kTapBytes);
+      mbar_expect_tx(wbar, L.w_bytes);
+      bulk_g2s(smem_u32(wsm), p.w_hi, wplane, wbar);
+      if (X3) bulk_g2s(smem_u32(wsm + wplane), p.w_lo, wplane, wbar);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const int n = t / p.tiles_per_img;
+        const int m0 = (t - n * p.tiles_per_img) * kBM;
+        const int len = npix < HWx - m0 ? npix : HWx - m0;
+        mbar_wait(empty0 + 8 * stage, phase ^ 1);
+        const uint32_t fb = full0 + 8 * stage;
+        mbar_expect_tx(fb, static_cast<uint32_t>(L.planes * 2 * len * 16));
+        uint8_t* st = slabs + stage * L.stage_bytes;
+        for (int pl = 0; pl < L.planes; ++pl) {
+          const __nv_bfloat16* xp = pl == 0 ? p.x_hi : p.x_lo;
+          for (int grp = 0; grp < 2; ++grp) {
+            const __nv_bfloat16* src = xp + ((static_cast<size_t>(n) * 2 + grp) * HWx + m0) * 8;
+            bulk_g2s(smem_u32(st + pl * L.plane_bytes + grp * L.group_bytes), src, static_cast<uint32_t>(len * 16), fb);
+          }
+        }
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------ MMA issuer
+      constexpr uint32_t idesc = umma_idesc_bf16(kBM, kCout);
+      mbar_wait(wbar, 0);
+      const uint32_t wplane = static_cast<uint32_t>(L.taps * kTapBytes);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1);
+        mbar_wait(full0 + 8 * stage, phase);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * kCout;
+        const uint32_t a0 = smem_u32(slabs + stage * L.stage_bytes);
+        const uint32_t b0 = smem_u32(wsm);
+        for (int tap = 0; tap < L.taps; ++tap) {
+          const int r = tap / p.kk, s = tap - r * p.kk;
+          const uint32_t off = static_cast<uint32_t>(r * p.Wx + s) * 16;
+          const uint32_t bt = b0 + tap * kTapBytes;
+          umma_bf16(d_tmem, desc_kmajor_none(a0 + off, L.group_bytes), desc_kmajor_none(bt, kCout * 16), idesc,
+                    tap > 0 ? 1u : 0u);
+          if (X3) {
+            umma_bf16(d_tmem, desc_kmajor_none(a0 + off, L.group_bytes), desc_kmajor_none(bt + wplane, kCout * 16),
+                      idesc, 1u);
+            umma_bf16(d_tmem, desc_kmajor_none(a0 + L.plane_bytes + off, L.group_bytes),
+                      desc_kmajor_none(bt, kCout * 16), idesc, 1u);
+          }
+        }
+        umma_commit(empty0 + 8 * stage);
+        umma_commit(tfull0 + 8 * acc);
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
+        }
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp < 6) {
+    // ------------------------------------------------ epilogue
+    const int quad = warp & 3;
+    const int row = quad * 32 + lane;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    const int HoWx = p.Ho * p.Wx;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      const int n = t / p.tiles_per_img;
+      const int m = (t - n * p.tiles_per_img) * kBM + row;
+      const int oh = m / p.Wx, ow = m - (m / p.Wx) * p.Wx;
+      const bool valid = m < HoWx && ow < p.Wo;
+      mbar_wait(tfull0 + 8 * acc, acc_phase);
+      tc_fence_after();
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * kCout;
+      float v[4][16];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld16_nowait(t_row + c * 16, v[c]);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty0 + 8 * acc);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+      if (!valid) continue;
+      const size_t off = ((static_cast<size_t>(n) * p.Ho + oh) * p.Wo + ow) * kCout;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint4 hi[2], lo[2];
+        __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(hi);
+        __nv_bfloat162* l2 = reinterpret_cast<__nv_bfloat162*>(lo);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int co = c * 16 + 2 * e;
+          float a = v[c][2 * e] * __ldg(p.scale + co) + __ldg(p.shift + co);
+          float b = v[c][2 * e + 1] * __ldg(p.scale + co + 1) + __ldg(p.shift + co + 1);
+          if (p.relu) {
+            a = a > 0.0f ? a : 0.0f;
+            b = b > 0.0f ? b : 0.0f;
+          }
+          const __nv_bfloat162 hh = __floats2bfloat162_rn(a, b);
+          h2[e] = hh;
+          const float2 hf = __bfloat1622float2(hh);
+          l2[e] = __floats2bfloat162_rn(a - hf.x, b - hf.y);
+        }
+        uint4* oh4 = reinterpret_cast<uint4*>(p.out_hi + off + c * 16);
+        oh4[0] = hi[0];
+        oh4[1] = hi[1];
+        if (p.out_lo) {
+          uint4* ol4 = reinterpret_cast<uint4*>(p.out_lo + off + c * 16);
+          ol4[0] = lo[0];
+          ol4[1] = lo[1];
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+    __syncwarp();
+    tmem_dealloc(tmem_base, 2 * kCout);
+  }
+}
+
+// One thread per (image, channel group, X pixel): 8 channels -> 16-byte stores.
+__global__ void stem_s2d_kernel(const float* x, const int* count, int C, int H, int W, int stride, int pad, int Hx,
+                                int Wx, __nv_bfloat16* x_hi, __nv_bfloat16* x_lo) {
+  const long long HWx = static_cast<long long>(Hx) * Wx;
+  const long long total = static_cast<long long>(*count) * 2 * HWx;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long pix = i % HWx;
+    const int grp = static_cast<int>((i / HWx) % 2);
+    const long long n = i / (2 * HWx);
+    const int I = static_cast<int>(pix / Wx), J = static_cast<int>(pix % Wx);
+    const float* xn = x + n * C * H * W;
+    float v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int q = grp * 8 + e;
+      int c, ih, iw;
+      if (stride == 2) {
+        c = q >> 2;
+        ih = 2 * I + ((q >> 1) & 1) - pad;
+        iw = 2 * J + (q & 1) - pad;
+      } else {
+        c = q;
+        ih = I - pad;
+        iw = J - pad;
+      }
+      v[e] = (c < C && ih >= 0 && ih < H && iw >= 0 && iw < W) ? xn[(static_cast<long long>(c) * H + ih) * W + iw]
+                                                               : 0.0f;
+    }
+    uint4 h4, l4;
+    __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&h4);
+    __nv_bfloat162* l2 = reinterpret_cast<__nv_bfloat162*>(&l4);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const __nv_bfloat162 hh = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+      h2[e] = hh;
+      const float2 hf = __bfloat1622float2(hh);
+      l2[e] = __floats2bfloat162_rn(v[2 * e] - hf.x, v[2 * e + 1] - hf.y);
+    }
+    reinterpret_cast<uint4*>(x_hi)[i] = h4;
+    if (x_lo) reinterpret_cast<uint4*>(x_lo)[i] = l4;
+  }
+}
+
+}  // namespace
+
+StemGeom stem_geom(int H, int W, int k, int stride, int pad) {
+  StemGeom g;
+  g.Ho = (H + 2 * pad - k) / stride + 1;
+  g.Wo = (W + 2 * pad - k) / stride + 1;
+  if (stride == 2) {
+    g.kk = (k + 1) / 2;
+    g.Hx = g.Ho + g.kk - 1;
+    g.Wx = g.Wo + g.kk - 1;
+  } else {
+    g.kk = k;
+    g.Hx = H + 2 * pad;
+    g.Wx = W + 2 * pad;
+  }
+  return g;
+}
+
+void stem_weights(const double* w, int Cout, int C, int k, int stride, const StemGeom& g, float* out) {
+  // out[tap][grp][o][e], channel q = grp*8 + e of X
+  for (int tr = 0; tr < g.kk; ++tr)
+    for (int ts = 0; ts < g.kk; ++ts)
+      for (int grp = 0; grp < 2; ++grp)
+        for (int o = 0; o < Cout; ++o)
+          for (int e = 0; e < 8; ++e) {
+            const int q = grp * 8 + e;
+            int c, r, s;
+            if (stride == 2) {
+              c = q >> 2;
+              r = 2 * tr + ((q >> 1) & 1);
+              s = 2 * ts + (q & 1);
+            } else {
+              c = q;
+              r = tr;
+              s = ts;
+            }
+            double v = 0.0;
+            if (c < C && r < k && s < k) v = w[((static_cast<size_t>(o) * C + c) * k + r) * k + s];
+            out[(((static_cast<size_t>(tr) * g.kk + ts) * 2 + grp) * Cout + o) * 8 + e] = static_cast<float>(v);
+          }
+}
+
+void launch_stem_s2d(const float* x, const int* count, int max_n, int C, int H, int W, int stride, int pad,
+                     const StemGeom& g, __nv_bfloat16* x_hi, __nv_bfloat16* x_lo, cudaStream_t s) {
+  const long long total = static_cast<long long>(max_n) * 2 * g.Hx * g.Wx;
+  long long blocks = (total + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  stem_s2d_kernel<<<static_cast<int>(blocks), 256, 0, s>>>(x, count, C, H, W, stride, pad, g.Hx, g.Wx, x_hi, x_lo);
+}
+
+cudaError_t tc_stem_launch(const StemParams& p, int num_sms, cudaStream_t stream) {
+  const bool x3 = p.x_lo != nullptr;
+  const StemSmem L = stem_smem(x3 ? 1 : 0, p.kk, p.Wx);
+  if (L.stages < 2) return cudaErrorInvalidValue;
+  const size_t smem = L.w_bytes + static_cast<size_t>(L.stages) * L.stage_bytes + 256 + 1024;
+  const long long tiles = static_cast<long long>(p.count_static) * p.tiles_per_img;
+  if (tiles <= 0) return cudaSuccess;
+  const int grid = tiles < num_sms ? static_cast<int>(tiles) : num_sms;
+  if (x3) {
+    cudaError_t e = cudaFuncSetAttribute(tc_stem_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    tc_stem_kernel<true><<<grid, 192, smem, stream>>>(p);
+  } else {
+    cudaError_t e = cudaFuncSetAttribute(tc_stem_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    tc_stem_kernel<false><<<grid, 192, smem, stream>>>(p);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace lcb

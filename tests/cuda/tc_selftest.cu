@@ -64,6 +64,17 @@ static T* dev_copy(const std::vector<T>& h) {
 }
 
 static int g_sms = 148;
+static bool g_tstore = getenv("LCB_TSTORE") != nullptr;
+static bool g_mmares = getenv("LCB_MMARES") != nullptr;
+static __nv_bfloat16* g_eye = nullptr;
+static __nv_bfloat16* eye256() {
+  if (!g_eye) {
+    std::vector<__nv_bfloat16> e(256 * 256, __float2bfloat16(0.0f));
+    for (int i = 0; i < 256; ++i) e[i * 257] = __float2bfloat16(1.0f);
+    g_eye = dev_copy(e);
+  }
+  return g_eye;
+}
 static int g_fail = 0;
 
 static void report(const char* name, double max_rel, double tol) {
@@ -82,7 +93,7 @@ static void conv_test(const char* name, int N, int H, int W, int C, int Cout, in
   for (auto& v : wt) v = static_cast<float>((urand() * 2 - 1) * 0.1);
   std::vector<float> scale(Cout), shift(Cout);
   for (int i = 0; i < Cout; ++i) {
-    scale[i] = static_cast<float>(0.5 + urand());
+    scale[i] = g_mmares ? 1.0f : static_cast<float>(0.5 + urand());
     shift[i] = static_cast<float>(urand() - 0.5);
   }
   std::vector<float> res(static_cast<size_t>(N) * Ho * Wo * Cout);
@@ -215,6 +226,22 @@ static void conv_test(const char* name, int N, int H, int W, int C, int Cout, in
     g_fail++;
     return;
   }
+  if (g_tstore) {
+    int bw, bh;
+    tc_conv_store_box(hb, wb, bw, bh);
+    p.tma_store = encode_out_map(&p.tmO[0], dO_hi, Cout, Wo, Ho, N, bw, bh) &&
+                  encode_out_map(&p.tmO[1], dO_lo, Cout, Wo, Ho, N, bw, bh);
+  }
+  if (g_mmares && use_res) {
+    // residual via identity K-steps; scale must be folded (test uses scale = 1 then)
+    if (encode_act_map(&p.tmR[0], dR_hi, Cout, Wo, Ho, N, 1, wb, hb, 1) &&
+        encode_act_map(&p.tmR[1], dR_lo, Cout, Wo, Ho, N, 1, wb, hb, 1) &&
+        encode_weight_map(&p.tmE, eye256(), 256, 256, BN)) {
+      p.nres = BN / 64;
+      p.res_hi = nullptr;
+      p.res_lo = nullptr;
+    }
+  }
   CK(tc_conv_launch(p, BN, g_sms, 0));
   CK(cudaDeviceSynchronize());
   std::vector<__nv_bfloat16> oh(on), ol(on);
@@ -236,7 +263,8 @@ static void conv_test(const char* name, int N, int H, int W, int C, int Cout, in
       if (d > max_rel) max_rel = d;
     }
   char label[160];
-  snprintf(label, sizeof label, "%s BN=%d hb=%d wb=%d ipt=%d ks=%d", name, BN, hb, wb, ipt, ks_max);
+  snprintf(label, sizeof label, "%s BN=%d hb=%d wb=%d ipt=%d ks=%d%s%s", name, BN, hb, wb, ipt, ks_max,
+           p.tma_store ? " tma-store" : "", p.nres ? " mma-res" : "");
   // bf16 output rounding dominates in plain mode (2^-8); x3 keeps hi+lo (~2^-16).
   report(label, max_rel + (bad_unwritten ? 1.0 : 0.0), x3 ? 2e-4 : 1.2e-2);
   cudaFree(dA_hi);
@@ -477,6 +505,21 @@ static void perf_conv(const char* name, int N, int nsurv, int H, int W, int C, i
     printf("%s: encode failed\n", name);
     return;
   }
+  if (g_tstore) {
+    int bw, bh;
+    tc_conv_store_box(hb, wb, bw, bh);
+    p.tma_store = encode_out_map(&p.tmO[0], o_hi, Cout, Wo, Ho, N, bw, bh) &&
+                  encode_out_map(&p.tmO[1], o_lo, Cout, Wo, Ho, N, bw, bh);
+  }
+  if (g_mmares && use_res) {
+    if (encode_act_map(&p.tmR[0], r_hi, Cout, Wo, Ho, N, 1, wb, hb, 1) &&
+        encode_act_map(&p.tmR[1], r_lo, Cout, Wo, Ho, N, 1, wb, hb, 1) &&
+        encode_weight_map(&p.tmE, eye256(), 256, 256, BN)) {
+      p.nres = BN / 64;
+      p.res_hi = nullptr;
+      p.res_lo = nullptr;
+    }
+  }
   for (int i = 0; i < 3; ++i) CK(tc_conv_launch(p, BN, g_sms, 0));
   CK(cudaDeviceSynchronize());
   cudaEvent_t e0, e1;
@@ -517,20 +560,28 @@ static void perf_conv(const char* name, int N, int nsurv, int H, int W, int C, i
   cudaFree(dWs); cudaFree(dCtr); cudaFree(dTrace);
 }
 
+static int g_only = -1;  // --one K: run only layer config K
+static int g_idx = 0;
+static void perf_layers(bool trace);
+#define PERF(...)                              \
+  do {                                         \
+    if (g_only < 0 || g_only == g_idx) perf_conv(__VA_ARGS__); \
+    ++g_idx;                                   \
+  } while (0)
 static void perf_layers(bool trace) {
   // ResNet-18 CIFAR shapes at the survivor counts of a compacted step.
-  perf_conv("r18 b1 conv 64", 256, 256, 32, 32, 64, 64, 3, 1, true, true, 32, trace);
-  perf_conv("r18 b1 conv 64 bf16", 256, 256, 32, 32, 64, 64, 3, 1, false, true, 32, false);
-  perf_conv("r18 b3 conv1 s2", 256, 159, 32, 32, 64, 128, 3, 2, true, false, 32, false);
-  perf_conv("r18 b3 conv2", 256, 159, 16, 16, 128, 128, 3, 1, true, true, 32, false);
-  perf_conv("r18 b5 conv2", 256, 98, 8, 8, 256, 256, 3, 1, true, true, 32, trace);
-  perf_conv("r18 b8 conv2", 256, 16, 4, 4, 512, 512, 3, 1, true, true, 32, trace);
-  perf_conv("r18 b8 conv2 full", 256, 256, 4, 4, 512, 512, 3, 1, true, true, 32, false);
+  PERF("r18 b1 conv 64", 256, 256, 32, 32, 64, 64, 3, 1, true, true, 32, trace);
+  PERF("r18 b1 conv 64 bf16", 256, 256, 32, 32, 64, 64, 3, 1, false, true, 32, false);
+  PERF("r18 b3 conv1 s2", 256, 159, 32, 32, 64, 128, 3, 2, true, false, 32, false);
+  PERF("r18 b3 conv2", 256, 159, 16, 16, 128, 128, 3, 1, true, true, 32, false);
+  PERF("r18 b5 conv2", 256, 98, 8, 8, 256, 256, 3, 1, true, true, 32, trace);
+  PERF("r18 b8 conv2", 256, 16, 4, 4, 512, 512, 3, 1, true, true, 32, trace);
+  PERF("r18 b8 conv2 full", 256, 256, 4, 4, 512, 512, 3, 1, true, true, 32, false);
   // ResNet-50 ImageNet layer1/layer4 shapes (batch 128).
-  perf_conv("r50 l1 1x1 64->64", 128, 128, 56, 56, 64, 64, 1, 1, true, false, 32, false);
-  perf_conv("r50 l1 3x3 64", 128, 128, 56, 56, 64, 64, 3, 1, true, false, 32, trace);
-  perf_conv("r50 l1 1x1 64->256 res", 128, 128, 56, 56, 64, 256, 1, 1, true, true, 32, trace);
-  perf_conv("r50 l4 3x3 512", 128, 15, 7, 7, 512, 512, 3, 1, true, false, 32, false);
+  PERF("r50 l1 1x1 64->64", 128, 128, 56, 56, 64, 64, 1, 1, true, false, 32, false);
+  PERF("r50 l1 3x3 64", 128, 128, 56, 56, 64, 64, 3, 1, true, false, 32, trace);
+  PERF("r50 l1 1x1 64->256 res", 128, 128, 56, 56, 64, 256, 1, 1, true, true, 32, trace);
+  PERF("r50 l4 3x3 512", 128, 15, 7, 7, 512, 512, 3, 1, true, false, 32, false);
 }
 
 int main(int argc, char** argv) {
@@ -562,6 +613,11 @@ int main(int argc, char** argv) {
   conv_test("conv1x1 s2 8->4 bf16 splitK", 6, 8, 8, 256, 512, 1, 2, false, false, false, true, 256, 4);
   if (argc > 1 && strcmp(argv[1], "--layers") == 0) {
     perf_layers(argc > 2 && strcmp(argv[2], "--trace") == 0);
+    return 0;
+  }
+  if (argc > 2 && strcmp(argv[1], "--one") == 0) {
+    g_only = atoi(argv[2]);
+    perf_layers(false);
     return 0;
   }
   if (argc > 1 && strcmp(argv[1], "--perf") == 0) {

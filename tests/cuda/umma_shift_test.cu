@@ -59,7 +59,7 @@ struct Maps {
 
 // out[variant][shift][128][64] fp32; variants: 0 SW128 base_off 0, 1 SW128
 // base_off (addr>>7)&7, 2 no-swizzle (lbo=region, sbo=128), 3 no-swizzle swapped.
-__global__ void __launch_bounds__(128, 1) shift_kernel(const __grid_constant__ Maps m, float* out) {
+__global__ void __launch_bounds__(128, 1) shift_kernel(const __grid_constant__ Maps m, float* out, int only_v) {
   extern __shared__ uint8_t raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
   uint8_t* a_sw = sm;                       // 256 x 128 B = 32 KB
@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(128, 1) shift_kernel(const __grid_constant__ M
   mbar_wait(smem_u32(&bar[0]), 0);
   uint32_t phase = 0;
   constexpr uint32_t idesc = umma_idesc_bf16(128, kN);
-  for (int v = 0; v < 4; ++v) {
+  for (int v = only_v; v <= only_v; ++v) {
     for (int si = 0; si < kNS; ++si) {
       const int sh = kShifts[si];
       if (threadIdx.x == 0) {
@@ -141,7 +141,8 @@ typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void
                              const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-int main() {
+int main(int argc, char** argv) {
+  const int only_v = argc > 1 ? atoi(argv[1]) : 0;
   void* fp = nullptr;
   cudaDriverEntryPointQueryResult q;
   CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fp, cudaEnableDefault, &q));
@@ -193,13 +194,13 @@ int main() {
   CK(cudaMalloc(&dOut, on * 4));
   CK(cudaMemset(dOut, 0, on * 4));
   CK(cudaFuncSetAttribute(shift_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 90 * 1024));
-  shift_kernel<<<1, 128, 90 * 1024>>>(m, dOut);
+  shift_kernel<<<1, 128, 90 * 1024>>>(m, dOut, only_v);
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
   std::vector<float> out(on);
   CK(cudaMemcpy(out.data(), dOut, on * 4, cudaMemcpyDeviceToHost));
   const char* names[4] = {"SW128 base_off=0", "SW128 base_off=(a>>7)&7", "NONE lbo=K sbo=M", "NONE lbo=M sbo=K"};
-  for (int v = 0; v < 4; ++v) {
+  for (int v = only_v; v <= only_v; ++v) {
     printf("%-26s", names[v]);
     for (int si = 0; si < kNS; ++si) {
       const int sh = hShifts[si];
