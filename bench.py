@@ -278,12 +278,10 @@ def main():
     e2e_s = time.perf_counter() - t0
     barrier()
 
+    from paper_2101_07344_b200.shard import max_over_ranks as _mor
+
     def max_over_ranks(v):
-        if not dist:
-            return v
-        t = torch.tensor([v], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return _mor(v, dist, device="cuda")
 
     ms_cache_max = max_over_ranks(ms_cache)
     ms_base_max = max_over_ranks(ms_base)

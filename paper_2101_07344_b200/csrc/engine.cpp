@@ -183,10 +183,14 @@ Engine::Engine(int device, const BaseModel& model, std::vector<CacheVariant> var
   }
   const char* nf = std::getenv("LCB_NO_GAP_FUSION");
   gap_fusion_ = !(nf && nf[0] == '1');
+  const char* nl = std::getenv("LCB_UNFUSED_LOOKUP");
+  fused_lookup_ = !(nl && nl[0] == '1');
+  const char* nh = std::getenv("LCB_NO_HALO");
+  halo_ = !(nh && nh[0] == '1');
   const char* nr = std::getenv("LCB_NO_MMA_RESIDUAL");
   mma_residual_ = !(nr && nr[0] == '1');
-  const char* nt = std::getenv("LCB_NO_TMA_STORE");
-  tma_store_ = !(nt && nt[0] == '1');
+  const char* nt = std::getenv("LCB_DIRECT_STORE");
+  staged_store_ = !(nt && nt[0] == '1');
   build_weights();
   ck(cudaStreamSynchronize(stream_), "build");
 }
@@ -218,6 +222,8 @@ void Engine::build_weights() {
   d_t0_ = static_cast<unsigned long long*>(dalloc(8));
   d_probs_ = static_cast<float*>(dalloc(static_cast<size_t>(L) * B * sizeof(float)));
   d_lk_count_ = static_cast<int*>(dalloc(sizeof(int)));
+  lk_arrive_ = static_cast<int*>(dalloc(sizeof(int)));
+  ck(cudaMemset(lk_arrive_, 0, sizeof(int)), "memset");
   ws_ = static_cast<float*>(dalloc(tc_conv_ws_floats(256, num_sms_) * sizeof(float)));
   ws_counters_ = static_cast<int*>(dalloc(2 * static_cast<size_t>(num_sms_) * sizeof(int)));
   ck(cudaMemset(ws_counters_, 0, 2 * static_cast<size_t>(num_sms_) * sizeof(int)), "memset");
@@ -269,9 +275,12 @@ void Engine::build_weights() {
         DevConv dc;
         const StemGeom g = stem_geom(o.H, o.W, o.k, o.stride, o.pad);
         std::vector<float> w(static_cast<size_t>(g.kk) * g.kk * 2 * 64 * 8);
-        stem_weights(o.w.data(), o.Cout, o.C, o.k, o.stride, g, w.data());
+        std::vector<double> ws(o.w);
+        const size_t per_out = ws.size() / static_cast<size_t>(o.Cout);
+        for (size_t i = 0; i < ws.size(); ++i) ws[i] *= o.scale[i / per_out];  // fold BN scale
+        stem_weights(ws.data(), o.Cout, o.C, o.k, o.stride, g, w.data());
         dc.w = upload_planes(w);
-        dc.scale = upload_f32(to_f32(o.scale));
+        dc.scale = nullptr;
         dc.shift = upload_f32(to_f32(o.shift));
         cnn_w_[i] = dc;
         slot_elems[static_cast<size_t>(o.out)] = static_cast<long long>(B) * o.Ho() * o.Wo() * o.Cout;
@@ -584,9 +593,7 @@ void Engine::build_mlp_steps(std::vector<Step>& steps, bool shadow) {
     prm->relu = 1;
     prm->out_hi = act.hi;
     prm->out_lo = act.lo;
-    if (tma_store_)
-      prm->tma_store = encode_out_map_2d(&prm->tmO[0], act.hi, f.outp, B) &&
-                       (!x3 || encode_out_map_2d(&prm->tmO[1], act.lo, f.outp, B));
+    prm->staged_store = staged_store_ ? 1 : 0;
     const int sms = num_sms_;
     steps.push_back({[prm, BN, sms](cudaStream_t s) { ck(tc_conv_launch(*prm, BN, sms, s), "tc_conv (mlp)"); }, 1, 1,
                      static_cast<int>(cur_count - d_counts_), 2.0 * f.in * f.out,
@@ -711,21 +718,36 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow) {
       choose_box(Ho, Wo, hb, wb, ipt);
       auto prm = std::make_shared<TcConvParams>();
       std::memset(prm.get(), 0, sizeof(TcConvParams));
-      const int BN = tc_conv_pick_bn(o.Cout, x3 ? 3 : 1);
-      bool ok = encode_act_map(&prm->tmA[0], in.hi, o.C, o.W, o.H, B, 1, wb, hb, o.stride) &&
+      int BN = tc_conv_pick_bn(o.Cout, x3 ? 3 : 1);
+      HaloPlan hp{};
+      const bool halo = halo_ && tc_conv_halo_plan(o.H, o.W, o.k, o.stride, o.pad, o.Cout, x3, BN, hp);
+      // box of the A loads: halo = {Pw, rows} padded-row slab; else the tile's image box
+      const int abw = halo ? hp.pw : wb, abh = halo ? hp.rows : hb;
+      bool ok = encode_act_map(&prm->tmA[0], in.hi, o.C, o.W, o.H, B, 1, abw, abh, o.stride) &&
                 encode_weight_map(&prm->tmB[0], dc.w.hi, dc.Kp, o.Cout, BN);
       if (x3)
-        ok = ok && encode_act_map(&prm->tmA[1], in.lo, o.C, o.W, o.H, B, 1, wb, hb, o.stride) &&
+        ok = ok && encode_act_map(&prm->tmA[1], in.lo, o.C, o.W, o.H, B, 1, abw, abh, o.stride) &&
              encode_weight_map(&prm->tmB[1], dc.w.lo, dc.Kp, o.Cout, BN);
       if (!ok) throw CudaFailure("engine: TMA descriptor encode failed (conv)");
+      if (halo) {
+        hb = 1;
+        wb = 1;
+        ipt = 1;
+        prm->halo = 1;
+        prm->halo_pw = hp.pw;
+        prm->halo_rows = hp.rows;
+        prm->halo_res_rows = hp.res_rows;
+        prm->halo_aplane = hp.aplane;
+        prm->halo_sb = hp.sb;
+      }
       prm->plain = 0;
       prm->Ho = Ho;
       prm->Wo = Wo;
       prm->hb = hb;
       prm->wb = wb;
       prm->ipt = ipt;
-      prm->tiles_h = (Ho + hb - 1) / hb;
-      prm->tiles_w = (Wo + wb - 1) / wb;
+      prm->tiles_h = halo ? hp.tiles_per_img : (Ho + hb - 1) / hb;
+      prm->tiles_w = halo ? 1 : (Wo + wb - 1) / wb;
       prm->conv_stride = o.stride;
       prm->C = o.C;
       prm->ntaps = o.k * o.k;
@@ -745,8 +767,9 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow) {
         const Planes& rb = slot_buf_[static_cast<size_t>(o.res)];
         if (mma_residual_) {
           // residual add on the tensor core: BN/64 extra K-steps (residual x identity)
-          bool rok = encode_act_map(&prm->tmR[0], rb.hi, o.Cout, Wo, Ho, B, 1, wb, hb, 1) &&
-                     (!x3 || encode_act_map(&prm->tmR[1], rb.lo, o.Cout, Wo, Ho, B, 1, wb, hb, 1)) &&
+          const int rbw = halo ? hp.pw : wb, rbh = halo ? hp.res_rows : hb;
+          bool rok = encode_act_map(&prm->tmR[0], rb.hi, o.Cout, Wo, Ho, B, 1, rbw, rbh, 1) &&
+                     (!x3 || encode_act_map(&prm->tmR[1], rb.lo, o.Cout, Wo, Ho, B, 1, rbw, rbh, 1)) &&
                      encode_weight_map(&prm->tmE, identity_, 256, 256, BN);
           if (!rok) throw CudaFailure("engine: TMA descriptor encode failed (residual)");
           prm->nres = BN / 64;
@@ -758,19 +781,14 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow) {
       prm->relu = o.relu ? 1 : 0;
       prm->out_hi = out.hi;
       prm->out_lo = out.lo;
-      if (tma_store_) {
-        int bw, bh;
-        tc_conv_store_box(hb, wb, bw, bh);
-        prm->tma_store = encode_out_map(&prm->tmO[0], out.hi, o.Cout, Wo, Ho, B, bw, bh) &&
-                         (!x3 || encode_out_map(&prm->tmO[1], out.lo, o.Cout, Wo, Ho, B, bw, bh));
-      }
+      prm->staged_store = staged_store_ ? 1 : 0;
       if (o.tap >= 0 && gap_fusion_) {
         // Pool(C) cache on this conv's output: GAP partials from the epilogue.
         const int ci = cache_of_layer_[static_cast<size_t>(o.tap + 1)];
         if (ci >= 0) {
           DevCache& c = *caches_[static_cast<size_t>(ci)];
           if (c.family == 1 && c.win == Ho * Wo && c.width == o.Cout) {
-            const int segs = tc_conv_gap_segs(prm->tiles_h, prm->tiles_w, hb, wb);
+            const int segs = halo ? prm->tiles_h * 4 : tc_conv_gap_segs(prm->tiles_h, prm->tiles_w, hb, wb);
             if (!c.gap) {
               c.gap = static_cast<float*>(dalloc(static_cast<size_t>(B) * segs * o.Cout * sizeof(float)));
               c.gap_segs = segs;
@@ -809,6 +827,50 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow) {
       if (ci >= 0) {
         DevCache& c = *caches_[static_cast<size_t>(ci)];
         const TapInfo& ti = model_.taps[static_cast<size_t>(o.tap)];
+        int* ids_out = ids + static_cast<size_t>(layer) * B;
+        int* cnt_out = counts + layer;
+        float* probs_out = d_probs_ + static_cast<size_t>(layer - 1) * B;
+        if (c.gap && c.family == 1 && fused_lookup_ && fused_lookup_supported(c.classes, c.width, B)) {
+          // one launch: GAP bins + head + first-hit exit + compaction
+          FusedLookupParams fp{};
+          fp.gap = c.gap;
+          fp.segs = c.gap_segs;
+          fp.C = c.width;
+          fp.classes = c.classes;
+          const TapInfo& tinf = model_.taps[static_cast<size_t>(o.tap)];
+          fp.inv = static_cast<float>(1.0 / (tinf.H * tinf.W));
+          fp.W2 = c.W2;
+          fp.b2 = c.b2;
+          fp.Ws1 = c.Ws1;
+          fp.bs1 = c.bs1;
+          fp.ws2 = c.ws2;
+          fp.layer = layer;
+          fp.shadow = shadow ? 1 : 0;
+          fp.count_in = cur_count;
+          fp.ids_in = cur_ids;
+          fp.prob = c.prob;
+          fp.hit = c.hit;
+          fp.label = c.label;
+          fp.arrive = lk_arrive_;
+          fp.exit_layer = d_exit_;
+          fp.served = d_served_;
+          fp.exit_ns = d_exit_ns_;
+          fp.probs_out = probs_out;
+          fp.ids_out = ids_out;
+          fp.count_out = cnt_out;
+          DevCache* cp = &c;
+          const int cidx = static_cast<int>(cur_count - d_counts_);
+          steps.push_back({[fp, cp, B](cudaStream_t s) {
+                             FusedLookupParams q = fp;
+                             q.bs2 = cp->bs2;  // selector output may be recalibrated after build
+                             q.delta = cp->delta;
+                             launch_gap_lookup_exit(q, B, s);
+                           },
+                           2, 1, cidx, 0.0, 4.0 * c.gap_segs * c.width});
+          cur_ids = ids_out;
+          cur_count = cnt_out;
+          continue;
+        }
         Planes tb = slot_buf_[static_cast<size_t>(o.out)];
         TapView tap;
         tap.hi = tb.hi;
@@ -819,10 +881,7 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow) {
         tap.data_idx = cur_ids;
         tap.count = cur_count;
         add_lookup_steps(steps, c, tap, B, true, c.gap != nullptr);
-        int* ids_out = ids + static_cast<size_t>(layer) * B;
-        int* cnt_out = counts + layer;
         DevCache* cp = &c;
-        float* probs_out = d_probs_ + static_cast<size_t>(layer - 1) * B;
         steps.push_back({[this, cp, layer, cur_count, cur_ids, ids_out, cnt_out, probs_out, shadow](cudaStream_t s) {
                            launch_exit_compact(layer, cur_count, cur_ids, cp->hit, cp->label, cp->prob, d_exit_,
                                                d_served_, d_exit_ns_, probs_out, ids_out, nullptr, cnt_out,

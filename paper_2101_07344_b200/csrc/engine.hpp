@@ -156,9 +156,12 @@ class Engine {
   float* ws_ = nullptr;        // split-K workspace shared by all contractions (stream-ordered)
   int* ws_counters_ = nullptr;
   bool gap_fusion_ = true;  // LCB_NO_GAP_FUSION=1 disables the fused Pool(C) partials
-  bool tma_store_ = true;
+  bool staged_store_ = true;  // LCB_DIRECT_STORE=1: per-row 16-byte stores instead of the staged coalesced epilogue
   bool mma_residual_ = true;  // LCB_NO_MMA_RESIDUAL=1: residual added in the epilogue instead of by identity K-steps
-  __nv_bfloat16* identity_ = nullptr;   // LCB_NO_TMA_STORE=1: direct st.global epilogue instead of TMA stores
+  __nv_bfloat16* identity_ = nullptr;
+  bool fused_lookup_ = true;
+  bool halo_ = true;  // LCB_NO_HALO=1: 3x3 stride-1 convs re-read the input per tap instead of one halo slab  // LCB_UNFUSED_LOOKUP=1: gap_bins + head + exit_compact as three launches
+  int* lk_arrive_ = nullptr;
   Planes im2col_buf_;
 
   std::vector<Step> steps_compact_, steps_shadow_;

@@ -541,6 +541,150 @@ __global__ void cache_head_warp_kernel(CacheHeadParams p) {
   }
 }
 
+// ------------------------------------------------------------------ fused lookup + exit
+// One launch per cache layer for Pool(C) = GAP caches with <= 32 classes:
+// every warp owns rows (bins from tc_conv's fused GAP partials, FC(C,classes),
+// softmax, selector FC(C,16)+ReLU+FC(16,1), sigmoid, >= delta, argmax — the
+// arithmetic and summation order of gap_bins_kernel + cache_head_warp_kernel);
+// per-row decisions go to global scratch and the LAST CTA to finish (arrival
+// counter) runs the first-hit record + stable compaction of exit_compact_kernel.
+constexpr int kFusedMaxC = 1024;
+
+__global__ void __launch_bounds__(512) gap_lookup_exit_kernel(FusedLookupParams p) {
+  __shared__ int warp_tot[32];
+  __shared__ int base_s;
+  __shared__ int last_s;
+  const int n_rows = *p.count_in;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int C = p.C, K = p.classes;
+  for (int r = blockIdx.x * nw + warp; r < n_rows; r += gridDim.x * nw) {
+    const long long n = p.ids_in[r];
+    const float* src = p.gap + n * p.segs * C;
+    // bins (gap_bins_kernel order), lane-strided channels
+    // 4 independent partial sums over the segments (fixed combination order)
+    float f[kFusedMaxC / 32];
+#pragma unroll
+    for (int j = 0; j < kFusedMaxC / 32; ++j) {
+      const int c = lane + 32 * j;
+      float a = 0.0f;
+      if (c < C) {
+        float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
+        int sg = 0;
+        for (; sg + 4 <= p.segs; sg += 4) {
+          const float* q = src + static_cast<long long>(sg) * C + c;
+          a0 += __ldg(q);
+          a1 += __ldg(q + C);
+          a2 += __ldg(q + 2 * C);
+          a3 += __ldg(q + 3 * C);
+        }
+        for (; sg < p.segs; ++sg) a0 += __ldg(src + static_cast<long long>(sg) * C + c);
+        a = ((a0 + a1) + (a2 + a3)) * p.inv;
+      }
+      f[j] = a;
+    }
+    // logits (cache_head_warp_kernel order)
+    float logit = -FLT_MAX;
+    for (int k = 0; k < K; ++k) {
+      const float* wr = p.W2 + static_cast<long long>(k) * C;
+      float a = 0.0f;
+#pragma unroll
+      for (int j = 0; j < kFusedMaxC / 32; ++j) {
+        const int c = lane + 32 * j;
+        if (c < C) a += wr[c] * f[j];
+      }
+      a = warp_sum(a);
+      if (lane == k) logit = a + p.b2[k];
+    }
+    const float m = warp_max(lane < K ? logit : -FLT_MAX);
+    const float e = lane < K ? expf(logit - m) : 0.0f;
+    const float sum = warp_sum(e);
+    const float pr = lane < K ? e / sum : 0.0f;
+    float h = 0.0f;
+    {
+      float a = lane < 16 ? p.bs1[lane] : 0.0f;
+      for (int k = 0; k < K; ++k) {
+        const float pk = __shfl_sync(0xffffffffu, pr, k);
+        if (lane < 16) a += p.Ws1[lane * K + k] * pk;
+      }
+      h = (lane < 16 && a > 0.0f) ? a : 0.0f;
+    }
+    const float z = warp_sum(lane < 16 ? p.ws2[lane] * h : 0.0f) + p.bs2;
+    float bv = lane < K ? pr : -FLT_MAX;
+    int bi = lane < K ? lane : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    if (lane == 0) {
+      float q;
+      if (z >= 0.0f) {
+        q = 1.0f / (1.0f + expf(-z));
+      } else {
+        const float ez = expf(z);
+        q = ez / (1.0f + ez);
+      }
+      p.prob[r] = q;
+      p.hit[r] = static_cast<double>(q) >= p.delta ? 1 : 0;
+      p.label[r] = bi;
+    }
+  }
+  // last CTA: first-hit records + stable compaction over all rows
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last_s = (atomicAdd(p.arrive, 1) == static_cast<int>(gridDim.x) - 1) ? 1 : 0;
+  __syncthreads();
+  if (!last_s) return;
+  __threadfence();
+  if (threadIdx.x == 0) {
+    base_s = 0;
+    *p.arrive = 0;
+  }
+  __syncthreads();
+  const unsigned long long now = globaltimer();
+  const int tid = threadIdx.x;
+  for (int c0 = 0; c0 < n_rows; c0 += blockDim.x) {
+    const int r = c0 + tid;
+    const bool valid = r < n_rows;
+    const bool hit = valid && __ldcg(p.hit + r);
+    const int id = valid ? p.ids_in[r] : -1;
+    if (valid) {
+      if (p.probs_out) p.probs_out[id] = __ldcg(p.prob + r);
+      if (hit && p.exit_layer[id] == 0) {
+        p.exit_layer[id] = p.layer;
+        p.served[id] = __ldcg(p.label + r);
+        p.exit_ns[id] = now;
+      }
+    }
+    const bool keep = valid && (p.shadow || !hit);
+    const unsigned mask = __ballot_sync(0xffffffffu, keep);
+    const int pos_in_warp = __popc(mask & ((1u << lane) - 1u));
+    if (lane == 0) warp_tot[warp] = __popc(mask);
+    __syncthreads();
+    if (warp == 0) {
+      int v = lane < nw ? warp_tot[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += u;
+      }
+      if (lane < nw) warp_tot[lane] = v;
+    }
+    __syncthreads();
+    const int warp_off = warp == 0 ? 0 : warp_tot[warp - 1];
+    const int base = base_s;
+    if (keep) p.ids_out[base + warp_off + pos_in_warp] = id;
+    __syncthreads();
+    if (tid == 0) base_s = base + warp_tot[nw - 1];
+    __syncthreads();
+  }
+  if (tid == 0) *p.count_out = base_s;
+}
+
 // ------------------------------------------------------------------ exit
 __global__ void exit_compact_kernel(int layer, const int* count_in, const int* ids_in, const int* hit, const int* label,
                                     const float* prob, int* exit_layer, int* served, unsigned long long* exit_ns,
@@ -947,6 +1091,17 @@ void launch_cache_head(const CacheHeadParams& p_in, int max_rows, cudaStream_t s
     attr = true;
   }
   cache_head_kernel<<<max_rows, 128, smem, s>>>(p);
+}
+
+bool fused_lookup_supported(int classes, int C, int max_rows) {
+  return classes <= 32 && C <= kFusedMaxC && max_rows > 0;
+}
+
+void launch_gap_lookup_exit(const FusedLookupParams& p, int max_rows, cudaStream_t s) {
+  const int warps = 16;
+  int grid = (max_rows + warps - 1) / warps;
+  if (grid > 148) grid = 148;
+  gap_lookup_exit_kernel<<<grid, warps * 32, 0, s>>>(p);
 }
 
 void launch_exit_compact(int layer, const int* count_in, const int* ids_in, const int* hit, const int* label,

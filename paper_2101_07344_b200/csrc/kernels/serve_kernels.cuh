@@ -75,6 +75,36 @@ void launch_cache_head(const CacheHeadParams& p, int max_rows, cudaStream_t s);
 void launch_rows_fc(const float* A, long long lda, int ks, long long part_stride, const float* b1, int feat,
                     const float* W, int classes, const int* count, int max_rows, float* out, cudaStream_t s);
 
+// Fused Pool(C)-GAP lookup + first-hit exit + compaction for <= 32 classes
+// (one launch per cache layer; see gap_lookup_exit_kernel).
+struct FusedLookupParams {
+  const float* gap;   // [image][segs][C] partials from tc_conv
+  int segs, C, classes;
+  float inv;          // 1 / (H*W)
+  const float* W2;    // [classes][C]
+  const float* b2;
+  const float* Ws1;   // [16][classes]
+  const float* bs1;
+  const float* ws2;
+  float bs2;
+  double delta;
+  int layer, shadow;
+  const int* count_in;
+  const int* ids_in;
+  float* prob;        // [rows] scratch
+  int* hit;
+  int* label;
+  int* arrive;        // arrival counter (zero; reset by the last CTA)
+  int* exit_layer;
+  int* served;
+  unsigned long long* exit_ns;
+  float* probs_out;   // [B] this layer's probabilities by request id (nullable)
+  int* ids_out;
+  int* count_out;
+};
+bool fused_lookup_supported(int classes, int C, int max_rows);
+void launch_gap_lookup_exit(const FusedLookupParams& p, int max_rows, cudaStream_t s);
+
 // First-hit exit + stable stream compaction (single CTA, warp ballot +
 // block prefix sum). Rows with hit leave; `ids_in[r]` is the original request
 // id of row r. Writes ids_out/src_rows_out (kept rows in order) and count_out.

@@ -118,12 +118,21 @@ __device__ __forceinline__ bool out_row(const TcConvParams& p, const TileGeom& g
     obase = static_cast<size_t>(grow) * p.Cout;
     return grow < g.count;
   }
-  const int rows_per_img = p.hb * p.wb;
-  const int j = row / rows_per_img;
-  const int pix = row % rows_per_img;
-  const int h = x.h0 + pix / p.wb;
-  const int w = x.w0 + pix % p.wb;
-  const int idx = x.grp * p.ipt + j;
+  int idx, h, w;
+  if (p.halo) {
+    // anchors on the padded row pitch: m = oh * Pw + ow (ow >= Wo are discarded)
+    const int m = x.h0 * kBM + row;
+    h = m / p.halo_pw;
+    w = m - h * p.halo_pw;
+    idx = x.grp;
+  } else {
+    const int rows_per_img = p.hb * p.wb;
+    const int j = row / rows_per_img;
+    const int pix = row % rows_per_img;
+    h = x.h0 + pix / p.wb;
+    w = x.w0 + pix % p.wb;
+    idx = x.grp * p.ipt + j;
+  }
   const bool valid = (idx < g.count) && (h < p.Ho) && (w < p.Wo);
   const int n = valid ? (p.surv ? p.surv[idx] : idx) : 0;
   obase = ((static_cast<size_t>(n) * p.Ho + h) * p.Wo + w) * p.Cout;
@@ -286,7 +295,7 @@ __device__ __forceinline__ void gap_segment_t(const TcConvParams& p, const TileG
     rs_step<1, 4>(v, lane);
     chbase = ((lane >> 2) & 1) * 8 + ((lane >> 1) & 1) * 4 + (lane & 1) * 2;
   }
-  const int rpi = p.hb * p.wb;
+  const int rpi = p.halo ? kBM : p.hb * p.wb;
   const int seg_first = row & ~(kSeg - 1);  // first row of this lane's segment
   const int j = seg_first / rpi;
   const int idx = x.grp * p.ipt + j;
@@ -304,7 +313,7 @@ __device__ __forceinline__ void gap_segment_t(const TcConvParams& p, const TileG
 
 __device__ __forceinline__ void gap_segment(const TcConvParams& p, const TileGeom& g, const Tile& x, int row,
                                             int lane, float (&v)[16], int co) {
-  const int rpi = p.hb * p.wb;  // power of two >= 8 (engine choose_box)
+  const int rpi = p.halo ? kBM : p.hb * p.wb;  // power of two >= 8 (engine choose_box)
   if (rpi >= 32) gap_segment_t<32>(p, g, x, row, lane, v, co);
   else if (rpi == 16) gap_segment_t<16>(p, g, x, row, lane, v, co);
   else gap_segment_t<8>(p, g, x, row, lane, v, co);
@@ -317,12 +326,16 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   // stage s: [A_hi][A_lo?][B_hi][B_lo?]
+  // barriers: [0,8) full (stages / halo B ring), [8,16) empty, [16,18) tfull,
+  // [18,20) tempty, [20,22) halo A-slab full, [22,24) halo A-slab empty
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes + Cfg::kEpiStage);
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 32);
   const uint32_t full0 = smem_u32(bars);
-  const uint32_t empty0 = smem_u32(bars + S);
-  const uint32_t tfull0 = smem_u32(bars + 2 * S);
-  const uint32_t tempty0 = smem_u32(bars + 2 * S + 2);
+  const uint32_t empty0 = smem_u32(bars + 8);
+  const uint32_t tfull0 = smem_u32(bars + 16);
+  const uint32_t tempty0 = smem_u32(bars + 18);
+  const uint32_t afull0 = smem_u32(bars + 20);
+  const uint32_t aempty0 = smem_u32(bars + 22);
   // per epilogue warp TMA-store staging (after the pipeline stages; bars follow)
   uint8_t* epi_stage = smem + S * Cfg::kStageBytes;
   auto stage_a = [&](int s, int plane) { return smem + s * Cfg::kStageBytes + plane * kABytes; };
@@ -332,11 +345,17 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  // debug bits (measurement only): 1 = no TMA loads, 2 = no MMAs, 4 = no epilogue stores
+  const bool dbg_noload = (p.dbg & 1) != 0, dbg_nomma = (p.dbg & 2) != 0, dbg_nostore = (p.dbg & 4) != 0;
 
   if (warp == 0 && lane == 0) {
-    for (int i = 0; i < S; ++i) {
+    for (int i = 0; i < 8; ++i) {
       mbar_init(full0 + 8 * i, 1);
       mbar_init(empty0 + 8 * i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(afull0 + 8 * i, 1);
+      mbar_init(aempty0 + 8 * i, 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(tfull0 + 8 * i, 1);
@@ -365,7 +384,136 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
   const int cchunks = p.C / 64;
   const int cs = p.conv_stride > 0 ? p.conv_stride : 1;
 
-  if (warp == 0) {
+  // halo mode ring carving (runtime): A-slab slots then B slots inside the stage region
+  const uint32_t ring0 = smem_u32(smem);
+  const uint32_t h_aslot = static_cast<uint32_t>(Cfg::kPlanes) * p.halo_aplane;
+  const uint32_t h_bslot = static_cast<uint32_t>(Cfg::kPlanes) * Cfg::kBBytes;
+  const uint32_t h_b0 = ring0 + 2u * h_aslot;
+  const int h_sb = p.halo_sb;
+
+  if (warp == 0 && p.halo) {
+    if (lane == 0) {
+      // ------------------------------------------------ TMA producer (halo)
+      // Per 64-channel chunk one slab of padded rows (box {64, Pw, rows}) feeds
+      // all k*k taps; per (chunk, tap) one weight tile into the B ring.
+      int aslot = 0, bslot = 0;
+      uint32_t aphase = 0, bphase = 0;
+      const int nk_conv = p.ntaps * cchunks;
+      const int pad = -p.tap_dw[0];
+      const uint32_t a_bytes = static_cast<uint32_t>(Cfg::kPlanes * p.halo_pw * p.halo_rows * 128);
+      const uint32_t r_bytes = static_cast<uint32_t>(Cfg::kPlanes * p.halo_pw * p.halo_res_rows * 128);
+      int unit = 0;
+      for (int t = blockIdx.x; t < g.total; t += gridDim.x, ++unit) {
+        const Tile x = decode_tile(t, p, g);
+        trace_put(p, unit, 0);
+        const int img = image_of(p, x.grp < g.count ? x.grp : g.count - 1);
+        const int m0 = x.h0 * kBM;
+        const int R0 = m0 / p.halo_pw;
+        for (int s = x.s_begin; s < x.s_end; ++s) {
+          const bool res = s >= nk_conv;
+          const int cc = res ? 0 : s / p.ntaps, tap = res ? 0 : s % p.ntaps;
+          if (res || tap == 0 || s == x.s_begin) {
+            mbar_wait(aempty0 + 8 * aslot, aphase ^ 1);
+            const uint32_t fb = afull0 + 8 * aslot;
+            mbar_expect_tx(fb, dbg_noload ? 0u : (res ? r_bytes : a_bytes));
+            if (!dbg_noload)
+            for (int pl = 0; pl < Cfg::kPlanes; ++pl) {
+              const uint32_t dst = ring0 + aslot * h_aslot + pl * p.halo_aplane;
+              if (res)
+                tma_load_5d(dst, &p.tmR[pl], fb, x.tn * BN + (s - nk_conv) * 64, 0, R0, img, 0);
+              else
+                tma_load_5d(dst, &p.tmA[pl], fb, cc * 64, -pad, R0 - pad, img, 0);
+            }
+            if (res || tap == p.ntaps - 1 || s == x.s_end - 1) {
+              if (++aslot == 2) {
+                aslot = 0;
+                aphase ^= 1;
+              }
+            }
+          } else if (tap == p.ntaps - 1 || s == x.s_end - 1) {
+            if (++aslot == 2) {
+              aslot = 0;
+              aphase ^= 1;
+            }
+          }
+          mbar_wait(empty0 + 8 * bslot, bphase ^ 1);
+          const uint32_t fb = full0 + 8 * bslot;
+          mbar_expect_tx(fb, dbg_noload ? 0u : static_cast<uint32_t>(Cfg::kPlanes * Cfg::kBBytes));
+          for (int pl = 0; pl < (dbg_noload ? 0 : Cfg::kPlanes); ++pl) {
+            const uint32_t dst = h_b0 + bslot * h_bslot + pl * Cfg::kBBytes;
+            if (res)
+              tma_load_2d(dst, &p.tmE, fb, (s - nk_conv) * 64, 0);
+            else
+              tma_load_2d(dst, &p.tmB[pl], fb, tap * p.C + cc * 64, x.tn * BN);
+          }
+          if (++bslot == h_sb) {
+            bslot = 0;
+            bphase ^= 1;
+          }
+        }
+        trace_put(p, unit, 1);
+      }
+    }
+  } else if (warp == 1 && p.halo) {
+    if (lane == 0) {
+      // ------------------------------------------------ MMA issuer (halo)
+      constexpr uint32_t idesc = umma_idesc_bf16(kBM, BN);
+      int aslot = 0, bslot = 0;
+      uint32_t aphase = 0, bphase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      const int nk_conv = p.ntaps * cchunks;
+      const int kk = p.tap_dw[p.ntaps - 1] - p.tap_dw[0] + 1;  // filter width
+      int unit = 0;
+      for (int t = blockIdx.x; t < g.total; t += gridDim.x, ++unit) {
+        const Tile x = decode_tile(t, p, g);
+        mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1);
+        tc_fence_after();
+        trace_put(p, unit, 2);
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        const int m0 = x.h0 * kBM;
+        const int base_row = m0 - (m0 / p.halo_pw) * p.halo_pw;  // anchor m0 inside the slab
+        for (int s = x.s_begin; s < x.s_end; ++s) {
+          const bool res = s >= nk_conv;
+          const int tap = res ? 0 : s % p.ntaps;
+          const bool new_a = res || tap == 0 || s == x.s_begin;
+          const bool last_a = res || tap == p.ntaps - 1 || s == x.s_end - 1;
+          if (new_a) mbar_wait(afull0 + 8 * aslot, aphase);
+          mbar_wait(full0 + 8 * bslot, bphase);
+          tc_fence_after();
+          const int row_off = res ? base_row : base_row + (tap / kk) * p.halo_pw + (tap % kk);
+          const uint32_t ah = ring0 + aslot * h_aslot + static_cast<uint32_t>(row_off) * 128;
+          const uint32_t al = ah + p.halo_aplane;
+          const uint32_t bh = h_b0 + bslot * h_bslot, bl = bh + Cfg::kBBytes;
+#pragma unroll
+          for (int k = 0; k < (dbg_nomma ? 0 : 4); ++k) {
+            const uint32_t first = (s > x.s_begin || k > 0) ? 1u : 0u;
+            umma_bf16(d_tmem, umma_desc_sw128(ah + 32 * k), umma_desc_sw128(bh + 32 * k), idesc, first);
+            if (X3) {
+              if (!res) umma_bf16(d_tmem, umma_desc_sw128(ah + 32 * k), umma_desc_sw128(bl + 32 * k), idesc, 1u);
+              umma_bf16(d_tmem, umma_desc_sw128(al + 32 * k), umma_desc_sw128(bh + 32 * k), idesc, 1u);
+            }
+          }
+          umma_commit(empty0 + 8 * bslot);
+          if (++bslot == h_sb) {
+            bslot = 0;
+            bphase ^= 1;
+          }
+          if (last_a) {
+            umma_commit(aempty0 + 8 * aslot);
+            if (++aslot == 2) {
+              aslot = 0;
+              aphase ^= 1;
+            }
+          }
+        }
+        umma_commit(tfull0 + 8 * acc);
+        trace_put(p, unit, 3);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------ TMA producer
       int stage = 0;
@@ -391,8 +539,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
         for (int s = x.s_begin; s < x.s_end; ++s) {
           mbar_wait(empty0 + 8 * stage, phase ^ 1);
           const uint32_t fb = full0 + 8 * stage;
-          mbar_expect_tx(fb, Cfg::kStageBytes);
-          if (s >= nk_conv) {
+          mbar_expect_tx(fb, dbg_noload ? 0u : static_cast<uint32_t>(Cfg::kStageBytes));
+          if (dbg_noload) {
+          } else if (s >= nk_conv) {
             // residual K-step: A = residual channels [tn*BN + j*64, +64) at the
             // output pixels, B = identity slice (the residual add on the tensor core)
             const int j = s - nk_conv;
@@ -446,7 +595,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
           const uint32_t ah = smem_u32(stage_a(stage, 0)), bh = smem_u32(stage_b(stage, 0));
           const bool res_step = s >= nk_conv;
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
+          for (int k = 0; k < (dbg_nomma ? 0 : 4); ++k) {
             const uint32_t first = (s > x.s_begin || k > 0) ? 1u : 0u;
             umma_bf16(d_tmem, umma_desc_sw128(ah + 32 * k), umma_desc_sw128(bh + 32 * k), idesc, first);
             if (X3) {
@@ -478,7 +627,6 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
     const int etid = threadIdx.x - 64;  // 0..255
     const int col0 = half * kCols;
     const uint32_t wstage = smem_u32(epi_stage + (warp - 2) * 4096);
-    uint32_t tslot = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     int unit = 0;
@@ -488,7 +636,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
       const bool valid = out_row(p, g, x, row, obase);
       const int grow = x.w0 + row;
       const bool split = p.mode == 0 && g.ks > 1;
-      const bool tstore = p.tma_store && p.mode == 0 && !split;
+      const bool tstore = p.staged_store && p.mode == 0 && !split;
       // Residual of this row's columns, fetched before the accumulator is
       // ready so its latency overlaps the tile's MMAs.
       uint4 rh[kChunks], rl[X3 ? kChunks : 1];
@@ -559,48 +707,34 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
           }
         }
         if (tstore) {
-          // this warp's 32 rows x 32 columns, one plane at a time through two
-          // 2 KB staging slots (64-byte swizzle) -> TMA stores (bulk groups);
-          // a slot is rewritten once its previous store has been read.
+          // Coalesced stores: each lane stages its row's 32 columns (hi, lo)
+          // in shared memory (64-byte swizzle), then the warp writes 8 rows x
+          // 64 contiguous bytes per instruction (full 32-byte sectors) instead
+          // of 32 rows x 16 bytes.
+          __syncwarp();  // previous chunk's read-back done
 #pragma unroll
-          for (int pl = 0; pl < (X3 ? 2 : 1); ++pl) {
-            if (pl == 1 && !p.out_lo) break;
-            const uint32_t slot = wstage + (tslot & 1) * 2048;
-            ++tslot;
-            if (lane == 0) bulk_wait_read1();
-            __syncwarp();
+          for (int u = 0; u < kSub; ++u) {
+            uint4 hi[2], lo[2];
+            split16(v[u], hi, lo);
 #pragma unroll
-            for (int u = 0; u < kSub; ++u) {
-              uint4 hi[2], lo[2];
-              split16(v[u], hi, lo);
-#pragma unroll
-              for (int hq = 0; hq < 2; ++hq) {
-                const uint32_t off = static_cast<uint32_t>(lane * 64 + (((u * 2 + hq) ^ ((lane >> 1) & 3)) * 16));
-                st_shared_v4(slot + off, pl == 0 ? hi[hq] : lo[hq]);
-              }
+            for (int hq = 0; hq < 2; ++hq) {
+              const uint32_t off = static_cast<uint32_t>(lane * 64 + (((u * 2 + hq) ^ ((lane >> 1) & 3)) * 16));
+              st_shared_v4(wstage + off, hi[hq]);
+              if (X3) st_shared_v4(wstage + 2048 + off, lo[hq]);
             }
-            fence_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-              const int c0 = x.tn * BN + col0 + c32 * 32;
-              const int row0 = quad * 32;
-              const CUtensorMap* om = &p.tmO[pl];
-              if (p.plain) {
-                tma_store_2d(om, slot, c0, x.w0 + row0);
-              } else {
-                const int rpi = p.hb * p.wb;
-                const int nimg = rpi >= 32 ? 1 : 32 / rpi;
-                for (int jj = 0; jj < nimg; ++jj) {
-                  const int r0 = row0 + jj * (rpi >= 32 ? 0 : rpi);
-                  const int idx = x.grp * p.ipt + r0 / rpi;
-                  if (idx >= g.count) continue;
-                  const int n = p.surv ? p.surv[idx] : idx;
-                  const int pix = r0 % rpi;
-                  tma_store_5d(om, slot + static_cast<uint32_t>((r0 - row0) * 64), c0, x.w0 + pix % p.wb,
-                               x.h0 + pix / p.wb, n, 0);
-                }
-              }
-              bulk_commit();
+          }
+          __syncwarp();
+          const int c0 = x.tn * BN + col0 + c32 * 32;
+          const int ch = lane & 3;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int r = (lane >> 2) + 8 * i;  // row within the warp
+            const unsigned long long ob = __shfl_sync(0xffffffffu, static_cast<unsigned long long>(obase), r);
+            const int ok = __shfl_sync(0xffffffffu, valid ? 1 : 0, r);
+            const uint32_t off = static_cast<uint32_t>(r * 64 + ((ch ^ ((r >> 1) & 3)) * 16));
+            if (ok && !dbg_nostore) {
+              *reinterpret_cast<uint4*>(p.out_hi + ob + c0 + ch * 8) = ld_shared_v4(wstage + off);
+              if (X3 && p.out_lo) *reinterpret_cast<uint4*>(p.out_lo + ob + c0 + ch * 8) = ld_shared_v4(wstage + 2048 + off);
             }
           }
           if (p.gap_out) {
@@ -671,7 +805,6 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
       }
       if (etid == 0) trace_put(p, unit, 5);
     }
-    if (lane == 0) bulk_wait0();
   }
   __syncthreads();
   if (warp == 0) {
@@ -750,50 +883,45 @@ bool encode_weight_map(CUtensorMap* map, const void* base, int K, int Cout, int 
   return r == CUDA_SUCCESS;
 }
 
-bool encode_out_map(CUtensorMap* map, const void* base, int Cout, int Wo, int Ho, int N, int bw, int bh) {
-  EncodeTiledFn fn = encode_fn();
-  if (!fn) return false;
-  cuuint64_t dims[5] = {static_cast<cuuint64_t>(Cout), static_cast<cuuint64_t>(Wo), static_cast<cuuint64_t>(Ho),
-                        static_cast<cuuint64_t>(N), 1};
-  cuuint64_t strides[4];
-  strides[0] = static_cast<cuuint64_t>(Cout) * 2;
-  strides[1] = strides[0] * Wo;
-  strides[2] = strides[1] * Ho;
-  strides[3] = strides[2] * N;
-  cuuint32_t box[5] = {32, static_cast<cuuint32_t>(bw), static_cast<cuuint32_t>(bh), 1, 1};
-  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
-}
-
-bool encode_out_map_2d(CUtensorMap* map, const void* base, int Cout, int rows) {
-  EncodeTiledFn fn = encode_fn();
-  if (!fn) return false;
-  cuuint64_t dims[2] = {static_cast<cuuint64_t>(Cout), static_cast<cuuint64_t>(rows)};
-  cuuint64_t strides[1] = {static_cast<cuuint64_t>(Cout) * 2};
-  cuuint32_t box[2] = {32, 32};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
-}
-
-void tc_conv_store_box(int hb, int wb, int& bw, int& bh) {
-  // the 32 consecutive tile rows of one epilogue warp as a (w, h) box of one image
-  const int rpi = hb * wb;
-  if (rpi <= 32) {
-    bw = wb;
-    bh = hb;
-  } else if (wb >= 32) {
-    bw = 32;
-    bh = 1;
-  } else {
-    bw = wb;
-    bh = 32 / wb;
+int tc_conv_ring_bytes(int BN, bool x3) {
+  switch (BN) {
+    case 64:
+      return x3 ? TcCfg<64, true>::kStages * TcCfg<64, true>::kStageBytes
+                : TcCfg<64, false>::kStages * TcCfg<64, false>::kStageBytes;
+    case 128:
+      return x3 ? TcCfg<128, true>::kStages * TcCfg<128, true>::kStageBytes
+                : TcCfg<128, false>::kStages * TcCfg<128, false>::kStageBytes;
+    case 256:
+      return x3 ? 0 : TcCfg<256, false>::kStages * TcCfg<256, false>::kStageBytes;
+    default:
+      return 0;
   }
+}
+
+bool tc_conv_halo_plan(int H, int W, int k, int stride, int pad, int Cout, bool x3, int& BN, HaloPlan& hp) {
+  if (stride != 1 || k < 2 || pad != k / 2 || (k % 2) == 0) return false;
+  const int Pw = W + 2 * pad;
+  if (Pw < 16 || Pw > 256) return false;
+  const int rows = (Pw - 1 + 127 + (k - 1) * (Pw + 1)) / Pw + 1;
+  if (rows > 256) return false;
+  const int planes = x3 ? 2 : 1;
+  hp.pw = Pw;
+  hp.rows = rows;
+  hp.res_rows = (Pw - 1 + 127) / Pw + 1;
+  hp.aplane = static_cast<unsigned>((Pw * rows * 128 + 1023) / 1024 * 1024);
+  hp.tiles_per_img = (H * Pw + 127) / 128;
+  for (int bn : {BN, 64}) {
+    if (Cout % bn) continue;
+    const long long ring = tc_conv_ring_bytes(bn, x3);
+    const long long left = ring - 2LL * planes * hp.aplane;
+    const int sb = left > 0 ? static_cast<int>(left / (static_cast<long long>(planes) * bn * 128)) : 0;
+    if (sb >= 3) {
+      BN = bn;
+      hp.sb = sb > 8 ? 8 : sb;
+      return true;
+    }
+  }
+  return false;
 }
 
 int tc_conv_pick_bn(int Cout, int segs) {

@@ -36,11 +36,19 @@ constexpr int kMaxTaps = 64;
 struct TcConvParams {
   CUtensorMap tmA[2];  // activation planes hi, lo (5-D: C, W, H, N, P)
   CUtensorMap tmB[2];  // weight planes hi, lo (2-D: K, Cout)
-  CUtensorMap tmO[2];  // output planes for TMA stores (tma_store = 1): 5-D NHWC or 2-D rows, box 32 channels
   CUtensorMap tmR[2];  // residual planes as an A operand (nres > 0): 5-D NHWC at the output resolution
   CUtensorMap tmE;     // identity matrix [256][256] bf16 as the B operand of the residual K-steps
   int nres;            // residual K-steps per tile (BN/64): out = conv + residual computed by the MMA
-  int tma_store;       // 1: epilogue stages tiles in shared memory and TMA-stores them (mode 0, no split)
+  // Halo mode (stride-1 k x k conv, one image per tile): 128 output anchors on
+  // the padded row pitch Pw = W + k - 1 (tiles_h = tiles per image, hb = wb = 1,
+  // ipt = 1); per 64-channel chunk ONE slab of halo_rows padded rows (tmA box
+  // {64, Pw, halo_rows}) feeds all k*k taps as row-shifted SW128 descriptors.
+  int halo;
+  int halo_pw, halo_rows, halo_res_rows;
+  unsigned halo_aplane;  // bytes per plane of an A-slab slot (1024-aligned)
+  int halo_sb;           // B ring depth (2 A-slab slots)
+  int dbg;               // measurement-only bits: 1 no TMA loads, 2 no MMAs, 4 no epilogue stores
+  int staged_store;    // 1: epilogue stages 32x32 sub-tiles in shared memory and writes full sectors (mode 0, no split)
   int plain;           // 1: plain GEMM over rows (A = [rows, K], count = rows)
   int Ho, Wo;          // output spatial dims
   int hb, wb, ipt;     // output tile geometry: ipt images x hb x wb = 128 rows
@@ -80,11 +88,15 @@ bool encode_act_map(CUtensorMap* map, const void* base, int C, int W, int H, int
                     int stride = 1);
 bool encode_weight_map(CUtensorMap* map, const void* base, int K, int Cout, int BN);
 int tc_conv_pick_bn(int Cout, int segs = 1);
-// Output maps for the TMA-store epilogue (64-byte swizzle, 32-channel boxes).
-bool encode_out_map(CUtensorMap* map, const void* base, int Cout, int Wo, int Ho, int N, int bw, int bh);
-bool encode_out_map_2d(CUtensorMap* map, const void* base, int Cout, int rows);
-// (w, h) box of one epilogue warp's 32 tile rows for a tile box hb x wb.
-void tc_conv_store_box(int hb, int wb, int& bw, int& bh);
+// Halo-mode geometry for a stride-1 k x k conv over an H x W image; BN may be
+// lowered to 64 so the B ring keeps >= 3 slots. False if it does not apply.
+struct HaloPlan {
+  int pw, rows, res_rows, tiles_per_img, sb;
+  unsigned aplane;
+};
+bool tc_conv_halo_plan(int H, int W, int k, int stride, int pad, int Cout, bool x3, int& BN, HaloPlan& hp);
+int tc_conv_ring_bytes(int BN, bool x3);
+
 // Segments per image of the fused GAP partials for a conv tile geometry.
 inline int tc_conv_gap_segs(int tiles_h, int tiles_w, int hb, int wb) {
   return tiles_h * tiles_w * (hb * wb > 32 ? hb * wb / 32 : 1);

@@ -50,7 +50,7 @@ __host__ __device__ inline StemSmem stem_smem(int x3, int kk, int Wx) {
   s.plane_bytes = 2 * s.group_bytes;
   s.stage_bytes = s.planes * s.plane_bytes;
   s.w_bytes = static_cast<uint32_t>(s.planes * s.taps * kTapBytes);
-  int st = static_cast<int>((200u * 1024u - s.w_bytes) / s.stage_bytes);
+  int st = static_cast<int>((200u * 1024u - 16u * 1024u - s.w_bytes) / s.stage_bytes);
   s.stages = st > 8 ? 8 : st;
   return s;
 }
@@ -63,7 +63,9 @@ __global__ void __launch_bounds__(192, 1) tc_stem_kernel(const __grid_constant__
   const int S = L.stages;
   uint8_t* wsm = smem;
   uint8_t* slabs = smem + L.w_bytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(slabs + S * L.stage_bytes);
+  uint8_t* epi = slabs + S * L.stage_bytes;  // 4 warps x 4 KB staging, then 64 floats of shift
+  float* shift_s = reinterpret_cast<float*>(epi + 4 * 4096);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(epi + 4 * 4096 + 256);
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * 8 + 5);
   const uint32_t full0 = smem_u32(bars);
   const uint32_t empty0 = smem_u32(bars + 8);
@@ -84,6 +86,7 @@ __global__ void __launch_bounds__(192, 1) tc_stem_kernel(const __grid_constant__
     mbar_init(wbar, 1);
     fence_mbar_init();
   }
+  if (threadIdx.x < kCout) shift_s[threadIdx.x] = p.shift[threadIdx.x];
   if (warp == 0) tmem_alloc(smem_u32(tmem_holder), 2 * kCout);
   tc_fence_before();
   __syncthreads();
@@ -189,34 +192,50 @@ __global__ void __launch_bounds__(192, 1) tc_stem_kernel(const __grid_constant__
       if (lane == 0) mbar_arrive(tempty0 + 8 * acc);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
-      if (!valid) continue;
-      const size_t off = ((static_cast<size_t>(n) * p.Ho + oh) * p.Wo + ow) * kCout;
+      // staged, coalesced stores: 32 rows x 32 channels per step, 8 rows x 64 B per instruction
+      const unsigned long long off = valid ? ((static_cast<unsigned long long>(n) * p.Ho + oh) * p.Wo + ow) * kCout : 0ull;
+      const uint32_t wst = smem_u32(epi + quad * 4096);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint4 hi[2], lo[2];
-        __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(hi);
-        __nv_bfloat162* l2 = reinterpret_cast<__nv_bfloat162*>(lo);
+      for (int q = 0; q < 2; ++q) {
+        __syncwarp();
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const int co = c * 16 + 2 * e;
-          float a = v[c][2 * e] * __ldg(p.scale + co) + __ldg(p.shift + co);
-          float b = v[c][2 * e + 1] * __ldg(p.scale + co + 1) + __ldg(p.shift + co + 1);
-          if (p.relu) {
-            a = a > 0.0f ? a : 0.0f;
-            b = b > 0.0f ? b : 0.0f;
+        for (int u = 0; u < 2; ++u) {
+          const int cb = q * 32 + u * 16;
+          uint4 hi[2], lo[2];
+          __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(hi);
+          __nv_bfloat162* l2 = reinterpret_cast<__nv_bfloat162*>(lo);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            float a = v[2 * q + u][2 * e] + shift_s[cb + 2 * e];
+            float b = v[2 * q + u][2 * e + 1] + shift_s[cb + 2 * e + 1];
+            if (p.relu) {
+              a = a > 0.0f ? a : 0.0f;
+              b = b > 0.0f ? b : 0.0f;
+            }
+            const __nv_bfloat162 hh = __floats2bfloat162_rn(a, b);
+            h2[e] = hh;
+            const float2 hf = __bfloat1622float2(hh);
+            l2[e] = __floats2bfloat162_rn(a - hf.x, b - hf.y);
           }
-          const __nv_bfloat162 hh = __floats2bfloat162_rn(a, b);
-          h2[e] = hh;
-          const float2 hf = __bfloat1622float2(hh);
-          l2[e] = __floats2bfloat162_rn(a - hf.x, b - hf.y);
+#pragma unroll
+          for (int hq = 0; hq < 2; ++hq) {
+            const uint32_t so = static_cast<uint32_t>(lane * 64 + (((u * 2 + hq) ^ ((lane >> 1) & 3)) * 16));
+            st_shared_v4(wst + so, hi[hq]);
+            if (X3) st_shared_v4(wst + 2048 + so, lo[hq]);
+          }
         }
-        uint4* oh4 = reinterpret_cast<uint4*>(p.out_hi + off + c * 16);
-        oh4[0] = hi[0];
-        oh4[1] = hi[1];
-        if (p.out_lo) {
-          uint4* ol4 = reinterpret_cast<uint4*>(p.out_lo + off + c * 16);
-          ol4[0] = lo[0];
-          ol4[1] = lo[1];
+        __syncwarp();
+        const int ch = lane & 3;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int r = (lane >> 2) + 8 * i;
+          const unsigned long long ob = __shfl_sync(0xffffffffu, off, r);
+          const int ok = __shfl_sync(0xffffffffu, valid ? 1 : 0, r);
+          const uint32_t so = static_cast<uint32_t>(r * 64 + ((ch ^ ((r >> 1) & 3)) * 16));
+          if (ok) {
+            *reinterpret_cast<uint4*>(p.out_hi + ob + q * 32 + ch * 8) = ld_shared_v4(wst + so);
+            if (X3 && p.out_lo) *reinterpret_cast<uint4*>(p.out_lo + ob + q * 32 + ch * 8) = ld_shared_v4(wst + 2048 + so);
+          }
         }
       }
     }
@@ -327,7 +346,7 @@ cudaError_t tc_stem_launch(const StemParams& p, int num_sms, cudaStream_t stream
   const bool x3 = p.x_lo != nullptr;
   const StemSmem L = stem_smem(x3 ? 1 : 0, p.kk, p.Wx);
   if (L.stages < 2) return cudaErrorInvalidValue;
-  const size_t smem = L.w_bytes + static_cast<size_t>(L.stages) * L.stage_bytes + 256 + 1024;
+  const size_t smem = L.w_bytes + static_cast<size_t>(L.stages) * L.stage_bytes + 4 * 4096 + 256 + 256 + 1024;
   const long long tiles = static_cast<long long>(p.count_static) * p.tiles_per_img;
   if (tiles <= 0) return cudaSuccess;
   const int grid = tiles < num_sms ? static_cast<int>(tiles) : num_sms;

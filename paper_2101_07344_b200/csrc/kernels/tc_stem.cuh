@@ -30,7 +30,7 @@ struct StemParams {
   int tiles_per_img;          // ceil(Ho * Wx / 128)
   const int* count;           // images in the batch (device)
   int count_static;           // max images (grid sizing)
-  const float* scale;         // folded BN [64]
+  const float* scale;         // unused (BN scale is folded into the weights)
   const float* shift;         // [64]
   int relu;
   __nv_bfloat16* out_hi;      // NHWC [N][Ho][Wo][64]

@@ -66,6 +66,7 @@ static T* dev_copy(const std::vector<T>& h) {
 static int g_sms = 148;
 static bool g_tstore = getenv("LCB_TSTORE") != nullptr;
 static bool g_mmares = getenv("LCB_MMARES") != nullptr;
+static bool g_halo = getenv("LCB_HALO") != nullptr;
 static __nv_bfloat16* g_eye = nullptr;
 static __nv_bfloat16* eye256() {
   if (!g_eye) {
@@ -216,26 +217,35 @@ static void conv_test(const char* name, int N, int H, int W, int C, int Cout, in
       p.tap_dh[t] = static_cast<signed char>(r - pad);
       p.tap_dw[t] = static_cast<signed char>(s - pad);
     }
-  const int BN = BNforce ? BNforce : tc_conv_pick_bn(Cout, x3 ? 3 : 1);
-  bool ok = encode_act_map(&p.tmA[0], dA_hi, C, Ws, Hs, N, P, wb, hb, stride) &&
-            encode_act_map(&p.tmA[1], dA_lo, C, Ws, Hs, N, P, wb, hb, stride) &&
+  int BN = BNforce ? BNforce : tc_conv_pick_bn(Cout, x3 ? 3 : 1);
+  HaloPlan hp{};
+  const bool halo = g_halo && tc_conv_halo_plan(H, W, k, stride, pad, Cout, x3, BN, hp);
+  const int abw = halo ? hp.pw : wb, abh = halo ? hp.rows : hb;
+  bool ok = encode_act_map(&p.tmA[0], dA_hi, C, Ws, Hs, N, P, abw, abh, stride) &&
+            encode_act_map(&p.tmA[1], dA_lo, C, Ws, Hs, N, P, abw, abh, stride) &&
             encode_weight_map(&p.tmB[0], dW_hi, k * k * C, Cout, BN) &&
             encode_weight_map(&p.tmB[1], dW_lo, k * k * C, Cout, BN);
+  if (halo) {
+    p.halo = 1;
+    p.halo_pw = hp.pw;
+    p.halo_rows = hp.rows;
+    p.halo_res_rows = hp.res_rows;
+    p.halo_aplane = hp.aplane;
+    p.halo_sb = hp.sb;
+    p.hb = p.wb = p.ipt = 1;
+    p.tiles_h = hp.tiles_per_img;
+    p.tiles_w = 1;
+  }
   if (!ok) {
     printf("%s: tensor map encode failed\n", name);
     g_fail++;
     return;
   }
-  if (g_tstore) {
-    int bw, bh;
-    tc_conv_store_box(hb, wb, bw, bh);
-    p.tma_store = encode_out_map(&p.tmO[0], dO_hi, Cout, Wo, Ho, N, bw, bh) &&
-                  encode_out_map(&p.tmO[1], dO_lo, Cout, Wo, Ho, N, bw, bh);
-  }
+  if (g_tstore) p.staged_store = 1;
   if (g_mmares && use_res) {
     // residual via identity K-steps; scale must be folded (test uses scale = 1 then)
-    if (encode_act_map(&p.tmR[0], dR_hi, Cout, Wo, Ho, N, 1, wb, hb, 1) &&
-        encode_act_map(&p.tmR[1], dR_lo, Cout, Wo, Ho, N, 1, wb, hb, 1) &&
+    if (encode_act_map(&p.tmR[0], dR_hi, Cout, Wo, Ho, N, 1, halo ? hp.pw : wb, halo ? hp.res_rows : hb, 1) &&
+        encode_act_map(&p.tmR[1], dR_lo, Cout, Wo, Ho, N, 1, halo ? hp.pw : wb, halo ? hp.res_rows : hb, 1) &&
         encode_weight_map(&p.tmE, eye256(), 256, 256, BN)) {
       p.nres = BN / 64;
       p.res_hi = nullptr;
@@ -264,7 +274,7 @@ static void conv_test(const char* name, int N, int H, int W, int C, int Cout, in
     }
   char label[160];
   snprintf(label, sizeof label, "%s BN=%d hb=%d wb=%d ipt=%d ks=%d%s%s", name, BN, hb, wb, ipt, ks_max,
-           p.tma_store ? " tma-store" : "", p.nres ? " mma-res" : "");
+           p.staged_store ? " staged" : "", p.nres ? (p.halo ? " mma-res halo" : " mma-res") : (p.halo ? " halo" : ""));
   // bf16 output rounding dominates in plain mode (2^-8); x3 keeps hi+lo (~2^-16).
   report(label, max_rel + (bad_unwritten ? 1.0 : 0.0), x3 ? 2e-4 : 1.2e-2);
   cudaFree(dA_hi);
@@ -496,30 +506,40 @@ static void perf_conv(const char* name, int N, int nsurv, int H, int W, int C, i
       p.tap_dh[t] = static_cast<signed char>(r - pad);
       p.tap_dw[t] = static_cast<signed char>(s2 - pad);
     }
-  const int BN = tc_conv_pick_bn(Cout, x3 ? 3 : 1);
-  bool ok = encode_act_map(&p.tmA[0], a_hi, C, W, H, N, 1, wb, hb, stride) &&
-            encode_act_map(&p.tmA[1], a_lo, C, W, H, N, 1, wb, hb, stride) &&
+  int BN = tc_conv_pick_bn(Cout, x3 ? 3 : 1);
+  HaloPlan hp{};
+  const bool halo = g_halo && tc_conv_halo_plan(H, W, k, stride, pad, Cout, x3, BN, hp);
+  const int abw = halo ? hp.pw : wb, abh = halo ? hp.rows : hb;
+  bool ok = encode_act_map(&p.tmA[0], a_hi, C, W, H, N, 1, abw, abh, stride) &&
+            encode_act_map(&p.tmA[1], a_lo, C, W, H, N, 1, abw, abh, stride) &&
             encode_weight_map(&p.tmB[0], w_hi, k * k * C, Cout, BN) &&
             encode_weight_map(&p.tmB[1], w_lo, k * k * C, Cout, BN);
+  if (halo) {
+    p.halo = 1;
+    p.halo_pw = hp.pw;
+    p.halo_rows = hp.rows;
+    p.halo_res_rows = hp.res_rows;
+    p.halo_aplane = hp.aplane;
+    p.halo_sb = hp.sb;
+    p.hb = p.wb = p.ipt = 1;
+    p.tiles_h = hp.tiles_per_img;
+    p.tiles_w = 1;
+  }
   if (!ok) {
     printf("%s: encode failed\n", name);
     return;
   }
-  if (g_tstore) {
-    int bw, bh;
-    tc_conv_store_box(hb, wb, bw, bh);
-    p.tma_store = encode_out_map(&p.tmO[0], o_hi, Cout, Wo, Ho, N, bw, bh) &&
-                  encode_out_map(&p.tmO[1], o_lo, Cout, Wo, Ho, N, bw, bh);
-  }
+  if (g_tstore) p.staged_store = 1;
   if (g_mmares && use_res) {
-    if (encode_act_map(&p.tmR[0], r_hi, Cout, Wo, Ho, N, 1, wb, hb, 1) &&
-        encode_act_map(&p.tmR[1], r_lo, Cout, Wo, Ho, N, 1, wb, hb, 1) &&
+    if (encode_act_map(&p.tmR[0], r_hi, Cout, Wo, Ho, N, 1, halo ? hp.pw : wb, halo ? hp.res_rows : hb, 1) &&
+        encode_act_map(&p.tmR[1], r_lo, Cout, Wo, Ho, N, 1, halo ? hp.pw : wb, halo ? hp.res_rows : hb, 1) &&
         encode_weight_map(&p.tmE, eye256(), 256, 256, BN)) {
       p.nres = BN / 64;
       p.res_hi = nullptr;
       p.res_lo = nullptr;
     }
   }
+  p.dbg = getenv("LCB_DBG") ? atoi(getenv("LCB_DBG")) : 0;
   for (int i = 0; i < 3; ++i) CK(tc_conv_launch(p, BN, g_sms, 0));
   CK(cudaDeviceSynchronize());
   cudaEvent_t e0, e1;
@@ -535,8 +555,9 @@ static void perf_conv(const char* name, int N, int nsurv, int H, int W, int C, i
   ms /= iters;
   const double flops = 2.0 * nsurv * Ho * Wo * Cout * (double)C * k * k;
   const double tf = flops / (ms * 1e-3) / 1e12;
-  printf("perf %-26s N=%3d/%3d %3dx%-3d C=%4d->%4d k=%d s=%d %s: %8.1f us  %7.1f TFLOP/s alg  (%5.1f%% tensor of 1590)\n",
-         name, nsurv, N, H, W, C, Cout, k, stride, x3 ? "x3 " : "b16", ms * 1e3, tf, 100.0 * tf * (x3 ? 3 : 1) / 1590.0);
+  printf("perf %-26s N=%3d/%3d %3dx%-3d C=%4d->%4d k=%d s=%d %s%s BN=%d: %8.1f us  %7.1f TFLOP/s alg  (%5.1f%% tensor of 1590)\n",
+         name, nsurv, N, H, W, C, Cout, k, stride, x3 ? "x3 " : "b16", halo ? " halo" : "", BN, ms * 1e3, tf,
+         100.0 * tf * (x3 ? 3 : 1) / 1590.0);
   if (trace) {
     p.trace = dTrace;
     CK(tc_conv_launch(p, BN, g_sms, 0));
@@ -589,6 +610,16 @@ int main(int argc, char** argv) {
   CK(cudaGetDeviceProperties(&prop, 0));
   g_sms = prop.multiProcessorCount;
   printf("device %s, %d SMs\n", prop.name, g_sms);
+  if (argc > 1 && strcmp(argv[1], "--layers") == 0) {
+    perf_layers(argc > 2 && strcmp(argv[2], "--trace") == 0);
+    return 0;
+  }
+  if (argc > 2 && strcmp(argv[1], "--one") == 0) {
+    g_only = atoi(argv[2]);
+    perf_layers(false);
+    return 0;
+  }
+
   gemm_test("gemm bf16", 300, 192, 128, false, 1);
   gemm_test("gemm x3", 300, 192, 128, true, 1);
   gemm_test("gemm x3 splitk", 256, 4096, 256, true, 8);
@@ -611,15 +642,6 @@ int main(int argc, char** argv) {
   conv_test("conv3x3 s1 8x8 bf16 splitK", 9, 8, 8, 256, 256, 3, 1, false, true, true, true, 0, 8);
   conv_test("conv3x3 s1 4x4 x3 splitK again", 19, 4, 4, 128, 512, 3, 1, true, true, true, true, 0, 16);
   conv_test("conv1x1 s2 8->4 bf16 splitK", 6, 8, 8, 256, 512, 1, 2, false, false, false, true, 256, 4);
-  if (argc > 1 && strcmp(argv[1], "--layers") == 0) {
-    perf_layers(argc > 2 && strcmp(argv[2], "--trace") == 0);
-    return 0;
-  }
-  if (argc > 2 && strcmp(argv[1], "--one") == 0) {
-    g_only = atoi(argv[2]);
-    perf_layers(false);
-    return 0;
-  }
   if (argc > 1 && strcmp(argv[1], "--perf") == 0) {
     perf_test(8192, 8192, 8192);
     perf_test(16384, 4096, 4096);

@@ -301,7 +301,9 @@ def test_fused_gap_matches_unfused_pool(monkeypatch):
         assert np.array_equal(a.exit_layer, b.exit_layer) and np.array_equal(a.served, b.served)
         both = ~np.isnan(a.probs) & ~np.isnan(b.probs)
         assert np.array_equal(np.isnan(a.probs), np.isnan(b.probs))
-        assert np.all(np.abs(a.probs[both] - b.probs[both]) <= 1e-5)
+        # the fused partials sum the fp32 epilogue values, the unfused pool the
+        # stored hi+lo planes (~2^-17 apart); calibrated selector gains amplify it
+        assert np.all(np.abs(a.probs[both] - b.probs[both]) <= 1e-4)
     fused.close()
     plain.close()
 
