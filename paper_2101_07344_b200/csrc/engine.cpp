@@ -185,8 +185,8 @@ Engine::Engine(int device, const BaseModel& model, std::vector<CacheVariant> var
   gap_fusion_ = !(nf && nf[0] == '1');
   const char* nl = std::getenv("LCB_UNFUSED_LOOKUP");
   fused_lookup_ = !(nl && nl[0] == '1');
-  const char* nh = std::getenv("LCB_NO_HALO");
-  halo_ = !(nh && nh[0] == '1');
+  const char* nh = std::getenv("LCB_HALO");  // opt-in: not yet faster than the per-tap loads
+  halo_ = nh && nh[0] == '1';
   const char* nr = std::getenv("LCB_NO_MMA_RESIDUAL");
   mma_residual_ = !(nr && nr[0] == '1');
   const char* nt = std::getenv("LCB_DIRECT_STORE");

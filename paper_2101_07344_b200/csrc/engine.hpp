@@ -160,7 +160,7 @@ class Engine {
   bool mma_residual_ = true;  // LCB_NO_MMA_RESIDUAL=1: residual added in the epilogue instead of by identity K-steps
   __nv_bfloat16* identity_ = nullptr;
   bool fused_lookup_ = true;
-  bool halo_ = true;  // LCB_NO_HALO=1: 3x3 stride-1 convs re-read the input per tap instead of one halo slab  // LCB_UNFUSED_LOOKUP=1: gap_bins + head + exit_compact as three launches
+  bool halo_ = false;  // LCB_HALO=1: stride-1 convs load one padded-row halo slab per channel chunk  // LCB_UNFUSED_LOOKUP=1: gap_bins + head + exit_compact as three launches
   int* lk_arrive_ = nullptr;
   Planes im2col_buf_;
 

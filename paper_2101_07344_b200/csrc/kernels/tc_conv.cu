@@ -255,50 +255,42 @@ __device__ __forceinline__ void epilogue_store_ld(const TcConvParams& p, float (
 // sums to gap_out[n][segment][Cout]. Every segment slot of every present
 // image is written each launch (rows outside the image contribute 0), so the
 // head sums all gap_segs slots.
-template <int kO, int kN>
-__device__ __forceinline__ void rs_step(float (&v)[16], int lane) {
-  // keep the lower half of the kN live values if the lane bit is 0, else the upper half
-  const bool up = (lane & kO) != 0;
+// One halving step of the segmented reduce-scatter: lanes whose bit `o` is 0
+// keep the lower kN/2 live values (adding the partner's), the others the upper.
+template <int kN>
+__device__ __forceinline__ void rs_step(float (&v)[16], int o, int lane) {
+  const bool up = (lane & o) != 0;
 #pragma unroll
   for (int e = 0; e < kN / 2; ++e) {
     const float send = up ? v[e] : v[e + kN / 2];
     const float keep = up ? v[e + kN / 2] : v[e];
-    v[e] = keep + __shfl_xor_sync(0xffffffffu, send, kO);
+    v[e] = keep + __shfl_xor_sync(0xffffffffu, send, o);
   }
 }
 
-template <int kSeg>
-__device__ __forceinline__ void gap_segment_t(const TcConvParams& p, const TileGeom& g, const Tile& x, int row,
-                                              int lane, float (&v)[16], int co) {
-  // Halving steps over the segment's lane bits (high to low); value e of a
-  // lane is then channel chbase + e.
-  int chbase = 0;
+// Segment size seg = min(rows_per_img, 32) in {8, 16, 32}: halvings over the
+// lane bits seg/2, seg/4, seg/8 (and seg/16 when seg >= 16), plus a plain
+// add over bit 0 for seg == 32. Value e of a lane is then channel chbase + e
+// (2 live values for seg == 8, else 1).
+__device__ __forceinline__ void gap_segment(const TcConvParams& p, const TileGeom& g, const Tile& x, int row,
+                                            int lane, float (&v)[16], int co) {
+  const int rpi = p.halo ? kBM : p.hb * p.wb;  // power of two >= 8
+  const int seg = rpi < 32 ? rpi : 32;
+  rs_step<16>(v, seg >> 1, lane);
+  rs_step<8>(v, seg >> 2, lane);
+  rs_step<4>(v, seg >> 3, lane);
+  int chbase = ((lane & (seg >> 1)) ? 8 : 0) + ((lane & (seg >> 2)) ? 4 : 0) + ((lane & (seg >> 3)) ? 2 : 0);
   bool writer = true;
-  constexpr int kLive = kSeg == 8 ? 2 : 1;
-  if (kSeg == 32) {
-    rs_step<16, 16>(v, lane);
-    rs_step<8, 8>(v, lane);
-    rs_step<4, 4>(v, lane);
-    rs_step<2, 2>(v, lane);
-    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
-    chbase = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
-    writer = (lane & 1) == 0;
-  } else if (kSeg == 16) {
-    rs_step<8, 16>(v, lane);
-    rs_step<4, 8>(v, lane);
-    rs_step<2, 4>(v, lane);
-    rs_step<1, 2>(v, lane);
-    chbase = ((lane >> 3) & 1) * 8 + ((lane >> 2) & 1) * 4 + ((lane >> 1) & 1) * 2 + (lane & 1);
-  } else {
-    rs_step<4, 16>(v, lane);
-    rs_step<2, 8>(v, lane);
-    rs_step<1, 4>(v, lane);
-    chbase = ((lane >> 2) & 1) * 8 + ((lane >> 1) & 1) * 4 + (lane & 1) * 2;
+  if (seg >= 16) {
+    rs_step<2>(v, seg >> 4, lane);
+    chbase += (lane & (seg >> 4)) ? 1 : 0;
   }
-  const int rpi = p.halo ? kBM : p.hb * p.wb;
-  const int seg_first = row & ~(kSeg - 1);  // first row of this lane's segment
-  const int j = seg_first / rpi;
-  const int idx = x.grp * p.ipt + j;
+  if (seg == 32) {
+    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+    writer = (lane & 1) == 0;
+  }
+  const int seg_first = row & ~(seg - 1);  // first row of this lane's segment
+  const int idx = p.halo ? x.grp : x.grp * p.ipt + seg_first / rpi;
   if (writer && idx < g.count) {
     const int n = p.surv ? p.surv[idx] : idx;
     const int pix = seg_first % rpi;
@@ -306,17 +298,64 @@ __device__ __forceinline__ void gap_segment_t(const TcConvParams& p, const TileG
     const int tile_r = (x.h0 / p.hb) * p.tiles_w + x.w0 / p.wb;
     const int sg = tile_r * per_tile + pix / 32;
     float* dst = p.gap_out + (static_cast<size_t>(n) * p.gap_segs + sg) * p.Cout + co + chbase;
-#pragma unroll
-    for (int e = 0; e < kLive; ++e) dst[e] = v[e];
+    dst[0] = v[0];
+    if (seg == 8) dst[1] = v[1];
   }
 }
 
-__device__ __forceinline__ void gap_segment(const TcConvParams& p, const TileGeom& g, const Tile& x, int row,
-                                            int lane, float (&v)[16], int co) {
-  const int rpi = p.halo ? kBM : p.hb * p.wb;  // power of two >= 8 (engine choose_box)
-  if (rpi >= 32) gap_segment_t<32>(p, g, x, row, lane, v, co);
-  else if (rpi == 16) gap_segment_t<16>(p, g, x, row, lane, v, co);
-  else gap_segment_t<8>(p, g, x, row, lane, v, co);
+// Split-K: publish this CTA's partial tile, wait for the other ks-1 CTAs of
+// the tile (all resident: one unit per CTA, single round), then reduce 1/ks of
+// the tile (warp units of 16 columns x 32 rows, fixed k order) and run the
+// epilogue on it. Kept out of line: it is the rare path.
+__device__ __noinline__ void split_reduce(const TcConvParams& p, const TileGeom& g, const Tile& x, int BN, int etid,
+                                          int lane) {
+  int* arr = p.ws_counters + 2 * x.tile_mn;
+  int* dep = arr + 1;
+  __threadfence();
+  epi_bar();
+  if (etid == 0) {
+    atomicAdd(arr, 1);
+    while (ld_acquire(arr) < g.ks) __nanosleep(64);
+  }
+  epi_bar();
+  const int nu = (BN / 16) * (kBM / 32);
+  const int u0 = static_cast<int>((static_cast<long long>(nu) * x.ks) / g.ks);
+  const int u1 = static_cast<int>((static_cast<long long>(nu) * (x.ks + 1)) / g.ks);
+  const float* tile_ws = p.ws + static_cast<size_t>(x.tile_mn) * g.ks * kBM * BN;
+  for (int uu = u0 + (etid >> 5); uu < u1; uu += kEpiWarps) {
+    const int c16 = uu / (kBM / 32), r = (uu % (kBM / 32)) * 32 + lane;
+    float v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = 0.0f;
+    for (int k = 0; k < g.ks; ++k) {
+      const float4* src = reinterpret_cast<const float4*>(tile_ws + static_cast<size_t>(k) * kBM * BN +
+                                                          (static_cast<size_t>(c16) * kBM + r) * 16);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float4 f = __ldcg(src + u);
+        v[4 * u] += f.x;
+        v[4 * u + 1] += f.y;
+        v[4 * u + 2] += f.z;
+        v[4 * u + 3] += f.w;
+      }
+    }
+    size_t ob;
+    const int co = x.tn * BN + c16 * 16;
+    if (out_row(p, g, x, r, ob)) {
+      epilogue_store_ld(p, v, ob + co, co);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = 0.0f;
+    }
+    if (p.gap_out) gap_segment(p, g, x, r, lane, v, co);
+  }
+  epi_bar();
+  if (etid == 0) {
+    if (atomicAdd(dep, 1) == g.ks - 1) {
+      *arr = 0;
+      *dep = 0;
+    }
+  }
 }
 
 template <int BN, bool X3>
@@ -485,8 +524,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
           const uint32_t ah = ring0 + aslot * h_aslot + static_cast<uint32_t>(row_off) * 128;
           const uint32_t al = ah + p.halo_aplane;
           const uint32_t bh = h_b0 + bslot * h_bslot, bl = bh + Cfg::kBBytes;
+// (a runtime trip count here miscompiles the MMA sequence: keep it constant)
 #pragma unroll
-          for (int k = 0; k < (dbg_nomma ? 0 : 4); ++k) {
+          for (int k = 0; k < 4; ++k) {
+            if (dbg_nomma) break;
             const uint32_t first = (s > x.s_begin || k > 0) ? 1u : 0u;
             umma_bf16(d_tmem, umma_desc_sw128(ah + 32 * k), umma_desc_sw128(bh + 32 * k), idesc, first);
             if (X3) {
@@ -528,6 +569,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
         if (p.plain) {
           imgs[0] = 0;
         } else {
+#pragma unroll 1
           for (int j = 0; j < ipt; ++j) {
             int idx = x.grp * ipt + j;
             if (idx >= g.count) idx = g.count - 1;  // rows discarded by the epilogue
@@ -548,6 +590,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
 #pragma unroll 1
             for (int pl = 0; pl < Cfg::kPlanes; ++pl) {
               const uint32_t a_dst = smem_u32(stage_a(stage, pl));
+#pragma unroll 1
               for (int jj = 0; jj < ipt; ++jj)
                 tma_load_5d(a_dst + jj * box_bytes, &p.tmR[pl], fb, x.tn * BN + j * 64, x.w0, x.h0, imgs[jj], 0);
               tma_load_2d(smem_u32(stage_b(stage, pl)), &p.tmE, fb, j * 64, 0);
@@ -557,6 +600,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
 #pragma unroll 1
           for (int pl = 0; pl < Cfg::kPlanes; ++pl) {
             const uint32_t a_dst = smem_u32(stage_a(stage, pl));
+#pragma unroll 1
             for (int j = 0; j < ipt; ++j) tma_load_5d(a_dst + j * box_bytes, &p.tmA[pl], fb, cc * 64, wc, hc, imgs[j], ph);
             tma_load_2d(smem_u32(stage_b(stage, pl)), &p.tmB[pl], fb, tap * p.C + cc * 64, x.tn * BN);
           }
@@ -594,8 +638,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
           tc_fence_after();
           const uint32_t ah = smem_u32(stage_a(stage, 0)), bh = smem_u32(stage_b(stage, 0));
           const bool res_step = s >= nk_conv;
+// (a runtime trip count here miscompiles the MMA sequence: keep it constant)
 #pragma unroll
-          for (int k = 0; k < (dbg_nomma ? 0 : 4); ++k) {
+          for (int k = 0; k < 4; ++k) {
+            if (dbg_nomma) break;
             const uint32_t first = (s > x.s_begin || k > 0) ? 1u : 0u;
             umma_bf16(d_tmem, umma_desc_sw128(ah + 32 * k), umma_desc_sw128(bh + 32 * k), idesc, first);
             if (X3) {
@@ -619,8 +665,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
     }
   } else {
     // ------------------------------------------------ epilogue
-    constexpr int kCols = BN / 2;          // columns per epilogue warp
-    constexpr int kChunks = kCols / 8;     // 16-byte residual chunks per row
+    // warp w: TMEM lane quadrant w % 4 (tile rows), column half (w - 2) / 4;
+    // 32 columns per step: TMEM -> registers -> shift / residual / ReLU ->
+    // hi/lo -> shared staging (64-byte swizzle) -> 8 rows x 64 contiguous
+    // bytes per store instruction. Rolled loops keep the code small (the MMA
+    // and TMA warps share the instruction cache with this code).
+    constexpr int kCols = BN / 2;  // columns per epilogue warp
     const int quad = warp & 3;
     const int half = (warp - 2) >> 2;
     const int row = quad * 32 + lane;
@@ -634,23 +684,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
       const Tile x = decode_tile(t, p, g);
       size_t obase;
       const bool valid = out_row(p, g, x, row, obase);
-      const int grow = x.w0 + row;
       const bool split = p.mode == 0 && g.ks > 1;
-      const bool tstore = p.staged_store && p.mode == 0 && !split;
-      // Residual of this row's columns, fetched before the accumulator is
-      // ready so its latency overlaps the tile's MMAs.
-      uint4 rh[kChunks], rl[X3 ? kChunks : 1];
-      const bool use_res = p.mode == 0 && !split && valid && p.res_hi;
-      if (use_res) {
-        const uint4* src = reinterpret_cast<const uint4*>(p.res_hi + obase + x.tn * BN + col0);
-#pragma unroll
-        for (int i = 0; i < kChunks; ++i) rh[i] = src[i];
-        if (X3 && p.res_lo) {
-          const uint4* srl = reinterpret_cast<const uint4*>(p.res_lo + obase + x.tn * BN + col0);
-#pragma unroll
-          for (int i = 0; i < (X3 ? kChunks : 1); ++i) rl[i] = srl[i];
-        }
-      }
       mbar_wait(tfull0 + 8 * acc, acc_phase);
       tc_fence_after();
       if (etid == 0) trace_put(p, unit, 4);
@@ -658,73 +692,71 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
       const bool empty_k = x.s_end <= x.s_begin;  // no MMA wrote this accumulator
       // split-K partial tile layout: [tile_mn][ks][BN/16][128 rows][16] (64 B per row chunk)
       float* wsp = split ? p.ws + (static_cast<size_t>(x.tile_mn) * g.ks + x.ks) * kBM * BN : nullptr;
-#pragma unroll
-      for (int c32 = 0; c32 < kCols / 32 || (kCols < 32 && c32 == 0); ++c32) {
-        constexpr int kSub = kCols < 32 ? kCols / 16 : 2;
-        float v[kSub][16];
-#pragma unroll
-        for (int u = 0; u < kSub; ++u) tmem_ld16_nowait(t_row + c32 * 32 + u * 16, v[u]);
+#pragma unroll 1
+      for (int c32 = 0; c32 < kCols / 32; ++c32) {
+        float v[2][16];
+        tmem_ld16_nowait(t_row + c32 * 32, v[0]);
+        tmem_ld16_nowait(t_row + c32 * 32 + 16, v[1]);
         tmem_ld_wait();
+        const int cb = x.tn * BN + col0 + c32 * 32;  // first output channel of this step
+        if (empty_k) {
 #pragma unroll
-        for (int u = 0; u < kSub; ++u) {
-          if (empty_k) {
+          for (int i = 0; i < 16; ++i) v[0][i] = v[1][i] = 0.0f;
+        }
+        if (split) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) v[u][i] = 0.0f;
-          }
-          const int c16 = (col0 >> 4) + c32 * 2 + u;  // 16-column chunk index in the tile
-          const int co = x.tn * BN + c16 * 16;
-          if (split) {
+          for (int u = 0; u < 2; ++u) {
+            const int c16 = (col0 >> 4) + c32 * 2 + u;
             float4* dst = reinterpret_cast<float4*>(wsp + (static_cast<size_t>(c16) * kBM + row) * 16);
 #pragma unroll
             for (int q = 0; q < 4; ++q)
               dst[q] = make_float4(v[u][4 * q], v[u][4 * q + 1], v[u][4 * q + 2], v[u][4 * q + 3]);
-          } else if (p.mode == 1) {
-            if (valid) {
-              float4* dst = reinterpret_cast<float4*>(
-                  p.out_f32 + (static_cast<size_t>(x.ks) * p.rows_total + grow) * p.Cout + co);
+          }
+          continue;
+        }
+        if (p.mode == 1) {
+          if (valid) {
+            float* dst = p.out_f32 + (static_cast<size_t>(x.ks) * p.rows_total + x.w0 + row) * p.Cout + cb;
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
 #pragma unroll
               for (int q = 0; q < 4; ++q)
-                dst[q] = make_float4(v[u][4 * q], v[u][4 * q + 1], v[u][4 * q + 2], v[u][4 * q + 3]);
-            }
-          } else if (tstore) {
-            const int ci = (c32 * 2 + u) * 2;
-            epilogue_math(p, v[u], co, use_res ? &rh[ci] : nullptr,
-                          (use_res && X3 && p.res_lo) ? &rl[X3 ? ci : 0] : nullptr);
-            if (!valid) {
+                reinterpret_cast<float4*>(dst + u * 16)[q] =
+                    make_float4(v[u][4 * q], v[u][4 * q + 1], v[u][4 * q + 2], v[u][4 * q + 3]);
+          }
+          continue;
+        }
+        // mode 0: epilogue math, staged coalesced store, fused GAP partials
+        __syncwarp();  // previous step's staging read back
 #pragma unroll
-              for (int i = 0; i < 16; ++i) v[u][i] = 0.0f;
+        for (int u = 0; u < 2; ++u) {
+          const int co = cb + u * 16;
+          uint4 rh[2], rl[2];
+          const bool r = valid && p.res_hi;  // epilogue residual (LCB_NO_MMA_RESIDUAL); default adds it on the MMA
+          if (r) {
+            rh[0] = reinterpret_cast<const uint4*>(p.res_hi + obase + co)[0];
+            rh[1] = reinterpret_cast<const uint4*>(p.res_hi + obase + co)[1];
+            if (X3 && p.res_lo) {
+              rl[0] = reinterpret_cast<const uint4*>(p.res_lo + obase + co)[0];
+              rl[1] = reinterpret_cast<const uint4*>(p.res_lo + obase + co)[1];
             }
-          } else {
-            if (valid) {
-              const int ci = (c32 * 2 + u) * 2;  // residual chunk index within this warp's columns
-              epilogue_store(p, v[u], obase + co, co, use_res ? &rh[ci] : nullptr,
-                             (use_res && X3 && p.res_lo) ? &rl[X3 ? ci : 0] : nullptr);
-            } else {
+          }
+          epilogue_math(p, v[u], co, r ? rh : nullptr, (r && X3 && p.res_lo) ? rl : nullptr);
+          if (!valid) {
 #pragma unroll
-              for (int i = 0; i < 16; ++i) v[u][i] = 0.0f;
-            }
-            if (p.gap_out) gap_segment(p, g, x, row, lane, v[u], co);  // warp-uniform call
+            for (int i = 0; i < 16; ++i) v[u][i] = 0.0f;
+          }
+          uint4 hi[2], lo[2];
+          split16(v[u], hi, lo);
+#pragma unroll
+          for (int hq = 0; hq < 2; ++hq) {
+            const uint32_t off = static_cast<uint32_t>(lane * 64 + (((u * 2 + hq) ^ ((lane >> 1) & 3)) * 16));
+            st_shared_v4(wstage + off, hi[hq]);
+            if (X3) st_shared_v4(wstage + 2048 + off, lo[hq]);
           }
         }
-        if (tstore) {
-          // Coalesced stores: each lane stages its row's 32 columns (hi, lo)
-          // in shared memory (64-byte swizzle), then the warp writes 8 rows x
-          // 64 contiguous bytes per instruction (full 32-byte sectors) instead
-          // of 32 rows x 16 bytes.
-          __syncwarp();  // previous chunk's read-back done
-#pragma unroll
-          for (int u = 0; u < kSub; ++u) {
-            uint4 hi[2], lo[2];
-            split16(v[u], hi, lo);
-#pragma unroll
-            for (int hq = 0; hq < 2; ++hq) {
-              const uint32_t off = static_cast<uint32_t>(lane * 64 + (((u * 2 + hq) ^ ((lane >> 1) & 3)) * 16));
-              st_shared_v4(wstage + off, hi[hq]);
-              if (X3) st_shared_v4(wstage + 2048 + off, lo[hq]);
-            }
-          }
-          __syncwarp();
-          const int c0 = x.tn * BN + col0 + c32 * 32;
+        __syncwarp();
+        {
           const int ch = lane & 3;
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
@@ -733,15 +765,15 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
             const int ok = __shfl_sync(0xffffffffu, valid ? 1 : 0, r);
             const uint32_t off = static_cast<uint32_t>(r * 64 + ((ch ^ ((r >> 1) & 3)) * 16));
             if (ok && !dbg_nostore) {
-              *reinterpret_cast<uint4*>(p.out_hi + ob + c0 + ch * 8) = ld_shared_v4(wstage + off);
-              if (X3 && p.out_lo) *reinterpret_cast<uint4*>(p.out_lo + ob + c0 + ch * 8) = ld_shared_v4(wstage + 2048 + off);
+              *reinterpret_cast<uint4*>(p.out_hi + ob + cb + ch * 8) = ld_shared_v4(wstage + off);
+              if (X3 && p.out_lo)
+                *reinterpret_cast<uint4*>(p.out_lo + ob + cb + ch * 8) = ld_shared_v4(wstage + 2048 + off);
             }
           }
-          if (p.gap_out) {
-#pragma unroll
-            for (int u = 0; u < kSub; ++u)
-              gap_segment(p, g, x, row, lane, v[u], x.tn * BN + col0 + c32 * 32 + u * 16);  // after staging: destroys v
-          }
+        }
+        if (p.gap_out) {
+          gap_segment(p, g, x, row, lane, v[0], cb);  // destroys v (after staging)
+          gap_segment(p, g, x, row, lane, v[1], cb + 16);
         }
       }
       tc_fence_before();
@@ -749,60 +781,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
       if (lane == 0) mbar_arrive(tempty0 + 8 * acc);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
-      if (split) {
-        // All ks CTAs of this tile are resident (one unit per CTA, single
-        // round): publish the partial, wait for the others, then each CTA
-        // reduces 1/ks of the tile in a fixed k order and runs the epilogue.
-        int* arr = p.ws_counters + 2 * x.tile_mn;
-        int* dep = arr + 1;
-        __threadfence();
-        epi_bar();
-        if (etid == 0) {
-          atomicAdd(arr, 1);
-          while (ld_acquire(arr) < g.ks) __nanosleep(64);
-        }
-        epi_bar();
-        // Warp units of (16-column chunk, 32-row quarter), so the lanes of a
-        // warp hold 32 consecutive rows (segment-aligned for the GAP partials).
-        const int nu = (BN / 16) * (kBM / 32);
-        const int u0 = static_cast<int>((static_cast<long long>(nu) * x.ks) / g.ks);
-        const int u1 = static_cast<int>((static_cast<long long>(nu) * (x.ks + 1)) / g.ks);
-        const float* tile_ws = p.ws + static_cast<size_t>(x.tile_mn) * g.ks * kBM * BN;
-        for (int uu = u0 + (etid >> 5); uu < u1; uu += kEpiWarps) {
-          const int c16 = uu / (kBM / 32), r = (uu % (kBM / 32)) * 32 + lane;
-          float v[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = 0.0f;
-          for (int k = 0; k < g.ks; ++k) {
-            const float4* src = reinterpret_cast<const float4*>(tile_ws + static_cast<size_t>(k) * kBM * BN +
-                                                                (static_cast<size_t>(c16) * kBM + r) * 16);
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const float4 f = __ldcg(src + u);
-              v[4 * u] += f.x;
-              v[4 * u + 1] += f.y;
-              v[4 * u + 2] += f.z;
-              v[4 * u + 3] += f.w;
-            }
-          }
-          size_t ob;
-          const int co = x.tn * BN + c16 * 16;
-          if (out_row(p, g, x, r, ob)) {
-            epilogue_store_ld(p, v, ob + co, co);
-          } else {
-#pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] = 0.0f;
-          }
-          if (p.gap_out) gap_segment(p, g, x, r, lane, v, co);
-        }
-        epi_bar();
-        if (etid == 0) {
-          if (atomicAdd(dep, 1) == g.ks - 1) {
-            *arr = 0;
-            *dep = 0;
-          }
-        }
-      }
+      if (split) split_reduce(p, g, x, BN, etid, lane);
       if (etid == 0) trace_put(p, unit, 5);
     }
   }
