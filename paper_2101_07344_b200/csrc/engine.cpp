@@ -432,13 +432,19 @@ void Engine::build_weights() {
 
 // ------------------------------------------------------------------ lookups
 void Engine::add_lookup_steps(std::vector<Step>& steps, DevCache& c, const TapView& tap, int max_rows,
-                              bool stage_gather, bool fused_gap) {
+                              bool stage_gather, bool fused_gap, const ExitParams* ex) {
   DevCache* cp = &c;
   const long long L2 = model_.num_blocks + 2;
   const int cidx = (tap.count >= d_counts_ && tap.count < d_counts_ + L2) ? static_cast<int>(tap.count - d_counts_) : -1;
   const double eb = prec_ == kPrecX3 ? 4.0 : 2.0;  // bytes per activation element (hi + lo planes)
   const double tap_bytes = static_cast<double>(c.D) * eb;
-  if (c.family == 1 && fused_gap && c.gap) {
+  // Pool(C) with <= 32 classes: the head itself sums the conv's fused GAP partials.
+  const bool head_gap = c.family == 1 && fused_gap && c.gap && fused_lookup_ &&
+                        fused_lookup_supported(c.classes, c.width, max_rows);
+  double head_bytes = 0.0;  // per surviving row, beyond the (L2-resident) head weights
+  if (head_gap) {
+    head_bytes = 4.0 * c.gap_segs * c.width;
+  } else if (c.family == 1 && fused_gap && c.gap) {
     steps.push_back({[cp, tap, max_rows](cudaStream_t s) {
                        launch_gap_bins(cp->gap, cp->gap_segs, tap.C, tap.HW, tap.data_idx, tap.count, max_rows,
                                        cp->feats, s);
@@ -505,7 +511,9 @@ void Engine::add_lookup_steps(std::vector<Step>& steps, DevCache& c, const TapVi
                      1, cidx, 2.0 * static_cast<double>(c.D) * c.h, tap_bytes});
   }
   const int rows_total = max_rows;
-  steps.push_back({[cp, tap, max_rows, rows_total](cudaStream_t s) {
+  const ExitParams exv = ex ? *ex : ExitParams{};
+  const float gap_inv = head_gap ? static_cast<float>(1.0 / tap.HW) : 0.0f;
+  steps.push_back({[cp, tap, max_rows, rows_total, exv, head_gap, gap_inv](cudaStream_t s) {
                      CacheHeadParams p{};
                      p.family = cp->family;
                      p.classes = cp->classes;
@@ -529,9 +537,33 @@ void Engine::add_lookup_steps(std::vector<Step>& steps, DevCache& c, const TapVi
                      p.pr_out = cp->pr_out;
                      p.logits_out = cp->logits_out;
                      p.fc_scratch = cp->fc_scratch;
+                     if (head_gap) {
+                       p.gap = cp->gap;
+                       p.gap_segs = cp->gap_segs;
+                       p.gap_inv = gap_inv;
+                       p.gap_ids = tap.data_idx;
+                     }
+                     p.ex = exv;
                      launch_cache_head(p, max_rows, s);
                    },
-                   2, (c.classes > 32 && c.family != 2) ? 2 : 1, cidx, 0.0, 0.0});
+                   2, (c.classes > 32 && c.family != 2) ? 2 : 1, cidx, 0.0, head_bytes});
+}
+
+ExitParams Engine::exit_params(int layer, bool shadow, const int* ids_in, int* ids_out, int* src_rows_out,
+                               int* count_out) {
+  ExitParams e{};
+  e.arrive = lk_arrive_;
+  e.layer = layer;
+  e.shadow = shadow ? 1 : 0;
+  e.ids_in = ids_in;
+  e.exit_layer = d_exit_;
+  e.served = d_served_;
+  e.exit_ns = d_exit_ns_;
+  e.probs_out = d_probs_ + static_cast<size_t>(layer - 1) * max_batch_;
+  e.ids_out = ids_out;
+  e.src_rows_out = src_rows_out;
+  e.count_out = count_out;
+  return e;
 }
 
 // ------------------------------------------------------------------ MLP serve
@@ -610,18 +642,11 @@ void Engine::build_mlp_steps(std::vector<Step>& steps, bool shadow) {
       tap.HW = 1;
       tap.data_idx = nullptr;
       tap.count = cur_count;
-      add_lookup_steps(steps, c, tap, B, false);
       int* ids_out = ids + static_cast<size_t>(layer) * B;
       int* src_out = src + static_cast<size_t>(layer) * B;
       int* cnt_out = counts + layer;
-      DevCache* cp = &c;
-      float* probs_out = d_probs_ + static_cast<size_t>(layer - 1) * B;
-      steps.push_back({[this, cp, layer, cur_count, cur_ids, ids_out, src_out, cnt_out, probs_out, shadow](cudaStream_t s) {
-                         launch_exit_compact(layer, cur_count, cur_ids, cp->hit, cp->label, cp->prob, d_exit_,
-                                             d_served_, d_exit_ns_, probs_out, ids_out, src_out, cnt_out, shadow ? 1 : 0,
-                                             s);
-                       },
-                       3});
+      const ExitParams ex = exit_params(layer, shadow, cur_ids, ids_out, src_out, cnt_out);
+      add_lookup_steps(steps, c, tap, B, false, false, &ex);
       if (!shadow) {
         Planes dst = mlp_cin_[static_cast<size_t>(b)];
         const long long row_elems = f.outp;
@@ -829,48 +854,6 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow) {
         const TapInfo& ti = model_.taps[static_cast<size_t>(o.tap)];
         int* ids_out = ids + static_cast<size_t>(layer) * B;
         int* cnt_out = counts + layer;
-        float* probs_out = d_probs_ + static_cast<size_t>(layer - 1) * B;
-        if (c.gap && c.family == 1 && fused_lookup_ && fused_lookup_supported(c.classes, c.width, B)) {
-          // one launch: GAP bins + head + first-hit exit + compaction
-          FusedLookupParams fp{};
-          fp.gap = c.gap;
-          fp.segs = c.gap_segs;
-          fp.C = c.width;
-          fp.classes = c.classes;
-          const TapInfo& tinf = model_.taps[static_cast<size_t>(o.tap)];
-          fp.inv = static_cast<float>(1.0 / (tinf.H * tinf.W));
-          fp.W2 = c.W2;
-          fp.b2 = c.b2;
-          fp.Ws1 = c.Ws1;
-          fp.bs1 = c.bs1;
-          fp.ws2 = c.ws2;
-          fp.layer = layer;
-          fp.shadow = shadow ? 1 : 0;
-          fp.count_in = cur_count;
-          fp.ids_in = cur_ids;
-          fp.prob = c.prob;
-          fp.hit = c.hit;
-          fp.label = c.label;
-          fp.arrive = lk_arrive_;
-          fp.exit_layer = d_exit_;
-          fp.served = d_served_;
-          fp.exit_ns = d_exit_ns_;
-          fp.probs_out = probs_out;
-          fp.ids_out = ids_out;
-          fp.count_out = cnt_out;
-          DevCache* cp = &c;
-          const int cidx = static_cast<int>(cur_count - d_counts_);
-          steps.push_back({[fp, cp, B](cudaStream_t s) {
-                             FusedLookupParams q = fp;
-                             q.bs2 = cp->bs2;  // selector output may be recalibrated after build
-                             q.delta = cp->delta;
-                             launch_gap_lookup_exit(q, B, s);
-                           },
-                           2, 1, cidx, 0.0, 4.0 * c.gap_segs * c.width});
-          cur_ids = ids_out;
-          cur_count = cnt_out;
-          continue;
-        }
         Planes tb = slot_buf_[static_cast<size_t>(o.out)];
         TapView tap;
         tap.hi = tb.hi;
@@ -880,14 +863,8 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow) {
         tap.HW = ti.H * ti.W;
         tap.data_idx = cur_ids;
         tap.count = cur_count;
-        add_lookup_steps(steps, c, tap, B, true, c.gap != nullptr);
-        DevCache* cp = &c;
-        steps.push_back({[this, cp, layer, cur_count, cur_ids, ids_out, cnt_out, probs_out, shadow](cudaStream_t s) {
-                           launch_exit_compact(layer, cur_count, cur_ids, cp->hit, cp->label, cp->prob, d_exit_,
-                                               d_served_, d_exit_ns_, probs_out, ids_out, nullptr, cnt_out,
-                                               shadow ? 1 : 0, s);
-                         },
-                         3});
+        const ExitParams ex = exit_params(layer, shadow, cur_ids, ids_out, nullptr, cnt_out);
+        add_lookup_steps(steps, c, tap, B, true, c.gap != nullptr, &ex);
         cur_ids = ids_out;
         cur_count = cnt_out;
       }

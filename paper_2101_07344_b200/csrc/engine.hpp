@@ -99,7 +99,8 @@ class Engine {
   void build_mlp_steps(std::vector<Step>& steps, bool shadow);
   void build_cnn_steps(std::vector<Step>& steps, bool shadow);
   void add_lookup_steps(std::vector<Step>& steps, DevCache& c, const TapView& tap, int max_rows, bool stage_gather,
-                        bool fused_gap = false);
+                        bool fused_gap = false, const ExitParams* ex = nullptr);
+  ExitParams exit_params(int layer, bool shadow, const int* ids_in, int* ids_out, int* src_rows_out, int* count_out);
   std::vector<Step>& steps_for(bool shadow);
   void* dalloc(size_t bytes);
   Planes alloc_planes(size_t elems);

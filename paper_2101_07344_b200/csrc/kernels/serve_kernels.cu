@@ -158,19 +158,158 @@ __global__ void pool_channels_kernel(TapView t, int gch, int width, float inv, f
   }
 }
 
-// Fused-GAP bins: bin c = (sum over the tap conv's segment partials, fixed
-// order) x 1/HW; the partials were written by tc_conv's epilogue.
-__global__ void gap_bins_kernel(const float* gap, int segs, int C, float inv, const int* data_idx, const int* count,
-                                float* bins) {
+// ------------------------------------------------------------------ GAP reductions
+// Lookup kernels run one CTA of kLk threads per request row; the reductions
+// below keep many independent 16-byte loads in flight per thread (the
+// surviving-row counts are small, so latency, not bandwidth, is the enemy)
+// and combine partial sums in a fixed order (deterministic).
+constexpr int kLk = 256;
+
+__device__ __forceinline__ void add4(float4& a, const float4 b) {
+  a.x += b.x;
+  a.y += b.y;
+  a.z += b.z;
+  a.w += b.w;
+}
+
+// feat[c] = inv * sum_seg src[seg][c] for one image's fused GAP partials
+// (tc_conv epilogue, [segs][C] fp32, C % 4 == 0). Thread layout: float4
+// column j, segment group g; 4 interleaved chains per thread, then the groups
+// in ascending order. red: kLk float4 of shared scratch. Ends with a barrier.
+__device__ void gap_feats_block(const float* __restrict__ src, int segs, int C, float inv, float* feat, float4* red) {
+  const int tid = threadIdx.x;
+  const int C4 = C >> 2;
+  const float4* s4 = reinterpret_cast<const float4*>(src);
+  if (C4 >= kLk) {
+    for (int j = tid; j < C4; j += kLk) {
+      float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
+      int sg = 0;
+      for (; sg + 4 <= segs; sg += 4) {
+        add4(a0, __ldg(s4 + static_cast<long long>(sg) * C4 + j));
+        add4(a1, __ldg(s4 + static_cast<long long>(sg + 1) * C4 + j));
+        add4(a2, __ldg(s4 + static_cast<long long>(sg + 2) * C4 + j));
+        add4(a3, __ldg(s4 + static_cast<long long>(sg + 3) * C4 + j));
+      }
+      for (; sg < segs; ++sg) add4(a0, __ldg(s4 + static_cast<long long>(sg) * C4 + j));
+      add4(a0, a1);
+      add4(a2, a3);
+      add4(a0, a2);
+      feat[4 * j] = a0.x * inv;
+      feat[4 * j + 1] = a0.y * inv;
+      feat[4 * j + 2] = a0.z * inv;
+      feat[4 * j + 3] = a0.w * inv;
+    }
+  } else {
+    const int G = kLk / C4;
+    const int j = tid % C4, g = tid / C4;
+    float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
+    if (g < G) {
+      int sg = g;
+      for (; sg + 3 * G < segs; sg += 4 * G) {
+        add4(a0, __ldg(s4 + static_cast<long long>(sg) * C4 + j));
+        add4(a1, __ldg(s4 + static_cast<long long>(sg + G) * C4 + j));
+        add4(a2, __ldg(s4 + static_cast<long long>(sg + 2 * G) * C4 + j));
+        add4(a3, __ldg(s4 + static_cast<long long>(sg + 3 * G) * C4 + j));
+      }
+      for (; sg < segs; sg += G) add4(a0, __ldg(s4 + static_cast<long long>(sg) * C4 + j));
+    }
+    add4(a0, a1);
+    add4(a2, a3);
+    add4(a0, a2);
+    red[tid] = a0;
+    __syncthreads();
+    if (tid < C4) {
+      float4 t = red[tid];
+      for (int q = 1; q < G; ++q) add4(t, red[q * C4 + tid]);
+      feat[4 * tid] = t.x * inv;
+      feat[4 * tid + 1] = t.y * inv;
+      feat[4 * tid + 2] = t.z * inv;
+      feat[4 * tid + 3] = t.w * inv;
+    }
+  }
+  __syncthreads();
+}
+
+// feat[c] = (1/HW) * sum_pixel tap[pixel][c] over one image's NHWC tap
+// (hi + lo bf16, C % 8 == 0): 8 channels per 16-byte load, pixel groups of
+// threads with 2 chains each, groups combined in ascending order. red: kLk*8
+// floats of shared scratch. Ends with a barrier.
+__device__ void tap_gap_block(const TapView& t, long long rowb, int C, int HW, float* feat, float* red) {
+  const int tid = threadIdx.x;
+  const int C8 = C >> 3;
+  const float inv = 1.0f / HW;
+  if (C8 >= kLk) {
+    for (int j = tid; j < C8; j += kLk) {
+      float a[8] = {0, 0, 0, 0, 0, 0, 0, 0}, b[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      int q = 0;
+      for (; q + 2 <= HW; q += 2) {
+        float v[8], w[8];
+        ld_tap8(t, rowb + static_cast<long long>(q) * C + 8 * j, v);
+        ld_tap8(t, rowb + static_cast<long long>(q + 1) * C + 8 * j, w);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          a[e] += v[e];
+          b[e] += w[e];
+        }
+      }
+      if (q < HW) {
+        float v[8];
+        ld_tap8(t, rowb + static_cast<long long>(q) * C + 8 * j, v);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) a[e] += v[e];
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) feat[8 * j + e] = (a[e] + b[e]) * inv;
+    }
+  } else {
+    const int G = kLk / C8;
+    const int j = tid % C8, g = tid / C8;
+    float a[8] = {0, 0, 0, 0, 0, 0, 0, 0}, b[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (g < G) {
+      int q = g;
+      for (; q + G < HW; q += 2 * G) {
+        float v[8], w[8];
+        ld_tap8(t, rowb + static_cast<long long>(q) * C + 8 * j, v);
+        ld_tap8(t, rowb + static_cast<long long>(q + G) * C + 8 * j, w);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          a[e] += v[e];
+          b[e] += w[e];
+        }
+      }
+      if (q < HW) {
+        float v[8];
+        ld_tap8(t, rowb + static_cast<long long>(q) * C + 8 * j, v);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) a[e] += v[e];
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) red[tid * 8 + e] = a[e] + b[e];
+    __syncthreads();
+    if (tid < C8) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        float s = red[tid * 8 + e];
+        for (int q = 1; q < G; ++q) s += red[(q * C8 + tid) * 8 + e];
+        feat[8 * tid + e] = s * inv;
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// Fused-GAP bins for heads that need them in global memory (classes > 32:
+// the batched logits GEMM reads them): bins[r][c], one CTA per row.
+__global__ void __launch_bounds__(kLk) gap_bins_kernel(const float* gap, int segs, int C, float inv,
+                                                       const int* data_idx, const int* count, float* bins) {
+  extern __shared__ float feat_s[];
+  __shared__ float4 red[kLk];
   const int r = blockIdx.x;
   if (r >= *count) return;
   const long long n = data_idx ? data_idx[r] : r;
-  const float* src = gap + n * segs * C;
-  for (int c = blockIdx.y * blockDim.x + threadIdx.x; c < C; c += gridDim.y * blockDim.x) {
-    float a = 0.0f;
-    for (int sg = 0; sg < segs; ++sg) a += src[static_cast<long long>(sg) * C + c];
-    bins[static_cast<long long>(r) * C + c] = a * inv;
-  }
+  gap_feats_block(gap + n * segs * C, segs, C, inv, feat_s, red);
+  for (int c = threadIdx.x; c < C; c += kLk) bins[static_cast<long long>(r) * C + c] = feat_s[c];
 }
 
 // Generic: one thread per bin, sequential over its flat window.
@@ -254,66 +393,114 @@ __global__ void conv1d_partials_kernel(TapView t, long long D, int kernel, int s
 // consumer adds b[k] + sum_z part[z][r][k] in ascending z (fixed order). A is
 // a dense fp32 [rows][feat] matrix (kMode 0) or the FC(h) cache hidden layer
 // relu(b1[o] + sum_s partials[s][r][o]) (kMode 1, split-K partials of the
-// tensor-core GEMM). Every 16-row tile reads its W slice once instead of
-// once per row: the logits GEMM of heads with many classes (ImageNet).
-constexpr int kFcBM = 16, kFcBN = 64, kFcBK = 32;
+// tensor-core GEMM). CTA tile 32 rows x 128 classes x 32-deep K chunks staged
+// in shared memory (k-major, so each thread's 4 rows and 4 classes are one
+// 16-byte load each); 4 x 4 register micro-tile per thread. Every row tile
+// reads its W slice once: the logits GEMM of heads with many classes.
+constexpr int kFcBM = 32, kFcBN = 128, kFcBK = 32;
+
+__host__ __device__ inline int rows_fc_slice(int feat) { return feat <= 512 ? 64 : (feat <= 1024 ? 128 : 256); }
 
 template <int kMode>
-__global__ void __launch_bounds__(256) rows_fc_kernel(const float* A, long long lda, int ks, long long part_stride,
-                                                      const float* b1, int feat, int kslice, const float* W,
-                                                      int classes, const int* count, long long max_rows, float* out) {
-  __shared__ float As[kFcBM][kFcBK + 1];
-  __shared__ float Ws[kFcBN][kFcBK + 1];
+__global__ void __launch_bounds__(256) rows_fc_kernel(const float* __restrict__ A, long long lda, int ks,
+                                                      long long part_stride, const float* __restrict__ b1, int feat,
+                                                      int kslice, const float* __restrict__ W, int classes,
+                                                      const int* count, long long max_rows, float* out) {
+  __shared__ __align__(16) float As[kFcBK][kFcBM + 4];
+  __shared__ __align__(16) float Ws[kFcBK][kFcBN + 4];
   const int n = *count;
   const int r0 = blockIdx.y * kFcBM, k0 = blockIdx.x * kFcBN;
   if (r0 >= n) return;
   const int z = blockIdx.z;
   const int oz0 = z * kslice, oz1 = oz0 + kslice < feat ? oz0 + kslice : feat;
   const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
-  float acc[2][2] = {{0.0f, 0.0f}, {0.0f, 0.0f}};
-  for (int o0 = oz0; o0 < oz1; o0 += kFcBK) {
+  const bool vec = (feat & 3) == 0 && (lda & 3) == 0;
+  float acc[4][4];
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const int idx = tid + i * 256, rr = idx >> 5, oo = idx & 31;
-      const int r = r0 + rr, o = o0 + oo;
-      float v = 0.0f;
-      if (r < n && o < oz1) {
-        if (kMode == 0) {
-          v = A[static_cast<long long>(r) * lda + o];
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
+  for (int o0 = oz0; o0 < oz1; o0 += kFcBK) {
+    {  // A tile: row tid/8, 4 consecutive o at (tid%8)*4
+      const int rr = tid >> 3, oo = (tid & 7) * 4;
+      const int r = r0 + rr;
+      float v[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+      if (r < n) {
+        if (vec && o0 + oo + 4 <= oz1) {
+          if (kMode == 0) {
+            const float4 f = __ldg(reinterpret_cast<const float4*>(A + static_cast<long long>(r) * lda + o0 + oo));
+            v[0] = f.x, v[1] = f.y, v[2] = f.z, v[3] = f.w;
+          } else {
+            const float4 bb = __ldg(reinterpret_cast<const float4*>(b1 + o0 + oo));
+            v[0] = bb.x, v[1] = bb.y, v[2] = bb.z, v[3] = bb.w;
+            for (int s = 0; s < ks; ++s) {
+              const float4 f = __ldg(reinterpret_cast<const float4*>(A + static_cast<long long>(s) * part_stride +
+                                                                     static_cast<long long>(r) * lda + o0 + oo));
+              v[0] += f.x, v[1] += f.y, v[2] += f.z, v[3] += f.w;
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) v[e] = v[e] > 0.0f ? v[e] : 0.0f;
+          }
         } else {
-          float a = b1[o];
-          for (int s = 0; s < ks; ++s) a += A[static_cast<long long>(s) * part_stride + static_cast<long long>(r) * lda + o];
-          v = a > 0.0f ? a : 0.0f;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int o = o0 + oo + e;
+            if (o < oz1) {
+              if (kMode == 0) {
+                v[e] = A[static_cast<long long>(r) * lda + o];
+              } else {
+                float a = b1[o];
+                for (int s = 0; s < ks; ++s)
+                  a += A[static_cast<long long>(s) * part_stride + static_cast<long long>(r) * lda + o];
+                v[e] = a > 0.0f ? a : 0.0f;
+              }
+            }
+          }
         }
       }
-      As[rr][oo] = v;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) As[oo + e][rr] = v[e];
     }
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int idx = tid + i * 256, kk = idx >> 5, oo = idx & 31;
-      const int k = k0 + kk, o = o0 + oo;
-      Ws[kk][oo] = (k < classes && o < oz1) ? W[static_cast<long long>(k) * feat + o] : 0.0f;
+    for (int i = 0; i < 4; ++i) {  // W tile: class (tid/8) + 32 i, 4 consecutive o
+      const int kk = (tid >> 3) + 32 * i, oo = (tid & 7) * 4;
+      const int k = k0 + kk;
+      float v[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+      if (k < classes) {
+        if (vec && o0 + oo + 4 <= oz1) {
+          const float4 f = __ldg(reinterpret_cast<const float4*>(W + static_cast<long long>(k) * feat + o0 + oo));
+          v[0] = f.x, v[1] = f.y, v[2] = f.z, v[3] = f.w;
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (o0 + oo + e < oz1) v[e] = W[static_cast<long long>(k) * feat + o0 + oo + e];
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) Ws[oo + e][kk] = v[e];
     }
     __syncthreads();
     const int olim = oz1 - o0 < kFcBK ? oz1 - o0 : kFcBK;
+#pragma unroll 4
     for (int o = 0; o < olim; ++o) {
-      const float a0 = As[2 * ty][o], a1 = As[2 * ty + 1][o];
-      const float w0 = Ws[tx][o], w1 = Ws[tx + 32][o];
-      acc[0][0] += a0 * w0;
-      acc[0][1] += a0 * w1;
-      acc[1][0] += a1 * w0;
-      acc[1][1] += a1 * w1;
+      const float4 a = *reinterpret_cast<const float4*>(&As[o][ty * 4]);
+      const float4 w = *reinterpret_cast<const float4*>(&Ws[o][tx * 4]);
+      const float av[4] = {a.x, a.y, a.z, a.w}, wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] += av[i] * wv[j];
     }
     __syncthreads();
   }
   float* outz = out + static_cast<long long>(z) * max_rows * classes;
 #pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const int r = r0 + 2 * ty + i;
+  for (int i = 0; i < 4; ++i) {
+    const int r = r0 + ty * 4 + i;
     if (r >= n) continue;
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int k = k0 + tx + 32 * j;
+    for (int j = 0; j < 4; ++j) {
+      const int k = k0 + tx * 4 + j;
       if (k < classes) outz[static_cast<long long>(r) * classes + k] = acc[i][j];
     }
   }
@@ -327,96 +514,69 @@ __device__ __forceinline__ float fc_logit(const float* part, int nz, long long z
 }
 
 // Global average pool of the surviving images' final activations (NHWC,
-// image ids[r]) -> feats [rows][C]; per channel a sequential pixel sum, then
-// x (1/HW) as the base head's GAP.
-__global__ void gap_rows_kernel(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int C, int HW, const int* ids,
-                                const int* count, float* feats) {
+// image ids[r]) -> feats [rows][C] (the base head's GAP), one CTA per row.
+__global__ void __launch_bounds__(kLk) gap_rows_kernel(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int C, int HW,
+                                                       const int* ids, const int* count, float* feats) {
+  extern __shared__ float feat_s[];
+  __shared__ float red[kLk * 8];
   const int r = blockIdx.x;
   if (r >= *count) return;
-  const long long n = ids[r];
   TapView t;
   t.hi = hi;
   t.lo = lo;
-  const float inv = 1.0f / HW;
-  for (int c = blockIdx.y * blockDim.x + threadIdx.x; c < C; c += gridDim.y * blockDim.x) {
-    float a = 0.0f;
-    for (int q = 0; q < HW; ++q) a += ld_tap(t, (n * HW + q) * C + c);
-    feats[static_cast<long long>(r) * C + c] = a * inv;
+  tap_gap_block(t, static_cast<long long>(ids[r]) * HW * C, C, HW, feat_s, red);
+  for (int c = threadIdx.x; c < C; c += kLk) feats[static_cast<long long>(r) * C + c] = feat_s[c];
+}
+
+// logits[k] = b[k] + W[k] . feat for k < classes: warp per class, lanes
+// strided over the features (4 independent chains), fixed combination order.
+__device__ void block_logits(const float* __restrict__ W, const float* __restrict__ b, int classes, int nf,
+                             const float* feat, float* logits) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int k = warp; k < classes; k += kLk / 32) {
+    const float* wr = W + static_cast<long long>(k) * nf;
+    float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
+    int o = lane;
+    for (; o + 96 < nf; o += 128) {
+      a0 += __ldg(wr + o) * feat[o];
+      a1 += __ldg(wr + o + 32) * feat[o + 32];
+      a2 += __ldg(wr + o + 64) * feat[o + 64];
+      a3 += __ldg(wr + o + 96) * feat[o + 96];
+    }
+    for (; o < nf; o += 32) a0 += __ldg(wr + o) * feat[o];
+    const float a = warp_sum((a0 + a1) + (a2 + a3));
+    if (lane == 0) logits[k] = a + b[k];
   }
 }
 
-// ------------------------------------------------------------------ head
-// Reference lookup (cache.cpp:259-265): pr = softmax(pred(tap)),
-// p = sigmoid(sel(pr)), hit = p >= delta (inclusive); label = argmax(pr).
-__global__ void cache_head_kernel(CacheHeadParams p) {
-  extern __shared__ float sm[];
-  __shared__ float red[32];
-  __shared__ float hsel[16];
-  __shared__ int best_idx_s[4];
-  __shared__ float best_val_s[4];
-  const int r = blockIdx.x;
-  if (r >= *p.count) return;
-  const int C = p.classes;
-  float* logits = sm;        // [C]
-  float* feat = sm + C;      // [feat]
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+// Shared scratch of one row's head.
+struct HeadSmem {
+  float red[32];
+  float hsel[16];
+  float bv[32];
+  int bi[32];
+};
 
-  if (p.pre_logits) {
-    for (int k = tid; k < C; k += blockDim.x) logits[k] = fc_logit(p.pre_logits, p.pre_nz, p.pre_zstride, p.b2, r, C, k);
-  } else if (p.family == 2) {
-    for (int k = tid; k < C; k += blockDim.x) {
-      float a = p.b2[k];
-      for (int c = 0; c < p.feat; ++c) a += p.feats[(static_cast<long long>(r) * p.feat + c) * C + k];
-      logits[k] = a;
-    }
-  } else {
-    if (p.family == 1) {
-      for (int o = tid; o < p.feat; o += blockDim.x) feat[o] = p.feats[static_cast<long long>(r) * p.feat + o];
-    } else {
-      for (int j = tid; j < p.feat; j += blockDim.x) {
-        float a = p.b1[j];
-        for (int s = 0; s < p.ks; ++s) a += p.feats[(static_cast<long long>(s) * p.rows_total + r) * p.hp + j];
-        feat[j] = a > 0.0f ? a : 0.0f;
-      }
-    }
-    __syncthreads();
-    for (int k = warp; k < C; k += nw) {
-      const float* wr = p.W2 + static_cast<long long>(k) * p.feat;
-      float a = 0.0f;
-      for (int o = lane; o < p.feat; o += 32) a += wr[o] * feat[o];
-      a = warp_sum(a);
-      if (lane == 0) logits[k] = a + p.b2[k];
-    }
-  }
-  __syncthreads();
-  // softmax (losses.cpp:35-46)
+// softmax(logits) (losses.cpp:35-46), selector FC(C,16)+ReLU+FC(16,1),
+// branch-stable sigmoid (losses.cpp:26-33), inclusive p >= delta
+// (cache.cpp:259-265), argmax(pr) with the lowest index on ties
+// (tensor.hpp:57-63). logits complete in shared memory; pr: shared [classes].
+__device__ void head_block(const CacheHeadParams& p, int r, const float* logits, float* pr, HeadSmem& hs) {
+  const int C = p.classes;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = kLk / 32;
   float m = -FLT_MAX;
-  for (int k = tid; k < C; k += blockDim.x) m = fmaxf(m, logits[k]);
-  m = block_max(m, red);
+  for (int k = tid; k < C; k += kLk) m = fmaxf(m, logits[k]);
+  m = block_max(m, hs.red);
   float part = 0.0f;
-  for (int k = tid; k < C; k += blockDim.x) part += expf(logits[k] - m);
-  const float sum = block_sum(part, red);
-  float* pr = feat;  // reuse
-  __syncthreads();
-  for (int k = tid; k < C; k += blockDim.x) pr[k] = expf(logits[k] - m) / sum;
-  __syncthreads();
-  // selector FC(C,16) + ReLU
-  for (int j = warp; j < 16; j += nw) {
-    const float* wr = p.Ws1 + j * C;
-    float a = 0.0f;
-    for (int k = lane; k < C; k += 32) a += wr[k] * pr[k];
-    a = warp_sum(a);
-    if (lane == 0) {
-      a += p.bs1[j];
-      hsel[j] = a > 0.0f ? a : 0.0f;
-    }
-  }
-  // argmax(pr), lowest index on ties (tensor.hpp:57-63)
+  for (int k = tid; k < C; k += kLk) part += expf(logits[k] - m);
+  const float sum = block_sum(part, hs.red);
   float bv = -FLT_MAX;
   int bi = 0x7fffffff;
-  for (int k = tid; k < C; k += blockDim.x) {
-    if (pr[k] > bv) {
-      bv = pr[k];
+  for (int k = tid; k < C; k += kLk) {
+    const float q = expf(logits[k] - m) / sum;
+    pr[k] = q;
+    if (q > bv) {
+      bv = q;
       bi = k;
     }
   }
@@ -430,20 +590,36 @@ __global__ void cache_head_kernel(CacheHeadParams p) {
     }
   }
   if (lane == 0) {
-    best_val_s[warp] = bv;
-    best_idx_s[warp] = bi;
+    hs.bv[warp] = bv;
+    hs.bi[warp] = bi;
+  }
+  __syncthreads();
+  // selector hidden unit j on warp j % nw
+  for (int j = warp; j < 16; j += nw) {
+    const float* wr = p.Ws1 + j * C;
+    float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
+    int k = lane;
+    for (; k + 96 < C; k += 128) {
+      a0 += __ldg(wr + k) * pr[k];
+      a1 += __ldg(wr + k + 32) * pr[k + 32];
+      a2 += __ldg(wr + k + 64) * pr[k + 64];
+      a3 += __ldg(wr + k + 96) * pr[k + 96];
+    }
+    for (; k < C; k += 32) a0 += __ldg(wr + k) * pr[k];
+    const float a = warp_sum((a0 + a1) + (a2 + a3)) + p.bs1[j];
+    if (lane == 0) hs.hsel[j] = a > 0.0f ? a : 0.0f;
   }
   __syncthreads();
   if (tid == 0) {
-    float v = best_val_s[0];
-    int i = best_idx_s[0];
+    float v = hs.bv[0];
+    int i = hs.bi[0];
     for (int w = 1; w < nw; ++w)
-      if (best_val_s[w] > v || (best_val_s[w] == v && best_idx_s[w] < i)) {
-        v = best_val_s[w];
-        i = best_idx_s[w];
+      if (hs.bv[w] > v || (hs.bv[w] == v && hs.bi[w] < i)) {
+        v = hs.bv[w];
+        i = hs.bi[w];
       }
     float z = p.bs2;
-    for (int j = 0; j < 16; ++j) z += p.ws2[j] * hsel[j];
+    for (int j = 0; j < 16; ++j) z += p.ws2[j] * hs.hsel[j];
     float q;
     if (z >= 0.0f) {
       q = 1.0f / (1.0f + expf(-z));
@@ -456,268 +632,50 @@ __global__ void cache_head_kernel(CacheHeadParams p) {
     p.label[r] = i;
   }
   if (p.pr_out)
-    for (int k = tid; k < C; k += blockDim.x) p.pr_out[static_cast<long long>(r) * C + k] = pr[k];
+    for (int k = tid; k < C; k += kLk) p.pr_out[static_cast<long long>(r) * C + k] = pr[k];
   if (p.logits_out)
-    for (int k = tid; k < C; k += blockDim.x) p.logits_out[static_cast<long long>(r) * C + k] = logits[k];
+    for (int k = tid; k < C; k += kLk) p.logits_out[static_cast<long long>(r) * C + k] = logits[k];
 }
 
-// Warp-per-row form of the same head for classes <= 32 (no block barriers):
-// lane k owns class k; features are streamed lane-strided.
-__global__ void cache_head_warp_kernel(CacheHeadParams p) {
-  extern __shared__ float smw[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r = blockIdx.x * (blockDim.x >> 5) + warp;
-  if (r >= *p.count) return;
-  const int C = p.classes;
-  float logit = -FLT_MAX;
-  if (p.family == 2) {
-    if (lane < C) {
-      float a = p.b2[lane];
-      for (int c = 0; c < p.feat; ++c) a += p.feats[(static_cast<long long>(r) * p.feat + c) * C + lane];
-      logit = a;
-    }
-  } else {
-    float* feat = smw + warp * p.feat;
-    if (p.family == 1) {
-      for (int o = lane; o < p.feat; o += 32) feat[o] = p.feats[static_cast<long long>(r) * p.feat + o];
-    } else {
-      for (int j = lane; j < p.feat; j += 32) {
-        float a = p.b1[j];
-        for (int s = 0; s < p.ks; ++s) a += p.feats[(static_cast<long long>(s) * p.rows_total + r) * p.hp + j];
-        feat[j] = a > 0.0f ? a : 0.0f;
-      }
-    }
-    __syncwarp();
-    for (int k = 0; k < C; ++k) {
-      const float* wr = p.W2 + static_cast<long long>(k) * p.feat;
-      float a = 0.0f;
-      for (int o = lane; o < p.feat; o += 32) a += wr[o] * feat[o];
-      a = warp_sum(a);
-      if (lane == k) logit = a + p.b2[k];
-    }
-  }
-  const float m = warp_max(lane < C ? logit : -FLT_MAX);
-  const float e = lane < C ? expf(logit - m) : 0.0f;
-  const float sum = warp_sum(e);
-  const float pr = lane < C ? e / sum : 0.0f;
-  // selector FC(C,16) + ReLU: lane j < 16 owns hidden unit j
-  float h = 0.0f;
-  {
-    float a = lane < 16 ? p.bs1[lane] : 0.0f;
-    for (int k = 0; k < C; ++k) {
-      const float pk = __shfl_sync(0xffffffffu, pr, k);
-      if (lane < 16) a += p.Ws1[lane * C + k] * pk;
-    }
-    h = (lane < 16 && a > 0.0f) ? a : 0.0f;
-  }
-  const float z = warp_sum(lane < 16 ? p.ws2[lane] * h : 0.0f) + p.bs2;
-  // argmax(pr), lowest index on ties
-  float bv = lane < C ? pr : -FLT_MAX;
-  int bi = lane < C ? lane : 0x7fffffff;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-    if (ov > bv || (ov == bv && oi < bi)) {
-      bv = ov;
-      bi = oi;
-    }
-  }
-  if (lane == 0) {
-    float q;
-    if (z >= 0.0f) {
-      q = 1.0f / (1.0f + expf(-z));
-    } else {
-      const float ez = expf(z);
-      q = ez / (1.0f + ez);
-    }
-    p.prob[r] = q;
-    p.hit[r] = static_cast<double>(q) >= p.delta ? 1 : 0;
-    p.label[r] = bi;
-  }
-  if (lane < C) {
-    if (p.pr_out) p.pr_out[static_cast<long long>(r) * C + lane] = pr;
-    if (p.logits_out) p.logits_out[static_cast<long long>(r) * C + lane] = logit;
-  }
-}
-
-// ------------------------------------------------------------------ fused lookup + exit
-// One launch per cache layer for Pool(C) = GAP caches with <= 32 classes:
-// every warp owns rows (bins from tc_conv's fused GAP partials, FC(C,classes),
-// softmax, selector FC(C,16)+ReLU+FC(16,1), sigmoid, >= delta, argmax — the
-// arithmetic and summation order of gap_bins_kernel + cache_head_warp_kernel);
-// per-row decisions go to global scratch and the LAST CTA to finish (arrival
-// counter) runs the first-hit record + stable compaction of exit_compact_kernel.
-constexpr int kFusedMaxC = 1024;
-
-__global__ void __launch_bounds__(512) gap_lookup_exit_kernel(FusedLookupParams p) {
+// Arrival of every CTA of a head launch; the LAST one records first hits and
+// compacts the surviving rows in order (warp ballot + block prefix sum):
+// exit_compact of serve_one (serving.cpp:112-121) without its own launch.
+__device__ void exit_tail(const ExitParams& e, int n, const float* prob, const int* hit, const int* label) {
+  __shared__ int last_s, base_s;
   __shared__ int warp_tot[32];
-  __shared__ int base_s;
-  __shared__ int last_s;
-  const int n_rows = *p.count_in;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  const int C = p.C, K = p.classes;
-  for (int r = blockIdx.x * nw + warp; r < n_rows; r += gridDim.x * nw) {
-    const long long n = p.ids_in[r];
-    const float* src = p.gap + n * p.segs * C;
-    // bins (gap_bins_kernel order), lane-strided channels
-    // 4 independent partial sums over the segments (fixed combination order)
-    float f[kFusedMaxC / 32];
-#pragma unroll
-    for (int j = 0; j < kFusedMaxC / 32; ++j) {
-      const int c = lane + 32 * j;
-      float a = 0.0f;
-      if (c < C) {
-        float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
-        int sg = 0;
-        for (; sg + 4 <= p.segs; sg += 4) {
-          const float* q = src + static_cast<long long>(sg) * C + c;
-          a0 += __ldg(q);
-          a1 += __ldg(q + C);
-          a2 += __ldg(q + 2 * C);
-          a3 += __ldg(q + 3 * C);
-        }
-        for (; sg < p.segs; ++sg) a0 += __ldg(src + static_cast<long long>(sg) * C + c);
-        a = ((a0 + a1) + (a2 + a3)) * p.inv;
-      }
-      f[j] = a;
-    }
-    // logits (cache_head_warp_kernel order)
-    float logit = -FLT_MAX;
-    for (int k = 0; k < K; ++k) {
-      const float* wr = p.W2 + static_cast<long long>(k) * C;
-      float a = 0.0f;
-#pragma unroll
-      for (int j = 0; j < kFusedMaxC / 32; ++j) {
-        const int c = lane + 32 * j;
-        if (c < C) a += wr[c] * f[j];
-      }
-      a = warp_sum(a);
-      if (lane == k) logit = a + p.b2[k];
-    }
-    const float m = warp_max(lane < K ? logit : -FLT_MAX);
-    const float e = lane < K ? expf(logit - m) : 0.0f;
-    const float sum = warp_sum(e);
-    const float pr = lane < K ? e / sum : 0.0f;
-    float h = 0.0f;
-    {
-      float a = lane < 16 ? p.bs1[lane] : 0.0f;
-      for (int k = 0; k < K; ++k) {
-        const float pk = __shfl_sync(0xffffffffu, pr, k);
-        if (lane < 16) a += p.Ws1[lane * K + k] * pk;
-      }
-      h = (lane < 16 && a > 0.0f) ? a : 0.0f;
-    }
-    const float z = warp_sum(lane < 16 ? p.ws2[lane] * h : 0.0f) + p.bs2;
-    float bv = lane < K ? pr : -FLT_MAX;
-    int bi = lane < K ? lane : 0x7fffffff;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ov > bv || (ov == bv && oi < bi)) {
-        bv = ov;
-        bi = oi;
-      }
-    }
-    if (lane == 0) {
-      float q;
-      if (z >= 0.0f) {
-        q = 1.0f / (1.0f + expf(-z));
-      } else {
-        const float ez = expf(z);
-        q = ez / (1.0f + ez);
-      }
-      p.prob[r] = q;
-      p.hit[r] = static_cast<double>(q) >= p.delta ? 1 : 0;
-      p.label[r] = bi;
-    }
-  }
-  // last CTA: first-hit records + stable compaction over all rows
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) last_s = (atomicAdd(p.arrive, 1) == static_cast<int>(gridDim.x) - 1) ? 1 : 0;
+  if (threadIdx.x == 0) last_s = (atomicAdd(e.arrive, 1) == static_cast<int>(gridDim.x) - 1) ? 1 : 0;
   __syncthreads();
   if (!last_s) return;
   __threadfence();
-  if (threadIdx.x == 0) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  if (tid == 0) {
     base_s = 0;
-    *p.arrive = 0;
+    *e.arrive = 0;
   }
-  __syncthreads();
-  const unsigned long long now = globaltimer();
-  const int tid = threadIdx.x;
-  for (int c0 = 0; c0 < n_rows; c0 += blockDim.x) {
-    const int r = c0 + tid;
-    const bool valid = r < n_rows;
-    const bool hit = valid && __ldcg(p.hit + r);
-    const int id = valid ? p.ids_in[r] : -1;
-    if (valid) {
-      if (p.probs_out) p.probs_out[id] = __ldcg(p.prob + r);
-      if (hit && p.exit_layer[id] == 0) {
-        p.exit_layer[id] = p.layer;
-        p.served[id] = __ldcg(p.label + r);
-        p.exit_ns[id] = now;
-      }
-    }
-    const bool keep = valid && (p.shadow || !hit);
-    const unsigned mask = __ballot_sync(0xffffffffu, keep);
-    const int pos_in_warp = __popc(mask & ((1u << lane) - 1u));
-    if (lane == 0) warp_tot[warp] = __popc(mask);
-    __syncthreads();
-    if (warp == 0) {
-      int v = lane < nw ? warp_tot[lane] : 0;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int u = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += u;
-      }
-      if (lane < nw) warp_tot[lane] = v;
-    }
-    __syncthreads();
-    const int warp_off = warp == 0 ? 0 : warp_tot[warp - 1];
-    const int base = base_s;
-    if (keep) p.ids_out[base + warp_off + pos_in_warp] = id;
-    __syncthreads();
-    if (tid == 0) base_s = base + warp_tot[nw - 1];
-    __syncthreads();
-  }
-  if (tid == 0) *p.count_out = base_s;
-}
-
-// ------------------------------------------------------------------ exit
-__global__ void exit_compact_kernel(int layer, const int* count_in, const int* ids_in, const int* hit, const int* label,
-                                    const float* prob, int* exit_layer, int* served, unsigned long long* exit_ns,
-                                    float* probs_out, int* ids_out, int* src_rows_out, int* count_out, int shadow) {
-  __shared__ int warp_tot[32];
-  __shared__ int base_s;
-  const int n = *count_in;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) base_s = 0;
   __syncthreads();
   const unsigned long long now = globaltimer();
   for (int c0 = 0; c0 < n; c0 += blockDim.x) {
     const int r = c0 + tid;
     const bool valid = r < n;
-    const bool h = valid && hit[r];
-    const int id = valid ? ids_in[r] : -1;
+    const bool h = valid && __ldcg(hit + r);
+    const int id = valid ? e.ids_in[r] : -1;
     if (valid) {
-      if (probs_out) probs_out[id] = prob[r];
-      if (h && exit_layer[id] == 0) {
-        exit_layer[id] = layer;
-        served[id] = label[r];
-        exit_ns[id] = now;
+      if (e.probs_out) e.probs_out[id] = __ldcg(prob + r);
+      if (h && e.exit_layer[id] == 0) {
+        e.exit_layer[id] = e.layer;
+        e.served[id] = __ldcg(label + r);
+        e.exit_ns[id] = now;
       }
     }
-    const bool keep = valid && (shadow || !h);
+    const bool keep = valid && (e.shadow || !h);
     const unsigned mask = __ballot_sync(0xffffffffu, keep);
     const int pos_in_warp = __popc(mask & ((1u << lane) - 1u));
     if (lane == 0) warp_tot[warp] = __popc(mask);
     __syncthreads();
     if (warp == 0) {
-      const int nw = blockDim.x >> 5;
       int v = lane < nw ? warp_tot[lane] : 0;
-      // inclusive scan
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int u = __shfl_up_sync(0xffffffffu, v, o);
@@ -726,17 +684,66 @@ __global__ void exit_compact_kernel(int layer, const int* count_in, const int* i
       if (lane < nw) warp_tot[lane] = v;  // inclusive prefix
     }
     __syncthreads();
-    const int warp_off = warp == 0 ? 0 : warp_tot[warp - 1];
-    const int base = base_s;
+    const int pos = base_s + (warp == 0 ? 0 : warp_tot[warp - 1]) + pos_in_warp;
     if (keep) {
-      ids_out[base + warp_off + pos_in_warp] = id;
-      if (src_rows_out) src_rows_out[base + warp_off + pos_in_warp] = r;
+      e.ids_out[pos] = id;
+      if (e.src_rows_out) e.src_rows_out[pos] = r;
     }
     __syncthreads();
-    if (tid == 0) base_s = base + warp_tot[(blockDim.x >> 5) - 1];
+    if (tid == 0) base_s += warp_tot[nw - 1];
     __syncthreads();
   }
-  if (tid == 0) *count_out = base_s;
+  if (tid == 0) *e.count_out = base_s;
+}
+
+// ------------------------------------------------------------------ head
+// Reference lookup (cache.cpp:259-265): pr = softmax(pred(tap)),
+// p = sigmoid(sel(pr)), hit = p >= delta (inclusive); label = argmax(pr).
+// One CTA per row. Logits come from (in order of precedence) the batched
+// split-K GEMM partials, the fused GAP partials (Pool(C), classes <= 32),
+// the Conv(k,s) chunk partials, or the pooled bins / FC(h) hidden partials.
+// With p.ex.arrive the last CTA also runs the exit + compaction.
+__global__ void __launch_bounds__(kLk) cache_head_kernel(CacheHeadParams p) {
+  extern __shared__ float sm[];
+  __shared__ HeadSmem hs;
+  __shared__ float4 red4[kLk];
+  const int r = blockIdx.x;
+  const int n = *p.count;
+  const int C = p.classes;
+  if (r < n) {
+    float* logits = sm;    // [C]
+    float* feat = sm + C;  // [max(feat, C)]
+    const int tid = threadIdx.x;
+    if (p.pre_logits) {
+      for (int k = tid; k < C; k += kLk) logits[k] = fc_logit(p.pre_logits, p.pre_nz, p.pre_zstride, p.b2, r, C, k);
+    } else if (p.family == 2) {
+      for (int k = tid; k < C; k += kLk) {
+        float a = p.b2[k];
+        const float* q = p.feats + static_cast<long long>(r) * p.feat * C + k;
+#pragma unroll 4
+        for (int c = 0; c < p.feat; ++c) a += __ldg(q + static_cast<long long>(c) * C);
+        logits[k] = a;
+      }
+    } else {
+      if (p.gap) {
+        const long long img = p.gap_ids ? p.gap_ids[r] : r;
+        gap_feats_block(p.gap + img * p.gap_segs * p.feat, p.gap_segs, p.feat, p.gap_inv, feat, red4);
+      } else if (p.family == 1) {
+        for (int o = tid; o < p.feat; o += kLk) feat[o] = __ldg(p.feats + static_cast<long long>(r) * p.feat + o);
+      } else {
+        for (int j = tid; j < p.feat; j += kLk) {
+          float a = p.b1[j];
+          for (int s = 0; s < p.ks; ++s) a += __ldg(p.feats + (static_cast<long long>(s) * p.rows_total + r) * p.hp + j);
+          feat[j] = a > 0.0f ? a : 0.0f;
+        }
+      }
+      __syncthreads();
+      block_logits(p.W2, p.b2, C, p.feat, feat, logits);
+    }
+    __syncthreads();
+    head_block(p, r, logits, feat, hs);
+  }
+  if (p.ex.arrive) exit_tail(p.ex, n, p.prob, p.hit, p.label);
 }
 
 __global__ void gather_rows_kernel(const __nv_bfloat16* src_hi, const __nv_bfloat16* src_lo, __nv_bfloat16* dst_hi,
@@ -783,13 +790,14 @@ __global__ void split_taps_nchw_kernel(const float* x, int C, int HW, long long 
 
 // Base head (base_model.cpp:48-49): logits -> softmax -> argmax (serving.cpp:108).
 template <bool kGap>
-__global__ void base_head_kernel(const __nv_bfloat16* hi, const __nv_bfloat16* lo, long long row_stride, int C, int HW,
-                                 const float* W, const float* b, int classes, const int* ids, const int* count,
-                                 int* base_pred, float* logits_out, int* exit_layer, int* served,
-                                 unsigned long long* exit_ns, const float* pre_logits, int pre_nz,
-                                 long long pre_zstride) {
+__global__ void __launch_bounds__(kLk) base_head_kernel(const __nv_bfloat16* hi, const __nv_bfloat16* lo,
+                                                        long long row_stride, int C, int HW, const float* W,
+                                                        const float* b, int classes, const int* ids, const int* count,
+                                                        int* base_pred, float* logits_out, int* exit_layer, int* served,
+                                                        unsigned long long* exit_ns, const float* pre_logits,
+                                                        int pre_nz, long long pre_zstride) {
   extern __shared__ float sm[];
-  __shared__ float red[32];
+  __shared__ float red[kLk * 8];
   __shared__ int bi_s[32];
   __shared__ float bv_s[32];
   const int r = blockIdx.x;
@@ -798,40 +806,31 @@ __global__ void base_head_kernel(const __nv_bfloat16* hi, const __nv_bfloat16* l
   const long long n = kGap ? id : r;
   float* feat = sm;          // [C]
   float* logits = sm + C;    // [classes]
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = kLk / 32;
   TapView t;
   t.hi = hi;
   t.lo = lo;
   if (pre_logits) {
-    for (int k = tid; k < classes; k += blockDim.x) logits[k] = fc_logit(pre_logits, pre_nz, pre_zstride, b, r, classes, k);
-  }
-  for (int c = tid; c < C && !pre_logits; c += blockDim.x) {
+    for (int k = tid; k < classes; k += kLk) logits[k] = fc_logit(pre_logits, pre_nz, pre_zstride, b, r, classes, k);
+  } else {
     if (kGap) {
-      float a = 0.0f;
-      for (int q = 0; q < HW; ++q) a += ld_tap(t, n * row_stride + static_cast<long long>(q) * C + c);
-      feat[c] = a * (1.0f / HW);
+      tap_gap_block(t, n * row_stride, C, HW, feat, red);
     } else {
-      feat[c] = ld_tap(t, n * row_stride + c);
+      for (int c = tid; c < C; c += kLk) feat[c] = ld_tap(t, n * row_stride + c);
+      __syncthreads();
     }
-  }
-  __syncthreads();
-  for (int k = warp; k < classes && !pre_logits; k += nw) {
-    const float* wr = W + static_cast<long long>(k) * C;
-    float a = 0.0f;
-    for (int c = lane; c < C; c += 32) a += wr[c] * feat[c];
-    a = warp_sum(a);
-    if (lane == 0) logits[k] = a + b[k];
+    block_logits(W, b, classes, C, feat, logits);
   }
   __syncthreads();
   float m = -FLT_MAX;
-  for (int k = tid; k < classes; k += blockDim.x) m = fmaxf(m, logits[k]);
+  for (int k = tid; k < classes; k += kLk) m = fmaxf(m, logits[k]);
   m = block_max(m, red);
   float part = 0.0f;
-  for (int k = tid; k < classes; k += blockDim.x) part += expf(logits[k] - m);
+  for (int k = tid; k < classes; k += kLk) part += expf(logits[k] - m);
   const float sum = block_sum(part, red);
   float bv = -FLT_MAX;
   int bi = 0x7fffffff;
-  for (int k = tid; k < classes; k += blockDim.x) {
+  for (int k = tid; k < classes; k += kLk) {
     const float pk = expf(logits[k] - m) / sum;
     if (pk > bv) {
       bv = pk;
@@ -867,7 +866,7 @@ __global__ void base_head_kernel(const __nv_bfloat16* hi, const __nv_bfloat16* l
     }
   }
   if (logits_out)
-    for (int k = tid; k < classes; k += blockDim.x) logits_out[static_cast<long long>(id) * classes + k] = logits[k];
+    for (int k = tid; k < classes; k += kLk) logits_out[static_cast<long long>(id) * classes + k] = logits[k];
 }
 
 // One thread per (output pixel, 8 consecutive K entries): 16-byte stores.
@@ -1027,7 +1026,8 @@ void launch_gap_bins(const float* gap, int segs, int C, int HW, const int* data_
                      float* bins, cudaStream_t s) {
   if (max_rows <= 0) return;
   const float inv = static_cast<float>(1.0 / HW);
-  gap_bins_kernel<<<dim3(max_rows, (C + 255) / 256), 256, 0, s>>>(gap, segs, C, inv, data_idx, count, bins);
+  gap_bins_kernel<<<max_rows, kLk, static_cast<size_t>(C) * sizeof(float), s>>>(gap, segs, C, inv, data_idx, count,
+                                                                                 bins);
 }
 
 void launch_conv1d_partials(const TapView& tap, int max_rows, long long D, int kernel, int stride, int out_dim,
@@ -1044,18 +1044,21 @@ void launch_conv1d_partials(const TapView& tap, int max_rows, long long D, int k
                                                                     classes, chunk_elems, nchunks, partials);
 }
 
-int rows_fc_splits(int feat) { return (feat + kRowsFcSlice - 1) / kRowsFcSlice; }
+int rows_fc_splits(int feat) {
+  const int sl = rows_fc_slice(feat);
+  return (feat + sl - 1) / sl;
+}
 
 void launch_rows_fc(const float* A, long long lda, int ks, long long part_stride, const float* b1, int feat,
                     const float* W, int classes, const int* count, int max_rows, float* out, cudaStream_t s) {
   if (max_rows <= 0) return;
   const dim3 grid((classes + kFcBN - 1) / kFcBN, (max_rows + kFcBM - 1) / kFcBM, rows_fc_splits(feat));
   if (ks > 0)
-    rows_fc_kernel<1><<<grid, 256, 0, s>>>(A, lda, ks, part_stride, b1, feat, kRowsFcSlice, W, classes, count,
+    rows_fc_kernel<1><<<grid, 256, 0, s>>>(A, lda, ks, part_stride, b1, feat, rows_fc_slice(feat), W, classes, count,
                                            max_rows, out);
   else
-    rows_fc_kernel<0><<<grid, 256, 0, s>>>(A, lda, 0, 0, nullptr, feat, kRowsFcSlice, W, classes, count, max_rows,
-                                           out);
+    rows_fc_kernel<0><<<grid, 256, 0, s>>>(A, lda, 0, 0, nullptr, feat, rows_fc_slice(feat), W, classes, count,
+                                           max_rows, out);
 }
 
 void launch_cache_head(const CacheHeadParams& p_in, int max_rows, cudaStream_t s) {
@@ -1071,44 +1074,20 @@ void launch_cache_head(const CacheHeadParams& p_in, int max_rows, cudaStream_t s
     p.pre_logits = p.fc_scratch;
     p.pre_nz = rows_fc_splits(p.feat);
     p.pre_zstride = static_cast<long long>(max_rows) * p.classes;
-  }
-  if (!p.pre_logits && p.classes <= 32 && (p.family == 2 || p.feat <= 4096)) {
-    const int warps = 4;
-    const size_t smem = p.family == 2 ? 0 : static_cast<size_t>(warps) * p.feat * sizeof(float);
-    static bool wattr = false;
-    if (!wattr) {
-      cudaFuncSetAttribute(cache_head_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      wattr = true;
-    }
-    cache_head_warp_kernel<<<(max_rows + warps - 1) / warps, 32 * warps, smem, s>>>(p);
-    return;
+    p.gap = nullptr;
   }
   const int feat_len = (p.family == 2 || p.pre_logits) ? p.classes : (p.feat > p.classes ? p.feat : p.classes);
   const size_t smem = static_cast<size_t>(p.classes + feat_len) * sizeof(float);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(cache_head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(cache_head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     attr = true;
   }
-  cache_head_kernel<<<max_rows, 128, smem, s>>>(p);
+  cache_head_kernel<<<max_rows, kLk, smem, s>>>(p);
 }
 
 bool fused_lookup_supported(int classes, int C, int max_rows) {
-  return classes <= 32 && C <= kFusedMaxC && max_rows > 0;
-}
-
-void launch_gap_lookup_exit(const FusedLookupParams& p, int max_rows, cudaStream_t s) {
-  const int warps = 16;
-  int grid = (max_rows + warps - 1) / warps;
-  if (grid > 148) grid = 148;
-  gap_lookup_exit_kernel<<<grid, warps * 32, 0, s>>>(p);
-}
-
-void launch_exit_compact(int layer, const int* count_in, const int* ids_in, const int* hit, const int* label,
-                         const float* prob, int* exit_layer, int* served, unsigned long long* exit_ns, float* probs_out,
-                         int* ids_out, int* src_rows_out, int* count_out, int shadow, cudaStream_t s) {
-  exit_compact_kernel<<<1, 1024, 0, s>>>(layer, count_in, ids_in, hit, label, prob, exit_layer, served, exit_ns,
-                                         probs_out, ids_out, src_rows_out, count_out, shadow);
+  return classes <= 32 && C % 4 == 0 && C <= 16384 && max_rows > 0;
 }
 
 void launch_gather_rows(const __nv_bfloat16* src_hi, const __nv_bfloat16* src_lo, __nv_bfloat16* dst_hi,
@@ -1140,7 +1119,7 @@ void launch_mlp_head(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int dp, i
                      int* exit_layer, int* served, unsigned long long* exit_ns, cudaStream_t s) {
   if (max_rows <= 0) return;
   const size_t smem = static_cast<size_t>(dim + classes) * sizeof(float);
-  base_head_kernel<false><<<max_rows, 128, smem, s>>>(hi, lo, dp, dim, 1, W, b, classes, ids, count, base_pred,
+  base_head_kernel<false><<<max_rows, kLk, smem, s>>>(hi, lo, dp, dim, 1, W, b, classes, ids, count, base_pred,
                                                       logits_out, exit_layer, served, exit_ns, nullptr, 0, 0);
 }
 
@@ -1152,13 +1131,13 @@ void launch_cnn_head(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int C, in
   const float* pre = nullptr;
   if (classes > 32 && feats_scratch && logits_scratch) {
     // Many classes: GAP rows, one batched logits GEMM, then the per-row softmax/argmax.
-    int gy = (C + 255) / 256;
-    gap_rows_kernel<<<dim3(max_rows, gy), 256, 0, s>>>(hi, lo, C, HW, ids, count, feats_scratch);
+    gap_rows_kernel<<<max_rows, kLk, static_cast<size_t>(C) * sizeof(float), s>>>(hi, lo, C, HW, ids, count,
+                                                                                  feats_scratch);
     launch_rows_fc(feats_scratch, C, 0, 0, nullptr, C, W, classes, count, max_rows, logits_scratch, s);
     pre = logits_scratch;
   }
   const size_t smem = static_cast<size_t>(C + classes) * sizeof(float);
-  base_head_kernel<true><<<max_rows, 256, smem, s>>>(hi, lo, static_cast<long long>(C) * HW, C, HW, W, b, classes, ids,
+  base_head_kernel<true><<<max_rows, kLk, smem, s>>>(hi, lo, static_cast<long long>(C) * HW, C, HW, W, b, classes, ids,
                                                      count, base_pred, logits_out, exit_layer, served, exit_ns, pre,
                                                      rows_fc_splits(C), static_cast<long long>(max_rows) * classes);
 }

@@ -26,6 +26,25 @@ struct TapView {
   const int* count;         // rows in this layer
 };
 
+// First-hit exit + stable stream compaction fused into the LAST CTA of a
+// lookup head launch (arrival counter): rows with hit leave; ids_in[r] is the
+// original request id of row r; kept rows go to ids_out (and their row index
+// to src_rows_out, nullable), their number to count_out. shadow != 0: every
+// row stays (probing continues) but only the first hit of a request is
+// recorded (serve_one, serving.cpp:112-121).
+struct ExitParams {
+  int* arrive;               // nullptr = no exit/compaction (lookup-only)
+  int layer, shadow;
+  const int* ids_in;
+  int* exit_layer;
+  int* served;
+  unsigned long long* exit_ns;
+  float* probs_out;          // [B] this layer's probabilities by request id (nullable)
+  int* ids_out;
+  int* src_rows_out;         // nullable
+  int* count_out;
+};
+
 // Per-row cache head inputs (one of three predictor families).
 struct CacheHeadParams {
   int family;              // 0 = FC(h), 1 = Pool(width), 2 = Conv(k,s)
@@ -44,6 +63,12 @@ struct CacheHeadParams {
   float bs2;
   double delta;
   const int* count;
+  // Pool(C) = GAP from tc_conv's fused partials gap[image][gap_segs][feat]
+  // (nullable): the head sums them itself (classes <= 32) instead of reading feats.
+  const float* gap;
+  int gap_segs;
+  float gap_inv;           // 1 / (H*W)
+  const int* gap_ids;      // row r -> image id
   // outputs (row-indexed)
   float* prob;             // [rows] selector probability
   int* hit;                // [rows]
@@ -56,9 +81,9 @@ struct CacheHeadParams {
   const float* pre_logits;
   int pre_nz;
   long long pre_zstride;
+  ExitParams ex;           // ex.arrive != nullptr: fused first-hit exit + compaction
 };
 
-constexpr int kRowsFcSlice = 256;  // K-slice of the batched logits GEMM
 int rows_fc_splits(int feat);
 
 void launch_pool_bins(const TapView& tap, int max_rows, int win, int width, float* bins, cudaStream_t s);
@@ -68,52 +93,17 @@ void launch_gap_bins(const float* gap, int segs, int C, int HW, const int* data_
 void launch_conv1d_partials(const TapView& tap, int max_rows, long long D, int kernel, int stride, int out_dim,
                             const float* w1, float b1, const float* W2, int classes, int chunk_elems, int nchunks,
                             float* partials, cudaStream_t s);
+// Head (+ batched logits GEMM for classes > 32) and, with p.ex.arrive, the
+// fused exit/compaction: one or two launches per cache layer.
 void launch_cache_head(const CacheHeadParams& p, int max_rows, cudaStream_t s);
 // out[z][r][k] = sum_{o in slice z} A(r,o) W[k][o] for r < *count, z < rows_fc_splits(feat)
-// (slices of kRowsFcSlice, ascending o inside a slice; out z-stride = max_rows*classes).
+// (ascending o inside a slice; out z-stride = max_rows*classes).
 // ks == 0: A dense [rows][lda]; ks > 0: A(r,o) = relu(b1[o] + sum_s A[s*part_stride + r*lda + o]).
 void launch_rows_fc(const float* A, long long lda, int ks, long long part_stride, const float* b1, int feat,
                     const float* W, int classes, const int* count, int max_rows, float* out, cudaStream_t s);
 
-// Fused Pool(C)-GAP lookup + first-hit exit + compaction for <= 32 classes
-// (one launch per cache layer; see gap_lookup_exit_kernel).
-struct FusedLookupParams {
-  const float* gap;   // [image][segs][C] partials from tc_conv
-  int segs, C, classes;
-  float inv;          // 1 / (H*W)
-  const float* W2;    // [classes][C]
-  const float* b2;
-  const float* Ws1;   // [16][classes]
-  const float* bs1;
-  const float* ws2;
-  float bs2;
-  double delta;
-  int layer, shadow;
-  const int* count_in;
-  const int* ids_in;
-  float* prob;        // [rows] scratch
-  int* hit;
-  int* label;
-  int* arrive;        // arrival counter (zero; reset by the last CTA)
-  int* exit_layer;
-  int* served;
-  unsigned long long* exit_ns;
-  float* probs_out;   // [B] this layer's probabilities by request id (nullable)
-  int* ids_out;
-  int* count_out;
-};
+// Pool(C) caches whose head reads the GAP partials directly (one launch per layer).
 bool fused_lookup_supported(int classes, int C, int max_rows);
-void launch_gap_lookup_exit(const FusedLookupParams& p, int max_rows, cudaStream_t s);
-
-// First-hit exit + stable stream compaction (single CTA, warp ballot +
-// block prefix sum). Rows with hit leave; `ids_in[r]` is the original request
-// id of row r. Writes ids_out/src_rows_out (kept rows in order) and count_out.
-// shadow != 0: every row stays (probing continues) but only the first hit of
-// each request is recorded.
-void launch_exit_compact(int layer, const int* count_in, const int* ids_in, const int* hit, const int* label,
-                         const float* prob, int* exit_layer, int* served, unsigned long long* exit_ns,
-                         float* probs_out /*[B] for this layer*/, int* ids_out, int* src_rows_out, int* count_out,
-                         int shadow, cudaStream_t s);
 
 // Copies rows src_rows[j] of src into row j of dst (hi and lo planes).
 void launch_gather_rows(const __nv_bfloat16* src_hi, const __nv_bfloat16* src_lo, __nv_bfloat16* dst_hi,
