@@ -24,14 +24,43 @@ struct TcCfg {
   static constexpr int kStageBytes = kPlanes * (kABytes + kBBytes);
   static constexpr int kStagesRaw = (192 * 1024) / kStageBytes;
   static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
-  static constexpr int kEpiStage = 8 * 4096;  // per epilogue warp: 32 rows x 64 B x 2 planes (TMA store staging)
-  static constexpr int kSmem = kStages * kStageBytes + kEpiStage + 1024 /*bars*/ + 1024 /*align*/;
+  static constexpr int kEpiWarpBytes = kPlanes * 2048;  // per epilogue warp: 32 rows x 64 B per plane
+  static constexpr int kEpiStage = 8 * kEpiWarpBytes;
+  static constexpr int kShiftBytes = 2 * BN * 4;  // per-tile shift values, double-buffered with the accumulators
+  static constexpr int kSmem = kStages * kStageBytes + kEpiStage + 1024 /*bars*/ + kShiftBytes + 1024 /*align*/;
   static constexpr uint32_t kTmemCols = 2 * BN;
   static_assert(kStages >= 2, "pipeline needs at least two stages");
 };
 
+// Division by a launch-constant divisor through a multiply-high (dividends
+// < 2^31): the persistent loops decode a tile per iteration in every role, and
+// runtime integer divisions were a large share of the epilogue's instructions.
+struct FastDiv {
+  uint32_t d, m, s;
+  __device__ __forceinline__ void init(int div) {
+    d = static_cast<uint32_t>(div < 1 ? 1 : div);
+    if (d == 1) {
+      m = 0;
+      s = 0;
+    } else {
+      const uint32_t l = 32 - __clz(d - 1);  // ceil(log2 d)
+      const uint32_t pw = 31 + l;
+      m = static_cast<uint32_t>(((1ull << pw) + d - 1) / d);
+      s = pw - 32;
+    }
+  }
+  __device__ __forceinline__ int div(int x) const {
+    return d == 1 ? x : static_cast<int>(__umulhi(static_cast<uint32_t>(x), m) >> s);
+  }
+  __device__ __forceinline__ void divmod(int x, int& q, int& r) const {
+    q = div(x);
+    r = x - q * static_cast<int>(d);
+  }
+};
+
 struct TileGeom {
   int count, n_groups, tiles_w, tiles_img, tiles_n, tiles_mn, ks, total, nk;
+  FastDiv fks, ftn, fimg, ftw;
 };
 
 __device__ __forceinline__ TileGeom tile_geom(const TcConvParams& p, int BN) {
@@ -62,26 +91,33 @@ __device__ __forceinline__ TileGeom tile_geom(const TcConvParams& p, int BN) {
     g.ks = 1;
   }
   g.total = g.tiles_mn * g.ks;
+  g.fks.init(g.ks);
+  g.ftn.init(g.tiles_n);
+  g.fimg.init(g.tiles_img);
+  g.ftw.init(g.tiles_w);
   return g;
 }
 
 struct Tile {
-  int tn, ks, tile_mn, grp, h0, w0, s_begin, s_end;
+  int tn, ks, tile_mn, grp, th, tw, h0, w0, s_begin, s_end;
 };
 
 __device__ __forceinline__ Tile decode_tile(int t, const TcConvParams& p, const TileGeom& g) {
   Tile x;
-  x.ks = t % g.ks;
-  t /= g.ks;
-  x.tile_mn = t;
-  x.tn = t % g.tiles_n;
-  const int tm = t / g.tiles_n;
-  x.grp = tm / g.tiles_img;
-  const int r = tm % g.tiles_img;
-  x.h0 = (r / g.tiles_w) * p.hb;
-  x.w0 = (r % g.tiles_w) * p.wb;
-  x.s_begin = static_cast<int>((static_cast<long long>(g.nk) * x.ks) / g.ks);
-  x.s_end = static_cast<int>((static_cast<long long>(g.nk) * (x.ks + 1)) / g.ks);
+  int tm, r;
+  g.fks.divmod(t, x.tile_mn, x.ks);
+  g.ftn.divmod(x.tile_mn, tm, x.tn);
+  g.fimg.divmod(tm, x.grp, r);
+  g.ftw.divmod(r, x.th, x.tw);
+  x.h0 = x.th * p.hb;
+  x.w0 = x.tw * p.wb;
+  if (g.ks == 1) {
+    x.s_begin = 0;
+    x.s_end = g.nk;
+  } else {  // nk * ks < 2^31
+    x.s_begin = g.fks.div(g.nk * x.ks);
+    x.s_end = g.fks.div(g.nk * (x.ks + 1));
+  }
   return x;
 }
 
@@ -111,38 +147,63 @@ __device__ __forceinline__ void trace_put(const TcConvParams& p, int unit, int f
     p.trace[(blockIdx.x * kTraceUnits + unit) * 8 + field] = clk();
 }
 
+// Tile-invariant part of a tile row's output coordinates: image slot j and
+// pixel offset (dh, dw) inside the ipt x hb x wb box (computed once per thread).
+struct RowGeom {
+  int j, dh, dw;
+  FastDiv fpw;  // halo: padded row pitch
+};
+__device__ __forceinline__ RowGeom row_geom(const TcConvParams& p, int row) {
+  RowGeom rg;
+  rg.fpw.init(p.halo ? p.halo_pw : 1);
+  if (p.plain || p.halo) {
+    rg.j = rg.dh = rg.dw = 0;
+  } else {
+    const int rows_per_img = p.hb * p.wb;
+    rg.j = row / rows_per_img;
+    const int pix = row % rows_per_img;
+    rg.dh = pix / p.wb;
+    rg.dw = pix % p.wb;
+  }
+  return rg;
+}
+
 // Output element offset of tile row `row` (NHWC (n, h, w, 0) or plain row start).
-__device__ __forceinline__ bool out_row(const TcConvParams& p, const TileGeom& g, const Tile& x, int row, size_t& obase) {
+// img: the row's image id (surviving-request slot resolved), img_ok: the
+// tile's image slot exists (the row itself may still lie outside the image).
+__device__ __forceinline__ bool out_row(const TcConvParams& p, const TileGeom& g, const Tile& x, int row,
+                                        const RowGeom& rg, size_t& obase, int& img, bool& img_ok) {
   if (p.plain) {
     const int grow = x.w0 + row;
     obase = static_cast<size_t>(grow) * p.Cout;
-    return grow < g.count;
+    img = grow;
+    img_ok = grow < g.count;
+    return img_ok;
   }
   int idx, h, w;
   if (p.halo) {
     // anchors on the padded row pitch: m = oh * Pw + ow (ow >= Wo are discarded)
     const int m = x.h0 * kBM + row;
-    h = m / p.halo_pw;
-    w = m - h * p.halo_pw;
+    rg.fpw.divmod(m, h, w);
     idx = x.grp;
   } else {
-    const int rows_per_img = p.hb * p.wb;
-    const int j = row / rows_per_img;
-    const int pix = row % rows_per_img;
-    h = x.h0 + pix / p.wb;
-    w = x.w0 + pix % p.wb;
-    idx = x.grp * p.ipt + j;
+    h = x.h0 + rg.dh;
+    w = x.w0 + rg.dw;
+    idx = x.grp * p.ipt + rg.j;
   }
-  const bool valid = (idx < g.count) && (h < p.Ho) && (w < p.Wo);
-  const int n = valid ? (p.surv ? p.surv[idx] : idx) : 0;
+  img_ok = idx < g.count;
+  const bool valid = img_ok && (h < p.Ho) && (w < p.Wo);
+  const int n = img_ok ? (p.surv ? p.surv[idx] : idx) : 0;
+  img = n;
   obase = ((static_cast<size_t>(n) * p.Ho + h) * p.Wo + w) * p.Cout;
   return valid;
 }
 
 // scale/shift, residual (prefetched 16-byte chunks), ReLU, hi/lo split and
 // NHWC store of 16 channels.
-__device__ __forceinline__ void epilogue_math(const TcConvParams& p, float (&v)[16], int co, const uint4* rh,
-                                              const uint4* rl) {
+// sh: the 16 shift values of these columns (shared-memory copy or global), nullable.
+__device__ __forceinline__ void epilogue_math(const TcConvParams& p, float (&v)[16], int co, const float* sh,
+                                              const uint4* rh, const uint4* rl) {
   if (p.scale) {
     const float4* sc = reinterpret_cast<const float4*>(p.scale + co);
 #pragma unroll
@@ -154,11 +215,11 @@ __device__ __forceinline__ void epilogue_math(const TcConvParams& p, float (&v)[
       v[4 * q + 3] *= s4.w;
     }
   }
-  if (p.shift) {
-    const float4* sh = reinterpret_cast<const float4*>(p.shift + co);
+  if (sh) {
+    const float4* sh4 = reinterpret_cast<const float4*>(sh);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const float4 s4 = __ldg(sh + q);
+      const float4 s4 = sh4[q];
       v[4 * q] += s4.x;
       v[4 * q + 1] += s4.y;
       v[4 * q + 2] += s4.z;
@@ -209,7 +270,7 @@ __device__ __forceinline__ void split16(const float (&v)[16], uint4 (&hi)[2], ui
 
 __device__ __forceinline__ void epilogue_store(const TcConvParams& p, float (&v)[16], size_t off, int co,
                                                const uint4* rh, const uint4* rl) {
-  epilogue_math(p, v, co, rh, rl);
+  epilogue_math(p, v, co, p.shift ? p.shift + co : nullptr, rh, rl);
   uint4 hi[2], lo[2];
   __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(hi);
   __nv_bfloat162* l2 = reinterpret_cast<__nv_bfloat162*>(lo);
@@ -272,8 +333,9 @@ __device__ __forceinline__ void rs_step(float (&v)[16], int o, int lane) {
 // lane bits seg/2, seg/4, seg/8 (and seg/16 when seg >= 16), plus a plain
 // add over bit 0 for seg == 32. Value e of a lane is then channel chbase + e
 // (2 live values for seg == 8, else 1).
-__device__ __forceinline__ void gap_segment(const TcConvParams& p, const TileGeom& g, const Tile& x, int row,
-                                            int lane, float (&v)[16], int co) {
+// img / img_ok: this lane's image (every row of a segment lies in one image).
+__device__ __forceinline__ void gap_segment(const TcConvParams& p, const Tile& x, int row, int lane, float (&v)[16],
+                                            int co, int img, bool img_ok) {
   const int rpi = p.halo ? kBM : p.hb * p.wb;  // power of two >= 8
   const int seg = rpi < 32 ? rpi : 32;
   rs_step<16>(v, seg >> 1, lane);
@@ -290,14 +352,12 @@ __device__ __forceinline__ void gap_segment(const TcConvParams& p, const TileGeo
     writer = (lane & 1) == 0;
   }
   const int seg_first = row & ~(seg - 1);  // first row of this lane's segment
-  const int idx = p.halo ? x.grp : x.grp * p.ipt + seg_first / rpi;
-  if (writer && idx < g.count) {
-    const int n = p.surv ? p.surv[idx] : idx;
-    const int pix = seg_first % rpi;
-    const int per_tile = rpi > 32 ? rpi / 32 : 1;
-    const int tile_r = (x.h0 / p.hb) * p.tiles_w + x.w0 / p.wb;
-    const int sg = tile_r * per_tile + pix / 32;
-    float* dst = p.gap_out + (static_cast<size_t>(n) * p.gap_segs + sg) * p.Cout + co + chbase;
+  if (writer && img_ok) {
+    const int pix = seg_first & (rpi - 1);
+    const int per_tile = rpi > 32 ? rpi >> 5 : 1;
+    const int tile_r = x.th * p.tiles_w + x.tw;
+    const int sg = tile_r * per_tile + (pix >> 5);
+    float* dst = p.gap_out + (static_cast<size_t>(img) * p.gap_segs + sg) * p.Cout + co + chbase;
     dst[0] = v[0];
     if (seg == 8) dst[1] = v[1];
   }
@@ -340,14 +400,16 @@ __device__ __noinline__ void split_reduce(const TcConvParams& p, const TileGeom&
       }
     }
     size_t ob;
+    int img;
+    bool img_ok;
     const int co = x.tn * BN + c16 * 16;
-    if (out_row(p, g, x, r, ob)) {
+    if (out_row(p, g, x, r, row_geom(p, r), ob, img, img_ok)) {
       epilogue_store_ld(p, v, ob + co, co);
     } else {
 #pragma unroll
       for (int i = 0; i < 16; ++i) v[i] = 0.0f;
     }
-    if (p.gap_out) gap_segment(p, g, x, r, lane, v, co);
+    if (p.gap_out) gap_segment(p, x, r, lane, v, co, img, img_ok);
   }
   epi_bar();
   if (etid == 0) {
@@ -369,6 +431,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
   // [18,20) tempty, [20,22) halo A-slab full, [22,24) halo A-slab empty
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes + Cfg::kEpiStage);
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 32);
+  float* shift_s = reinterpret_cast<float*>(smem + S * Cfg::kStageBytes + Cfg::kEpiStage + 1024);  // [2][BN]
   const uint32_t full0 = smem_u32(bars);
   const uint32_t empty0 = smem_u32(bars + 8);
   const uint32_t tfull0 = smem_u32(bars + 16);
@@ -676,20 +739,47 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
     const int row = quad * 32 + lane;
     const int etid = threadIdx.x - 64;  // 0..255
     const int col0 = half * kCols;
-    const uint32_t wstage = smem_u32(epi_stage + (warp - 2) * 4096);
+    const uint32_t wstage = smem_u32(epi_stage + (warp - 2) * Cfg::kEpiWarpBytes);
     int acc = 0;
     uint32_t acc_phase = 0;
     int unit = 0;
+    // the output row of the NEXT tile is resolved one tile ahead (its
+    // survivor-id load then overlaps this tile's epilogue)
+    size_t obase_n = 0;
+    bool valid_n = false, img_ok_n = false;
+    int img_n = 0;
+    const RowGeom rg = row_geom(p, row);
+    if (static_cast<int>(blockIdx.x) < g.total)
+      valid_n = out_row(p, g, decode_tile(blockIdx.x, p, g), row, rg, obase_n, img_n, img_ok_n);
     for (int t = blockIdx.x; t < g.total; t += gridDim.x, ++unit) {
       const Tile x = decode_tile(t, p, g);
-      size_t obase;
-      const bool valid = out_row(p, g, x, row, obase);
+      const size_t obase = obase_n;
+      const bool valid = valid_n, img_ok = img_ok_n;
+      const int img = img_n;
+      if (t + static_cast<int>(gridDim.x) < g.total)
+        valid_n = out_row(p, g, decode_tile(t + gridDim.x, p, g), row, rg, obase_n, img_n, img_ok_n);
       const bool split = p.mode == 0 && g.ks > 1;
+      // this tile's shift values -> shared (one coalesced load; the buffer of
+      // tile t-2 is free: every epilogue warp passed this barrier at tile t-1)
+      float* shs = shift_s + acc * BN;
+      if (p.shift && p.mode == 0) {
+        for (int i = etid; i < BN; i += kEpiThreads) shs[i] = __ldg(p.shift + x.tn * BN + i);
+        epi_bar();
+      }
       mbar_wait(tfull0 + 8 * acc, acc_phase);
       tc_fence_after();
       if (etid == 0) trace_put(p, unit, 4);
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * BN + col0;
       const bool empty_k = x.s_end <= x.s_begin;  // no MMA wrote this accumulator
+      // rows this lane stores in the coalesced phase (lane/4 + 8i of the warp's 32)
+      size_t st_ob[4];
+      bool st_ok[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int r = (lane >> 2) + 8 * i;
+        st_ob[i] = __shfl_sync(0xffffffffu, static_cast<unsigned long long>(obase), r);
+        st_ok[i] = __shfl_sync(0xffffffffu, valid ? 1 : 0, r) != 0;
+      }
       // split-K partial tile layout: [tile_mn][ks][BN/16][128 rows][16] (64 B per row chunk)
       float* wsp = split ? p.ws + (static_cast<size_t>(x.tile_mn) * g.ks + x.ks) * kBM * BN : nullptr;
 #pragma unroll 1
@@ -741,7 +831,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
               rl[1] = reinterpret_cast<const uint4*>(p.res_lo + obase + co)[1];
             }
           }
-          epilogue_math(p, v[u], co, r ? rh : nullptr, (r && X3 && p.res_lo) ? rl : nullptr);
+          epilogue_math(p, v[u], co, p.shift ? shs + (co - x.tn * BN) : nullptr, r ? rh : nullptr,
+                        (r && X3 && p.res_lo) ? rl : nullptr);
           if (!valid) {
 #pragma unroll
             for (int i = 0; i < 16; ++i) v[u][i] = 0.0f;
@@ -761,19 +852,17 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const int r = (lane >> 2) + 8 * i;  // row within the warp
-            const unsigned long long ob = __shfl_sync(0xffffffffu, static_cast<unsigned long long>(obase), r);
-            const int ok = __shfl_sync(0xffffffffu, valid ? 1 : 0, r);
             const uint32_t off = static_cast<uint32_t>(r * 64 + ((ch ^ ((r >> 1) & 3)) * 16));
-            if (ok && !dbg_nostore) {
-              *reinterpret_cast<uint4*>(p.out_hi + ob + cb + ch * 8) = ld_shared_v4(wstage + off);
+            if (st_ok[i] && !dbg_nostore) {
+              *reinterpret_cast<uint4*>(p.out_hi + st_ob[i] + cb + ch * 8) = ld_shared_v4(wstage + off);
               if (X3 && p.out_lo)
-                *reinterpret_cast<uint4*>(p.out_lo + ob + cb + ch * 8) = ld_shared_v4(wstage + 2048 + off);
+                *reinterpret_cast<uint4*>(p.out_lo + st_ob[i] + cb + ch * 8) = ld_shared_v4(wstage + 2048 + off);
             }
           }
         }
         if (p.gap_out) {
-          gap_segment(p, g, x, row, lane, v[0], cb);  // destroys v (after staging)
-          gap_segment(p, g, x, row, lane, v[1], cb + 16);
+          gap_segment(p, x, row, lane, v[0], cb, img, img_ok);  // destroys v (after staging)
+          gap_segment(p, x, row, lane, v[1], cb + 16, img, img_ok);
         }
       }
       tc_fence_before();

@@ -493,7 +493,7 @@ static void perf_conv(const char* name, int N, int nsurv, int H, int W, int C, i
   p.count = dCnt;
   p.count_static = N;
   p.mode = 0;
-  p.scale = dScale;
+  p.scale = nullptr;  // the engine folds the BN scale into the weights
   p.shift = dShift;
   p.res_hi = use_res ? r_hi : nullptr;
   p.res_lo = use_res && x3 ? r_lo : nullptr;
