@@ -534,8 +534,10 @@ void Engine::add_lookup_steps(std::vector<Step>& steps, DevCache& c, const TapVi
                      p.prob = cp->prob;
                      p.hit = cp->hit;
                      p.label = cp->label;
-                     p.pr_out = cp->pr_out;
-                     p.logits_out = cp->logits_out;
+                     if (!exv.arrive) {  // lookup-only entry point returns pr/logits; serving does not
+                       p.pr_out = cp->pr_out;
+                       p.logits_out = cp->logits_out;
+                     }
                      p.fc_scratch = cp->fc_scratch;
                      if (head_gap) {
                        p.gap = cp->gap;

@@ -1,6 +1,7 @@
 // Serve-path kernels (see serve_kernels.cuh). All cache-head arithmetic is
 // fp32 with deterministic (fixed-order) reductions; only the activations are
 // bf16 hi (+lo) planes.
+#include "pdl.cuh"
 #include "serve_kernels.cuh"
 
 #include <cfloat>
@@ -101,6 +102,8 @@ __device__ float block_max(float v, float* scratch) {
 // Case A: win divides HW -> bins are channel strips; each thread owns whole
 // strips of 8 channels and streams them (16-byte loads).
 __global__ void pool_strips_kernel(TapView t, int win, int width, float inv, float* bins) {
+  pdl_wait();
+  pdl_trigger();
   const int r = blockIdx.x;
   if (r >= *t.count) return;
   const long long n = t.data_idx ? t.data_idx[r] : r;
@@ -125,6 +128,8 @@ __global__ void pool_strips_kernel(TapView t, int win, int width, float inv, flo
 // Case B: win = gch * HW (gch divides 64): per-channel totals over 32 pixel
 // ranges, combined in a fixed order, then gch channels per bin.
 __global__ void pool_channels_kernel(TapView t, int gch, int width, float inv, float* bins) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float part[32][65];
   __shared__ float tot[64];
   const int r = blockIdx.x;
@@ -303,6 +308,8 @@ __device__ void tap_gap_block(const TapView& t, long long rowb, int C, int HW, f
 // the batched logits GEMM reads them): bins[r][c], one CTA per row.
 __global__ void __launch_bounds__(kLk) gap_bins_kernel(const float* gap, int segs, int C, float inv,
                                                        const int* data_idx, const int* count, float* bins) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ float feat_s[];
   __shared__ float4 red[kLk];
   const int r = blockIdx.x;
@@ -314,6 +321,8 @@ __global__ void __launch_bounds__(kLk) gap_bins_kernel(const float* gap, int seg
 
 // Generic: one thread per bin, sequential over its flat window.
 __global__ void pool_generic_kernel(TapView t, int win, int width, float inv, float* bins) {
+  pdl_wait();
+  pdl_trigger();
   const int r = blockIdx.x;
   if (r >= *t.count) return;
   const long long n = t.data_idx ? t.data_idx[r] : r;
@@ -335,6 +344,8 @@ __global__ void pool_generic_kernel(TapView t, int win, int width, float inv, fl
 __global__ void conv1d_partials_kernel(TapView t, long long D, int kernel, int stride, int out_dim, const float* w1,
                                        float b1, const float* W2, int classes, int chunk_elems, int nchunks,
                                        float* partials) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ float xs[];
   __shared__ float red[32];
   const int r = blockIdx.x;
@@ -401,11 +412,78 @@ constexpr int kFcBM = 32, kFcBN = 128, kFcBK = 32;
 
 __host__ __device__ inline int rows_fc_slice(int feat) { return feat <= 512 ? 64 : (feat <= 1024 ? 128 : 256); }
 
+// One K-chunk of the A and W tiles into registers: A row tid/8, W classes
+// tid/8 + 32 i, 4 consecutive o at (tid % 8) * 4.
+template <int kMode>
+__device__ __forceinline__ void rows_fc_load(const float* __restrict__ A, long long lda, int ks, long long part_stride,
+                                             const float* __restrict__ b1, int feat, const float* __restrict__ W,
+                                             int classes, int n, int r0, int k0, int o0, int oz1, bool vec,
+                                             float (&va)[4], float (&vw)[4][4]) {
+  const int tid = threadIdx.x;
+  const int oo = (tid & 7) * 4;
+  {
+    const int r = r0 + (tid >> 3);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) va[e] = 0.0f;
+    if (r < n) {
+      if (vec && o0 + oo + 4 <= oz1) {
+        if (kMode == 0) {
+          const float4 f = __ldg(reinterpret_cast<const float4*>(A + static_cast<long long>(r) * lda + o0 + oo));
+          va[0] = f.x, va[1] = f.y, va[2] = f.z, va[3] = f.w;
+        } else {
+          const float4 bb = __ldg(reinterpret_cast<const float4*>(b1 + o0 + oo));
+          va[0] = bb.x, va[1] = bb.y, va[2] = bb.z, va[3] = bb.w;
+          for (int s = 0; s < ks; ++s) {
+            const float4 f = __ldg(reinterpret_cast<const float4*>(A + static_cast<long long>(s) * part_stride +
+                                                                   static_cast<long long>(r) * lda + o0 + oo));
+            va[0] += f.x, va[1] += f.y, va[2] += f.z, va[3] += f.w;
+          }
+#pragma unroll
+          for (int e = 0; e < 4; ++e) va[e] = va[e] > 0.0f ? va[e] : 0.0f;
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int o = o0 + oo + e;
+          if (o < oz1) {
+            if (kMode == 0) {
+              va[e] = A[static_cast<long long>(r) * lda + o];
+            } else {
+              float a = b1[o];
+              for (int s = 0; s < ks; ++s)
+                a += A[static_cast<long long>(s) * part_stride + static_cast<long long>(r) * lda + o];
+              va[e] = a > 0.0f ? a : 0.0f;
+            }
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int k = k0 + (tid >> 3) + 32 * i;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) vw[i][e] = 0.0f;
+    if (k < classes) {
+      if (vec && o0 + oo + 4 <= oz1) {
+        const float4 f = __ldg(reinterpret_cast<const float4*>(W + static_cast<long long>(k) * feat + o0 + oo));
+        vw[i][0] = f.x, vw[i][1] = f.y, vw[i][2] = f.z, vw[i][3] = f.w;
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (o0 + oo + e < oz1) vw[i][e] = W[static_cast<long long>(k) * feat + o0 + oo + e];
+      }
+    }
+  }
+}
+
 template <int kMode>
 __global__ void __launch_bounds__(256) rows_fc_kernel(const float* __restrict__ A, long long lda, int ks,
                                                       long long part_stride, const float* __restrict__ b1, int feat,
                                                       int kslice, const float* __restrict__ W, int classes,
                                                       const int* count, long long max_rows, float* out) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ __align__(16) float As[kFcBK][kFcBM + 4];
   __shared__ __align__(16) float Ws[kFcBK][kFcBN + 4];
   const int n = *count;
@@ -420,66 +498,22 @@ __global__ void __launch_bounds__(256) rows_fc_kernel(const float* __restrict__ 
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
+  float va[4], vw[4][4];
+  // register double buffering: chunk c+1 is in flight while chunk c is multiplied
+  rows_fc_load<kMode>(A, lda, ks, part_stride, b1, feat, W, classes, n, r0, k0, oz0, oz1, vec, va, vw);
   for (int o0 = oz0; o0 < oz1; o0 += kFcBK) {
-    {  // A tile: row tid/8, 4 consecutive o at (tid%8)*4
+    {
       const int rr = tid >> 3, oo = (tid & 7) * 4;
-      const int r = r0 + rr;
-      float v[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-      if (r < n) {
-        if (vec && o0 + oo + 4 <= oz1) {
-          if (kMode == 0) {
-            const float4 f = __ldg(reinterpret_cast<const float4*>(A + static_cast<long long>(r) * lda + o0 + oo));
-            v[0] = f.x, v[1] = f.y, v[2] = f.z, v[3] = f.w;
-          } else {
-            const float4 bb = __ldg(reinterpret_cast<const float4*>(b1 + o0 + oo));
-            v[0] = bb.x, v[1] = bb.y, v[2] = bb.z, v[3] = bb.w;
-            for (int s = 0; s < ks; ++s) {
-              const float4 f = __ldg(reinterpret_cast<const float4*>(A + static_cast<long long>(s) * part_stride +
-                                                                     static_cast<long long>(r) * lda + o0 + oo));
-              v[0] += f.x, v[1] += f.y, v[2] += f.z, v[3] += f.w;
-            }
 #pragma unroll
-            for (int e = 0; e < 4; ++e) v[e] = v[e] > 0.0f ? v[e] : 0.0f;
-          }
-        } else {
+      for (int e = 0; e < 4; ++e) As[oo + e][rr] = va[e];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int o = o0 + oo + e;
-            if (o < oz1) {
-              if (kMode == 0) {
-                v[e] = A[static_cast<long long>(r) * lda + o];
-              } else {
-                float a = b1[o];
-                for (int s = 0; s < ks; ++s)
-                  a += A[static_cast<long long>(s) * part_stride + static_cast<long long>(r) * lda + o];
-                v[e] = a > 0.0f ? a : 0.0f;
-              }
-            }
-          }
-        }
-      }
+      for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) As[oo + e][rr] = v[e];
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {  // W tile: class (tid/8) + 32 i, 4 consecutive o
-      const int kk = (tid >> 3) + 32 * i, oo = (tid & 7) * 4;
-      const int k = k0 + kk;
-      float v[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-      if (k < classes) {
-        if (vec && o0 + oo + 4 <= oz1) {
-          const float4 f = __ldg(reinterpret_cast<const float4*>(W + static_cast<long long>(k) * feat + o0 + oo));
-          v[0] = f.x, v[1] = f.y, v[2] = f.z, v[3] = f.w;
-        } else {
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            if (o0 + oo + e < oz1) v[e] = W[static_cast<long long>(k) * feat + o0 + oo + e];
-        }
-      }
-#pragma unroll
-      for (int e = 0; e < 4; ++e) Ws[oo + e][kk] = v[e];
+        for (int e = 0; e < 4; ++e) Ws[oo + e][rr + 32 * i] = vw[i][e];
     }
     __syncthreads();
+    if (o0 + kFcBK < oz1)
+      rows_fc_load<kMode>(A, lda, ks, part_stride, b1, feat, W, classes, n, r0, k0, o0 + kFcBK, oz1, vec, va, vw);
     const int olim = oz1 - o0 < kFcBK ? oz1 - o0 : kFcBK;
 #pragma unroll 4
     for (int o = 0; o < olim; ++o) {
@@ -517,6 +551,8 @@ __device__ __forceinline__ float fc_logit(const float* part, int nz, long long z
 // image ids[r]) -> feats [rows][C] (the base head's GAP), one CTA per row.
 __global__ void __launch_bounds__(kLk) gap_rows_kernel(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int C, int HW,
                                                        const int* ids, const int* count, float* feats) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ float feat_s[];
   __shared__ float red[kLk * 8];
   const int r = blockIdx.x;
@@ -537,6 +573,7 @@ __device__ void block_logits(const float* __restrict__ W, const float* __restric
     const float* wr = W + static_cast<long long>(k) * nf;
     float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
     int o = lane;
+#pragma unroll 4
     for (; o + 96 < nf; o += 128) {
       a0 += __ldg(wr + o) * feat[o];
       a1 += __ldg(wr + o + 32) * feat[o + 32];
@@ -599,7 +636,8 @@ __device__ void head_block(const CacheHeadParams& p, int r, const float* logits,
     const float* wr = p.Ws1 + j * C;
     float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
     int k = lane;
-    for (; k + 96 < C; k += 128) {
+#pragma unroll 4
+    for (; k + 96 < C; k += 128) {  // unrolled: 16 independent weight loads in flight per lane
       a0 += __ldg(wr + k) * pr[k];
       a1 += __ldg(wr + k + 32) * pr[k + 32];
       a2 += __ldg(wr + k + 64) * pr[k + 64];
@@ -704,6 +742,8 @@ __device__ void exit_tail(const ExitParams& e, int n, const float* prob, const i
 // the Conv(k,s) chunk partials, or the pooled bins / FC(h) hidden partials.
 // With p.ex.arrive the last CTA also runs the exit + compaction.
 __global__ void __launch_bounds__(kLk) cache_head_kernel(CacheHeadParams p) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ float sm[];
   __shared__ HeadSmem hs;
   __shared__ float4 red4[kLk];
@@ -748,6 +788,8 @@ __global__ void __launch_bounds__(kLk) cache_head_kernel(CacheHeadParams p) {
 
 __global__ void gather_rows_kernel(const __nv_bfloat16* src_hi, const __nv_bfloat16* src_lo, __nv_bfloat16* dst_hi,
                                    __nv_bfloat16* dst_lo, long long row_elems, const int* src_rows, const int* count) {
+  pdl_wait();
+  pdl_trigger();
   const int j = blockIdx.x;
   if (j >= *count) return;
   const long long s = src_rows[j];
@@ -764,6 +806,8 @@ __global__ void gather_rows_kernel(const __nv_bfloat16* src_hi, const __nv_bfloa
 
 __global__ void split_rows_kernel(const float* x, int in_dim, int dp, const int* ids, const int* count,
                                   __nv_bfloat16* hi, __nv_bfloat16* lo) {
+  pdl_wait();
+  pdl_trigger();
   const int j = blockIdx.x;
   if (j >= *count) return;
   const long long src = ids ? ids[j] : j;
@@ -775,6 +819,8 @@ __global__ void split_rows_kernel(const float* x, int in_dim, int dp, const int*
 
 __global__ void split_taps_nchw_kernel(const float* x, int C, int HW, long long row_stride, __nv_bfloat16* hi,
                                        __nv_bfloat16* lo) {
+  pdl_wait();
+  pdl_trigger();
   const int r = blockIdx.x;
   const long long D = static_cast<long long>(C) * HW;
   for (long long i = blockIdx.y * blockDim.x + threadIdx.x; i < row_stride; i += gridDim.y * blockDim.x) {
@@ -796,6 +842,8 @@ __global__ void __launch_bounds__(kLk) base_head_kernel(const __nv_bfloat16* hi,
                                                         int* base_pred, float* logits_out, int* exit_layer, int* served,
                                                         unsigned long long* exit_ns, const float* pre_logits,
                                                         int pre_nz, long long pre_zstride) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ float sm[];
   __shared__ float red[kLk * 8];
   __shared__ int bi_s[32];
@@ -872,6 +920,8 @@ __global__ void __launch_bounds__(kLk) base_head_kernel(const __nv_bfloat16* hi,
 // One thread per (output pixel, 8 consecutive K entries): 16-byte stores.
 __global__ void stem_im2col_kernel(const float* x, const int* count, int C, int H, int W, int k, int stride, int pad,
                                    int Ho, int Wo, int Kp, __nv_bfloat16* hi, __nv_bfloat16* lo) {
+  pdl_wait();
+  pdl_trigger();
   const int kg = Kp / 8;
   const int pix = Ho * Wo;
   const long long total = static_cast<long long>(*count) * pix * kg;
@@ -914,6 +964,8 @@ __global__ void stem_im2col_kernel(const float* x, const int* count, int C, int 
 __global__ void phase_split_kernel(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int H, int W, int C, int N,
                                    int Hs, int Ws, const int* ids, const int* count, __nv_bfloat16* ohi,
                                    __nv_bfloat16* olo) {
+  pdl_wait();
+  pdl_trigger();
   const int j = blockIdx.x;
   if (j >= *count) return;
   const long long n = ids[j];
@@ -942,6 +994,8 @@ __global__ void phase_split_kernel(const __nv_bfloat16* hi, const __nv_bfloat16*
 __global__ void maxpool_kernel(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int H, int W, int C, int k, int stride,
                                int pad, int Ho, int Wo, const int* ids, const int* count, __nv_bfloat16* ohi,
                                __nv_bfloat16* olo) {
+  pdl_wait();
+  pdl_trigger();
   // One thread per (output pixel, 8 channels): 16-byte loads/stores; per
   // channel the first maximum in (r, s) order wins (hi and lo move together).
   const int j = blockIdx.x;
@@ -987,11 +1041,15 @@ __global__ void maxpool_kernel(const __nv_bfloat16* hi, const __nv_bfloat16* lo,
   }
 }
 
-__global__ void stamp_kernel(unsigned long long* t0) { *t0 = globaltimer(); }
+__global__ void stamp_kernel(unsigned long long* t0) {
+  pdl_wait();
+  pdl_trigger(); *t0 = globaltimer(); }
 
 __global__ void init_batch_kernel(const int* batch, int max_batch, int* ids0, int* count0, int* rows_out, int rows_mult,
                                   int* exit_layer, int* served, int* base_pred, unsigned long long* exit_ns,
                                   float* probs, int L) {
+  pdl_wait();
+  pdl_trigger();
   const int B = *batch;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < max_batch; i += gridDim.x * blockDim.x) {
     ids0[i] = i;
@@ -1013,12 +1071,12 @@ void launch_pool_bins(const TapView& tap, int max_rows, int win, int width, floa
   const float inv = static_cast<float>(1.0 / win);
   if (max_rows <= 0) return;
   if (tap.HW > 1 && tap.C % 64 == 0 && win <= tap.HW && tap.HW % win == 0 && tap.HW / win >= 32) {
-    pool_strips_kernel<<<dim3(max_rows, tap.C / 64), 256, 0, s>>>(tap, win, width, inv, bins);
+    launch_pdl(pool_strips_kernel, dim3(dim3(max_rows, tap.C / 64)), dim3(256), 0, s, tap, win, width, inv, bins);
   } else if (tap.HW > 1 && tap.C % 64 == 0 && win % tap.HW == 0 && 64 % (win / tap.HW) == 0) {
-    pool_channels_kernel<<<dim3(max_rows, tap.C / 64), 256, 0, s>>>(tap, win / tap.HW, width, inv, bins);
+    launch_pdl(pool_channels_kernel, dim3(dim3(max_rows, tap.C / 64)), dim3(256), 0, s, tap, win / tap.HW, width, inv, bins);
   } else {
     const int gy = (width + 255) / 256 < 64 ? (width + 255) / 256 : 64;
-    pool_generic_kernel<<<dim3(max_rows, gy), 256, 0, s>>>(tap, win, width, inv, bins);
+    launch_pdl(pool_generic_kernel, dim3(dim3(max_rows, gy)), dim3(256), 0, s, tap, win, width, inv, bins);
   }
 }
 
@@ -1026,7 +1084,7 @@ void launch_gap_bins(const float* gap, int segs, int C, int HW, const int* data_
                      float* bins, cudaStream_t s) {
   if (max_rows <= 0) return;
   const float inv = static_cast<float>(1.0 / HW);
-  gap_bins_kernel<<<max_rows, kLk, static_cast<size_t>(C) * sizeof(float), s>>>(gap, segs, C, inv, data_idx, count,
+  launch_pdl(gap_bins_kernel, dim3(max_rows), dim3(kLk), static_cast<size_t>(C) * sizeof(float), s, gap, segs, C, inv, data_idx, count,
                                                                                  bins);
 }
 
@@ -1040,7 +1098,7 @@ void launch_conv1d_partials(const TapView& tap, int max_rows, long long D, int k
     cudaFuncSetAttribute(conv1d_partials_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  conv1d_partials_kernel<<<dim3(max_rows, nchunks), 256, smem, s>>>(tap, D, kernel, stride, out_dim, w1, b1, W2,
+  launch_pdl(conv1d_partials_kernel, dim3(dim3(max_rows, nchunks)), dim3(256), smem, s, tap, D, kernel, stride, out_dim, w1, b1, W2,
                                                                     classes, chunk_elems, nchunks, partials);
 }
 
@@ -1054,10 +1112,10 @@ void launch_rows_fc(const float* A, long long lda, int ks, long long part_stride
   if (max_rows <= 0) return;
   const dim3 grid((classes + kFcBN - 1) / kFcBN, (max_rows + kFcBM - 1) / kFcBM, rows_fc_splits(feat));
   if (ks > 0)
-    rows_fc_kernel<1><<<grid, 256, 0, s>>>(A, lda, ks, part_stride, b1, feat, rows_fc_slice(feat), W, classes, count,
+    launch_pdl(rows_fc_kernel<1>, dim3(grid), dim3(256), 0, s, A, lda, ks, part_stride, b1, feat, rows_fc_slice(feat), W, classes, count,
                                            max_rows, out);
   else
-    rows_fc_kernel<0><<<grid, 256, 0, s>>>(A, lda, 0, 0, nullptr, feat, rows_fc_slice(feat), W, classes, count,
+    launch_pdl(rows_fc_kernel<0>, dim3(grid), dim3(256), 0, s, A, lda, 0, 0, nullptr, feat, rows_fc_slice(feat), W, classes, count,
                                            max_rows, out);
 }
 
@@ -1083,7 +1141,7 @@ void launch_cache_head(const CacheHeadParams& p_in, int max_rows, cudaStream_t s
     cudaFuncSetAttribute(cache_head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     attr = true;
   }
-  cache_head_kernel<<<max_rows, kLk, smem, s>>>(p);
+  launch_pdl(cache_head_kernel, dim3(max_rows), dim3(kLk), smem, s, p);
 }
 
 bool fused_lookup_supported(int classes, int C, int max_rows) {
@@ -1097,13 +1155,13 @@ void launch_gather_rows(const __nv_bfloat16* src_hi, const __nv_bfloat16* src_lo
   const long long nv = row_elems / 8;
   int gy = static_cast<int>((nv + 255) / 256);
   if (gy > 64) gy = 64;
-  gather_rows_kernel<<<dim3(max_rows, gy), 256, 0, s>>>(src_hi, src_lo, dst_hi, dst_lo, row_elems, src_rows, count);
+  launch_pdl(gather_rows_kernel, dim3(dim3(max_rows, gy)), dim3(256), 0, s, src_hi, src_lo, dst_hi, dst_lo, row_elems, src_rows, count);
 }
 
 void launch_split_rows(const float* x, int in_dim, int dp, const int* ids, const int* count, int max_rows,
                        __nv_bfloat16* hi, __nv_bfloat16* lo, cudaStream_t s) {
   if (max_rows <= 0) return;
-  split_rows_kernel<<<max_rows, 256, 0, s>>>(x, in_dim, dp, ids, count, hi, lo);
+  launch_pdl(split_rows_kernel, dim3(max_rows), dim3(256), 0, s, x, in_dim, dp, ids, count, hi, lo);
 }
 
 void launch_split_taps_nchw(const float* x, int C, int HW, int rows, long long row_stride, __nv_bfloat16* hi,
@@ -1111,7 +1169,7 @@ void launch_split_taps_nchw(const float* x, int C, int HW, int rows, long long r
   if (rows <= 0) return;
   int gy = static_cast<int>((row_stride + 255) / 256);
   if (gy > 128) gy = 128;
-  split_taps_nchw_kernel<<<dim3(rows, gy), 256, 0, s>>>(x, C, HW, row_stride, hi, lo);
+  launch_pdl(split_taps_nchw_kernel, dim3(dim3(rows, gy)), dim3(256), 0, s, x, C, HW, row_stride, hi, lo);
 }
 
 void launch_mlp_head(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int dp, int dim, const float* W, const float* b,
@@ -1119,7 +1177,7 @@ void launch_mlp_head(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int dp, i
                      int* exit_layer, int* served, unsigned long long* exit_ns, cudaStream_t s) {
   if (max_rows <= 0) return;
   const size_t smem = static_cast<size_t>(dim + classes) * sizeof(float);
-  base_head_kernel<false><<<max_rows, kLk, smem, s>>>(hi, lo, dp, dim, 1, W, b, classes, ids, count, base_pred,
+  launch_pdl(base_head_kernel<false>, dim3(max_rows), dim3(kLk), smem, s, hi, lo, dp, dim, 1, W, b, classes, ids, count, base_pred,
                                                       logits_out, exit_layer, served, exit_ns, nullptr, 0, 0);
 }
 
@@ -1131,13 +1189,13 @@ void launch_cnn_head(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int C, in
   const float* pre = nullptr;
   if (classes > 32 && feats_scratch && logits_scratch) {
     // Many classes: GAP rows, one batched logits GEMM, then the per-row softmax/argmax.
-    gap_rows_kernel<<<max_rows, kLk, static_cast<size_t>(C) * sizeof(float), s>>>(hi, lo, C, HW, ids, count,
+    launch_pdl(gap_rows_kernel, dim3(max_rows), dim3(kLk), static_cast<size_t>(C) * sizeof(float), s, hi, lo, C, HW, ids, count,
                                                                                   feats_scratch);
     launch_rows_fc(feats_scratch, C, 0, 0, nullptr, C, W, classes, count, max_rows, logits_scratch, s);
     pre = logits_scratch;
   }
   const size_t smem = static_cast<size_t>(C + classes) * sizeof(float);
-  base_head_kernel<true><<<max_rows, kLk, smem, s>>>(hi, lo, static_cast<long long>(C) * HW, C, HW, W, b, classes, ids,
+  launch_pdl(base_head_kernel<true>, dim3(max_rows), dim3(kLk), smem, s, hi, lo, static_cast<long long>(C) * HW, C, HW, W, b, classes, ids,
                                                      count, base_pred, logits_out, exit_layer, served, exit_ns, pre,
                                                      rows_fc_splits(C), static_cast<long long>(max_rows) * classes);
 }
@@ -1148,7 +1206,7 @@ void launch_stem_im2col(const float* x, const int* count, int max_n, int C, int 
   long long blocks = (total + 255) / 256;
   if (blocks > 148 * 32) blocks = 148 * 32;
   if (blocks < 1) blocks = 1;
-  stem_im2col_kernel<<<static_cast<int>(blocks), 256, 0, s>>>(x, count, C, H, W, k, stride, pad, Ho, Wo, Kp, hi, lo);
+  launch_pdl(stem_im2col_kernel, dim3(static_cast<int>(blocks)), dim3(256), 0, s, x, count, C, H, W, k, stride, pad, Ho, Wo, Kp, hi, lo);
 }
 
 void launch_phase_split(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int H, int W, int C, int N, int Hs, int Ws,
@@ -1158,7 +1216,7 @@ void launch_phase_split(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int H,
   const long long per = 4LL * Hs * Ws * (C / 8);
   int gy = static_cast<int>((per + 255) / 256);
   if (gy > 64) gy = 64;
-  phase_split_kernel<<<dim3(max_rows, gy), 256, 0, s>>>(hi, lo, H, W, C, N, Hs, Ws, ids, count, ohi, olo);
+  launch_pdl(phase_split_kernel, dim3(dim3(max_rows, gy)), dim3(256), 0, s, hi, lo, H, W, C, N, Hs, Ws, ids, count, ohi, olo);
 }
 
 void launch_maxpool(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int H, int W, int C, int k, int stride, int pad,
@@ -1168,16 +1226,16 @@ void launch_maxpool(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int H, int
   const long long per = static_cast<long long>(Ho) * Wo * (C / 8);
   int gy = static_cast<int>((per + 255) / 256);
   if (gy > 128) gy = 128;
-  maxpool_kernel<<<dim3(max_rows, gy), 256, 0, s>>>(hi, lo, H, W, C, k, stride, pad, Ho, Wo, ids, count, ohi, olo);
+  launch_pdl(maxpool_kernel, dim3(dim3(max_rows, gy)), dim3(256), 0, s, hi, lo, H, W, C, k, stride, pad, Ho, Wo, ids, count, ohi, olo);
 }
 
-void launch_stamp_start(unsigned long long* t0, cudaStream_t s) { stamp_kernel<<<1, 1, 0, s>>>(t0); }
+void launch_stamp_start(unsigned long long* t0, cudaStream_t s) { launch_pdl(stamp_kernel, dim3(1), dim3(1), 0, s, t0); }
 
 void launch_init_batch(const int* batch, int max_batch, int* ids0, int* count0, int* rows_out, int rows_mult,
                        int* exit_layer, int* served, int* base_pred, unsigned long long* exit_ns, float* probs, int L,
                        cudaStream_t s) {
   const int blocks = (max_batch + 255) / 256 > 0 ? (max_batch + 255) / 256 : 1;
-  init_batch_kernel<<<blocks, 256, 0, s>>>(batch, max_batch, ids0, count0, rows_out, rows_mult, exit_layer, served,
+  launch_pdl(init_batch_kernel, dim3(blocks), dim3(256), 0, s, batch, max_batch, ids0, count0, rows_out, rows_mult, exit_layer, served,
                                            base_pred, exit_ns, probs, L);
 }
 

@@ -7,6 +7,7 @@
 //                 column half (w - 2) / 4 of the tile (two warps per quadrant)
 // Pipelines: smem ring full/empty (TMA <-> MMA), TMEM double buffer
 // tfull/tempty (MMA <-> epilogue), split-K tile counters (CTA <-> CTA).
+#include "pdl.cuh"
 #include "sm100_prims.cuh"
 #include "tc_conv.cuh"
 
@@ -481,6 +482,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  // everything above is independent of upstream kernels (programmatic launch)
+  pdl_wait();
+  pdl_trigger();
 
   const TileGeom g = tile_geom(p, BN);
   const int cchunks = p.C / 64;
@@ -912,8 +916,7 @@ cudaError_t launch_cfg(const TcConvParams& p, int num_sms, cudaStream_t stream) 
   if (p.mode == 0 && p.ks_max > 1) tiles *= p.ks_max;
   if (tiles <= 0) return cudaSuccess;
   const int grid = tiles < num_sms ? static_cast<int>(tiles) : num_sms;
-  tc_conv_kernel<BN, X3><<<grid, kThreads, Cfg::kSmem, stream>>>(p);
-  return cudaGetLastError();
+  return launch_pdl(tc_conv_kernel<BN, X3>, dim3(grid), dim3(kThreads), Cfg::kSmem, stream, p);
 }
 
 }  // namespace

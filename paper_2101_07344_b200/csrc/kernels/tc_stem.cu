@@ -6,6 +6,7 @@
 //   warp 1     : MMA issuer (lane 0): k'^2 taps x {1, 3} MMAs (M128 N64 K16)
 //   warps 2..5 : epilogue (TMEM lane quadrant warp % 4): folded BN, ReLU,
 //                hi/lo split, NHWC store of the valid anchors
+#include "pdl.cuh"
 #include "sm100_prims.cuh"
 #include "tc_stem.cuh"
 
@@ -92,6 +93,8 @@ __global__ void __launch_bounds__(192, 1) tc_stem_kernel(const __grid_constant__
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  pdl_wait();  // programmatic launch: the prologue above overlaps the previous kernel
+  pdl_trigger();
 
   const int count = *p.count;
   const int total = count * p.tiles_per_img;
@@ -250,6 +253,8 @@ __global__ void __launch_bounds__(192, 1) tc_stem_kernel(const __grid_constant__
 // One thread per (image, channel group, X pixel): 8 channels -> 16-byte stores.
 __global__ void stem_s2d_kernel(const float* x, const int* count, int C, int H, int W, int stride, int pad, int Hx,
                                 int Wx, __nv_bfloat16* x_hi, __nv_bfloat16* x_lo) {
+  pdl_wait();
+  pdl_trigger();
   const long long HWx = static_cast<long long>(Hx) * Wx;
   const long long total = static_cast<long long>(*count) * 2 * HWx;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
@@ -339,7 +344,7 @@ void launch_stem_s2d(const float* x, const int* count, int max_n, int C, int H, 
   long long blocks = (total + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
-  stem_s2d_kernel<<<static_cast<int>(blocks), 256, 0, s>>>(x, count, C, H, W, stride, pad, g.Hx, g.Wx, x_hi, x_lo);
+  launch_pdl(stem_s2d_kernel, dim3(static_cast<int>(blocks)), dim3(256), 0, s, x, count, C, H, W, stride, pad, g.Hx, g.Wx, x_hi, x_lo);
 }
 
 cudaError_t tc_stem_launch(const StemParams& p, int num_sms, cudaStream_t stream) {
@@ -354,12 +359,12 @@ cudaError_t tc_stem_launch(const StemParams& p, int num_sms, cudaStream_t stream
     cudaError_t e = cudaFuncSetAttribute(tc_stem_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    tc_stem_kernel<true><<<grid, 192, smem, stream>>>(p);
+    launch_pdl(tc_stem_kernel<true>, dim3(grid), dim3(192), smem, stream, p);
   } else {
     cudaError_t e = cudaFuncSetAttribute(tc_stem_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    tc_stem_kernel<false><<<grid, 192, smem, stream>>>(p);
+    launch_pdl(tc_stem_kernel<false>, dim3(grid), dim3(192), smem, stream, p);
   }
   return cudaGetLastError();
 }
