@@ -300,25 +300,45 @@ def main():
     tc = prof["kind"] == 1
     tc_ms = float(prof["ms"][tc].sum())
     tc_flops = float(prof["flops"][tc].sum())
+    tc_bytes = float(prof["bytes"][tc].sum())
     lk = prof["kind"] == 2
     lk_ms = float(prof["ms"][lk].sum())
     lk_bytes = float(prof["bytes"][lk].sum())
     step_ms = float(prof["ms"].sum())
     hbm, bf16_burst, bf16_sus, peak_src = load_peaks()
     mma_factor = 3.0 if args.precision == "bf16x3" else 1.0
-    achieved = tc_flops / (tc_ms * 1e-3) / 1e12 if tc_ms else 0.0
+    # Per contraction launch: tensor floor (MMA FLOPs at the bf16 peak) and HBM
+    # floor (algorithmic bytes: input + output + residual once, at the copy
+    # bandwidth); the binding floor summed over launches / their measured time
+    # is the combined roofline fraction.
+    t_tc = prof["flops"][tc] * mma_factor / (bf16_burst * 1e12) * 1e3
+    t_hbm = prof["bytes"][tc] / (hbm * 1e9) * 1e3
+    floor_ms = float(np.maximum(t_tc, t_hbm).sum())
+    bound = "tensor" if float(t_tc.sum()) >= float(t_hbm.sum()) else "hbm"
+    ach_tf = tc_flops / (tc_ms * 1e-3) / 1e12 if tc_ms else 0.0
+    ach_gb = tc_bytes / (tc_ms * 1e-3) / 1e9 if tc_ms else 0.0
     traffic = None
     tpath = os.path.join(ROOT, "profiles", f"traffic_{args.config}_{args.precision}.json")
     if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
-    roofline = {"bound": "tensor", "kernel": "tc_conv_kernel (tcgen05 implicit-GEMM conv)",
-                "achieved": achieved, "peak": bf16_burst, "unit": "TFLOP/s", "frac": achieved / bf16_burst,
-                "traffic": traffic, "peak_source": f"{peak_src} bf16 burst (MEASURED_PEAKS.json)",
+        traffic = json.load(open(tpath)).get("dram_bytes_per_step")
+    roofline = {"bound": bound, "kernel": "tc_conv_kernel + tc_stem_kernel (tcgen05 implicit-GEMM convs)",
+                "achieved": ach_tf if bound == "tensor" else ach_gb,
+                "peak": bf16_burst if bound == "tensor" else hbm,
+                "unit": "TFLOP/s" if bound == "tensor" else "GB/s",
+                "frac": (ach_tf * mma_factor / bf16_burst) if bound == "tensor" else ach_gb / hbm,
+                "traffic": traffic, "algorithmic_bytes_per_step": tc_bytes,
+                "peak_source": f"{peak_src} (MEASURED_PEAKS.json: bf16 burst {bf16_burst} TFLOP/s, HBM {hbm} GB/s)",
                 "algorithmic_flops_per_step": tc_flops, "kernel_ms_per_step": tc_ms,
                 "share_of_step": tc_ms / step_ms if step_ms else None,
                 "mma_flops_per_algorithmic_flop": mma_factor,
-                "tensor_pipe_frac": achieved * mma_factor / bf16_burst}
-    roofline_lookup = {"bound": "hbm", "achieved": lk_bytes / (lk_ms * 1e-3) / 1e9 if lk_ms else 0.0,
+                "tensor_pipe_frac": ach_tf * mma_factor / bf16_burst, "hbm_frac": ach_gb / hbm,
+                "combined_floor_ms_per_step": floor_ms,
+                "combined_frac": floor_ms / tc_ms if tc_ms else None,
+                "definition": "per launch floor = max(MMA FLOPs / bf16 peak, algorithmic bytes / HBM peak); "
+                              "combined_frac = sum of floors / sum of measured launch times (CUDA events, "
+                              "one un-graphed batch)"}
+    roofline_lookup = {"bound": "latency (per-row heads over L2-resident GAP partials; HBM bytes are negligible)",
+                       "achieved": lk_bytes / (lk_ms * 1e-3) / 1e9 if lk_ms else 0.0,
                        "peak": hbm, "unit": "GB/s",
                        "frac": (lk_bytes / (lk_ms * 1e-3) / 1e9 / hbm) if lk_ms else 0.0,
                        "kernel_ms_per_step": lk_ms, "share_of_step": lk_ms / step_ms if step_ms else None}

@@ -388,6 +388,7 @@ __device__ __noinline__ void split_reduce(const TcConvParams& p, const TileGeom&
     float v[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = 0.0f;
+#pragma unroll 6  // the partial loads of 6 k's go out together; the adds keep ascending k order
     for (int k = 0; k < g.ks; ++k) {
       const float4* src = reinterpret_cast<const float4*>(tile_ws + static_cast<size_t>(k) * kBM * BN +
                                                           (static_cast<size_t>(c16) * kBM + r) * 16);

@@ -1,10 +1,10 @@
 // tcgen05 stem convolution over the space-to-depth image X (see tc_stem.cuh).
 //
-// Warp roles (192 threads, one persistent CTA per SM):
+// Warp roles (320 threads, one persistent CTA per SM):
 //   warp 0     : producer (lane 0): resident weights once, then one X slab per
 //                tile (bulk copies, 2 groups x planes) into a ring of stages
 //   warp 1     : MMA issuer (lane 0): k'^2 taps x {1, 3} MMAs (M128 N64 K16)
-//   warps 2..5 : epilogue (TMEM lane quadrant warp % 4): folded BN, ReLU,
+//   warps 2..9 : epilogue (TMEM lane quadrant warp % 4, column half (warp-2)/4): folded BN, ReLU,
 //                hi/lo split, NHWC store of the valid anchors
 #include "pdl.cuh"
 #include "sm100_prims.cuh"
@@ -51,22 +51,22 @@ __host__ __device__ inline StemSmem stem_smem(int x3, int kk, int Wx) {
   s.plane_bytes = 2 * s.group_bytes;
   s.stage_bytes = s.planes * s.plane_bytes;
   s.w_bytes = static_cast<uint32_t>(s.planes * s.taps * kTapBytes);
-  int st = static_cast<int>((200u * 1024u - 16u * 1024u - s.w_bytes) / s.stage_bytes);
+  int st = static_cast<int>((220u * 1024u - 34u * 1024u - s.w_bytes) / s.stage_bytes);
   s.stages = st > 8 ? 8 : st;
   return s;
 }
 
 template <bool X3>
-__global__ void __launch_bounds__(192, 1) tc_stem_kernel(const __grid_constant__ StemParams p) {
+__global__ void __launch_bounds__(320, 1) tc_stem_kernel(const __grid_constant__ StemParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const StemSmem L = stem_smem(X3 ? 1 : 0, p.kk, p.Wx);
   const int S = L.stages;
   uint8_t* wsm = smem;
   uint8_t* slabs = smem + L.w_bytes;
-  uint8_t* epi = slabs + S * L.stage_bytes;  // 4 warps x 4 KB staging, then 64 floats of shift
-  float* shift_s = reinterpret_cast<float*>(epi + 4 * 4096);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(epi + 4 * 4096 + 256);
+  uint8_t* epi = slabs + S * L.stage_bytes;  // 8 warps x 4 KB staging, then 64 floats of shift
+  float* shift_s = reinterpret_cast<float*>(epi + 8 * 4096);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(epi + 8 * 4096 + 256);
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * 8 + 5);
   const uint32_t full0 = smem_u32(bars);
   const uint32_t empty0 = smem_u32(bars + 8);
@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(192, 1) tc_stem_kernel(const __grid_constant__
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(tfull0 + 8 * i, 1);
-      mbar_init(tempty0 + 8 * i, 4);
+      mbar_init(tempty0 + 8 * i, 8);
     }
     mbar_init(wbar, 1);
     fence_mbar_init();
@@ -171,9 +171,11 @@ __global__ void __launch_bounds__(192, 1) tc_stem_kernel(const __grid_constant__
         if (acc == 0) acc_phase ^= 1;
       }
     }
-  } else if (warp < 6) {
-    // ------------------------------------------------ epilogue
+  } else {
+    // ------------------------------------------------ epilogue (8 warps: TMEM lane quadrant warp % 4,
+    // column half (warp - 2) / 4)
     const int quad = warp & 3;
+    const int q = (warp - 2) >> 2;
     const int row = quad * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -186,9 +188,9 @@ __global__ void __launch_bounds__(192, 1) tc_stem_kernel(const __grid_constant__
       mbar_wait(tfull0 + 8 * acc, acc_phase);
       tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * kCout;
-      float v[4][16];
+      float v[2][16];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld16_nowait(t_row + c * 16, v[c]);
+      for (int c = 0; c < 2; ++c) tmem_ld16_nowait(t_row + q * 32 + c * 16, v[c]);
       tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
@@ -197,9 +199,8 @@ __global__ void __launch_bounds__(192, 1) tc_stem_kernel(const __grid_constant__
       if (acc == 0) acc_phase ^= 1;
       // staged, coalesced stores: 32 rows x 32 channels per step, 8 rows x 64 B per instruction
       const unsigned long long off = valid ? ((static_cast<unsigned long long>(n) * p.Ho + oh) * p.Wo + ow) * kCout : 0ull;
-      const uint32_t wst = smem_u32(epi + quad * 4096);
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
+      const uint32_t wst = smem_u32(epi + (warp - 2) * 4096);
+      {
         __syncwarp();
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
@@ -209,8 +210,8 @@ __global__ void __launch_bounds__(192, 1) tc_stem_kernel(const __grid_constant__
           __nv_bfloat162* l2 = reinterpret_cast<__nv_bfloat162*>(lo);
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
-            float a = v[2 * q + u][2 * e] + shift_s[cb + 2 * e];
-            float b = v[2 * q + u][2 * e + 1] + shift_s[cb + 2 * e + 1];
+            float a = v[u][2 * e] + shift_s[cb + 2 * e];
+            float b = v[u][2 * e + 1] + shift_s[cb + 2 * e + 1];
             if (p.relu) {
               a = a > 0.0f ? a : 0.0f;
               b = b > 0.0f ? b : 0.0f;
@@ -351,7 +352,7 @@ cudaError_t tc_stem_launch(const StemParams& p, int num_sms, cudaStream_t stream
   const bool x3 = p.x_lo != nullptr;
   const StemSmem L = stem_smem(x3 ? 1 : 0, p.kk, p.Wx);
   if (L.stages < 2) return cudaErrorInvalidValue;
-  const size_t smem = L.w_bytes + static_cast<size_t>(L.stages) * L.stage_bytes + 4 * 4096 + 256 + 256 + 1024;
+  const size_t smem = L.w_bytes + static_cast<size_t>(L.stages) * L.stage_bytes + 8 * 4096 + 256 + 256 + 1024;
   const long long tiles = static_cast<long long>(p.count_static) * p.tiles_per_img;
   if (tiles <= 0) return cudaSuccess;
   const int grid = tiles < num_sms ? static_cast<int>(tiles) : num_sms;
@@ -359,12 +360,12 @@ cudaError_t tc_stem_launch(const StemParams& p, int num_sms, cudaStream_t stream
     cudaError_t e = cudaFuncSetAttribute(tc_stem_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    launch_pdl(tc_stem_kernel<true>, dim3(grid), dim3(192), smem, stream, p);
+    launch_pdl(tc_stem_kernel<true>, dim3(grid), dim3(320), smem, stream, p);
   } else {
     cudaError_t e = cudaFuncSetAttribute(tc_stem_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    launch_pdl(tc_stem_kernel<false>, dim3(grid), dim3(192), smem, stream, p);
+    launch_pdl(tc_stem_kernel<false>, dim3(grid), dim3(320), smem, stream, p);
   }
   return cudaGetLastError();
 }
