@@ -181,7 +181,9 @@ __device__ __forceinline__ void add4(float4& a, const float4 b) {
 // (tc_conv epilogue, [segs][C] fp32, C % 4 == 0). Thread layout: float4
 // column j, segment group g; 4 interleaved chains per thread, then the groups
 // in ascending order. red: kLk float4 of shared scratch. Ends with a barrier.
+template <int kT = kLk>
 __device__ void gap_feats_block(const float* __restrict__ src, int segs, int C, float inv, float* feat, float4* red) {
+  constexpr int kLk = kT;  // threads of the calling CTA
   const int tid = threadIdx.x;
   const int C4 = C >> 2;
   const float4* s4 = reinterpret_cast<const float4*>(src);
@@ -306,17 +308,18 @@ __device__ void tap_gap_block(const TapView& t, long long rowb, int C, int HW, f
 
 // Fused-GAP bins for heads that need them in global memory (classes > 32:
 // the batched logits GEMM reads them): bins[r][c], one CTA per row.
-__global__ void __launch_bounds__(kLk) gap_bins_kernel(const float* gap, int segs, int C, float inv,
-                                                       const int* data_idx, const int* count, float* bins) {
+constexpr int kGapBinsThreads = 1024;
+__global__ void __launch_bounds__(kGapBinsThreads) gap_bins_kernel(const float* gap, int segs, int C, float inv,
+                                                                   const int* data_idx, const int* count, float* bins) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ float feat_s[];
-  __shared__ float4 red[kLk];
+  __shared__ float4 red[kGapBinsThreads];
   const int r = blockIdx.x;
   if (r >= *count) return;
   const long long n = data_idx ? data_idx[r] : r;
-  gap_feats_block(gap + n * segs * C, segs, C, inv, feat_s, red);
-  for (int c = threadIdx.x; c < C; c += kLk) bins[static_cast<long long>(r) * C + c] = feat_s[c];
+  gap_feats_block<kGapBinsThreads>(gap + n * segs * C, segs, C, inv, feat_s, red);
+  for (int c = threadIdx.x; c < C; c += kGapBinsThreads) bins[static_cast<long long>(r) * C + c] = feat_s[c];
 }
 
 // Generic: one thread per bin, sequential over its flat window.
@@ -543,7 +546,8 @@ __global__ void __launch_bounds__(256) rows_fc_kernel(const float* __restrict__ 
 __device__ __forceinline__ float fc_logit(const float* part, int nz, long long zstride, const float* b, int r,
                                           int classes, int k) {
   float a = b[k];
-  for (int z = 0; z < nz; ++z) a += part[z * zstride + static_cast<long long>(r) * classes + k];
+#pragma unroll 8  // loads of 8 slices in flight; adds stay in ascending z
+  for (int z = 0; z < nz; ++z) a += __ldg(part + z * zstride + static_cast<long long>(r) * classes + k);
   return a;
 }
 
@@ -991,13 +995,17 @@ __global__ void phase_split_kernel(const __nv_bfloat16* hi, const __nv_bfloat16*
   }
 }
 
-__global__ void maxpool_kernel(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int H, int W, int C, int k, int stride,
-                               int pad, int Ho, int Wo, const int* ids, const int* count, __nv_bfloat16* ohi,
-                               __nv_bfloat16* olo) {
+// Max-pool (the ResNet stem's 3x3 s2 pool) over the surviving images, NHWC
+// hi (+lo): one thread per (output pixel, 8 channels), 16-byte loads/stores;
+// per channel the first maximum in (r, s) order wins (hi and lo move
+// together). kK > 0: compile-time window (all k*k loads in flight at once).
+template <int kK>
+__global__ void maxpool_kernel(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int H, int W, int C, int k_rt,
+                               int stride, int pad, int Ho, int Wo, const int* ids, const int* count,
+                               __nv_bfloat16* ohi, __nv_bfloat16* olo) {
   pdl_wait();
   pdl_trigger();
-  // One thread per (output pixel, 8 channels): 16-byte loads/stores; per
-  // channel the first maximum in (r, s) order wins (hi and lo move together).
+  const int k = kK > 0 ? kK : k_rt;
   const int j = blockIdx.x;
   if (j >= *count) return;
   const long long n = ids[j];
@@ -1011,26 +1019,30 @@ __global__ void maxpool_kernel(const __nv_bfloat16* hi, const __nv_bfloat16* lo,
     uint4 bh = make_uint4(0, 0, 0, 0), bl = make_uint4(0, 0, 0, 0);
 #pragma unroll
     for (int e = 0; e < 8; ++e) best[e] = -FLT_MAX;
-    for (int r = 0; r < k; ++r) {
-      const int ih = oh * stride + r - pad;
-      if (ih < 0 || ih >= H) continue;
-      for (int s2 = 0; s2 < k; ++s2) {
-        const int iw = ow * stride + s2 - pad;
-        if (iw < 0 || iw >= W) continue;
-        const long long src = ((n * H + ih) * W + iw) * C + c8 * 8;
-        const uint4 vh = *reinterpret_cast<const uint4*>(hi + src);
-        const uint4 vl = lo ? *reinterpret_cast<const uint4*>(lo + src) : make_uint4(0, 0, 0, 0);
-        const __nv_bfloat16* h8 = reinterpret_cast<const __nv_bfloat16*>(&vh);
-        const __nv_bfloat16* l8 = reinterpret_cast<const __nv_bfloat16*>(&vl);
-        __nv_bfloat16* bh8 = reinterpret_cast<__nv_bfloat16*>(&bh);
-        __nv_bfloat16* bl8 = reinterpret_cast<__nv_bfloat16*>(&bl);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const float v = __bfloat162float(h8[e]) + __bfloat162float(l8[e]);
-          if (v > best[e]) {
-            best[e] = v;
-            bh8[e] = h8[e];
-            bl8[e] = l8[e];
+    for (int r = 0; r < (kK > 0 ? kK : 1); ++r) {
+#pragma unroll
+      for (int s2 = 0; s2 < (kK > 0 ? kK : 1); ++s2) {
+        for (int rr = r; rr < (kK > 0 ? r + 1 : k); ++rr) {
+          for (int ss = s2; ss < (kK > 0 ? s2 + 1 : k); ++ss) {
+            const int ih = oh * stride + rr - pad, iw = ow * stride + ss - pad;
+            if (ih < 0 || ih >= H || iw < 0 || iw >= W) continue;
+            const long long src = ((n * H + ih) * W + iw) * C + c8 * 8;
+            const uint4 vh = __ldg(reinterpret_cast<const uint4*>(hi + src));
+            const uint4 vl = lo ? __ldg(reinterpret_cast<const uint4*>(lo + src)) : make_uint4(0, 0, 0, 0);
+            const __nv_bfloat16* h8 = reinterpret_cast<const __nv_bfloat16*>(&vh);
+            const __nv_bfloat16* l8 = reinterpret_cast<const __nv_bfloat16*>(&vl);
+            __nv_bfloat16* bh8 = reinterpret_cast<__nv_bfloat16*>(&bh);
+            __nv_bfloat16* bl8 = reinterpret_cast<__nv_bfloat16*>(&bl);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const float v = __bfloat162float(h8[e]) + __bfloat162float(l8[e]);
+              if (v > best[e]) {
+                best[e] = v;
+                bh8[e] = h8[e];
+                bl8[e] = l8[e];
+              }
+            }
           }
         }
       }
@@ -1084,7 +1096,7 @@ void launch_gap_bins(const float* gap, int segs, int C, int HW, const int* data_
                      float* bins, cudaStream_t s) {
   if (max_rows <= 0) return;
   const float inv = static_cast<float>(1.0 / HW);
-  launch_pdl(gap_bins_kernel, dim3(max_rows), dim3(kLk), static_cast<size_t>(C) * sizeof(float), s, gap, segs, C, inv, data_idx, count,
+  launch_pdl(gap_bins_kernel, dim3(max_rows), dim3(kGapBinsThreads), static_cast<size_t>(C) * sizeof(float), s, gap, segs, C, inv, data_idx, count,
                                                                                  bins);
 }
 
@@ -1226,7 +1238,12 @@ void launch_maxpool(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int H, int
   const long long per = static_cast<long long>(Ho) * Wo * (C / 8);
   int gy = static_cast<int>((per + 255) / 256);
   if (gy > 128) gy = 128;
-  launch_pdl(maxpool_kernel, dim3(dim3(max_rows, gy)), dim3(256), 0, s, hi, lo, H, W, C, k, stride, pad, Ho, Wo, ids, count, ohi, olo);
+  if (k == 3)
+    launch_pdl(maxpool_kernel<3>, dim3(max_rows, gy), dim3(256), 0, s, hi, lo, H, W, C, k, stride, pad, Ho, Wo, ids,
+               count, ohi, olo);
+  else
+    launch_pdl(maxpool_kernel<0>, dim3(max_rows, gy), dim3(256), 0, s, hi, lo, H, W, C, k, stride, pad, Ho, Wo, ids,
+               count, ohi, olo);
 }
 
 void launch_stamp_start(unsigned long long* t0, cudaStream_t s) { launch_pdl(stamp_kernel, dim3(1), dim3(1), 0, s, t0); }

@@ -369,14 +369,16 @@ __device__ __forceinline__ void gap_segment(const TcConvParams& p, const Tile& x
 // the tile (warp units of 16 columns x 32 rows, fixed k order) and run the
 // epilogue on it. Kept out of line: it is the rare path.
 __device__ __noinline__ void split_reduce(const TcConvParams& p, const TileGeom& g, const Tile& x, int BN, int etid,
-                                          int lane) {
+                                          int lane, int unit) {
   int* arr = p.ws_counters + 2 * x.tile_mn;
   int* dep = arr + 1;
   __threadfence();
   epi_bar();
   if (etid == 0) {
+    trace_put(p, unit, 6);
     atomicAdd(arr, 1);
     while (ld_acquire(arr) < g.ks) __nanosleep(64);
+    trace_put(p, unit, 7);
   }
   epi_bar();
   const int nu = (BN / 16) * (kBM / 32);
@@ -562,7 +564,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
       }
     }
   } else if (warp == 1 && p.halo) {
-    if (lane == 0) {
+    {  // whole warp: uniform operands, elect.sync issues
       // ------------------------------------------------ MMA issuer (halo)
       constexpr uint32_t idesc = umma_idesc_bf16(kBM, BN);
       int aslot = 0, bslot = 0;
@@ -576,7 +578,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
         const Tile x = decode_tile(t, p, g);
         mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1);
         tc_fence_after();
-        trace_put(p, unit, 2);
+        if (lane == 0) trace_put(p, unit, 2);
         const uint32_t d_tmem = tmem_base + acc * BN;
         const int m0 = x.h0 * kBM;
         const int base_row = m0 - (m0 / p.halo_pw) * p.halo_pw;  // anchor m0 inside the slab
@@ -588,36 +590,40 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
           if (new_a) mbar_wait(afull0 + 8 * aslot, aphase);
           mbar_wait(full0 + 8 * bslot, bphase);
           tc_fence_after();
-          const int row_off = res ? base_row : base_row + (tap / kk) * p.halo_pw + (tap % kk);
+          int row_off = res ? base_row : base_row + (tap / kk) * p.halo_pw + (tap % kk);
+          if (p.dbg & 8) row_off &= ~7;  // measurement only: 8-row-aligned operand starts (wrong values)
           const uint32_t ah = ring0 + aslot * h_aslot + static_cast<uint32_t>(row_off) * 128;
           const uint32_t al = ah + p.halo_aplane;
           const uint32_t bh = h_b0 + bslot * h_bslot, bl = bh + Cfg::kBBytes;
 // (a runtime trip count here miscompiles the MMA sequence: keep it constant)
+          // K-advance of 16 bf16 = 32 bytes = +2 in the descriptor's address field
+          const uint64_t dah = umma_desc_sw128(ah), dal = umma_desc_sw128(al);
+          const uint64_t dbh = umma_desc_sw128(bh), dbl = umma_desc_sw128(bl);
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             if (dbg_nomma) break;
             const uint32_t first = (s > x.s_begin || k > 0) ? 1u : 0u;
-            umma_bf16(d_tmem, umma_desc_sw128(ah + 32 * k), umma_desc_sw128(bh + 32 * k), idesc, first);
+            umma_bf16_warp(d_tmem, dah + 2 * k, dbh + 2 * k, idesc, first);
             if (X3) {
-              if (!res) umma_bf16(d_tmem, umma_desc_sw128(ah + 32 * k), umma_desc_sw128(bl + 32 * k), idesc, 1u);
-              umma_bf16(d_tmem, umma_desc_sw128(al + 32 * k), umma_desc_sw128(bh + 32 * k), idesc, 1u);
+              if (!res) umma_bf16_warp(d_tmem, dah + 2 * k, dbl + 2 * k, idesc, 1u);
+              umma_bf16_warp(d_tmem, dal + 2 * k, dbh + 2 * k, idesc, 1u);
             }
           }
-          umma_commit(empty0 + 8 * bslot);
+          umma_commit_warp(empty0 + 8 * bslot);
           if (++bslot == h_sb) {
             bslot = 0;
             bphase ^= 1;
           }
           if (last_a) {
-            umma_commit(aempty0 + 8 * aslot);
+            umma_commit_warp(aempty0 + 8 * aslot);
             if (++aslot == 2) {
               aslot = 0;
               aphase ^= 1;
             }
           }
         }
-        umma_commit(tfull0 + 8 * acc);
-        trace_put(p, unit, 3);
+        umma_commit_warp(tfull0 + 8 * acc);
+        if (lane == 0) trace_put(p, unit, 3);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
@@ -686,7 +692,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // whole warp: uniform operands, elect.sync issues
       // ------------------------------------------------ MMA issuer
       constexpr uint32_t idesc = umma_idesc_bf16(kBM, BN);
       int stage = 0;
@@ -698,7 +704,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
         const Tile x = decode_tile(t, p, g);
         mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1);
         tc_fence_after();
-        trace_put(p, unit, 2);
+        if (lane == 0) trace_put(p, unit, 2);
         const uint32_t d_tmem = tmem_base + acc * BN;
         const int nk_conv = p.ntaps * (p.C / 64);
         for (int s = x.s_begin; s < x.s_end; ++s) {
@@ -706,27 +712,30 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
           tc_fence_after();
           const uint32_t ah = smem_u32(stage_a(stage, 0)), bh = smem_u32(stage_b(stage, 0));
           const bool res_step = s >= nk_conv;
+          // K-advance of 16 bf16 = 32 bytes = +2 in the descriptor's address field
+          const uint64_t dah = umma_desc_sw128(ah), dbh = umma_desc_sw128(bh);
+          const uint64_t dal = umma_desc_sw128(smem_u32(stage_a(stage, X3 ? 1 : 0)));
+          const uint64_t dbl = umma_desc_sw128(smem_u32(stage_b(stage, X3 ? 1 : 0)));
 // (a runtime trip count here miscompiles the MMA sequence: keep it constant)
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             if (dbg_nomma) break;
             const uint32_t first = (s > x.s_begin || k > 0) ? 1u : 0u;
-            umma_bf16(d_tmem, umma_desc_sw128(ah + 32 * k), umma_desc_sw128(bh + 32 * k), idesc, first);
+            umma_bf16_warp(d_tmem, dah + 2 * k, dbh + 2 * k, idesc, first);
             if (X3) {
-              const uint32_t al = smem_u32(stage_a(stage, 1)), bl = smem_u32(stage_b(stage, 1));
               if (!res_step)  // identity has no lo plane
-                umma_bf16(d_tmem, umma_desc_sw128(ah + 32 * k), umma_desc_sw128(bl + 32 * k), idesc, 1u);
-              umma_bf16(d_tmem, umma_desc_sw128(al + 32 * k), umma_desc_sw128(bh + 32 * k), idesc, 1u);
+                umma_bf16_warp(d_tmem, dah + 2 * k, dbl + 2 * k, idesc, 1u);
+              umma_bf16_warp(d_tmem, dal + 2 * k, dbh + 2 * k, idesc, 1u);
             }
           }
-          umma_commit(empty0 + 8 * stage);
+          umma_commit_warp(empty0 + 8 * stage);
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit(tfull0 + 8 * acc);
-        trace_put(p, unit, 3);
+        umma_commit_warp(tfull0 + 8 * acc);
+        if (lane == 0) trace_put(p, unit, 3);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
@@ -875,7 +884,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
       if (lane == 0) mbar_arrive(tempty0 + 8 * acc);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
-      if (split) split_reduce(p, g, x, BN, etid, lane);
+      if (split) split_reduce(p, g, x, BN, etid, lane, unit);
       if (etid == 0) trace_put(p, unit, 5);
     }
   }

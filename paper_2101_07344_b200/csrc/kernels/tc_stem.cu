@@ -148,17 +148,23 @@ __global__ void __launch_bounds__(320, 1) tc_stem_kernel(const __grid_constant__
         const uint32_t d_tmem = tmem_base + acc * kCout;
         const uint32_t a0 = smem_u32(slabs + stage * L.stage_bytes);
         const uint32_t b0 = smem_u32(wsm);
-        for (int tap = 0; tap < L.taps; ++tap) {
-          const int r = tap / p.kk, s = tap - r * p.kk;
-          const uint32_t off = static_cast<uint32_t>(r * p.Wx + s) * 16;
-          const uint32_t bt = b0 + tap * kTapBytes;
-          umma_bf16(d_tmem, desc_kmajor_none(a0 + off, L.group_bytes), desc_kmajor_none(bt, kCout * 16), idesc,
-                    tap > 0 ? 1u : 0u);
-          if (X3) {
-            umma_bf16(d_tmem, desc_kmajor_none(a0 + off, L.group_bytes), desc_kmajor_none(bt + wplane, kCout * 16),
-                      idesc, 1u);
-            umma_bf16(d_tmem, desc_kmajor_none(a0 + L.plane_bytes + off, L.group_bytes),
-                      desc_kmajor_none(bt, kCout * 16), idesc, 1u);
+        // descriptors built once per tile; a tap moves the start address field
+        // (bits 0-13, 16-byte units) by its row shift / weight offset
+        const uint64_t da_hi = desc_kmajor_none(a0, L.group_bytes);
+        const uint64_t da_lo = desc_kmajor_none(a0 + L.plane_bytes, L.group_bytes);
+        const uint64_t db_hi = desc_kmajor_none(b0, kCout * 16);
+        const uint64_t db_lo = desc_kmajor_none(b0 + wplane, kCout * 16);
+        uint32_t accum = 0;
+        uint64_t bo = 0;
+        for (int r = 0; r < p.kk; ++r) {
+          uint64_t ao = static_cast<uint64_t>(r * p.Wx);
+          for (int s = 0; s < p.kk; ++s, ++ao, bo += kTapBytes / 16) {
+            umma_bf16(d_tmem, da_hi + ao, db_hi + bo, idesc, accum);
+            if (X3) {
+              umma_bf16(d_tmem, da_hi + ao, db_lo + bo, idesc, 1u);
+              umma_bf16(d_tmem, da_lo + ao, db_hi + bo, idesc, 1u);
+            }
+            accum = 1u;
           }
         }
         umma_commit(empty0 + 8 * stage);

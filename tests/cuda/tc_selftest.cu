@@ -566,13 +566,13 @@ static void perf_conv(const char* name, int N, int nsurv, int H, int W, int C, i
     CK(cudaMemcpy(tr.data(), dTrace, tr.size() * 8, cudaMemcpyDeviceToHost));
     for (int cta = 0; cta < 2; ++cta) {
       const unsigned long long t0 = tr[(cta * 32) * 8 + 0];
-      printf("  trace CTA %d (cycles from first TMA issue): unit: tma0 tmaN | mma0 mmaN | epi0 epiN\n", cta);
+      printf("  trace CTA %d (cycles from first TMA issue): unit: tma0 tmaN | mma0 mmaN | epi0 epiN | split: fenced waited\n", cta);
       for (int u = 0; u < 32; ++u) {
         const unsigned long long* q = &tr[(cta * 32 + u) * 8];
         if (!q[0] && !q[4]) break;
         auto rel = [&](unsigned long long v) { return v ? (long long)(v - t0) : -1LL; };
-        printf("   %2d: %8lld %8lld | %8lld %8lld | %8lld %8lld\n", u, rel(q[0]), rel(q[1]), rel(q[2]), rel(q[3]),
-               rel(q[4]), rel(q[5]));
+        printf("   %2d: %8lld %8lld | %8lld %8lld | %8lld %8lld | %8lld %8lld\n", u, rel(q[0]), rel(q[1]), rel(q[2]),
+               rel(q[3]), rel(q[4]), rel(q[5]), rel(q[6]), rel(q[7]));
       }
     }
   }
