@@ -122,7 +122,9 @@ def build_deployment(cfg_name, batch, precision, device, seed=2101):
         vs = []
         for l in range(1, m.num_blocks + 1):
             C, H, W = m.tap(l)
-            vs.append(lcb.build_variant(l, 0, f"Pool({C})", m.tap_dim(l), classes, seed + l))
+            # C4 (VGG-16): FC and pool cache models on alternate taps; else Pool(C) = GAP heads
+            a = ("FC(256)" if l % 2 == 0 else f"Pool({C})") if arch.startswith("vgg") else f"Pool({C})"
+            vs.append(lcb.build_variant(l, 0, a, m.tap_dim(l), classes, seed + l))
         side = 32 if arch.endswith("cifar") else 224
         calib = image_inputs(min(batch, 256), 3, side, side, seed + 2)
         gen = lambda B, s: image_inputs(B, 3, side, side, s)  # noqa: E731
@@ -190,6 +192,9 @@ def main():
     ap.add_argument("--precision", default="bf16x3", choices=["bf16x3", "bf16"])
     ap.add_argument("--cpu-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sweep", default="",
+                    help="comma-separated thresholds: C4 confidence-threshold sweep (req/s, hit rate and agreement "
+                         "with the base model per threshold) instead of the single-threshold line")
     args = ap.parse_args()
     assert args.warmup >= 3 or args.impl == "reference", "timing rules: at least 3 warm-up steps"
 
@@ -200,8 +205,9 @@ def main():
     B = args.batch or dflt_batch
     metric = "requests/sec with learned caches (p50/p99 latency, no-cache req/s, hit rate alongside)"
     config = {"workload": args.config, "baseline_config": cfg_str, "batch_per_gpu": B, "global_batch": B * world,
-              "caches": "Pool(C) GAP head + FC(16) selector after every block" if family == "cnn" else
-              "one build_variant cache per block (FC/Pool/Conv menu)",
+              "caches": ("FC(256) / Pool(C) heads on alternate pool-stage taps + FC(16) selector"
+                         if arch and arch.startswith("vgg") else "Pool(C) GAP head + FC(16) selector after every block")
+              if family == "cnn" else "one build_variant cache per block (FC/Pool/Conv menu)",
               "exit_profile_full_fraction": full_frac, "precision": args.precision,
               "l2": "flushed (256 MiB write) between timed steps, outside the events",
               "parallelism": f"dp{world} (request shards, no collectives)"}
@@ -253,6 +259,33 @@ def main():
                 lats.append(r.latency_ms.copy())
                 exits.append(r.exit_layer.copy())
         return total_ms, lats, exits
+
+    if args.sweep:
+        rows = []
+        for d in [float(t) for t in args.sweep.split(",")]:
+            for v in vs:
+                dep.set_delta(v.layer, d)
+            run_steps(dep, in_ptr, args.warmup, False)
+            ms, lats, exits = run_steps(dep, in_ptr, args.steps, True)
+            sh = dep.serve(inputs[0], shadow=True)
+            ex = np.concatenate(exits)
+            lat = np.concatenate(lats)
+            hit = sh.exit_layer > 0
+            rows.append({"delta": d, "requests_per_s": B * args.steps * world / (ms / 1e3),
+                         "ms_per_step": ms / args.steps, "hit_rate": float(np.mean(ex > 0)),
+                         "p50_ms": float(lcb.nearest_rank(lat, 0.5)), "p99_ms": float(lcb.nearest_rank(lat, 0.99)),
+                         "agreement_with_base": float(np.mean(sh.served == sh.base_pred)),
+                         "hit_accuracy": float(np.mean(sh.served[hit] == sh.base_pred[hit])) if hit.any() else 1.0})
+        line = {"metric": "requests/sec vs confidence threshold (C4 sweep; hit rate, agreement with the base model)",
+                "value": rows[0]["requests_per_s"], "unit": "requests/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "bf16x3 (hi/lo bf16 split, fp32 accumulate: fp32-class)" if args.precision == "bf16x3"
+                else "bf16", "data": "synthetic", "config": dict(config, sweep=args.sweep), "sweep": rows}
+        if rank == 0:
+            print(json.dumps(line))
+        if dist:
+            dist.destroy_process_group()
+        return
 
     # warm-up (graph capture happens here)
     run_steps(dep, in_ptr, args.warmup, False)

@@ -157,6 +157,19 @@ int lc_engine_counts(lc_engine* e, int* counts);
 int lc_lookup_batch(lc_engine* e, int layer, const float* taps, int B, int* hit, int* label, float* prob, float* pr,
                     float* logits);
 
+/* measure_metrics (cache.cpp:316-335) for every attached cache at every
+ * threshold of grid[G] (G <= 64), batched: one shadow serve of the B host
+ * requests (every cache probed, full base pass), then confusion counts per
+ * layer and threshold, counts [blocks][G][4] = {tp, fp, tn, fn}: hit = selector
+ * probability >= threshold, agree = argmax(pr) == base prediction. Layers
+ * without a cache get zeros. Replaces the per-record lookup loop of
+ * measure_metrics / explore_variants (cache.cpp:316-335, 337-...). */
+int lc_measure_metrics(lc_engine* e, const float* inputs, int B, const double* grid, int G, long long* counts);
+/* tune_delta (cache.cpp:267-307) for every attached cache over the same batch:
+ * deltas[blocks] (NaN where no cache); apply != 0 sets the engine thresholds. */
+int lc_tune_delta(lc_engine* e, const float* inputs, int B, double target_accuracy, const double* grid, int G,
+                  double* deltas, int apply);
+
 /* Device time of `iters` graph replays of a B-request batch (CUDA events on the engine stream). */
 int lc_engine_time(lc_engine* e, int B, unsigned flags, int iters, double* ms_per_batch);
 /* One batch from lc_engine_input(), CUDA events around it on the engine stream; synchronous. */

@@ -61,6 +61,8 @@ def ref() -> C.CDLL:
             "ref_forward_logits": (I, [P, pD, pD]),
             "ref_lookup": (I, [P, pD, I, pI, pD, pD, pD]),
             "ref_simulate": (I, [P, C.POINTER(P), I, pD, I, pI, pI, pI, I, pD]),
+            "ref_measure_metrics": (I, [P, P, pD, I, C.POINTER(LL), pD, pD]),
+            "ref_tune_delta": (I, [P, P, pD, I, D, pD, I, pD]),
             "ref_pipeline": (I, [C.c_char_p, U64, I, I, I, I, C.c_char_p, I, I, D]),
             "ref_gen_workload": (I, [C.c_char_p, I, D, D, D, D, U64, C.POINTER(LL), C.POINTER(LL), pI, LL]),
             "ref_rng_stream": (I, [U64, I, I, pD, C.POINTER(U64)]),
@@ -225,6 +227,25 @@ def ref_simulate(model: RefModel, variants: Sequence[RefVariant], inputs: np.nda
     _check(ref().ref_simulate(model.h, arr, len(variants), _dp(x), B, _ip(hl), _ip(sv), _ip(bp), threads,
                               C.byref(el)))
     return hl, sv, bp, el.value
+
+
+def ref_measure_metrics(model: RefModel, variant: RefVariant, inputs: np.ndarray):
+    """The reference's measure_metrics (cache.cpp:316-335) over collect_taps of
+    the rows of `inputs`: ({tp, fp, tn, fn}, hit_rate, accuracy)."""
+    x = np.ascontiguousarray(inputs, np.float64)
+    cnt = (LL * 4)()
+    hr, acc = C.c_double(), C.c_double()
+    _check(ref().ref_measure_metrics(model.h, variant.h, _dp(x), x.shape[0], cnt, C.byref(hr), C.byref(acc)))
+    return {"tp": cnt[0], "fp": cnt[1], "tn": cnt[2], "fn": cnt[3]}, hr.value, acc.value
+
+
+def ref_tune_delta(model: RefModel, variant: RefVariant, inputs: np.ndarray, target: float, grid) -> float:
+    """The reference's tune_delta (cache.cpp:267-307) on a copy of the variant."""
+    x = np.ascontiguousarray(inputs, np.float64)
+    g = np.ascontiguousarray(grid, np.float64)
+    d = C.c_double()
+    _check(ref().ref_tune_delta(model.h, variant.h, _dp(x), x.shape[0], target, _dp(g), len(g), C.byref(d)))
+    return d.value
 
 
 # ------------------------------------------------------------------ text format -> numpy

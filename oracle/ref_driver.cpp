@@ -298,6 +298,42 @@ int ref_simulate(void* mp, void** vars, int nv, const double* inputs, int B, int
   });
 }
 
+// ------------------------------------------------------------------ explore measurement
+// measure_metrics (cache.cpp:316-335) and tune_delta (cache.cpp:267-307) of one
+// variant over the records collect_taps (cache.cpp:142-154) makes from the rows
+// of `inputs` (labels unused by both). counts = {tp, fp, tn, fn}.
+int ref_measure_metrics(void* mp, void* vp, const double* inputs, int B, long long* counts, double* hit_rate,
+                        double* accuracy) {
+  return guard([&] {
+    const BaseModel& m = *static_cast<BaseModel*>(mp);
+    const CacheVariant& v = *static_cast<CacheVariant*>(vp);
+    std::vector<Sample> samples(static_cast<std::size_t>(B));
+    for (int i = 0; i < B; ++i)
+      samples[static_cast<std::size_t>(i)].x = vec_of(inputs + static_cast<std::size_t>(i) * m.input_dim(), m.input_dim());
+    const std::vector<TapRecord> recs = collect_taps(m, samples);
+    const VariantMetrics r = measure_metrics(v, recs, CostModel{});
+    counts[0] = r.tp;
+    counts[1] = r.fp;
+    counts[2] = r.tn;
+    counts[3] = r.fn;
+    *hit_rate = r.hit_rate;
+    *accuracy = r.accuracy;
+  });
+}
+
+int ref_tune_delta(void* mp, void* vp, const double* inputs, int B, double target, const double* grid, int ng,
+                   double* delta) {
+  return guard([&] {
+    const BaseModel& m = *static_cast<BaseModel*>(mp);
+    CacheVariant v = *static_cast<CacheVariant*>(vp);
+    std::vector<Sample> samples(static_cast<std::size_t>(B));
+    for (int i = 0; i < B; ++i)
+      samples[static_cast<std::size_t>(i)].x = vec_of(inputs + static_cast<std::size_t>(i) * m.input_dim(), m.input_dim());
+    const std::vector<TapRecord> recs = collect_taps(m, samples);
+    *delta = tune_delta(v, recs, target, std::vector<double>(grid, grid + ng));
+  });
+}
+
 // ------------------------------------------------------------------ pipeline
 // Trained deployment in the style of test_acceptance.cpp:69-137: dataset ->
 // train_base -> collect_taps -> explore_variants -> compose_relaxed ->

@@ -365,6 +365,54 @@ class Deployment:
                                   _fptr(lg)))
         return {"hit": hit, "label": label, "prob": prob, "pr": pr, "logits": lg}
 
+    def measure_metrics(self, inputs: np.ndarray, deltas: Sequence[float] = None) -> Dict[int, List[Dict]]:
+        """Batched measure_metrics (cache.cpp:316-335) of every attached cache at
+        every threshold in `deltas` (default: each variant's own delta) over one
+        shadow serve of `inputs`: {layer: [{delta, tp, fp, tn, fn, hit_rate,
+        accuracy}, ...]} with the reference's definitions (hit_rate =
+        (tp+fp)/total, accuracy = tp/(tp+fp), 1 when nothing hits)."""
+        x = np.ascontiguousarray(inputs, dtype=np.float32)
+        B = x.shape[0]
+        if deltas is None:
+            grid = sorted({float(v.delta) for v in self.variants})
+        else:
+            grid = [float(d) for d in deltas]
+        g = np.ascontiguousarray(grid, np.float64)
+        cnt = np.zeros((self.blocks, len(g), 4), np.int64)
+        check(lib.lc_measure_metrics(self._h, _fptr(x), B, _dptr(g), len(g),
+                                     cnt.ctypes.data_as(C.POINTER(C.c_longlong))))
+        out = {}
+        own = {v.layer: float(v.delta) for v in self.variants}
+        for v in self.variants:
+            rows = []
+            for j, d in enumerate(grid):
+                if deltas is None and d != own[v.layer]:
+                    continue
+                tp, fp, tn, fn = (int(c) for c in cnt[v.layer - 1, j])
+                hits = tp + fp
+                total = tp + fp + tn + fn
+                rows.append({"delta": d, "tp": tp, "fp": fp, "tn": tn, "fn": fn,
+                             "hit_rate": hits / total if total else 0.0,
+                             "accuracy": tp / hits if hits else 1.0})
+            out[v.layer] = rows
+        return out
+
+    def tune_delta(self, inputs: np.ndarray, target_accuracy: float, grid: Sequence[float],
+                   apply: bool = True) -> Dict[int, float]:
+        """Batched tune_delta (cache.cpp:267-307) for every attached cache: the
+        smallest threshold of `grid` whose hit accuracy reaches the target (else
+        the most accurate). apply: set the engine's thresholds (and the variants')."""
+        x = np.ascontiguousarray(inputs, dtype=np.float32)
+        g = np.ascontiguousarray(list(grid), np.float64)
+        d = np.zeros(self.blocks, np.float64)
+        check(lib.lc_tune_delta(self._h, _fptr(x), x.shape[0], float(target_accuracy), _dptr(g), len(g), _dptr(d),
+                                1 if apply else 0))
+        out = {v.layer: float(d[v.layer - 1]) for v in self.variants}
+        if apply:
+            for v in self.variants:
+                v.delta = out[v.layer]
+        return out
+
     def time_batch(self, B: int, iters: int, shadow: bool = False) -> float:
         ms = C.c_double()
         check(lib.lc_engine_time(self._h, B, LC_SERVE_SHADOW if shadow else 0, iters, C.byref(ms)))

@@ -1,7 +1,11 @@
 // extern "C" boundary (include/latecache_b200.h). Exceptions from the host
 // restatement and the engine are mapped to status codes exactly where the
 // reference would throw (std::invalid_argument / std::runtime_error).
+#include <algorithm>
 #include <cmath>
+#include <limits>
+#include <utility>
+#include <vector>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -411,6 +415,67 @@ int lc_serve_batch(lc_engine* e, const float* inputs, int B, unsigned flags, int
     lcb::Engine& en = eng(e);
     en.serve_host(inputs, B, (flags & LC_SERVE_SHADOW) != 0, (flags & LC_SERVE_NO_GRAPH) == 0);
     en.copy_results(B, exit_layer, served, base_pred, probs, latency_ms);
+  });
+}
+
+// measure_metrics (cache.cpp:316-335) for every attached cache at every
+// threshold of the grid, over one shadow serve of the B host requests.
+int lc_measure_metrics(lc_engine* e, const float* inputs, int B, const double* grid, int G, long long* counts) {
+  return guard([&] {
+    need(inputs, "inputs");
+    need(grid, "grid");
+    need(counts, "counts");
+    lcb::Engine& en = eng(e);
+    if (B <= 0 || B > en.max_batch()) throw std::invalid_argument("measure_metrics: batch outside [1, max_batch]");
+    if (G <= 0 || G > 64) throw std::invalid_argument("measure_metrics: threshold grid must hold 1..64 values");
+    const size_t bytes = static_cast<size_t>(B) * static_cast<size_t>(en.input_dim()) * sizeof(float);
+    if (cudaSetDevice(en.device()) != cudaSuccess ||
+        cudaMemcpyAsync(en.input_buffer(), inputs, bytes, cudaMemcpyHostToDevice, en.stream()) != cudaSuccess)
+      throw lcb::CudaFailure("measure_metrics: input copy failed");
+    en.measure(B, grid, G, counts);
+  });
+}
+
+// tune_delta (cache.cpp:267-307) per attached cache from the same counts:
+// ascending grid; the first threshold whose hit accuracy tp/(tp+fp) (1 when
+// nothing hits) reaches the target wins, else the most accurate one (first
+// on ties). deltas[blocks]: NaN where no cache is attached; apply != 0 sets
+// the engine's thresholds.
+int lc_tune_delta(lc_engine* e, const float* inputs, int B, double target_accuracy, const double* grid, int G,
+                  double* deltas, int apply) {
+  return guard([&] {
+    need(deltas, "deltas");
+    need(grid, "grid");
+    if (G <= 0 || G > 64) throw std::invalid_argument("tune_delta: empty threshold grid");
+    lcb::Engine& en = eng(e);
+    std::vector<std::pair<double, int>> sorted;
+    for (int g = 0; g < G; ++g) sorted.push_back({grid[g], g});
+    std::stable_sort(sorted.begin(), sorted.end(),
+                     [](const std::pair<double, int>& a, const std::pair<double, int>& b) { return a.first < b.first; });
+    const int L = en.blocks();
+    std::vector<long long> counts(static_cast<size_t>(L) * G * 4);
+    const int st = lc_measure_metrics(e, inputs, B, grid, G, counts.data());
+    if (st != LC_OK) throw std::runtime_error(lc_last_error());
+    for (int l = 1; l <= L; ++l) {
+      deltas[l - 1] = std::numeric_limits<double>::quiet_NaN();
+      if (!en.has_cache(l)) continue;
+      double best_delta = sorted.front().first, best_acc = -1.0;
+      for (const auto& dg : sorted) {
+        const long long* c = &counts[(static_cast<size_t>(l - 1) * G + dg.second) * 4];
+        const long long hits = c[0] + c[1];
+        const double acc = hits == 0 ? 1.0 : static_cast<double>(c[0]) / static_cast<double>(hits);
+        if (acc >= target_accuracy) {
+          best_delta = dg.first;  // smallest qualifying threshold maximises the hit rate
+          break;
+        }
+        if (acc > best_acc) {
+          best_acc = acc;
+          best_delta = dg.first;
+        }
+      }
+      deltas[l - 1] = best_delta;
+      if (apply) en.set_delta(l, best_delta);
+    }
   });
 }
 

@@ -221,6 +221,9 @@ void Engine::build_weights() {
   d_exit_ns_ = static_cast<unsigned long long*>(dalloc(static_cast<size_t>(B) * 8));
   d_t0_ = static_cast<unsigned long long*>(dalloc(8));
   d_probs_ = static_cast<float*>(dalloc(static_cast<size_t>(L) * B * sizeof(float)));
+  d_labels_ = static_cast<int*>(dalloc(static_cast<size_t>(L) * B * sizeof(int)));
+  d_grid_ = static_cast<double*>(dalloc(64 * sizeof(double)));
+  d_conf_ = static_cast<unsigned long long*>(dalloc(static_cast<size_t>(L) * 64 * 4 * sizeof(unsigned long long)));
   d_lk_count_ = static_cast<int*>(dalloc(sizeof(int)));
   lk_arrive_ = static_cast<int*>(dalloc(sizeof(int)));
   ck(cudaMemset(lk_arrive_, 0, sizeof(int)), "memset");
@@ -562,6 +565,7 @@ ExitParams Engine::exit_params(int layer, bool shadow, const int* ids_in, int* i
   e.served = d_served_;
   e.exit_ns = d_exit_ns_;
   e.probs_out = d_probs_ + static_cast<size_t>(layer - 1) * max_batch_;
+  e.labels_out = d_labels_ + static_cast<size_t>(layer - 1) * max_batch_;
   e.ids_out = ids_out;
   e.src_rows_out = src_rows_out;
   e.count_out = count_out;
@@ -928,6 +932,22 @@ void Engine::serve_host(const float* x, int B, bool shadow, bool use_graph) {
                      stream_),
      "input upload");
   serve(B, shadow, use_graph);
+}
+
+void Engine::measure(int B, const double* grid, int G, long long* counts) {
+  std::lock_guard<std::recursive_mutex> dev_lock(dev_stream(device_).mu);
+  require(G > 0 && G <= 64, "measure: threshold grid must hold 1..64 values");
+  const int L = model_.num_blocks;
+  serve(B, true, true);
+  ck(cudaMemcpyAsync(d_grid_, grid, static_cast<size_t>(G) * sizeof(double), cudaMemcpyHostToDevice, stream_),
+     "grid h2d");
+  launch_confusion(d_probs_, d_labels_, d_base_, max_batch_, d_batch_, L, d_grid_, G, d_conf_, stream_);
+  ck(cudaGetLastError(), "confusion");
+  std::vector<unsigned long long> h(static_cast<size_t>(L) * G * 4);
+  ck(cudaMemcpyAsync(h.data(), d_conf_, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream_),
+     "counts d2h");
+  ck(cudaStreamSynchronize(stream_), "measure sync");
+  for (size_t i = 0; i < h.size(); ++i) counts[i] = static_cast<long long>(h[i]);
 }
 
 void Engine::synchronize() { ck(cudaStreamSynchronize(stream_), "synchronize"); }

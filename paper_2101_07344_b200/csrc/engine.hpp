@@ -73,8 +73,16 @@ class Engine {
   // ----- lookup only (reference lookup() on caller-provided NCHW-flat taps)
   void lookup(int layer, const float* taps_dev, int B, int* hit, int* label, float* prob, float* pr, float* logits);
 
+  // Batched measure_metrics / tune_delta support (cache.cpp:267-335): a
+  // shadow serve of the B staged requests (every cache probed, full base
+  // pass), then confusion counts {tp, fp, tn, fn} per layer and threshold.
+  // counts: host [blocks][G][4]; rows of layers without a cache are zero.
+  void measure(int B, const double* grid, int G, long long* counts);
   void set_delta(int layer, double delta);
   double delta(int layer) const;
+  bool has_cache(int layer) const {
+    return layer >= 1 && layer < static_cast<int>(cache_of_layer_.size()) && cache_of_layer_[static_cast<size_t>(layer)] >= 0;
+  }
   void set_selector_out(int layer, double gain, double bias);
 
   // ----- introspection
@@ -131,6 +139,9 @@ class Engine {
   unsigned long long* d_exit_ns_ = nullptr;
   unsigned long long* d_t0_ = nullptr;
   float* d_probs_ = nullptr;
+  int* d_labels_ = nullptr;   // [blocks][max_batch] argmax(pr) of every probed layer
+  double* d_grid_ = nullptr;  // measure(): threshold grid (<= 64)
+  unsigned long long* d_conf_ = nullptr;  // measure(): [blocks][64][4]
 
   // MLP weights: per block FC (padded) + head
   struct DevFC {

@@ -705,6 +705,7 @@ __device__ void exit_tail(const ExitParams& e, int n, const float* prob, const i
     const int id = valid ? e.ids_in[r] : -1;
     if (valid) {
       if (e.probs_out) e.probs_out[id] = __ldcg(prob + r);
+      if (e.labels_out) e.labels_out[id] = __ldcg(label + r);
       if (h && e.exit_layer[id] == 0) {
         e.exit_layer[id] = e.layer;
         e.served[id] = __ldcg(label + r);
@@ -1077,7 +1078,37 @@ __global__ void init_batch_kernel(const int* batch, int max_batch, int* ids0, in
   }
 }
 
+__global__ void __launch_bounds__(256) confusion_kernel(const float* probs, const int* labels, const int* base_pred,
+                                                       int max_batch, const int* batch, const double* grid, int G,
+                                                       unsigned long long* counts) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ unsigned int cnt[64][4];
+  const int l = blockIdx.x;
+  for (int i = threadIdx.x; i < 64 * 4; i += blockDim.x) cnt[i / 4][i % 4] = 0u;
+  __syncthreads();
+  const int B = *batch;
+  for (int i = threadIdx.x; i < B; i += blockDim.x) {
+    const float p = probs[static_cast<long long>(l) * max_batch + i];
+    if (p != p) continue;  // not probed
+    const bool agree = labels[static_cast<long long>(l) * max_batch + i] == base_pred[i];
+    for (int g = 0; g < G; ++g) {
+      const bool hit = static_cast<double>(p) >= grid[g];
+      atomicAdd(&cnt[g][hit ? (agree ? 0 : 1) : (agree ? 3 : 2)], 1u);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < G * 4; i += blockDim.x)
+    counts[(static_cast<long long>(l) * G + i / 4) * 4 + i % 4] = cnt[i / 4][i % 4];
+}
+
 }  // namespace
+
+void launch_confusion(const float* probs, const int* labels, const int* base_pred, int max_batch, const int* batch,
+                      int L, const double* grid, int G, unsigned long long* counts, cudaStream_t s) {
+  if (L <= 0 || G <= 0) return;
+  launch_pdl(confusion_kernel, dim3(L), dim3(256), 0, s, probs, labels, base_pred, max_batch, batch, grid, G, counts);
+}
 
 void launch_pool_bins(const TapView& tap, int max_rows, int win, int width, float* bins, cudaStream_t s) {
   const float inv = static_cast<float>(1.0 / win);

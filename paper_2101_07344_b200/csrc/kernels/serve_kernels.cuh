@@ -40,6 +40,7 @@ struct ExitParams {
   int* served;
   unsigned long long* exit_ns;
   float* probs_out;          // [B] this layer's probabilities by request id (nullable)
+  int* labels_out;           // [B] this layer's argmax(pr) by request id (nullable)
   int* ids_out;
   int* src_rows_out;         // nullable
   int* count_out;
@@ -101,6 +102,13 @@ void launch_cache_head(const CacheHeadParams& p, int max_rows, cudaStream_t s);
 // ks == 0: A dense [rows][lda]; ks > 0: A(r,o) = relu(b1[o] + sum_s A[s*part_stride + r*lda + o]).
 void launch_rows_fc(const float* A, long long lda, int ks, long long part_stride, const float* b1, int feat,
                     const float* W, int classes, const int* count, int max_rows, float* out, cudaStream_t s);
+
+// Confusion counts of measure_metrics (cache.cpp:316-335) for every probed
+// layer at every threshold of `grid` (device, G <= 64): counts[l][g] =
+// {tp, fp, tn, fn} over the requests whose layer-l probability was recorded
+// (probs not NaN); agree = (label == base_pred), hit = (double)p >= grid[g].
+void launch_confusion(const float* probs, const int* labels, const int* base_pred, int max_batch, const int* batch,
+                      int L, const double* grid, int G, unsigned long long* counts, cudaStream_t s);
 
 // Pool(C) caches whose head reads the GAP partials directly (one launch per layer).
 bool fused_lookup_supported(int classes, int C, int max_rows);

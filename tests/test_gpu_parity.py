@@ -236,7 +236,10 @@ def _cnn_deployment(arch, classes, seed, B, precision="bf16x3", cache="Pool", fu
     vs = []
     for l in range(1, m.num_blocks + 1):
         C, H, W = m.tap(l)
-        a = f"Pool({C})" if cache == "Pool" else cache
+        if cache == "FC+Pool":  # BASELINE C4: FC and pool cache models on alternate taps
+            a = f"Pool({C})" if l % 2 else "FC(256)"
+        else:
+            a = f"Pool({C})" if cache == "Pool" else cache
         vs.append(lcb.build_variant(l, 0, a, m.tap_dim(l), classes, seed + l))
     side = 32 if arch.endswith("cifar") else 224
     calib = image_inputs(B, 3, side, side, seed=seed + 100)
@@ -323,6 +326,37 @@ def test_resnet50_serve_vs_oracle():
     dep.close()
 
 
+@pytest.mark.parametrize("delta", [0.5, 0.9])
+def test_vgg16_fc_pool_caches_vs_oracle(delta):
+    """BASELINE C4: VGG-16 CIFAR with FC(256) and Pool(C) cache models on
+    alternate pool-stage taps, at two points of the confidence-threshold sweep."""
+    m, vs = _cnn_deployment("vgg16_cifar", 10, 41, 64, cache="FC+Pool", full_fraction=0.2)
+    for v in vs:
+        v.delta = delta
+    x = image_inputs(24, 3, 32, 32, seed=14)
+    dep = lcb.Deployment(m, vs, precision="bf16x3", max_batch=32)
+    exit_o, served_o, base_o, probs_o, gaps, _, _ = _oracle_cnn(m, vs, x)
+    deltas = {v.layer: v.delta for v in vs}
+    for shadow in (True, False):
+        res = dep.serve(x, shadow=shadow)
+        compare_serve(res, exit_o, served_o, base_o, probs_o, deltas, shadow, label_gap=gaps)
+    dep.close()
+
+
+def test_resnet152_serve_vs_oracle():
+    """BASELINE C5 shape (ResNet-152, 50 bottleneck blocks, 1000 classes) on a
+    small batch against the fp64 restatement."""
+    m, vs = _cnn_deployment("resnet152", 1000, 51, 4, full_fraction=0.3)
+    x = image_inputs(3, 3, 224, 224, seed=15)
+    dep = lcb.Deployment(m, vs, precision="bf16x3", max_batch=4)
+    exit_o, served_o, base_o, probs_o, gaps, _, _ = _oracle_cnn(m, vs, x, threads=os.cpu_count() or 8)
+    deltas = {v.layer: v.delta for v in vs}
+    for shadow in (True, False):
+        res = dep.serve(x, shadow=shadow)
+        compare_serve(res, exit_o, served_o, base_o, probs_o, deltas, shadow, label_gap=gaps)
+    dep.close()
+
+
 def test_resnet18_cnn_lookups_on_oracle_taps():
     """Cache heads of every family on real CNN taps (NCHW-flat from the fp64
     oracle), through the engine's lookup entry point."""
@@ -380,3 +414,43 @@ def test_cpp_dropin_against_reference_library():
         pytest.skip("oracle/_ref/test_dropin not built (make -C oracle dropin)")
     r = subprocess.run([exe, os.path.join(GOLDEN, "trained")], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "DROPIN OK" in r.stdout, r.stdout + r.stderr
+
+
+# ------------------------------------------------------------------ explore measurement (§8f rank 1)
+@requires_ref
+def test_measure_metrics_and_tune_delta_vs_reference():
+    """Batched measure_metrics / tune_delta (one shadow serve + confusion counts
+    on the GPU) against the reference's per-record loops (cache.cpp:267-335)
+    run by oracle/_ref on the same trained deployment and records."""
+    model_txt, vtxt, X, _, _ = _load_trained()
+    x = X[:512]
+    m = lcb.load_base_model(model_txt)
+    vs = [lcb.load_variant(t) for t in vtxt]
+    dep = lcb.Deployment(m, vs, precision="bf16x3", max_batch=len(x))
+    rm = O.RefModel.load(model_txt)
+    rvs = [O.RefVariant.load(t) for t in vtxt]
+    grid = [0.5, 0.55, 0.6, 0.65, 0.7, 0.75, 0.8, 0.85, 0.9, 0.95]  # cache.hpp:99
+    ours = dep.measure_metrics(x, grid)
+    sh = dep.serve(x, shadow=True)  # GPU probabilities at every layer: in-band accounting
+    for v, rv in zip(vs, rvs):
+        for row in ours[v.layer]:
+            rv.set_delta(row["delta"])
+            ref_c, ref_hr, ref_acc = O.ref_measure_metrics(rm, rv, x)
+            p = sh.probs[v.layer - 1]
+            band = int(np.sum(np.abs(p.astype(np.float64) - row["delta"]) < BAND))
+            diff = sum(abs(row[k] - ref_c[k]) for k in ("tp", "fp", "tn", "fn"))
+            assert diff <= 2 * band, (v.layer, row, ref_c, band)
+            if diff == 0:
+                assert abs(row["hit_rate"] - ref_hr) < 1e-12 and abs(row["accuracy"] - ref_acc) < 1e-12
+    for target in (0.8, 0.95, 0.999):
+        tuned = dep.tune_delta(x, target, grid, apply=False)
+        for v, rv in zip(vs, rvs):
+            assert tuned[v.layer] == O.ref_tune_delta(rm, rv, x, target, grid), (v.layer, target)
+    # applied thresholds drive the serve path
+    tuned = dep.tune_delta(x, 0.95, grid, apply=True)
+    res = dep.serve(x)
+    for v in vs:
+        assert v.delta == tuned[v.layer]
+        hit_here = res.exit_layer == v.layer
+        assert np.all(sh.probs[v.layer - 1][hit_here] >= tuned[v.layer] - BAND)
+    dep.close()
