@@ -115,7 +115,7 @@ def build_deployment(cfg_name, batch, precision, device, seed=2101):
     if family == "mlp":
         m = lcb.make_base_model(3072, classes, C1_WIDTHS, 8, seed)
         vs = [lcb.build_variant(l + 1, l, C1_MENU[l], m.tap_dim(l + 1), classes, seed + 1) for l in range(8)]
-        calib = mlp_inputs(min(batch, 512), 3072, seed + 2)
+        calib = mlp_inputs(min(max(batch, 128), 512), 3072, seed + 2)
         gen = lambda B, s: mlp_inputs(B, 3072, s)  # noqa: E731
     else:
         m = lcb.make_cnn_model(arch, classes, seed)
@@ -126,7 +126,7 @@ def build_deployment(cfg_name, batch, precision, device, seed=2101):
             a = ("FC(256)" if l % 2 == 0 else f"Pool({C})") if arch.startswith("vgg") else f"Pool({C})"
             vs.append(lcb.build_variant(l, 0, a, m.tap_dim(l), classes, seed + l))
         side = 32 if arch.endswith("cifar") else 224
-        calib = image_inputs(min(batch, 256), 3, side, side, seed + 2)
+        calib = image_inputs(min(max(batch, 128), 256), 3, side, side, seed + 2)  # >= 128 images even at batch 1
         gen = lambda B, s: image_inputs(B, 3, side, side, s)  # noqa: E731
     fr = calibrate_variants(m, vs, calib, full_frac, precision=precision, device=device)
     dep = lcb.Deployment(m, vs, precision=precision, max_batch=batch, device=device)
