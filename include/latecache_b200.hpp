@@ -212,7 +212,56 @@ class Deployment {
 
   void set_delta(int layer, double delta) { check(lc_engine_set_delta(h_.get(), layer, delta)); }
 
+  // measure_metrics (cache.cpp:316-335) of every attached cache at every
+  // threshold of `grid`, over the records these inputs make (one batch of at
+  // most max_batch): result[layer - 1][g] (zero rows where no cache).
+  struct Confusion {
+    long long tp = 0, fp = 0, tn = 0, fn = 0;
+    double hit_rate() const {
+      const long long n = tp + fp + tn + fn;
+      return n ? static_cast<double>(tp + fp) / static_cast<double>(n) : 0.0;
+    }
+    double accuracy() const { return tp + fp ? static_cast<double>(tp) / static_cast<double>(tp + fp) : 1.0; }
+  };
+  std::vector<std::vector<Confusion>> measure_metrics(const std::vector<std::vector<double>>& inputs,
+                                                      const std::vector<double>& grid) {
+    const std::vector<float> x = flatten(inputs);
+    const int B = static_cast<int>(inputs.size()), G = static_cast<int>(grid.size());
+    std::vector<long long> c(static_cast<size_t>(model_.num_blocks) * G * 4);
+    check(lc_measure_metrics(h_.get(), x.data(), B, grid.data(), G, c.data()));
+    std::vector<std::vector<Confusion>> out(static_cast<size_t>(model_.num_blocks), std::vector<Confusion>(G));
+    for (int l = 0; l < model_.num_blocks; ++l)
+      for (int g = 0; g < G; ++g) {
+        const long long* q = &c[(static_cast<size_t>(l) * G + g) * 4];
+        out[l][g] = Confusion{q[0], q[1], q[2], q[3]};
+      }
+    return out;
+  }
+
+  // tune_delta (cache.cpp:267-307) for every attached cache; applies the
+  // thresholds to this deployment. result[layer - 1] (NaN where no cache).
+  std::vector<double> tune_delta(const std::vector<std::vector<double>>& inputs, double target_accuracy,
+                                 const std::vector<double>& grid) {
+    const std::vector<float> x = flatten(inputs);
+    std::vector<double> d(static_cast<size_t>(model_.num_blocks));
+    check(lc_tune_delta(h_.get(), x.data(), static_cast<int>(inputs.size()), target_accuracy, grid.data(),
+                        static_cast<int>(grid.size()), d.data(), 1));
+    return d;
+  }
+
  private:
+  std::vector<float> flatten(const std::vector<std::vector<double>>& inputs) const {
+    const long long D = model_.input_dim();
+    if (inputs.empty() || static_cast<int>(inputs.size()) > max_batch_)
+      throw std::invalid_argument("measure: record count outside [1, max_batch]");
+    std::vector<float> x(inputs.size() * static_cast<size_t>(D));
+    for (size_t i = 0; i < inputs.size(); ++i) {
+      if (static_cast<long long>(inputs[i].size()) != D) throw std::invalid_argument("forward: input dim mismatch");
+      for (long long j = 0; j < D; ++j) x[i * D + j] = static_cast<float>(inputs[i][j]);
+    }
+    return x;
+  }
+
   BaseModel model_;
   int max_batch_;
   std::shared_ptr<lc_engine> h_;
