@@ -145,7 +145,7 @@ __device__ __forceinline__ unsigned long long clk() {
 constexpr int kTraceCtas = 8, kTraceUnits = 32;
 __device__ __forceinline__ void trace_put(const TcConvParams& p, int unit, int field) {
   if (p.trace && blockIdx.x < kTraceCtas && unit < kTraceUnits)
-    p.trace[(blockIdx.x * kTraceUnits + unit) * 8 + field] = clk();
+    p.trace[(blockIdx.x * kTraceUnits + unit) * 16 + field] = clk();
 }
 
 // Tile-invariant part of a tile row's output coordinates: image slot j and
@@ -368,8 +368,9 @@ __device__ __forceinline__ void gap_segment(const TcConvParams& p, const Tile& x
 // the tile (all resident: one unit per CTA, single round), then reduce 1/ks of
 // the tile (warp units of 16 columns x 32 rows, fixed k order) and run the
 // epilogue on it. Kept out of line: it is the rare path.
+// scratch: >= 8 warps x 2 KB of shared memory (the epilogue staging area).
 __device__ __noinline__ void split_reduce(const TcConvParams& p, const TileGeom& g, const Tile& x, int BN, int etid,
-                                          int lane, int unit) {
+                                          int lane, int unit, uint8_t* scratch) {
   int* arr = p.ws_counters + 2 * x.tile_mn;
   int* dep = arr + 1;
   __threadfence();
@@ -385,36 +386,73 @@ __device__ __noinline__ void split_reduce(const TcConvParams& p, const TileGeom&
   const int u0 = static_cast<int>((static_cast<long long>(nu) * x.ks) / g.ks);
   const int u1 = static_cast<int>((static_cast<long long>(nu) * (x.ks + 1)) / g.ks);
   const float* tile_ws = p.ws + static_cast<size_t>(x.tile_mn) * g.ks * kBM * BN;
-  for (int uu = u0 + (etid >> 5); uu < u1; uu += kEpiWarps) {
+  if (etid == 0) trace_put(p, unit, 8);
+  // wpu warps share a unit (32 rows x 16 columns): warp `sub` sums the
+  // partials k in [sub*ks/wpu, (sub+1)*ks/wpu) (all its loads in flight at
+  // once), parks the sum in shared memory, and the unit's first warp adds the
+  // wpu sums in ascending sub order (fixed association: deterministic).
+  const int warp = etid >> 5;
+  const int nunits = u1 - u0;
+  int wpu = 1;
+  while (nunits > 0 && wpu * 2 * nunits <= kEpiWarps) wpu *= 2;  // (a CTA may own no unit: nu < ks)
+  const int per_round = kEpiWarps / wpu;
+  float4* park = reinterpret_cast<float4*>(scratch);  // [warp][4][32] float4
+  for (int base = u0; base < u1; base += per_round) {
+    const int uu = base + warp / wpu, sub = warp % wpu;
     const int c16 = uu / (kBM / 32), r = (uu % (kBM / 32)) * 32 + lane;
     float v[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = 0.0f;
+    if (uu < u1) {
+      const int k0 = (g.ks * sub) / wpu, k1 = (g.ks * (sub + 1)) / wpu;
 #pragma unroll 6  // the partial loads of 6 k's go out together; the adds keep ascending k order
-    for (int k = 0; k < g.ks; ++k) {
-      const float4* src = reinterpret_cast<const float4*>(tile_ws + static_cast<size_t>(k) * kBM * BN +
-                                                          (static_cast<size_t>(c16) * kBM + r) * 16);
+      for (int k = k0; k < k1; ++k) {
+        // layout [k][c16][q][row] float4: a warp's load of one q is 512 contiguous bytes
+        const float4* src = reinterpret_cast<const float4*>(tile_ws + static_cast<size_t>(k) * kBM * BN) +
+                            static_cast<size_t>(c16) * 4 * kBM + r;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const float4 f = __ldcg(src + u);
-        v[4 * u] += f.x;
-        v[4 * u + 1] += f.y;
-        v[4 * u + 2] += f.z;
-        v[4 * u + 3] += f.w;
+        for (int u = 0; u < 4; ++u) {
+          const float4 f = __ldcg(src + u * kBM);
+          v[4 * u] += f.x;
+          v[4 * u + 1] += f.y;
+          v[4 * u + 2] += f.z;
+          v[4 * u + 3] += f.w;
+        }
+      }
+      if (wpu > 1) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          park[(warp * 4 + u) * 32 + lane] = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
       }
     }
-    size_t ob;
-    int img;
-    bool img_ok;
-    const int co = x.tn * BN + c16 * 16;
-    if (out_row(p, g, x, r, row_geom(p, r), ob, img, img_ok)) {
-      epilogue_store_ld(p, v, ob + co, co);
-    } else {
+    if (wpu > 1) epi_bar();
+    if (uu < u1 && sub == 0) {
+      for (int w = 1; w < wpu; ++w) {
 #pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = 0.0f;
+        for (int u = 0; u < 4; ++u) {
+          const float4 f = park[((warp + w) * 4 + u) * 32 + lane];
+          v[4 * u] += f.x;
+          v[4 * u + 1] += f.y;
+          v[4 * u + 2] += f.z;
+          v[4 * u + 3] += f.w;
+        }
+      }
+      size_t ob;
+      int img;
+      bool img_ok;
+      const int co = x.tn * BN + c16 * 16;
+      if (out_row(p, g, x, r, row_geom(p, r), ob, img, img_ok)) {
+        epilogue_store_ld(p, v, ob + co, co);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = 0.0f;
+      }
+      if (p.gap_out) gap_segment(p, x, r, lane, v, co, img, img_ok);
+      if (lane == 0) trace_put(p, unit, 9 + (warp < 2 ? warp : 1));
     }
-    if (p.gap_out) gap_segment(p, x, r, lane, v, co, img, img_ok);
+    if (wpu > 1) epi_bar();  // park slots reused by the next round
   }
+  if (etid == 0) trace_put(p, unit, 11);
   epi_bar();
   if (etid == 0) {
     if (atomicAdd(dep, 1) == g.ks - 1) {
@@ -794,7 +832,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
         st_ob[i] = __shfl_sync(0xffffffffu, static_cast<unsigned long long>(obase), r);
         st_ok[i] = __shfl_sync(0xffffffffu, valid ? 1 : 0, r) != 0;
       }
-      // split-K partial tile layout: [tile_mn][ks][BN/16][128 rows][16] (64 B per row chunk)
+      // split-K partial tile layout: [tile_mn][ks][BN/16][4 float4 groups][128 rows] (coalesced per warp)
       float* wsp = split ? p.ws + (static_cast<size_t>(x.tile_mn) * g.ks + x.ks) * kBM * BN : nullptr;
 #pragma unroll 1
       for (int c32 = 0; c32 < kCols / 32; ++c32) {
@@ -811,10 +849,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
             const int c16 = (col0 >> 4) + c32 * 2 + u;
-            float4* dst = reinterpret_cast<float4*>(wsp + (static_cast<size_t>(c16) * kBM + row) * 16);
+            float4* dst = reinterpret_cast<float4*>(wsp) + static_cast<size_t>(c16) * 4 * kBM + row;
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-              dst[q] = make_float4(v[u][4 * q], v[u][4 * q + 1], v[u][4 * q + 2], v[u][4 * q + 3]);
+              __stcg(dst + q * kBM, make_float4(v[u][4 * q], v[u][4 * q + 1], v[u][4 * q + 2], v[u][4 * q + 3]));
           }
           continue;
         }
@@ -884,7 +922,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
       if (lane == 0) mbar_arrive(tempty0 + 8 * acc);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
-      if (split) split_reduce(p, g, x, BN, etid, lane, unit);
+      if (split) split_reduce(p, g, x, BN, etid, lane, unit, epi_stage);
       if (etid == 0) trace_put(p, unit, 5);
     }
   }

@@ -466,8 +466,8 @@ static void perf_conv(const char* name, int N, int nsurv, int H, int W, int C, i
   CK(cudaMalloc(&dCtr, 4 * g_sms * 4));
   CK(cudaMemset(dCtr, 0, 4 * g_sms * 4));
   unsigned long long* dTrace;
-  CK(cudaMalloc(&dTrace, 8 * 32 * 8 * 8));
-  CK(cudaMemset(dTrace, 0, 8 * 32 * 8 * 8));
+  CK(cudaMalloc(&dTrace, 8 * 32 * 16 * 8));
+  CK(cudaMemset(dTrace, 0, 8 * 32 * 16 * 8));
   TcConvParams p;
   memset(&p, 0, sizeof(p));
   int hb, wb, ipt;
@@ -562,17 +562,18 @@ static void perf_conv(const char* name, int N, int nsurv, int H, int W, int C, i
     p.trace = dTrace;
     CK(tc_conv_launch(p, BN, g_sms, 0));
     CK(cudaDeviceSynchronize());
-    std::vector<unsigned long long> tr(8 * 32 * 8);
+    std::vector<unsigned long long> tr(8 * 32 * 16);
     CK(cudaMemcpy(tr.data(), dTrace, tr.size() * 8, cudaMemcpyDeviceToHost));
     for (int cta = 0; cta < 2; ++cta) {
-      const unsigned long long t0 = tr[(cta * 32) * 8 + 0];
+      const unsigned long long t0 = tr[(cta * 32) * 16 + 0];
       printf("  trace CTA %d (cycles from first TMA issue): unit: tma0 tmaN | mma0 mmaN | epi0 epiN | split: fenced waited\n", cta);
       for (int u = 0; u < 32; ++u) {
-        const unsigned long long* q = &tr[(cta * 32 + u) * 8];
+        const unsigned long long* q = &tr[(cta * 32 + u) * 16];
         if (!q[0] && !q[4]) break;
         auto rel = [&](unsigned long long v) { return v ? (long long)(v - t0) : -1LL; };
-        printf("   %2d: %8lld %8lld | %8lld %8lld | %8lld %8lld | %8lld %8lld\n", u, rel(q[0]), rel(q[1]), rel(q[2]),
-               rel(q[3]), rel(q[4]), rel(q[5]), rel(q[6]), rel(q[7]));
+        printf("   %2d: %8lld %8lld | %8lld %8lld | %8lld %8lld | %8lld %8lld | red %8lld w0 %8lld w1 %8lld end %8lld\n",
+               u, rel(q[0]), rel(q[1]), rel(q[2]), rel(q[3]), rel(q[4]), rel(q[5]), rel(q[6]), rel(q[7]), rel(q[8]),
+               rel(q[9]), rel(q[10]), rel(q[11]));
       }
     }
   }
