@@ -143,6 +143,15 @@ int lc_engine_stage_input(lc_engine* e, const float* src, int B, int on_device);
  * (ms from batch start to the request's exit). Output pointers are nullable. */
 int lc_serve_batch(lc_engine* e, const float* inputs, int B, unsigned flags, int* exit_layer, int* served,
                    int* base_pred, float* probs, double* latency_ms);
+/* Pipelined form of lc_serve_batch (two slots): submit enqueues the H2D copy
+ * of `inputs` (pinned host memory for a truly asynchronous copy) on a copy
+ * stream, the serve and the result D2H on the engine stream, and returns at
+ * once with the slot id; the next submit's upload overlaps this batch's
+ * compute. collect waits for the slot and returns the lc_serve_batch outputs.
+ * A slot must be collected before its next reuse (else its results are dropped). */
+int lc_serve_submit(lc_engine* e, const float* inputs, int B, unsigned flags, int* slot);
+int lc_serve_collect(lc_engine* e, int slot, int B, int* exit_layer, int* served, int* base_pred, float* probs,
+                     double* latency_ms);
 /* Same, input already in lc_engine_input(); enqueued asynchronously. */
 int lc_serve_device(lc_engine* e, int B, unsigned flags);
 int lc_engine_sync(lc_engine* e);

@@ -88,6 +88,8 @@ def _load() -> C.CDLL:
         "lc_engine_counts": (I, [P, pI]),
         "lc_lookup_batch": (I, [P, I, pF, I, pI, pI, pF, pF, pF]),
         "lc_measure_metrics": (I, [P, pF, I, pD, I, C.POINTER(C.c_longlong)]),
+        "lc_serve_submit": (I, [P, pF, I, C.c_uint, pI]),
+        "lc_serve_collect": (I, [P, I, I, pI, pI, pI, pF, pD]),
         "lc_tune_delta": (I, [P, pF, I, C.c_double, pD, I, pD, I]),
         "lc_engine_time": (I, [P, I, C.c_uint, I, pD]),
         "lc_engine_kernel_count": (I, [P, C.c_uint, I]),
@@ -134,5 +136,5 @@ EXPORTED_SYMBOLS = [
     "lc_engine_set_delta", "lc_engine_set_selector_out", "lc_engine_input", "lc_serve_batch", "lc_serve_device",
     "lc_engine_sync", "lc_engine_results", "lc_engine_counts", "lc_lookup_batch", "lc_engine_time",
     "lc_engine_kernel_count", "lc_engine_profile", "lc_serve_timed", "lc_engine_stage_input",
-    "lc_measure_metrics", "lc_tune_delta",
+    "lc_measure_metrics", "lc_tune_delta", "lc_serve_submit", "lc_serve_collect",
 ]

@@ -321,6 +321,26 @@ class Deployment:
         check(lib.lc_serve_batch(self._h, _fptr(x), B, flags, _iptr(el), _iptr(sv), _iptr(bp), _fptr(pr), _dptr(lat)))
         return ServeResult(el, sv, bp, pr, lat)
 
+    def submit(self, inputs: np.ndarray, shadow: bool = False) -> tuple:
+        """Pipelined serve: enqueue one batch (H2D on a copy stream overlapping the
+        previous batch's compute) and return a ticket for collect(). `inputs`
+        should live in pinned host memory (e.g. a torch pin_memory() tensor's
+        numpy view) for the copy to be asynchronous; it must stay alive until collect."""
+        x = np.ascontiguousarray(inputs, dtype=np.float32)
+        slot = C.c_int()
+        check(lib.lc_serve_submit(self._h, _fptr(x), x.shape[0], LC_SERVE_SHADOW if shadow else 0, C.byref(slot)))
+        return (slot.value, x.shape[0], x)
+
+    def collect(self, ticket: tuple) -> ServeResult:
+        slot, B, _ = ticket
+        el = np.zeros(B, np.int32)
+        sv = np.zeros(B, np.int32)
+        bp = np.zeros(B, np.int32)
+        pr = np.zeros((self.blocks, B), np.float32)
+        lat = np.zeros(B, np.float64)
+        check(lib.lc_serve_collect(self._h, slot, B, _iptr(el), _iptr(sv), _iptr(bp), _fptr(pr), _dptr(lat)))
+        return ServeResult(el, sv, bp, pr, lat)
+
     def stage_input_device(self, src_ptr: int, B: int) -> None:
         """Copy B inputs from device memory (raw pointer) into the engine's input buffer."""
         check(lib.lc_engine_stage_input(self._h, C.c_void_p(src_ptr), B, 1))

@@ -479,6 +479,19 @@ int lc_tune_delta(lc_engine* e, const float* inputs, int B, double target_accura
   });
 }
 
+int lc_serve_submit(lc_engine* e, const float* inputs, int B, unsigned flags, int* slot) {
+  return guard([&] {
+    need(inputs, "inputs");
+    need(slot, "slot");
+    *slot = eng(e).submit(inputs, B, (flags & LC_SERVE_SHADOW) != 0);
+  });
+}
+
+int lc_serve_collect(lc_engine* e, int slot, int B, int* exit_layer, int* served, int* base_pred, float* probs,
+                     double* latency_ms) {
+  return guard([&] { eng(e).collect(slot, B, exit_layer, served, base_pred, probs, latency_ms); });
+}
+
 int lc_serve_device(lc_engine* e, int B, unsigned flags) {
   return guard([&] { eng(e).serve(B, (flags & LC_SERVE_SHADOW) != 0, (flags & LC_SERVE_NO_GRAPH) == 0); });
 }

@@ -201,6 +201,17 @@ Engine::~Engine() {
     if (g) cudaGraphExecDestroy(g);
   for (void* p : allocs_) cudaFree(p);
   if (h_batch_) cudaFreeHost(h_batch_);
+  if (copy_stream_) cudaStreamSynchronize(copy_stream_);
+  for (Slot& sl : slots_) {
+    if (sl.h_exit) cudaFreeHost(sl.h_exit);
+    if (sl.h_served) cudaFreeHost(sl.h_served);
+    if (sl.h_base) cudaFreeHost(sl.h_base);
+    if (sl.h_probs) cudaFreeHost(sl.h_probs);
+    if (sl.h_ns) cudaFreeHost(sl.h_ns);
+    for (cudaEvent_t e : {sl.in_done, sl.in_free, sl.out_done})
+      if (e) cudaEventDestroy(e);
+  }
+  if (copy_stream_) cudaStreamDestroy(copy_stream_);
   if (ev0_) cudaEventDestroy(ev0_);
   if (ev1_) cudaEventDestroy(ev1_);
 }
@@ -904,8 +915,7 @@ void Engine::serve(int B, bool shadow, bool use_graph) {
   std::lock_guard<std::recursive_mutex> dev_lock(dev_stream(device_).mu);
   require(B > 0 && B <= max_batch_, "serve: batch size " + std::to_string(B) + " outside [1, max_batch]");
   ck(cudaSetDevice(device_), "cudaSetDevice");
-  *h_batch_ = B;
-  ck(cudaMemcpyAsync(d_batch_, h_batch_, sizeof(int), cudaMemcpyHostToDevice, stream_), "batch size");
+  launch_set_int(d_batch_, B, stream_);
   std::vector<Step>& st = steps_for(shadow);
   if (!use_graph) {
     for (Step& s : st) s.run(stream_);
@@ -932,6 +942,75 @@ void Engine::serve_host(const float* x, int B, bool shadow, bool use_graph) {
                      stream_),
      "input upload");
   serve(B, shadow, use_graph);
+}
+
+void Engine::init_slots() {
+  if (copy_stream_) return;
+  const int L = model_.num_blocks, B = max_batch_;
+  ck(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking), "copy stream");
+  for (Slot& sl : slots_) {
+    sl.d_in = static_cast<float*>(dalloc(static_cast<size_t>(B) * model_.input_dim() * sizeof(float)));
+    ck(cudaMallocHost(&sl.h_exit, static_cast<size_t>(B) * sizeof(int)), "cudaMallocHost");
+    ck(cudaMallocHost(&sl.h_served, static_cast<size_t>(B) * sizeof(int)), "cudaMallocHost");
+    ck(cudaMallocHost(&sl.h_base, static_cast<size_t>(B) * sizeof(int)), "cudaMallocHost");
+    ck(cudaMallocHost(&sl.h_probs, static_cast<size_t>(L) * B * sizeof(float)), "cudaMallocHost");
+    ck(cudaMallocHost(&sl.h_ns, static_cast<size_t>(B + 1) * 8), "cudaMallocHost");
+    ck(cudaEventCreateWithFlags(&sl.in_done, cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&sl.in_free, cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&sl.out_done, cudaEventDisableTiming), "event");
+    ck(cudaEventRecord(sl.in_free, stream_), "event");
+  }
+}
+
+int Engine::submit(const float* x, int B, bool shadow) {
+  std::lock_guard<std::recursive_mutex> dev_lock(dev_stream(device_).mu);
+  require(B > 0 && B <= max_batch_, "submit: batch size " + std::to_string(B) + " outside [1, max_batch]");
+  ck(cudaSetDevice(device_), "cudaSetDevice");
+  init_slots();
+  const int id = next_slot_;
+  next_slot_ ^= 1;
+  Slot& sl = slots_[id];
+  if (sl.busy) ck(cudaEventSynchronize(sl.out_done), "slot wait");  // uncollected results are dropped
+  const size_t bytes = static_cast<size_t>(B) * model_.input_dim() * sizeof(float);
+  // H2D on the copy stream once the slot's previous staging copy was consumed
+  ck(cudaStreamWaitEvent(copy_stream_, sl.in_free, 0), "wait");
+  ck(cudaMemcpyAsync(sl.d_in, x, bytes, cudaMemcpyHostToDevice, copy_stream_), "input upload");
+  ck(cudaEventRecord(sl.in_done, copy_stream_), "event");
+  // compute stream: stage into the graph's input buffer, serve, results to host
+  ck(cudaStreamWaitEvent(stream_, sl.in_done, 0), "wait");
+  ck(cudaMemcpyAsync(d_x_, sl.d_in, bytes, cudaMemcpyDeviceToDevice, stream_), "input stage");
+  ck(cudaEventRecord(sl.in_free, stream_), "event");
+  serve(B, shadow, true);
+  const int L = model_.num_blocks;
+  ck(cudaMemcpyAsync(sl.h_exit, d_exit_, B * sizeof(int), cudaMemcpyDeviceToHost, stream_), "d2h");
+  ck(cudaMemcpyAsync(sl.h_served, d_served_, B * sizeof(int), cudaMemcpyDeviceToHost, stream_), "d2h");
+  ck(cudaMemcpyAsync(sl.h_base, d_base_, B * sizeof(int), cudaMemcpyDeviceToHost, stream_), "d2h");
+  ck(cudaMemcpy2DAsync(sl.h_probs, static_cast<size_t>(B) * sizeof(float), d_probs_,
+                       static_cast<size_t>(max_batch_) * sizeof(float), static_cast<size_t>(B) * sizeof(float), L,
+                       cudaMemcpyDeviceToHost, stream_),
+     "d2h");
+  ck(cudaMemcpyAsync(sl.h_ns, d_exit_ns_, static_cast<size_t>(B) * 8, cudaMemcpyDeviceToHost, stream_), "d2h");
+  ck(cudaMemcpyAsync(sl.h_ns + B, d_t0_, 8, cudaMemcpyDeviceToHost, stream_), "d2h");
+  ck(cudaEventRecord(sl.out_done, stream_), "event");
+  sl.B = B;
+  sl.busy = true;
+  return id;
+}
+
+void Engine::collect(int slot, int B, int* exit_layer, int* served, int* base, float* probs_LB, double* latency_ms) {
+  require(slot == 0 || slot == 1, "collect: bad slot");
+  Slot& sl = slots_[slot];
+  require(sl.busy, "collect: slot holds no submitted batch");
+  require(B == sl.B, "collect: batch size differs from the submitted one");
+  ck(cudaEventSynchronize(sl.out_done), "collect");
+  const size_t n = static_cast<size_t>(B);
+  if (exit_layer) std::memcpy(exit_layer, sl.h_exit, n * sizeof(int));
+  if (served) std::memcpy(served, sl.h_served, n * sizeof(int));
+  if (base) std::memcpy(base, sl.h_base, n * sizeof(int));
+  if (probs_LB) std::memcpy(probs_LB, sl.h_probs, static_cast<size_t>(model_.num_blocks) * n * sizeof(float));
+  if (latency_ms)
+    for (size_t i = 0; i < n; ++i) latency_ms[i] = static_cast<double>(sl.h_ns[i] - sl.h_ns[n]) * 1e-6;
+  sl.busy = false;
 }
 
 void Engine::measure(int B, const double* grid, int G, long long* counts) {
@@ -998,8 +1077,7 @@ void Engine::lookup(int layer, const float* taps_dev, int B, int* hit, int* labe
     tap.count = d_lk_count_;
     add_lookup_steps(c.lookup_steps, c, tap, max_batch_, false);
   }
-  *h_batch_ = B;
-  ck(cudaMemcpyAsync(d_lk_count_, h_batch_, sizeof(int), cudaMemcpyHostToDevice, stream_), "count");
+  launch_set_int(d_lk_count_, B, stream_);
   launch_split_taps_nchw(taps_dev, ti.C, mlp ? 1 : ti.H * ti.W, B, row_stride, lk_tap_.hi, lk_tap_.lo, stream_);
   for (Step& s : c.lookup_steps) s.run(stream_);
   ck(cudaGetLastError(), "lookup");
@@ -1059,8 +1137,7 @@ std::vector<StepProfile> Engine::profile(int B, bool shadow) {
   std::lock_guard<std::recursive_mutex> dev_lock(dev_stream(device_).mu);
   require(B > 0 && B <= max_batch_, "profile: batch outside [1, max_batch]");
   ck(cudaSetDevice(device_), "cudaSetDevice");
-  *h_batch_ = B;
-  ck(cudaMemcpyAsync(d_batch_, h_batch_, sizeof(int), cudaMemcpyHostToDevice, stream_), "batch size");
+  launch_set_int(d_batch_, B, stream_);
   std::vector<Step>& st = steps_for(shadow);
   std::vector<cudaEvent_t> ev(st.size() + 1);
   for (auto& e : ev) ck(cudaEventCreate(&e), "event");

@@ -59,6 +59,12 @@ class Engine {
   // request runs full depth; base_pred for all; first hit recorded).
   void serve(int B, bool shadow, bool use_graph);
   void serve_host(const float* x, int B, bool shadow, bool use_graph);
+  // Pipelined serving from pinned host memory (two slots): the H2D copy of a
+  // submitted batch runs on a copy stream while the previous batch computes;
+  // results come back by D2H into the slot's pinned buffers. submit returns
+  // the slot; collect waits for it and copies the results out.
+  int submit(const float* x_pinned, int B, bool shadow);
+  void collect(int slot, int B, int* exit_layer, int* served, int* base, float* probs_LB, double* latency_ms);
   void synchronize();
   // Results (device pointers, indexed by request id).
   const int* exit_layer() const { return d_exit_; }
@@ -180,6 +186,21 @@ class Engine {
   bool built_compact_ = false, built_shadow_ = false;
   cudaGraphExec_t graph_[2] = {nullptr, nullptr};
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
+  struct Slot {
+    float* d_in = nullptr;  // staged input [max_batch][input_dim]
+    int* h_exit = nullptr;  // pinned results
+    int* h_served = nullptr;
+    int* h_base = nullptr;
+    float* h_probs = nullptr;  // [blocks][max_batch]
+    unsigned long long* h_ns = nullptr;  // [max_batch + 1]: exit times, then t0
+    cudaEvent_t in_done = nullptr, in_free = nullptr, out_done = nullptr;
+    int B = 0;
+    bool busy = false;
+  };
+  Slot slots_[2];
+  int next_slot_ = 0;
+  cudaStream_t copy_stream_ = nullptr;
+  void init_slots();
 
   // lookup-only scratch
   Planes lk_tap_;

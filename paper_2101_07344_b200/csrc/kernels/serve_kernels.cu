@@ -1054,6 +1054,12 @@ __global__ void maxpool_kernel(const __nv_bfloat16* hi, const __nv_bfloat16* lo,
   }
 }
 
+__global__ void set_int_kernel(int* p, int v) {
+  pdl_wait();
+  pdl_trigger();
+  *p = v;
+}
+
 __global__ void stamp_kernel(unsigned long long* t0) {
   pdl_wait();
   pdl_trigger(); *t0 = globaltimer(); }
@@ -1276,6 +1282,8 @@ void launch_maxpool(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int H, int
     launch_pdl(maxpool_kernel<0>, dim3(max_rows, gy), dim3(256), 0, s, hi, lo, H, W, C, k, stride, pad, Ho, Wo, ids,
                count, ohi, olo);
 }
+
+void launch_set_int(int* p, int v, cudaStream_t s) { launch_pdl(set_int_kernel, dim3(1), dim3(1), 0, s, p, v); }
 
 void launch_stamp_start(unsigned long long* t0, cudaStream_t s) { launch_pdl(stamp_kernel, dim3(1), dim3(1), 0, s, t0); }
 

@@ -151,6 +151,9 @@ void launch_maxpool(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int H, int
                     __nv_bfloat16* olo, cudaStream_t s);
 
 void launch_stamp_start(unsigned long long* t0, cudaStream_t s);
+// *p = v as a stream-ordered kernel (the value travels in the launch parameters,
+// so back-to-back submissions never race on a host staging word).
+void launch_set_int(int* p, int v, cudaStream_t s);
 // Batch prologue: B = *batch; ids0 = identity, count0 = B, rows_out = B *
 // rows_mult (stem GEMM rows, nullable), outputs reset, probs [L][max_batch] = NaN.
 void launch_init_batch(const int* batch, int max_batch, int* ids0, int* count0, int* rows_out, int rows_mult,

@@ -454,3 +454,26 @@ def test_measure_metrics_and_tune_delta_vs_reference():
         hit_here = res.exit_layer == v.layer
         assert np.all(sh.probs[v.layer - 1][hit_here] >= tuned[v.layer] - BAND)
     dep.close()
+
+
+def test_pipelined_submit_collect_matches_serve():
+    """The pipelined e2e entry point (two slots in flight, uploads on a copy
+    stream) returns exactly what the synchronous serve returns per batch."""
+    import torch
+    m, vs = _cnn_deployment("resnet18_cifar", 10, 21, 64)
+    dep = lcb.Deployment(m, vs, precision="bf16x3", max_batch=32)
+    xs = [torch.from_numpy(image_inputs(32, 3, 32, 32, seed=40 + k).astype(np.float32)).pin_memory() for k in range(5)]
+    ref = [dep.serve(x.numpy()) for x in xs]
+    pending, got = [], []
+    for x in xs:
+        pending.append(dep.submit(x.numpy()))
+        if len(pending) == 2:
+            got.append(dep.collect(pending.pop(0)))
+    while pending:
+        got.append(dep.collect(pending.pop(0)))
+    for a, b in zip(ref, got):
+        assert np.array_equal(a.exit_layer, b.exit_layer) and np.array_equal(a.served, b.served)
+        assert np.array_equal(a.base_pred, b.base_pred)
+        assert np.array_equal(a.probs, b.probs, equal_nan=True)
+        assert np.all(b.latency_ms >= 0)
+    dep.close()
