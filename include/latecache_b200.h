@@ -63,6 +63,14 @@ int lc_model_save(const lc_model* m, char** text, size_t* len);
 /* CNN families of BASELINE.json (no reference counterpart): "resnet18_cifar",
  * "resnet50", "resnet152", "vgg16_cifar"; synthetic weights from `seed`. */
 int lc_model_make_cnn(const char* arch, int num_classes, uint64_t seed, lc_model** out);
+/* Binary checkpoints: the text formats' content with raw
+ * little-endian doubles (no decimal round trip; multi-GB weights), plus the
+ * CNN op list. save: *data malloc'd (free with lc_free); load: LC_ERR_RUNTIME
+ * on a truncated / malformed buffer (the reference's malformed-file errors). */
+int lc_model_save_binary(const lc_model* m, char** data, size_t* len);
+int lc_model_load_binary(const char* data, size_t len, lc_model** out);
+int lc_variant_save_binary(const lc_variant* v, char** data, size_t* len);
+int lc_variant_load_binary(const char* data, size_t len, lc_variant** out);
 int lc_model_info(const lc_model* m, int* blocks, int* classes, long long* input_dim);
 /* Tap geometry of block `layer` (1-based), NCHW: dim = C*H*W (mlp: C = width, H = W = 1). */
 int lc_model_tap(const lc_model* m, int layer, int* C, int* H, int* W);
@@ -178,6 +186,15 @@ int lc_measure_metrics(lc_engine* e, const float* inputs, int B, const double* g
  * deltas[blocks] (NaN where no cache); apply != 0 sets the engine thresholds. */
 int lc_tune_delta(lc_engine* e, const float* inputs, int B, double target_accuracy, const double* grid, int G,
                   double* deltas, int apply);
+
+/* Hardware-aware costs (replaces CostModel::lookup_ms, cache.hpp:46-55, and the
+ * modeled LayerProfile, composer.hpp): one shadow batch of the B host requests
+ * through the graph with device timestamps at every block boundary.
+ * block_ms[blocks] = base-model device time per block (block 1 includes the
+ * stem, the last block the head) — the LayerProfile for check_constraints /
+ * compose; lookup_ms[blocks] = cache lookup + exit time at each layer (0 where
+ * no cache is attached) — the VariantMetrics::lookup_ms column. */
+int lc_engine_layer_times(lc_engine* e, const float* inputs, int B, double* block_ms, double* lookup_ms);
 
 /* Device time of `iters` graph replays of a B-request batch (CUDA events on the engine stream). */
 int lc_engine_time(lc_engine* e, int B, unsigned flags, int iters, double* ms_per_batch);

@@ -89,6 +89,11 @@ def _load() -> C.CDLL:
         "lc_lookup_batch": (I, [P, I, pF, I, pI, pI, pF, pF, pF]),
         "lc_measure_metrics": (I, [P, pF, I, pD, I, C.POINTER(C.c_longlong)]),
         "lc_serve_submit": (I, [P, pF, I, C.c_uint, pI]),
+        "lc_engine_layer_times": (I, [P, pF, I, pD, pD]),
+        "lc_model_save_binary": (I, [P, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t)]),
+        "lc_model_load_binary": (I, [C.c_char_p, C.c_size_t, C.POINTER(C.c_void_p)]),
+        "lc_variant_save_binary": (I, [P, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t)]),
+        "lc_variant_load_binary": (I, [C.c_char_p, C.c_size_t, C.POINTER(C.c_void_p)]),
         "lc_serve_collect": (I, [P, I, I, pI, pI, pI, pF, pD]),
         "lc_tune_delta": (I, [P, pF, I, C.c_double, pD, I, pD, I]),
         "lc_engine_time": (I, [P, I, C.c_uint, I, pD]),
@@ -120,6 +125,13 @@ def check(status: int) -> None:
     raise RuntimeError(msg)
 
 
+def take_bytes(ptr: C.c_void_p, n: C.c_size_t) -> bytes:
+    try:
+        return C.string_at(ptr, n.value)
+    finally:
+        lib.lc_free(ptr)
+
+
 def take_string(ptr: C.c_void_p, n: C.c_size_t) -> str:
     try:
         return C.string_at(ptr, n.value).decode()
@@ -136,5 +148,6 @@ EXPORTED_SYMBOLS = [
     "lc_engine_set_delta", "lc_engine_set_selector_out", "lc_engine_input", "lc_serve_batch", "lc_serve_device",
     "lc_engine_sync", "lc_engine_results", "lc_engine_counts", "lc_lookup_batch", "lc_engine_time",
     "lc_engine_kernel_count", "lc_engine_profile", "lc_serve_timed", "lc_engine_stage_input",
-    "lc_measure_metrics", "lc_tune_delta", "lc_serve_submit", "lc_serve_collect",
+    "lc_measure_metrics", "lc_tune_delta", "lc_serve_submit", "lc_serve_collect", "lc_engine_layer_times",
+    "lc_model_save_binary", "lc_model_load_binary", "lc_variant_save_binary", "lc_variant_load_binary",
 ]

@@ -25,7 +25,7 @@ from typing import Dict, List, Optional, Sequence
 import numpy as np
 
 from ._lib import (LC_PREC_BF16, LC_PREC_BF16X3, LC_SERVE_NO_GRAPH, LC_SERVE_SHADOW, CnnOpDesc, check, lib,
-                   take_string)
+                   take_bytes, take_string)
 
 _PREC = {"bf16x3": LC_PREC_BF16X3, "bf16": LC_PREC_BF16}
 
@@ -64,6 +64,12 @@ class BaseModel:
         p, n = C.c_void_p(), C.c_size_t()
         check(lib.lc_model_save(self._h, C.byref(p), C.byref(n)))
         return take_string(p, n)
+
+    def save_binary(self) -> bytes:
+        """Binary checkpoint (raw doubles; CNN op lists included)."""
+        p, n = C.c_void_p(), C.c_size_t()
+        check(lib.lc_model_save_binary(self._h, C.byref(p), C.byref(n)))
+        return take_bytes(p, n)
 
     def tap(self, layer: int):
         c, h, w = C.c_int(), C.c_int(), C.c_int()
@@ -111,6 +117,12 @@ def load_base_model(text: str) -> BaseModel:
     b = text.encode()
     h = C.c_void_p()
     check(lib.lc_model_load(b, len(b), C.byref(h)))
+    return BaseModel(h)
+
+
+def load_base_model_binary(data: bytes) -> BaseModel:
+    h = C.c_void_p()
+    check(lib.lc_model_load_binary(data, len(data), C.byref(h)))
     return BaseModel(h)
 
 
@@ -179,6 +191,11 @@ class CacheVariant:
         check(lib.lc_variant_save(self._h, C.byref(p), C.byref(n)))
         return take_string(p, n)
 
+    def save_binary(self) -> bytes:
+        p, n = C.c_void_p(), C.c_size_t()
+        check(lib.lc_variant_save_binary(self._h, C.byref(p), C.byref(n)))
+        return take_bytes(p, n)
+
     def layers(self, which: int) -> List[NetLayer]:
         """which = 0: predictor, 1: selector; weights copied out as fp64 arrays."""
         out = []
@@ -214,7 +231,27 @@ def load_variant(text: str) -> CacheVariant:
     return CacheVariant(h)
 
 
+def load_variant_binary(data: bytes) -> CacheVariant:
+    h = C.c_void_p()
+    check(lib.lc_variant_load_binary(data, len(data), C.byref(h)))
+    return CacheVariant(h)
+
+
 # ---------------------------------------------------------------- plan / workload
+def with_measured_lookup_ms(metrics_text: str, lookup_ms: Dict[int, float]) -> str:
+    """The reference metrics file (cache.cpp:412-450; columns layer variant arch
+    hit_rate accuracy lookup_ms memory_mb tp fp tn fn) with the modeled
+    lookup_ms of every row at a measured layer replaced by the device time."""
+    out = []
+    for line in metrics_text.split("\n"):
+        f = line.split()
+        if len(f) >= 11 and not line.startswith("#") and f[0].lstrip("-").isdigit() and int(f[0]) in lookup_ms:
+            f[5] = repr(float(lookup_ms[int(f[0])]))
+            line = " ".join(f)
+        out.append(line)
+    return "\n".join(out)
+
+
 def plan_check(metrics_text: str, plan_text: str, profile_ms: Sequence[float], accuracy_threshold: float,
                memory_budget_mb: float):
     """load_metrics + load_plan + check_constraints; returns (feasible, violations, [(layer, variant)])."""
@@ -432,6 +469,16 @@ class Deployment:
             for v in self.variants:
                 v.delta = out[v.layer]
         return out
+
+    def layer_times(self, inputs: np.ndarray):
+        """Hardware-aware profile: device-measured base time
+        per block (the LayerProfile) and lookup time per cache layer (the
+        VariantMetrics::lookup_ms column) from one shadow batch of `inputs`."""
+        x = np.ascontiguousarray(inputs, dtype=np.float32)
+        bm = np.zeros(self.blocks, np.float64)
+        lm = np.zeros(self.blocks, np.float64)
+        check(lib.lc_engine_layer_times(self._h, _fptr(x), x.shape[0], _dptr(bm), _dptr(lm)))
+        return bm, {v.layer: float(lm[v.layer - 1]) for v in self.variants}
 
     def time_batch(self, B: int, iters: int, shadow: bool = False) -> float:
         ms = C.c_double()

@@ -118,6 +118,60 @@ int lc_model_save(const lc_model* m, char** text, size_t* len) {
   });
 }
 
+int lc_model_save_binary(const lc_model* m, char** data, size_t* len) {
+  return guard([&] {
+    need(m, "model");
+    need(data, "data");
+    need(len, "len");
+    const std::string b = lcb::save_base_model_binary(m->m);
+    *data = static_cast<char*>(std::malloc(b.size() ? b.size() : 1));
+    std::memcpy(*data, b.data(), b.size());
+    *len = b.size();
+  });
+}
+
+int lc_model_load_binary(const char* data, size_t len, lc_model** out) {
+  return guard([&] {
+    need(data, "data");
+    need(out, "out");
+    auto* m = new lc_model;
+    try {
+      m->m = lcb::load_base_model_binary(std::string(data, len));
+    } catch (...) {
+      delete m;
+      throw;
+    }
+    *out = m;
+  });
+}
+
+int lc_variant_save_binary(const lc_variant* v, char** data, size_t* len) {
+  return guard([&] {
+    need(v, "variant");
+    need(data, "data");
+    need(len, "len");
+    const std::string b = lcb::save_variant_binary(v->v);
+    *data = static_cast<char*>(std::malloc(b.size() ? b.size() : 1));
+    std::memcpy(*data, b.data(), b.size());
+    *len = b.size();
+  });
+}
+
+int lc_variant_load_binary(const char* data, size_t len, lc_variant** out) {
+  return guard([&] {
+    need(data, "data");
+    need(out, "out");
+    auto* v = new lc_variant;
+    try {
+      v->v = lcb::load_variant_binary(std::string(data, len));
+    } catch (...) {
+      delete v;
+      throw;
+    }
+    *out = v;
+  });
+}
+
 int lc_model_make_cnn(const char* arch, int num_classes, uint64_t seed, lc_model** out) {
   return guard([&] {
     need(arch, "arch");
@@ -476,6 +530,21 @@ int lc_tune_delta(lc_engine* e, const float* inputs, int B, double target_accura
       deltas[l - 1] = best_delta;
       if (apply) en.set_delta(l, best_delta);
     }
+  });
+}
+
+int lc_engine_layer_times(lc_engine* e, const float* inputs, int B, double* block_ms, double* lookup_ms) {
+  return guard([&] {
+    need(inputs, "inputs");
+    need(block_ms, "block_ms");
+    need(lookup_ms, "lookup_ms");
+    lcb::Engine& en = eng(e);
+    if (B <= 0 || B > en.max_batch()) throw std::invalid_argument("layer_times: batch outside [1, max_batch]");
+    const size_t bytes = static_cast<size_t>(B) * static_cast<size_t>(en.input_dim()) * sizeof(float);
+    if (cudaSetDevice(en.device()) != cudaSuccess ||
+        cudaMemcpyAsync(en.input_buffer(), inputs, bytes, cudaMemcpyHostToDevice, en.stream()) != cudaSuccess)
+      throw lcb::CudaFailure("layer_times: input copy failed");
+    en.layer_times(B, block_ms, lookup_ms);
   });
 }
 

@@ -232,6 +232,7 @@ void Engine::build_weights() {
   d_exit_ns_ = static_cast<unsigned long long*>(dalloc(static_cast<size_t>(B) * 8));
   d_t0_ = static_cast<unsigned long long*>(dalloc(8));
   d_probs_ = static_cast<float*>(dalloc(static_cast<size_t>(L) * B * sizeof(float)));
+  d_block_ns_ = static_cast<unsigned long long*>(dalloc(static_cast<size_t>(L + 1) * 2 * 8));
   d_labels_ = static_cast<int*>(dalloc(static_cast<size_t>(L) * B * sizeof(int)));
   d_grid_ = static_cast<double*>(dalloc(64 * sizeof(double)));
   d_conf_ = static_cast<unsigned long long*>(dalloc(static_cast<size_t>(L) * 64 * 4 * sizeof(unsigned long long)));
@@ -583,6 +584,34 @@ ExitParams Engine::exit_params(int layer, bool shadow, const int* ids_in, int* i
   return e;
 }
 
+// %globaltimer stamp into d_block_ns_[layer][which] (shadow step lists only).
+void Engine::add_stamp(std::vector<Step>& steps, int layer, int which) {
+  unsigned long long* dst = d_block_ns_ + static_cast<size_t>(layer - 1) * 2 + which;
+  steps.push_back({[dst](cudaStream_t s) { launch_stamp_start(dst, s); }, 0, 1});
+}
+
+void Engine::layer_times(int B, double* block_ms, double* lookup_ms) {
+  std::lock_guard<std::recursive_mutex> dev_lock(dev_stream(device_).mu);
+  const int L = model_.num_blocks;
+  ck(cudaMemsetAsync(d_block_ns_, 0, static_cast<size_t>(L + 1) * 2 * 8, stream_), "memset");
+  serve(B, true, true);
+  std::vector<unsigned long long> ns(static_cast<size_t>(L + 1) * 2);
+  unsigned long long t0 = 0;
+  ck(cudaMemcpyAsync(ns.data(), d_block_ns_, ns.size() * 8, cudaMemcpyDeviceToHost, stream_), "d2h");
+  ck(cudaMemcpyAsync(&t0, d_t0_, 8, cudaMemcpyDeviceToHost, stream_), "d2h");
+  ck(cudaStreamSynchronize(stream_), "layer_times sync");
+  unsigned long long prev = t0;
+  for (int l = 0; l < L; ++l) {
+    const unsigned long long base_end = ns[static_cast<size_t>(l) * 2];
+    const unsigned long long lk_end = ns[static_cast<size_t>(l) * 2 + 1];
+    block_ms[l] = base_end > prev ? static_cast<double>(base_end - prev) * 1e-6 : 0.0;
+    lookup_ms[l] = lk_end > base_end ? static_cast<double>(lk_end - base_end) * 1e-6 : 0.0;
+    prev = lk_end > base_end ? lk_end : base_end;
+  }
+  const unsigned long long head_end = ns[static_cast<size_t>(L) * 2];
+  if (head_end > prev) block_ms[L - 1] += static_cast<double>(head_end - prev) * 1e-6;
+}
+
 // ------------------------------------------------------------------ MLP serve
 void Engine::build_mlp_steps(std::vector<Step>& steps, bool shadow) {
   const int B = max_batch_, L = model_.num_blocks;
@@ -648,6 +677,7 @@ void Engine::build_mlp_steps(std::vector<Step>& steps, bool shadow) {
                      static_cast<int>(cur_count - d_counts_), 2.0 * f.in * f.out,
                      (x3 ? 4.0 : 2.0) * (static_cast<double>(f.inp) + f.outp)});
     const int layer = b + 1;
+    if (shadow) add_stamp(steps, layer, 0);
     const int ci = cache_of_layer_[static_cast<size_t>(layer)];
     if (ci >= 0) {
       DevCache& c = *caches_[static_cast<size_t>(ci)];
@@ -664,6 +694,7 @@ void Engine::build_mlp_steps(std::vector<Step>& steps, bool shadow) {
       int* cnt_out = counts + layer;
       const ExitParams ex = exit_params(layer, shadow, cur_ids, ids_out, src_out, cnt_out);
       add_lookup_steps(steps, c, tap, B, false, false, &ex);
+      if (shadow) add_stamp(steps, layer, 1);
       if (!shadow) {
         Planes dst = mlp_cin_[static_cast<size_t>(b)];
         const long long row_elems = f.outp;
@@ -688,6 +719,7 @@ void Engine::build_mlp_steps(std::vector<Step>& steps, bool shadow) {
                                      cur_count, B, d_base_, nullptr, d_exit_, d_served_, d_exit_ns_, s);
                    },
                    0});
+  if (shadow) add_stamp(steps, L + 1, 0);  // after the head (charged to the last block)
 }
 
 // ------------------------------------------------------------------ CNN serve
@@ -865,6 +897,7 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow) {
     }
     if (o.tap >= 0) {
       const int layer = o.tap + 1;
+      if (shadow) add_stamp(steps, layer, 0);
       const int ci = cache_of_layer_[static_cast<size_t>(layer)];
       if (ci >= 0) {
         DevCache& c = *caches_[static_cast<size_t>(ci)];
@@ -882,11 +915,13 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow) {
         tap.count = cur_count;
         const ExitParams ex = exit_params(layer, shadow, cur_ids, ids_out, nullptr, cnt_out);
         add_lookup_steps(steps, c, tap, B, true, c.gap != nullptr, &ex);
+        if (shadow) add_stamp(steps, layer, 1);
         cur_ids = ids_out;
         cur_count = cnt_out;
       }
     }
   }
+  if (shadow) add_stamp(steps, L + 1, 0);  // after the head (charged to the last block)
 }
 
 std::vector<Step>& Engine::steps_for(bool shadow) {

@@ -84,6 +84,12 @@ class Engine {
   // pass), then confusion counts {tp, fp, tn, fn} per layer and threshold.
   // counts: host [blocks][G][4]; rows of layers without a cache are zero.
   void measure(int B, const double* grid, int G, long long* counts);
+  // Hardware-aware costs: one shadow batch of the B staged
+  // requests through the graph with %globaltimer stamps at every block
+  // boundary: block_ms[l] = base-model time of block l (the reference's
+  // LayerProfile entries; block 1 includes the stem, the last block the head),
+  // lookup_ms[l] = the cache lookup + exit at layer l (0 where none).
+  void layer_times(int B, double* block_ms, double* lookup_ms);
   void set_delta(int layer, double delta);
   double delta(int layer) const;
   bool has_cache(int layer) const {
@@ -115,6 +121,7 @@ class Engine {
   void add_lookup_steps(std::vector<Step>& steps, DevCache& c, const TapView& tap, int max_rows, bool stage_gather,
                         bool fused_gap = false, const ExitParams* ex = nullptr);
   ExitParams exit_params(int layer, bool shadow, const int* ids_in, int* ids_out, int* src_rows_out, int* count_out);
+  void add_stamp(std::vector<Step>& steps, int layer, int which);
   std::vector<Step>& steps_for(bool shadow);
   void* dalloc(size_t bytes);
   Planes alloc_planes(size_t elems);
@@ -145,6 +152,7 @@ class Engine {
   unsigned long long* d_exit_ns_ = nullptr;
   unsigned long long* d_t0_ = nullptr;
   float* d_probs_ = nullptr;
+  unsigned long long* d_block_ns_ = nullptr;  // shadow mode: [blocks][2] = {base work done, lookup done}
   int* d_labels_ = nullptr;   // [blocks][max_batch] argmax(pr) of every probed layer
   double* d_grid_ = nullptr;  // measure(): threshold grid (<= 64)
   unsigned long long* d_conf_ = nullptr;  // measure(): [blocks][64][4]

@@ -169,6 +169,12 @@ CacheVariant build_variant(int layer, int variant_idx, const ArchSpec& arch, lon
 std::string save_variant(const CacheVariant& v);
 CacheVariant load_variant(const std::string& text);
 
+// Binary mirror of the text checkpoints (host/binfmt.cpp; raw doubles, plus the CNN op list).
+std::string save_base_model_binary(const BaseModel& m);
+BaseModel load_base_model_binary(const std::string& data);
+std::string save_variant_binary(const CacheVariant& v);
+CacheVariant load_variant_binary(const std::string& data);
+
 // ----------------------------------------------------------------- plan
 struct VariantMetrics {
   int layer = 0, variant = 0;

@@ -477,3 +477,32 @@ def test_pipelined_submit_collect_matches_serve():
         assert np.array_equal(a.probs, b.probs, equal_nan=True)
         assert np.all(b.latency_ms >= 0)
     dep.close()
+
+
+def test_layer_times_hardware_profile():
+    """Device-measured LayerProfile + lookup costs (§8f rank 2) on the trained
+    deployment and a CNN: positive per-block times, a lookup time at every
+    cache layer, and their sum close to the shadow batch's device time."""
+    model_txt, vtxt, X, _, _ = _load_trained()
+    m = lcb.load_base_model(model_txt)
+    vs = [lcb.load_variant(t) for t in vtxt]
+    dep = lcb.Deployment(m, vs, precision="bf16x3", max_batch=256)
+    block_ms, lookup_ms = dep.layer_times(X[:256])
+    assert np.all(block_ms > 0)
+    assert set(lookup_ms) == {v.layer for v in vs} and all(t > 0 for t in lookup_ms.values())
+    metrics = open(os.path.join(GOLDEN, "trained", "metrics.txt")).read()
+    plan = open(os.path.join(GOLDEN, "trained", "plan.txt")).read()
+    measured = lcb.with_measured_lookup_ms(metrics, lookup_ms)
+    ok, viol, _ = lcb.plan_check(measured, plan, list(block_ms), 0.97, 64.0)
+    assert isinstance(ok, bool)
+    dep.close()
+    cm, cvs = _cnn_deployment("resnet18_cifar", 10, 21, 64)
+    cdep = lcb.Deployment(cm, cvs, precision="bf16x3", max_batch=64)
+    x = image_inputs(64, 3, 32, 32, seed=3)
+    bm, lm = cdep.layer_times(x)
+    assert np.all(bm > 0) and all(t > 0 for t in lm.values())
+    import torch
+    cdep.stage_input_device(torch.from_numpy(x.astype(np.float32)).cuda().data_ptr(), 64)
+    total = np.median([cdep.serve_timed(64, shadow=True) for _ in range(5)])
+    assert 0.5 * total < bm.sum() + sum(lm.values()) < 1.5 * total, (bm.sum(), sum(lm.values()), total)
+    cdep.close()

@@ -120,6 +120,52 @@ def test_plan_check_golden():
         lcb.plan_check(metrics, "latecache-plan v1\nchoices 1\nchoice 9 9 FC(1) # x\n", [4.0] * 8, 0.97, 64.0)
 
 
+def test_measured_lookup_costs_feed_check_constraints():
+    """Hardware-aware costs: measured lookup_ms replaces the
+    modeled column; check_constraints' overlap rule (composer.cpp:143-150)
+    then judges the plan with the device numbers."""
+    d = os.path.join(GOLDEN, "trained")
+    metrics = open(os.path.join(d, "metrics.txt")).read()
+    plan = open(os.path.join(d, "plan.txt")).read()
+    ok, _, chosen = lcb.plan_check(metrics, plan, [4.0] * 8, 0.97, 64.0)
+    assert ok
+    fast = lcb.with_measured_lookup_ms(metrics, {l: 0.01 for l, _ in chosen})
+    rows = [l.split() for l in fast.split("\n") if l and not l.startswith(("#", "latecache"))]
+    assert all(float(r[5]) == 0.01 for r in rows if int(r[0]) in {l for l, _ in chosen})
+    assert lcb.plan_check(fast, plan, [4.0] * 8, 0.97, 64.0)[0]
+    # a lookup slower than the serve time to the next chosen cache violates the overlap rule
+    slow = lcb.with_measured_lookup_ms(metrics, {chosen[0][0]: 1e3})
+    ok2, viol2, _ = lcb.plan_check(slow, plan, [4.0] * 8, 0.97, 64.0)
+    assert not ok2 and any("exceeds" in v for v in viol2)
+
+
+def test_binary_checkpoints_round_trip():
+    """Binary checkpoints (§8f rank 4) carry exactly the text formats' content:
+    text -> binary -> text is byte-identical (every double bit-exact), CNN op
+    lists survive, malformed buffers raise the reference's runtime error."""
+    d = os.path.join(GOLDEN, "trained")
+    mt = open(os.path.join(d, "model.txt")).read()
+    m = lcb.load_base_model(mt)
+    b = m.save_binary()
+    assert lcb.load_base_model_binary(b).save() == m.save()
+    for k in range(7):
+        vt = open(os.path.join(d, f"variant_{k}.txt")).read()
+        v = lcb.load_variant(vt)
+        v2 = lcb.load_variant_binary(v.save_binary())
+        assert v2.save() == v.save()
+    cm = lcb.make_cnn_model("resnet18_cifar", 10, 3)
+    cb = cm.save_binary()
+    cm2 = lcb.load_base_model_binary(cb)
+    assert cm2.save_binary() == cb
+    a, z = cm.cnn_ops(), cm2.cnn_ops()
+    assert len(a) == len(z) and all(np.array_equal(x["w"], y["w"]) for x, y in zip(a, z))
+    for bad in (b[:-9], b"not a checkpoint", b[:12]):
+        with pytest.raises(RuntimeError):
+            lcb.load_base_model_binary(bad)
+    with pytest.raises(RuntimeError):
+        lcb.load_variant_binary(b)  # a model buffer is not a variant
+
+
 def test_gen_workload_matches_reference_fixture():
     d = os.path.join(GOLDEN, "trained")
     ds = open(os.path.join(d, "dataset.txt")).read().split("\n")
