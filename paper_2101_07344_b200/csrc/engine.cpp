@@ -803,6 +803,16 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow) {
         ok = ok && encode_act_map(&prm->tmA[1], in.lo, o.C, o.W, o.H, B, 1, abw, abh, o.stride) &&
              encode_weight_map(&prm->tmB[1], dc.w.lo, dc.Kp, o.Cout, BN);
       if (!ok) throw CudaFailure("engine: TMA descriptor encode failed (conv)");
+      if (!halo && ipt > 1) {
+        bool mok = encode_act_map(&prm->tmAm[0], in.hi, o.C, o.W, o.H, B, 1, abw, abh, o.stride, ipt) &&
+                   (!x3 || encode_act_map(&prm->tmAm[1], in.lo, o.C, o.W, o.H, B, 1, abw, abh, o.stride, ipt));
+        if (mok && o.res >= 0 && mma_residual_) {
+          const Planes& rb = slot_buf_[static_cast<size_t>(o.res)];
+          mok = encode_act_map(&prm->tmRm[0], rb.hi, o.Cout, Wo, Ho, B, 1, wb, hb, 1, ipt) &&
+                (!x3 || encode_act_map(&prm->tmRm[1], rb.lo, o.Cout, Wo, Ho, B, 1, wb, hb, 1, ipt));
+        }
+        prm->multi_img = mok ? 1 : 0;
+      }
       if (halo) {
         hb = 1;
         wb = 1;

@@ -688,6 +688,13 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
             imgs[j] = image_of(p, idx);
           }
         }
+        // one box for all ipt images when their ids are consecutive
+        bool consec = p.multi_img != 0 && ipt > 1 && x.grp * ipt + ipt <= g.count;
+        for (int j = 1; consec && j < ipt; ++j) consec = imgs[j] == imgs[0] + j;
+        // per tile: which maps and how many boxes per plane (the K-step loop stays branch-free)
+        const CUtensorMap* mapA = consec ? p.tmAm : p.tmA;
+        const CUtensorMap* mapR = consec ? p.tmRm : p.tmR;
+        const int nbox = consec ? 1 : ipt;
         const int nk_conv = p.ntaps * cchunks;
         int cc = x.s_begin % cchunks, tap = x.s_begin / cchunks;
         for (int s = x.s_begin; s < x.s_end; ++s) {
@@ -703,8 +710,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
             for (int pl = 0; pl < Cfg::kPlanes; ++pl) {
               const uint32_t a_dst = smem_u32(stage_a(stage, pl));
 #pragma unroll 1
-              for (int jj = 0; jj < ipt; ++jj)
-                tma_load_5d(a_dst + jj * box_bytes, &p.tmR[pl], fb, x.tn * BN + j * 64, x.w0, x.h0, imgs[jj], 0);
+              for (int jj = 0; jj < nbox; ++jj)
+                tma_load_5d(a_dst + jj * box_bytes, &mapR[pl], fb, x.tn * BN + j * 64, x.w0, x.h0, imgs[jj], 0);
               tma_load_2d(smem_u32(stage_b(stage, pl)), &p.tmE, fb, j * 64, 0);
             }
           } else {
@@ -713,7 +720,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
           for (int pl = 0; pl < Cfg::kPlanes; ++pl) {
             const uint32_t a_dst = smem_u32(stage_a(stage, pl));
 #pragma unroll 1
-            for (int j = 0; j < ipt; ++j) tma_load_5d(a_dst + j * box_bytes, &p.tmA[pl], fb, cc * 64, wc, hc, imgs[j], ph);
+            for (int j = 0; j < nbox; ++j) tma_load_5d(a_dst + j * box_bytes, &mapA[pl], fb, cc * 64, wc, hc, imgs[j], ph);
             tma_load_2d(smem_u32(stage_b(stage, pl)), &p.tmB[pl], fb, tap * p.C + cc * 64, x.tn * BN);
           }
           }
@@ -969,7 +976,8 @@ cudaError_t launch_cfg(const TcConvParams& p, int num_sms, cudaStream_t stream) 
 
 }  // namespace
 
-bool encode_act_map(CUtensorMap* map, const void* base, int C, int W, int H, int N, int P, int wb, int hb, int stride) {
+bool encode_act_map(CUtensorMap* map, const void* base, int C, int W, int H, int N, int P, int wb, int hb, int stride,
+                    int nbox) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[5] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H),
@@ -981,7 +989,8 @@ bool encode_act_map(CUtensorMap* map, const void* base, int C, int W, int H, int
   strides[3] = strides[2] * N;
   const cuuint32_t st = static_cast<cuuint32_t>(stride < 1 ? 1 : stride);
   // With traversal stride st, TMA loads boxDim/st elements: box = wanted * st.
-  cuuint32_t box[5] = {64, static_cast<cuuint32_t>(wb) * st, static_cast<cuuint32_t>(hb) * st, 1, 1};
+  cuuint32_t box[5] = {64, static_cast<cuuint32_t>(wb) * st, static_cast<cuuint32_t>(hb) * st,
+                       static_cast<cuuint32_t>(nbox < 1 ? 1 : nbox), 1};
   cuuint32_t estr[5] = {1, st, st, 1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,

@@ -38,6 +38,13 @@ struct TcConvParams {
   CUtensorMap tmB[2];  // weight planes hi, lo (2-D: K, Cout)
   CUtensorMap tmR[2];  // residual planes as an A operand (nres > 0): 5-D NHWC at the output resolution
   CUtensorMap tmE;     // identity matrix [256][256] bf16 as the B operand of the residual K-steps
+  // ipt > 1 (several small images per tile): the same maps with box N-extent
+  // ipt, used when the tile's ipt image ids are consecutive (always at full
+  // batch / shadow mode, often in early compacted layers): one TMA box per
+  // plane instead of ipt (per-box cost dominates 4x4 / 8x8 images)
+  CUtensorMap tmAm[2];
+  CUtensorMap tmRm[2];
+  int multi_img;       // 1: tmAm (and tmRm when nres > 0) are valid
   int nres;            // residual K-steps per tile (BN/64): out = conv + residual computed by the MMA
   // Halo mode (stride-1 k x k conv, one image per tile): 128 output anchors on
   // the padded row pitch Pw = W + k - 1 (tiles_h = tiles per image, hb = wb = 1,
@@ -85,7 +92,7 @@ struct TcConvParams {
 
 // Host helpers (tc_conv.cu).
 bool encode_act_map(CUtensorMap* map, const void* base, int C, int W, int H, int N, int P, int wb, int hb,
-                    int stride = 1);
+                    int stride = 1, int nbox = 1);
 bool encode_weight_map(CUtensorMap* map, const void* base, int K, int Cout, int BN);
 int tc_conv_pick_bn(int Cout, int segs = 1);
 // Halo-mode geometry for a stride-1 k x k conv over an H x W image; BN may be
