@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -963,7 +964,15 @@ void Engine::serve(int B, bool shadow, bool use_graph) {
   launch_set_int(d_batch_, B, stream_);
   std::vector<Step>& st = steps_for(shadow);
   if (!use_graph) {
-    for (Step& s : st) s.run(stream_);
+    static const bool sync_steps = std::getenv("LCB_SYNC_STEPS") != nullptr;  // debug: locate a failing step
+    for (size_t i = 0; i < st.size(); ++i) {
+      st[i].run(stream_);
+      if (sync_steps) {
+        std::fprintf(stderr, "lcb step %zu (kind %d) ...", i, st[i].kind);
+        ck(cudaStreamSynchronize(stream_), "step");
+        std::fprintf(stderr, " done\n");
+      }
+    }
     ck(cudaGetLastError(), "serve");
     return;
   }

@@ -667,62 +667,82 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
       }
     }
   } else if (warp == 0) {
-    if (lane == 0) {
-      // ------------------------------------------------ TMA producer
+    {
+      // ------------------------------------------------ TMA producer (whole warp)
+      // A stage's TMA boxes (per plane: nbox activation boxes + one weight
+      // box) are spread over the lanes and issued by one warp instruction: a
+      // single thread issuing them back to back is latency-bound (~2x slower
+      // on the 5-D activation boxes, tests/cuda/tma_lat.cu).
       int stage = 0;
       uint32_t phase = 0;
       const int box_bytes = p.hb * p.wb * 128;
       int unit = 0;
       for (int t = blockIdx.x; t < g.total; t += gridDim.x, ++unit) {
         const Tile x = decode_tile(t, p, g);
-        trace_put(p, unit, 0);
-        int imgs[16];
+        if (lane == 0) trace_put(p, unit, 0);
         const int ipt = p.plain ? 1 : p.ipt;
-        if (p.plain) {
-          imgs[0] = 0;
-        } else {
-#pragma unroll 1
-          for (int j = 0; j < ipt; ++j) {
-            int idx = x.grp * ipt + j;
-            if (idx >= g.count) idx = g.count - 1;  // rows discarded by the epilogue
-            imgs[j] = image_of(p, idx);
-          }
+        // lane j < ipt: image of the tile's j-th slot (rows of missing slots are discarded by the epilogue)
+        int my_img = 0;
+        if (!p.plain && lane < ipt) {
+          int idx = x.grp * ipt + lane;
+          if (idx >= g.count) idx = g.count - 1;
+          my_img = image_of(p, idx);
         }
+        const int img0 = __shfl_sync(0xffffffffu, my_img, 0);
         // one box for all ipt images when their ids are consecutive
-        bool consec = p.multi_img != 0 && ipt > 1 && x.grp * ipt + ipt <= g.count;
-        for (int j = 1; consec && j < ipt; ++j) consec = imgs[j] == imgs[0] + j;
-        // per tile: which maps and how many boxes per plane (the K-step loop stays branch-free)
+        const bool consec = p.multi_img != 0 && ipt > 1 && x.grp * ipt + ipt <= g.count &&
+                            __all_sync(0xffffffffu, lane >= ipt || my_img == img0 + lane);
         const CUtensorMap* mapA = consec ? p.tmAm : p.tmA;
         const CUtensorMap* mapR = consec ? p.tmRm : p.tmR;
         const int nbox = consec ? 1 : ipt;
+        // this lane's task in every stage: plane pl, box j (j == nbox: the B box)
+        const int ntask = Cfg::kPlanes * (nbox + 1);
+        const int pl = lane / (nbox + 1), jb = lane % (nbox + 1);
+        const int img_j = __shfl_sync(0xffffffffu, my_img, jb < nbox ? jb : 0);
         const int nk_conv = p.ntaps * cchunks;
         int cc = x.s_begin % cchunks, tap = x.s_begin / cchunks;
         for (int s = x.s_begin; s < x.s_end; ++s) {
           mbar_wait(empty0 + 8 * stage, phase ^ 1);
           const uint32_t fb = full0 + 8 * stage;
-          mbar_expect_tx(fb, dbg_noload ? 0u : static_cast<uint32_t>(Cfg::kStageBytes));
-          if (dbg_noload) {
-          } else if (s >= nk_conv) {
-            // residual K-step: A = residual channels [tn*BN + j*64, +64) at the
-            // output pixels, B = identity slice (the residual add on the tensor core)
-            const int j = s - nk_conv;
-#pragma unroll 1
-            for (int pl = 0; pl < Cfg::kPlanes; ++pl) {
-              const uint32_t a_dst = smem_u32(stage_a(stage, pl));
-#pragma unroll 1
-              for (int jj = 0; jj < nbox; ++jj)
-                tma_load_5d(a_dst + jj * box_bytes, &mapR[pl], fb, x.tn * BN + j * 64, x.w0, x.h0, imgs[jj], 0);
-              tma_load_2d(smem_u32(stage_b(stage, pl)), &p.tmE, fb, j * 64, 0);
+          if (lane == 0) mbar_expect_tx(fb, dbg_noload ? 0u : static_cast<uint32_t>(Cfg::kStageBytes));
+          __syncwarp();
+          if (!dbg_noload && ntask > 32 && lane == 0) {
+            // tiny images (> 15 per tile) with scattered ids: one lane walks all boxes
+            for (int q = 0; q < Cfg::kPlanes; ++q) {
+              const uint32_t a0 = smem_u32(stage_a(stage, q));
+              for (int j = 0; j < nbox; ++j) {
+                int idx = x.grp * ipt + j;
+                if (idx >= g.count) idx = g.count - 1;
+                const int im = image_of(p, idx);
+                if (s >= nk_conv)
+                  tma_load_5d(a0 + j * box_bytes, &mapR[q], fb, x.tn * BN + (s - nk_conv) * 64, x.w0, x.h0, im, 0);
+                else
+                  tma_load_5d(a0 + j * box_bytes, &mapA[q], fb, cc * 64, x.w0 * cs + p.tap_dw[tap],
+                              x.h0 * cs + p.tap_dh[tap], im, p.tap_phase[tap]);
+              }
+              if (s >= nk_conv)
+                tma_load_2d(smem_u32(stage_b(stage, q)), &p.tmE, fb, (s - nk_conv) * 64, 0);
+              else
+                tma_load_2d(smem_u32(stage_b(stage, q)), &p.tmB[q], fb, tap * p.C + cc * 64, x.tn * BN);
             }
-          } else {
-          const int wc = x.w0 * cs + p.tap_dw[tap], hc = x.h0 * cs + p.tap_dh[tap], ph = p.tap_phase[tap];
-#pragma unroll 1
-          for (int pl = 0; pl < Cfg::kPlanes; ++pl) {
-            const uint32_t a_dst = smem_u32(stage_a(stage, pl));
-#pragma unroll 1
-            for (int j = 0; j < nbox; ++j) tma_load_5d(a_dst + j * box_bytes, &mapA[pl], fb, cc * 64, wc, hc, imgs[j], ph);
-            tma_load_2d(smem_u32(stage_b(stage, pl)), &p.tmB[pl], fb, tap * p.C + cc * 64, x.tn * BN);
-          }
+          } else if (!dbg_noload && ntask <= 32 && lane < ntask) {
+            const uint32_t a_dst = smem_u32(stage_a(stage, pl)) + jb * box_bytes;
+            if (s >= nk_conv) {
+              // residual K-step: A = residual channels [tn*BN + j*64, +64) at the
+              // output pixels, B = identity slice (the residual add on the tensor core)
+              const int j = s - nk_conv;
+              if (jb < nbox)
+                tma_load_5d(a_dst, &mapR[pl], fb, x.tn * BN + j * 64, x.w0, x.h0, img_j, 0);
+              else
+                tma_load_2d(smem_u32(stage_b(stage, pl)), &p.tmE, fb, j * 64, 0);
+            } else {
+              if (jb < nbox) {
+                const int wc = x.w0 * cs + p.tap_dw[tap], hc = x.h0 * cs + p.tap_dh[tap], ph = p.tap_phase[tap];
+                tma_load_5d(a_dst, &mapA[pl], fb, cc * 64, wc, hc, img_j, ph);
+              } else {
+                tma_load_2d(smem_u32(stage_b(stage, pl)), &p.tmB[pl], fb, tap * p.C + cc * 64, x.tn * BN);
+              }
+            }
           }
           if (++cc == cchunks) {
             cc = 0;
@@ -733,7 +753,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
             phase ^= 1;
           }
         }
-        trace_put(p, unit, 1);
+        if (lane == 0) trace_put(p, unit, 1);
       }
     }
   } else if (warp == 1) {

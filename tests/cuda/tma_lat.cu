@@ -112,6 +112,43 @@ __device__ __forceinline__ void tma_load_3d_(uint32_t dst, const void* tmap, uin
       : "memory");
 }
 
+// Issue-parallel variant: the per_stage boxes of a stage are issued by per_stage
+// lanes of the warp in one instruction (lane 0 arms the barrier).
+__global__ void tma_lanes_kernel(const __grid_constant__ CUtensorMap map, int W, int H, int N, int wb, int hb,
+                                 int depth, int iters, int per_stage, unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bars[16];
+  const int lane = threadIdx.x;
+  if (lane == 0) {
+    for (int i = 0; i < 16; ++i) mbar_init(smem_u32(&bars[i]), 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (lane >= per_stage) return;
+  const uint32_t bytes = static_cast<uint32_t>(wb * hb) * 128;
+  uint32_t phase[16] = {};
+  unsigned int seed = blockIdx.x * 2654435761u + lane * 977u;
+  const unsigned long long t0 = clk();
+  for (int it = 0; it < iters; ++it) {
+    const int slot = it % depth;
+    if (it >= depth) {
+      mbar_wait(smem_u32(&bars[slot]), phase[slot]);
+      phase[slot] ^= 1;
+    }
+    if (lane == 0) mbar_expect_tx(smem_u32(&bars[slot]), bytes * per_stage);
+    seed = seed * 1664525u + 1013904223u;
+    const int n = (seed >> 8) % N, h0 = ((seed >> 4) % (H / hb)) * hb;
+    tma_load_5d(smem_u32(sm + (slot * per_stage + lane) * bytes), &map, smem_u32(&bars[slot]), 0, 0, h0, n, 0);
+  }
+  for (int k = 0; k < depth; ++k) {
+    const int slot = (iters + k) % depth;
+    mbar_wait(smem_u32(&bars[slot]), phase[slot]);
+    phase[slot] ^= 1;
+  }
+  if (lane == 0) out[blockIdx.x] = clk() - t0;
+}
+
 // dims = 3: (C, W, H*N); 4: (C, W, H, N). Same boxes {64, wb, hb(, 1)} as tc_conv's A loads.
 __global__ void tmaN_kernel(const __grid_constant__ CUtensorMap map, int dims, int W, int H, int N, int wb, int hb,
                             int depth, int iters, int per_stage, unsigned long long* out) {
@@ -214,6 +251,25 @@ int main() {
     __nv_bfloat16* act;
     cudaMalloc(&act, static_cast<size_t>(N) * H * W * C * 2);
     cudaMemset(act, 0, static_cast<size_t>(N) * H * W * C * 2);
+    for (int wbhb : {0, 1}) {
+      const int wb = wbhb ? 4 : 32, hb = 4;
+      CUtensorMap map;
+      if (!encode_act_map(&map, act, C, W, H, N, 1, wb, hb, 1)) return 1;
+      for (int ps : {1, 2, 4, 8}) {
+        const int iters = 1000, depth = 4;
+        const int smem = depth * ps * wb * hb * 128 + 1024;
+        cudaFuncSetAttribute(tma_lanes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        tma_lanes_kernel<<<148, 32, smem>>>(map, W, H, N, wb, hb, depth, iters, ps, d);
+        cudaDeviceSynchronize();
+        unsigned long long h[148];
+        cudaMemcpy(h, d, 148 * 8, cudaMemcpyDeviceToHost);
+        double mx = 0;
+        for (int i = 0; i < 148; ++i) mx = h[i] > mx ? h[i] : mx;
+        const double cyc = mx / iters;
+        printf("lanes: 5-D box {64,%d,%d} x%d per stage from %d lanes, depth 4: %7.1f cycles/stage, %6.1f B/clk/SM (%s)\n",
+               wb, hb, ps, ps, cyc, double(ps) * wb * hb * 128 / cyc, cudaGetErrorString(cudaGetLastError()));
+      }
+    }
     void* fp = nullptr;
     cudaDriverEntryPointQueryResult q;
     cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fp, cudaEnableDefault, &q);
