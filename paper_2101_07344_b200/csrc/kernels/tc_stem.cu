@@ -102,12 +102,16 @@ __global__ void __launch_bounds__(320, 1) tc_stem_kernel(const __grid_constant__
   const int npix = kBM + (p.kk - 1) * (p.Wx + 1);
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ------------------------------------------------ producer
+    {
+      // ------------------------------------------------ producer (whole warp:
+      // the planes x groups bulk copies of a slab go out from separate lanes)
       const uint32_t wplane = static_cast<uint32_t>(L.taps * kTapBytes);
-      mbar_expect_tx(wbar, L.w_bytes);
-      bulk_g2s(smem_u32(wsm), p.w_hi, wplane, wbar);
-      if (X3) bulk_g2s(smem_u32(wsm + wplane), p.w_lo, wplane, wbar);
+      if (lane == 0) {
+        mbar_expect_tx(wbar, L.w_bytes);
+        bulk_g2s(smem_u32(wsm), p.w_hi, wplane, wbar);
+        if (X3) bulk_g2s(smem_u32(wsm + wplane), p.w_lo, wplane, wbar);
+      }
+      const int pl = lane >> 1, grp = lane & 1;  // lane's copy: plane, channel group
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
@@ -116,14 +120,13 @@ __global__ void __launch_bounds__(320, 1) tc_stem_kernel(const __grid_constant__
         const int len = npix < HWx - m0 ? npix : HWx - m0;
         mbar_wait(empty0 + 8 * stage, phase ^ 1);
         const uint32_t fb = full0 + 8 * stage;
-        mbar_expect_tx(fb, static_cast<uint32_t>(L.planes * 2 * len * 16));
-        uint8_t* st = slabs + stage * L.stage_bytes;
-        for (int pl = 0; pl < L.planes; ++pl) {
+        if (lane == 0) mbar_expect_tx(fb, static_cast<uint32_t>(L.planes * 2 * len * 16));
+        __syncwarp();
+        if (pl < L.planes) {
+          uint8_t* st = slabs + stage * L.stage_bytes;
           const __nv_bfloat16* xp = pl == 0 ? p.x_hi : p.x_lo;
-          for (int grp = 0; grp < 2; ++grp) {
-            const __nv_bfloat16* src = xp + ((static_cast<size_t>(n) * 2 + grp) * HWx + m0) * 8;
-            bulk_g2s(smem_u32(st + pl * L.plane_bytes + grp * L.group_bytes), src, static_cast<uint32_t>(len * 16), fb);
-          }
+          const __nv_bfloat16* src = xp + ((static_cast<size_t>(n) * 2 + grp) * HWx + m0) * 8;
+          bulk_g2s(smem_u32(st + pl * L.plane_bytes + grp * L.group_bytes), src, static_cast<uint32_t>(len * 16), fb);
         }
         if (++stage == S) {
           stage = 0;
