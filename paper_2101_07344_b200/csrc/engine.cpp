@@ -186,6 +186,8 @@ Engine::Engine(int device, const BaseModel& model, std::vector<CacheVariant> var
   gap_fusion_ = !(nf && nf[0] == '1');
   const char* nl = std::getenv("LCB_UNFUSED_LOOKUP");
   fused_lookup_ = !(nl && nl[0] == '1');
+  const char* ns = std::getenv("LCB_NO_STACKED");
+  stacked_ = !(ns && ns[0] == '1');
   const char* nh = std::getenv("LCB_HALO");  // opt-in: not yet faster than the per-tap loads
   halo_ = nh && nh[0] == '1';
   const char* nr = std::getenv("LCB_NO_MMA_RESIDUAL");
@@ -837,6 +839,9 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow) {
       prm->C = o.C;
       prm->ntaps = o.k * o.k;
       prm->segs = x3 ? 3 : 1;
+      // many K-steps per tile: MMA-issue bound -> fewer, wider MMAs (the wider
+      // accumulator costs epilogue TMEM reads, which only pays for k x k convs)
+      prm->stacked = (x3 && o.k > 1 && stacked_) ? 1 : 0;
       prm->Cout = o.Cout;
       prm->ksplit = 1;
       prm->ks_max = 32;

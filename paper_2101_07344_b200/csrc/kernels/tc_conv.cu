@@ -29,7 +29,13 @@ struct TcCfg {
   static constexpr int kEpiStage = 8 * kEpiWarpBytes;
   static constexpr int kShiftBytes = 2 * BN * 4;  // per-tile shift values, double-buffered with the accumulators
   static constexpr int kSmem = kStages * kStageBytes + kEpiStage + 1024 /*bars*/ + kShiftBytes + 1024 /*align*/;
-  static constexpr uint32_t kTmemCols = 2 * BN;
+  // bf16x3 accumulators are 2*BN columns wide: with p.stacked the hi*hi and
+  // hi*lo products are ONE N = 2*BN MMA over the stage's contiguous
+  // [B_hi; B_lo] rows into [cols 0, BN) and [BN, 2BN), lo*hi goes into the
+  // low half, and the epilogue adds the halves (2 MMAs per K16 group instead of
+  // 3: an MMA costs ~38 + 0.375*N cycles and re-reads its A fragment).
+  static constexpr int kAccCols = X3 ? 2 * BN : BN;
+  static constexpr uint32_t kTmemCols = 2 * kAccCols;
   static_assert(kStages >= 2, "pipeline needs at least two stages");
 };
 
@@ -605,6 +611,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
     {  // whole warp: uniform operands, elect.sync issues
       // ------------------------------------------------ MMA issuer (halo)
       constexpr uint32_t idesc = umma_idesc_bf16(kBM, BN);
+      constexpr uint32_t idesc2 = umma_idesc_bf16(kBM, X3 ? 2 * BN : BN);  // stacked [B_hi; B_lo]
+      const bool stacked = X3 && p.stacked != 0;
       int aslot = 0, bslot = 0;
       uint32_t aphase = 0, bphase = 0;
       int acc = 0;
@@ -617,7 +625,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
         mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1);
         tc_fence_after();
         if (lane == 0) trace_put(p, unit, 2);
-        const uint32_t d_tmem = tmem_base + acc * BN;
+        const uint32_t d_tmem = tmem_base + acc * Cfg::kAccCols;
         const int m0 = x.h0 * kBM;
         const int base_row = m0 - (m0 / p.halo_pw) * p.halo_pw;  // anchor m0 inside the slab
         for (int s = x.s_begin; s < x.s_end; ++s) {
@@ -641,10 +649,15 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
           for (int k = 0; k < 4; ++k) {
             if (dbg_nomma) break;
             const uint32_t first = (s > x.s_begin || k > 0) ? 1u : 0u;
-            umma_bf16_warp(d_tmem, dah + 2 * k, dbh + 2 * k, idesc, first);
-            if (X3) {
-              if (!res) umma_bf16_warp(d_tmem, dah + 2 * k, dbl + 2 * k, idesc, 1u);
+            if (stacked && !res) {  // [hi*hi | hi*lo] in one MMA, then lo*hi into the low half
+              umma_bf16_warp(d_tmem, dah + 2 * k, dbh + 2 * k, idesc2, first);
               umma_bf16_warp(d_tmem, dal + 2 * k, dbh + 2 * k, idesc, 1u);
+            } else {
+              umma_bf16_warp(d_tmem, dah + 2 * k, dbh + 2 * k, idesc, first);
+              if (X3) {
+                if (!res) umma_bf16_warp(d_tmem, dah + 2 * k, dbl + 2 * k, idesc, 1u);
+                umma_bf16_warp(d_tmem, dal + 2 * k, dbh + 2 * k, idesc, 1u);
+              }
             }
           }
           umma_commit_warp(empty0 + 8 * bslot);
@@ -760,6 +773,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
     {  // whole warp: uniform operands, elect.sync issues
       // ------------------------------------------------ MMA issuer
       constexpr uint32_t idesc = umma_idesc_bf16(kBM, BN);
+      constexpr uint32_t idesc2 = umma_idesc_bf16(kBM, X3 ? 2 * BN : BN);  // stacked [B_hi; B_lo]
+      const bool stacked = X3 && p.stacked != 0;
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -770,7 +785,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
         mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1);
         tc_fence_after();
         if (lane == 0) trace_put(p, unit, 2);
-        const uint32_t d_tmem = tmem_base + acc * BN;
+        const uint32_t d_tmem = tmem_base + acc * Cfg::kAccCols;
         const int nk_conv = p.ntaps * (p.C / 64);
         for (int s = x.s_begin; s < x.s_end; ++s) {
           mbar_wait(full0 + 8 * stage, phase);
@@ -786,11 +801,16 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
           for (int k = 0; k < 4; ++k) {
             if (dbg_nomma) break;
             const uint32_t first = (s > x.s_begin || k > 0) ? 1u : 0u;
-            umma_bf16_warp(d_tmem, dah + 2 * k, dbh + 2 * k, idesc, first);
-            if (X3) {
-              if (!res_step)  // identity has no lo plane
-                umma_bf16_warp(d_tmem, dah + 2 * k, dbl + 2 * k, idesc, 1u);
+            if (stacked && !res_step) {  // [hi*hi | hi*lo] in one MMA, then lo*hi into the low half
+              umma_bf16_warp(d_tmem, dah + 2 * k, dbh + 2 * k, idesc2, first);
               umma_bf16_warp(d_tmem, dal + 2 * k, dbh + 2 * k, idesc, 1u);
+            } else {
+              umma_bf16_warp(d_tmem, dah + 2 * k, dbh + 2 * k, idesc, first);
+              if (X3) {
+                if (!res_step)  // identity has no lo plane
+                  umma_bf16_warp(d_tmem, dah + 2 * k, dbl + 2 * k, idesc, 1u);
+                umma_bf16_warp(d_tmem, dal + 2 * k, dbh + 2 * k, idesc, 1u);
+              }
             }
           }
           umma_commit_warp(empty0 + 8 * stage);
@@ -848,8 +868,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
       mbar_wait(tfull0 + 8 * acc, acc_phase);
       tc_fence_after();
       if (etid == 0) trace_put(p, unit, 4);
-      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * BN + col0;
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * Cfg::kAccCols + col0;
       const bool empty_k = x.s_end <= x.s_begin;  // no MMA wrote this accumulator
+      // stacked: the hi*lo half holds data only if a conv K-step initialised it
+      const bool upper = X3 && p.stacked != 0 && x.s_begin < p.ntaps * (p.C / 64);
       // rows this lane stores in the coalesced phase (lane/4 + 8i of the warp's 32)
       size_t st_ob[4];
       bool st_ok[4];
@@ -866,7 +888,19 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
         float v[2][16];
         tmem_ld16_nowait(t_row + c32 * 32, v[0]);
         tmem_ld16_nowait(t_row + c32 * 32 + 16, v[1]);
-        tmem_ld_wait();
+        if (upper) {
+          float w[2][16];
+          tmem_ld16_nowait(t_row + BN + c32 * 32, w[0]);
+          tmem_ld16_nowait(t_row + BN + c32 * 32 + 16, w[1]);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            v[0][i] += w[0][i];
+            v[1][i] += w[1][i];
+          }
+        } else {
+          tmem_ld_wait();
+        }
         const int cb = x.tn * BN + col0 + c32 * 32;  // first output channel of this step
         if (empty_k) {
 #pragma unroll

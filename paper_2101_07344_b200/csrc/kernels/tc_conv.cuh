@@ -45,6 +45,7 @@ struct TcConvParams {
   CUtensorMap tmAm[2];
   CUtensorMap tmRm[2];
   int multi_img;       // 1: tmAm (and tmRm when nres > 0) are valid
+  int stacked;         // bf16x3: hi*hi + hi*lo as one N = 2*BN MMA (see tc_conv.cu TcCfg)
   int nres;            // residual K-steps per tile (BN/64): out = conv + residual computed by the MMA
   // Halo mode (stride-1 k x k conv, one image per tile): 128 output anchors on
   // the padded row pitch Pw = W + k - 1 (tiles_h = tiles per image, hb = wb = 1,

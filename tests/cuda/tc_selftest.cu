@@ -197,6 +197,7 @@ static void conv_test(const char* name, int N, int H, int W, int C, int Cout, in
   p.ws = dWs;
   p.ws_counters = dCtr;
   p.segs = x3 ? 3 : 1;
+  p.stacked = (x3 && k > 1 && !getenv("LCB_NO_STACKED")) ? 1 : 0;
   p.Cout = Cout;
   p.ksplit = 1;
   p.surv = dSurv;
@@ -320,6 +321,7 @@ static void gemm_test(const char* name, int M, int K, int Cout, bool x3, int ksp
   p.C = K;
   p.ntaps = 1;
   p.segs = x3 ? 3 : 1;
+  p.stacked = 0;  // plain GEMM (1x1): three MMAs per K16 group
   p.Cout = Cout;
   p.ksplit = ksplit;
   p.count = dCnt;
@@ -484,6 +486,7 @@ static void perf_conv(const char* name, int N, int nsurv, int H, int W, int C, i
   p.C = C;
   p.ntaps = k * k;
   p.segs = x3 ? 3 : 1;
+  p.stacked = (x3 && k > 1 && !getenv("LCB_NO_STACKED")) ? 1 : 0;
   p.Cout = Cout;
   p.ksplit = 1;
   p.ks_max = ks_max;
