@@ -570,6 +570,7 @@ __global__ void __launch_bounds__(kLk) gap_rows_kernel(const __nv_bfloat16* hi, 
 
 // logits[k] = b[k] + W[k] . feat for k < classes: warp per class, lanes
 // strided over the features (4 independent chains), fixed combination order.
+template <bool kSmemW = false>
 __device__ void block_logits(const float* __restrict__ W, const float* __restrict__ b, int classes, int nf,
                              const float* feat, float* logits) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -579,15 +580,20 @@ __device__ void block_logits(const float* __restrict__ W, const float* __restric
     int o = lane;
 #pragma unroll 4
     for (; o + 96 < nf; o += 128) {
-      a0 += __ldg(wr + o) * feat[o];
-      a1 += __ldg(wr + o + 32) * feat[o + 32];
-      a2 += __ldg(wr + o + 64) * feat[o + 64];
-      a3 += __ldg(wr + o + 96) * feat[o + 96];
+      a0 += (kSmemW ? wr[o] : __ldg(wr + o)) * feat[o];
+      a1 += (kSmemW ? wr[o + 32] : __ldg(wr + o + 32)) * feat[o + 32];
+      a2 += (kSmemW ? wr[o + 64] : __ldg(wr + o + 64)) * feat[o + 64];
+      a3 += (kSmemW ? wr[o + 96] : __ldg(wr + o + 96)) * feat[o + 96];
     }
-    for (; o < nf; o += 32) a0 += __ldg(wr + o) * feat[o];
+    for (; o < nf; o += 32) a0 += (kSmemW ? wr[o] : __ldg(wr + o)) * feat[o];
     const float a = warp_sum((a0 + a1) + (a2 + a3));
     if (lane == 0) logits[k] = a + b[k];
   }
+}
+
+// Fused-GAP heads stage W2 + Ws1 in shared memory when they fit (48 KB).
+__host__ __device__ inline bool head_stages_weights(const CacheHeadParams& p) {
+  return p.gap != nullptr && p.classes * (p.feat + 16) <= 12288;
 }
 
 // Shared scratch of one row's head.
@@ -602,7 +608,9 @@ struct HeadSmem {
 // branch-stable sigmoid (losses.cpp:26-33), inclusive p >= delta
 // (cache.cpp:259-265), argmax(pr) with the lowest index on ties
 // (tensor.hpp:57-63). logits complete in shared memory; pr: shared [classes].
-__device__ void head_block(const CacheHeadParams& p, int r, const float* logits, float* pr, HeadSmem& hs) {
+// ws1: the selector's first layer [16][classes] (shared-memory copy or p.Ws1).
+__device__ void head_block(const CacheHeadParams& p, int r, const float* logits, float* pr, HeadSmem& hs,
+                           const float* ws1) {
   const int C = p.classes;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = kLk / 32;
   float m = -FLT_MAX;
@@ -637,17 +645,17 @@ __device__ void head_block(const CacheHeadParams& p, int r, const float* logits,
   __syncthreads();
   // selector hidden unit j on warp j % nw
   for (int j = warp; j < 16; j += nw) {
-    const float* wr = p.Ws1 + j * C;
+    const float* wr = ws1 + j * C;
     float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
     int k = lane;
 #pragma unroll 4
     for (; k + 96 < C; k += 128) {  // unrolled: 16 independent weight loads in flight per lane
-      a0 += __ldg(wr + k) * pr[k];
-      a1 += __ldg(wr + k + 32) * pr[k + 32];
-      a2 += __ldg(wr + k + 64) * pr[k + 64];
-      a3 += __ldg(wr + k + 96) * pr[k + 96];
+      a0 += wr[k] * pr[k];
+      a1 += wr[k + 32] * pr[k + 32];
+      a2 += wr[k + 64] * pr[k + 64];
+      a3 += wr[k + 96] * pr[k + 96];
     }
-    for (; k < C; k += 32) a0 += __ldg(wr + k) * pr[k];
+    for (; k < C; k += 32) a0 += wr[k] * pr[k];
     const float a = warp_sum((a0 + a1) + (a2 + a3)) + p.bs1[j];
     if (lane == 0) hs.hsel[j] = a > 0.0f ? a : 0.0f;
   }
@@ -747,18 +755,28 @@ __device__ void exit_tail(const ExitParams& e, int n, const float* prob, const i
 // the Conv(k,s) chunk partials, or the pooled bins / FC(h) hidden partials.
 // With p.ex.arrive the last CTA also runs the exit + compaction.
 __global__ void __launch_bounds__(kLk) cache_head_kernel(CacheHeadParams p) {
-  pdl_wait();
-  pdl_trigger();
   extern __shared__ float sm[];
   __shared__ HeadSmem hs;
   __shared__ float4 red4[kLk];
   const int r = blockIdx.x;
-  const int n = *p.count;
   const int C = p.classes;
+  float* logits = sm;    // [C]
+  float* feat = sm + C;  // [max(feat, C)]
+  const int tid = threadIdx.x;
+  // fused-GAP heads (<= 32 classes): the static head weights are staged in
+  // shared memory BEFORE the programmatic-launch wait, i.e. while the tap's
+  // conv is still draining (launch_cache_head sizes the region)
+  const bool stage_w = head_stages_weights(p);
+  float* w2s = feat + (p.feat > C ? p.feat : C);  // [C][feat]
+  float* ws1s = w2s + C * p.feat;                 // [16][C]
+  if (stage_w) {
+    for (int i = tid; i < C * p.feat; i += kLk) w2s[i] = __ldg(p.W2 + i);
+    for (int i = tid; i < 16 * C; i += kLk) ws1s[i] = __ldg(p.Ws1 + i);
+  }
+  pdl_wait();
+  pdl_trigger();
+  const int n = *p.count;
   if (r < n) {
-    float* logits = sm;    // [C]
-    float* feat = sm + C;  // [max(feat, C)]
-    const int tid = threadIdx.x;
     if (p.pre_logits) {
       for (int k = tid; k < C; k += kLk) logits[k] = fc_logit(p.pre_logits, p.pre_nz, p.pre_zstride, p.b2, r, C, k);
     } else if (p.family == 2) {
@@ -783,10 +801,13 @@ __global__ void __launch_bounds__(kLk) cache_head_kernel(CacheHeadParams p) {
         }
       }
       __syncthreads();
-      block_logits(p.W2, p.b2, C, p.feat, feat, logits);
+      if (stage_w)
+        block_logits<true>(w2s, p.b2, C, p.feat, feat, logits);
+      else
+        block_logits(p.W2, p.b2, C, p.feat, feat, logits);
     }
     __syncthreads();
-    head_block(p, r, logits, feat, hs);
+    head_block(p, r, logits, feat, hs, stage_w ? ws1s : p.Ws1);
   }
   if (p.ex.arrive) exit_tail(p.ex, n, p.prob, p.hit, p.label);
 }
@@ -1184,7 +1205,8 @@ void launch_cache_head(const CacheHeadParams& p_in, int max_rows, cudaStream_t s
     p.gap = nullptr;
   }
   const int feat_len = (p.family == 2 || p.pre_logits) ? p.classes : (p.feat > p.classes ? p.feat : p.classes);
-  const size_t smem = static_cast<size_t>(p.classes + feat_len) * sizeof(float);
+  size_t smem = static_cast<size_t>(p.classes + feat_len) * sizeof(float);
+  if (head_stages_weights(p)) smem += static_cast<size_t>(p.classes) * (p.feat + 16) * sizeof(float);  // W2 + Ws1
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(cache_head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
