@@ -506,3 +506,39 @@ def test_layer_times_hardware_profile():
     total = np.median([cdep.serve_timed(64, shadow=True) for _ in range(5)])
     assert 0.5 * total < bm.sum() + sum(lm.values()) < 1.5 * total, (bm.sum(), sum(lm.values()), total)
     cdep.close()
+
+
+@pytest.mark.parametrize("cfg", ["resnet18_cifar", "resnet50"])
+def test_full_size_invariants(cfg):
+    """BASELINE sizes (R18 b256, R50 b128, bench-calibrated selectors), through
+    size-independent properties: the compacted serve makes exactly the shadow
+    serve's decisions (exit layer, label, probabilities where probed), the
+    no-cache engine's base prediction equals the shadow pass's, serves are
+    bit-identical run to run, and the pipelined submit/collect path returns the
+    synchronous results."""
+    import torch
+    from bench import CONFIGS, build_deployment
+    B = CONFIGS[cfg][3]
+    m, vs, dep, base, gen, _ = build_deployment(cfg, B, "bf16x3", 0)
+    x = gen(B, 99).astype(np.float32)
+    sh = dep.serve(x, shadow=True)
+    cp = dep.serve(x)
+    assert np.array_equal(cp.exit_layer, sh.exit_layer) and np.array_equal(cp.served, sh.served)
+    probed = ~np.isnan(cp.probs)
+    # compaction changes the tile grouping / split-K factor of the deeper convs
+    # (fp32 summation order), so probabilities agree within the contract's
+    # close_rel(1e-3), not bit for bit (calibrated selector gains amplify it)
+    assert np.all(close_rel(cp.probs[probed], sh.probs[probed]))
+    miss = cp.exit_layer == 0
+    assert np.array_equal(cp.base_pred[miss], sh.base_pred[miss])
+    nc = base.serve(x)
+    assert np.array_equal(nc.base_pred, sh.base_pred) and np.all(nc.exit_layer == 0)
+    again = dep.serve(x)
+    assert np.array_equal(again.exit_layer, cp.exit_layer) and np.array_equal(again.probs, cp.probs, equal_nan=True)
+    pinned = torch.from_numpy(x).pin_memory()
+    t = dep.submit(pinned.numpy())
+    pr = dep.collect(t)
+    assert np.array_equal(pr.exit_layer, cp.exit_layer) and np.array_equal(pr.served, cp.served)
+    assert 0.5 < np.mean(cp.exit_layer > 0) <= 1.0  # calibrated selectors: most requests exit early
+    dep.close()
+    base.close()
