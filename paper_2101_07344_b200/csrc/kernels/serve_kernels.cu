@@ -168,7 +168,7 @@ __global__ void pool_channels_kernel(TapView t, int gch, int width, float inv, f
 // below keep many independent 16-byte loads in flight per thread (the
 // surviving-row counts are small, so latency, not bandwidth, is the enemy)
 // and combine partial sums in a fixed order (deterministic).
-constexpr int kLk = 256;
+constexpr int kLk = 512;
 
 __device__ __forceinline__ void add4(float4& a, const float4 b) {
   a.x += b.x;
