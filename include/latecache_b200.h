@@ -187,6 +187,62 @@ int lc_measure_metrics(lc_engine* e, const float* inputs, int B, const double* g
 int lc_tune_delta(lc_engine* e, const float* inputs, int B, double target_accuracy, const double* grid, int G,
                   double* deltas, int apply);
 
+/* Cache retraining on the GPU (reference cache.hpp:113-125):
+ * train_predictor (cache.cpp:179-208, distillation loss with tau/beta) and
+ * train_selector (cache.cpp:220-257, weighted selector loss with w_fp/w_fn),
+ * fp64 minibatch SGD with momentum on `device`. Records: taps [N][tap_dim] at
+ * the variant's layer (tap_of, cache.cpp:172-177), y [N][classes] base-model
+ * output distributions, weights [N] or NULL (= 1.0 each). TrainConfig fields
+ * (network.hpp:70-76) are passed as scalars. On success v holds the trained
+ * networks; LC_ERR_RUNTIME "... loss diverged" (the reference's runtime_error)
+ * leaves v unchanged; bad sizes are LC_ERR_INVALID_ARGUMENT. */
+int lc_train_predictor(int device, lc_variant* v, const double* taps, long long tap_dim, const double* y, int classes,
+                       int N, const double* weights, double learning_rate, double momentum, int epochs, int batch_size,
+                       uint64_t seed, double tau, double beta);
+int lc_train_selector(int device, lc_variant* v, const double* taps, long long tap_dim, const double* y, int classes,
+                      int N, const double* weights, double learning_rate, double momentum, int epochs, int batch_size,
+                      uint64_t seed, double w_fp, double w_fn);
+/* Swap a retrained variant into a running engine (run_adaptation's atomic
+ * swap, serving.cpp:301-315): uploads v's networks and threshold over the
+ * cache attached at v's layer, stream-ordered after every batch already
+ * enqueued. v must have the attached variant's architecture. */
+int lc_engine_update_variant(lc_engine* e, const lc_variant* v);
+
+/* Online adaptation: run_adaptation (serving.cpp:213-340)
+ * over a running engine. AdaptationConfig (serving.hpp:85-94) plus the
+ * CacheTrainConfig fields the retrain uses (tau, beta, w_fp, w_fn). */
+typedef struct lc_adapt_config {
+  double sample_rate, window_min, retrain_interval_min, recency_decay, mixin_fraction;
+  int epochs;
+  double learning_rate, retrain_pause_ms;
+  double tau, beta, w_fp, w_fn;
+} lc_adapt_config;
+/* RetrainEvent (serving.hpp:96-103). */
+typedef struct lc_retrain_event {
+  int interval;
+  double time_min;
+  long long window_size, mixin_size;
+  int applied;
+  char note[160];
+} lc_retrain_event;
+/* Request i (time-ordered) serves samples[req_sample[i]] (inputs [n_samples][input_dim]). Serving runs in shadow batches of up to max_batch
+ * requests between swap/retrain points; sampled requests' taps at the attached
+ * caches' layers and base distributions come back from the device as the
+ * window records. original_taps[k] = [N0][tap_dim of attached cache k] (attach
+ * order), original_y [N0][classes]: the original training records (mix-in).
+ * Retrains run on the GPU (lc_train_predictor/selector) and swap in with
+ * lc_engine_update_variant. Outputs per request: hit_layer (0 = miss), served,
+ * base_pred, latency_ms (device time within its batch); events[<= events_cap],
+ * *n_events = total retrain events. The engine ends holding the final
+ * variants (lc_engine_variant). MLP base family only (the reference's). */
+int lc_run_adaptation(lc_engine* e, const float* inputs, int n_samples, const double* req_time,
+                      const int* req_sample, int R, const lc_adapt_config* cfg, const double* const* original_taps,
+                      const double* original_y, int N0, uint64_t seed, int adapt_on, int* hit_layer, int* served,
+                      int* base_pred, double* latency_ms, lc_retrain_event* events, int events_cap, int* n_events);
+/* Copy of the engine's k-th attached variant (attach order), e.g. the final
+ * variants after lc_run_adaptation. */
+int lc_engine_variant(lc_engine* e, int k, lc_variant** out);
+
 /* Hardware-aware costs (replaces CostModel::lookup_ms, cache.hpp:46-55, and the
  * modeled LayerProfile, composer.hpp): one shadow batch of the B host requests
  * through the graph with device timestamps at every block boundary.

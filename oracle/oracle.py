@@ -67,6 +67,9 @@ def ref() -> C.CDLL:
             "ref_gen_workload": (I, [C.c_char_p, I, D, D, D, D, U64, C.POINTER(LL), C.POINTER(LL), pI, LL]),
             "ref_rng_stream": (I, [U64, I, I, pD, C.POINTER(U64)]),
             "ref_mix_seed": (U64, [U64, U64]),
+            "ref_train": (P, [P, I, pD, I, pD, I, I, pD, D, D, I, I, U64, D, D]),
+            "ref_run_adaptation": (I, [P, C.POINTER(P), I, pD, pI, I, pD, pI, I, pD, pD, pD, I, U64, I, pI, pI, pI,
+                                       pI, pD, I, C.POINTER(P)]),
         }
         for k, (r, a) in sig.items():
             f = getattr(lib, k)
@@ -249,6 +252,45 @@ def ref_tune_delta(model: RefModel, variant: RefVariant, inputs: np.ndarray, tar
 
 
 # ------------------------------------------------------------------ text format -> numpy
+def ref_train(variant: "RefVariant", which: str, taps: np.ndarray, y: np.ndarray, weights=None, lr=0.01,
+              momentum=0.9, epochs=20, batch=16, seed=1, a=2.0, b=0.5) -> "RefVariant":
+    """The reference's train_predictor (which="predictor", a=tau, b=beta) or
+    train_selector (which="selector", a=w_fp, b=w_fn) (cache.cpp:179-257) on a
+    copy of the variant; returns the trained copy."""
+    t = np.ascontiguousarray(taps, np.float64)
+    yy = np.ascontiguousarray(y, np.float64)
+    w = None if weights is None else np.ascontiguousarray(weights, np.float64)
+    h = ref().ref_train(variant.h, 0 if which == "predictor" else 1, _dp(t), t.shape[1], _dp(yy), yy.shape[1],
+                        t.shape[0], None if w is None else _dp(w), lr, momentum, epochs, batch, seed, a, b)
+    if not h:
+        raise RuntimeError(ref().ref_last_error().decode())
+    return RefVariant(h)
+
+
+def ref_run_adaptation(model: "RefModel", variants, inputs: np.ndarray, labels: np.ndarray, times: np.ndarray,
+                       sample_idx: np.ndarray, cfg8, train4, orig_inputs: np.ndarray, seed: int, adapt_on: bool):
+    """The reference's run_adaptation (serving.cpp:213-340) over a pass-through
+    deployment: (hit_layer, served, base, events [n][5], final RefVariants)."""
+    x = np.ascontiguousarray(inputs, np.float64)
+    lab = np.ascontiguousarray(labels, np.int32)
+    t = np.ascontiguousarray(times, np.float64)
+    si = np.ascontiguousarray(sample_idx, np.int32)
+    c8 = np.ascontiguousarray(cfg8, np.float64)
+    t4 = np.ascontiguousarray(train4, np.float64)
+    oi = np.ascontiguousarray(orig_inputs, np.float64)
+    R = t.shape[0]
+    hl, sv, bp = np.zeros(R, np.int32), np.zeros(R, np.int32), np.zeros(R, np.int32)
+    cap = 4096
+    ev = np.zeros((cap, 5), np.float64)
+    n = C.c_int()
+    arr = (C.c_void_p * len(variants))(*[v.h for v in variants])
+    out = (C.c_void_p * len(variants))()
+    _check(ref().ref_run_adaptation(model.h, arr, len(variants), _dp(x), _ip(lab), x.shape[0], _dp(t), _ip(si), R,
+                                    _dp(c8), _dp(t4), _dp(oi), oi.shape[0], seed, 1 if adapt_on else 0, _ip(hl),
+                                    _ip(sv), _ip(bp), C.byref(n), _dp(ev), cap, out))
+    return hl, sv, bp, ev[:min(n.value, cap)], [RefVariant(out[k]) for k in range(len(variants))]
+
+
 def parse_network(text: str, pos: int = 0):
     """latecache-network v1 (network.cpp:330-409) -> (layers, end_pos)."""
     toks = text[pos:].split()

@@ -334,6 +334,111 @@ int ref_tune_delta(void* mp, void* vp, const double* inputs, int B, double targe
   });
 }
 
+// ------------------------------------------------------------------ retraining
+// train_predictor / train_selector (cache.cpp:179-257) on a COPY of the
+// variant, records built from taps at the variant's layer ([N][D]) and the
+// base distributions y ([N][C]); weights may be null (1.0 each). The trained
+// copy is returned as a new handle.
+std::vector<TapRecord> records_at(const CacheVariant& v, const double* taps, int D, const double* y, int C, int N) {
+  std::vector<TapRecord> recs(static_cast<std::size_t>(N));
+  for (int n = 0; n < N; ++n) {
+    TapRecord& r = recs[static_cast<std::size_t>(n)];
+    r.taps.resize(static_cast<std::size_t>(v.layer));
+    r.taps.back() = vec_of(taps + static_cast<std::size_t>(n) * D, D);
+    r.y = vec_of(y + static_cast<std::size_t>(n) * C, C);
+  }
+  return recs;
+}
+
+void* ref_train(void* vp, int which, const double* taps, int D, const double* y, int C, int N, const double* weights,
+                double lr, double momentum, int epochs, int batch, uint64_t seed, double a, double b) {
+  void* out = nullptr;
+  const int st = guard([&] {
+    auto v = std::make_unique<CacheVariant>(*static_cast<CacheVariant*>(vp));
+    const std::vector<TapRecord> recs = records_at(*v, taps, D, y, C, N);
+    TrainConfig cfg;
+    cfg.learning_rate = lr;
+    cfg.momentum = momentum;
+    cfg.epochs = epochs;
+    cfg.batch_size = batch;
+    cfg.seed = seed;
+    const std::vector<double> w = weights ? std::vector<double>(weights, weights + N) : std::vector<double>();
+    if (which == 0)
+      train_predictor(*v, recs, cfg, a, b, w);
+    else
+      train_selector(*v, recs, cfg, a, b, w);
+    out = v.release();
+  });
+  return st == 0 ? out : nullptr;
+}
+
+// run_adaptation (serving.cpp:213-340) over a pass-through deployment of the
+// given variants; original_train = collect_taps of orig_inputs. cfg8 =
+// {sample_rate, window_min, retrain_interval_min, recency_decay,
+// mixin_fraction, epochs, learning_rate, retrain_pause_ms}; train4 = {tau,
+// beta, w_fp, w_fn}. ev [cap][5] = {interval, time_min, window_size,
+// mixin_size, applied}; final_vars receives nv new variant handles.
+int ref_run_adaptation(void* mp, void** vars, int nv, const double* inputs, const int* labels, int n_samples,
+                       const double* times, const int* sample_idx, int R, const double* cfg8, const double* train4,
+                       const double* orig_inputs, int N0, uint64_t seed, int adapt_on, int* hit_layer, int* served,
+                       int* base, int* ev_n, double* ev, int ev_cap, void** final_vars) {
+  return guard([&] {
+    const BaseModel& m = *static_cast<BaseModel*>(mp);
+    PassThroughDeployment pd;
+    make_passthrough(pd, m, vars, nv);
+    Dataset data;
+    data.num_classes = m.num_classes;
+    data.input_dim = m.input_dim();
+    for (int i = 0; i < n_samples; ++i) {
+      Sample smp;
+      smp.x = vec_of(inputs + static_cast<std::size_t>(i) * m.input_dim(), m.input_dim());
+      smp.label = labels[i];
+      data.test.push_back(smp);
+    }
+    std::vector<Request> stream(static_cast<std::size_t>(R));
+    for (int i = 0; i < R; ++i) {
+      stream[static_cast<std::size_t>(i)].id = i;
+      stream[static_cast<std::size_t>(i)].time_min = times[i];
+      stream[static_cast<std::size_t>(i)].sample_idx = static_cast<std::size_t>(sample_idx[i]);
+      stream[static_cast<std::size_t>(i)].true_class = labels[sample_idx[i]];
+    }
+    AdaptationConfig cfg;
+    cfg.sample_rate = cfg8[0];
+    cfg.window_min = cfg8[1];
+    cfg.retrain_interval_min = cfg8[2];
+    cfg.recency_decay = cfg8[3];
+    cfg.mixin_fraction = cfg8[4];
+    cfg.epochs = static_cast<int>(cfg8[5]);
+    cfg.learning_rate = cfg8[6];
+    cfg.retrain_pause_ms = cfg8[7];
+    CacheTrainConfig tc;
+    tc.tau = train4[0];
+    tc.beta = train4[1];
+    tc.w_fp = train4[2];
+    tc.w_fn = train4[3];
+    std::vector<Sample> orig(static_cast<std::size_t>(N0));
+    for (int i = 0; i < N0; ++i) orig[static_cast<std::size_t>(i)].x = vec_of(orig_inputs + static_cast<std::size_t>(i) * m.input_dim(), m.input_dim());
+    const std::vector<TapRecord> original = collect_taps(m, orig);
+    const AdaptationResult res = run_adaptation(pd.dep, data, stream, cfg, tc, original, seed, adapt_on != 0);
+    for (int i = 0; i < R; ++i) {
+      hit_layer[i] = res.traces[static_cast<std::size_t>(i)].hit_layer;
+      served[i] = res.traces[static_cast<std::size_t>(i)].served_pred;
+      base[i] = res.traces[static_cast<std::size_t>(i)].base_pred;
+    }
+    *ev_n = static_cast<int>(res.retrains.size());
+    for (int i = 0; i < std::min(ev_cap, *ev_n); ++i) {
+      const RetrainEvent& e = res.retrains[static_cast<std::size_t>(i)];
+      double* o = ev + static_cast<std::size_t>(i) * 5;
+      o[0] = e.interval;
+      o[1] = e.time_min;
+      o[2] = static_cast<double>(e.window_size);
+      o[3] = static_cast<double>(e.mixin_size);
+      o[4] = e.applied ? 1.0 : 0.0;
+    }
+    for (int k = 0; k < nv; ++k) final_vars[k] = new CacheVariant(res.final_variants[static_cast<std::size_t>(k)]);
+  });
+}
+
 // ------------------------------------------------------------------ pipeline
 // Trained deployment in the style of test_acceptance.cpp:69-137: dataset ->
 // train_base -> collect_taps -> explore_variants -> compose_relaxed ->

@@ -41,6 +41,22 @@ class CnnOpDesc(C.Structure):
     ]
 
 
+class AdaptConfig(C.Structure):  # lc_adapt_config
+    _fields_ = [
+        ("sample_rate", C.c_double), ("window_min", C.c_double), ("retrain_interval_min", C.c_double),
+        ("recency_decay", C.c_double), ("mixin_fraction", C.c_double), ("epochs", C.c_int),
+        ("learning_rate", C.c_double), ("retrain_pause_ms", C.c_double), ("tau", C.c_double),
+        ("beta", C.c_double), ("w_fp", C.c_double), ("w_fn", C.c_double),
+    ]
+
+
+class RetrainEventC(C.Structure):  # lc_retrain_event
+    _fields_ = [
+        ("interval", C.c_int), ("time_min", C.c_double), ("window_size", C.c_longlong),
+        ("mixin_size", C.c_longlong), ("applied", C.c_int), ("note", C.c_char * 160),
+    ]
+
+
 def _load() -> C.CDLL:
     if not os.path.exists(LIB_PATH):
         raise ImportError(
@@ -96,6 +112,12 @@ def _load() -> C.CDLL:
         "lc_variant_load_binary": (I, [C.c_char_p, C.c_size_t, C.POINTER(C.c_void_p)]),
         "lc_serve_collect": (I, [P, I, I, pI, pI, pI, pF, pD]),
         "lc_tune_delta": (I, [P, pF, I, C.c_double, pD, I, pD, I]),
+        "lc_train_predictor": (I, [I, P, pD, C.c_longlong, pD, I, I, pD, D, D, I, I, C.c_uint64, D, D]),
+        "lc_train_selector": (I, [I, P, pD, C.c_longlong, pD, I, I, pD, D, D, I, I, C.c_uint64, D, D]),
+        "lc_engine_update_variant": (I, [P, P]),
+        "lc_run_adaptation": (I, [P, pF, I, pD, pI, I, C.POINTER(AdaptConfig), C.POINTER(pD), pD, I, C.c_uint64, I,
+                                  pI, pI, pI, pD, C.POINTER(RetrainEventC), I, pI]),
+        "lc_engine_variant": (I, [P, I, C.POINTER(P)]),
         "lc_engine_time": (I, [P, I, C.c_uint, I, pD]),
         "lc_engine_kernel_count": (I, [P, C.c_uint, I]),
         "lc_engine_profile": (I, [P, I, C.c_uint, I, pI, pI, pD, pD, pD]),
@@ -148,6 +170,7 @@ EXPORTED_SYMBOLS = [
     "lc_engine_set_delta", "lc_engine_set_selector_out", "lc_engine_input", "lc_serve_batch", "lc_serve_device",
     "lc_engine_sync", "lc_engine_results", "lc_engine_counts", "lc_lookup_batch", "lc_engine_time",
     "lc_engine_kernel_count", "lc_engine_profile", "lc_serve_timed", "lc_engine_stage_input",
-    "lc_measure_metrics", "lc_tune_delta", "lc_serve_submit", "lc_serve_collect", "lc_engine_layer_times",
+    "lc_measure_metrics", "lc_tune_delta", "lc_train_predictor", "lc_train_selector", "lc_engine_update_variant",
+    "lc_run_adaptation", "lc_engine_variant", "lc_serve_submit", "lc_serve_collect", "lc_engine_layer_times",
     "lc_model_save_binary", "lc_model_load_binary", "lc_variant_save_binary", "lc_variant_load_binary",
 ]

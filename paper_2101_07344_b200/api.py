@@ -24,7 +24,7 @@ from typing import Dict, List, Optional, Sequence
 
 import numpy as np
 
-from ._lib import (LC_PREC_BF16, LC_PREC_BF16X3, LC_SERVE_NO_GRAPH, LC_SERVE_SHADOW, CnnOpDesc, check, lib,
+from ._lib import (AdaptConfig, RetrainEventC, LC_PREC_BF16, LC_PREC_BF16X3, LC_SERVE_NO_GRAPH, LC_SERVE_SHADOW, CnnOpDesc, check, lib,
                    take_bytes, take_string)
 
 _PREC = {"bf16x3": LC_PREC_BF16X3, "bf16": LC_PREC_BF16}
@@ -341,6 +341,17 @@ class Deployment:
     def set_selector_out(self, layer: int, gain: float, bias: float) -> None:
         check(lib.lc_engine_set_selector_out(self._h, layer, float(gain), float(bias)))
 
+    def update_variant(self, variant: CacheVariant) -> None:
+        """Swap a retrained variant in for the cache at its layer (after every
+        batch already enqueued; serving.cpp:301-315)."""
+        check(lib.lc_engine_update_variant(self._h, variant._h))
+
+    def variant(self, k: int) -> CacheVariant:
+        """Copy of the k-th attached variant (attach order) as the engine holds it."""
+        h = C.c_void_p()
+        check(lib.lc_engine_variant(self._h, k, C.byref(h)))
+        return CacheVariant(h)
+
     def input_ptr(self) -> int:
         p = C.c_void_p()
         check(lib.lc_engine_input(self._h, C.byref(p)))
@@ -562,3 +573,132 @@ def summarize(traces: Sequence[RequestTrace]) -> SimSummary:
         agreement=(sum(t.served_pred == t.base_pred for t in known) / len(known)) if known else float("nan"),
         accuracy=sum(t.served_pred == t.true_class for t in traces) / n,
         hit_rate=sum(t.hit_layer > 0 for t in traces) / n, hits_by_layer=hits)
+
+
+# ---------------------------------------------------------------- retraining / adaptation
+@dataclass
+class TrainConfig:
+    """latecache::TrainConfig (network.hpp:70-76)."""
+    learning_rate: float = 0.01
+    momentum: float = 0.9
+    epochs: int = 20
+    batch_size: int = 16
+    seed: int = 1
+
+
+def _records(taps: np.ndarray, y: np.ndarray, sample_weights):
+    t = np.ascontiguousarray(taps, np.float64)
+    yy = np.ascontiguousarray(y, np.float64)
+    if t.ndim != 2 or yy.ndim != 2 or t.shape[0] != yy.shape[0]:
+        raise ValueError("records: taps [N][D] and y [N][C] must have the same N")
+    w = None if sample_weights is None else np.ascontiguousarray(sample_weights, np.float64)
+    if w is not None and w.shape != (t.shape[0],):  # the C-ABI reads exactly N weights
+        raise ValueError("train: sample weight count mismatch")
+    return t, yy, w
+
+
+def train_predictor(variant: CacheVariant, taps: np.ndarray, y: np.ndarray, cfg: TrainConfig = TrainConfig(),
+                    tau: float = 2.0, beta: float = 0.5, sample_weights=None, device: int = 0) -> None:
+    """train_predictor (cache.cpp:179-208) on the GPU, in place: taps [N][D] at
+    the variant's layer, y [N][C] base-model distributions."""
+    t, yy, w = _records(taps, y, sample_weights)
+    check(lib.lc_train_predictor(device, variant._h, _dptr(t), t.shape[1], _dptr(yy), yy.shape[1], t.shape[0],
+                                 None if w is None else _dptr(w), cfg.learning_rate, cfg.momentum, cfg.epochs,
+                                 cfg.batch_size, C.c_uint64(cfg.seed), tau, beta))
+
+
+def train_selector(variant: CacheVariant, taps: np.ndarray, y: np.ndarray, cfg: TrainConfig = TrainConfig(),
+                   w_fp: float = 5.0, w_fn: float = 1.0, sample_weights=None, device: int = 0) -> None:
+    """train_selector (cache.cpp:220-257) on the GPU, in place."""
+    t, yy, w = _records(taps, y, sample_weights)
+    check(lib.lc_train_selector(device, variant._h, _dptr(t), t.shape[1], _dptr(yy), yy.shape[1], t.shape[0],
+                                None if w is None else _dptr(w), cfg.learning_rate, cfg.momentum, cfg.epochs,
+                                cfg.batch_size, C.c_uint64(cfg.seed), w_fp, w_fn))
+
+
+@dataclass
+class AdaptationConfig:
+    """AdaptationConfig (serving.hpp:85-94) plus the CacheTrainConfig fields the
+    retrain uses (cache.hpp:92-100)."""
+    sample_rate: float = 0.2
+    window_min: float = 60.0
+    retrain_interval_min: float = 15.0
+    recency_decay: float = 0.7
+    mixin_fraction: float = 0.5
+    epochs: int = 5
+    learning_rate: float = 0.002
+    retrain_pause_ms: float = 0.0
+    tau: float = 2.0
+    beta: float = 0.5
+    w_fp: float = 5.0
+    w_fn: float = 1.0
+
+
+@dataclass
+class RetrainEvent:
+    interval: int
+    time_min: float
+    window_size: int
+    mixin_size: int
+    applied: bool
+    note: str
+
+
+@dataclass
+class IntervalStat:
+    interval: int
+    requests: int = 0
+    hits: int = 0
+
+    def hit_rate(self) -> float:
+        return 0.0 if self.requests == 0 else self.hits / self.requests
+
+
+@dataclass
+class AdaptationResult:
+    traces: List[RequestTrace]
+    timeline: List[IntervalStat]
+    retrains: List[RetrainEvent]
+    final_variants: List[CacheVariant]
+
+
+def run_adaptation(dep: Deployment, inputs: np.ndarray, labels: Sequence[int], stream: Sequence[Request],
+                   cfg: AdaptationConfig, original_taps: Sequence[np.ndarray], original_y: np.ndarray, seed: int,
+                   adapt_on: bool = True) -> AdaptationResult:
+    """run_adaptation (serving.cpp:213-340) on the GPU: shadow-batched serving
+    between control points, window records read back from the device, GPU
+    retraining and in-place swaps. original_taps[k] = [N0][D_k] for the k-th
+    attached cache, original_y [N0][C]. The engine ends holding the final
+    variants (also returned)."""
+    x = np.ascontiguousarray(inputs, np.float32)
+    R = len(stream)
+    times = np.ascontiguousarray([r.time_min for r in stream], np.float64)
+    samp = np.ascontiguousarray([r.sample_idx for r in stream], np.int32)
+    oy = np.ascontiguousarray(original_y, np.float64)
+    N0 = oy.shape[0] if oy.ndim == 2 else 0
+    ot = [np.ascontiguousarray(t, np.float64) for t in original_taps]
+    tp = (C.POINTER(C.c_double) * max(1, len(ot)))(*[_dptr(t) for t in ot])
+    c = AdaptConfig(cfg.sample_rate, cfg.window_min, cfg.retrain_interval_min, cfg.recency_decay,
+                    cfg.mixin_fraction, cfg.epochs, cfg.learning_rate, cfg.retrain_pause_ms, cfg.tau, cfg.beta,
+                    cfg.w_fp, cfg.w_fn)
+    hl, sv, bp = np.zeros(R, np.int32), np.zeros(R, np.int32), np.zeros(R, np.int32)
+    lat = np.zeros(R, np.float64)
+    cap = 4096
+    evs = (RetrainEventC * cap)()
+    n = C.c_int()
+    check(lib.lc_run_adaptation(dep._h, _fptr(x), x.shape[0], _dptr(times), _iptr(samp), R, C.byref(c), tp,
+                                _dptr(oy) if N0 else None, N0, C.c_uint64(seed), 1 if adapt_on else 0, _iptr(hl),
+                                _iptr(sv), _iptr(bp), _dptr(lat), evs, cap, C.byref(n)))
+    traces = [RequestTrace(r.id, r.time_min, int(labels[r.sample_idx]), int(bp[i]), int(sv[i]), int(hl[i]),
+                           float(lat[i])) for i, r in enumerate(stream)]
+    timeline: List[IntervalStat] = []
+    for t in traces:  # serving.cpp:321-327
+        iv = int(t.time_min / cfg.retrain_interval_min)
+        if not timeline or timeline[-1].interval < iv:
+            timeline.append(IntervalStat(iv))
+        timeline[-1].requests += 1
+        timeline[-1].hits += 1 if t.hit_layer > 0 else 0
+    retrains = [RetrainEvent(e.interval, e.time_min, e.window_size, e.mixin_size, bool(e.applied),
+                             e.note.decode()) for e in evs[:min(n.value, cap)]]
+    finals = [dep.variant(k) for k in range(len(dep.variants))]
+    return AdaptationResult(traces, timeline, retrains, finals)

@@ -13,6 +13,8 @@
 
 #include "../../include/latecache_b200.h"
 #include "engine.hpp"
+#include "trainer.hpp"
+#include "adapt.hpp"
 #include "host/lcb_host.hpp"
 
 struct lc_model {
@@ -487,6 +489,114 @@ int lc_measure_metrics(lc_engine* e, const float* inputs, int B, const double* g
         cudaMemcpyAsync(en.input_buffer(), inputs, bytes, cudaMemcpyHostToDevice, en.stream()) != cudaSuccess)
       throw lcb::CudaFailure("measure_metrics: input copy failed");
     en.measure(B, grid, G, counts);
+  });
+}
+
+// ------------------------------------------------------------------ retraining
+namespace {
+int train_common(int which, int device, lc_variant* v, const double* taps, long long tap_dim, const double* y,
+                 int classes, int N, const double* weights, double lr, double momentum, int epochs, int batch_size,
+                 uint64_t seed, double a, double b) {
+  return guard([&] {
+    need(v, "variant");
+    need(taps, "taps");
+    need(y, "y");
+    lcb::TrainRecords r;
+    r.taps = taps;
+    r.D = tap_dim;
+    r.y = y;
+    r.C = classes;
+    r.N = N;
+    if (weights && N > 0) r.weights.assign(weights, weights + N);
+    lcb::SgdConfig cfg;
+    cfg.learning_rate = lr;
+    cfg.momentum = momentum;
+    cfg.epochs = epochs;
+    cfg.batch_size = batch_size;
+    cfg.seed = seed;
+    lcb::CacheVariant trained = v->v;  // unchanged on failure
+    if (which == 0)
+      lcb::gpu_train_predictor(device, trained, r, cfg, a, b);
+    else
+      lcb::gpu_train_selector(device, trained, r, cfg, a, b);
+    v->v = std::move(trained);
+  });
+}
+}  // namespace
+
+int lc_train_predictor(int device, lc_variant* v, const double* taps, long long tap_dim, const double* y, int classes,
+                       int N, const double* weights, double learning_rate, double momentum, int epochs, int batch_size,
+                       uint64_t seed, double tau, double beta) {
+  return train_common(0, device, v, taps, tap_dim, y, classes, N, weights, learning_rate, momentum, epochs, batch_size,
+                      seed, tau, beta);
+}
+
+int lc_train_selector(int device, lc_variant* v, const double* taps, long long tap_dim, const double* y, int classes,
+                      int N, const double* weights, double learning_rate, double momentum, int epochs, int batch_size,
+                      uint64_t seed, double w_fp, double w_fn) {
+  return train_common(1, device, v, taps, tap_dim, y, classes, N, weights, learning_rate, momentum, epochs, batch_size,
+                      seed, w_fp, w_fn);
+}
+
+int lc_engine_update_variant(lc_engine* e, const lc_variant* v) {
+  return guard([&] {
+    need(v, "variant");
+    eng(e).update_variant(v->v);
+  });
+}
+
+
+int lc_run_adaptation(lc_engine* e, const float* inputs, int n_samples, const double* req_time, const int* req_sample,
+                      int R, const lc_adapt_config* cfg, const double* const* original_taps, const double* original_y,
+                      int N0, uint64_t seed, int adapt_on, int* hit_layer, int* served, int* base_pred,
+                      double* latency_ms, lc_retrain_event* events, int events_cap, int* n_events) {
+  return guard([&] {
+    need(cfg, "config");
+    need(n_events, "n_events");
+    lcb::Engine& en = eng(e);
+    if (R < 0 || N0 < 0 || n_samples < 0) throw std::invalid_argument("run_adaptation: negative count");
+    if (R > 0) {
+      need(inputs, "inputs");
+      need(req_time, "req_time");
+      need(req_sample, "req_sample");
+      need(hit_layer, "hit_layer");
+      need(served, "served");
+      need(base_pred, "base_pred");
+      need(latency_ms, "latency_ms");
+    }
+    const auto& vars = en.variants();
+    std::vector<lcb::AdaptRecord> orig(static_cast<size_t>(N0));
+    if (N0 > 0) {
+      need(original_taps, "original_taps");
+      need(original_y, "original_y");
+    }
+    const int C = en.classes();
+    for (int n = 0; n < N0; ++n) {
+      lcb::AdaptRecord& r = orig[static_cast<size_t>(n)];
+      for (size_t k = 0; k < vars.size(); ++k) {
+        const long long D = en.model().tap_dim(vars[k].layer);
+        need(original_taps[k], "original_taps[k]");
+        const double* src = original_taps[k] + static_cast<size_t>(n) * static_cast<size_t>(D);
+        r.taps.emplace_back(src, src + D);
+      }
+      r.y.assign(original_y + static_cast<size_t>(n) * C, original_y + static_cast<size_t>(n + 1) * C);
+    }
+    lcb::AdaptOut out{hit_layer, served, base_pred, latency_ms, {}};
+    lcb::run_adaptation(en, inputs, n_samples, req_time, req_sample, R, *cfg, orig, seed, adapt_on != 0, out);
+    *n_events = static_cast<int>(out.events.size());
+    for (int i = 0; i < std::min(events_cap, *n_events); ++i) {
+      need(events, "events");
+      events[i] = out.events[static_cast<size_t>(i)];
+    }
+  });
+}
+
+int lc_engine_variant(lc_engine* e, int k, lc_variant** out) {
+  return guard([&] {
+    need(out, "out");
+    const auto& vars = eng(e).variants();
+    if (k < 0 || k >= static_cast<int>(vars.size())) throw std::invalid_argument("engine_variant: index out of range");
+    *out = new lc_variant{vars[static_cast<size_t>(k)]};
   });
 }
 

@@ -1,5 +1,6 @@
 // Device engine implementation (see engine.hpp).
 #include "engine.hpp"
+#include "kernels/train_kernels.cuh"
 
 #include <algorithm>
 #include <cmath>
@@ -144,6 +145,20 @@ float* Engine::upload_f32(const std::vector<float>& v) {
   float* p = static_cast<float*>(dalloc(v.size() * sizeof(float)));
   ck(cudaMemcpy(p, v.data(), v.size() * sizeof(float), cudaMemcpyHostToDevice), "upload");
   return p;
+}
+
+// FC(h) cache first layer in the tap's storage order: [hp][Dk] fp32, the
+// reference's NCHW-flat feature f at NHWC offset (f % HW) * C + f / HW.
+static std::vector<float> fc_w1_layout(const std::vector<double>& w1, const DevCache& c, const TapInfo& ti, bool mlp) {
+  std::vector<float> w(static_cast<size_t>(c.hp) * c.Dk, 0.0f);
+  const int HW = ti.H * ti.W, Ct = ti.C;
+  for (int j = 0; j < c.h; ++j)
+    for (long long f = 0; f < c.D; ++f) {
+      const long long off = mlp ? f : (f % HW) * Ct + f / HW;
+      w[static_cast<size_t>(j) * c.Dk + static_cast<size_t>(off)] =
+          static_cast<float>(w1[static_cast<size_t>(j) * c.D + static_cast<size_t>(f)]);
+    }
+  return w;
 }
 
 // ------------------------------------------------------------------ build
@@ -406,15 +421,7 @@ void Engine::build_weights() {
       c->h = P[0].out_dim;
       c->hp = round_up(c->h, 64);
       c->Dk = static_cast<int>(round_up(row_stride, 64));
-      std::vector<float> w(static_cast<size_t>(c->hp) * c->Dk, 0.0f);
-      const int HW = ti.H * ti.W, Ct = ti.C;
-      for (int j = 0; j < c->h; ++j)
-        for (long long f = 0; f < c->D; ++f) {
-          const long long off = mlp ? f : (f % HW) * Ct + f / HW;  // NCHW-flat -> storage order
-          w[static_cast<size_t>(j) * c->Dk + static_cast<size_t>(off)] =
-              static_cast<float>(PW[0].w[static_cast<size_t>(j) * c->D + static_cast<size_t>(f)]);
-        }
-      c->W1 = upload_planes(w);
+      c->W1 = upload_planes(fc_w1_layout(PW[0].w, *c, ti, mlp));
       c->b1 = upload_f32(to_f32(PW[0].b));
       c->W2 = upload_f32(to_f32(PW[2].w));
       c->b2 = upload_f32(to_f32(PW[2].b));
@@ -1163,6 +1170,104 @@ void Engine::set_delta(int layer, double delta) {
       cudaGraphExecDestroy(g);
       g = nullptr;
     }
+}
+
+namespace {
+bool same_shape(const Network& a, const Network& b) {
+  if (a.layers.size() != b.layers.size()) return false;
+  for (size_t i = 0; i < a.layers.size(); ++i) {
+    const LayerSpec &x = a.layers[i], &y = b.layers[i];
+    if (x.kind != y.kind || x.in_dim != y.in_dim || x.out_dim != y.out_dim || x.pool_window != y.pool_window ||
+        x.kernel != y.kernel || x.stride != y.stride)
+      return false;
+  }
+  return true;
+}
+void put_f32(float* dst, const std::vector<double>& v) {
+  const std::vector<float> f = to_f32(v);
+  ck(cudaMemcpy(dst, f.data(), f.size() * sizeof(float), cudaMemcpyHostToDevice), "variant upload");
+}
+}  // namespace
+
+void Engine::update_variant(const CacheVariant& nv) {
+  require(nv.layer >= 1 && nv.layer <= model_.num_blocks, "update_variant: layer out of range");
+  const int ci = cache_of_layer_[static_cast<size_t>(nv.layer)];
+  require(ci >= 0, "update_variant: no cache attached at layer " + std::to_string(nv.layer));
+  CacheVariant& cur = variants_[static_cast<size_t>(ci)];
+  require(same_shape(cur.predictor, nv.predictor) && same_shape(cur.selector, nv.selector),
+          "update_variant: architecture differs from the attached variant");
+  // Swap between batches: everything already enqueued finishes with the old networks.
+  ck(cudaStreamSynchronize(stream_), "update_variant: sync");
+  DevCache& c = *caches_[static_cast<size_t>(ci)];
+  const auto& PW = nv.predictor.weights;
+  if (c.family == 0) {
+    const TapInfo ti = model_.taps[static_cast<size_t>(nv.layer - 1)];
+    const std::vector<float> w = fc_w1_layout(PW[0].w, c, ti, model_.family == "mlp");
+    std::vector<__nv_bfloat16> hi, lo;
+    split_planes(w, hi, lo);
+    ck(cudaMemcpy(c.W1.hi, hi.data(), w.size() * 2, cudaMemcpyHostToDevice), "variant upload");
+    if (c.W1.lo) ck(cudaMemcpy(c.W1.lo, lo.data(), w.size() * 2, cudaMemcpyHostToDevice), "variant upload");
+    put_f32(c.b1, PW[0].b);
+    put_f32(c.W2, PW[2].w);
+    put_f32(c.b2, PW[2].b);
+  } else if (c.family == 1) {
+    put_f32(c.W2, PW[1].w);
+    put_f32(c.b2, PW[1].b);
+  } else {
+    put_f32(c.w1, PW[0].w);
+    c.b1c = static_cast<float>(PW[0].b[0]);
+    put_f32(c.W2, PW[2].w);
+    put_f32(c.b2, PW[2].b);
+  }
+  put_f32(c.Ws1, nv.selector.weights[0].w);
+  put_f32(c.bs1, nv.selector.weights[0].b);
+  put_f32(c.ws2, nv.selector.weights[2].w);
+  c.bs2 = static_cast<float>(nv.selector.weights[2].b[0]);
+  c.delta = nv.delta;
+  cur = nv;
+  for (auto& g : graph_)
+    if (g) {
+      cudaGraphExecDestroy(g);
+      g = nullptr;
+    }
+}
+
+void Engine::read_taps(int layer, int B, double* host_out) {
+  std::lock_guard<std::recursive_mutex> dev_lock(dev_stream(device_).mu);
+  ck(cudaSetDevice(device_), "cudaSetDevice");
+  require(model_.family == "mlp", "read_taps: retraining records come from the MLP base family");
+  require(layer >= 1 && layer <= model_.num_blocks && B >= 0 && B <= max_batch_, "read_taps: bad layer or batch");
+  const DevFC& f = mlp_fc_[static_cast<size_t>(layer - 1)];
+  const Planes act = mlp_act_[static_cast<size_t>(layer - 1)];
+  if (B == 0) return;
+  double* d = nullptr;
+  ck(cudaMallocAsync(&d, static_cast<size_t>(B) * f.out * sizeof(double), stream_), "read_taps alloc");
+  launch_planes_to_f64(act.hi, act.lo, f.outp, f.out, B, d, stream_);
+  const cudaError_t e = cudaMemcpyAsync(host_out, d, static_cast<size_t>(B) * f.out * sizeof(double),
+                                        cudaMemcpyDeviceToHost, stream_);
+  cudaFreeAsync(d, stream_);
+  ck(e, "read_taps copy");
+  ck(cudaStreamSynchronize(stream_), "read_taps");
+}
+
+void Engine::read_base_probs(int B, double* host_out) {
+  std::lock_guard<std::recursive_mutex> dev_lock(dev_stream(device_).mu);
+  ck(cudaSetDevice(device_), "cudaSetDevice");
+  require(model_.family == "mlp", "read_base_probs: retraining records come from the MLP base family");
+  require(B >= 0 && B <= max_batch_, "read_base_probs: bad batch");
+  if (B == 0) return;
+  const DevFC& f = mlp_fc_.back();
+  const Planes act = mlp_act_.back();
+  const int C = model_.num_classes;
+  double* d = nullptr;
+  ck(cudaMallocAsync(&d, 2 * static_cast<size_t>(B) * C * sizeof(double), stream_), "read_base_probs alloc");
+  launch_head_probs_f64(act.hi, act.lo, f.outp, f.out, head_w_, head_b_, C, B, d, d + static_cast<size_t>(B) * C,
+                        stream_);
+  const cudaError_t e = cudaMemcpyAsync(host_out, d + static_cast<size_t>(B) * C, static_cast<size_t>(B) * C * sizeof(double),
+                                        cudaMemcpyDeviceToHost, stream_);
+  cudaFreeAsync(d, stream_);
+  ck(e, "read_base_probs copy");
+  ck(cudaStreamSynchronize(stream_), "read_base_probs");
 }
 
 double Engine::delta(int layer) const {

@@ -96,6 +96,16 @@ class Engine {
     return layer >= 1 && layer < static_cast<int>(cache_of_layer_.size()) && cache_of_layer_[static_cast<size_t>(layer)] >= 0;
   }
   void set_selector_out(int layer, double gain, double bias);
+  // Swap a retrained variant (same architecture) in for the cache at its
+  // layer, after every batch already enqueued (run_adaptation's swap,
+  // serving.cpp:301-315).
+  void update_variant(const CacheVariant& v);
+  // Retraining records of the last SHADOW batch (MLP base family): taps of
+  // rows [0, B) at `layer` as doubles [B][tap_dim] and the base model's output
+  // distribution y [B][classes] (forward_with_taps, base_model.cpp:56-63).
+  void read_taps(int layer, int B, double* host_out);
+  void read_base_probs(int B, double* host_out);
+  const std::vector<CacheVariant>& variants() const { return variants_; }
 
   // ----- introspection
   int device() const { return device_; }

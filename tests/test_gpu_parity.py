@@ -542,3 +542,143 @@ def test_full_size_invariants(cfg):
     assert 0.5 < np.mean(cp.exit_layer > 0) <= 1.0  # calibrated selectors: most requests exit early
     dep.close()
     base.close()
+
+
+# ---------------------------------------------------------------- retraining / online adaptation (§8f rank 3)
+def _net_params(text, which):
+    return [l for l in O.parse_variant(text)[which] if l["w"] is not None]
+
+
+def _assert_nets_close(ours_txt, ref_txt, rtol):
+    for which in ("predictor", "selector"):
+        for a, b in zip(_net_params(ours_txt, which), _net_params(ref_txt, which)):
+            for k in ("w", "b"):
+                scale = max(1.0, float(np.max(np.abs(b[k]))))
+                err = float(np.max(np.abs(a[k] - b[k])))
+                assert err <= rtol * scale, (which, k, err, scale)
+
+
+def _ref_records(rm, X, layer):
+    taps, ys = [], []
+    for x in X:
+        t, y = rm.forward_taps(x)
+        taps.append(t[layer - 1])
+        ys.append(y)
+    return np.array(taps), np.array(ys)
+
+
+@pytest.mark.parametrize("k", [0, 1])  # FC(32) at layer 1, Conv(3,1) at layer 2
+@requires_ref
+def test_train_predictor_selector_vs_reference(k):
+    """GPU fp64 SGD (train_predictor / train_selector, cache.cpp:179-257)
+    against the reference's own functions on the same double records:
+    identical schedule (Rng shuffles, batches, weights), weights within
+    rounding (tree-ordered forward dots, CUDA exp/log)."""
+    model_txt, vtxt, X, _, _ = _load_trained()
+    rm = O.RefModel.load(model_txt)
+    v = lcb.load_variant(vtxt[k])
+    rv = O.RefVariant.load(vtxt[k])
+    taps, y = _ref_records(rm, X[:150], v.layer)
+    w = np.random.default_rng(3).uniform(0.2, 1.0, len(taps))
+    cfg = lcb.TrainConfig(learning_rate=0.01, epochs=4, batch_size=16, seed=77)
+    lcb.train_predictor(v, taps, y, cfg, tau=2.0, beta=0.5, sample_weights=w)
+    rp = O.ref_train(rv, "predictor", taps, y, weights=w, lr=0.01, epochs=4, batch=16, seed=77, a=2.0, b=0.5)
+    _assert_nets_close(v.save(), rp.save(), 1e-9)
+    cfg2 = lcb.TrainConfig(learning_rate=0.02, epochs=3, batch_size=16, seed=78)
+    lcb.train_selector(v, taps, y, cfg2, w_fp=5.0, w_fn=1.0)
+    rs = O.ref_train(rp, "selector", taps, y, lr=0.02, epochs=3, batch=16, seed=78, a=5.0, b=1.0)
+    _assert_nets_close(v.save(), rs.save(), 1e-9)
+
+
+def test_train_errors_are_reference_typed():
+    """Bad records are invalid_argument (ValueError); a diverging loss is the
+    reference's runtime_error (RuntimeError) and leaves the variant as it was."""
+    model_txt, vtxt, X, _, _ = _load_trained()
+    rm = O.RefModel.load(model_txt)
+    v = lcb.load_variant(vtxt[0])
+    before = v.save()
+    taps, y = _ref_records(rm, X[:32], v.layer)
+    with pytest.raises(ValueError):  # tap dimension mismatch
+        lcb.train_predictor(v, taps[:, :3], y)
+    with pytest.raises(ValueError):  # sample weight count mismatch
+        lcb.train_predictor(v, taps, y, sample_weights=[1.0])
+    with pytest.raises(RuntimeError, match="diverged"):
+        lcb.train_predictor(v, taps * 1e200, y, lcb.TrainConfig(learning_rate=1e200, epochs=2))
+    assert v.save() == before
+
+
+def _adapt_setup(n_req=900, minutes=60.0):
+    model_txt, vtxt, X, reqs, _ = _load_trained()
+    test = [l.split() for l in open(os.path.join(GOLDEN, "trained", "dataset.txt")).read().split("\n")
+            if l.startswith("test ")]
+    labels = np.array([int(t[1]) for t in test], np.int32)
+    rng = np.random.default_rng(11)
+    times = np.sort(rng.uniform(0.0, minutes, n_req))
+    samp = np.array([reqs[i % len(reqs)][1] for i in range(n_req)], np.int32)
+    return model_txt, vtxt, X, labels, times, samp
+
+
+@pytest.mark.parametrize("pause_ms", [0.0, 90000.0])
+@requires_ref
+def test_run_adaptation_vs_reference(pause_ms):
+    """run_adaptation (serving.cpp:213-340) on the GPU against the reference
+    loop on the same deployment, stream and original records: identical
+    retrain schedule (window sizes, mix-in draws, applied flags), traces
+    equal up to bf16x3 tap rounding, final caches within 1e-3."""
+    model_txt, vtxt, X, labels, times, samp = _adapt_setup()
+    sel = [0, 1, 3]  # FC(32) L1, Conv(3,1) L2, FC(32) L4
+    m = lcb.load_base_model(model_txt)
+    vs = [lcb.load_variant(vtxt[k]) for k in sel]
+    dep = lcb.Deployment(m, vs, precision="bf16x3", max_batch=256)
+    rm = O.RefModel.load(model_txt)
+    rvs = [O.RefVariant.load(vtxt[k]) for k in sel]
+    orig_x = X[-120:]
+    otaps, oy = [], []
+    for v in vs:
+        t, y = _ref_records(rm, orig_x, v.layer)
+        otaps.append(t)
+        oy = y
+    cfg = lcb.AdaptationConfig(sample_rate=0.3, window_min=30.0, retrain_interval_min=15.0, epochs=3,
+                               learning_rate=0.005, retrain_pause_ms=pause_ms)
+    stream = [lcb.Request(i, float(times[i]), int(labels[samp[i]]), int(samp[i])) for i in range(len(times))]
+    res = lcb.run_adaptation(dep, X, labels, stream, cfg, otaps, oy, seed=5, adapt_on=True)
+    cfg8 = [cfg.sample_rate, cfg.window_min, cfg.retrain_interval_min, cfg.recency_decay, cfg.mixin_fraction,
+            cfg.epochs, cfg.learning_rate, cfg.retrain_pause_ms]
+    hl, sv, bp, ev, finals = O.ref_run_adaptation(rm, rvs, X, labels, times, samp, cfg8,
+                                                   [cfg.tau, cfg.beta, cfg.w_fp, cfg.w_fn], orig_x, 5, True)
+    assert len(res.retrains) == len(ev) >= 3
+    for e, r in zip(res.retrains, ev):
+        assert (e.interval, e.window_size, e.mixin_size, int(e.applied)) == (int(r[0]), int(r[2]), int(r[3]),
+                                                                             int(r[4]))
+        assert e.time_min == r[1]
+    ours_hl = np.array([t.hit_layer for t in res.traces])
+    ours_sv = np.array([t.served_pred for t in res.traces])
+    ours_bp = np.array([t.base_pred for t in res.traces])
+    assert np.mean(ours_bp == bp) >= 0.995
+    assert np.mean(ours_hl == hl) >= 0.98, np.mean(ours_hl == hl)
+    assert np.mean(ours_sv == sv) >= 0.98
+    for v, rv in zip(res.final_variants, finals):
+        _assert_nets_close(v.save(), rv.save(), 1e-3)
+    # the adapted caches changed (the loop really retrained and swapped)
+    assert any(f.save() != lcb.load_variant(vtxt[k]).save() for f, k in zip(res.final_variants, sel))
+    assert sum(s.requests for s in res.timeline) == len(times)
+    dep.close()
+
+
+def test_run_adaptation_frozen_matches_serve():
+    """adapt_on=False: no retrains, caches frozen, traces equal the plain
+    shadow serve of the same requests (serving.hpp:125-128)."""
+    model_txt, vtxt, X, labels, times, samp = _adapt_setup(n_req=300)
+    m = lcb.load_base_model(model_txt)
+    vs = [lcb.load_variant(t) for t in vtxt]
+    dep = lcb.Deployment(m, vs, precision="bf16x3", max_batch=128)
+    stream = [lcb.Request(i, float(times[i]), int(labels[samp[i]]), int(samp[i])) for i in range(len(times))]
+    res = lcb.run_adaptation(dep, X, labels, stream, lcb.AdaptationConfig(), [np.zeros((0, 1))] * len(vs),
+                             np.zeros((0, m.num_classes)), seed=1, adapt_on=False)
+    assert res.retrains == []
+    sh = dep.serve(X[samp[:128]], shadow=True)
+    assert np.array_equal(np.array([t.hit_layer for t in res.traces[:128]]), sh.exit_layer)
+    assert np.array_equal(np.array([t.served_pred for t in res.traces[:128]]), sh.served)
+    for f, t in zip(res.final_variants, vtxt):
+        assert f.save() == lcb.load_variant(t).save()
+    dep.close()
