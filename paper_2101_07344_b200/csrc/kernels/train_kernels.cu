@@ -59,6 +59,68 @@ __global__ void fc_forward_kernel(const double* __restrict__ x, long long ld, co
   }
 }
 
+// Wide-input FC forward: a CTA owns 32 outputs (4 per warp) x one 256-wide
+// slice of the input (blockIdx.y); the slice of 16 samples is staged in
+// shared memory once and reused by all 32 outputs.
+constexpr int kSplitRows = 16;
+constexpr int kSplitChunk = 256;
+constexpr int kSplitOuts = 32;
+__global__ void __launch_bounds__(256) fc_forward_split_kernel(const double* __restrict__ x, long long ld,
+                                                               const int* __restrict__ rows, int nb,
+                                                               const double* __restrict__ w, int in, int out,
+                                                               double* __restrict__ part) {
+  __shared__ double xs[kSplitRows][kSplitChunk];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j0 = blockIdx.y * kSplitChunk;
+  const int jn = min(kSplitChunk, in - j0);
+  for (int k0 = 0; k0 < nb; k0 += kSplitRows) {
+    const int kn = min(kSplitRows, nb - k0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < kSplitRows * kSplitChunk; e += blockDim.x) {
+      const int q = e / kSplitChunk, j = e % kSplitChunk;
+      xs[q][j] = (q < kn && j < jn) ? x[row_of(rows, k0 + q) * ld + j0 + j] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int t = 0; t < kSplitOuts / 8; ++t) {
+      const int o = blockIdx.x * kSplitOuts + warp * (kSplitOuts / 8) + t;
+      if (o >= out) break;
+      const double* wr = w + static_cast<long long>(o) * in + j0;
+      double acc[kSplitRows];
+#pragma unroll
+      for (int q = 0; q < kSplitRows; ++q) acc[q] = 0.0;
+#pragma unroll 4
+      for (int j = lane; j < jn; j += 32) {
+        const double wj = wr[j];
+#pragma unroll
+        for (int q = 0; q < kSplitRows; ++q) acc[q] += wj * xs[q][j];
+      }
+#pragma unroll
+      for (int q = 0; q < kSplitRows; ++q) {
+#pragma unroll
+        for (int off = 16; off; off >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], off);
+      }
+      if (lane < kn) {
+        double v = acc[0];
+#pragma unroll
+        for (int q = 1; q < kSplitRows; ++q)
+          if (lane == q) v = acc[q];
+        part[(static_cast<long long>(blockIdx.y) * nb + k0 + lane) * out + o] = v;
+      }
+    }
+  }
+}
+
+__global__ void fc_forward_reduce_kernel(const double* __restrict__ part, int ksplit, int nb, int out,
+                                         const double* __restrict__ b, double* __restrict__ y) {
+  const long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (e >= static_cast<long long>(nb) * out) return;
+  const int o = static_cast<int>(e % out);
+  double acc = 0.0;
+  for (int s = 0; s < ksplit; ++s) acc += part[static_cast<long long>(s) * nb * out + e];
+  y[e] = dadd(b[o], acc);
+}
+
 // ReLU / AvgPool / Conv1d forward: one thread per (sample, output).
 __global__ void elem_forward_kernel(TrainLayer L, const double* __restrict__ x, long long ld,
                                     const int* __restrict__ rows, int nb, double* __restrict__ y) {
@@ -129,6 +191,78 @@ __global__ void fc_wgrad_sgd_kernel(TrainLayer L, const double* __restrict__ x, 
     sgd_update(L.w + e, L.vw + e, acc, lr, mom);
   } else {
     const int o = static_cast<int>(e - nw);
+    for (int k = 0; k < nb; ++k) acc = dadd(acc, dmul(scale[k], g[static_cast<long long>(k) * L.out + o]));
+    sgd_update(L.b + o, L.vb + o, acc, lr, mom);
+  }
+}
+
+// Same, two adjacent weights per thread (16-byte loads/stores; even `in`).
+__global__ void fc_wgrad_sgd2_kernel(TrainLayer L, const double* __restrict__ x, long long ld,
+                                     const int* __restrict__ rows, const double* __restrict__ g,
+                                     const double* __restrict__ scale, int nb, double lr, double mom) {
+  const long long nw2 = static_cast<long long>(L.out) * L.in / 2;
+  const long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (e >= nw2 + L.out) return;
+  if (e < nw2) {
+    const int o = static_cast<int>(2 * e / L.in), j = static_cast<int>(2 * e % L.in);
+    double a0 = 0.0, a1 = 0.0;
+    for (int k = 0; k < nb; ++k) {
+      const double gk = g[static_cast<long long>(k) * L.out + o], sk = scale[k];
+      const double2 xv = *reinterpret_cast<const double2*>(x + row_of(rows, k) * ld + j);
+      a0 = dadd(a0, dmul(sk, dmul(gk, xv.x)));
+      a1 = dadd(a1, dmul(sk, dmul(gk, xv.y)));
+    }
+    double2* wp = reinterpret_cast<double2*>(L.w) + e;
+    double2* vp = reinterpret_cast<double2*>(L.vw) + e;
+    double2 wv = *wp, vv = *vp;
+    sgd_update(&wv.x, &vv.x, a0, lr, mom);
+    sgd_update(&wv.y, &vv.y, a1, lr, mom);
+    *wp = wv;
+    *vp = vv;
+  } else {
+    const int o = static_cast<int>(e - nw2);
+    double acc = 0.0;
+    for (int k = 0; k < nb; ++k) acc = dadd(acc, dmul(scale[k], g[static_cast<long long>(k) * L.out + o]));
+    sgd_update(L.b + o, L.vb + o, acc, lr, mom);
+  }
+}
+
+// Same, a 4-output x 2-input block per thread: each x pair loaded once for
+// four outputs (out % 4 == 0, even `in`).
+__global__ void fc_wgrad_sgd42_kernel(TrainLayer L, const double* __restrict__ x, long long ld,
+                                      const int* __restrict__ rows, const double* __restrict__ g,
+                                      const double* __restrict__ scale, int nb, double lr, double mom) {
+  const int in2 = L.in / 2;
+  const long long nblk = static_cast<long long>(L.out / 4) * in2;
+  const long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (e >= nblk + L.out) return;
+  if (e < nblk) {
+    const int o0 = static_cast<int>(e / in2) * 4, j = static_cast<int>(e % in2) * 2;
+    double a[4][2] = {};
+    for (int k = 0; k < nb; ++k) {
+      const double sk = scale[k];
+      const double2 xv = *reinterpret_cast<const double2*>(x + row_of(rows, k) * ld + j);
+      const double* gk = g + static_cast<long long>(k) * L.out + o0;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        a[r][0] = dadd(a[r][0], dmul(sk, dmul(gk[r], xv.x)));
+        a[r][1] = dadd(a[r][1], dmul(sk, dmul(gk[r], xv.y)));
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const long long idx = (static_cast<long long>(o0 + r) * L.in + j) / 2;
+      double2* wp = reinterpret_cast<double2*>(L.w) + idx;
+      double2* vp = reinterpret_cast<double2*>(L.vw) + idx;
+      double2 wv = *wp, vv = *vp;
+      sgd_update(&wv.x, &vv.x, a[r][0], lr, mom);
+      sgd_update(&wv.y, &vv.y, a[r][1], lr, mom);
+      *wp = wv;
+      *vp = vv;
+    }
+  } else {
+    const int o = static_cast<int>(e - nblk);
+    double acc = 0.0;
     for (int k = 0; k < nb; ++k) acc = dadd(acc, dmul(scale[k], g[static_cast<long long>(k) * L.out + o]));
     sgd_update(L.b + o, L.vb + o, acc, lr, mom);
   }
@@ -333,13 +467,184 @@ __global__ void softmax_rows_kernel(const double* __restrict__ x, int N, int C, 
   for (int i = 0; i < C; ++i) o[i] /= sum;
 }
 
+constexpr int kFusedThreads = 1024;
+
+__global__ void __launch_bounds__(kFusedThreads, 1)
+    sgd_fused_kernel(FusedNet net, const double* __restrict__ x, long long ld, const int* __restrict__ rows_all,
+                     const double* __restrict__ scale_all, const int* __restrict__ boff, const int* __restrict__ bnb,
+                     int nbatches, FusedLoss loss, double lr, double mom, double* g, double* gx, int* bad) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int bi = 0; bi < nbatches; ++bi) {
+    const int off = boff[bi], nb = bnb[bi];
+    const int* rows = rows_all + off;
+    const double* scale = scale_all + off;
+    // ---- forward (network.cpp:104-164), serial dots in the reference's order
+    for (int i = 0; i < net.nl; ++i) {
+      const TrainLayer& L = net.L[i];
+      const double* in = i == 0 ? x : net.act[i];
+      const long long in_ld = i == 0 ? ld : L.in;
+      double* out = net.act[i + 1];
+      for (int e = tid; e < nb * L.out; e += nt) {
+        const int k = e / L.out, o = e % L.out;
+        const double* xr = in + (i == 0 ? static_cast<long long>(rows[k]) : k) * in_ld;
+        double v;
+        if (L.kind == 0) {
+          v = L.b[o];
+          const double* wr = L.w + static_cast<long long>(o) * L.in;
+          for (int j = 0; j < L.in; ++j) v = dadd(v, dmul(wr[j], xr[j]));
+        } else if (L.kind == 1) {
+          v = xr[o] > 0.0 ? xr[o] : 0.0;
+        } else if (L.kind == 2) {
+          double acc = 0.0;
+          for (int t = 0; t < L.window; ++t) acc = dadd(acc, xr[static_cast<long long>(o) * L.window + t]);
+          v = dmul(acc, 1.0 / L.window);
+        } else {
+          v = L.b[0];
+          for (int t = 0; t < L.kernel; ++t) v = dadd(v, dmul(L.w[t], xr[static_cast<long long>(o) * L.stride + t]));
+        }
+        out[e] = v;
+      }
+      __syncthreads();
+    }
+    // ---- loss gradient, one thread per sample (serial over classes)
+    const double* outp = net.act[net.nl];
+    for (int k = tid; k < nb; k += nt) {
+      const long long r = rows[k];
+      if (loss.kind == 0) {
+        const int C = loss.C;
+        const double tau = loss.a, beta = loss.b;
+        const double* l = outp + static_cast<long long>(k) * C;
+        const double* pt = loss.p_tau + r * C;
+        double m = l[0], mt = l[0] / tau;
+        for (int i = 1; i < C; ++i) {
+          m = std_max(m, l[i]);
+          mt = std_max(mt, l[i] / tau);
+        }
+        double sm = 0.0, st = 0.0;
+        for (int i = 0; i < C; ++i) sm = dadd(sm, exp(__dsub_rn(l[i], m)));
+        for (int i = 0; i < C; ++i) st = dadd(st, exp(__dsub_rn(__ddiv_rn(l[i], tau), mt)));
+        const int h = loss.hard[r];
+        double kl = 0.0, qh = 0.0;
+        for (int i = 0; i < C; ++i) {
+          const double q = __ddiv_rn(exp(__dsub_rn(l[i], m)), sm);
+          const double qt = __ddiv_rn(exp(__dsub_rn(__ddiv_rn(l[i], tau), mt)), st);
+          if (i == h) qh = q;
+          if (pt[i] > 0.0) kl = dadd(kl, dmul(pt[i], __dsub_rn(log(pt[i]), log(std_max(qt, kTinyProb)))));
+          const double hd = dmul(beta, __dsub_rn(q, i == h ? 1.0 : 0.0));
+          const double sf = dmul(dmul(__dsub_rn(1.0, beta), tau), __dsub_rn(qt, pt[i]));
+          g[static_cast<long long>(k) * C + i] = dadd(hd, sf);
+        }
+        kl = std_max(kl, 0.0);
+        const double lossv = beta * -log(std_max(qh, kTinyProb)) + (1.0 - beta) * tau * tau * kl;
+        if (!isfinite(lossv)) atomicOr(bad, 1);
+      } else {
+        const double z = outp[k];
+        double sg;
+        if (z >= 0.0) {
+          sg = __ddiv_rn(1.0, dadd(1.0, exp(-z)));
+        } else {
+          const double ez = exp(z);
+          sg = __ddiv_rn(ez, dadd(1.0, ez));
+        }
+        double lossv;
+        if (loss.target[r] == 1) {
+          lossv = loss.b * softplus(-z);
+          g[k] = dmul(-loss.b, __dsub_rn(1.0, sg));
+        } else {
+          lossv = loss.a * softplus(z);
+          g[k] = dmul(loss.a, sg);
+        }
+        if (!isfinite(lossv)) atomicOr(bad, 1);
+      }
+    }
+    __syncthreads();
+    // ---- backward + SGD, last layer first
+    double* gc = g;
+    double* gn = gx;
+    for (int i = net.nl - 1; i >= 0; --i) {
+      const TrainLayer& L = net.L[i];
+      const double* in = i == 0 ? x : net.act[i];
+      const long long in_ld = i == 0 ? ld : L.in;
+      if (i > 0) {
+        for (int e = tid; e < nb * L.in; e += nt) {
+          const int k = e / L.in, j = e % L.in;
+          const double* gk = gc + static_cast<long long>(k) * L.out;
+          double v = 0.0;
+          if (L.kind == 0) {
+            for (int o = 0; o < L.out; ++o) v = dadd(v, dmul(L.w[static_cast<long long>(o) * L.in + j], gk[o]));
+          } else if (L.kind == 1) {
+            v = in[e] > 0.0 ? gk[j] : 0.0;
+          } else if (L.kind == 2) {
+            v = dmul(gk[j / L.window], 1.0 / L.window);
+          } else {
+            int o_lo = j - L.kernel + 1;
+            o_lo = o_lo <= 0 ? 0 : (o_lo + L.stride - 1) / L.stride;
+            int o_hi = j / L.stride;
+            if (o_hi > L.out - 1) o_hi = L.out - 1;
+            for (int o = o_lo; o <= o_hi; ++o) v = dadd(v, dmul(L.w[j - o * L.stride], gk[o]));
+          }
+          gn[e] = v;
+        }
+        __syncthreads();
+      }
+      if (L.kind == 0) {
+        const long long nw = static_cast<long long>(L.out) * L.in;
+        for (long long e = tid; e < nw + L.out; e += nt) {
+          double acc = 0.0;
+          if (e < nw) {
+            const int o = static_cast<int>(e / L.in), j = static_cast<int>(e % L.in);
+            for (int k = 0; k < nb; ++k) {
+              const double* xr = in + (i == 0 ? static_cast<long long>(rows[k]) : k) * in_ld;
+              acc = dadd(acc, dmul(scale[k], dmul(gc[static_cast<long long>(k) * L.out + o], xr[j])));
+            }
+            sgd_update(L.w + e, L.vw + e, acc, lr, mom);
+          } else {
+            const int o = static_cast<int>(e - nw);
+            for (int k = 0; k < nb; ++k) acc = dadd(acc, dmul(scale[k], gc[static_cast<long long>(k) * L.out + o]));
+            sgd_update(L.b + o, L.vb + o, acc, lr, mom);
+          }
+        }
+      } else if (L.kind == 3) {
+        for (int t = tid; t <= L.kernel; t += nt) {  // t == kernel: bias
+          double acc = 0.0;
+          for (int k = 0; k < nb; ++k) {
+            const double* gk = gc + static_cast<long long>(k) * L.out;
+            const double* xr = in + (i == 0 ? static_cast<long long>(rows[k]) : k) * in_ld;
+            double sk = 0.0;  // backward(): lg.w[t] += go * x[o*stride + t], o ascending
+            for (int o = 0; o < L.out; ++o)
+              sk = dadd(sk, t < L.kernel ? dmul(gk[o], xr[static_cast<long long>(o) * L.stride + t]) : gk[o]);
+            acc = dadd(acc, dmul(scale[k], sk));
+          }
+          if (t < L.kernel)
+            sgd_update(L.w + t, L.vw + t, acc, lr, mom);
+          else
+            sgd_update(L.b, L.vb, acc, lr, mom);
+        }
+      }
+      __syncthreads();
+      if (i > 0) {
+        double* tmp = gc;
+        gc = gn;
+        gn = tmp;
+      }
+    }
+  }
+}
+
 inline unsigned blocks_for(long long n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
 
 }  // namespace
 
+int train_fc_ksplit(int in) { return in < 2048 ? 1 : (in + kSplitChunk - 1) / kSplitChunk; }
+
 void launch_train_forward(const TrainLayer& L, const double* act_in, long long in_ld, const int* rows, int nb,
                           double* act_out, cudaStream_t s) {
-  if (L.kind == 0) {
+  if (L.kind == 0 && L.ksplit > 1 && L.part) {
+    fc_forward_split_kernel<<<dim3((L.out + kSplitOuts - 1) / kSplitOuts, L.ksplit), 256, 0, s>>>(
+        act_in, in_ld, rows, nb, L.w, L.in, L.out, L.part);
+    fc_forward_reduce_kernel<<<blocks_for(static_cast<long long>(nb) * L.out, 256), 256, 0, s>>>(
+        L.part, L.ksplit, nb, L.out, L.b, act_out);
+  } else if (L.kind == 0) {
     fc_forward_kernel<<<blocks_for(static_cast<long long>(L.out) * 32, 256), 256, 0, s>>>(act_in, in_ld, rows, nb, L.w,
                                                                                           L.b, L.in, L.out, act_out);
   } else {
@@ -355,7 +660,13 @@ void launch_train_backward_data(const TrainLayer& L, const double* act_in, const
 
 void launch_train_wgrad_sgd(const TrainLayer& L, const double* act_in, long long in_ld, const int* rows,
                             const double* g, const double* scale, int nb, double lr, double momentum, cudaStream_t s) {
-  if (L.kind == 0) {
+  if (L.kind == 0 && L.in % 2 == 0 && in_ld % 2 == 0 && L.out % 4 == 0 && L.in >= 512) {
+    const long long n = static_cast<long long>(L.out / 4) * (L.in / 2) + L.out;
+    fc_wgrad_sgd42_kernel<<<blocks_for(n, 256), 256, 0, s>>>(L, act_in, in_ld, rows, g, scale, nb, lr, momentum);
+  } else if (L.kind == 0 && L.in % 2 == 0 && in_ld % 2 == 0) {
+    const long long n = static_cast<long long>(L.out) * L.in / 2 + L.out;
+    fc_wgrad_sgd2_kernel<<<blocks_for(n, 256), 256, 0, s>>>(L, act_in, in_ld, rows, g, scale, nb, lr, momentum);
+  } else if (L.kind == 0) {
     const long long n = static_cast<long long>(L.out) * L.in + L.out;
     fc_wgrad_sgd_kernel<<<blocks_for(n, 256), 256, 0, s>>>(L, act_in, in_ld, rows, g, scale, nb, lr, momentum);
   } else if (L.kind == 3) {
@@ -379,6 +690,13 @@ void launch_selector_grad(const double* logit, const int* target, const int* row
 
 void launch_softmax_labels(double* x, int N, int C, const int* hard, int* agree, cudaStream_t s) {
   softmax_labels_kernel<<<blocks_for(N, 128), 128, 0, s>>>(x, N, C, hard, agree);
+}
+
+void launch_sgd_fused(const FusedNet& net, const double* x, long long ld, const int* rows, const double* scale,
+                      const int* batch_off, const int* batch_nb, int nbatches, const FusedLoss& loss, double lr,
+                      double momentum, double* g, double* gx, int* bad, cudaStream_t s) {
+  sgd_fused_kernel<<<1, kFusedThreads, 0, s>>>(net, x, ld, rows, scale, batch_off, batch_nb, nbatches, loss, lr,
+                                               momentum, g, gx, bad);
 }
 
 void launch_planes_to_f64(const void* hi, const void* lo, long long ld, long long D, int B, double* out,

@@ -20,7 +20,14 @@ struct TrainLayer {
   double* b = nullptr;   // FC [out]; Conv1d [1]
   double* vw = nullptr;  // momentum buffers (zero at start, SgdOptimizer ctor)
   double* vb = nullptr;
+  // FC with a wide input: the forward splits the input range over `ksplit`
+  // CTAs per output group and reduces the partials ([ksplit][rows][out]) in
+  // a second pass (deterministic order).
+  int ksplit = 1;
+  double* part = nullptr;
 };
+// ksplit for an FC of input width `in` (1 = single-pass kernel).
+int train_fc_ksplit(int in);
 
 // act_out[k][:] = layer(act_in[k][:]) for k < nb. When rows != nullptr the
 // input row of sample k is act_in[rows[k]] (records gathered in place).
@@ -46,6 +53,29 @@ void launch_selector_grad(const double* logit, const int* target, const int* row
 // Row softmax in place [N][C] plus the agreement label argmax(logits) == hard
 // (selector_labels, cache.cpp:210-218).
 void launch_softmax_labels(double* x, int N, int C, const int* hard, int* agree, cudaStream_t s);
+
+// Whole-schedule SGD in ONE thread block for small networks (the
+// reference's MLP-tap caches: a few thousand parameters): every minibatch's
+// forward, loss gradient, backward and update run back to back inside the
+// block with __syncthreads between phases — no launches, and every sum is
+// serial in the reference's order (forward dots included).
+constexpr int kFusedMaxLayers = 4;
+struct FusedNet {
+  int nl = 0;
+  TrainLayer L[kFusedMaxLayers];
+  double* act[kFusedMaxLayers + 1] = {};  // act[i + 1] = output of layer i, [batch][out]
+};
+struct FusedLoss {
+  int kind = 0;  // 0 distillation (predictor), 1 weighted selector loss
+  int C = 0;
+  double a = 0.0, b = 0.0;  // (tau, beta) or (w_fp, w_fn)
+  const double* p_tau = nullptr;
+  const int* hard = nullptr;    // distillation hard labels
+  const int* target = nullptr;  // selector agreement labels
+};
+void launch_sgd_fused(const FusedNet& net, const double* x, long long ld, const int* rows, const double* scale,
+                      const int* batch_off, const int* batch_nb, int nbatches, const FusedLoss& loss, double lr,
+                      double momentum, double* g, double* gx, int* bad, cudaStream_t s);
 
 // Tap readback for retraining records: rows [B] of hi(+lo) bf16 planes
 // (row stride `ld`, D features) as doubles.

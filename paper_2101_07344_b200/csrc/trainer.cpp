@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -18,16 +19,18 @@ void tck(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw CudaFailure(std::string("train: ") + what + ": " + cudaGetErrorString(e));
 }
 
-// Device allocations released on scope exit (also on throw).
+// Stream-ordered device allocations (the CUDA pool allocator: no device-wide
+// sync per retrain), released on scope exit (also on throw).
 class Arena {
  public:
+  explicit Arena(cudaStream_t s) : s_(s) {}
   ~Arena() {
-    for (void* p : ptrs_) cudaFree(p);
+    for (void* p : ptrs_) cudaFreeAsync(p, s_);
   }
   template <typename T>
   T* alloc(size_t n) {
     void* p = nullptr;
-    tck(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)), "cudaMalloc");
+    tck(cudaMallocAsync(&p, std::max<size_t>(n, 1) * sizeof(T), s_), "cudaMallocAsync");
     ptrs_.push_back(p);
     return static_cast<T*>(p);
   }
@@ -39,6 +42,7 @@ class Arena {
   }
 
  private:
+  cudaStream_t s_;
   std::vector<void*> ptrs_;
 };
 
@@ -51,11 +55,14 @@ struct DeviceGuard {
   ~DeviceGuard() { cudaSetDevice(prev); }
 };
 
-struct StreamGuard {
-  cudaStream_t s = nullptr;
-  StreamGuard() { tck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate"); }
-  ~StreamGuard() { cudaStreamDestroy(s); }
-};
+// One training stream per device and host thread, created on first use.
+cudaStream_t train_stream(int device) {
+  thread_local std::vector<cudaStream_t> streams;
+  if (static_cast<int>(streams.size()) <= device) streams.resize(static_cast<size_t>(device) + 1, nullptr);
+  cudaStream_t& s = streams[static_cast<size_t>(device)];
+  if (!s) tck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+  return s;
+}
 
 int kind_code(LayerKind k) {
   switch (k) {
@@ -91,6 +98,10 @@ struct DevNet {
         L.vb = A.alloc<double>(w.b.size());
         tck(cudaMemsetAsync(L.vw, 0, w.w.size() * sizeof(double), s), "memset");
         tck(cudaMemsetAsync(L.vb, 0, w.b.size() * sizeof(double), s), "memset");
+      }
+      if (L.kind == 0) {
+        L.ksplit = train_fc_ksplit(L.in);
+        if (L.ksplit > 1) L.part = A.alloc<double>(static_cast<size_t>(L.ksplit) * rows * L.out);
       }
       layers.push_back(L);
       act.push_back(A.alloc<double>(static_cast<size_t>(rows) * sp.out_dim));
@@ -207,23 +218,61 @@ int read_flag(const int* d, cudaStream_t s) {
   return h;
 }
 
-// Minibatch SGD over `net` with inputs = rows of x; `grad` writes the output
-// gradient of each batch (and raises the divergence flag).
-template <typename GradFn>
+// Small networks train in one thread block (launch_sgd_fused): the
+// reference's MLP-tap caches have a few thousand parameters, where a
+// launch per phase would dominate. Bigger ones (CNN-tap caches) run one
+// kernel per phase across the GPU, the whole schedule captured as one graph.
+bool fused_fits(const DevNet& net, const FusedLoss& loss, int batch) {
+  if (const char* e = std::getenv("LCB_TRAIN_UNFUSED"); e && e[0] == '1') return false;
+  if (net.layers.size() > static_cast<size_t>(kFusedMaxLayers)) return false;
+  if (loss.kind == 0 && loss.C > 64) return false;
+  long long params = 0, serial = 0;
+  for (const TrainLayer& L : net.layers) {
+    if (L.kind == 0) params += static_cast<long long>(L.out) * L.in + L.out;
+    if (L.kind == 3) serial = std::max<long long>(serial, static_cast<long long>(L.out) * batch);
+    serial = std::max<long long>(serial, L.in);
+  }
+  return params <= 65536 && serial <= 8192;
+}
+
+// Minibatch SGD over `net` with inputs = rows of x.
 void run_sgd(DevNet& net, const double* x, long long ld, const Schedule& sc, const SgdConfig& cfg, Arena& A,
-             cudaStream_t s, GradFn&& grad) {
+             cudaStream_t s, const FusedLoss& loss, int* bad) {
   int* d_rows = A.upload(sc.rows.data(), sc.rows.size(), s);
   double* d_scale = A.upload(sc.scale.data(), sc.scale.size(), s);
   const size_t gsz = static_cast<size_t>(cfg.batch_size) * static_cast<size_t>(net.max_dim());
   double* g = A.alloc<double>(gsz);
   double* gx = A.alloc<double>(gsz);
+  if (fused_fits(net, loss, cfg.batch_size)) {
+    FusedNet fn;
+    fn.nl = static_cast<int>(net.layers.size());
+    for (int i = 0; i < fn.nl; ++i) {
+      fn.L[i] = net.layers[static_cast<size_t>(i)];
+      fn.act[i + 1] = net.act[static_cast<size_t>(i) + 1];
+    }
+    std::vector<int> off, nb;
+    for (const auto& [o, n] : sc.batches) {
+      off.push_back(o);
+      nb.push_back(n);
+    }
+    const int* d_off = A.upload(off.data(), off.size(), s);
+    const int* d_nb = A.upload(nb.data(), nb.size(), s);
+    launch_sgd_fused(fn, x, ld, d_rows, d_scale, d_off, d_nb, static_cast<int>(off.size()), loss, cfg.learning_rate,
+                     cfg.momentum, g, gx, bad, s);
+    tck(cudaGetLastError(), "sgd_fused launch");
+    tck(cudaStreamSynchronize(s), "train");
+    return;
+  }
   // One graph for the whole schedule: it is fully known up front.
   cudaGraph_t graph = nullptr;
   tck(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture");
   for (const auto& [off, nb] : sc.batches) {
     const int* rows = d_rows + off;
     net.forward(x, ld, rows, nb, s);
-    grad(net.act.back(), rows, nb, g);
+    if (loss.kind == 0)
+      launch_distill_grad(net.act.back(), loss.p_tau, loss.hard, rows, nb, loss.C, loss.a, loss.b, g, bad, s);
+    else
+      launch_selector_grad(net.act.back(), loss.target, rows, nb, loss.a, loss.b, g, bad, s);
     net.backward_step(x, ld, rows, nb, g, gx, d_scale + off, cfg.learning_rate, cfg.momentum, s);
   }
   tck(cudaStreamEndCapture(s, &graph), "capture end");
@@ -248,9 +297,8 @@ void gpu_train_predictor(int device, CacheVariant& v, const TrainRecords& r, con
   if (beta < 0.0 || beta > 1.0) throw std::invalid_argument("distill_loss: beta must lie in [0, 1]");
   const std::vector<double> weights = resolve_weights(r, who);
   DeviceGuard dg(device);
-  StreamGuard sg;
-  cudaStream_t s = sg.s;
-  Arena A;
+  cudaStream_t s = train_stream(device);
+  Arena A(s);
   const Uploaded u = upload_records(r, A, s);
   double* p_tau = A.alloc<double>(static_cast<size_t>(r.N) * r.C);
   int* hard = A.alloc<int>(r.N);
@@ -260,10 +308,14 @@ void gpu_train_predictor(int device, CacheVariant& v, const TrainRecords& r, con
   if (read_flag(bad, s) & 2) throw std::invalid_argument("soften: probabilities must be nonnegative and not all zero");
   DevNet net(v.predictor, cfg.batch_size, A, s);
   const Schedule sc = make_schedule(r.N, cfg, 0x90ed, weights);
-  const int C = r.C;
-  run_sgd(net, u.X, r.D, sc, cfg, A, s, [&](const double* logits, const int* rows, int nb, double* g) {
-    launch_distill_grad(logits, p_tau, hard, rows, nb, C, tau, beta, g, bad, s);
-  });
+  FusedLoss loss;
+  loss.kind = 0;
+  loss.C = r.C;
+  loss.a = tau;
+  loss.b = beta;
+  loss.p_tau = p_tau;
+  loss.hard = hard;
+  run_sgd(net, u.X, r.D, sc, cfg, A, s, loss, bad);
   if (read_flag(bad, s)) throw std::runtime_error("train_predictor: loss diverged");
   net.download(v.predictor, s);
 }
@@ -275,9 +327,8 @@ void gpu_train_selector(int device, CacheVariant& v, const TrainRecords& r, cons
   if (w_fp <= 0.0 || w_fn <= 0.0) throw std::invalid_argument("weighted_selector_loss: weights must be positive");
   const std::vector<double> weights = resolve_weights(r, who);
   DeviceGuard dg(device);
-  StreamGuard sg;
-  cudaStream_t s = sg.s;
-  Arena A;
+  cudaStream_t s = train_stream(device);
+  Arena A(s);
   const Uploaded u = upload_records(r, A, s);
   int* hard = A.alloc<int>(r.N);
   int* agree = A.alloc<int>(r.N);
@@ -302,9 +353,13 @@ void gpu_train_selector(int device, CacheVariant& v, const TrainRecords& r, cons
   launch_softmax_labels(inputs, r.N, r.C, hard, agree, s);
   DevNet net(v.selector, cfg.batch_size, A, s);
   const Schedule sc = make_schedule(r.N, cfg, 0x5e1ec7, weights);
-  run_sgd(net, inputs, r.C, sc, cfg, A, s, [&](const double* logit, const int* rows, int nb, double* g) {
-    launch_selector_grad(logit, agree, rows, nb, w_fp, w_fn, g, bad, s);
-  });
+  FusedLoss loss;
+  loss.kind = 1;
+  loss.C = r.C;
+  loss.a = w_fp;
+  loss.b = w_fn;
+  loss.target = agree;
+  run_sgd(net, inputs, r.C, sc, cfg, A, s, loss, bad);
   if (read_flag(bad, s)) throw std::runtime_error("train_selector: loss diverged");
   net.download(v.selector, s);
 }

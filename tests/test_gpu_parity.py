@@ -567,13 +567,16 @@ def _ref_records(rm, X, layer):
     return np.array(taps), np.array(ys)
 
 
+@pytest.mark.parametrize("unfused", [False, True])  # one-block schedule / per-phase kernels in a graph
 @pytest.mark.parametrize("k", [0, 1])  # FC(32) at layer 1, Conv(3,1) at layer 2
 @requires_ref
-def test_train_predictor_selector_vs_reference(k):
+def test_train_predictor_selector_vs_reference(k, unfused, monkeypatch):
     """GPU fp64 SGD (train_predictor / train_selector, cache.cpp:179-257)
     against the reference's own functions on the same double records:
     identical schedule (Rng shuffles, batches, weights), weights within
     rounding (tree-ordered forward dots, CUDA exp/log)."""
+    if unfused:
+        monkeypatch.setenv("LCB_TRAIN_UNFUSED", "1")
     model_txt, vtxt, X, _, _ = _load_trained()
     rm = O.RefModel.load(model_txt)
     v = lcb.load_variant(vtxt[k])
@@ -587,6 +590,24 @@ def test_train_predictor_selector_vs_reference(k):
     cfg2 = lcb.TrainConfig(learning_rate=0.02, epochs=3, batch_size=16, seed=78)
     lcb.train_selector(v, taps, y, cfg2, w_fp=5.0, w_fn=1.0)
     rs = O.ref_train(rp, "selector", taps, y, lr=0.02, epochs=3, batch=16, seed=78, a=5.0, b=1.0)
+    _assert_nets_close(v.save(), rs.save(), 1e-9)
+
+
+@requires_ref
+def test_train_wide_tap_cache_vs_reference():
+    """A CNN-sized tap (4096 features) into FC(64): the split-input forward
+    and the 4x2 weight-gradient kernels (not the one-block schedule)."""
+    D, C, N = 4096, 10, 48
+    v = lcb.build_variant(2, 0, "FC(64)", D, C, 21)
+    rv = O.RefVariant.build(2, 0, "FC(64)", D, C, 21)
+    rng = np.random.default_rng(5)
+    taps = np.maximum(rng.standard_normal((N, D)), 0.0)
+    y = rng.dirichlet(np.ones(C), N)
+    lcb.train_predictor(v, taps, y, lcb.TrainConfig(learning_rate=0.01, epochs=2, batch_size=16, seed=3))
+    rp = O.ref_train(rv, "predictor", taps, y, lr=0.01, epochs=2, batch=16, seed=3, a=2.0, b=0.5)
+    _assert_nets_close(v.save(), rp.save(), 1e-9)
+    lcb.train_selector(v, taps, y, lcb.TrainConfig(learning_rate=0.02, epochs=2, batch_size=16, seed=4))
+    rs = O.ref_train(rp, "selector", taps, y, lr=0.02, epochs=2, batch=16, seed=4, a=5.0, b=1.0)
     _assert_nets_close(v.save(), rs.save(), 1e-9)
 
 
