@@ -468,29 +468,85 @@ __global__ void softmax_rows_kernel(const double* __restrict__ x, int N, int C, 
 }
 
 constexpr int kFusedThreads = 1024;
+constexpr int kFusedMaxC = 64;  // distillation classes handled by the fused schedule
 
 __global__ void __launch_bounds__(kFusedThreads, 1)
-    sgd_fused_kernel(FusedNet net, const double* __restrict__ x, long long ld, const int* __restrict__ rows_all,
+    sgd_fused_kernel(FusedNet gnet, const double* __restrict__ x, long long ld, const int* __restrict__ rows_all,
                      const double* __restrict__ scale_all, const int* __restrict__ boff, const int* __restrict__ bnb,
-                     int nbatches, FusedLoss loss, double lr, double mom, double* g, double* gx, int* bad) {
+                     int nbatches, FusedLoss loss, double lr, double mom, int rows_cap, int max_dim, int* bad) {
+  // Everything but the records lives in shared memory for the whole
+  // schedule: weights, momentum, activations and gradients (the serial
+  // per-thread loops would otherwise pay L2 latency per step).
+  __shared__ double lsm[kFusedThreads / 32][2 * kFusedMaxC];
+  __shared__ FusedNet net;
+  extern __shared__ double dsm[];
   const int tid = threadIdx.x, nt = blockDim.x;
+  if (tid == 0) {
+    net = gnet;
+    double* p = dsm;
+    for (int i = 0; i < gnet.nl; ++i) {
+      TrainLayer& L = net.L[i];
+      if (L.kind == 0 || L.kind == 3) {
+        const int nw = L.kind == 0 ? L.out * L.in : L.kernel, nbias = L.kind == 0 ? L.out : 1;
+        L.w = p;
+        L.b = p + nw;
+        L.vw = p + nw + nbias;
+        L.vb = p + 2 * nw + nbias;
+        p += 2 * (nw + nbias);
+      }
+    }
+    for (int i = 0; i < gnet.nl; ++i) {
+      net.act[i + 1] = p;
+      p += static_cast<long long>(rows_cap) * gnet.L[i].out;
+    }
+  }
+  __syncthreads();
+  for (int i = 0; i < gnet.nl; ++i) {
+    const TrainLayer& G = gnet.L[i];
+    const TrainLayer& L = net.L[i];
+    if (G.kind == 0 || G.kind == 3) {
+      const int nw = G.kind == 0 ? G.out * G.in : G.kernel, nbias = G.kind == 0 ? G.out : 1;
+      for (int e = tid; e < nw; e += nt) {
+        L.w[e] = G.w[e];
+        L.vw[e] = G.vw[e];
+      }
+      for (int e = tid; e < nbias; e += nt) {
+        L.b[e] = G.b[e];
+        L.vb[e] = G.vb[e];
+      }
+    }
+  }
+  double* g = net.act[net.nl] + static_cast<long long>(rows_cap) * gnet.L[gnet.nl - 1].out;
+  double* gx = g + static_cast<long long>(rows_cap) * max_dim;
+  double* xs = gx + static_cast<long long>(rows_cap) * max_dim;  // the batch's input rows [rows_cap][in]
+  double* ss = xs + static_cast<long long>(rows_cap) * gnet.L[0].in;  // per-sample gradient scales
+  const int in0 = gnet.L[0].in;
+  __syncthreads();
   for (int bi = 0; bi < nbatches; ++bi) {
     const int off = boff[bi], nb = bnb[bi];
     const int* rows = rows_all + off;
-    const double* scale = scale_all + off;
+    // stage the batch's records and scales (all loads in flight at once)
+    for (int e = tid; e < nb * in0; e += nt) {
+      const int k = e / in0, j = e % in0;
+      xs[e] = __ldg(x + static_cast<long long>(__ldg(rows + k)) * ld + j);
+    }
+    for (int k = tid; k < nb; k += nt) ss[k] = __ldg(scale_all + off + k);
+    __syncthreads();
+    const double* scale = ss;
     // ---- forward (network.cpp:104-164), serial dots in the reference's order
     for (int i = 0; i < net.nl; ++i) {
       const TrainLayer& L = net.L[i];
-      const double* in = i == 0 ? x : net.act[i];
-      const long long in_ld = i == 0 ? ld : L.in;
+      const double* in = i == 0 ? xs : net.act[i];
+      const long long in_ld = L.in;
       double* out = net.act[i + 1];
       for (int e = tid; e < nb * L.out; e += nt) {
         const int k = e / L.out, o = e % L.out;
-        const double* xr = in + (i == 0 ? static_cast<long long>(rows[k]) : k) * in_ld;
+        const double* xr = in + static_cast<long long>(k) * in_ld;
         double v;
         if (L.kind == 0) {
           v = L.b[o];
           const double* wr = L.w + static_cast<long long>(o) * L.in;
+#pragma unroll 8
           for (int j = 0; j < L.in; ++j) v = dadd(v, dmul(wr[j], xr[j]));
         } else if (L.kind == 1) {
           v = xr[o] > 0.0 ? xr[o] : 0.0;
@@ -506,38 +562,55 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       }
       __syncthreads();
     }
-    // ---- loss gradient, one thread per sample (serial over classes)
+    // ---- loss gradient: distillation one warp per sample (exps in parallel
+    // across lanes, sums serial in lane 0), selector one thread per sample
     const double* outp = net.act[net.nl];
-    for (int k = tid; k < nb; k += nt) {
-      const long long r = rows[k];
-      if (loss.kind == 0) {
-        const int C = loss.C;
-        const double tau = loss.a, beta = loss.b;
+    if (loss.kind == 0) {
+      const int C = loss.C, warp = tid >> 5, lane = tid & 31;
+      const double tau = loss.a, beta = loss.b;
+      for (int k = warp; k < nb; k += nt >> 5) {
+        const long long r = rows[k];
         const double* l = outp + static_cast<long long>(k) * C;
         const double* pt = loss.p_tau + r * C;
+        double* eq = lsm[warp];
+        double* et = lsm[warp] + kFusedMaxC;
         double m = l[0], mt = l[0] / tau;
         for (int i = 1; i < C; ++i) {
           m = std_max(m, l[i]);
           mt = std_max(mt, l[i] / tau);
         }
+        for (int i = lane; i < C; i += 32) {
+          eq[i] = exp(__dsub_rn(l[i], m));
+          et[i] = exp(__dsub_rn(__ddiv_rn(l[i], tau), mt));
+        }
+        __syncwarp();
         double sm = 0.0, st = 0.0;
-        for (int i = 0; i < C; ++i) sm = dadd(sm, exp(__dsub_rn(l[i], m)));
-        for (int i = 0; i < C; ++i) st = dadd(st, exp(__dsub_rn(__ddiv_rn(l[i], tau), mt)));
+        for (int i = 0; i < C; ++i) sm = dadd(sm, eq[i]);
+        for (int i = 0; i < C; ++i) st = dadd(st, et[i]);
         const int h = loss.hard[r];
-        double kl = 0.0, qh = 0.0;
-        for (int i = 0; i < C; ++i) {
-          const double q = __ddiv_rn(exp(__dsub_rn(l[i], m)), sm);
-          const double qt = __ddiv_rn(exp(__dsub_rn(__ddiv_rn(l[i], tau), mt)), st);
-          if (i == h) qh = q;
-          if (pt[i] > 0.0) kl = dadd(kl, dmul(pt[i], __dsub_rn(log(pt[i]), log(std_max(qt, kTinyProb)))));
+        for (int i = lane; i < C; i += 32) {
+          const double q = __ddiv_rn(eq[i], sm);
+          const double qt = __ddiv_rn(et[i], st);
           const double hd = dmul(beta, __dsub_rn(q, i == h ? 1.0 : 0.0));
           const double sf = dmul(dmul(__dsub_rn(1.0, beta), tau), __dsub_rn(qt, pt[i]));
           g[static_cast<long long>(k) * C + i] = dadd(hd, sf);
         }
-        kl = std_max(kl, 0.0);
-        const double lossv = beta * -log(std_max(qh, kTinyProb)) + (1.0 - beta) * tau * tau * kl;
-        if (!isfinite(lossv)) atomicOr(bad, 1);
-      } else {
+        if (lane == 0) {
+          double kl = 0.0;
+          for (int i = 0; i < C; ++i)
+            if (pt[i] > 0.0)
+              kl = dadd(kl, dmul(pt[i], __dsub_rn(log(pt[i]), log(std_max(__ddiv_rn(et[i], st), kTinyProb)))));
+          kl = std_max(kl, 0.0);
+          const double lossv =
+              beta * -log(std_max(__ddiv_rn(eq[h], sm), kTinyProb)) + (1.0 - beta) * tau * tau * kl;
+          if (!isfinite(lossv)) atomicOr(bad, 1);
+        }
+        __syncwarp();
+      }
+    }
+    for (int k = tid; k < nb && loss.kind == 1; k += nt) {
+      const long long r = rows[k];
+      {
         const double z = outp[k];
         double sg;
         if (z >= 0.0) {
@@ -563,8 +636,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     double* gn = gx;
     for (int i = net.nl - 1; i >= 0; --i) {
       const TrainLayer& L = net.L[i];
-      const double* in = i == 0 ? x : net.act[i];
-      const long long in_ld = i == 0 ? ld : L.in;
+      const double* in = i == 0 ? xs : net.act[i];
+      const long long in_ld = L.in;
       if (i > 0) {
         for (int e = tid; e < nb * L.in; e += nt) {
           const int k = e / L.in, j = e % L.in;
@@ -593,8 +666,9 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
           double acc = 0.0;
           if (e < nw) {
             const int o = static_cast<int>(e / L.in), j = static_cast<int>(e % L.in);
+#pragma unroll 4
             for (int k = 0; k < nb; ++k) {
-              const double* xr = in + (i == 0 ? static_cast<long long>(rows[k]) : k) * in_ld;
+              const double* xr = in + static_cast<long long>(k) * in_ld;
               acc = dadd(acc, dmul(scale[k], dmul(gc[static_cast<long long>(k) * L.out + o], xr[j])));
             }
             sgd_update(L.w + e, L.vw + e, acc, lr, mom);
@@ -609,7 +683,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
           double acc = 0.0;
           for (int k = 0; k < nb; ++k) {
             const double* gk = gc + static_cast<long long>(k) * L.out;
-            const double* xr = in + (i == 0 ? static_cast<long long>(rows[k]) : k) * in_ld;
+            const double* xr = in + static_cast<long long>(k) * in_ld;
             double sk = 0.0;  // backward(): lg.w[t] += go * x[o*stride + t], o ascending
             for (int o = 0; o < L.out; ++o)
               sk = dadd(sk, t < L.kernel ? dmul(gk[o], xr[static_cast<long long>(o) * L.stride + t]) : gk[o]);
@@ -627,6 +701,15 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         gc = gn;
         gn = tmp;
       }
+    }
+  }
+  for (int i = 0; i < gnet.nl; ++i) {
+    const TrainLayer& G = gnet.L[i];
+    const TrainLayer& L = net.L[i];
+    if (G.kind == 0 || G.kind == 3) {
+      const int nw = G.kind == 0 ? G.out * G.in : G.kernel, nbias = G.kind == 0 ? G.out : 1;
+      for (int e = tid; e < nw; e += nt) G.w[e] = L.w[e];
+      for (int e = tid; e < nbias; e += nt) G.b[e] = L.b[e];
     }
   }
 }
@@ -692,11 +775,29 @@ void launch_softmax_labels(double* x, int N, int C, const int* hard, int* agree,
   softmax_labels_kernel<<<blocks_for(N, 128), 128, 0, s>>>(x, N, C, hard, agree);
 }
 
-void launch_sgd_fused(const FusedNet& net, const double* x, long long ld, const int* rows, const double* scale,
-                      const int* batch_off, const int* batch_nb, int nbatches, const FusedLoss& loss, double lr,
-                      double momentum, double* g, double* gx, int* bad, cudaStream_t s) {
-  sgd_fused_kernel<<<1, kFusedThreads, 0, s>>>(net, x, ld, rows, scale, batch_off, batch_nb, nbatches, loss, lr,
-                                               momentum, g, gx, bad);
+size_t sgd_fused_smem_bytes(const FusedNet& net, int rows_cap, int max_dim) {
+  size_t n = 0;
+  for (int i = 0; i < net.nl; ++i) {
+    const TrainLayer& L = net.L[i];
+    if (L.kind == 0) n += 2 * (static_cast<size_t>(L.out) * L.in + L.out);
+    if (L.kind == 3) n += 2 * (static_cast<size_t>(L.kernel) + 1);
+    n += static_cast<size_t>(rows_cap) * L.out;
+  }
+  n += 2 * static_cast<size_t>(rows_cap) * max_dim;
+  n += static_cast<size_t>(rows_cap) * (net.L[0].in + 1);  // staged input rows + scales
+  return n * sizeof(double);
+}
+
+cudaError_t launch_sgd_fused(const FusedNet& net, const double* x, long long ld, const int* rows, const double* scale,
+                             const int* batch_off, const int* batch_nb, int nbatches, const FusedLoss& loss,
+                             double lr, double momentum, int rows_cap, int max_dim, int* bad, cudaStream_t s) {
+  const size_t smem = sgd_fused_smem_bytes(net, rows_cap, max_dim);
+  const cudaError_t e =
+      cudaFuncSetAttribute(sgd_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  sgd_fused_kernel<<<1, kFusedThreads, smem, s>>>(net, x, ld, rows, scale, batch_off, batch_nb, nbatches, loss, lr,
+                                                  momentum, rows_cap, max_dim, bad);
+  return cudaGetLastError();
 }
 
 void launch_planes_to_f64(const void* hi, const void* lo, long long ld, long long D, int B, double* out,

@@ -73,9 +73,13 @@ struct FusedLoss {
   const int* hard = nullptr;    // distillation hard labels
   const int* target = nullptr;  // selector agreement labels
 };
-void launch_sgd_fused(const FusedNet& net, const double* x, long long ld, const int* rows, const double* scale,
-                      const int* batch_off, const int* batch_nb, int nbatches, const FusedLoss& loss, double lr,
-                      double momentum, double* g, double* gx, int* bad, cudaStream_t s);
+// Shared memory the fused schedule needs: weights + momentum + activations
+// of rows_cap samples + two gradient buffers of rows_cap x max_dim.
+size_t sgd_fused_smem_bytes(const FusedNet& net, int rows_cap, int max_dim);
+constexpr size_t kFusedSmemMax = 190 * 1024;
+cudaError_t launch_sgd_fused(const FusedNet& net, const double* x, long long ld, const int* rows, const double* scale,
+                             const int* batch_off, const int* batch_nb, int nbatches, const FusedLoss& loss,
+                             double lr, double momentum, int rows_cap, int max_dim, int* bad, cudaStream_t s);
 
 // Tap readback for retraining records: rows [B] of hi(+lo) bf16 planes
 // (row stride `ld`, D features) as doubles.

@@ -222,17 +222,26 @@ int read_flag(const int* d, cudaStream_t s) {
 // reference's MLP-tap caches have a few thousand parameters, where a
 // launch per phase would dominate. Bigger ones (CNN-tap caches) run one
 // kernel per phase across the GPU, the whole schedule captured as one graph.
+FusedNet fused_view(const DevNet& net) {
+  FusedNet fn;
+  fn.nl = static_cast<int>(net.layers.size());
+  for (int i = 0; i < fn.nl && i < kFusedMaxLayers; ++i) {
+    fn.L[i] = net.layers[static_cast<size_t>(i)];
+    fn.act[i + 1] = net.act[static_cast<size_t>(i) + 1];
+  }
+  return fn;
+}
+
 bool fused_fits(const DevNet& net, const FusedLoss& loss, int batch) {
   if (const char* e = std::getenv("LCB_TRAIN_UNFUSED"); e && e[0] == '1') return false;
   if (net.layers.size() > static_cast<size_t>(kFusedMaxLayers)) return false;
   if (loss.kind == 0 && loss.C > 64) return false;
-  long long params = 0, serial = 0;
+  long long serial = 0;
   for (const TrainLayer& L : net.layers) {
-    if (L.kind == 0) params += static_cast<long long>(L.out) * L.in + L.out;
     if (L.kind == 3) serial = std::max<long long>(serial, static_cast<long long>(L.out) * batch);
     serial = std::max<long long>(serial, L.in);
   }
-  return params <= 65536 && serial <= 8192;
+  return serial <= 8192 && sgd_fused_smem_bytes(fused_view(net), batch, net.max_dim()) <= kFusedSmemMax;
 }
 
 // Minibatch SGD over `net` with inputs = rows of x.
@@ -244,12 +253,6 @@ void run_sgd(DevNet& net, const double* x, long long ld, const Schedule& sc, con
   double* g = A.alloc<double>(gsz);
   double* gx = A.alloc<double>(gsz);
   if (fused_fits(net, loss, cfg.batch_size)) {
-    FusedNet fn;
-    fn.nl = static_cast<int>(net.layers.size());
-    for (int i = 0; i < fn.nl; ++i) {
-      fn.L[i] = net.layers[static_cast<size_t>(i)];
-      fn.act[i + 1] = net.act[static_cast<size_t>(i) + 1];
-    }
     std::vector<int> off, nb;
     for (const auto& [o, n] : sc.batches) {
       off.push_back(o);
@@ -257,9 +260,9 @@ void run_sgd(DevNet& net, const double* x, long long ld, const Schedule& sc, con
     }
     const int* d_off = A.upload(off.data(), off.size(), s);
     const int* d_nb = A.upload(nb.data(), nb.size(), s);
-    launch_sgd_fused(fn, x, ld, d_rows, d_scale, d_off, d_nb, static_cast<int>(off.size()), loss, cfg.learning_rate,
-                     cfg.momentum, g, gx, bad, s);
-    tck(cudaGetLastError(), "sgd_fused launch");
+    tck(launch_sgd_fused(fused_view(net), x, ld, d_rows, d_scale, d_off, d_nb, static_cast<int>(off.size()), loss,
+                         cfg.learning_rate, cfg.momentum, cfg.batch_size, net.max_dim(), bad, s),
+        "sgd_fused launch");
     tck(cudaStreamSynchronize(s), "train");
     return;
   }

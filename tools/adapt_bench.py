@@ -108,7 +108,7 @@ def main():
     cfg = lcb.AdaptationConfig(sample_rate=0.2, window_min=60.0, retrain_interval_min=15.0, epochs=5,
                                learning_rate=0.002)
     stream = [lcb.Request(i, float(times[i]), int(labels[samp[i]]), int(samp[i])) for i in range(n_req)]
-    lcb.run_adaptation(dep, X, labels, stream[:300], cfg, otaps, oy, seed=5, adapt_on=True)  # warm-up
+    lcb.run_adaptation(dep, X, labels, stream, cfg, otaps, oy, seed=5, adapt_on=True)  # warm-up (all paths)
     dep.close()
     dep = lcb.Deployment(m, [lcb.load_variant(vtxt[k]) for k in sel], precision="bf16x3", max_batch=256)
     t0 = time.perf_counter()
