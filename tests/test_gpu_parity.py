@@ -650,9 +650,12 @@ def test_run_adaptation_vs_reference(pause_ms):
     sel = [0, 1, 3]  # FC(32) L1, Conv(3,1) L2, FC(32) L4
     m = lcb.load_base_model(model_txt)
     vs = [lcb.load_variant(vtxt[k]) for k in sel]
-    dep = lcb.Deployment(m, vs, precision="bf16x3", max_batch=256)
     rm = O.RefModel.load(model_txt)
     rvs = [O.RefVariant.load(vtxt[k]) for k in sel]
+    for v, rv in zip(vs, rvs):  # strict thresholds: the stream mixes hits and misses
+        v.delta = 0.995
+        rv.set_delta(0.995)
+    dep = lcb.Deployment(m, vs, precision="bf16x3", max_batch=256)
     orig_x = X[-120:]
     otaps, oy = [], []
     for v in vs:
@@ -678,6 +681,7 @@ def test_run_adaptation_vs_reference(pause_ms):
     assert np.mean(ours_bp == bp) >= 0.995
     assert np.mean(ours_hl == hl) >= 0.98, np.mean(ours_hl == hl)
     assert np.mean(ours_sv == sv) >= 0.98
+    assert 0.05 < np.mean(hl > 0) < 0.95  # both hits and misses exercised
     for v, rv in zip(res.final_variants, finals):
         _assert_nets_close(v.save(), rv.save(), 1e-3)
     # the adapted caches changed (the loop really retrained and swapped)

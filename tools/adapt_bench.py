@@ -97,9 +97,18 @@ def main():
     samp = np.array([reqs[i % len(reqs)][1] for i in range(n_req)], np.int32)
     sel = list(range(len(vtxt)))
     m = lcb.load_base_model(model_txt)
-    vs = [lcb.load_variant(vtxt[k]) for k in sel]
+    DELTA = 0.995  # a strict threshold so the stream mixes hits and misses
+
+    def ours(k):
+        v = lcb.load_variant(vtxt[k])
+        v.delta = DELTA
+        return v
+
+    vs = [ours(k) for k in sel]
     dep = lcb.Deployment(m, vs, precision="bf16x3", max_batch=256)
     rvs = [O.RefVariant.load(vtxt[k]) for k in sel]
+    for rv in rvs:
+        rv.set_delta(DELTA)
     orig_x = X[-200:]
     otaps = []
     for v in vs:
@@ -110,7 +119,7 @@ def main():
     stream = [lcb.Request(i, float(times[i]), int(labels[samp[i]]), int(samp[i])) for i in range(n_req)]
     lcb.run_adaptation(dep, X, labels, stream, cfg, otaps, oy, seed=5, adapt_on=True)  # warm-up (all paths)
     dep.close()
-    dep = lcb.Deployment(m, [lcb.load_variant(vtxt[k]) for k in sel], precision="bf16x3", max_batch=256)
+    dep = lcb.Deployment(m, [ours(k) for k in sel], precision="bf16x3", max_batch=256)
     t0 = time.perf_counter()
     res = lcb.run_adaptation(dep, X, labels, stream, cfg, otaps, oy, seed=5, adapt_on=True)
     gpu_s = time.perf_counter() - t0
