@@ -123,6 +123,61 @@ inline void save_variant(std::ostream& out, const CacheVariant& v) {
   lc_free(s);
 }
 
+// TrainConfig (network.hpp:70-76).
+struct TrainConfig {
+  double learning_rate = 0.01;
+  double momentum = 0.9;
+  int epochs = 20;
+  int batch_size = 16;
+  uint64_t seed = 1;
+};
+
+namespace detail {
+inline void flat_records(const std::vector<std::vector<double>>& taps, const std::vector<std::vector<double>>& ys,
+                         std::vector<double>& t, std::vector<double>& y, long long& D, int& C) {
+  if (taps.empty() || taps.size() != ys.size()) throw std::invalid_argument("train: records/y count mismatch");
+  D = static_cast<long long>(taps[0].size());
+  C = static_cast<int>(ys[0].size());
+  for (size_t i = 0; i < taps.size(); ++i) {
+    if (static_cast<long long>(taps[i].size()) != D || static_cast<int>(ys[i].size()) != C)
+      throw std::invalid_argument("train: ragged records");
+    t.insert(t.end(), taps[i].begin(), taps[i].end());
+    y.insert(y.end(), ys[i].begin(), ys[i].end());
+  }
+}
+}  // namespace detail
+
+// train_predictor (cache.cpp:179-208) on the GPU: taps = each record's tap at
+// the variant's layer, ys = the base model's output distributions.
+inline void train_predictor(CacheVariant& v, const std::vector<std::vector<double>>& taps,
+                            const std::vector<std::vector<double>>& ys, const TrainConfig& cfg, double tau, double beta,
+                            const std::vector<double>& sample_weights = {}, int device = 0) {
+  std::vector<double> t, y;
+  long long D = 0;
+  int C = 0;
+  detail::flat_records(taps, ys, t, y, D, C);
+  if (!sample_weights.empty() && sample_weights.size() != taps.size())
+    throw std::invalid_argument("train_predictor: sample weight count mismatch");
+  check(lc_train_predictor(device, v.handle(), t.data(), D, y.data(), C, static_cast<int>(taps.size()),
+                           sample_weights.empty() ? nullptr : sample_weights.data(), cfg.learning_rate, cfg.momentum,
+                           cfg.epochs, cfg.batch_size, cfg.seed, tau, beta));
+}
+
+// train_selector (cache.cpp:220-257) on the GPU.
+inline void train_selector(CacheVariant& v, const std::vector<std::vector<double>>& taps,
+                           const std::vector<std::vector<double>>& ys, const TrainConfig& cfg, double w_fp, double w_fn,
+                           const std::vector<double>& sample_weights = {}, int device = 0) {
+  std::vector<double> t, y;
+  long long D = 0;
+  int C = 0;
+  detail::flat_records(taps, ys, t, y, D, C);
+  if (!sample_weights.empty() && sample_weights.size() != taps.size())
+    throw std::invalid_argument("train_selector: sample weight count mismatch");
+  check(lc_train_selector(device, v.handle(), t.data(), D, y.data(), C, static_cast<int>(taps.size()),
+                          sample_weights.empty() ? nullptr : sample_weights.data(), cfg.learning_rate, cfg.momentum,
+                          cfg.epochs, cfg.batch_size, cfg.seed, w_fp, w_fn));
+}
+
 // latecache::LookupResult (cache.hpp:131-135)
 struct LookupResult {
   bool hit = false;
@@ -211,6 +266,9 @@ class Deployment {
   }
 
   void set_delta(int layer, double delta) { check(lc_engine_set_delta(h_.get(), layer, delta)); }
+  // run_adaptation's swap (serving.cpp:301-315): a retrained variant replaces
+  // the attached cache at its layer after the batches already enqueued.
+  void swap_in(const CacheVariant& v) { check(lc_engine_update_variant(h_.get(), v.handle())); }
 
   // measure_metrics (cache.cpp:316-335) of every attached cache at every
   // threshold of `grid`, over the records these inputs make (one batch of at

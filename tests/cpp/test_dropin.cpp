@@ -128,6 +128,51 @@ int main(int argc, char** argv) {
       if (std::fabs(want.selector_prob - ref_vars[k].delta) >= 1e-4) CHECK(want.hit == got[i].hit);
     }
   }
+  // retraining (cache.cpp:179-257): the reference's train_predictor /
+  // train_selector and the façade's GPU versions on the same records, then
+  // the swap into the running deployment
+  {
+    const int k = 0;
+    const int layer = ref_vars[k].layer;
+    std::vector<latecache::Sample> samples(data.test.begin(), data.test.begin() + 120);
+    const std::vector<latecache::TapRecord> recs = latecache::collect_taps(ref_model, samples);
+    std::vector<std::vector<double>> taps, ys;
+    for (const auto& r : recs) {
+      taps.push_back(r.taps[static_cast<size_t>(layer - 1)].data);
+      ys.push_back(r.y.data);
+    }
+    latecache::TrainConfig rc;
+    rc.learning_rate = 0.01;
+    rc.epochs = 3;
+    rc.seed = 41;
+    latecache::CacheVariant ref_v = ref_vars[k];
+    latecache::train_predictor(ref_v, recs, rc, 2.0, 0.5, {});
+    latecache::train_selector(ref_v, recs, rc, 5.0, 1.0, {});
+    latecache_b200::TrainConfig bc;
+    bc.learning_rate = 0.01;
+    bc.epochs = 3;
+    bc.seed = 41;
+    latecache_b200::CacheVariant& v = b200_vars[k];
+    latecache_b200::train_predictor(v, taps, ys, bc, 2.0, 0.5);
+    latecache_b200::train_selector(v, taps, ys, bc, 5.0, 1.0);
+    std::ostringstream a, b;
+    latecache::save_variant(a, ref_v);
+    latecache_b200::save_variant(b, v);
+    std::istringstream ai(a.str()), bi(b.str());
+    const latecache::CacheVariant back = latecache::load_variant(bi);  // parse ours with the reference
+    double err = 0.0;
+    for (size_t i = 0; i < back.predictor.weights.size(); ++i)
+      for (size_t j = 0; j < back.predictor.weights[i].w.data.size(); ++j)
+        err = std::max(err, std::fabs(back.predictor.weights[i].w.data[j] - ref_v.predictor.weights[i].w.data[j]));
+    for (size_t i = 0; i < back.selector.weights.size(); ++i)
+      for (size_t j = 0; j < back.selector.weights[i].w.data.size(); ++j)
+        err = std::max(err, std::fabs(back.selector.weights[i].w.data[j] - ref_v.selector.weights[i].w.data[j]));
+    CHECK(err <= 1e-9);
+    dep.swap_in(v);
+    const auto got = dep.lookup(layer, {taps[0]});
+    const latecache::LookupResult want = latecache::lookup(ref_v, recs[0].taps[static_cast<size_t>(layer - 1)]);
+    CHECK(std::fabs(want.selector_prob - got[0].selector_prob) <= 1e-3);
+  }
   // reference error types survive the boundary
   bool threw = false;
   try {
