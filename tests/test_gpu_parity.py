@@ -707,3 +707,84 @@ def test_run_adaptation_frozen_matches_serve():
     for f, t in zip(res.final_variants, vtxt):
         assert f.save() == lcb.load_variant(t).save()
     dep.close()
+
+
+def _adapt_pair(cfg, sel=(0,), n_req=720, minutes=6.0, selector_out=None, seed=31, adapt_on=True, delta=None):
+    model_txt, vtxt, X, labels, times, samp = _adapt_setup(n_req=n_req, minutes=minutes)
+    m = lcb.load_base_model(model_txt)
+    rm = O.RefModel.load(model_txt)
+    vs = [lcb.load_variant(vtxt[k]) for k in sel]
+    rvs = [O.RefVariant.load(vtxt[k]) for k in sel]
+    for v, rv in zip(vs, rvs):
+        if selector_out is not None:
+            v.set_selector_out(*selector_out)
+            rv.set_selector_out(*selector_out)
+        if delta is not None:
+            v.delta = delta
+            rv.set_delta(delta)
+    orig_x = X[-100:]
+    otaps = []
+    oy = None
+    for v in vs:
+        t, oy = _ref_records(rm, orig_x, v.layer)
+        otaps.append(t)
+    dep = lcb.Deployment(m, vs, precision="bf16x3", max_batch=256)
+    stream = [lcb.Request(i, float(times[i]), int(labels[samp[i]]), int(samp[i])) for i in range(len(times))]
+    res = lcb.run_adaptation(dep, X, labels, stream, cfg, otaps, oy, seed=seed, adapt_on=adapt_on)
+    cfg8 = [cfg.sample_rate, cfg.window_min, cfg.retrain_interval_min, cfg.recency_decay, cfg.mixin_fraction,
+            cfg.epochs, cfg.learning_rate, cfg.retrain_pause_ms]
+    ref = O.ref_run_adaptation(rm, rvs, X, labels, times, samp, cfg8, [cfg.tau, cfg.beta, cfg.w_fp, cfg.w_fn],
+                               orig_x, seed, adapt_on)
+    before = [lcb.load_variant(vtxt[k]).save() for k in sel]
+    dep.close()
+    return res, ref, before
+
+
+@requires_ref
+def test_adaptation_schedule_window_and_mixin():
+    """test_serving.cpp:563-595 on the GPU loop: retrains at every interval
+    boundary with the declared window and mix-in sizes, deterministic reruns."""
+    cfg = lcb.AdaptationConfig(sample_rate=1.0, retrain_interval_min=2.0, window_min=2.0, epochs=2)
+    res, (hl, sv, bp, ev, finals), _ = _adapt_pair(cfg)
+    assert [(e.interval, e.time_min) for e in res.retrains] == [(1, 2.0), (2, 4.0)]
+    assert all(e.applied for e in res.retrains)
+    for e, r in zip(res.retrains, ev):
+        assert (e.window_size, e.mixin_size) == (int(r[2]), int(r[3]))
+        assert e.mixin_size == min(100, e.window_size)  # fraction 0.5 -> one per window sample, capped
+    again, _, _ = _adapt_pair(cfg)
+    assert [(t.hit_layer, t.served_pred) for t in again.traces] == [(t.hit_layer, t.served_pred) for t in res.traces]
+    assert again.final_variants[0].save() == res.final_variants[0].save()  # bit-deterministic on the GPU
+    assert np.mean(np.array([t.hit_layer for t in res.traces]) == hl) >= 0.98
+
+
+@requires_ref
+def test_adaptation_diverging_retrains_are_discarded():
+    """test_serving.cpp:597-620: an infinite learning rate diverges; every
+    retrain notes it, the old caches keep serving, traces equal the static run."""
+    cfg = lcb.AdaptationConfig(sample_rate=1.0, retrain_interval_min=2.0, window_min=2.0, epochs=3,
+                               learning_rate=float("inf"))
+    res, (hl, sv, bp, ev, finals), before = _adapt_pair(cfg)
+    assert len(res.retrains) == 2 and all("diverged" in e.note for e in res.retrains), [e.note for e in res.retrains]
+    static, _, _ = _adapt_pair(lcb.AdaptationConfig(), adapt_on=False)
+    assert [t.hit_layer for t in res.traces] == [t.hit_layer for t in static.traces]
+    assert res.final_variants[0].save() == before[0]
+    assert np.array_equal(np.array([t.hit_layer for t in res.traces]), hl)
+
+
+@requires_ref
+def test_adaptation_wakes_a_dead_cache_after_the_pause():
+    """test_serving.cpp:622-667: a silenced selector cannot hit before the first
+    retrain; retraining wakes it, and a swap pause delays the wake-up."""
+    cfg = lcb.AdaptationConfig(sample_rate=1.0, retrain_interval_min=2.0, window_min=4.0, mixin_fraction=0.0,
+                               epochs=25, learning_rate=0.01)
+    res, (hl, sv, bp, ev, finals), _ = _adapt_pair(cfg, n_req=960, minutes=8.0, selector_out=(0.0, -3.0))
+    t = np.array([r.time_min for r in res.traces])
+    h = np.array([r.hit_layer for r in res.traces])
+    assert np.all(h[t < 2.0] == 0) and np.sum(h[t >= 2.0] > 0) > 0
+    assert np.mean(h == hl) >= 0.98
+    paused = lcb.AdaptationConfig(sample_rate=1.0, retrain_interval_min=2.0, window_min=4.0, mixin_fraction=0.0,
+                                  epochs=25, learning_rate=0.01, retrain_pause_ms=2.0 * 60000.0)
+    res2, (hl2, _, _, _, _), _ = _adapt_pair(paused, n_req=960, minutes=8.0, selector_out=(0.0, -3.0))
+    h2 = np.array([r.hit_layer for r in res2.traces])
+    assert np.all(h2[t < 4.0] == 0) and np.sum(h2[t >= 4.0] > 0) > 0
+    assert np.mean(h2 == hl2) >= 0.98
