@@ -469,25 +469,43 @@ __global__ void softmax_rows_kernel(const double* __restrict__ x, int N, int C, 
 
 constexpr int kFusedThreads = 1024;
 constexpr int kFusedMaxC = 64;  // distillation classes handled by the fused schedule
+constexpr int kLossWarps = 16;  // warps computing per-sample distillation gradients
+
+// Layer view inside the fused kernel: every array is a 32-bit offset into
+// the dynamic shared memory (LDS/STS addressing, no generic pointers).
+struct FusedLayerOff {
+  int kind, in, out, window, kernel, stride;
+  int ws;                 // FC weight row stride: odd, so lanes over outputs hit distinct banks
+  int w, b, vw, vb, act;  // act = this layer's output [rows_cap][out]
+};
 
 __global__ void __launch_bounds__(kFusedThreads, 1)
     sgd_fused_kernel(FusedNet gnet, const double* __restrict__ x, long long ld, const int* __restrict__ rows_all,
                      const double* __restrict__ scale_all, const int* __restrict__ boff, const int* __restrict__ bnb,
                      int nbatches, FusedLoss loss, double lr, double mom, int rows_cap, int max_dim, int* bad) {
   // Everything but the records lives in shared memory for the whole
-  // schedule: weights, momentum, activations and gradients (the serial
-  // per-thread loops would otherwise pay L2 latency per step).
-  __shared__ double lsm[kFusedThreads / 32][2 * kFusedMaxC];
-  __shared__ FusedNet net;
+  // schedule: weights, momentum, activations, gradients and each batch's
+  // staged input rows.
+  __shared__ double lsm[kLossWarps][3 * kFusedMaxC];
+  __shared__ FusedLayerOff fl[kFusedMaxLayers];
+  __shared__ int offs[4];  // g, gx, xs, ss
   extern __shared__ double dsm[];
-  const int tid = threadIdx.x, nt = blockDim.x;
+  const int tid = threadIdx.x, nt = blockDim.x, nl = gnet.nl;
   if (tid == 0) {
-    net = gnet;
-    double* p = dsm;
-    for (int i = 0; i < gnet.nl; ++i) {
-      TrainLayer& L = net.L[i];
-      if (L.kind == 0 || L.kind == 3) {
-        const int nw = L.kind == 0 ? L.out * L.in : L.kernel, nbias = L.kind == 0 ? L.out : 1;
+    int p = 0;
+    for (int i = 0; i < nl; ++i) {
+      const TrainLayer& G = gnet.L[i];
+      FusedLayerOff& L = fl[i];
+      L.kind = G.kind;
+      L.in = G.in;
+      L.out = G.out;
+      L.window = G.window;
+      L.kernel = G.kernel;
+      L.stride = G.stride;
+      L.ws = G.in | 1;
+      L.w = L.b = L.vw = L.vb = 0;
+      if (G.kind == 0 || G.kind == 3) {
+        const int nw = G.kind == 0 ? G.out * L.ws : G.kernel, nbias = G.kind == 0 ? G.out : 1;
         L.w = p;
         L.b = p + nw;
         L.vw = p + nw + nbias;
@@ -495,93 +513,98 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         p += 2 * (nw + nbias);
       }
     }
-    for (int i = 0; i < gnet.nl; ++i) {
-      net.act[i + 1] = p;
-      p += static_cast<long long>(rows_cap) * gnet.L[i].out;
+    for (int i = 0; i < nl; ++i) {
+      fl[i].act = p;
+      p += rows_cap * gnet.L[i].out;
     }
+    offs[0] = p;
+    offs[1] = p + rows_cap * max_dim;
+    offs[2] = p + 2 * rows_cap * max_dim;
+    offs[3] = offs[2] + rows_cap * gnet.L[0].in;
   }
   __syncthreads();
-  for (int i = 0; i < gnet.nl; ++i) {
+  for (int i = 0; i < nl; ++i) {
     const TrainLayer& G = gnet.L[i];
-    const TrainLayer& L = net.L[i];
     if (G.kind == 0 || G.kind == 3) {
+      const FusedLayerOff L = fl[i];
       const int nw = G.kind == 0 ? G.out * G.in : G.kernel, nbias = G.kind == 0 ? G.out : 1;
       for (int e = tid; e < nw; e += nt) {
-        L.w[e] = G.w[e];
-        L.vw[e] = G.vw[e];
+        const int d = G.kind == 0 ? (e / G.in) * L.ws + e % G.in : e;
+        dsm[L.w + d] = G.w[e];
+        dsm[L.vw + d] = G.vw[e];
       }
       for (int e = tid; e < nbias; e += nt) {
-        L.b[e] = G.b[e];
-        L.vb[e] = G.vb[e];
+        dsm[L.b + e] = G.b[e];
+        dsm[L.vb + e] = G.vb[e];
       }
     }
   }
-  double* g = net.act[net.nl] + static_cast<long long>(rows_cap) * gnet.L[gnet.nl - 1].out;
-  double* gx = g + static_cast<long long>(rows_cap) * max_dim;
-  double* xs = gx + static_cast<long long>(rows_cap) * max_dim;  // the batch's input rows [rows_cap][in]
-  double* ss = xs + static_cast<long long>(rows_cap) * gnet.L[0].in;  // per-sample gradient scales
   const int in0 = gnet.L[0].in;
+  const int xs = offs[2], ss = offs[3];
   __syncthreads();
   for (int bi = 0; bi < nbatches; ++bi) {
     const int off = boff[bi], nb = bnb[bi];
     const int* rows = rows_all + off;
-    // stage the batch's records and scales (all loads in flight at once)
     for (int e = tid; e < nb * in0; e += nt) {
-      const int k = e / in0, j = e % in0;
-      xs[e] = __ldg(x + static_cast<long long>(__ldg(rows + k)) * ld + j);
+      const int k = e / in0, j = e - k * in0;
+      dsm[xs + e] = __ldg(x + static_cast<long long>(__ldg(rows + k)) * ld + j);
     }
-    for (int k = tid; k < nb; k += nt) ss[k] = __ldg(scale_all + off + k);
+    for (int k = tid; k < nb; k += nt) dsm[ss + k] = __ldg(scale_all + off + k);
     __syncthreads();
-    const double* scale = ss;
     // ---- forward (network.cpp:104-164), serial dots in the reference's order
-    for (int i = 0; i < net.nl; ++i) {
-      const TrainLayer& L = net.L[i];
-      const double* in = i == 0 ? xs : net.act[i];
-      const long long in_ld = L.in;
-      double* out = net.act[i + 1];
+    for (int i = 0; i < nl; ++i) {
+      const FusedLayerOff L = fl[i];
+      const int in = i == 0 ? xs : fl[i - 1].act;
       for (int e = tid; e < nb * L.out; e += nt) {
-        const int k = e / L.out, o = e % L.out;
-        const double* xr = in + static_cast<long long>(k) * in_ld;
+        const int k = e / L.out, o = e - k * L.out;
+        const int xr = in + k * L.in;
         double v;
         if (L.kind == 0) {
-          v = L.b[o];
-          const double* wr = L.w + static_cast<long long>(o) * L.in;
+          v = dsm[L.b + o];
+          const int wr = L.w + o * L.ws;
 #pragma unroll 8
-          for (int j = 0; j < L.in; ++j) v = dadd(v, dmul(wr[j], xr[j]));
+          for (int j = 0; j < L.in; ++j) v = dadd(v, dmul(dsm[wr + j], dsm[xr + j]));
         } else if (L.kind == 1) {
-          v = xr[o] > 0.0 ? xr[o] : 0.0;
+          const double u = dsm[xr + o];
+          v = u > 0.0 ? u : 0.0;
         } else if (L.kind == 2) {
           double acc = 0.0;
-          for (int t = 0; t < L.window; ++t) acc = dadd(acc, xr[static_cast<long long>(o) * L.window + t]);
+          for (int t = 0; t < L.window; ++t) acc = dadd(acc, dsm[xr + o * L.window + t]);
           v = dmul(acc, 1.0 / L.window);
         } else {
-          v = L.b[0];
-          for (int t = 0; t < L.kernel; ++t) v = dadd(v, dmul(L.w[t], xr[static_cast<long long>(o) * L.stride + t]));
+          v = dsm[L.b];
+          for (int t = 0; t < L.kernel; ++t) v = dadd(v, dmul(dsm[L.w + t], dsm[xr + o * L.stride + t]));
         }
-        out[e] = v;
+        dsm[L.act + e] = v;
       }
       __syncthreads();
     }
-    // ---- loss gradient: distillation one warp per sample (exps in parallel
-    // across lanes, sums serial in lane 0), selector one thread per sample
-    const double* outp = net.act[net.nl];
+    // ---- loss gradient into g: distillation one warp per sample (exps in
+    // parallel across lanes, sums serial in lane 0), selector one thread per sample
+    const int outp = fl[nl - 1].act;
+    const int g0 = offs[0];
     if (loss.kind == 0) {
       const int C = loss.C, warp = tid >> 5, lane = tid & 31;
       const double tau = loss.a, beta = loss.b;
-      for (int k = warp; k < nb; k += nt >> 5) {
+      // per-class values computed across lanes; every order-sensitive step
+      // (max chains, sums, the kl accumulation) stays serial in class order
+      for (int k = warp; k < nb && warp < kLossWarps; k += kLossWarps) {
         const long long r = rows[k];
-        const double* l = outp + static_cast<long long>(k) * C;
+        const int l = outp + k * C;
         const double* pt = loss.p_tau + r * C;
         double* eq = lsm[warp];
         double* et = lsm[warp] + kFusedMaxC;
-        double m = l[0], mt = l[0] / tau;
+        double* kt = lsm[warp] + 2 * kFusedMaxC;
+        for (int i = lane; i < C; i += 32) et[i] = __ddiv_rn(dsm[l + i], tau);
+        __syncwarp();
+        double m = dsm[l], mt = et[0];
         for (int i = 1; i < C; ++i) {
-          m = std_max(m, l[i]);
-          mt = std_max(mt, l[i] / tau);
+          m = std_max(m, dsm[l + i]);
+          mt = std_max(mt, et[i]);
         }
         for (int i = lane; i < C; i += 32) {
-          eq[i] = exp(__dsub_rn(l[i], m));
-          et[i] = exp(__dsub_rn(__ddiv_rn(l[i], tau), mt));
+          eq[i] = exp(__dsub_rn(dsm[l + i], m));
+          et[i] = exp(__dsub_rn(et[i], mt));
         }
         __syncwarp();
         double sm = 0.0, st = 0.0;
@@ -593,13 +616,14 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
           const double qt = __ddiv_rn(et[i], st);
           const double hd = dmul(beta, __dsub_rn(q, i == h ? 1.0 : 0.0));
           const double sf = dmul(dmul(__dsub_rn(1.0, beta), tau), __dsub_rn(qt, pt[i]));
-          g[static_cast<long long>(k) * C + i] = dadd(hd, sf);
+          dsm[g0 + k * C + i] = dadd(hd, sf);
+          kt[i] = pt[i] > 0.0 ? dmul(pt[i], __dsub_rn(log(pt[i]), log(std_max(qt, kTinyProb)))) : 0.0;
         }
+        __syncwarp();
         if (lane == 0) {
           double kl = 0.0;
           for (int i = 0; i < C; ++i)
-            if (pt[i] > 0.0)
-              kl = dadd(kl, dmul(pt[i], __dsub_rn(log(pt[i]), log(std_max(__ddiv_rn(et[i], st), kTinyProb)))));
+            if (pt[i] > 0.0) kl = dadd(kl, kt[i]);
           kl = std_max(kl, 0.0);
           const double lossv =
               beta * -log(std_max(__ddiv_rn(eq[h], sm), kTinyProb)) + (1.0 - beta) * tau * tau * kl;
@@ -607,11 +631,10 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         }
         __syncwarp();
       }
-    }
-    for (int k = tid; k < nb && loss.kind == 1; k += nt) {
-      const long long r = rows[k];
-      {
-        const double z = outp[k];
+    } else {
+      for (int k = tid; k < nb; k += nt) {
+        const long long r = rows[k];
+        const double z = dsm[outp + k];
         double sg;
         if (z >= 0.0) {
           sg = __ddiv_rn(1.0, dadd(1.0, exp(-z)));
@@ -622,94 +645,95 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         double lossv;
         if (loss.target[r] == 1) {
           lossv = loss.b * softplus(-z);
-          g[k] = dmul(-loss.b, __dsub_rn(1.0, sg));
+          dsm[g0 + k] = dmul(-loss.b, __dsub_rn(1.0, sg));
         } else {
           lossv = loss.a * softplus(z);
-          g[k] = dmul(loss.a, sg);
+          dsm[g0 + k] = dmul(loss.a, sg);
         }
         if (!isfinite(lossv)) atomicOr(bad, 1);
       }
     }
     __syncthreads();
     // ---- backward + SGD, last layer first
-    double* gc = g;
-    double* gn = gx;
-    for (int i = net.nl - 1; i >= 0; --i) {
-      const TrainLayer& L = net.L[i];
-      const double* in = i == 0 ? xs : net.act[i];
-      const long long in_ld = L.in;
+    int gc = offs[0], gn = offs[1];
+    for (int i = nl - 1; i >= 0; --i) {
+      const FusedLayerOff L = fl[i];
+      const int in = i == 0 ? xs : fl[i - 1].act;
       if (i > 0) {
         for (int e = tid; e < nb * L.in; e += nt) {
-          const int k = e / L.in, j = e % L.in;
-          const double* gk = gc + static_cast<long long>(k) * L.out;
+          const int k = e / L.in, j = e - k * L.in;
+          const int gk = gc + k * L.out;
           double v = 0.0;
           if (L.kind == 0) {
-            for (int o = 0; o < L.out; ++o) v = dadd(v, dmul(L.w[static_cast<long long>(o) * L.in + j], gk[o]));
+#pragma unroll 4
+            for (int o = 0; o < L.out; ++o) v = dadd(v, dmul(dsm[L.w + o * L.ws + j], dsm[gk + o]));
           } else if (L.kind == 1) {
-            v = in[e] > 0.0 ? gk[j] : 0.0;
+            v = dsm[in + e] > 0.0 ? dsm[gk + j] : 0.0;
           } else if (L.kind == 2) {
-            v = dmul(gk[j / L.window], 1.0 / L.window);
+            v = dmul(dsm[gk + j / L.window], 1.0 / L.window);
           } else {
             int o_lo = j - L.kernel + 1;
             o_lo = o_lo <= 0 ? 0 : (o_lo + L.stride - 1) / L.stride;
             int o_hi = j / L.stride;
             if (o_hi > L.out - 1) o_hi = L.out - 1;
-            for (int o = o_lo; o <= o_hi; ++o) v = dadd(v, dmul(L.w[j - o * L.stride], gk[o]));
+            for (int o = o_lo; o <= o_hi; ++o) v = dadd(v, dmul(dsm[L.w + j - o * L.stride], dsm[gk + o]));
           }
-          gn[e] = v;
+          dsm[gn + e] = v;
         }
         __syncthreads();
       }
       if (L.kind == 0) {
-        const long long nw = static_cast<long long>(L.out) * L.in;
-        for (long long e = tid; e < nw + L.out; e += nt) {
+        const int nw = L.out * L.in;
+        for (int e = tid; e < nw + L.out; e += nt) {
           double acc = 0.0;
           if (e < nw) {
-            const int o = static_cast<int>(e / L.in), j = static_cast<int>(e % L.in);
+            const int o = e / L.in, j = e - o * L.in;
 #pragma unroll 4
-            for (int k = 0; k < nb; ++k) {
-              const double* xr = in + static_cast<long long>(k) * in_ld;
-              acc = dadd(acc, dmul(scale[k], dmul(gc[static_cast<long long>(k) * L.out + o], xr[j])));
-            }
-            sgd_update(L.w + e, L.vw + e, acc, lr, mom);
+            for (int k = 0; k < nb; ++k)
+              acc = dadd(acc, dmul(dsm[ss + k], dmul(dsm[gc + k * L.out + o], dsm[in + k * L.in + j])));
+            const int d = o * L.ws + j;
+            const double vn = dadd(dmul(mom, dsm[L.vw + d]), acc);
+            dsm[L.vw + d] = vn;
+            dsm[L.w + d] = __dsub_rn(dsm[L.w + d], dmul(lr, vn));
           } else {
-            const int o = static_cast<int>(e - nw);
-            for (int k = 0; k < nb; ++k) acc = dadd(acc, dmul(scale[k], gc[static_cast<long long>(k) * L.out + o]));
-            sgd_update(L.b + o, L.vb + o, acc, lr, mom);
+            const int o = e - nw;
+            for (int k = 0; k < nb; ++k) acc = dadd(acc, dmul(dsm[ss + k], dsm[gc + k * L.out + o]));
+            const double vn = dadd(dmul(mom, dsm[L.vb + o]), acc);
+            dsm[L.vb + o] = vn;
+            dsm[L.b + o] = __dsub_rn(dsm[L.b + o], dmul(lr, vn));
           }
         }
       } else if (L.kind == 3) {
         for (int t = tid; t <= L.kernel; t += nt) {  // t == kernel: bias
           double acc = 0.0;
           for (int k = 0; k < nb; ++k) {
-            const double* gk = gc + static_cast<long long>(k) * L.out;
-            const double* xr = in + static_cast<long long>(k) * in_ld;
+            const int gk = gc + k * L.out, xr = in + k * L.in;
             double sk = 0.0;  // backward(): lg.w[t] += go * x[o*stride + t], o ascending
             for (int o = 0; o < L.out; ++o)
-              sk = dadd(sk, t < L.kernel ? dmul(gk[o], xr[static_cast<long long>(o) * L.stride + t]) : gk[o]);
-            acc = dadd(acc, dmul(scale[k], sk));
+              sk = dadd(sk, t < L.kernel ? dmul(dsm[gk + o], dsm[xr + o * L.stride + t]) : dsm[gk + o]);
+            acc = dadd(acc, dmul(dsm[ss + k], sk));
           }
-          if (t < L.kernel)
-            sgd_update(L.w + t, L.vw + t, acc, lr, mom);
-          else
-            sgd_update(L.b, L.vb, acc, lr, mom);
+          const int wi = t < L.kernel ? L.w + t : L.b, vi = t < L.kernel ? L.vw + t : L.vb;
+          const double vn = dadd(dmul(mom, dsm[vi]), acc);
+          dsm[vi] = vn;
+          dsm[wi] = __dsub_rn(dsm[wi], dmul(lr, vn));
         }
       }
       __syncthreads();
       if (i > 0) {
-        double* tmp = gc;
+        const int tmp = gc;
         gc = gn;
         gn = tmp;
       }
     }
   }
-  for (int i = 0; i < gnet.nl; ++i) {
+  for (int i = 0; i < nl; ++i) {
     const TrainLayer& G = gnet.L[i];
-    const TrainLayer& L = net.L[i];
     if (G.kind == 0 || G.kind == 3) {
+      const FusedLayerOff L = fl[i];
       const int nw = G.kind == 0 ? G.out * G.in : G.kernel, nbias = G.kind == 0 ? G.out : 1;
-      for (int e = tid; e < nw; e += nt) G.w[e] = L.w[e];
-      for (int e = tid; e < nbias; e += nt) G.b[e] = L.b[e];
+      for (int e = tid; e < nw; e += nt) G.w[e] = dsm[L.w + (G.kind == 0 ? (e / G.in) * L.ws + e % G.in : e)];
+      for (int e = tid; e < nbias; e += nt) G.b[e] = dsm[L.b + e];
     }
   }
 }
@@ -779,7 +803,7 @@ size_t sgd_fused_smem_bytes(const FusedNet& net, int rows_cap, int max_dim) {
   size_t n = 0;
   for (int i = 0; i < net.nl; ++i) {
     const TrainLayer& L = net.L[i];
-    if (L.kind == 0) n += 2 * (static_cast<size_t>(L.out) * L.in + L.out);
+    if (L.kind == 0) n += 2 * (static_cast<size_t>(L.out) * (L.in | 1) + L.out);
     if (L.kind == 3) n += 2 * (static_cast<size_t>(L.kernel) + 1);
     n += static_cast<size_t>(rows_cap) * L.out;
   }
