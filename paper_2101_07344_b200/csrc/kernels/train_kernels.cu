@@ -488,7 +488,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   // staged input rows.
   __shared__ double lsm[kLossWarps][3 * kFusedMaxC];
   __shared__ FusedLayerOff fl[kFusedMaxLayers];
-  __shared__ int offs[4];  // g, gx, xs, ss
+  __shared__ int offs[5];  // g, gx, xs, ss, conv per-sample weight-gradient sums
   extern __shared__ double dsm[];
   const int tid = threadIdx.x, nt = blockDim.x, nl = gnet.nl;
   if (tid == 0) {
@@ -521,6 +521,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     offs[1] = p + rows_cap * max_dim;
     offs[2] = p + 2 * rows_cap * max_dim;
     offs[3] = offs[2] + rows_cap * gnet.L[0].in;
+    offs[4] = offs[3] + rows_cap;
   }
   __syncthreads();
   for (int i = 0; i < nl; ++i) {
@@ -704,15 +705,25 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
           }
         }
       } else if (L.kind == 3) {
-        for (int t = tid; t <= L.kernel; t += nt) {  // t == kernel: bias
-          double acc = 0.0;
-          for (int k = 0; k < nb; ++k) {
-            const int gk = gc + k * L.out, xr = in + k * L.in;
-            double sk = 0.0;  // backward(): lg.w[t] += go * x[o*stride + t], o ascending
-            for (int o = 0; o < L.out; ++o)
-              sk = dadd(sk, t < L.kernel ? dmul(dsm[gk + o], dsm[xr + o * L.stride + t]) : dsm[gk + o]);
-            acc = dadd(acc, dmul(dsm[ss + k], sk));
+        // backward(): per sample lg.w[t] += go * x[o*stride + t] over o in
+        // order (one thread per (sample, tap)), then accumulate_grads over the
+        // samples in order (one thread per tap)
+        const int sk = offs[4], K1 = L.kernel + 1;
+        for (int e = tid; e < nb * K1; e += nt) {
+          const int k = e / K1, t = e - k * K1;
+          const int gk = gc + k * L.out, xr = in + k * L.in;
+          double v = 0.0;
+          if (t < L.kernel) {
+            for (int o = 0; o < L.out; ++o) v = dadd(v, dmul(dsm[gk + o], dsm[xr + o * L.stride + t]));
+          } else {
+            for (int o = 0; o < L.out; ++o) v = dadd(v, dsm[gk + o]);
           }
+          dsm[sk + e] = v;
+        }
+        __syncthreads();
+        for (int t = tid; t < K1; t += nt) {
+          double acc = 0.0;
+          for (int k = 0; k < nb; ++k) acc = dadd(acc, dmul(dsm[ss + k], dsm[sk + k * K1 + t]));
           const int wi = t < L.kernel ? L.w + t : L.b, vi = t < L.kernel ? L.vw + t : L.vb;
           const double vn = dadd(dmul(mom, dsm[vi]), acc);
           dsm[vi] = vn;
@@ -809,6 +820,10 @@ size_t sgd_fused_smem_bytes(const FusedNet& net, int rows_cap, int max_dim) {
   }
   n += 2 * static_cast<size_t>(rows_cap) * max_dim;
   n += static_cast<size_t>(rows_cap) * (net.L[0].in + 1);  // staged input rows + scales
+  int kmax = 0;
+  for (int i = 0; i < net.nl; ++i)
+    if (net.L[i].kind == 3 && net.L[i].kernel > kmax) kmax = net.L[i].kernel;
+  n += static_cast<size_t>(rows_cap) * (kmax + 1);  // conv per-sample weight-gradient sums
   return n * sizeof(double);
 }
 
