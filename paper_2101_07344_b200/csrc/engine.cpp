@@ -203,6 +203,7 @@ Engine::Engine(int device, const BaseModel& model, std::vector<CacheVariant> var
   fused_lookup_ = !(nl && nl[0] == '1');
   const char* ns = std::getenv("LCB_NO_STACKED");
   stacked_ = !(ns && ns[0] == '1');
+  if (const char* km = std::getenv("LCB_KS_MIN_STEPS")) ks_min_steps_ = std::atoi(km);
   const char* nh = std::getenv("LCB_HALO");  // opt-in: not yet faster than the per-tap loads
   halo_ = nh && nh[0] == '1';
   const char* nr = std::getenv("LCB_NO_MMA_RESIDUAL");
@@ -852,6 +853,7 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow) {
       prm->Cout = o.Cout;
       prm->ksplit = 1;
       prm->ks_max = 32;
+      prm->ks_min_steps = ks_min_steps_;
       prm->ws = ws_;
       prm->ws_counters = ws_counters_;
       prm->surv = cur_ids;

@@ -93,6 +93,10 @@ __device__ __forceinline__ TileGeom tile_geom(const TcConvParams& p, int BN) {
     int ks = static_cast<int>(gridDim.x) / g.tiles_mn;
     ks = ks > p.ks_max ? p.ks_max : ks;
     ks = ks > g.nk ? g.nk : ks;
+    if (p.ks_min_steps > 0) {
+      const int cap = g.nk / p.ks_min_steps;
+      ks = ks > cap ? cap : ks;
+    }
     g.ks = ks < 1 ? 1 : ks;
   } else {
     g.ks = 1;

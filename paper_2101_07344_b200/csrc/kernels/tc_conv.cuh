@@ -68,6 +68,7 @@ struct TcConvParams {
   int Cout;            // output channels (multiple of BN)
   int ksplit;          // mode 1: static split-K factor
   int ks_max;          // mode 0: dynamic split-K upper bound (1 = off)
+  int ks_min_steps;  // split-K: at least this many K-steps per split (0 = fill the grid)
   float* ws;           // mode 0 split-K workspace (fp32 partial tiles)
   int* ws_counters;    // per output tile arrival counters (zeroed; reset by the last CTA)
   const int* surv;     // survivor image list (nullptr = identity)
