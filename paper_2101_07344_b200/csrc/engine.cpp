@@ -1198,6 +1198,8 @@ void Engine::update_variant(const CacheVariant& nv) {
   CacheVariant& cur = variants_[static_cast<size_t>(ci)];
   require(same_shape(cur.predictor, nv.predictor) && same_shape(cur.selector, nv.selector),
           "update_variant: architecture differs from the attached variant");
+  std::lock_guard<std::recursive_mutex> dev_lock(dev_stream(device_).mu);
+  ck(cudaSetDevice(device_), "cudaSetDevice");
   // Swap between batches: everything already enqueued finishes with the old networks.
   ck(cudaStreamSynchronize(stream_), "update_variant: sync");
   DevCache& c = *caches_[static_cast<size_t>(ci)];
