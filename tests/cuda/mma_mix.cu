@@ -64,6 +64,60 @@ __global__ void mix_kernel(int steps, int mode, unsigned long long* out) {
   if (warp == 0) tmem_dealloc(tmem, 512);
 }
 
+// M = 64 rates (weights-as-A formulation): N in {64, 128, 256}, 48 MMAs per commit.
+template <int N>
+__global__ void m64_kernel(int iters, unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar;
+  __shared__ uint32_t holder;
+  const int warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < (16384 + N * 128) / 16; i += blockDim.x) reinterpret_cast<uint4*>(sm)[i] = make_uint4(0, 0, 0, 0);
+  if (threadIdx.x == 0) {
+    mbar_init(smem_u32(&bar), 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc(smem_u32(&holder), 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = holder;
+  unsigned long long t0 = 0, t1 = 0;
+  if (warp == 0) {
+    constexpr uint32_t idesc = umma_idesc_bf16(64, N);
+    const uint64_t da = umma_desc_sw128(smem_u32(sm)), db = umma_desc_sw128(smem_u32(sm + 16384));
+    uint32_t phase = 0;
+    t0 = clk();
+    for (int it = 0; it < iters; ++it) {
+      for (int k = 0; k < 48; ++k) umma_bf16_warp(tmem, da + 2 * (k & 3), db + 2 * (k & 3), idesc, k > 0);
+      umma_commit_warp(smem_u32(&bar));
+      mbar_wait(smem_u32(&bar), phase);
+      phase ^= 1;
+    }
+    t1 = clk();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) out[blockIdx.x] = t1 - t0;
+  if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
+template <int N>
+void run_m64() {
+  unsigned long long* d;
+  cudaMalloc(&d, 148 * 8);
+  const int iters = 500;
+  const int smem = 16384 + N * 128 + 1024;
+  cudaFuncSetAttribute(m64_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  m64_kernel<N><<<148, 128, smem>>>(iters, d);
+  cudaDeviceSynchronize();
+  unsigned long long h[148];
+  cudaMemcpy(h, d, 148 * 8, cudaMemcpyDeviceToHost);
+  const double cyc = double(h[0]) / (iters * 48.0);
+  printf("M= 64 N=%3d: %.1f cycles/MMA, %.0f MAC/clk/SM (err %s)\n", N, cyc, 64.0 * N * 16 / cyc,
+         cudaGetErrorString(cudaGetLastError()));
+  cudaFree(d);
+}
+
 template <int BN>
 void run(int mode) {
   unsigned long long* d;
@@ -87,5 +141,8 @@ int main() {
     run<64>(m);
     run<128>(m);
   }
+  run_m64<64>();
+  run_m64<128>();
+  run_m64<256>();
   return 0;
 }
