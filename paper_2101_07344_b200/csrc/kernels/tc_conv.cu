@@ -158,6 +158,14 @@ __device__ __forceinline__ void trace_put(const TcConvParams& p, int unit, int f
     p.trace[(blockIdx.x * kTraceUnits + unit) * 16 + field] = clk();
 }
 
+// Per-K-step wait/issue cycle counters (trace fields 12-14): compiled only
+// with -DLCB_TC_TRACE (tests/cuda/tc_selftest), since the MMA warp is
+// issue-bound and the extra instructions cost ~3 % in the library build.
+#ifdef LCB_TC_TRACE
+#define TC_TRACE(...) __VA_ARGS__
+#else
+#define TC_TRACE(...)
+#endif
 __device__ __forceinline__ void trace_val(const TcConvParams& p, int unit, int field, unsigned long long v) {
   if (p.trace && blockIdx.x < kTraceCtas && unit < kTraceUnits) p.trace[(blockIdx.x * kTraceUnits + unit) * 16 + field] = v;
 }
@@ -722,11 +730,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
         const int img_j = __shfl_sync(0xffffffffu, my_img, jb < nbox ? jb : 0);
         const int nk_conv = p.ntaps * cchunks;
         int cc = x.s_begin % cchunks, tap = x.s_begin / cchunks;
-        unsigned long long pw = 0;  // trace: cycles spent waiting for free stages
+        TC_TRACE(unsigned long long pw = 0;)  // cycles spent waiting for free stages
         for (int s = x.s_begin; s < x.s_end; ++s) {
-          const unsigned long long c0 = p.trace ? clk() : 0;
+          TC_TRACE(const unsigned long long c0 = p.trace ? clk() : 0;)
           mbar_wait(empty0 + 8 * stage, phase ^ 1);
-          if (p.trace) pw += clk() - c0;
+          TC_TRACE(if (p.trace) pw += clk() - c0;)
           const uint32_t fb = full0 + 8 * stage;
           if (lane == 0) mbar_expect_tx(fb, dbg_noload ? 0u : static_cast<uint32_t>(Cfg::kStageBytes));
           __syncwarp();
@@ -778,7 +786,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
           }
         }
         if (lane == 0) trace_put(p, unit, 1);
-        if (lane == 0) trace_val(p, unit, 14, pw);
+        TC_TRACE(if (lane == 0) trace_val(p, unit, 14, pw);)
       }
     }
   } else if (warp == 1) {
@@ -799,12 +807,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
         if (lane == 0) trace_put(p, unit, 2);
         const uint32_t d_tmem = tmem_base + acc * Cfg::kAccCols;
         const int nk_conv = p.ntaps * (p.C / 64);
-        unsigned long long mw = 0, mi = 0;  // trace: cycles waiting for data / issuing + committing
+        TC_TRACE(unsigned long long mw = 0, mi = 0;)  // cycles waiting for data / issuing + committing
         for (int s = x.s_begin; s < x.s_end; ++s) {
-          const unsigned long long c0 = p.trace ? clk() : 0;
+          TC_TRACE(const unsigned long long c0 = p.trace ? clk() : 0;)
           mbar_wait(full0 + 8 * stage, phase);
           tc_fence_after();
-          const unsigned long long c1 = p.trace ? clk() : 0;
+          TC_TRACE(const unsigned long long c1 = p.trace ? clk() : 0;)
           const uint32_t ah = smem_u32(stage_a(stage, 0)), bh = smem_u32(stage_b(stage, 0));
           const bool res_step = s >= nk_conv;
           // K-advance of 16 bf16 = 32 bytes = +2 in the descriptor's address field
@@ -829,10 +837,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
             }
           }
           umma_commit_warp(empty0 + 8 * stage);
-          if (p.trace) {
+          TC_TRACE(if (p.trace) {
             mw += c1 - c0;
             mi += clk() - c1;
-          }
+          })
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
@@ -840,10 +848,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
         }
         umma_commit_warp(tfull0 + 8 * acc);
         if (lane == 0) trace_put(p, unit, 3);
-        if (lane == 0) {
+        TC_TRACE(if (lane == 0) {
           trace_val(p, unit, 12, mw);
           trace_val(p, unit, 13, mi);
-        }
+        })
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }

@@ -1,5 +1,5 @@
 // Standalone numerics + timing check for the tcgen05 implicit-GEMM kernel.
-// Build: nvcc -std=c++17 -O2 -gencode arch=compute_100a,code=sm_100a
+// Build: nvcc -std=c++17 -O2 -DLCB_TC_TRACE -gencode arch=compute_100a,code=sm_100a
 //        -I paper_2101_07344_b200/csrc/kernels tests/cuda/tc_selftest.cu
 //        paper_2101_07344_b200/csrc/kernels/tc_conv.cu -o tc_selftest
 // Compares against an fp64 CPU restatement of the same convolution.
