@@ -131,6 +131,79 @@ __device__ __forceinline__ void umma_bf16_warp(uint32_t tmem_d, uint64_t adesc, 
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// One 64-channel K-step of the stacked bf16x3 product (4 x K16): per K16 an
+// N = 2*BN MMA of A_hi against [B_hi; B_lo] and an N = BN MMA of A_lo against
+// B_hi, all under ONE elect.sync (the MMA warp is issue-bound: fewer
+// instructions per MMA). Descriptors advance by +2 (32 bytes) per K16.
+__device__ __forceinline__ void umma_kstep_x3_stacked(uint32_t tmem_d, uint64_t dah, uint64_t dal, uint64_t dbh,
+                                                      uint32_t idesc2, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e, t;\n\t.reg .b64 a1, a2, a3, l1, l2, l3, b1, b2, b3;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "setp.eq.b32 t, 0, 0;\n\t"
+      "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
+      "add.s64 l1, %2, 2;\n\tadd.s64 l2, %2, 4;\n\tadd.s64 l3, %2, 6;\n\t"
+      "add.s64 b1, %3, 2;\n\tadd.s64 b2, %3, 4;\n\tadd.s64 b3, %3, 6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %3, %4, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %3, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %4, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], l1, b1, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %4, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], l2, b2, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %4, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], l3, b3, %5, t;\n\t}" ::"r"(tmem_d),
+      "l"(dah), "l"(dal), "l"(dbh), "r"(idesc2), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// One 64-channel K-step of the unstacked bf16x3 product: per K16 hi*hi,
+// hi*lo and lo*hi at N = BN, under one elect.sync.
+__device__ __forceinline__ void umma_kstep_x3_plain(uint32_t tmem_d, uint64_t dah, uint64_t dal, uint64_t dbh,
+                                                    uint64_t dbl, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e, t;\n\t.reg .b64 a1, a2, a3, l1, l2, l3, b1, b2, b3, c1, c2, c3;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "setp.eq.b32 t, 0, 0;\n\t"
+      "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
+      "add.s64 l1, %2, 2;\n\tadd.s64 l2, %2, 4;\n\tadd.s64 l3, %2, 6;\n\t"
+      "add.s64 b1, %3, 2;\n\tadd.s64 b2, %3, 4;\n\tadd.s64 b3, %3, 6;\n\t"
+      "add.s64 c1, %4, 2;\n\tadd.s64 c2, %4, 4;\n\tadd.s64 c3, %4, 6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %3, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %4, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %3, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, c1, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], l1, b1, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, c2, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], l2, b2, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, c3, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], l3, b3, %5, t;\n\t}" ::"r"(tmem_d),
+      "l"(dah), "l"(dal), "l"(dbh), "l"(dbl), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// One 64-channel K-step of a single bf16 product (4 x K16), one elect.sync.
+__device__ __forceinline__ void umma_kstep_bf16(uint32_t tmem_d, uint64_t dah, uint64_t dbh, uint32_t idesc,
+                                                uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e, t;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.eq.b32 t, 0, 0;\n\t"
+      "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
+      "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, t;\n\t}" ::"r"(tmem_d),
+      "l"(dah), "l"(dbh), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 __device__ __forceinline__ void umma_commit_warp(uint32_t bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"

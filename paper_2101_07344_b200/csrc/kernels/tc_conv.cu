@@ -819,6 +819,16 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
           const uint64_t dah = umma_desc_sw128(ah), dbh = umma_desc_sw128(bh);
           const uint64_t dal = umma_desc_sw128(smem_u32(stage_a(stage, X3 ? 1 : 0)));
           const uint64_t dbl = umma_desc_sw128(smem_u32(stage_b(stage, X3 ? 1 : 0)));
+          // whole K-steps under one elect.sync (the MMA warp is issue-bound);
+          // LCB_DBG bit 16 keeps the per-MMA path for A/B measurements
+          const bool fused_issue = !dbg_nomma && !(p.dbg & 16);
+          if (fused_issue && stacked && !res_step) {
+            umma_kstep_x3_stacked(d_tmem, dah, dal, dbh, idesc2, idesc, s > x.s_begin ? 1u : 0u);
+          } else if (fused_issue && X3 && !res_step) {
+            umma_kstep_x3_plain(d_tmem, dah, dal, dbh, dbl, idesc, s > x.s_begin ? 1u : 0u);
+          } else if (fused_issue && !X3) {
+            umma_kstep_bf16(d_tmem, dah, dbh, idesc, s > x.s_begin ? 1u : 0u);
+          } else
 // (a runtime trip count here miscompiles the MMA sequence: keep it constant)
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
