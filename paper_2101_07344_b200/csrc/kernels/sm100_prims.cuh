@@ -131,12 +131,14 @@ __device__ __forceinline__ void umma_bf16_warp(uint32_t tmem_d, uint64_t adesc, 
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// The K-step helpers end with the tcgen05.commit that releases the stage
+// (same elected lane, no second elect.sync).
 // One 64-channel K-step of the stacked bf16x3 product (4 x K16): per K16 an
 // N = 2*BN MMA of A_hi against [B_hi; B_lo] and an N = BN MMA of A_lo against
 // B_hi, all under ONE elect.sync (the MMA warp is issue-bound: fewer
 // instructions per MMA). Descriptors advance by +2 (32 bytes) per K16.
 __device__ __forceinline__ void umma_kstep_x3_stacked(uint32_t tmem_d, uint64_t dah, uint64_t dal, uint64_t dbh,
-                                                      uint32_t idesc2, uint32_t idesc, uint32_t accumulate) {
+                                                      uint32_t idesc2, uint32_t idesc, uint32_t accumulate, uint32_t bar) {
   asm volatile(
       "{\n\t.reg .pred p, e, t;\n\t.reg .b64 a1, a2, a3, l1, l2, l3, b1, b2, b3;\n\t"
       "elect.sync _|e, 0xffffffff;\n\t"
@@ -152,15 +154,16 @@ __device__ __forceinline__ void umma_kstep_x3_stacked(uint32_t tmem_d, uint64_t 
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %4, t;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], l2, b2, %5, t;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %4, t;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], l3, b3, %5, t;\n\t}" ::"r"(tmem_d),
-      "l"(dah), "l"(dal), "l"(dbh), "r"(idesc2), "r"(idesc), "r"(accumulate)
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], l3, b3, %5, t;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%7];\n\t}" ::"r"(tmem_d),
+      "l"(dah), "l"(dal), "l"(dbh), "r"(idesc2), "r"(idesc), "r"(accumulate), "r"(bar)
       : "memory");
 }
 
 // One 64-channel K-step of the unstacked bf16x3 product: per K16 hi*hi,
 // hi*lo and lo*hi at N = BN, under one elect.sync.
 __device__ __forceinline__ void umma_kstep_x3_plain(uint32_t tmem_d, uint64_t dah, uint64_t dal, uint64_t dbh,
-                                                    uint64_t dbl, uint32_t idesc, uint32_t accumulate) {
+                                                    uint64_t dbl, uint32_t idesc, uint32_t accumulate, uint32_t bar) {
   asm volatile(
       "{\n\t.reg .pred p, e, t;\n\t.reg .b64 a1, a2, a3, l1, l2, l3, b1, b2, b3, c1, c2, c3;\n\t"
       "elect.sync _|e, 0xffffffff;\n\t"
@@ -181,14 +184,15 @@ __device__ __forceinline__ void umma_kstep_x3_plain(uint32_t tmem_d, uint64_t da
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], l2, b2, %5, t;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %5, t;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, c3, %5, t;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], l3, b3, %5, t;\n\t}" ::"r"(tmem_d),
-      "l"(dah), "l"(dal), "l"(dbh), "l"(dbl), "r"(idesc), "r"(accumulate)
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], l3, b3, %5, t;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%7];\n\t}" ::"r"(tmem_d),
+      "l"(dah), "l"(dal), "l"(dbh), "l"(dbl), "r"(idesc), "r"(accumulate), "r"(bar)
       : "memory");
 }
 
 // One 64-channel K-step of a single bf16 product (4 x K16), one elect.sync.
 __device__ __forceinline__ void umma_kstep_bf16(uint32_t tmem_d, uint64_t dah, uint64_t dbh, uint32_t idesc,
-                                                uint32_t accumulate) {
+                                                uint32_t accumulate, uint32_t bar) {
   asm volatile(
       "{\n\t.reg .pred p, e, t;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
       "elect.sync _|e, 0xffffffff;\n\t"
@@ -199,8 +203,9 @@ __device__ __forceinline__ void umma_kstep_bf16(uint32_t tmem_d, uint64_t dah, u
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, t;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, t;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, t;\n\t}" ::"r"(tmem_d),
-      "l"(dah), "l"(dbh), "r"(idesc), "r"(accumulate)
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, t;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n\t}" ::"r"(tmem_d),
+      "l"(dah), "l"(dbh), "r"(idesc), "r"(accumulate), "r"(bar)
       : "memory");
 }
 

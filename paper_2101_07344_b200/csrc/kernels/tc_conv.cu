@@ -800,6 +800,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
       int acc = 0;
       uint32_t acc_phase = 0;
       int unit = 0;
+      const uint64_t dah0 = umma_desc_sw128(smem_u32(stage_a(0, 0))), dbh0 = umma_desc_sw128(smem_u32(stage_b(0, 0)));
+      const uint64_t dal0 = umma_desc_sw128(smem_u32(stage_a(0, X3 ? 1 : 0)));
+      const uint64_t dbl0 = umma_desc_sw128(smem_u32(stage_b(0, X3 ? 1 : 0)));
       for (int t = blockIdx.x; t < g.total; t += gridDim.x, ++unit) {
         const Tile x = decode_tile(t, p, g);
         mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1);
@@ -813,22 +816,23 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
           mbar_wait(full0 + 8 * stage, phase);
           tc_fence_after();
           TC_TRACE(const unsigned long long c1 = p.trace ? clk() : 0;)
-          const uint32_t ah = smem_u32(stage_a(stage, 0)), bh = smem_u32(stage_b(stage, 0));
           const bool res_step = s >= nk_conv;
-          // K-advance of 16 bf16 = 32 bytes = +2 in the descriptor's address field
-          const uint64_t dah = umma_desc_sw128(ah), dbh = umma_desc_sw128(bh);
-          const uint64_t dal = umma_desc_sw128(smem_u32(stage_a(stage, X3 ? 1 : 0)));
-          const uint64_t dbl = umma_desc_sw128(smem_u32(stage_b(stage, X3 ? 1 : 0)));
+          // K-advance of 16 bf16 = 32 bytes = +2 in the descriptor's address
+          // field; stage k's operands sit k * kStageBytes further (< 256 KB,
+          // so the 14-bit address field never carries)
+          const uint64_t so = static_cast<uint64_t>(stage) * (Cfg::kStageBytes >> 4);
+          const uint64_t dah = dah0 + so, dbh = dbh0 + so, dal = dal0 + so, dbl = dbl0 + so;
           // whole K-steps under one elect.sync (the MMA warp is issue-bound);
           // LCB_DBG bit 16 keeps the per-MMA path for A/B measurements
           const bool fused_issue = !dbg_nomma && !(p.dbg & 16);
+          const uint32_t eb = empty0 + 8 * stage;
           if (fused_issue && stacked && !res_step) {
-            umma_kstep_x3_stacked(d_tmem, dah, dal, dbh, idesc2, idesc, s > x.s_begin ? 1u : 0u);
+            umma_kstep_x3_stacked(d_tmem, dah, dal, dbh, idesc2, idesc, s > x.s_begin ? 1u : 0u, eb);
           } else if (fused_issue && X3 && !res_step) {
-            umma_kstep_x3_plain(d_tmem, dah, dal, dbh, dbl, idesc, s > x.s_begin ? 1u : 0u);
+            umma_kstep_x3_plain(d_tmem, dah, dal, dbh, dbl, idesc, s > x.s_begin ? 1u : 0u, eb);
           } else if (fused_issue && !X3) {
-            umma_kstep_bf16(d_tmem, dah, dbh, idesc, s > x.s_begin ? 1u : 0u);
-          } else
+            umma_kstep_bf16(d_tmem, dah, dbh, idesc, s > x.s_begin ? 1u : 0u, eb);
+          } else {
 // (a runtime trip count here miscompiles the MMA sequence: keep it constant)
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
@@ -846,7 +850,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
               }
             }
           }
-          umma_commit_warp(empty0 + 8 * stage);
+          umma_commit_warp(eb);
+          }
           TC_TRACE(if (p.trace) {
             mw += c1 - c0;
             mi += clk() - c1;
