@@ -441,6 +441,7 @@ __device__ __noinline__ void split_reduce(const TcConvParams& p, const TileGeom&
           v[4 * u + 3] += f.w;
         }
       }
+      TC_TRACE(if (warp == 0 && lane == 0 && base == u0) trace_val(p, unit, 15, clk());)
       if (wpu > 1) {
 #pragma unroll
         for (int u = 0; u < 4; ++u)
@@ -465,6 +466,7 @@ __device__ __noinline__ void split_reduce(const TcConvParams& p, const TileGeom&
       const int co = x.tn * BN + c16 * 16;
       if (out_row(p, g, x, r, row_geom(p, r), ob, img, img_ok)) {
         epilogue_store_ld(p, v, ob + co, co);
+        TC_TRACE(if (warp == 0 && lane == 0 && base == u0) trace_val(p, unit, 12, clk());)
       } else {
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[i] = 0.0f;

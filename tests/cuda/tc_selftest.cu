@@ -575,9 +575,9 @@ static void perf_conv(const char* name, int N, int nsurv, int H, int W, int C, i
         if (!q[0] && !q[4]) break;
         auto rel = [&](unsigned long long v) { return v ? (long long)(v - t0) : -1LL; };
         printf("   %2d: %8lld %8lld | %8lld %8lld | %8lld %8lld | %8lld %8lld | red %8lld w0 %8lld w1 %8lld end %8lld"
-               " | mma wait %6llu issue %6llu | tma wait %6llu\n",
+               " | mma wait %6llu issue %6llu | tma wait %6llu | red loads %lld stored %lld\n",
                u, rel(q[0]), rel(q[1]), rel(q[2]), rel(q[3]), rel(q[4]), rel(q[5]), rel(q[6]), rel(q[7]), rel(q[8]),
-               rel(q[9]), rel(q[10]), rel(q[11]), q[12], q[13], q[14]);
+               rel(q[9]), rel(q[10]), rel(q[11]), q[12], q[13], q[14], rel(q[15]), q[15] ? rel(q[12]) : -1LL);
       }
     }
   }
