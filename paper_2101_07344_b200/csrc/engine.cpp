@@ -204,6 +204,7 @@ Engine::Engine(int device, const BaseModel& model, std::vector<CacheVariant> var
   const char* ns = std::getenv("LCB_NO_STACKED");
   stacked_ = !(ns && ns[0] == '1');
   if (const char* km = std::getenv("LCB_KS_MIN_STEPS")) ks_min_steps_ = std::atoi(km);
+  if (const char* wp = std::getenv("LCB_NO_WPREFETCH")) wprefetch_ = !(wp[0] == '1');
   const char* nh = std::getenv("LCB_HALO");  // opt-in: not yet faster than the per-tap loads
   halo_ = nh && nh[0] == '1';
   const char* nr = std::getenv("LCB_NO_MMA_RESIDUAL");
@@ -854,6 +855,11 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow) {
       prm->ksplit = 1;
       prm->ks_max = 32;
       prm->ks_min_steps = ks_min_steps_;
+      if (wprefetch_) {
+        prm->wpre[0] = dc.w.hi;
+        prm->wpre[1] = dc.w.lo;
+        prm->wpre_bytes = static_cast<long long>(o.Cout) * dc.Kp * 2;
+      }
       prm->ws = ws_;
       prm->ws_counters = ws_counters_;
       prm->surv = cur_ids;

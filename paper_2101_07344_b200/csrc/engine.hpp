@@ -197,7 +197,8 @@ class Engine {
   __nv_bfloat16* identity_ = nullptr;
   bool fused_lookup_ = true;
   bool stacked_ = true;
-  int ks_min_steps_ = 0;  // LCB_KS_MIN_STEPS: split-K floor of K-steps per split (CNN convs)  // LCB_NO_STACKED=1: three MMAs per bf16x3 K16 group everywhere
+  int ks_min_steps_ = 0;
+  bool wprefetch_ = true;  // LCB_NO_WPREFETCH=1: no L2 prefetch of conv weights before the PDL wait  // LCB_KS_MIN_STEPS: split-K floor of K-steps per split (CNN convs)  // LCB_NO_STACKED=1: three MMAs per bf16x3 K16 group everywhere
   bool halo_ = false;  // LCB_HALO=1: stride-1 convs load one padded-row halo slab per channel chunk  // LCB_UNFUSED_LOOKUP=1: gap_bins + head + exit_compact as three launches
   int* lk_arrive_ = nullptr;
   Planes im2col_buf_;

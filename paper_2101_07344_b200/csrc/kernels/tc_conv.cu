@@ -547,6 +547,23 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  // weights do not depend on upstream kernels: warm L2 with this CTA's share
+  // while the previous kernel drains (short split-K units otherwise wait on
+  // first-touch HBM latency for every B box)
+  if (warp == 0 && p.wpre_bytes > 0) {
+    const long long chunk = ((p.wpre_bytes + gridDim.x - 1) / gridDim.x + 15) & ~15LL;
+    const long long off = static_cast<long long>(blockIdx.x) * chunk;
+    if (off < p.wpre_bytes) {
+      const long long len = p.wpre_bytes - off < chunk ? p.wpre_bytes - off : chunk;
+      if (lane < (X3 ? 2 : 1) && p.wpre[lane]) {
+        const char* base = static_cast<const char*>(p.wpre[lane]) + off;
+        for (long long o = 0; o < len; o += 65536) {
+          const unsigned n = static_cast<unsigned>(len - o < 65536 ? len - o : 65536);
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + o), "r"(n) : "memory");
+        }
+      }
+    }
+  }
   // everything above is independent of upstream kernels (programmatic launch)
   pdl_wait();
   pdl_trigger();

@@ -87,6 +87,10 @@ struct TcConvParams {
   float* gap_out;      // nullable: fused GAP partials [image][gap_segs][Cout] (NHWC conv mode only)
   int gap_segs;        // segments per image = tiles_h * tiles_w * max(1, hb*wb/32)
   unsigned long long* trace;  // nullable debug: clock64 stamps [8 CTAs][32 units][8]
+  // Weight planes to pull into L2 before the programmatic-launch wait (they do
+  // not depend on upstream kernels): each CTA prefetches 1/grid of each plane.
+  const void* wpre[2];
+  long long wpre_bytes;        // bytes per plane (0 = off)
   signed char tap_phase[kMaxTaps];
   signed char tap_dh[kMaxTaps];
   signed char tap_dw[kMaxTaps];
