@@ -485,6 +485,17 @@ __global__ void __launch_bounds__(256) rows_fc_kernel(const float* __restrict__ 
                                                       long long part_stride, const float* __restrict__ b1, int feat,
                                                       int kslice, const float* __restrict__ W, int classes,
                                                       const int* count, long long max_rows, float* out) {
+  {
+    // the weight slice this CTA multiplies does not depend on upstream
+    // kernels: pull it into L2 while the producer of A drains (one row of W
+    // per thread, 16-byte aligned rows only)
+    const int k = blockIdx.x * kFcBN + static_cast<int>(threadIdx.x);
+    const int oz0 = blockIdx.z * kslice, oz1 = oz0 + kslice < feat ? oz0 + kslice : feat;
+    if (threadIdx.x < kFcBN && k < classes && (feat & 3) == 0 && oz1 > oz0)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(W + static_cast<long long>(k) * feat + oz0),
+                   "r"(static_cast<unsigned>((oz1 - oz0) * 4))
+                   : "memory");
+  }
   pdl_wait();
   pdl_trigger();
   __shared__ __align__(16) float As[kFcBK][kFcBM + 4];
