@@ -43,3 +43,14 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
 }
 
 }  // namespace lcb
+
+// Per-device one-time setup (cudaFuncSetAttribute applies to the current
+// device only): true the first time it is called on each device.
+#include <atomic>
+inline bool first_on_device(std::atomic<unsigned long long>& done) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return true;
+  const unsigned long long bit = 1ull << dev;
+  return (done.fetch_or(bit) & bit) == 0;
+}
+

@@ -1174,11 +1174,9 @@ void launch_conv1d_partials(const TapView& tap, int max_rows, long long D, int k
                             float* partials, cudaStream_t s) {
   if (max_rows <= 0) return;
   const size_t smem = static_cast<size_t>(chunk_elems + kernel) * sizeof(float);
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr))
     cudaFuncSetAttribute(conv1d_partials_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
   launch_pdl(conv1d_partials_kernel, dim3(dim3(max_rows, nchunks)), dim3(256), smem, s, tap, D, kernel, stride, out_dim, w1, b1, W2,
                                                                     classes, chunk_elems, nchunks, partials);
 }
@@ -1218,11 +1216,9 @@ void launch_cache_head(const CacheHeadParams& p_in, int max_rows, cudaStream_t s
   const int feat_len = (p.family == 2 || p.pre_logits) ? p.classes : (p.feat > p.classes ? p.feat : p.classes);
   size_t smem = static_cast<size_t>(p.classes + feat_len) * sizeof(float);
   if (head_stages_weights(p)) smem += static_cast<size_t>(p.classes) * (p.feat + 16) * sizeof(float);  // W2 + Ws1
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr))
     cudaFuncSetAttribute(cache_head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    attr = true;
-  }
   launch_pdl(cache_head_kernel, dim3(max_rows), dim3(kLk), smem, s, p);
 }
 

@@ -1079,12 +1079,11 @@ EncodeTiledFn encode_fn() {
 template <int BN, bool X3>
 cudaError_t launch_cfg(const TcConvParams& p, int num_sms, cudaStream_t stream) {
   using Cfg = TcCfg<BN, X3>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static std::atomic<unsigned long long> attr_set{0};
+  if (first_on_device(attr_set)) {
     cudaError_t e =
         cudaFuncSetAttribute(tc_conv_kernel<BN, X3>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   long long tiles = tc_conv_max_tiles(p, BN);
   if (p.mode == 0 && p.ks_max > 1) tiles *= p.ks_max;
