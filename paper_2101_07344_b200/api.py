@@ -677,6 +677,14 @@ def run_adaptation(dep: Deployment, inputs: np.ndarray, labels: Sequence[int], s
     oy = np.ascontiguousarray(original_y, np.float64)
     N0 = oy.shape[0] if oy.ndim == 2 else 0
     ot = [np.ascontiguousarray(t, np.float64) for t in original_taps]
+    if N0:  # the C-ABI reads N0 rows of every attached cache's tap array
+        if len(ot) != len(dep.variants):
+            raise ValueError("run_adaptation: one original tap array per attached cache is required")
+        for t, v in zip(ot, dep.variants):
+            if t.shape != (N0, dep.model.tap_dim(v.layer)):
+                raise ValueError("run_adaptation: original record shape mismatch")
+        if oy.shape[1] != dep.classes:
+            raise ValueError("run_adaptation: original record shape mismatch")
     tp = (C.POINTER(C.c_double) * max(1, len(ot)))(*[_dptr(t) for t in ot])
     c = AdaptConfig(cfg.sample_rate, cfg.window_min, cfg.retrain_interval_min, cfg.recency_decay,
                     cfg.mixin_fraction, cfg.epochs, cfg.learning_rate, cfg.retrain_pause_ms, cfg.tau, cfg.beta,

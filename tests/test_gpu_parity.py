@@ -706,6 +706,12 @@ def test_run_adaptation_frozen_matches_serve():
     assert np.array_equal(np.array([t.served_pred for t in res.traces[:128]]), sh.served)
     for f, t in zip(res.final_variants, vtxt):
         assert f.save() == lcb.load_variant(t).save()
+    with pytest.raises(ValueError):  # original records must cover every attached cache
+        lcb.run_adaptation(dep, X, labels, stream, lcb.AdaptationConfig(), [np.zeros((4, 3))],
+                           np.zeros((4, m.num_classes)), seed=1)
+    with pytest.raises(ValueError):  # invalid config -> the reference's invalid_argument
+        lcb.run_adaptation(dep, X, labels, stream, lcb.AdaptationConfig(sample_rate=1.5), [np.zeros((0, 1))] * len(vs),
+                           np.zeros((0, m.num_classes)), seed=1)
     dep.close()
 
 
