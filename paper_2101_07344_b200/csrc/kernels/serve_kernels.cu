@@ -603,8 +603,14 @@ __device__ void block_logits(const float* __restrict__ W, const float* __restric
 }
 
 // Fused-GAP heads stage W2 + Ws1 in shared memory when they fit (48 KB).
+// Heads that do not stage W2 still stage the selector's first layer (16 x C)
+// before the wait when it fits (<= 64 KB): one L2 round trip off the tail.
+__host__ __device__ inline bool head_stages_ws1(const CacheHeadParams& p);
 __host__ __device__ inline bool head_stages_weights(const CacheHeadParams& p) {
   return p.gap != nullptr && p.classes * (p.feat + 16) <= 12288;
+}
+__host__ __device__ inline bool head_stages_ws1(const CacheHeadParams& p) {
+  return !head_stages_weights(p) && p.classes <= 1024;
 }
 
 // Shared scratch of one row's head.
@@ -778,10 +784,15 @@ __global__ void __launch_bounds__(kLk) cache_head_kernel(CacheHeadParams p) {
   // shared memory BEFORE the programmatic-launch wait, i.e. while the tap's
   // conv is still draining (launch_cache_head sizes the region)
   const bool stage_w = head_stages_weights(p);
-  float* w2s = feat + (p.feat > C ? p.feat : C);  // [C][feat]
-  float* ws1s = w2s + C * p.feat;                 // [16][C]
+  // same extent as launch_cache_head's feat_len
+  const int feat_len = (p.family == 2 || p.pre_logits) ? C : (p.feat > C ? p.feat : C);
+  float* w2s = feat + feat_len;                    // [C][feat]
+  const bool stage_s = head_stages_ws1(p);
+  float* ws1s = stage_w ? w2s + C * p.feat : w2s;  // [16][C]
   if (stage_w) {
     for (int i = tid; i < C * p.feat; i += kLk) w2s[i] = __ldg(p.W2 + i);
+  }
+  if (stage_w || stage_s) {
     for (int i = tid; i < 16 * C; i += kLk) ws1s[i] = __ldg(p.Ws1 + i);
   }
   pdl_wait();
@@ -818,7 +829,7 @@ __global__ void __launch_bounds__(kLk) cache_head_kernel(CacheHeadParams p) {
         block_logits(p.W2, p.b2, C, p.feat, feat, logits);
     }
     __syncthreads();
-    head_block(p, r, logits, feat, hs, stage_w ? ws1s : p.Ws1);
+    head_block(p, r, logits, feat, hs, (stage_w || stage_s) ? ws1s : p.Ws1);
   }
   if (p.ex.arrive) exit_tail(p.ex, n, p.prob, p.hit, p.label);
 }
@@ -1216,6 +1227,7 @@ void launch_cache_head(const CacheHeadParams& p_in, int max_rows, cudaStream_t s
   const int feat_len = (p.family == 2 || p.pre_logits) ? p.classes : (p.feat > p.classes ? p.feat : p.classes);
   size_t smem = static_cast<size_t>(p.classes + feat_len) * sizeof(float);
   if (head_stages_weights(p)) smem += static_cast<size_t>(p.classes) * (p.feat + 16) * sizeof(float);  // W2 + Ws1
+  else if (head_stages_ws1(p)) smem += static_cast<size_t>(p.classes) * 16 * sizeof(float);          // Ws1
   static std::atomic<unsigned long long> attr{0};
   if (first_on_device(attr))
     cudaFuncSetAttribute(cache_head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
