@@ -610,7 +610,9 @@ __host__ __device__ inline bool head_stages_weights(const CacheHeadParams& p) {
   return p.gap != nullptr && p.classes * (p.feat + 16) <= 12288;
 }
 __host__ __device__ inline bool head_stages_ws1(const CacheHeadParams& p) {
-  return !head_stages_weights(p) && p.classes <= 1024;
+  // batch-sized launches only: with a handful of rows the copy is not hidden
+  // behind the upstream kernel and the selector reads L2 directly anyway
+  return !head_stages_weights(p) && p.classes <= 1024 && p.rows_total >= 32;
 }
 
 // Shared scratch of one row's head.
@@ -771,6 +773,18 @@ __device__ void exit_tail(const ExitParams& e, int n, const float* prob, const i
 // split-K GEMM partials, the fused GAP partials (Pool(C), classes <= 32),
 // the Conv(k,s) chunk partials, or the pooled bins / FC(h) hidden partials.
 // With p.ex.arrive the last CTA also runs the exit + compaction.
+// Global -> shared copy of n floats by one kLk-thread CTA: 16-byte loads, 4 in
+// flight per thread (a scalar loop is a chain of L2 round trips when the copy
+// lands on the critical path, e.g. batch-1 serving).
+__device__ __forceinline__ void stage_floats(float* dst, const float* __restrict__ src, int n, int tid) {
+  const int n4 = (reinterpret_cast<uintptr_t>(src) & 15) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0 ? n / 4 : 0;
+  const float4* s4 = reinterpret_cast<const float4*>(src);
+  float4* d4 = reinterpret_cast<float4*>(dst);
+#pragma unroll 4
+  for (int i = tid; i < n4; i += kLk) d4[i] = __ldg(s4 + i);
+  for (int i = 4 * n4 + tid; i < n; i += kLk) dst[i] = __ldg(src + i);
+}
+
 __global__ void __launch_bounds__(kLk) cache_head_kernel(CacheHeadParams p) {
   extern __shared__ float sm[];
   __shared__ HeadSmem hs;
@@ -789,12 +803,8 @@ __global__ void __launch_bounds__(kLk) cache_head_kernel(CacheHeadParams p) {
   float* w2s = feat + feat_len;                    // [C][feat]
   const bool stage_s = head_stages_ws1(p);
   float* ws1s = stage_w ? w2s + C * p.feat : w2s;  // [16][C]
-  if (stage_w) {
-    for (int i = tid; i < C * p.feat; i += kLk) w2s[i] = __ldg(p.W2 + i);
-  }
-  if (stage_w || stage_s) {
-    for (int i = tid; i < 16 * C; i += kLk) ws1s[i] = __ldg(p.Ws1 + i);
-  }
+  if (stage_w) stage_floats(w2s, p.W2, C * p.feat, tid);
+  if (stage_w || stage_s) stage_floats(ws1s, p.Ws1, 16 * C, tid);
   pdl_wait();
   pdl_trigger();
   const int n = *p.count;
