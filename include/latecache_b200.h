@@ -147,24 +147,34 @@ int lc_engine_stage_input(lc_engine* e, const float* src, int B, int on_device);
  * end to end from HOST buffers: inputs [B][input_dim] fp32 in; per request
  * exit_layer (0 = miss, served by the base model), served label, base label
  * (-1 where compaction skipped the full pass), selector probability per
- * probed layer probs [blocks][B] (NaN = not probed), device-timed latency
- * (ms from batch start to the request's exit). Output pointers are nullable. */
+ * probed layer probs [blocks][B] (NaN = not probed), the base model's logits
+ * [B][classes] (pre-softmax head output, the reference's
+ * forward().activations[size-2], network.hpp:57-60; NaN rows where compaction
+ * skipped the full pass), device-timed latency (ms from batch start to the
+ * request's exit). Output pointers are nullable. */
 int lc_serve_batch(lc_engine* e, const float* inputs, int B, unsigned flags, int* exit_layer, int* served,
-                   int* base_pred, float* probs, double* latency_ms);
+                   int* base_pred, float* probs, float* logits, double* latency_ms);
 /* Pipelined form of lc_serve_batch (two slots): submit enqueues the H2D copy
  * of `inputs` (pinned host memory for a truly asynchronous copy) on a copy
  * stream, the serve and the result D2H on the engine stream, and returns at
- * once with the slot id; the next submit's upload overlaps this batch's
- * compute. collect waits for the slot and returns the lc_serve_batch outputs.
- * A slot must be collected before its next reuse (else its results are dropped). */
-int lc_serve_submit(lc_engine* e, const float* inputs, int B, unsigned flags, int* slot);
-int lc_serve_collect(lc_engine* e, int slot, int B, int* exit_layer, int* served, int* base_pred, float* probs,
-                     double* latency_ms);
+ * once with a ticket; the next submit's upload overlaps this batch's
+ * compute. collect waits for the ticket's batch and returns the lc_serve_batch
+ * outputs. A slot must be collected before its next reuse: a third submit
+ * drops the uncollected batch and its ticket then fails with
+ * LC_ERR_INVALID_ARGUMENT. */
+int lc_serve_submit(lc_engine* e, const float* inputs, int B, unsigned flags, int* ticket);
+int lc_serve_collect(lc_engine* e, int ticket, int B, int* exit_layer, int* served, int* base_pred, float* probs,
+                     float* logits, double* latency_ms);
 /* Same, input already in lc_engine_input(); enqueued asynchronously. */
 int lc_serve_device(lc_engine* e, int B, unsigned flags);
 int lc_engine_sync(lc_engine* e);
-int lc_engine_results(lc_engine* e, int B, int* exit_layer, int* served, int* base_pred, float* probs,
+int lc_engine_results(lc_engine* e, int B, int* exit_layer, int* served, int* base_pred, float* probs, float* logits,
                       double* latency_ms);
+/* forward_with_taps (base_model.cpp:56-63) tap read-back: runs the B host
+ * requests in shadow mode up to block `layer` and returns that block's tap
+ * as the reference's caches see it, out [B][tap_dim] fp32 NCHW-flat (the
+ * device's hi + lo planes summed). */
+int lc_engine_read_tap(lc_engine* e, const float* inputs, int B, int layer, float* out);
 /* Surviving requests after each block: counts[0..blocks] (counts[0] = B). */
 int lc_engine_counts(lc_engine* e, int* counts);
 
@@ -228,8 +238,8 @@ typedef struct lc_retrain_event {
 /* Request i (time-ordered) serves samples[req_sample[i]] (inputs [n_samples][input_dim]). Serving runs in shadow batches of up to max_batch
  * requests between swap/retrain points; sampled requests' taps at the attached
  * caches' layers and base distributions come back from the device as the
- * window records. original_taps[k] = [N0][tap_dim of attached cache k] (attach
- * order), original_y [N0][classes]: the original training records (mix-in).
+ * window records. original_taps[k] = [N0][tap_dim of attached cache k] (probe
+ * order: ascending layer, as make_plan sorts), original_y [N0][classes]: the original training records (mix-in).
  * Retrains run on the GPU (lc_train_predictor/selector) and swap in with
  * lc_engine_update_variant. Outputs per request: hit_layer (0 = miss), served,
  * base_pred, latency_ms (device time within its batch); events[<= events_cap],
@@ -239,7 +249,7 @@ int lc_run_adaptation(lc_engine* e, const float* inputs, int n_samples, const do
                       const int* req_sample, int R, const lc_adapt_config* cfg, const double* const* original_taps,
                       const double* original_y, int N0, uint64_t seed, int adapt_on, int* hit_layer, int* served,
                       int* base_pred, double* latency_ms, lc_retrain_event* events, int events_cap, int* n_events);
-/* Copy of the engine's k-th attached variant (attach order), e.g. the final
+/* Copy of the engine's k-th attached variant (probe order: ascending layer), e.g. the final
  * variants after lc_run_adaptation. */
 int lc_engine_variant(lc_engine* e, int k, lc_variant** out);
 

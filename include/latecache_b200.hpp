@@ -251,7 +251,7 @@ class Deployment {
       std::vector<int> exit_layer(B), served(B), base(B);
       std::vector<double> lat(B);
       check(lc_serve_batch(h_.get(), x.data(), B, shadow ? LC_SERVE_SHADOW : 0u, exit_layer.data(), served.data(),
-                           base.data(), nullptr, lat.data()));
+                           base.data(), nullptr, nullptr, lat.data()));
       for (int i = 0; i < B; ++i) {
         RequestTrace t;
         t.id = static_cast<long long>(s) + i;

@@ -454,6 +454,32 @@ def oracle_serve_mlp(model: dict, caches: Sequence[tuple], x: np.ndarray):
     return exit_l, served, base_p, probs
 
 
+def oracle_mlp_forward(model: dict, x: np.ndarray):
+    """forward() over a parsed make_base_model network (network.cpp:104-164) with
+    every activation kept: per block the post-ReLU tap (base_model.cpp:56-63,
+    tap_layers) and the base logits = activations[size-2] (network.hpp:57-60).
+    Returns (taps [blocks] -> [B][width], logits [B][classes])."""
+    net = OracleNet(model["layers"])
+    layers = model["layers"]
+    offs = [layers[0]["in_dim"]]
+    for l in layers:
+        offs.append(offs[-1] + l["out_dim"])
+    X = np.ascontiguousarray(x, np.float64)
+    B = X.shape[0]
+    taps = [np.zeros((B, model["tap_dims"][k]), np.float64) for k in range(model["blocks"])]
+    logits = np.zeros((B, model["classes"]), np.float64)
+    acts = np.zeros(offs[-1], np.float64)
+    out = np.zeros(layers[-1]["out_dim"], np.float64)
+    n = len(layers)
+    for i in range(B):
+        row = np.ascontiguousarray(X[i])
+        assert orc().lco_forward(net.ptr, net.n, _dp(row), _dp(out), _dp(acts)) == 0
+        for k, t in enumerate(model["tap_layers"]):
+            taps[k][i] = acts[offs[t]:offs[t] + layers[t]["out_dim"]]
+        logits[i] = acts[offs[n - 2]:offs[n - 2] + layers[n - 2]["out_dim"]]
+    return taps, logits
+
+
 def oracle_cnn_forward(ops: List[dict], nslots: int, x: np.ndarray, ntaps: int, tap_dims: Sequence[int],
                        classes: int, threads: int = 1):
     """lco_cnn_forward over the product's CNN op list (fp64, NCHW).

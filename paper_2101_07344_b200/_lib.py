@@ -97,10 +97,11 @@ def _load() -> C.CDLL:
         "lc_engine_set_delta": (I, [P, I, D]),
         "lc_engine_set_selector_out": (I, [P, I, D, D]),
         "lc_engine_input": (I, [P, C.POINTER(P)]),
-        "lc_serve_batch": (I, [P, pF, I, C.c_uint, pI, pI, pI, pF, pD]),
+        "lc_serve_batch": (I, [P, pF, I, C.c_uint, pI, pI, pI, pF, pF, pD]),
         "lc_serve_device": (I, [P, I, C.c_uint]),
         "lc_engine_sync": (I, [P]),
-        "lc_engine_results": (I, [P, I, pI, pI, pI, pF, pD]),
+        "lc_engine_results": (I, [P, I, pI, pI, pI, pF, pF, pD]),
+        "lc_engine_read_tap": (I, [P, pF, I, I, pF]),
         "lc_engine_counts": (I, [P, pI]),
         "lc_lookup_batch": (I, [P, I, pF, I, pI, pI, pF, pF, pF]),
         "lc_measure_metrics": (I, [P, pF, I, pD, I, C.POINTER(C.c_longlong)]),
@@ -110,7 +111,7 @@ def _load() -> C.CDLL:
         "lc_model_load_binary": (I, [C.c_char_p, C.c_size_t, C.POINTER(C.c_void_p)]),
         "lc_variant_save_binary": (I, [P, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t)]),
         "lc_variant_load_binary": (I, [C.c_char_p, C.c_size_t, C.POINTER(C.c_void_p)]),
-        "lc_serve_collect": (I, [P, I, I, pI, pI, pI, pF, pD]),
+        "lc_serve_collect": (I, [P, I, I, pI, pI, pI, pF, pF, pD]),
         "lc_tune_delta": (I, [P, pF, I, C.c_double, pD, I, pD, I]),
         "lc_train_predictor": (I, [I, P, pD, C.c_longlong, pD, I, I, pD, D, D, I, I, C.c_uint64, D, D]),
         "lc_train_selector": (I, [I, P, pD, C.c_longlong, pD, I, I, pD, D, D, I, I, C.c_uint64, D, D]),
@@ -173,4 +174,5 @@ EXPORTED_SYMBOLS = [
     "lc_measure_metrics", "lc_tune_delta", "lc_train_predictor", "lc_train_selector", "lc_engine_update_variant",
     "lc_run_adaptation", "lc_engine_variant", "lc_serve_submit", "lc_serve_collect", "lc_engine_layer_times",
     "lc_model_save_binary", "lc_model_load_binary", "lc_variant_save_binary", "lc_variant_load_binary",
+    "lc_engine_read_tap",
 ]

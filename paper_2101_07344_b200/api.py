@@ -305,6 +305,7 @@ class ServeResult:
     base_pred: np.ndarray   # -1 where compaction skipped the full pass
     probs: np.ndarray       # [blocks][B] selector probability per probed layer (NaN = not probed)
     latency_ms: np.ndarray  # device time from batch start to the request's exit
+    logits: np.ndarray = None  # [B][classes] base logits (NaN rows where compaction skipped the full pass)
 
 
 class Deployment:
@@ -317,7 +318,10 @@ class Deployment:
         check(lib.lc_engine_create(device, model._h, arr, len(variants), _PREC[precision], max_batch, C.byref(h)))
         self._h = h
         self.model = model
-        self.variants = list(variants)
+        # the engine probes (and indexes) its caches in ascending layer order
+        # (make_plan, composer.cpp:65-89); keep the same order here so every
+        # per-cache array (run_adaptation's original_taps, variant(k)) lines up
+        self.variants = sorted(variants, key=lambda v: v.layer)
         self.precision = precision
         self.max_batch = max_batch
         self.blocks = model.num_blocks
@@ -347,7 +351,7 @@ class Deployment:
         check(lib.lc_engine_update_variant(self._h, variant._h))
 
     def variant(self, k: int) -> CacheVariant:
-        """Copy of the k-th attached variant (attach order) as the engine holds it."""
+        """Copy of the k-th attached variant (probe order: ascending layer) as the engine holds it."""
         h = C.c_void_p()
         check(lib.lc_engine_variant(self._h, k, C.byref(h)))
         return CacheVariant(h)
@@ -364,10 +368,21 @@ class Deployment:
         sv = np.zeros(B, np.int32)
         bp = np.zeros(B, np.int32)
         pr = np.zeros((self.blocks, B), np.float32)
+        lg = np.zeros((B, self.classes), np.float32)
         lat = np.zeros(B, np.float64)
         flags = (LC_SERVE_SHADOW if shadow else 0) | (0 if graph else LC_SERVE_NO_GRAPH)
-        check(lib.lc_serve_batch(self._h, _fptr(x), B, flags, _iptr(el), _iptr(sv), _iptr(bp), _fptr(pr), _dptr(lat)))
-        return ServeResult(el, sv, bp, pr, lat)
+        check(lib.lc_serve_batch(self._h, _fptr(x), B, flags, _iptr(el), _iptr(sv), _iptr(bp), _fptr(pr), _fptr(lg),
+                                 _dptr(lat)))
+        return ServeResult(el, sv, bp, pr, lat, lg)
+
+    def read_tap(self, inputs: np.ndarray, layer: int) -> np.ndarray:
+        """forward_with_taps (base_model.cpp:56-63): the tap of block `layer` for
+        each input, [B][tap_dim] fp32 NCHW-flat, as the reference's caches see it."""
+        x = np.ascontiguousarray(inputs, dtype=np.float32)
+        B = x.shape[0]
+        out = np.zeros((B, self.model.tap_dim(layer)), np.float32)
+        check(lib.lc_engine_read_tap(self._h, _fptr(x), B, layer, _fptr(out)))
+        return out
 
     def submit(self, inputs: np.ndarray, shadow: bool = False) -> tuple:
         """Pipelined serve: enqueue one batch (H2D on a copy stream overlapping the
@@ -385,9 +400,11 @@ class Deployment:
         sv = np.zeros(B, np.int32)
         bp = np.zeros(B, np.int32)
         pr = np.zeros((self.blocks, B), np.float32)
+        lg = np.zeros((B, self.classes), np.float32)
         lat = np.zeros(B, np.float64)
-        check(lib.lc_serve_collect(self._h, slot, B, _iptr(el), _iptr(sv), _iptr(bp), _fptr(pr), _dptr(lat)))
-        return ServeResult(el, sv, bp, pr, lat)
+        check(lib.lc_serve_collect(self._h, slot, B, _iptr(el), _iptr(sv), _iptr(bp), _fptr(pr), _fptr(lg),
+                                   _dptr(lat)))
+        return ServeResult(el, sv, bp, pr, lat, lg)
 
     def stage_input_device(self, src_ptr: int, B: int) -> None:
         """Copy B inputs from device memory (raw pointer) into the engine's input buffer."""
@@ -411,9 +428,10 @@ class Deployment:
         sv = np.zeros(B, np.int32)
         bp = np.zeros(B, np.int32)
         pr = np.zeros((self.blocks, B), np.float32)
+        lg = np.zeros((B, self.classes), np.float32)
         lat = np.zeros(B, np.float64)
-        check(lib.lc_engine_results(self._h, B, _iptr(el), _iptr(sv), _iptr(bp), _fptr(pr), _dptr(lat)))
-        return ServeResult(el, sv, bp, pr, lat)
+        check(lib.lc_engine_results(self._h, B, _iptr(el), _iptr(sv), _iptr(bp), _fptr(pr), _fptr(lg), _dptr(lat)))
+        return ServeResult(el, sv, bp, pr, lat, lg)
 
     def counts(self) -> np.ndarray:
         c = np.zeros(self.blocks + 1, np.int32)
@@ -668,7 +686,8 @@ def run_adaptation(dep: Deployment, inputs: np.ndarray, labels: Sequence[int], s
     """run_adaptation (serving.cpp:213-340) on the GPU: shadow-batched serving
     between control points, window records read back from the device, GPU
     retraining and in-place swaps. original_taps[k] = [N0][D_k] for the k-th
-    attached cache, original_y [N0][C]. The engine ends holding the final
+    attached cache in probe order (ascending layer, = dep.variants[k]),
+    original_y [N0][C]. The engine ends holding the final
     variants (also returned)."""
     x = np.ascontiguousarray(inputs, np.float32)
     R = len(stream)

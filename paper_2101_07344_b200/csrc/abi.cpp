@@ -456,6 +456,9 @@ int lc_engine_stage_input(lc_engine* e, const float* src, int B, int on_device) 
     lcb::Engine& en = eng(e);
     if (B <= 0 || B > en.max_batch()) throw std::invalid_argument("stage_input: batch outside [1, max_batch]");
     const size_t bytes = static_cast<size_t>(B) * static_cast<size_t>(en.input_dim()) * sizeof(float);
+    // a device source was written by the caller's own streams (torch's, say),
+    // which the engine's non-blocking stream is not ordered after
+    if (on_device && cudaDeviceSynchronize() != cudaSuccess) throw lcb::CudaFailure("stage_input: device sync failed");
     if (cudaSetDevice(en.device()) != cudaSuccess ||
         cudaMemcpyAsync(en.input_buffer(), src, bytes, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                         en.stream()) != cudaSuccess ||
@@ -465,12 +468,12 @@ int lc_engine_stage_input(lc_engine* e, const float* src, int B, int on_device) 
 }
 
 int lc_serve_batch(lc_engine* e, const float* inputs, int B, unsigned flags, int* exit_layer, int* served,
-                   int* base_pred, float* probs, double* latency_ms) {
+                   int* base_pred, float* probs, float* logits, double* latency_ms) {
   return guard([&] {
     need(inputs, "inputs");
     lcb::Engine& en = eng(e);
     en.serve_host(inputs, B, (flags & LC_SERVE_SHADOW) != 0, (flags & LC_SERVE_NO_GRAPH) == 0);
-    en.copy_results(B, exit_layer, served, base_pred, probs, latency_ms);
+    en.copy_results(B, exit_layer, served, base_pred, probs, logits, latency_ms);
   });
 }
 
@@ -667,8 +670,9 @@ int lc_serve_submit(lc_engine* e, const float* inputs, int B, unsigned flags, in
 }
 
 int lc_serve_collect(lc_engine* e, int slot, int B, int* exit_layer, int* served, int* base_pred, float* probs,
+                     float* logits,
                      double* latency_ms) {
-  return guard([&] { eng(e).collect(slot, B, exit_layer, served, base_pred, probs, latency_ms); });
+  return guard([&] { eng(e).collect(slot, B, exit_layer, served, base_pred, probs, logits, latency_ms); });
 }
 
 int lc_serve_device(lc_engine* e, int B, unsigned flags) {
@@ -679,12 +683,26 @@ int lc_engine_sync(lc_engine* e) {
   return guard([&] { eng(e).synchronize(); });
 }
 
-int lc_engine_results(lc_engine* e, int B, int* exit_layer, int* served, int* base_pred, float* probs,
+int lc_engine_results(lc_engine* e, int B, int* exit_layer, int* served, int* base_pred, float* probs, float* logits,
                       double* latency_ms) {
   return guard([&] {
     lcb::Engine& en = eng(e);
     if (B <= 0 || B > en.max_batch()) throw std::invalid_argument("results: batch outside [1, max_batch]");
-    en.copy_results(B, exit_layer, served, base_pred, probs, latency_ms);
+    en.copy_results(B, exit_layer, served, base_pred, probs, logits, latency_ms);
+  });
+}
+
+int lc_engine_read_tap(lc_engine* e, const float* inputs, int B, int layer, float* out) {
+  return guard([&] {
+    need(inputs, "inputs");
+    need(out, "out");
+    lcb::Engine& en = eng(e);
+    if (B <= 0 || B > en.max_batch()) throw std::invalid_argument("read_tap: batch outside [1, max_batch]");
+    const size_t bytes = static_cast<size_t>(B) * static_cast<size_t>(en.input_dim()) * sizeof(float);
+    if (cudaSetDevice(en.device()) != cudaSuccess ||
+        cudaMemcpyAsync(en.input_buffer(), inputs, bytes, cudaMemcpyHostToDevice, en.stream()) != cudaSuccess)
+      throw lcb::CudaFailure("read_tap: input upload failed");
+    en.read_tap_nchw(layer, B, out);
   });
 }
 
@@ -704,17 +722,7 @@ int lc_lookup_batch(lc_engine* e, int layer, const float* taps, int B, int* hit,
   return guard([&] {
     need(taps, "taps");
     lcb::Engine& en = eng(e);
-    const long long D = en.model().tap_dim(layer);
-    float* d = nullptr;
-    if (cudaMalloc(&d, static_cast<size_t>(B) * D * sizeof(float)) != cudaSuccess)
-      throw lcb::CudaFailure("lookup: cudaMalloc failed");
-    struct Free {
-      float* p;
-      ~Free() { cudaFree(p); }
-    } guard_free{d};
-    if (cudaMemcpy(d, taps, static_cast<size_t>(B) * D * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess)
-      throw lcb::CudaFailure("lookup: h2d failed");
-    en.lookup(layer, d, B, hit, label, prob, pr, logits);
+    en.lookup_host(layer, taps, B, hit, label, prob, pr, logits);
   });
 }
 

@@ -92,7 +92,7 @@ void run_adaptation(Engine& en, const float* inputs, int n_samples, const double
                     static_cast<size_t>(in_dim) * sizeof(float));
       }
       en.serve_host(xb.data(), B, /*shadow=*/true, /*use_graph=*/true);
-      en.copy_results(B, out.hit_layer + b0, out.served + b0, out.base_pred + b0, nullptr, out.latency_ms + b0);
+      en.copy_results(B, out.hit_layer + b0, out.served + b0, out.base_pred + b0, nullptr, nullptr, out.latency_ms + b0);
       want.clear();
       for (int i = 0; i < B; ++i)
         if (sampled[static_cast<size_t>(b0 + i)]) want.push_back(i);

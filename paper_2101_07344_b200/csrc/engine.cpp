@@ -122,28 +122,36 @@ void* Engine::dalloc(size_t bytes) {
   allocs_.push_back(p);
   return p;
 }
-Planes Engine::alloc_planes(size_t elems) {
+// Every host->device write of the engine is ordered on stream_ (the stream all
+// of its kernels run on). Pageable cudaMemcpyAsync stages the source before it
+// returns, so the host vectors may die right after the call; the device-side
+// copy still lands in stream order, after any memset queued before it and
+// before any kernel queued after it.
+void Engine::h2d(void* dst, const void* src, size_t bytes) {
+  if (bytes) ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream_), "upload");
+}
+Planes Engine::alloc_planes(size_t elems, bool zero) {
   Planes p;
   p.elems = elems;
   p.hi = static_cast<__nv_bfloat16*>(dalloc(elems * 2));
-  ck(cudaMemsetAsync(p.hi, 0, elems * 2, stream_), "memset");
+  if (zero) ck(cudaMemsetAsync(p.hi, 0, elems * 2, stream_), "memset");
   if (prec_ == kPrecX3) {
     p.lo = static_cast<__nv_bfloat16*>(dalloc(elems * 2));
-    ck(cudaMemsetAsync(p.lo, 0, elems * 2, stream_), "memset");
+    if (zero) ck(cudaMemsetAsync(p.lo, 0, elems * 2, stream_), "memset");
   }
   return p;
 }
 Planes Engine::upload_planes(const std::vector<float>& v) {
-  Planes p = alloc_planes(v.size());
+  Planes p = alloc_planes(v.size(), false);  // fully overwritten below
   std::vector<__nv_bfloat16> hi, lo;
   split_planes(v, hi, lo);
-  ck(cudaMemcpy(p.hi, hi.data(), v.size() * 2, cudaMemcpyHostToDevice), "upload");
-  if (p.lo) ck(cudaMemcpy(p.lo, lo.data(), v.size() * 2, cudaMemcpyHostToDevice), "upload");
+  h2d(p.hi, hi.data(), v.size() * 2);
+  if (p.lo) h2d(p.lo, lo.data(), v.size() * 2);
   return p;
 }
 float* Engine::upload_f32(const std::vector<float>& v) {
   float* p = static_cast<float*>(dalloc(v.size() * sizeof(float)));
-  ck(cudaMemcpy(p, v.data(), v.size() * sizeof(float), cudaMemcpyHostToDevice), "upload");
+  h2d(p, v.data(), v.size() * sizeof(float));
   return p;
 }
 
@@ -174,7 +182,9 @@ Engine::Engine(int device, const BaseModel& model, std::vector<CacheVariant> var
   ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
   require(prop.major == 10, "engine: requires an sm_100 (B200) device");
   num_sms_ = prop.multiProcessorCount;
-  stream_ = dev_stream(device).stream;
+  DevStream& ds = dev_stream(device);
+  std::lock_guard<std::recursive_mutex> dev_lock(ds.mu);  // build work queues on the shared stream
+  stream_ = ds.stream;
   ck(cudaEventCreate(&ev0_), "event");
   ck(cudaEventCreate(&ev1_), "event");
 
@@ -227,6 +237,7 @@ Engine::~Engine() {
     if (sl.h_served) cudaFreeHost(sl.h_served);
     if (sl.h_base) cudaFreeHost(sl.h_base);
     if (sl.h_probs) cudaFreeHost(sl.h_probs);
+    if (sl.h_logits) cudaFreeHost(sl.h_logits);
     if (sl.h_ns) cudaFreeHost(sl.h_ns);
     for (cudaEvent_t e : {sl.in_done, sl.in_free, sl.out_done})
       if (e) cudaEventDestroy(e);
@@ -252,16 +263,17 @@ void Engine::build_weights() {
   d_exit_ns_ = static_cast<unsigned long long*>(dalloc(static_cast<size_t>(B) * 8));
   d_t0_ = static_cast<unsigned long long*>(dalloc(8));
   d_probs_ = static_cast<float*>(dalloc(static_cast<size_t>(L) * B * sizeof(float)));
+  d_logits_ = static_cast<float*>(dalloc(static_cast<size_t>(B) * model_.num_classes * sizeof(float)));
   d_block_ns_ = static_cast<unsigned long long*>(dalloc(static_cast<size_t>(L + 1) * 2 * 8));
   d_labels_ = static_cast<int*>(dalloc(static_cast<size_t>(L) * B * sizeof(int)));
   d_grid_ = static_cast<double*>(dalloc(64 * sizeof(double)));
   d_conf_ = static_cast<unsigned long long*>(dalloc(static_cast<size_t>(L) * 64 * 4 * sizeof(unsigned long long)));
   d_lk_count_ = static_cast<int*>(dalloc(sizeof(int)));
   lk_arrive_ = static_cast<int*>(dalloc(sizeof(int)));
-  ck(cudaMemset(lk_arrive_, 0, sizeof(int)), "memset");
+  ck(cudaMemsetAsync(lk_arrive_, 0, sizeof(int), stream_), "memset");
   ws_ = static_cast<float*>(dalloc(tc_conv_ws_floats(256, num_sms_) * sizeof(float)));
   ws_counters_ = static_cast<int*>(dalloc(2 * static_cast<size_t>(num_sms_) * sizeof(int)));
-  ck(cudaMemset(ws_counters_, 0, 2 * static_cast<size_t>(num_sms_) * sizeof(int)), "memset");
+  ck(cudaMemsetAsync(ws_counters_, 0, 2 * static_cast<size_t>(num_sms_) * sizeof(int), stream_), "memset");
 
   // ---------------- base model
   long long max_tap_storage = 0;
@@ -297,7 +309,7 @@ void Engine::build_weights() {
       std::vector<__nv_bfloat16> eye(256 * 256, __float2bfloat16_rn(0.0f));
       for (int i = 0; i < 256; ++i) eye[static_cast<size_t>(i) * 256 + i] = __float2bfloat16_rn(1.0f);
       identity_ = static_cast<__nv_bfloat16*>(dalloc(eye.size() * 2));
-      ck(cudaMemcpy(identity_, eye.data(), eye.size() * 2, cudaMemcpyHostToDevice), "identity upload");
+      h2d(identity_, eye.data(), eye.size() * 2);
     }
     cnn_w_.resize(model_.ops.size());
     std::vector<long long> slot_elems(static_cast<size_t>(model_.nslots), 0);
@@ -689,6 +701,7 @@ void Engine::build_mlp_steps(std::vector<Step>& steps, bool shadow) {
                      static_cast<int>(cur_count - d_counts_), 2.0 * f.in * f.out,
                      (x3 ? 4.0 : 2.0) * (static_cast<double>(f.inp) + f.outp)});
     const int layer = b + 1;
+    if (shadow) tap_step_end_[static_cast<size_t>(layer)] = static_cast<int>(steps.size());
     if (shadow) add_stamp(steps, layer, 0);
     const int ci = cache_of_layer_[static_cast<size_t>(layer)];
     if (ci >= 0) {
@@ -728,7 +741,7 @@ void Engine::build_mlp_steps(std::vector<Step>& steps, bool shadow) {
   const int classes = model_.num_classes;
   steps.push_back({[this, cur, last, classes, cur_ids, cur_count, B](cudaStream_t s) {
                      launch_mlp_head(cur.hi, cur.lo, last.outp, last.out, head_w_, head_b_, classes, cur_ids,
-                                     cur_count, B, d_base_, nullptr, d_exit_, d_served_, d_exit_ns_, s);
+                                     cur_count, B, d_base_, d_logits_, d_exit_, d_served_, d_exit_ns_, s);
                    },
                    0});
   if (shadow) add_stamp(steps, L + 1, 0);  // after the head (charged to the last block)
@@ -922,12 +935,13 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow) {
       float* ls = static_cast<float*>(dalloc(static_cast<size_t>(rows_fc_splits(C)) * B * classes * sizeof(float)));
       steps.push_back({[this, in, C, HW, classes, cur_ids, cur_count, B, fs, ls](cudaStream_t s) {
                          launch_cnn_head(in.hi, in.lo, C, HW, head_w_, head_b_, classes, cur_ids, cur_count, B,
-                                         d_base_, nullptr, d_exit_, d_served_, d_exit_ns_, fs, ls, s);
+                                         d_base_, d_logits_, d_exit_, d_served_, d_exit_ns_, fs, ls, s);
                        },
                        0, classes > 32 ? 3 : 1});
     }
     if (o.tap >= 0) {
       const int layer = o.tap + 1;
+      if (shadow) tap_step_end_[static_cast<size_t>(layer)] = static_cast<int>(steps.size());
       if (shadow) add_stamp(steps, layer, 0);
       const int ci = cache_of_layer_[static_cast<size_t>(layer)];
       if (ci >= 0) {
@@ -960,6 +974,7 @@ std::vector<Step>& Engine::steps_for(bool shadow) {
   bool& built = shadow ? built_shadow_ : built_compact_;
   if (!built) {
     st.clear();
+    if (shadow) tap_step_end_.assign(static_cast<size_t>(model_.num_blocks) + 1, -1);
     if (model_.family == "mlp") build_mlp_steps(st, shadow);
     else build_cnn_steps(st, shadow);
     built = true;
@@ -1028,6 +1043,7 @@ void Engine::init_slots() {
     ck(cudaMallocHost(&sl.h_served, static_cast<size_t>(B) * sizeof(int)), "cudaMallocHost");
     ck(cudaMallocHost(&sl.h_base, static_cast<size_t>(B) * sizeof(int)), "cudaMallocHost");
     ck(cudaMallocHost(&sl.h_probs, static_cast<size_t>(L) * B * sizeof(float)), "cudaMallocHost");
+    ck(cudaMallocHost(&sl.h_logits, static_cast<size_t>(B) * model_.num_classes * sizeof(float)), "cudaMallocHost");
     ck(cudaMallocHost(&sl.h_ns, static_cast<size_t>(B + 1) * 8), "cudaMallocHost");
     ck(cudaEventCreateWithFlags(&sl.in_done, cudaEventDisableTiming), "event");
     ck(cudaEventCreateWithFlags(&sl.in_free, cudaEventDisableTiming), "event");
@@ -1045,6 +1061,7 @@ int Engine::submit(const float* x, int B, bool shadow) {
   next_slot_ ^= 1;
   Slot& sl = slots_[id];
   if (sl.busy) ck(cudaEventSynchronize(sl.out_done), "slot wait");  // uncollected results are dropped
+  ++sl.gen;  // tickets of the dropped batch no longer match
   const size_t bytes = static_cast<size_t>(B) * model_.input_dim() * sizeof(float);
   // H2D on the copy stream once the slot's previous staging copy was consumed
   ck(cudaStreamWaitEvent(copy_stream_, sl.in_free, 0), "wait");
@@ -1063,18 +1080,33 @@ int Engine::submit(const float* x, int B, bool shadow) {
                        static_cast<size_t>(max_batch_) * sizeof(float), static_cast<size_t>(B) * sizeof(float), L,
                        cudaMemcpyDeviceToHost, stream_),
      "d2h");
+  ck(cudaMemcpyAsync(sl.h_logits, d_logits_, static_cast<size_t>(B) * model_.num_classes * sizeof(float),
+                     cudaMemcpyDeviceToHost, stream_),
+     "d2h");
   ck(cudaMemcpyAsync(sl.h_ns, d_exit_ns_, static_cast<size_t>(B) * 8, cudaMemcpyDeviceToHost, stream_), "d2h");
   ck(cudaMemcpyAsync(sl.h_ns + B, d_t0_, 8, cudaMemcpyDeviceToHost, stream_), "d2h");
   ck(cudaEventRecord(sl.out_done, stream_), "event");
   sl.B = B;
   sl.busy = true;
-  return id;
+  return static_cast<int>((sl.gen & 0x3fffffff) << 1) | id;
 }
 
-void Engine::collect(int slot, int B, int* exit_layer, int* served, int* base, float* probs_LB, double* latency_ms) {
-  require(slot == 0 || slot == 1, "collect: bad slot");
-  Slot& sl = slots_[slot];
+namespace {
+// Base logits exist only for requests whose full pass ran (base_pred >= 0).
+void mask_logits(float* logits, const int* base, int B, int classes) {
+  for (int i = 0; i < B; ++i)
+    if (base[i] < 0)
+      for (int k = 0; k < classes; ++k) logits[static_cast<size_t>(i) * classes + k] = std::nanf("");
+}
+}  // namespace
+
+void Engine::collect(int slot, int B, int* exit_layer, int* served, int* base, float* probs_LB, float* logits,
+                     double* latency_ms) {
+  require(slot >= 0, "collect: bad ticket");
+  Slot& sl = slots_[slot & 1];
   require(sl.busy, "collect: slot holds no submitted batch");
+  require(static_cast<unsigned>(slot >> 1) == (sl.gen & 0x3fffffff),
+          "collect: ticket superseded (its slot was reused by a later submit)");
   require(B == sl.B, "collect: batch size differs from the submitted one");
   ck(cudaEventSynchronize(sl.out_done), "collect");
   const size_t n = static_cast<size_t>(B);
@@ -1082,6 +1114,11 @@ void Engine::collect(int slot, int B, int* exit_layer, int* served, int* base, f
   if (served) std::memcpy(served, sl.h_served, n * sizeof(int));
   if (base) std::memcpy(base, sl.h_base, n * sizeof(int));
   if (probs_LB) std::memcpy(probs_LB, sl.h_probs, static_cast<size_t>(model_.num_blocks) * n * sizeof(float));
+  if (logits) {
+    const int C = model_.num_classes;
+    std::memcpy(logits, sl.h_logits, n * C * sizeof(float));
+    mask_logits(logits, sl.h_base, B, C);
+  }
   if (latency_ms)
     for (size_t i = 0; i < n; ++i) latency_ms[i] = static_cast<double>(sl.h_ns[i] - sl.h_ns[n]) * 1e-6;
   sl.busy = false;
@@ -1105,12 +1142,22 @@ void Engine::measure(int B, const double* grid, int G, long long* counts) {
 
 void Engine::synchronize() { ck(cudaStreamSynchronize(stream_), "synchronize"); }
 
-void Engine::copy_results(int B, int* exit_layer, int* served, int* base, float* probs_LB, double* latency_ms) {
+void Engine::copy_results(int B, int* exit_layer, int* served, int* base, float* probs_LB, float* logits,
+                          double* latency_ms) {
   std::lock_guard<std::recursive_mutex> dev_lock(dev_stream(device_).mu);
   ck(cudaSetDevice(device_), "cudaSetDevice");
+  std::vector<int> base_tmp;
+  if (logits && !base) {
+    base_tmp.resize(static_cast<size_t>(B));
+    base = base_tmp.data();
+  }
   if (exit_layer) ck(cudaMemcpyAsync(exit_layer, d_exit_, B * sizeof(int), cudaMemcpyDeviceToHost, stream_), "d2h");
   if (served) ck(cudaMemcpyAsync(served, d_served_, B * sizeof(int), cudaMemcpyDeviceToHost, stream_), "d2h");
   if (base) ck(cudaMemcpyAsync(base, d_base_, B * sizeof(int), cudaMemcpyDeviceToHost, stream_), "d2h");
+  if (logits)
+    ck(cudaMemcpyAsync(logits, d_logits_, static_cast<size_t>(B) * model_.num_classes * sizeof(float),
+                       cudaMemcpyDeviceToHost, stream_),
+       "d2h");
   if (probs_LB)
     for (int l = 0; l < model_.num_blocks; ++l)
       ck(cudaMemcpyAsync(probs_LB + static_cast<size_t>(l) * B, d_probs_ + static_cast<size_t>(l) * max_batch_,
@@ -1126,6 +1173,45 @@ void Engine::copy_results(int B, int* exit_layer, int* served, int* base, float*
   ck(cudaStreamSynchronize(stream_), "d2h sync");
   if (latency_ms)
     for (int i = 0; i < B; ++i) latency_ms[i] = static_cast<double>(ns[static_cast<size_t>(i)] - t0) * 1e-6;
+  if (logits) mask_logits(logits, base, B, model_.num_classes);
+}
+
+void Engine::read_tap_nchw(int layer, int B, float* host_out) {
+  std::lock_guard<std::recursive_mutex> dev_lock(dev_stream(device_).mu);
+  require(layer >= 1 && layer <= model_.num_blocks, "read_tap: layer out of range");
+  require(B > 0 && B <= max_batch_, "read_tap: batch outside [1, max_batch]");
+  ck(cudaSetDevice(device_), "cudaSetDevice");
+  launch_set_int(d_batch_, B, stream_);
+  std::vector<Step>& st = steps_for(true);
+  const int end = tap_step_end_[static_cast<size_t>(layer)];
+  require(end >= 0, "read_tap: no tap recorded for the layer");
+  for (int i = 0; i < end; ++i) st[static_cast<size_t>(i)].run(stream_);
+  const TapInfo& ti = model_.taps[static_cast<size_t>(layer - 1)];
+  Planes p;
+  long long row_stride = 0;
+  int C = 0, HW = 1;
+  if (model_.family == "mlp") {
+    p = mlp_act_[static_cast<size_t>(layer - 1)];
+    row_stride = mlp_fc_[static_cast<size_t>(layer - 1)].outp;
+    C = mlp_fc_[static_cast<size_t>(layer - 1)].out;
+  } else {
+    int slot = -1;
+    for (const CnnOp& o : model_.ops)
+      if (o.tap == layer - 1) slot = o.out;
+    require(slot >= 0, "read_tap: no op produces the tap");
+    p = slot_buf_[static_cast<size_t>(slot)];
+    row_stride = ti.dim();
+    C = ti.C;
+    HW = ti.H * ti.W;
+  }
+  const size_t n = static_cast<size_t>(B) * C * HW;
+  float* d = nullptr;
+  ck(cudaMallocAsync(reinterpret_cast<void**>(&d), n * sizeof(float), stream_), "read_tap alloc");
+  launch_planes_to_nchw(p.hi, p.lo, row_stride, C, HW, B, d, stream_);
+  const cudaError_t e = cudaMemcpyAsync(host_out, d, n * sizeof(float), cudaMemcpyDeviceToHost, stream_);
+  cudaFreeAsync(d, stream_);
+  ck(e, "read_tap copy");
+  ck(cudaStreamSynchronize(stream_), "read_tap");
 }
 
 void Engine::lookup(int layer, const float* taps_dev, int B, int* hit, int* label, float* prob, float* pr,
@@ -1166,7 +1252,31 @@ void Engine::lookup(int layer, const float* taps_dev, int B, int* hit, int* labe
   ck(cudaStreamSynchronize(stream_), "lookup sync");
 }
 
+void Engine::lookup_host(int layer, const float* taps_host, int B, int* hit, int* label, float* prob, float* pr,
+                         float* logits) {
+  std::lock_guard<std::recursive_mutex> dev_lock(dev_stream(device_).mu);
+  require(layer >= 1 && layer <= model_.num_blocks, "lookup: layer out of range");
+  require(B > 0 && B <= max_batch_, "lookup: batch outside [1, max_batch]");
+  ck(cudaSetDevice(device_), "cudaSetDevice");
+  const size_t bytes = static_cast<size_t>(B) * model_.tap_dim(layer) * sizeof(float);
+  float* d = nullptr;
+  ck(cudaMallocAsync(reinterpret_cast<void**>(&d), bytes, stream_), "lookup: alloc");
+  const cudaError_t e = cudaMemcpyAsync(d, taps_host, bytes, cudaMemcpyHostToDevice, stream_);
+  if (e != cudaSuccess) {
+    cudaFreeAsync(d, stream_);
+    ck(e, "lookup: h2d");
+  }
+  try {
+    lookup(layer, d, B, hit, label, prob, pr, logits);
+  } catch (...) {
+    cudaFreeAsync(d, stream_);
+    throw;
+  }
+  ck(cudaFreeAsync(d, stream_), "lookup: free");
+}
+
 void Engine::set_delta(int layer, double delta) {
+  std::lock_guard<std::recursive_mutex> dev_lock(dev_stream(device_).mu);
   require(layer >= 1 && layer <= model_.num_blocks, "set_delta: layer out of range");
   const int ci = cache_of_layer_[static_cast<size_t>(layer)];
   require(ci >= 0, "set_delta: no cache attached at layer " + std::to_string(layer));
@@ -1191,9 +1301,9 @@ bool same_shape(const Network& a, const Network& b) {
   }
   return true;
 }
-void put_f32(float* dst, const std::vector<double>& v) {
+void put_f32(float* dst, const std::vector<double>& v, cudaStream_t s) {
   const std::vector<float> f = to_f32(v);
-  ck(cudaMemcpy(dst, f.data(), f.size() * sizeof(float), cudaMemcpyHostToDevice), "variant upload");
+  ck(cudaMemcpyAsync(dst, f.data(), f.size() * sizeof(float), cudaMemcpyHostToDevice, s), "variant upload");
 }
 }  // namespace
 
@@ -1215,26 +1325,27 @@ void Engine::update_variant(const CacheVariant& nv) {
     const std::vector<float> w = fc_w1_layout(PW[0].w, c, ti, model_.family == "mlp");
     std::vector<__nv_bfloat16> hi, lo;
     split_planes(w, hi, lo);
-    ck(cudaMemcpy(c.W1.hi, hi.data(), w.size() * 2, cudaMemcpyHostToDevice), "variant upload");
-    if (c.W1.lo) ck(cudaMemcpy(c.W1.lo, lo.data(), w.size() * 2, cudaMemcpyHostToDevice), "variant upload");
-    put_f32(c.b1, PW[0].b);
-    put_f32(c.W2, PW[2].w);
-    put_f32(c.b2, PW[2].b);
+    h2d(c.W1.hi, hi.data(), w.size() * 2);
+    if (c.W1.lo) h2d(c.W1.lo, lo.data(), w.size() * 2);
+    put_f32(c.b1, PW[0].b, stream_);
+    put_f32(c.W2, PW[2].w, stream_);
+    put_f32(c.b2, PW[2].b, stream_);
   } else if (c.family == 1) {
-    put_f32(c.W2, PW[1].w);
-    put_f32(c.b2, PW[1].b);
+    put_f32(c.W2, PW[1].w, stream_);
+    put_f32(c.b2, PW[1].b, stream_);
   } else {
-    put_f32(c.w1, PW[0].w);
+    put_f32(c.w1, PW[0].w, stream_);
     c.b1c = static_cast<float>(PW[0].b[0]);
-    put_f32(c.W2, PW[2].w);
-    put_f32(c.b2, PW[2].b);
+    put_f32(c.W2, PW[2].w, stream_);
+    put_f32(c.b2, PW[2].b, stream_);
   }
-  put_f32(c.Ws1, nv.selector.weights[0].w);
-  put_f32(c.bs1, nv.selector.weights[0].b);
-  put_f32(c.ws2, nv.selector.weights[2].w);
+  put_f32(c.Ws1, nv.selector.weights[0].w, stream_);
+  put_f32(c.bs1, nv.selector.weights[0].b, stream_);
+  put_f32(c.ws2, nv.selector.weights[2].w, stream_);
   c.bs2 = static_cast<float>(nv.selector.weights[2].b[0]);
   c.delta = nv.delta;
   cur = nv;
+  ck(cudaStreamSynchronize(stream_), "update_variant: upload");
   for (auto& g : graph_)
     if (g) {
       cudaGraphExecDestroy(g);
@@ -1290,6 +1401,7 @@ double Engine::delta(int layer) const {
 // calibrate synthetic deployments to a target exit profile (the analogue of
 // the reference tests' force_selector, test_serving.cpp:123-129).
 void Engine::set_selector_out(int layer, double gain, double bias) {
+  std::lock_guard<std::recursive_mutex> dev_lock(dev_stream(device_).mu);
   const int ci = cache_of_layer_.at(static_cast<size_t>(layer));
   require(ci >= 0, "set_selector_out: no cache attached at layer " + std::to_string(layer));
   CacheVariant& v = variants_[static_cast<size_t>(ci)];
@@ -1297,7 +1409,9 @@ void Engine::set_selector_out(int layer, double gain, double bias) {
   v.selector.weights[2].b[0] = bias;
   DevCache& c = *caches_[static_cast<size_t>(ci)];
   const std::vector<float> w = to_f32(v.selector.weights[2].w);
-  ck(cudaMemcpy(c.ws2, w.data(), w.size() * sizeof(float), cudaMemcpyHostToDevice), "selector upload");
+  ck(cudaSetDevice(device_), "cudaSetDevice");
+  h2d(c.ws2, w.data(), w.size() * sizeof(float));
+  ck(cudaStreamSynchronize(stream_), "selector upload");
   c.bs2 = static_cast<float>(bias);
   for (auto& g : graph_)
     if (g) {

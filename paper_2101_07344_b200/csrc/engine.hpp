@@ -62,9 +62,11 @@ class Engine {
   // Pipelined serving from pinned host memory (two slots): the H2D copy of a
   // submitted batch runs on a copy stream while the previous batch computes;
   // results come back by D2H into the slot's pinned buffers. submit returns
-  // the slot; collect waits for it and copies the results out.
+  // a ticket ((generation << 1) | slot); collect waits for it and copies the
+  // results out, rejecting a ticket whose slot a later submit reused.
   int submit(const float* x_pinned, int B, bool shadow);
-  void collect(int slot, int B, int* exit_layer, int* served, int* base, float* probs_LB, double* latency_ms);
+  void collect(int slot, int B, int* exit_layer, int* served, int* base, float* probs_LB, float* logits,
+               double* latency_ms);
   void synchronize();
   // Results (device pointers, indexed by request id).
   const int* exit_layer() const { return d_exit_; }
@@ -74,10 +76,19 @@ class Engine {
   const unsigned long long* start_ns() const { return d_t0_; }
   const float* probs() const { return d_probs_; }  // [blocks][max_batch]
   const int* layer_counts() const { return d_counts_; }  // [blocks + 1]
-  void copy_results(int B, int* exit_layer, int* served, int* base, float* probs_LB, double* latency_ms);
+  // logits [B][classes]: the base model's pre-softmax output (network.hpp:57-60,
+  // activations[size-2]); rows of requests whose full pass compaction skipped are NaN.
+  void copy_results(int B, int* exit_layer, int* served, int* base, float* probs_LB, float* logits,
+                    double* latency_ms);
+  // Tap of block `layer` for requests [0, B) as the reference sees it (fp32,
+  // NCHW-flat, hi + lo): runs the batch staged in input_buffer() in shadow
+  // mode up to that block (direct launches) and reads the activation back.
+  void read_tap_nchw(int layer, int B, float* host_out);
 
   // ----- lookup only (reference lookup() on caller-provided NCHW-flat taps)
   void lookup(int layer, const float* taps_dev, int B, int* hit, int* label, float* prob, float* pr, float* logits);
+  void lookup_host(int layer, const float* taps_host, int B, int* hit, int* label, float* prob, float* pr,
+                   float* logits);
 
   // Batched measure_metrics / tune_delta support (cache.cpp:267-335): a
   // shadow serve of the B staged requests (every cache probed, full base
@@ -134,7 +145,8 @@ class Engine {
   void add_stamp(std::vector<Step>& steps, int layer, int which);
   std::vector<Step>& steps_for(bool shadow);
   void* dalloc(size_t bytes);
-  Planes alloc_planes(size_t elems);
+  void h2d(void* dst, const void* src, size_t bytes);
+  Planes alloc_planes(size_t elems, bool zero = true);
   Planes upload_planes(const std::vector<float>& v);
   float* upload_f32(const std::vector<float>& v);
 
@@ -162,6 +174,7 @@ class Engine {
   unsigned long long* d_exit_ns_ = nullptr;
   unsigned long long* d_t0_ = nullptr;
   float* d_probs_ = nullptr;
+  float* d_logits_ = nullptr;  // [max_batch][classes] base logits by request id
   unsigned long long* d_block_ns_ = nullptr;  // shadow mode: [blocks][2] = {base work done, lookup done}
   int* d_labels_ = nullptr;   // [blocks][max_batch] argmax(pr) of every probed layer
   double* d_grid_ = nullptr;  // measure(): threshold grid (<= 64)
@@ -204,6 +217,7 @@ class Engine {
   Planes im2col_buf_;
 
   std::vector<Step> steps_compact_, steps_shadow_;
+  std::vector<int> tap_step_end_;  // shadow step list: index one past the op producing tap l (by layer)
   bool built_compact_ = false, built_shadow_ = false;
   cudaGraphExec_t graph_[2] = {nullptr, nullptr};
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
@@ -213,9 +227,11 @@ class Engine {
     int* h_served = nullptr;
     int* h_base = nullptr;
     float* h_probs = nullptr;  // [blocks][max_batch]
+    float* h_logits = nullptr;  // [max_batch][classes]
     unsigned long long* h_ns = nullptr;  // [max_batch + 1]: exit times, then t0
     cudaEvent_t in_done = nullptr, in_free = nullptr, out_done = nullptr;
     int B = 0;
+    unsigned gen = 0;  // submit generation: tickets are (gen << 1) | slot
     bool busy = false;
   };
   Slot slots_[2];

@@ -892,6 +892,21 @@ __global__ void split_taps_nchw_kernel(const float* x, int C, int HW, long long 
   }
 }
 
+// Read-back of a stored tap as the reference sees it: fp32 hi + lo, NCHW-flat.
+__global__ void planes_to_nchw_kernel(const __nv_bfloat16* hi, const __nv_bfloat16* lo, long long row_stride, int C,
+                                      int HW, float* out) {
+  pdl_wait();
+  pdl_trigger();
+  const int r = blockIdx.x;
+  const long long D = static_cast<long long>(C) * HW;
+  for (long long f = blockIdx.y * blockDim.x + threadIdx.x; f < D; f += gridDim.y * blockDim.x) {
+    const long long i = r * row_stride + (f % HW) * C + f / HW;
+    float v = __bfloat162float(hi[i]);
+    if (lo) v += __bfloat162float(lo[i]);
+    out[r * D + f] = v;
+  }
+}
+
 // Base head (base_model.cpp:48-49): logits -> softmax -> argmax (serving.cpp:108).
 template <bool kGap>
 __global__ void __launch_bounds__(kLk) base_head_kernel(const __nv_bfloat16* hi, const __nv_bfloat16* lo,
@@ -1270,6 +1285,15 @@ void launch_split_taps_nchw(const float* x, int C, int HW, int rows, long long r
   int gy = static_cast<int>((row_stride + 255) / 256);
   if (gy > 128) gy = 128;
   launch_pdl(split_taps_nchw_kernel, dim3(dim3(rows, gy)), dim3(256), 0, s, x, C, HW, row_stride, hi, lo);
+}
+
+void launch_planes_to_nchw(const __nv_bfloat16* hi, const __nv_bfloat16* lo, long long row_stride, int C, int HW,
+                           int rows, float* out, cudaStream_t s) {
+  if (rows <= 0) return;
+  const long long D = static_cast<long long>(C) * HW;
+  int gy = static_cast<int>((D + 255) / 256);
+  if (gy > 128) gy = 128;
+  launch_pdl(planes_to_nchw_kernel, dim3(rows, gy), dim3(256), 0, s, hi, lo, row_stride, C, HW, out);
 }
 
 void launch_mlp_head(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int dp, int dim, const float* W, const float* b,

@@ -126,6 +126,10 @@ void launch_split_rows(const float* x, int in_dim, int dp, const int* ids, const
 void launch_split_taps_nchw(const float* x, int C, int HW, int rows, long long row_stride, __nv_bfloat16* hi,
                             __nv_bfloat16* lo, cudaStream_t s);
 
+// Stored tap rows [rows][row_stride] (NHWC, hi + lo) -> fp32 NCHW-flat [rows][C*HW].
+void launch_planes_to_nchw(const __nv_bfloat16* hi, const __nv_bfloat16* lo, long long row_stride, int C, int HW,
+                           int rows, float* out, cudaStream_t s);
+
 // MLP head: logits = W [classes][dim] . act + b, softmax, argmax -> base_pred.
 void launch_mlp_head(const __nv_bfloat16* hi, const __nv_bfloat16* lo, int dp, int dim, const float* W, const float* b,
                      int classes, const int* ids, const int* count, int max_rows, int* base_pred, float* logits_out,

@@ -185,3 +185,22 @@ def test_cnn_oracle_vs_torch_fp64():
     np.testing.assert_allclose(logits, lg.numpy(), rtol=1e-10, atol=1e-10)
     # activations stay O(1) through depth (synthetic weights are usable)
     assert 0.05 < np.abs(taps[-1]).mean() < 20
+
+
+@requires_ref
+def test_oracle_mlp_taps_and_logits_bit_exact_vs_reference():
+    """oracle_mlp_forward (taps after every block's ReLU and the base logits,
+    activations[size-2]) against the reference's forward_with_taps and forward
+    (oracle/_ref) on the golden trained model: the serve-path logits/taps
+    parity tests compare the GPU with exactly these values."""
+    d = os.path.join(GOLDEN, "trained")
+    txt = open(os.path.join(d, "model.txt")).read()
+    model = O.parse_model(txt)
+    rm = O.RefModel.load(txt)
+    x = np.random.default_rng(3).uniform(-1.5, 1.5, (16, model["layers"][0]["in_dim"]))
+    taps, logits = O.oracle_mlp_forward(model, x)
+    for i in range(16):
+        rt, _ = rm.forward_taps(x[i])
+        for k in range(model["blocks"]):
+            assert np.array_equal(taps[k][i], rt[k])
+        assert np.array_equal(logits[i], rm.logits(x[i]))
