@@ -2,11 +2,13 @@
 """Benchmark of the learned-cache serve path (BASELINE.json metric: requests/s
 and p50/p99 latency with learned caches vs no-cache; hit rate).
 
-Default workload = BASELINE.json configs[1]: ResNet-18 CIFAR-10 shape with a
-learned cache (Pool(C) = GAP head + selector) after every residual block,
-batch 256 per GPU, synthetic weights and N(0,1) images, selectors calibrated
-to the paper's R18-C10 exit profile (3.51 % of requests run the full model,
-PAPER.md:2873-2878). One step = one batch through the serve path on every GPU.
+Default workload = the north star's target, BASELINE.json configs[2]:
+ResNet-50 ImageNet 224x224 with a learned cache (Pool(C) = GAP head + FC(16)
+selector) after each of the 16 bottleneck blocks, batch 128 per GPU, synthetic
+weights and N(0,1) images, selectors calibrated to the paper's R50 exit profile
+(1.53 % of requests run the full model). One step = one
+batch through the serve path on every GPU. configs[1] (ResNet-18 CIFAR, batch
+256) is `--config resnet18_cifar`.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                   [--config resnet18_cifar|c1_mlp|resnet50|vgg16_cifar|resnet152]
@@ -134,44 +136,57 @@ def build_deployment(cfg_name, batch, precision, device, seed=2101):
     return m, vs, dep, base, gen, fr
 
 
+C1_WIDTHS = [64, 64, 128, 128, 256, 256, 512, 512]  # = paper_2101_07344_b200.synthetic.C1_WIDTHS
+C1_MENU = ["FC(1024)", "Pool(8192)", "Conv(3,1)", "FC(512)", "Pool(4096)", "Conv(5,2)", "FC(1024)", "Pool(8192)"]
+
+
 def cpu_reference(cfg_name, steps, warmup, seed=2101):
-    """The reference's CPU path on this host's cores (bounded sample per step)."""
+    """The reference's CPU path on this host's cores (bounded sample per step).
+
+    Never imports or loads the product library: the block-MLP config runs the
+    reference's own make_base_model / build_variant / simulate_model
+    (oracle/_ref, the unmodified reference compiled from its sources); the
+    CNN configs (no reference counterpart) build the same synthetic network
+    with oracle/cnn_models.py (bit-identical weights to make_cnn_model, pinned
+    by tests/test_oracle.py), run its fp64 forward through the C restatement
+    (oracle/lc_oracle.c) and every cache lookup through the reference's own
+    lookup() (oracle/_ref; the restatement when _ref is absent)."""
     from oracle import oracle as O
-    import paper_2101_07344_b200 as lcb
-    from paper_2101_07344_b200.synthetic import C1_MENU, C1_WIDTHS, image_inputs, mlp_inputs
     family, arch, classes, _, _, _ = CONFIGS[cfg_name]
     cores = os.cpu_count() or 1
+    have_ref = os.path.exists(O.REF_SO)
     if family == "mlp":
         rm = O.RefModel.make(3072, classes, C1_WIDTHS, 8, seed)
         rvs = [O.RefVariant.build(l + 1, l, C1_MENU[l], rm.tap_dims[l], classes, seed + 1) for l in range(8)]
         sample = 4096
-        x = mlp_inputs(sample, 3072, seed + 3)
+        x = np.random.default_rng(seed + 3).uniform(-1.5, 1.5, size=(sample, 3072))
         kind = "reference"
         run = lambda: O.ref_simulate(rm, rvs, x, threads=cores)  # noqa: E731
         desc = f"{sample} requests of the C1 block-MLP through the reference's simulate_model (oracle/_ref), " \
                f"request-sharded over {cores} threads"
     else:
-        m = lcb.make_cnn_model(arch, classes, seed)
-        ops = m.cnn_ops()
-        side = 32 if arch.endswith("cifar") else 224
+        from oracle.cnn_models import CnnModel
+        cm = CnnModel(arch, classes, seed)
+        side = cm.in_shape[1]
         sample = max(2 * cores, 16) if arch.endswith("cifar") else max(cores // 2, 4)
-        x = image_inputs(sample, 3, side, side, seed + 3)
-        vs = []
-        for l in range(1, m.num_blocks + 1):
-            C, H, W = m.tap(l)
-            v = lcb.build_variant(l, 0, f"Pool({C})", m.tap_dim(l), classes, seed + l)
-            pred, sel, d = O.variant_layers_from_product(v)
-            vs.append((O.OracleNet(pred), O.OracleNet(sel), d))
+        x = np.random.default_rng(seed + 3).standard_normal((sample, 3 * side * side))
+        if have_ref:
+            vs = [O.RefVariant.build(l, 0, f"Pool({cm.taps[l - 1][0]})", cm.tap_dims[l - 1], classes, seed + l)
+                  for l in range(1, cm.num_blocks + 1)]
+            look = lambda k, t: vs[k].lookup(t, classes)[0]  # noqa: E731
+        else:
+            raise RuntimeError("oracle/_ref (the compiled reference) is required for the reference arm")
         kind = "port"
 
         def run():
-            taps, logits = O.oracle_cnn_forward(ops, m.nslots, x, m.num_blocks, m.tap_dims, classes, threads=cores)
+            taps, _ = O.oracle_cnn_forward(cm.ops, cm.nslots, x, cm.num_blocks, cm.tap_dims, classes, threads=cores)
             for i in range(sample):
-                for l, (pn, sn, d) in enumerate(vs):
-                    if O.oracle_lookup(pn, sn, d, taps[l][i])[0]:
+                for k in range(cm.num_blocks):
+                    if look(k, taps[k][i]):
                         break
-        desc = f"{sample} images per step through the fp64 C restatement of {arch} (oracle/lc_oracle.c) + " \
-               f"the reference lookup restatement, image-sharded over {cores} threads (the reference has no CNN)"
+        desc = f"{sample} images per step: fp64 forward of {arch} through the C restatement (oracle/lc_oracle.c, " \
+               f"image-sharded over {cores} threads; the reference has no CNN) + the reference's own lookup() " \
+               f"(oracle/_ref) per cache until the first hit"
     for _ in range(max(0, warmup)):
         run()
     t0 = time.perf_counter()
@@ -187,7 +202,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="resnet18_cifar", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="resnet50", choices=sorted(CONFIGS))
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--precision", default="bf16x3", choices=["bf16x3", "bf16"])
     ap.add_argument("--cpu-steps", type=int, default=2)
@@ -216,6 +231,12 @@ def main():
         if rank != 0:
             return
         cb = cpu_reference(args.config, args.steps, args.warmup)
+        try:  # evidence that this arm ran without the product library
+            maps = open("/proc/self/maps").read()
+            cb["product_library_loaded"] = "liblatecache_b200" in maps
+            cb["reference_library_loaded"] = "liblatecache_ref" in maps
+        except OSError:
+            pass
         line = {"metric": metric, "value": cb["value"], "unit": "requests/s", "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
@@ -337,54 +358,74 @@ def main():
     hit_rate = float(np.mean(ex > 0))
     hits_by_layer = {int(l): int(np.sum(ex == l)) for l in range(1, m.num_blocks + 1) if np.sum(ex == l)}
 
-    # live roofline: per-step CUDA events over one (un-graphed) batch
+    # Roofline of the dominant kernels (the tcgen05 contractions), measured live.
+    # The graphed, timed step has no per-kernel events, so each kind's share of
+    # the step comes from one un-graphed batch with CUDA events around every
+    # launch (same step list, same survivors), applied to the timed graphed
+    # step: kernel ms per step = ms_per_step x share <= ms_per_step.
     stage(dep, 0)
     prof = dep.profile(B)
+    step_ms = float(prof["ms"].sum())
+    ms_step = ms_cache_max / args.steps
+
+    def kind_share(mask):
+        return float(prof["ms"][mask].sum()) / step_ms if step_ms else 0.0
+
     tc = prof["kind"] == 1
-    tc_ms = float(prof["ms"][tc].sum())
+    lk = prof["kind"] == 2
+    glue = prof["kind"] == 0
     tc_flops = float(prof["flops"][tc].sum())
     tc_bytes = float(prof["bytes"][tc].sum())
-    lk = prof["kind"] == 2
-    lk_ms = float(prof["ms"][lk].sum())
+    tc_ms = ms_step * kind_share(tc)
+    lk_ms = ms_step * kind_share(lk)
     lk_bytes = float(prof["bytes"][lk].sum())
-    step_ms = float(prof["ms"].sum())
+    glue_ms = ms_step * kind_share(glue)
+    glue_bytes = float(prof["bytes"][glue].sum())
     hbm, bf16_burst, bf16_sus, peak_src = load_peaks()
     mma_factor = 3.0 if args.precision == "bf16x3" else 1.0
     # Per contraction launch: tensor floor (MMA FLOPs at the bf16 peak) and HBM
     # floor (algorithmic bytes: input + output + residual once, at the copy
     # bandwidth); the binding floor summed over launches / their measured time
-    # is the combined roofline fraction.
+    # is the combined roofline fraction (from the un-graphed per-launch events).
     t_tc = prof["flops"][tc] * mma_factor / (bf16_burst * 1e12) * 1e3
     t_hbm = prof["bytes"][tc] / (hbm * 1e9) * 1e3
     floor_ms = float(np.maximum(t_tc, t_hbm).sum())
     bound = "tensor" if float(t_tc.sum()) >= float(t_hbm.sum()) else "hbm"
     ach_tf = tc_flops / (tc_ms * 1e-3) / 1e12 if tc_ms else 0.0
     ach_gb = tc_bytes / (tc_ms * 1e-3) / 1e9 if tc_ms else 0.0
-    traffic = None
+    traffic = traffic_src = None
     tpath = os.path.join(ROOT, "profiles", f"traffic_{args.config}_{args.precision}.json")
     if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get("dram_bytes_per_step")
+        tj = json.load(open(tpath))
+        traffic, traffic_src = tj.get("dram_bytes_per_step"), tj.get("source")
     roofline = {"bound": bound, "kernel": "tc_conv_kernel + tc_stem_kernel (tcgen05 implicit-GEMM convs)",
                 "achieved": ach_tf if bound == "tensor" else ach_gb,
                 "peak": bf16_burst if bound == "tensor" else hbm,
                 "unit": "TFLOP/s" if bound == "tensor" else "GB/s",
-                "frac": (ach_tf * mma_factor / bf16_burst) if bound == "tensor" else ach_gb / hbm,
-                "traffic": traffic, "algorithmic_bytes_per_step": tc_bytes,
+                "frac": (ach_tf / bf16_burst) if bound == "tensor" else ach_gb / hbm,
+                "traffic": traffic, "traffic_source": traffic_src, "algorithmic_bytes_per_step": tc_bytes,
                 "peak_source": f"{peak_src} (MEASURED_PEAKS.json: bf16 burst {bf16_burst} TFLOP/s, HBM {hbm} GB/s)",
-                "algorithmic_flops_per_step": tc_flops, "kernel_ms_per_step": tc_ms,
-                "share_of_step": tc_ms / step_ms if step_ms else None,
+                "algorithmic_flops_per_step": tc_flops, "kernel_ms_per_step": tc_ms, "ms_per_step": ms_step,
+                "share_of_step": kind_share(tc),
                 "mma_flops_per_algorithmic_flop": mma_factor,
-                "tensor_pipe_frac": ach_tf * mma_factor / bf16_burst, "hbm_frac": ach_gb / hbm,
+                "tensor_pipe_issue_frac": ach_tf * mma_factor / bf16_burst, "hbm_frac": ach_gb / hbm,
                 "combined_floor_ms_per_step": floor_ms,
-                "combined_frac": floor_ms / tc_ms if tc_ms else None,
-                "definition": "per launch floor = max(MMA FLOPs / bf16 peak, algorithmic bytes / HBM peak); "
-                              "combined_frac = sum of floors / sum of measured launch times (CUDA events, "
-                              "one un-graphed batch)"}
+                "combined_frac": floor_ms / float(prof["ms"][tc].sum()) if tc.any() else None,
+                "definition": "achieved = algorithmic FLOPs (2 x MACs executed on the surviving requests) / the "
+                              "contractions' time inside the timed graphed step (ms_per_step x their share of an "
+                              "un-graphed event-timed step); frac = achieved / peak. tensor_pipe_issue_frac counts "
+                              "the MMA FLOPs issued (x3 in bf16x3). combined_frac = sum of per-launch "
+                              "max(tensor floor, HBM floor) / sum of per-launch event times"}
     roofline_lookup = {"bound": "latency (per-row heads over L2-resident GAP partials; HBM bytes are negligible)",
                        "achieved": lk_bytes / (lk_ms * 1e-3) / 1e9 if lk_ms else 0.0,
                        "peak": hbm, "unit": "GB/s",
                        "frac": (lk_bytes / (lk_ms * 1e-3) / 1e9 / hbm) if lk_ms else 0.0,
-                       "kernel_ms_per_step": lk_ms, "share_of_step": lk_ms / step_ms if step_ms else None}
+                       "kernel_ms_per_step": lk_ms, "share_of_step": kind_share(lk)}
+    roofline_glue = {"bound": "hbm", "kernels": "stem space-to-depth, max-pool, base head, batch init",
+                     "algorithmic_bytes_per_step": glue_bytes, "kernel_ms_per_step": glue_ms,
+                     "achieved": glue_bytes / (glue_ms * 1e-3) / 1e9 if glue_ms else 0.0, "peak": hbm, "unit": "GB/s",
+                     "frac": glue_bytes / (glue_ms * 1e-3) / 1e9 / hbm if glue_ms else 0.0,
+                     "share_of_step": kind_share(glue)}
 
     line = {
         "metric": metric, "value": value, "unit": "requests/s", "n_gpus": world, "steps": args.steps,
@@ -402,9 +443,9 @@ def main():
         "hit_rate": hit_rate, "hits_by_layer": hits_by_layer,
         "e2e": {"value": total_req / e2e_max, "unit": "requests/s",
                 "h2d_bytes_per_step": int(inputs[0].nbytes),
-                "d2h_bytes_per_step": int(B * (4 * 3 + 8) + B * m.num_blocks * 4)},
+                "d2h_bytes_per_step": int(B * (4 * 3 + 8) + B * m.num_blocks * 4 + B * m.num_classes * 4 + 8)},
         "gpu_launches": dep.kernel_count() * args.steps,
-        "roofline": roofline, "roofline_lookup": roofline_lookup,
+        "roofline": roofline, "roofline_lookup": roofline_lookup, "roofline_glue": roofline_glue,
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

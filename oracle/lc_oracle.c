@@ -343,3 +343,75 @@ int lco_cnn_forward_batch(const lco_cnn_op* ops, int nops, int nbufs, size_t buf
   free(th);
   return err ? -1 : 0;
 }
+
+/* ------------------------------------------------------------ RNG
+ * rng.hpp:15-98 restated: splitmix64 seeding, xoshiro256**, 53-bit doubles,
+ * Box-Muller with a cached spare, mix_seed. */
+static unsigned long long lco_splitmix64(unsigned long long* state) {
+  unsigned long long z = (*state += 0x9e3779b97f4a7c15ULL);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+unsigned long long lco_mix_seed(unsigned long long seed, unsigned long long tag) {
+  unsigned long long s = seed + 0x9e3779b97f4a7c15ULL * (tag + 0x632be59bd9b4e019ULL);
+  const unsigned long long a = lco_splitmix64(&s);
+  const unsigned long long b = lco_splitmix64(&s);
+  return a ^ (b << 1);
+}
+
+void lco_rng_init(lco_rng* r, unsigned long long seed) {
+  unsigned long long sm = seed;
+  for (int i = 0; i < 4; ++i) r->s[i] = lco_splitmix64(&sm);
+  r->has_spare = 0;
+  r->spare = 0.0;
+}
+
+static unsigned long long lco_rotl(unsigned long long x, int k) { return (x << k) | (x >> (64 - k)); }
+
+static unsigned long long lco_next_u64(lco_rng* r) {
+  unsigned long long* s = r->s;
+  const unsigned long long result = lco_rotl(s[1] * 5, 7) * 9;
+  const unsigned long long t = s[1] << 17;
+  s[2] ^= s[0];
+  s[3] ^= s[1];
+  s[1] ^= s[2];
+  s[0] ^= s[3];
+  s[2] ^= t;
+  s[3] = lco_rotl(s[3], 45);
+  return result;
+}
+
+static double lco_next_double(lco_rng* r) { return (double)(lco_next_u64(r) >> 11) * 0x1.0p-53; }
+
+double lco_rng_uniform(lco_rng* r, double lo, double hi) { return lo + (hi - lo) * lco_next_double(r); }
+
+double lco_rng_normal(lco_rng* r) {
+  if (r->has_spare) {
+    r->has_spare = 0;
+    return r->spare;
+  }
+  const double u1 = 1.0 - lco_next_double(r);
+  const double u2 = lco_next_double(r);
+  const double rad = sqrt(-2.0 * log(u1));
+  const double theta = 2.0 * 3.14159265358979323846 * u2;
+  r->spare = rad * sin(theta);
+  r->has_spare = 1;
+  return rad * cos(theta);
+}
+
+void lco_rng_normal_fill(lco_rng* r, double* out, size_t n, double scale) {
+  for (size_t i = 0; i < n; ++i) out[i] = lco_rng_normal(r) * scale;
+}
+
+void lco_rng_uniform_fill(lco_rng* r, double* out, size_t n, double lo, double hi) {
+  for (size_t i = 0; i < n; ++i) out[i] = lco_rng_uniform(r, lo, hi);
+}
+
+void lco_rng_bn_fill(lco_rng* r, int n, double gain, double* scale, double* shift) {
+  for (int c = 0; c < n; ++c) {
+    scale[c] = gain * lco_rng_uniform(r, 0.8, 1.2);
+    shift[c] = lco_rng_uniform(r, -0.1, 0.1);
+  }
+}

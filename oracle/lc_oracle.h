@@ -90,6 +90,26 @@ int lco_cnn_forward_batch(const lco_cnn_op* ops, int nops, int nbufs, size_t buf
                           int B, int ntaps, double** taps_out, const size_t* tap_dims, double* logits, int classes,
                           int threads);
 
+/* ------------------------------------------------------------ RNG (rng.hpp:15-98)
+ * splitmix64 / xoshiro256** / Box-Muller with a spare, mix_seed: the reference's
+ * stream derivation. Used by oracle/cnn_models.py to rebuild the synthetic CNN
+ * weights without the product library (the reference arm of bench.py). */
+typedef struct {
+  unsigned long long s[4];
+  int has_spare;
+  double spare;
+} lco_rng;
+unsigned long long lco_mix_seed(unsigned long long seed, unsigned long long tag);
+void lco_rng_init(lco_rng* r, unsigned long long seed);
+double lco_rng_uniform(lco_rng* r, double lo, double hi);
+double lco_rng_normal(lco_rng* r);
+/* out[i] = normal() * scale, i < n */
+void lco_rng_normal_fill(lco_rng* r, double* out, size_t n, double scale);
+/* out[i] = uniform(lo, hi), i < n */
+void lco_rng_uniform_fill(lco_rng* r, double* out, size_t n, double lo, double hi);
+/* per channel c: scale[c] = gain * uniform(0.8, 1.2); shift[c] = uniform(-0.1, 0.1) */
+void lco_rng_bn_fill(lco_rng* r, int n, double gain, double* scale, double* shift);
+
 #ifdef __cplusplus
 }
 #endif

@@ -777,7 +777,8 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow) {
       steps.push_back({[this, o, g, X, counts, B](cudaStream_t s) {
                          launch_stem_s2d(d_x_, counts, B, o.C, o.H, o.W, o.stride, o.pad, g, X.hi, X.lo, s);
                        },
-                       0});
+                       0, 1, 0, 0.0,
+                       4.0 * o.C * o.H * o.W + (x3 ? 4.0 : 2.0) * 2.0 * g.Hx * g.Wx * 8});
       StemParams sp{};
       sp.x_hi = X.hi;
       sp.x_lo = x3 ? X.lo : nullptr;
@@ -806,7 +807,8 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow) {
                          launch_maxpool(in.hi, in.lo, o.H, o.W, o.C, o.k, o.stride, o.pad, Ho, Wo, cur_ids, cur_count,
                                         B, out.hi, out.lo, s);
                        },
-                       0});
+                       0, 1, static_cast<int>(cur_count - d_counts_), 0.0,
+                       (x3 ? 4.0 : 2.0) * (static_cast<double>(o.H) * o.W * o.C + static_cast<double>(Ho) * Wo * o.C)});
     } else if (o.kind == CnnOpKind::Conv) {
       const DevConv& dc = cnn_w_[i];
       Planes in = slot_buf_[static_cast<size_t>(o.in)], out = slot_buf_[static_cast<size_t>(o.out)];
@@ -937,7 +939,8 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow) {
                          launch_cnn_head(in.hi, in.lo, C, HW, head_w_, head_b_, classes, cur_ids, cur_count, B,
                                          d_base_, d_logits_, d_exit_, d_served_, d_exit_ns_, fs, ls, s);
                        },
-                       0, classes > 32 ? 3 : 1});
+                       0, classes > 32 ? 3 : 1, static_cast<int>(cur_count - d_counts_),
+                       2.0 * C * classes, (x3 ? 4.0 : 2.0) * static_cast<double>(C) * HW + 4.0 * classes});
     }
     if (o.tap >= 0) {
       const int layer = o.tap + 1;

@@ -204,3 +204,24 @@ def test_oracle_mlp_taps_and_logits_bit_exact_vs_reference():
         for k in range(model["blocks"]):
             assert np.array_equal(taps[k][i], rt[k])
         assert np.array_equal(logits[i], rm.logits(x[i]))
+
+
+@pytest.mark.parametrize("arch,classes", [("resnet18_cifar", 10), ("resnet50", 1000), ("vgg16_cifar", 10)])
+def test_oracle_cnn_builder_matches_product(arch, classes):
+    """oracle/cnn_models.py rebuilds the product's synthetic CNN (host/cnn.cpp)
+    from the reference RNG without the product library: same ops, geometry,
+    taps and weights bit for bit. bench.py's reference arm relies on it."""
+    import paper_2101_07344_b200 as lcb
+    from oracle.cnn_models import CnnModel
+    ours = CnnModel(arch, classes, 2101)
+    m = lcb.make_cnn_model(arch, classes, 2101)
+    prod = m.cnn_ops()
+    assert ours.nslots == m.nslots and ours.tap_dims == m.tap_dims and len(ours.ops) == len(prod)
+    for a, b in zip(ours.ops, prod):
+        for k in ("kind", "in", "out", "res", "C", "H", "W", "Cout", "k", "stride", "pad", "relu", "tap"):
+            assert a[k] == b[k], (k, a[k], b[k])
+        for k in ("w", "scale", "shift"):
+            if b[k] is None or len(b[k]) == 0:
+                assert a[k] is None or len(a[k]) == 0 or not np.any(a[k]), k
+            else:
+                assert np.array_equal(a[k], b[k]), k

@@ -53,5 +53,6 @@ for k, (n, t, b) in sorted(agg.items(), key=lambda x: -x[1][1]):
 if len(sys.argv) > 2:
     json.dump({"dram_bytes_per_step": tc_bytes, "launches": tc_n, "ncu_us_per_step": tc_us,
                "source": sys.argv[1].split("/")[-1],
+               "by_kernel": {k: {"launches": n, "ncu_us": t, "dram_bytes": b} for k, (n, t, b) in agg.items()},
                "note": "sum over the step's tc_conv/tc_stem launches of dram__bytes_read.sum + dram__bytes_write.sum "
                        "(ncu, cache control all = cold L2 per launch)"}, open(sys.argv[2], "w"), indent=1)
