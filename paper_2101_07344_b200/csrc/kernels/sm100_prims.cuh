@@ -209,6 +209,32 @@ __device__ __forceinline__ void umma_kstep_bf16(uint32_t tmem_d, uint64_t dah, u
       : "memory");
 }
 
+// One 64-channel residual K-step of bf16x3 (the residual add on the tensor
+// core: residual planes against an identity B, which has no lo plane): per
+// K16 hi*I and lo*I at N = BN, under one elect.sync, then the stage commit.
+__device__ __forceinline__ void umma_kstep_x3_res(uint32_t tmem_d, uint64_t dah, uint64_t dal, uint64_t dbh,
+                                                  uint32_t idesc, uint32_t accumulate, uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred p, e, t;\n\t.reg .b64 a1, a2, a3, l1, l2, l3, b1, b2, b3;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %5, 0;\n\t"
+      "setp.eq.b32 t, 0, 0;\n\t"
+      "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
+      "add.s64 l1, %2, 2;\n\tadd.s64 l2, %2, 4;\n\tadd.s64 l3, %2, 6;\n\t"
+      "add.s64 b1, %3, 2;\n\tadd.s64 b2, %3, 4;\n\tadd.s64 b3, %3, 6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %3, %4, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %3, %4, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %4, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], l1, b1, %4, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %4, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], l2, b2, %4, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %4, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], l3, b3, %4, t;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n\t}" ::"r"(tmem_d),
+      "l"(dah), "l"(dal), "l"(dbh), "r"(idesc), "r"(accumulate), "r"(bar)
+      : "memory");
+}
+
 __device__ __forceinline__ void umma_commit_warp(uint32_t bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"

@@ -152,10 +152,10 @@ __device__ __forceinline__ unsigned long long clk() {
 }
 
 // Trace slot (debug instrumentation): CTA < kTraceCtas, unit < kTraceUnits.
-constexpr int kTraceCtas = 8, kTraceUnits = 32;
+constexpr int kTraceCtas = 8, kTraceUnits = 32, kTraceFields = 32;
 __device__ __forceinline__ void trace_put(const TcConvParams& p, int unit, int field) {
   if (p.trace && blockIdx.x < kTraceCtas && unit < kTraceUnits)
-    p.trace[(blockIdx.x * kTraceUnits + unit) * 16 + field] = clk();
+    p.trace[(blockIdx.x * kTraceUnits + unit) * kTraceFields + field] = clk();
 }
 
 // Per-K-step wait/issue cycle counters (trace fields 12-14): compiled only
@@ -167,7 +167,7 @@ __device__ __forceinline__ void trace_put(const TcConvParams& p, int unit, int f
 #define TC_TRACE(...)
 #endif
 __device__ __forceinline__ void trace_val(const TcConvParams& p, int unit, int field, unsigned long long v) {
-  if (p.trace && blockIdx.x < kTraceCtas && unit < kTraceUnits) p.trace[(blockIdx.x * kTraceUnits + unit) * 16 + field] = v;
+  if (p.trace && blockIdx.x < kTraceCtas && unit < kTraceUnits) p.trace[(blockIdx.x * kTraceUnits + unit) * kTraceFields + field] = v;
 }
 
 // Tile-invariant part of a tile row's output coordinates: image slot j and
@@ -491,7 +491,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
   using Cfg = TcCfg<BN, X3>;
   constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned base for the swizzled operands, derived by offsetting
+  // the __shared__ array itself so the compiler keeps the shared address space
+  // (plain C++ accesses, e.g. the epilogue's shift values, become LDS rather
+  // than generic loads through the global path)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   // stage s: [A_hi][A_lo?][B_hi][B_lo?]
   // barriers: [0,8) full (stages / halo B ring), [8,16) empty, [16,18) tfull,
   // [18,20) tempty, [20,22) halo A-slab full, [22,24) halo A-slab empty
@@ -849,6 +853,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
             umma_kstep_x3_stacked(d_tmem, dah, dal, dbh, idesc2, idesc, s > x.s_begin ? 1u : 0u, eb);
           } else if (fused_issue && X3 && !res_step) {
             umma_kstep_x3_plain(d_tmem, dah, dal, dbh, dbl, idesc, s > x.s_begin ? 1u : 0u, eb);
+          } else if (fused_issue && X3 && res_step) {
+            umma_kstep_x3_res(d_tmem, dah, dal, dbh, idesc, s > x.s_begin ? 1u : 0u, eb);
           } else if (fused_issue && !X3) {
             umma_kstep_bf16(d_tmem, dah, dbh, idesc, s > x.s_begin ? 1u : 0u, eb);
           } else {

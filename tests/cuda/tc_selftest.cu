@@ -434,6 +434,7 @@ static void choose_box(int Ho, int Wo, int& hb, int& wb, int& ipt) {
 }
 
 // Timing of one conv layer shape (no CPU check): `nsurv` of N images survive.
+static bool g_force_trace = false;  // --one K --trace
 static void perf_conv(const char* name, int N, int nsurv, int H, int W, int C, int Cout, int k, int stride, bool x3,
                       bool use_res, int ks_max, bool trace) {
   const int pad = k / 2;
@@ -468,8 +469,8 @@ static void perf_conv(const char* name, int N, int nsurv, int H, int W, int C, i
   CK(cudaMalloc(&dCtr, 4 * g_sms * 4));
   CK(cudaMemset(dCtr, 0, 4 * g_sms * 4));
   unsigned long long* dTrace;
-  CK(cudaMalloc(&dTrace, 8 * 32 * 16 * 8));
-  CK(cudaMemset(dTrace, 0, 8 * 32 * 16 * 8));
+  CK(cudaMalloc(&dTrace, 8 * 32 * 32 * 8));
+  CK(cudaMemset(dTrace, 0, 8 * 32 * 32 * 8));
   TcConvParams p;
   memset(&p, 0, sizeof(p));
   int hb, wb, ipt;
@@ -561,23 +562,28 @@ static void perf_conv(const char* name, int N, int nsurv, int H, int W, int C, i
   printf("perf %-26s N=%3d/%3d %3dx%-3d C=%4d->%4d k=%d s=%d %s%s BN=%d: %8.1f us  %7.1f TFLOP/s alg  (%5.1f%% tensor of 1590)\n",
          name, nsurv, N, H, W, C, Cout, k, stride, x3 ? "x3 " : "b16", halo ? " halo" : "", BN, ms * 1e3, tf,
          100.0 * tf * (x3 ? 3 : 1) / 1590.0);
-  if (trace) {
+  if (trace || g_force_trace) {
     p.trace = dTrace;
     CK(tc_conv_launch(p, BN, g_sms, 0));
     CK(cudaDeviceSynchronize());
-    std::vector<unsigned long long> tr(8 * 32 * 16);
+    std::vector<unsigned long long> tr(8 * 32 * 32);
     CK(cudaMemcpy(tr.data(), dTrace, tr.size() * 8, cudaMemcpyDeviceToHost));
     for (int cta = 0; cta < 2; ++cta) {
-      const unsigned long long t0 = tr[(cta * 32) * 16 + 0];
+      const unsigned long long t0 = tr[(cta * 32) * 32 + 0];
       printf("  trace CTA %d (cycles from first TMA issue): unit: tma0 tmaN | mma0 mmaN | epi0 epiN | split: fenced waited\n", cta);
       for (int u = 0; u < 32; ++u) {
-        const unsigned long long* q = &tr[(cta * 32 + u) * 16];
+        const unsigned long long* q = &tr[(cta * 32 + u) * 32];
         if (!q[0] && !q[4]) break;
         auto rel = [&](unsigned long long v) { return v ? (long long)(v - t0) : -1LL; };
         printf("   %2d: %8lld %8lld | %8lld %8lld | %8lld %8lld | %8lld %8lld | red %8lld w0 %8lld w1 %8lld end %8lld"
                " | mma wait %6llu issue %6llu | tma wait %6llu | red loads %lld stored %lld\n",
                u, rel(q[0]), rel(q[1]), rel(q[2]), rel(q[3]), rel(q[4]), rel(q[5]), rel(q[6]), rel(q[7]), rel(q[8]),
                rel(q[9]), rel(q[10]), rel(q[11]), q[12], q[13], q[14], rel(q[15]), q[15] ? rel(q[12]) : -1LL);
+        if (q[16])
+          printf("       epi steps (from epi0): s0 data %lld staged %lld stored %lld | s1 data %lld staged %lld stored %lld\n",
+                 (long long)(q[16] - q[4]), (long long)(q[17] - q[4]), (long long)(q[18] - q[4]),
+                 q[20] ? (long long)(q[20] - q[4]) : -1LL, q[21] ? (long long)(q[21] - q[4]) : -1LL,
+                 q[22] ? (long long)(q[22] - q[4]) : -1LL);
       }
     }
   }
@@ -621,6 +627,7 @@ int main(int argc, char** argv) {
   }
   if (argc > 2 && strcmp(argv[1], "--one") == 0) {
     g_only = atoi(argv[2]);
+    g_force_trace = argc > 3 && strcmp(argv[3], "--trace") == 0;
     perf_layers(false);
     return 0;
   }
