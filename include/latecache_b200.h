@@ -254,13 +254,16 @@ int lc_run_adaptation(lc_engine* e, const float* inputs, int n_samples, const do
 int lc_engine_variant(lc_engine* e, int k, lc_variant** out);
 
 /* Hardware-aware costs (replaces CostModel::lookup_ms, cache.hpp:46-55, and the
- * modeled LayerProfile, composer.hpp): one shadow batch of the B host requests
- * through the graph with device timestamps at every block boundary.
+ * modeled LayerProfile, composer.hpp): one batch of the B host requests through
+ * the graph with device timestamps at every block boundary: flags
+ * LC_SERVE_SHADOW = every request runs every block (the reference's
+ * LayerProfile semantics), 0 = the compacted step (survivors only).
  * block_ms[blocks] = base-model device time per block (block 1 includes the
  * stem, the last block the head) — the LayerProfile for check_constraints /
  * compose; lookup_ms[blocks] = cache lookup + exit time at each layer (0 where
  * no cache is attached) — the VariantMetrics::lookup_ms column. */
-int lc_engine_layer_times(lc_engine* e, const float* inputs, int B, double* block_ms, double* lookup_ms);
+int lc_engine_layer_times(lc_engine* e, const float* inputs, int B, unsigned flags, double* block_ms,
+                          double* lookup_ms);
 
 /* Device time of `iters` graph replays of a B-request batch (CUDA events on the engine stream). */
 int lc_engine_time(lc_engine* e, int B, unsigned flags, int iters, double* ms_per_batch);

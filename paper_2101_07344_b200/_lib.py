@@ -106,7 +106,7 @@ def _load() -> C.CDLL:
         "lc_lookup_batch": (I, [P, I, pF, I, pI, pI, pF, pF, pF]),
         "lc_measure_metrics": (I, [P, pF, I, pD, I, C.POINTER(C.c_longlong)]),
         "lc_serve_submit": (I, [P, pF, I, C.c_uint, pI]),
-        "lc_engine_layer_times": (I, [P, pF, I, pD, pD]),
+        "lc_engine_layer_times": (I, [P, pF, I, C.c_uint, pD, pD]),
         "lc_model_save_binary": (I, [P, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t)]),
         "lc_model_load_binary": (I, [C.c_char_p, C.c_size_t, C.POINTER(C.c_void_p)]),
         "lc_variant_save_binary": (I, [P, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t)]),

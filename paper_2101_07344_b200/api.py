@@ -499,14 +499,16 @@ class Deployment:
                 v.delta = out[v.layer]
         return out
 
-    def layer_times(self, inputs: np.ndarray):
+    def layer_times(self, inputs: np.ndarray, shadow: bool = True):
         """Hardware-aware profile: device-measured base time
         per block (the LayerProfile) and lookup time per cache layer (the
-        VariantMetrics::lookup_ms column) from one shadow batch of `inputs`."""
+        VariantMetrics::lookup_ms column) from one shadow batch of `inputs`
+        (shadow=False: the compacted step, survivors only)."""
         x = np.ascontiguousarray(inputs, dtype=np.float32)
         bm = np.zeros(self.blocks, np.float64)
         lm = np.zeros(self.blocks, np.float64)
-        check(lib.lc_engine_layer_times(self._h, _fptr(x), x.shape[0], _dptr(bm), _dptr(lm)))
+        check(lib.lc_engine_layer_times(self._h, _fptr(x), x.shape[0], LC_SERVE_SHADOW if shadow else 0, _dptr(bm),
+                                        _dptr(lm)))
         return bm, {v.layer: float(lm[v.layer - 1]) for v in self.variants}
 
     def time_batch(self, B: int, iters: int, shadow: bool = False) -> float:

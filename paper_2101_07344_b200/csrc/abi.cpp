@@ -646,7 +646,8 @@ int lc_tune_delta(lc_engine* e, const float* inputs, int B, double target_accura
   });
 }
 
-int lc_engine_layer_times(lc_engine* e, const float* inputs, int B, double* block_ms, double* lookup_ms) {
+int lc_engine_layer_times(lc_engine* e, const float* inputs, int B, unsigned flags, double* block_ms,
+                          double* lookup_ms) {
   return guard([&] {
     need(inputs, "inputs");
     need(block_ms, "block_ms");
@@ -657,7 +658,7 @@ int lc_engine_layer_times(lc_engine* e, const float* inputs, int B, double* bloc
     if (cudaSetDevice(en.device()) != cudaSuccess ||
         cudaMemcpyAsync(en.input_buffer(), inputs, bytes, cudaMemcpyHostToDevice, en.stream()) != cudaSuccess)
       throw lcb::CudaFailure("layer_times: input copy failed");
-    en.layer_times(B, block_ms, lookup_ms);
+    en.layer_times(B, block_ms, lookup_ms, (flags & LC_SERVE_SHADOW) == 0);
   });
 }
 

@@ -111,6 +111,9 @@ struct DevCache {
   // fused GAP partials written by the tap conv's epilogue (Pool(C) caches)
   float* gap = nullptr;
   int gap_segs = 0;
+  // the tap conv also finishes the lookup: features only (conv_feat, the head
+  // runs separately on them) or the whole head + exit (conv_head)
+  bool conv_feat = false, conv_head = false;
   // lookup-only step list
   std::vector<Step> lookup_steps;
 };
@@ -211,6 +214,7 @@ Engine::Engine(int device, const BaseModel& model, std::vector<CacheVariant> var
   gap_fusion_ = !(nf && nf[0] == '1');
   const char* nl = std::getenv("LCB_UNFUSED_LOOKUP");
   fused_lookup_ = !(nl && nl[0] == '1');
+  if (const char* nc = std::getenv("LCB_NO_CONV_HEAD")) conv_head_ = !(nc[0] == '1');
   const char* ns = std::getenv("LCB_NO_STACKED");
   stacked_ = !(ns && ns[0] == '1');
   if (const char* km = std::getenv("LCB_KS_MIN_STEPS")) ks_min_steps_ = std::atoi(km);
@@ -270,6 +274,10 @@ void Engine::build_weights() {
   d_conf_ = static_cast<unsigned long long*>(dalloc(static_cast<size_t>(L) * 64 * 4 * sizeof(unsigned long long)));
   d_lk_count_ = static_cast<int*>(dalloc(sizeof(int)));
   lk_arrive_ = static_cast<int*>(dalloc(sizeof(int)));
+  row_tiles_ = static_cast<int*>(dalloc(static_cast<size_t>(B) * sizeof(int)));
+  ck(cudaMemsetAsync(row_tiles_, 0, static_cast<size_t>(B) * sizeof(int), stream_), "memset");
+  heads_done_ = static_cast<int*>(dalloc(sizeof(int)));
+  ck(cudaMemsetAsync(heads_done_, 0, sizeof(int), stream_), "memset");
   ck(cudaMemsetAsync(lk_arrive_, 0, sizeof(int), stream_), "memset");
   ws_ = static_cast<float*>(dalloc(tc_conv_ws_floats(256, num_sms_) * sizeof(float)));
   ws_counters_ = static_cast<int*>(dalloc(2 * static_cast<size_t>(num_sms_) * sizeof(int)));
@@ -483,6 +491,8 @@ void Engine::add_lookup_steps(std::vector<Step>& steps, DevCache& c, const TapVi
   double head_bytes = 0.0;  // per surviving row, beyond the (L2-resident) head weights
   if (head_gap) {
     head_bytes = 4.0 * c.gap_segs * c.width;
+  } else if (c.family == 1 && fused_gap && c.gap && c.conv_feat) {
+    // the tap conv already wrote the GAP features into c.feats
   } else if (c.family == 1 && fused_gap && c.gap) {
     steps.push_back({[cp, tap, max_rows](cudaStream_t s) {
                        launch_gap_bins(cp->gap, cp->gap_segs, tap.C, tap.HW, tap.data_idx, tap.count, max_rows,
@@ -614,11 +624,11 @@ void Engine::add_stamp(std::vector<Step>& steps, int layer, int which) {
   steps.push_back({[dst](cudaStream_t s) { launch_stamp_start(dst, s); }, 0, 1});
 }
 
-void Engine::layer_times(int B, double* block_ms, double* lookup_ms) {
+void Engine::layer_times(int B, double* block_ms, double* lookup_ms, bool compact) {
   std::lock_guard<std::recursive_mutex> dev_lock(dev_stream(device_).mu);
   const int L = model_.num_blocks;
   ck(cudaMemsetAsync(d_block_ns_, 0, static_cast<size_t>(L + 1) * 2 * 8, stream_), "memset");
-  serve(B, true, true);
+  serve_mode(B, compact ? kModeCompactStamped : kModeShadow, true);
   std::vector<unsigned long long> ns(static_cast<size_t>(L + 1) * 2);
   unsigned long long t0 = 0;
   ck(cudaMemcpyAsync(ns.data(), d_block_ns_, ns.size() * 8, cudaMemcpyDeviceToHost, stream_), "d2h");
@@ -637,7 +647,7 @@ void Engine::layer_times(int B, double* block_ms, double* lookup_ms) {
 }
 
 // ------------------------------------------------------------------ MLP serve
-void Engine::build_mlp_steps(std::vector<Step>& steps, bool shadow) {
+void Engine::build_mlp_steps(std::vector<Step>& steps, bool shadow, bool stamps) {
   const int B = max_batch_, L = model_.num_blocks;
   const bool x3 = prec_ == kPrecX3;
   int* ids = d_ids_;
@@ -702,7 +712,7 @@ void Engine::build_mlp_steps(std::vector<Step>& steps, bool shadow) {
                      (x3 ? 4.0 : 2.0) * (static_cast<double>(f.inp) + f.outp)});
     const int layer = b + 1;
     if (shadow) tap_step_end_[static_cast<size_t>(layer)] = static_cast<int>(steps.size());
-    if (shadow) add_stamp(steps, layer, 0);
+    if (stamps) add_stamp(steps, layer, 0);
     const int ci = cache_of_layer_[static_cast<size_t>(layer)];
     if (ci >= 0) {
       DevCache& c = *caches_[static_cast<size_t>(ci)];
@@ -719,7 +729,7 @@ void Engine::build_mlp_steps(std::vector<Step>& steps, bool shadow) {
       int* cnt_out = counts + layer;
       const ExitParams ex = exit_params(layer, shadow, cur_ids, ids_out, src_out, cnt_out);
       add_lookup_steps(steps, c, tap, B, false, false, &ex);
-      if (shadow) add_stamp(steps, layer, 1);
+      if (stamps) add_stamp(steps, layer, 1);
       if (!shadow) {
         Planes dst = mlp_cin_[static_cast<size_t>(b)];
         const long long row_elems = f.outp;
@@ -744,11 +754,11 @@ void Engine::build_mlp_steps(std::vector<Step>& steps, bool shadow) {
                                      cur_count, B, d_base_, d_logits_, d_exit_, d_served_, d_exit_ns_, s);
                    },
                    0});
-  if (shadow) add_stamp(steps, L + 1, 0);  // after the head (charged to the last block)
+  if (stamps) add_stamp(steps, L + 1, 0);  // after the head (charged to the last block)
 }
 
 // ------------------------------------------------------------------ CNN serve
-void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow) {
+void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow, bool stamps) {
   const int B = max_batch_, L = model_.num_blocks;
   const bool x3 = prec_ == kPrecX3;
   int* ids = d_ids_;
@@ -915,6 +925,46 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow) {
             }
             prm->gap_out = c.gap;
             prm->gap_segs = segs;
+            if (conv_head_ && fused_lookup_ && c.width % 4 == 0) {
+              // the lookup rides the conv: every row's GAP features (and, for
+              // <= 32 classes, its head and the layer's exit) come from the
+              // CTA that finishes the row's last tile
+              const int layer = o.tap + 1;
+              TcGapHead& gh = prm->gh;
+              gh.row_tiles = row_tiles_;
+              gh.inv = static_cast<float>(1.0 / (static_cast<double>(Ho) * Wo));
+              if (c.classes <= 32) {
+                const ExitParams ex = exit_params(layer, shadow, cur_ids, ids + static_cast<size_t>(layer) * B,
+                                                  nullptr, counts + layer);
+                gh.classes = c.classes;
+                gh.W2 = c.W2;
+                gh.b2 = c.b2;
+                gh.Ws1 = c.Ws1;
+                gh.bs1 = c.bs1;
+                gh.ws2 = c.ws2;
+                gh.bs2 = c.bs2;
+                gh.delta = c.delta;
+                gh.prob = c.prob;
+                gh.hit = c.hit;
+                gh.label = c.label;
+                gh.heads_done = heads_done_;
+                gh.layer = ex.layer;
+                gh.shadow = ex.shadow;
+                gh.ids_in = ex.ids_in;
+                gh.exit_layer = ex.exit_layer;
+                gh.served = ex.served;
+                gh.exit_ns = ex.exit_ns;
+                gh.probs_out = ex.probs_out;
+                gh.labels_out = ex.labels_out;
+                gh.ids_out = ex.ids_out;
+                gh.src_rows_out = ex.src_rows_out;
+                gh.count_out = ex.count_out;
+                c.conv_head = true;
+              } else {
+                gh.feat = c.feats;  // [B][width] bins for the separate head
+                c.conv_feat = true;
+              }
+            }
           }
         }
       }
@@ -925,7 +975,16 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow) {
           prm->tap_dh[t] = static_cast<signed char>(r - o.pad);
           prm->tap_dw[t] = static_cast<signed char>(sx - o.pad);
         }
-      steps.push_back({[prm, BN, sms](cudaStream_t s) { ck(tc_conv_launch(*prm, BN, sms, s), "tc_conv (conv)"); }, 1,
+      DevCache* head_cache = nullptr;  // threshold / selector bias are read at launch (set_delta, swaps)
+      if (prm->gh.row_tiles && prm->gh.classes) head_cache = caches_[static_cast<size_t>(cache_of_layer_[static_cast<size_t>(o.tap + 1)])].get();
+      steps.push_back({[prm, BN, sms, head_cache](cudaStream_t s) {
+                         if (head_cache) {
+                           prm->gh.delta = head_cache->delta;
+                           prm->gh.bs2 = head_cache->bs2;
+                         }
+                         ck(tc_conv_launch(*prm, BN, sms, s), "tc_conv (conv)");
+                       },
+                       1,
                        1, static_cast<int>(cur_count - d_counts_),
                        2.0 * Ho * Wo * o.Cout * static_cast<double>(o.C) * o.k * o.k,
                        (x3 ? 4.0 : 2.0) * (static_cast<double>(o.H) * o.W * o.C +
@@ -945,7 +1004,7 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow) {
     if (o.tap >= 0) {
       const int layer = o.tap + 1;
       if (shadow) tap_step_end_[static_cast<size_t>(layer)] = static_cast<int>(steps.size());
-      if (shadow) add_stamp(steps, layer, 0);
+      if (stamps) add_stamp(steps, layer, 0);
       const int ci = cache_of_layer_[static_cast<size_t>(layer)];
       if (ci >= 0) {
         DevCache& c = *caches_[static_cast<size_t>(ci)];
@@ -962,30 +1021,37 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow) {
         tap.data_idx = cur_ids;
         tap.count = cur_count;
         const ExitParams ex = exit_params(layer, shadow, cur_ids, ids_out, nullptr, cnt_out);
-        add_lookup_steps(steps, c, tap, B, true, c.gap != nullptr, &ex);
-        if (shadow) add_stamp(steps, layer, 1);
+        if (!c.conv_head) add_lookup_steps(steps, c, tap, B, true, c.gap != nullptr, &ex);
+        if (stamps) add_stamp(steps, layer, 1);
         cur_ids = ids_out;
         cur_count = cnt_out;
       }
     }
   }
-  if (shadow) add_stamp(steps, L + 1, 0);  // after the head (charged to the last block)
+  if (stamps) add_stamp(steps, L + 1, 0);  // after the head (charged to the last block)
 }
 
-std::vector<Step>& Engine::steps_for(bool shadow) {
-  std::vector<Step>& st = shadow ? steps_shadow_ : steps_compact_;
-  bool& built = shadow ? built_shadow_ : built_compact_;
-  if (!built) {
+std::vector<Step>& Engine::steps_for(bool shadow) { return steps_mode(shadow ? kModeShadow : kModeCompact); }
+
+// Step lists: compact (the product), shadow (with block-boundary stamps; also
+// the tap read-back prefix), compact with stamps (per-block device times of
+// the compacted step, tools/layer_times.py).
+std::vector<Step>& Engine::steps_mode(int mode) {
+  std::vector<Step>& st = steps_[mode];
+  if (!built_[mode]) {
     st.clear();
+    const bool shadow = mode == kModeShadow, stamps = mode != kModeCompact;
     if (shadow) tap_step_end_.assign(static_cast<size_t>(model_.num_blocks) + 1, -1);
-    if (model_.family == "mlp") build_mlp_steps(st, shadow);
-    else build_cnn_steps(st, shadow);
-    built = true;
+    if (model_.family == "mlp") build_mlp_steps(st, shadow, stamps);
+    else build_cnn_steps(st, shadow, stamps);
+    built_[mode] = true;
   }
   return st;
 }
 
-int Engine::num_steps(bool shadow) const { return static_cast<int>((shadow ? steps_shadow_ : steps_compact_).size()); }
+int Engine::num_steps(bool shadow) const {
+  return static_cast<int>(steps_[shadow ? kModeShadow : kModeCompact].size());
+}
 
 int Engine::count_kernels(bool shadow, int kind) {
   const auto& st = steps_for(shadow);
@@ -995,12 +1061,14 @@ int Engine::count_kernels(bool shadow, int kind) {
   return n;
 }
 
-void Engine::serve(int B, bool shadow, bool use_graph) {
+void Engine::serve(int B, bool shadow, bool use_graph) { serve_mode(B, shadow ? kModeShadow : kModeCompact, use_graph); }
+
+void Engine::serve_mode(int B, int mode, bool use_graph) {
   std::lock_guard<std::recursive_mutex> dev_lock(dev_stream(device_).mu);
   require(B > 0 && B <= max_batch_, "serve: batch size " + std::to_string(B) + " outside [1, max_batch]");
   ck(cudaSetDevice(device_), "cudaSetDevice");
   launch_set_int(d_batch_, B, stream_);
-  std::vector<Step>& st = steps_for(shadow);
+  std::vector<Step>& st = steps_mode(mode);
   if (!use_graph) {
     static const bool sync_steps = std::getenv("LCB_SYNC_STEPS") != nullptr;  // debug: locate a failing step
     for (size_t i = 0; i < st.size(); ++i) {
@@ -1014,7 +1082,7 @@ void Engine::serve(int B, bool shadow, bool use_graph) {
     ck(cudaGetLastError(), "serve");
     return;
   }
-  cudaGraphExec_t& ge = graph_[shadow ? 1 : 0];
+  cudaGraphExec_t& ge = graph_[mode];
   if (!ge) {
     cudaGraph_t g;
     ck(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "capture");

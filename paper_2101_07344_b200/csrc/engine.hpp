@@ -100,7 +100,8 @@ class Engine {
   // boundary: block_ms[l] = base-model time of block l (the reference's
   // LayerProfile entries; block 1 includes the stem, the last block the head),
   // lookup_ms[l] = the cache lookup + exit at layer l (0 where none).
-  void layer_times(int B, double* block_ms, double* lookup_ms);
+  // compact: the same stamps in the compacted step (survivors only).
+  void layer_times(int B, double* block_ms, double* lookup_ms, bool compact = false);
   void set_delta(int layer, double delta);
   double delta(int layer) const;
   bool has_cache(int layer) const {
@@ -137,8 +138,11 @@ class Engine {
 
  private:
   void build_weights();
-  void build_mlp_steps(std::vector<Step>& steps, bool shadow);
-  void build_cnn_steps(std::vector<Step>& steps, bool shadow);
+  enum { kModeCompact = 0, kModeShadow = 1, kModeCompactStamped = 2, kModes = 3 };
+  void build_mlp_steps(std::vector<Step>& steps, bool shadow, bool stamps);
+  void build_cnn_steps(std::vector<Step>& steps, bool shadow, bool stamps);
+  std::vector<Step>& steps_mode(int mode);
+  void serve_mode(int B, int mode, bool use_graph);
   void add_lookup_steps(std::vector<Step>& steps, DevCache& c, const TapView& tap, int max_rows, bool stage_gather,
                         bool fused_gap = false, const ExitParams* ex = nullptr);
   ExitParams exit_params(int layer, bool shadow, const int* ids_in, int* ids_out, int* src_rows_out, int* count_out);
@@ -214,12 +218,17 @@ class Engine {
   bool wprefetch_ = true;  // LCB_NO_WPREFETCH=1: no L2 prefetch of conv weights before the PDL wait  // LCB_KS_MIN_STEPS: split-K floor of K-steps per split (CNN convs)  // LCB_NO_STACKED=1: three MMAs per bf16x3 K16 group everywhere
   bool halo_ = false;  // LCB_HALO=1: stride-1 convs load one padded-row halo slab per channel chunk  // LCB_UNFUSED_LOOKUP=1: gap_bins + head + exit_compact as three launches
   int* lk_arrive_ = nullptr;
+  // lookup fused into the tap conv (TcGapHead): per-row tile arrivals and the
+  // head arrival counter (both zeroed, reset in-kernel); LCB_NO_CONV_HEAD=1 off
+  int* row_tiles_ = nullptr;
+  int* heads_done_ = nullptr;
+  bool conv_head_ = true;
   Planes im2col_buf_;
 
-  std::vector<Step> steps_compact_, steps_shadow_;
+  std::vector<Step> steps_[kModes];
   std::vector<int> tap_step_end_;  // shadow step list: index one past the op producing tap l (by layer)
-  bool built_compact_ = false, built_shadow_ = false;
-  cudaGraphExec_t graph_[2] = {nullptr, nullptr};
+  bool built_[kModes] = {false, false, false};
+  cudaGraphExec_t graph_[kModes] = {nullptr, nullptr, nullptr};
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
   struct Slot {
     float* d_in = nullptr;  // staged input [max_batch][input_dim]

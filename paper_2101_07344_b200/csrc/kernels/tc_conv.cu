@@ -7,6 +7,8 @@
 //                 column half (w - 2) / 4 of the tile (two warps per quadrant)
 // Pipelines: smem ring full/empty (TMA <-> MMA), TMEM double buffer
 // tfull/tempty (MMA <-> epilogue), split-K tile counters (CTA <-> CTA).
+#include <cfloat>
+
 #include "pdl.cuh"
 #include "sm100_prims.cuh"
 #include "tc_conv.cuh"
@@ -386,13 +388,179 @@ __device__ __forceinline__ void gap_segment(const TcConvParams& p, const Tile& x
   }
 }
 
+// ------------------------------------------------------------ fused lookup
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ float wsum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float wmax(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// First-hit exit + stable compaction over the layer's n rows, run by the
+// epilogue warps of the CTA that finished the last head (serve_one's first
+// hit, serving.cpp:112-121): warp ballot + prefix over the 8 warps.
+__device__ __noinline__ void gap_exit(const TcGapHead& h, int n, int etid, int lane, int* sint) {
+  __threadfence();
+  const int warp = etid >> 5;
+  int* warp_tot = sint;  // [kEpiWarps]
+  int base = 0;
+  const unsigned long long now = globaltimer_ns();
+  for (int c0 = 0; c0 < n; c0 += kEpiThreads) {
+    const int r = c0 + etid;
+    const bool valid = r < n;
+    const bool hit = valid && __ldcg(h.hit + r) != 0;
+    const int id = valid ? h.ids_in[r] : -1;
+    if (valid) {
+      const int lab = __ldcg(h.label + r);
+      if (h.probs_out) h.probs_out[id] = __ldcg(h.prob + r);
+      if (h.labels_out) h.labels_out[id] = lab;
+      if (hit && h.exit_layer[id] == 0) {
+        h.exit_layer[id] = h.layer;
+        h.served[id] = lab;
+        h.exit_ns[id] = now;
+      }
+    }
+    const bool keep = valid && (h.shadow || !hit);
+    const unsigned mask = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) warp_tot[warp] = __popc(mask);
+    epi_bar();
+    int before = 0, total = 0;
+    for (int w = 0; w < kEpiWarps; ++w) {
+      const int t = warp_tot[w];
+      before += w < warp ? t : 0;
+      total += t;
+    }
+    if (keep) {
+      const int pos = base + before + __popc(mask & ((1u << lane) - 1u));
+      h.ids_out[pos] = id;
+      if (h.src_rows_out) h.src_rows_out[pos] = r;
+    }
+    base += total;
+    epi_bar();  // warp_tot reused by the next chunk
+  }
+  if (etid == 0) {
+    *h.count_out = base;
+    *h.heads_done = 0;
+  }
+}
+
+// The GAP features of survivor row r (every tile of the row is complete and
+// its partials visible), then the row's cache head when classes > 0.
+// fs: >= Cout + 64 floats of shared scratch; sint: >= 64 ints.
+__device__ __noinline__ void gap_row_head(const TcConvParams& p, int n, int r, int etid, int lane, float* fs,
+                                          int* sint) {
+  const TcGapHead& h = p.gh;
+  __threadfence();
+  const int img = p.surv ? p.surv[r] : r;
+  const float* src = p.gap_out + static_cast<size_t>(img) * p.gap_segs * p.Cout;
+  for (int c = etid; c < p.Cout; c += kEpiThreads) {
+    float a = 0.0f;
+    for (int sg = 0; sg < p.gap_segs; ++sg) a += __ldcg(src + static_cast<size_t>(sg) * p.Cout + c);
+    a *= h.inv;
+    fs[c] = a;
+    if (h.feat) h.feat[static_cast<size_t>(r) * p.Cout + c] = a;
+  }
+  if (etid == 0) h.row_tiles[r] = 0;  // ready for the next launch
+  if (h.classes == 0) return;
+  float* lg = fs + p.Cout;  // [32] logits, then [32] pr
+  epi_bar();
+  const int warp = etid >> 5;
+  for (int k = warp; k < h.classes; k += kEpiWarps) {
+    const float* wr = h.W2 + static_cast<size_t>(k) * p.Cout;
+    float a0 = 0.0f, a1 = 0.0f;
+    int c = lane;
+    for (; c + 32 < p.Cout; c += 64) {
+      a0 += __ldg(wr + c) * fs[c];
+      a1 += __ldg(wr + c + 32) * fs[c + 32];
+    }
+    if (c < p.Cout) a0 += __ldg(wr + c) * fs[c];
+    const float a = wsum(a0 + a1);
+    if (lane == 0) lg[k] = a + __ldg(h.b2 + k);
+  }
+  epi_bar();
+  if (warp == 0) {
+    const bool in = lane < h.classes;
+    const float l = in ? lg[lane] : -FLT_MAX;
+    const float m = wmax(l);
+    const float e = in ? expf(l - m) : 0.0f;
+    const float sum = wsum(e);
+    const float q = in ? expf(l - m) / sum : 0.0f;
+    // argmax(pr), lowest index on ties (tensor.hpp:57-63)
+    float bv = in ? q : -FLT_MAX;
+    int bi = in ? lane : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    // selector FC(C,16) + ReLU + FC(16,1)
+    float z = h.bs2;
+    for (int j = 0; j < 16; ++j) {
+      const float a = wsum(in ? __ldg(h.Ws1 + j * h.classes + lane) * q : 0.0f) + __ldg(h.bs1 + j);
+      z += __ldg(h.ws2 + j) * (a > 0.0f ? a : 0.0f);
+    }
+    float pz;
+    if (z >= 0.0f) {
+      pz = 1.0f / (1.0f + expf(-z));
+    } else {
+      const float ez = expf(z);
+      pz = ez / (1.0f + ez);
+    }
+    if (lane == 0) {
+      h.prob[r] = pz;
+      h.hit[r] = static_cast<double>(pz) >= h.delta ? 1 : 0;
+      h.label[r] = bi;
+      __threadfence();
+      sint[63] = atomicAdd(h.heads_done, 1) == n - 1 ? 1 : 0;
+    }
+  }
+  epi_bar();
+  if (sint[63]) gap_exit(h, n, etid, lane, sint);
+}
+
+// After a tile's GAP partials are written by every epilogue warp: count the
+// tile against each of its survivor rows; rows completed here get their
+// features (and head) from this CTA.
+__device__ __noinline__ void gap_complete(const TcConvParams& p, const TileGeom& g, const Tile& x, int etid, int lane,
+                                          float* fs, int* sint) {
+  __threadfence();
+  epi_bar();
+  const int ipt = p.halo ? 1 : p.ipt;
+  const int target = p.tiles_h * g.tiles_w * g.tiles_n;
+  if (etid < ipt) {
+    const int idx = x.grp * ipt + etid;
+    int r = -1;
+    if (idx < g.count && atomicAdd(p.gh.row_tiles + idx, 1) == target - 1) r = idx;
+    sint[etid] = r;
+  }
+  epi_bar();
+  for (int j = 0; j < ipt; ++j) {
+    const int r = sint[j];
+    if (r >= 0) gap_row_head(p, g.count, r, etid, lane, fs, sint + 16);
+    epi_bar();
+  }
+}
+
 // Split-K: publish this CTA's partial tile, wait for the other ks-1 CTAs of
 // the tile (all resident: one unit per CTA, single round), then reduce 1/ks of
 // the tile (warp units of 16 columns x 32 rows, fixed k order) and run the
 // epilogue on it. Kept out of line: it is the rare path.
 // scratch: >= 8 warps x 2 KB of shared memory (the epilogue staging area).
-__device__ __noinline__ void split_reduce(const TcConvParams& p, const TileGeom& g, const Tile& x, int BN, int etid,
-                                          int lane, int unit, uint8_t* scratch) {
+__device__ __noinline__ bool split_reduce(const TcConvParams& p, const TileGeom& g, const Tile& x, int BN, int etid,
+                                          int lane, int unit, uint8_t* scratch, int* last_flag) {
   int* arr = p.ws_counters + 2 * x.tile_mn;
   int* dep = arr + 1;
   __threadfence();
@@ -477,13 +645,18 @@ __device__ __noinline__ void split_reduce(const TcConvParams& p, const TileGeom&
     if (wpu > 1) epi_bar();  // park slots reused by the next round
   }
   if (etid == 0) trace_put(p, unit, 11);
+  if (p.gh.row_tiles) __threadfence();  // this CTA's GAP partials visible before its arrival
   epi_bar();
   if (etid == 0) {
-    if (atomicAdd(dep, 1) == g.ks - 1) {
+    const bool last = atomicAdd(dep, 1) == g.ks - 1;
+    if (last) {
       *arr = 0;
       *dep = 0;
     }
+    *last_flag = last ? 1 : 0;
   }
+  epi_bar();
+  return *last_flag != 0;
 }
 
 template <int BN, bool X3>
@@ -574,6 +747,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
 
   const TileGeom g = tile_geom(p, BN);
   const int cchunks = p.C / 64;
+  // fused lookup with no rows: nobody finishes a head, so the compaction count is written here
+  if (p.gh.row_tiles && p.gh.classes && g.count == 0 && blockIdx.x == 0 && threadIdx.x == 0) *p.gh.count_out = 0;
+  int* const sint = reinterpret_cast<int*>(bars + 64);  // 64 ints of epilogue flags (in the barrier block)
   const int cs = p.conv_stride > 0 ? p.conv_stride : 1;
 
   // halo mode ring carving (runtime): A-slab slots then B slots inside the stage region
@@ -1054,7 +1230,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
       if (lane == 0) mbar_arrive(tempty0 + 8 * acc);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
-      if (split) split_reduce(p, g, x, BN, etid, lane, unit, epi_stage);
+      if (split) {
+        if (split_reduce(p, g, x, BN, etid, lane, unit, epi_stage, sint + 127) && p.gh.row_tiles)
+          gap_complete(p, g, x, etid, lane, reinterpret_cast<float*>(epi_stage), sint);
+      } else if (p.gh.row_tiles) {
+        gap_complete(p, g, x, etid, lane, reinterpret_cast<float*>(epi_stage), sint);
+      }
       if (etid == 0) trace_put(p, unit, 5);
     }
   }

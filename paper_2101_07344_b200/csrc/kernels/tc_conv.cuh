@@ -33,6 +33,45 @@ namespace lcb {
 
 constexpr int kMaxTaps = 64;
 
+// Lookup fused into the producing conv (the learned cache's Pool(C) = GAP
+// predictor, cache.cpp:104-140 with window H*W, on the tap this conv
+// writes). Every tile's epilogue writes GAP partials; per survivor row an
+// arrival counter finds the CTA that finishes the row's last tile, and that
+// CTA's epilogue warps sum the row's partials (fixed order) into the GAP
+// features. With classes > 0 (<= 32) they also run the cache head — logits =
+// W2 feat + b2, softmax (losses.cpp:35-46), selector FC(C,16)+ReLU+FC(16,1),
+// branch-stable sigmoid (losses.cpp:26-33), inclusive p >= delta
+// (cache.cpp:259-265), argmax(pr) with the lowest index on ties — and the CTA
+// finishing the LAST row's head records first hits and compacts the survivors
+// (serve_one, serving.cpp:112-121): no separate lookup launch.
+struct TcGapHead {
+  int* row_tiles;          // nullptr = off; [max_rows] per-row tile arrivals (zeroed, reset by the finisher)
+  float inv;               // 1 / (Ho * Wo)
+  float* feat;             // nullable: [max_rows][Cout] fp32 GAP features by row (for a separate head)
+  int classes;             // 0 = features only; else <= 32: fused head + exit
+  const float* W2;         // [classes][Cout]
+  const float* b2;         // [classes]
+  const float* Ws1;        // [16][classes]
+  const float* bs1;        // [16]
+  const float* ws2;        // [16]
+  float bs2;
+  double delta;
+  float* prob;             // row-indexed outputs
+  int* hit;
+  int* label;
+  int* heads_done;         // arrival counter over rows (zeroed, reset by the last)
+  int layer, shadow;
+  const int* ids_in;       // row -> request id
+  int* exit_layer;
+  int* served;
+  unsigned long long* exit_ns;
+  float* probs_out;        // by request id (nullable)
+  int* labels_out;         // by request id (nullable)
+  int* ids_out;
+  int* src_rows_out;       // nullable
+  int* count_out;
+};
+
 struct TcConvParams {
   CUtensorMap tmA[2];  // activation planes hi, lo (5-D: C, W, H, N, P)
   CUtensorMap tmB[2];  // weight planes hi, lo (2-D: K, Cout)
@@ -86,6 +125,7 @@ struct TcConvParams {
   float* out_f32;
   float* gap_out;      // nullable: fused GAP partials [image][gap_segs][Cout] (NHWC conv mode only)
   int gap_segs;        // segments per image = tiles_h * tiles_w * max(1, hb*wb/32)
+  TcGapHead gh;        // fused lookup on the GAP partials (gh.row_tiles != nullptr)
   unsigned long long* trace;  // nullable debug: clock64 stamps [8 CTAs][32 units][8]
   // Weight planes to pull into L2 before the programmatic-launch wait (they do
   // not depend on upstream kernels): each CTA prefetches 1/grid of each plane.
