@@ -222,7 +222,7 @@ class Engine {
   // head arrival counter (both zeroed, reset in-kernel); LCB_NO_CONV_HEAD=1 off
   int* row_tiles_ = nullptr;
   int* heads_done_ = nullptr;
-  bool conv_head_ = true;
+  bool conv_head_ = false;  // LCB_NO_CONV_HEAD=0 opts in (measured slower: profiles/r02_fused_head_ab.txt)
   Planes im2col_buf_;
 
   std::vector<Step> steps_[kModes];

@@ -1,6 +1,7 @@
 // Serve-path kernels (see serve_kernels.cuh). All cache-head arithmetic is
 // fp32 with deterministic (fixed-order) reductions; only the activations are
 // bf16 hi (+lo) planes.
+#include "gpu_sync.cuh"
 #include "pdl.cuh"
 #include "serve_kernels.cuh"
 
@@ -712,12 +713,10 @@ __device__ void head_block(const CacheHeadParams& p, int r, const float* logits,
 __device__ void exit_tail(const ExitParams& e, int n, const float* prob, const int* hit, const int* label) {
   __shared__ int last_s, base_s;
   __shared__ int warp_tot[32];
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last_s = (atomicAdd(e.arrive, 1) == static_cast<int>(gridDim.x) - 1) ? 1 : 0;
+  __syncthreads();  // the CTA's head results before its (acq_rel) arrival
+  if (threadIdx.x == 0) last_s = (atom_add_acq_rel_gpu(e.arrive, 1) == static_cast<int>(gridDim.x) - 1) ? 1 : 0;
   __syncthreads();
   if (!last_s) return;
-  __threadfence();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   if (tid == 0) {
     base_s = 0;

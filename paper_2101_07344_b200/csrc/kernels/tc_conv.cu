@@ -9,6 +9,7 @@
 // tfull/tempty (MMA <-> epilogue), split-K tile counters (CTA <-> CTA).
 #include <cfloat>
 
+#include "gpu_sync.cuh"
 #include "pdl.cuh"
 #include "sm100_prims.cuh"
 #include "tc_conv.cuh"
@@ -141,11 +142,6 @@ constexpr int kEpiThreads = kEpiWarps * 32;
 constexpr int kThreads = 64 + kEpiThreads;
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
-__device__ __forceinline__ int ld_acquire(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 
 __device__ __forceinline__ unsigned long long clk() {
   unsigned long long t;
@@ -408,8 +404,9 @@ __device__ __forceinline__ float wmax(float v) {
 // First-hit exit + stable compaction over the layer's n rows, run by the
 // epilogue warps of the CTA that finished the last head (serve_one's first
 // hit, serving.cpp:112-121): warp ballot + prefix over the 8 warps.
+// (Visibility of every head's hit/label/prob: the acq_rel arrival that made
+// this CTA the last one, then the epilogue barrier.)
 __device__ __noinline__ void gap_exit(const TcGapHead& h, int n, int etid, int lane, int* sint) {
-  __threadfence();
   const int warp = etid >> 5;
   int* warp_tot = sint;  // [kEpiWarps]
   int base = 0;
@@ -459,7 +456,6 @@ __device__ __noinline__ void gap_exit(const TcGapHead& h, int n, int etid, int l
 __device__ __noinline__ void gap_row_head(const TcConvParams& p, int n, int r, int etid, int lane, float* fs,
                                           int* sint) {
   const TcGapHead& h = p.gh;
-  __threadfence();
   const int img = p.surv ? p.surv[r] : r;
   const float* src = p.gap_out + static_cast<size_t>(img) * p.gap_segs * p.Cout;
   for (int c = etid; c < p.Cout; c += kEpiThreads) {
@@ -523,8 +519,7 @@ __device__ __noinline__ void gap_row_head(const TcConvParams& p, int n, int r, i
       h.prob[r] = pz;
       h.hit[r] = static_cast<double>(pz) >= h.delta ? 1 : 0;
       h.label[r] = bi;
-      __threadfence();
-      sint[63] = atomicAdd(h.heads_done, 1) == n - 1 ? 1 : 0;
+      sint[63] = atom_add_acq_rel_gpu(h.heads_done, 1) == n - 1 ? 1 : 0;
     }
   }
   epi_bar();
@@ -536,14 +531,13 @@ __device__ __noinline__ void gap_row_head(const TcConvParams& p, int n, int r, i
 // features (and head) from this CTA.
 __device__ __noinline__ void gap_complete(const TcConvParams& p, const TileGeom& g, const Tile& x, int etid, int lane,
                                           float* fs, int* sint) {
-  __threadfence();
-  epi_bar();
+  epi_bar();  // the tile's GAP partials (every epilogue warp) before the arrivals
   const int ipt = p.halo ? 1 : p.ipt;
   const int target = p.tiles_h * g.tiles_w * g.tiles_n;
   if (etid < ipt) {
     const int idx = x.grp * ipt + etid;
     int r = -1;
-    if (idx < g.count && atomicAdd(p.gh.row_tiles + idx, 1) == target - 1) r = idx;
+    if (idx < g.count && atom_add_acq_rel_gpu(p.gh.row_tiles + idx, 1) == target - 1) r = idx;
     sint[etid] = r;
   }
   epi_bar();
@@ -563,12 +557,11 @@ __device__ __noinline__ bool split_reduce(const TcConvParams& p, const TileGeom&
                                           int lane, int unit, uint8_t* scratch, int* last_flag) {
   int* arr = p.ws_counters + 2 * x.tile_mn;
   int* dep = arr + 1;
-  __threadfence();
-  epi_bar();
+  epi_bar();  // this CTA's partial tile stores before the arrival (acq_rel, cumulative)
   if (etid == 0) {
     trace_put(p, unit, 6);
-    atomicAdd(arr, 1);
-    while (ld_acquire(arr) < g.ks) __nanosleep(64);
+    atom_add_acq_rel_gpu(arr, 1);
+    while (ld_acquire_gpu(arr) < g.ks) __nanosleep(64);
     trace_put(p, unit, 7);
   }
   epi_bar();
@@ -645,10 +638,9 @@ __device__ __noinline__ bool split_reduce(const TcConvParams& p, const TileGeom&
     if (wpu > 1) epi_bar();  // park slots reused by the next round
   }
   if (etid == 0) trace_put(p, unit, 11);
-  if (p.gh.row_tiles) __threadfence();  // this CTA's GAP partials visible before its arrival
-  epi_bar();
+  epi_bar();  // this CTA's GAP partials visible before its arrival
   if (etid == 0) {
-    const bool last = atomicAdd(dep, 1) == g.ks - 1;
+    const bool last = atom_add_acq_rel_gpu(dep, 1) == g.ks - 1;
     if (last) {
       *arr = 0;
       *dep = 0;

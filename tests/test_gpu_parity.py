@@ -290,6 +290,23 @@ def test_resnet18_cifar_serve_vs_oracle(shadow):
     assert len(set(exit_o.tolist())) >= 3  # exits spread over several layers
 
 
+@pytest.mark.parametrize("shadow", [True, False])
+def test_conv_head_opt_in_vs_oracle(shadow, monkeypatch):
+    """Opt-in variant (LCB_NO_CONV_HEAD=0): the tap conv's epilogue finishes
+    each row's lookup (GAP sum, head, selector, threshold) and the last head
+    runs the first-hit exit + compaction. Slower than the separate head launch
+    today (profiles/r02_fused_head_ab.txt) but kept correct."""
+    monkeypatch.setenv("LCB_NO_CONV_HEAD", "0")
+    m, vs = _cnn_deployment("resnet18_cifar", 10, 21, 64)
+    x = image_inputs(24, 3, 32, 32, seed=5)
+    dep = lcb.Deployment(m, vs, precision="bf16x3", max_batch=32)
+    res = dep.serve(x, shadow=shadow)
+    exit_o, served_o, base_o, probs_o, gaps, _, _ = _oracle_cnn(m, vs, x)
+    deltas = {v.layer: v.delta for v in vs}
+    compare_serve(res, exit_o, served_o, base_o, probs_o, deltas, shadow, label_gap=gaps)
+    dep.close()
+
+
 def test_fused_gap_matches_unfused_pool(monkeypatch):
     """Pool(C) caches read GAP partials written by the tap conv's epilogue;
     the unfused path (LCB_NO_GAP_FUSION=1) pools the stored tap instead. Both
