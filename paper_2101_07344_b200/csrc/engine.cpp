@@ -215,6 +215,7 @@ Engine::Engine(int device, const BaseModel& model, std::vector<CacheVariant> var
   const char* nl = std::getenv("LCB_UNFUSED_LOOKUP");
   fused_lookup_ = !(nl && nl[0] == '1');
   if (const char* nc = std::getenv("LCB_NO_CONV_HEAD")) conv_head_ = !(nc[0] == '1');
+  if (const char* nw = std::getenv("LCB_NO_WIDE_LOOKUP")) wide_lookup_ = !(nw[0] == '1');
   const char* ns = std::getenv("LCB_NO_STACKED");
   stacked_ = !(ns && ns[0] == '1');
   if (const char* km = std::getenv("LCB_KS_MIN_STEPS")) ks_min_steps_ = std::atoi(km);
@@ -279,6 +280,8 @@ void Engine::build_weights() {
   heads_done_ = static_cast<int*>(dalloc(sizeof(int)));
   ck(cudaMemsetAsync(heads_done_, 0, sizeof(int), stream_), "memset");
   ck(cudaMemsetAsync(lk_arrive_, 0, sizeof(int), stream_), "memset");
+  wide_sync_ = static_cast<int*>(dalloc(2 * sizeof(int)));
+  ck(cudaMemsetAsync(wide_sync_, 0, 2 * sizeof(int), stream_), "memset");
   ws_ = static_cast<float*>(dalloc(tc_conv_ws_floats(256, num_sms_) * sizeof(float)));
   ws_counters_ = static_cast<int*>(dalloc(2 * static_cast<size_t>(num_sms_) * sizeof(int)));
   ck(cudaMemsetAsync(ws_counters_, 0, 2 * static_cast<size_t>(num_sms_) * sizeof(int), stream_), "memset");
@@ -493,6 +496,40 @@ void Engine::add_lookup_steps(std::vector<Step>& steps, DevCache& c, const TapVi
     head_bytes = 4.0 * c.gap_segs * c.width;
   } else if (c.family == 1 && fused_gap && c.gap && c.conv_feat) {
     // the tap conv already wrote the GAP features into c.feats
+  } else if (c.family == 1 && fused_gap && c.gap && wide_lookup_ && ex && c.fc_scratch &&
+             wide_lookup_supported(c.classes, c.width, num_sms_)) {
+    // many classes: GAP features, logits, head and exit in one persistent launch
+    const ExitParams exv = *ex;
+    const float gap_inv = static_cast<float>(1.0 / tap.HW);
+    int* gsync = wide_sync_;
+    const int sms = num_sms_;
+    steps.push_back({[cp, tap, max_rows, exv, gap_inv, gsync, sms](cudaStream_t s) {
+                       CacheHeadParams p{};
+                       p.family = 1;
+                       p.classes = cp->classes;
+                       p.feat = cp->width;
+                       p.rows_total = max_rows;
+                       p.W2 = cp->W2;
+                       p.b2 = cp->b2;
+                       p.Ws1 = cp->Ws1;
+                       p.bs1 = cp->bs1;
+                       p.ws2 = cp->ws2;
+                       p.bs2 = cp->bs2;
+                       p.delta = cp->delta;
+                       p.count = tap.count;
+                       p.prob = cp->prob;
+                       p.hit = cp->hit;
+                       p.label = cp->label;
+                       p.gap = cp->gap;
+                       p.gap_segs = cp->gap_segs;
+                       p.gap_inv = gap_inv;
+                       p.gap_ids = tap.data_idx;
+                       p.ex = exv;
+                       launch_wide_lookup(p, cp->feats, cp->fc_scratch, gsync, sms, s);
+                     },
+                     2, 1, cidx, 2.0 * c.width * c.classes,
+                     4.0 * c.gap_segs * c.width + 4.0 * c.width * c.classes / max_rows});
+    return;
   } else if (c.family == 1 && fused_gap && c.gap) {
     steps.push_back({[cp, tap, max_rows](cudaStream_t s) {
                        launch_gap_bins(cp->gap, cp->gap_segs, tap.C, tap.HW, tap.data_idx, tap.count, max_rows,

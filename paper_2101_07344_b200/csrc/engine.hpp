@@ -213,6 +213,7 @@ class Engine {
   bool mma_residual_ = true;  // LCB_NO_MMA_RESIDUAL=1: residual added in the epilogue instead of by identity K-steps
   __nv_bfloat16* identity_ = nullptr;
   bool fused_lookup_ = true;
+  bool wide_lookup_ = true;  // LCB_NO_WIDE_LOOKUP=1: GAP bins + logits GEMM + head as three launches
   bool stacked_ = true;
   int ks_min_steps_ = 0;
   bool wprefetch_ = true;  // LCB_NO_WPREFETCH=1: no L2 prefetch of conv weights before the PDL wait  // LCB_KS_MIN_STEPS: split-K floor of K-steps per split (CNN convs)  // LCB_NO_STACKED=1: three MMAs per bf16x3 K16 group everywhere
@@ -222,6 +223,7 @@ class Engine {
   // head arrival counter (both zeroed, reset in-kernel); LCB_NO_CONV_HEAD=1 off
   int* row_tiles_ = nullptr;
   int* heads_done_ = nullptr;
+  int* wide_sync_ = nullptr;  // grid barrier of the wide lookup (2 ints, self-resetting)
   bool conv_head_ = false;  // LCB_NO_CONV_HEAD=0 opts in (measured slower: profiles/r02_fused_head_ab.txt)
   Planes im2col_buf_;
 

@@ -618,37 +618,33 @@ __host__ __device__ inline bool head_stages_ws1(const CacheHeadParams& p) {
 
 // Shared scratch of one row's head.
 struct HeadSmem {
-  float red[32];
-  float hsel[16];
   float bv[32];
   int bi[32];
+  float part[32 * 17];  // per warp: 16 selector sums + the softmax denominator
+  float S;
 };
 
 // softmax(logits) (losses.cpp:35-46), selector FC(C,16)+ReLU+FC(16,1),
 // branch-stable sigmoid (losses.cpp:26-33), inclusive p >= delta
 // (cache.cpp:259-265), argmax(pr) with the lowest index on ties
-// (tensor.hpp:57-63). logits complete in shared memory; pr: shared [classes].
+// (tensor.hpp:57-63). logits complete in shared memory.
 // ws1: the selector's first layer [16][classes] (shared-memory copy or p.Ws1).
-__device__ void head_block(const CacheHeadParams& p, int r, const float* logits, float* pr, HeadSmem& hs,
+// Two passes over the classes: (1) max and argmax of the logits (softmax is
+// monotonic: argmax(pr) = argmax(logits), lowest index on ties); (2) e_k =
+// exp(l_k - max), S = sum e_k and the 16 selector sums sum_k Ws1[j][k] e_k in
+// one sweep, since sum_k Ws1[j][k] pr_k = (sum_k Ws1[j][k] e_k) / S. Two block
+// reductions instead of one per softmax/selector step.
+__device__ void head_block(const CacheHeadParams& p, int r, const float* logits, float* /*pr scratch*/, HeadSmem& hs,
                            const float* ws1) {
   const int C = p.classes;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = kLk / 32;
-  float m = -FLT_MAX;
-  for (int k = tid; k < C; k += kLk) m = fmaxf(m, logits[k]);
-  m = block_max(m, hs.red);
-  float part = 0.0f;
-  for (int k = tid; k < C; k += kLk) part += expf(logits[k] - m);
-  const float sum = block_sum(part, hs.red);
   float bv = -FLT_MAX;
   int bi = 0x7fffffff;
-  for (int k = tid; k < C; k += kLk) {
-    const float q = expf(logits[k] - m) / sum;
-    pr[k] = q;
-    if (q > bv) {
-      bv = q;
+  for (int k = tid; k < C; k += kLk)
+    if (logits[k] > bv) {  // ascending k: the lowest index wins within the thread
+      bv = logits[k];
       bi = k;
     }
-  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
@@ -663,46 +659,68 @@ __device__ void head_block(const CacheHeadParams& p, int r, const float* logits,
     hs.bi[warp] = bi;
   }
   __syncthreads();
-  // selector hidden unit j on warp j % nw
-  for (int j = warp; j < 16; j += nw) {
-    const float* wr = ws1 + j * C;
-    float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
-    int k = lane;
-#pragma unroll 4
-    for (; k + 96 < C; k += 128) {  // unrolled: 16 independent weight loads in flight per lane
-      a0 += wr[k] * pr[k];
-      a1 += wr[k + 32] * pr[k + 32];
-      a2 += wr[k + 64] * pr[k + 64];
-      a3 += wr[k + 96] * pr[k + 96];
+  float m = hs.bv[0];
+  int arg = hs.bi[0];
+  for (int w = 1; w < nw; ++w)
+    if (hs.bv[w] > m || (hs.bv[w] == m && hs.bi[w] < arg)) {
+      m = hs.bv[w];
+      arg = hs.bi[w];
     }
-    for (; k < C; k += 32) a0 += wr[k] * pr[k];
-    const float a = warp_sum((a0 + a1) + (a2 + a3)) + p.bs1[j];
-    if (lane == 0) hs.hsel[j] = a > 0.0f ? a : 0.0f;
+  float acc[17];
+#pragma unroll
+  for (int j = 0; j < 17; ++j) acc[j] = 0.0f;
+  for (int k = tid; k < C; k += kLk) {
+    const float e = expf(logits[k] - m);
+    acc[16] += e;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc[j] += ws1[j * C + k] * e;
+  }
+#pragma unroll
+  for (int j = 0; j < 17; ++j) acc[j] = warp_sum(acc[j]);
+  if (lane < 17) {
+    float v = acc[0];
+#pragma unroll
+    for (int j = 1; j < 17; ++j) v = lane == j ? acc[j] : v;
+    hs.part[warp * 17 + lane] = v;
   }
   __syncthreads();
-  if (tid == 0) {
-    float v = hs.bv[0];
-    int i = hs.bi[0];
-    for (int w = 1; w < nw; ++w)
-      if (hs.bv[w] > v || (hs.bv[w] == v && hs.bi[w] < i)) {
-        v = hs.bv[w];
-        i = hs.bi[w];
-      }
-    float z = p.bs2;
-    for (int j = 0; j < 16; ++j) z += p.ws2[j] * hs.hsel[j];
-    float q;
-    if (z >= 0.0f) {
-      q = 1.0f / (1.0f + expf(-z));
-    } else {
-      const float e = expf(z);
-      q = e / (1.0f + e);
+  if (warp == 0) {
+    // lane j < 17: the warps' partials of sum j in ascending warp order
+    float t = 0.0f;
+    if (lane < 17)
+      for (int w = 0; w < nw; ++w) t += hs.part[w * 17 + lane];
+    const float S = __shfl_sync(0xffffffffu, t, 16);
+    float h = 0.0f;
+    if (lane < 16) {
+      const float a = t / S + p.bs1[lane];
+      h = (a > 0.0f ? a : 0.0f) * p.ws2[lane];
     }
-    p.prob[r] = q;
-    p.hit[r] = static_cast<double>(q) >= p.delta ? 1 : 0;
-    p.label[r] = i;
+    // z = bs2 + sum_j ws2[j] * relu(hidden_j), j ascending
+    float hj[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) hj[j] = __shfl_sync(0xffffffffu, h, j);
+    if (lane == 0) {
+      float z = p.bs2;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) z += hj[j];
+      float q;
+      if (z >= 0.0f) {
+        q = 1.0f / (1.0f + expf(-z));
+      } else {
+        const float e = expf(z);
+        q = e / (1.0f + e);
+      }
+      p.prob[r] = q;
+      p.hit[r] = static_cast<double>(q) >= p.delta ? 1 : 0;
+      p.label[r] = arg;
+      hs.S = S;
+    }
   }
-  if (p.pr_out)
-    for (int k = tid; k < C; k += kLk) p.pr_out[static_cast<long long>(r) * C + k] = pr[k];
+  if (p.pr_out) {
+    __syncthreads();
+    const float S = hs.S;
+    for (int k = tid; k < C; k += kLk) p.pr_out[static_cast<long long>(r) * C + k] = expf(logits[k] - m) / S;
+  }
   if (p.logits_out)
     for (int k = tid; k < C; k += kLk) p.logits_out[static_cast<long long>(r) * C + k] = logits[k];
 }
@@ -841,6 +859,219 @@ __global__ void __launch_bounds__(kLk) cache_head_kernel(CacheHeadParams p) {
     head_block(p, r, logits, feat, hs, (stage_w || stage_s) ? ws1s : p.Ws1);
   }
   if (p.ex.arrive) exit_tail(p.ex, n, p.prob, p.hit, p.label);
+}
+
+// ------------------------------------------------------------ wide lookup
+// Pool(C) caches with many classes (ImageNet heads: C up to 2048, 1000
+// classes) in ONE persistent launch instead of three (GAP bins, logits GEMM,
+// per-row head): every CTA of the grid is resident (one per SM), and two grid
+// barriers separate the phases.
+//   pre-wait: the CTA's slice of W2 (classes [k0, k1)) and the selector's
+//             first layer Ws1 are staged in shared memory (static weights)
+//   phase 1 : feats[r][c] = inv * sum_seg gap[img(r)][seg][c] (units of one
+//             row x 64 channels; the segments split over 8 thread groups and
+//             combined in fixed order: deterministic)
+//   phase 2 : logits[r][k] = b2[k] + W2[k] . feats[r] for the CTA's classes,
+//             every row (W2 read from HBM/L2 once per launch)
+//   phase 3 : per row (CTA-strided): softmax, argmax, selector, sigmoid,
+//             inclusive threshold (head_block: cache.cpp:259-265)
+//   exit    : the last CTA records first hits and compacts (exit_tail)
+struct WideLookupParams {
+  CacheHeadParams h;  // classes, feat (= C), W2, b2, Ws1, bs1, ws2, bs2, delta, count, gap, gap_segs, gap_inv, gap_ids,
+                      // prob, hit, label, pr_out, logits_out, ex
+  float* feats;       // [max_rows][C] scratch
+  float* logits;      // [max_rows][classes] scratch
+  unsigned* gsync;    // arrival counter of the grid barriers (zero-initialised once)
+  int kpc;            // classes per CTA (phase 2)
+  unsigned long long* stamps;  // nullable: CTA 0's %globaltimer at each phase boundary [8]
+};
+
+// Grid barrier over a monotonic arrival counter (one thread per CTA; every
+// CTA resident). Each launch adds exactly kWideSyncPeriod to the counter (2 x
+// gridDim.x arrivals, then CTA 0 pads to the period), so the launch's base is
+// the counter rounded down to the period: u32 wrap-around is harmless since
+// the period divides 2^32. Arrivals are fire-and-forget releases (no
+// round trip to learn who was last); every CTA polls with acquire loads.
+constexpr unsigned kWideSyncPeriod = 512;  // >= 2 * grid
+__device__ __forceinline__ void grid_arrive(unsigned* cnt) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void grid_barrier(unsigned* cnt, unsigned base, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    grid_arrive(cnt);
+    while (ld_acquire_u32(cnt) - base < target) __nanosleep(20);
+  }
+  __syncthreads();
+}
+
+// One halving step of a reduce-scatter over the lanes: lanes whose bit `o`
+// is set keep the upper kN/2 values (adding the partner's), the others the lower.
+template <int kN>
+__device__ __forceinline__ void rs_halve(float (&v)[32], int o, int lane) {
+  const bool up = (lane & o) != 0;
+#pragma unroll
+  for (int e = 0; e < kN / 2; ++e) {
+    const float send = up ? v[e] : v[e + kN / 2];
+    const float keep = up ? v[e + kN / 2] : v[e];
+    v[e] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+  }
+}
+
+constexpr int kWideSegGroups = kLk / 16;  // 16 float4 columns (64 channels) x 32 segment groups
+constexpr int kWideFeatChunk = 8192;      // floats of feature rows staged per phase-2 chunk
+
+__global__ void __launch_bounds__(kLk, 1) wide_lookup_kernel(WideLookupParams q) {
+  extern __shared__ __align__(16) float wsm[];
+  __shared__ HeadSmem hs;
+  __shared__ float4 red4[kLk];
+  __shared__ float wpart[64 * 32];  // phase-2 partial sums [row block x slice][32]
+  const CacheHeadParams& p = q.h;
+#define STAMP(i) \
+  if (q.stamps && blockIdx.x == 0 && threadIdx.x == 0) q.stamps[i] = globaltimer();
+  STAMP(0);
+  const int C = p.feat, K = p.classes, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int k0 = blockIdx.x * q.kpc;
+  const int k1 = k0 + q.kpc < K ? k0 + q.kpc : K;
+  const int nk = k1 > k0 ? k1 - k0 : 0;
+  float* w2s = wsm;                                        // [kpc][C]
+  float* ws1s = w2s + static_cast<size_t>(q.kpc) * C;       // [16][K]
+  float* lrow = ws1s + 16 * K;                              // [K] logits of the row
+  float* prow = lrow + K;                                   // [K] pr
+  float* fchunk = prow + K;                                 // [kWideFeatChunk] feature rows
+  if (nk > 0) stage_floats(w2s, p.W2 + static_cast<long long>(k0) * C, nk * C, tid);
+  stage_floats(ws1s, p.Ws1, 16 * K, tid);
+  pdl_wait();
+  STAMP(1);
+  const int n = *p.count;
+  // this launch's barrier base: no CTA can have passed barrier 1 yet, so the
+  // counter lies in [base, base + gridDim.x)
+  const unsigned sync_base = tid == 0 ? (ld_acquire_u32(q.gsync) & ~(kWideSyncPeriod - 1u)) : 0u;
+  // ---- phase 1: GAP features of every row. Unit = (row, 64 channels); the
+  // CTA takes 4 of its units at once (all their loads in flight), threads =
+  // 16 float4 columns x 32 segment groups, groups combined in fixed order.
+  {
+    const int C4 = C >> 2;
+    const int col_units = (C4 + 15) / 16, total = n * col_units;
+    const int j = tid & 15, g = tid >> 4;
+    float4* scr = reinterpret_cast<float4*>(fchunk);  // [4][kLk]
+    for (int ub = blockIdx.x; ub < total; ub += 4 * gridDim.x) {
+      const float4* base[4];
+      bool ok[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int uu = ub + u * gridDim.x;
+        const int r = uu / col_units, c4 = (uu % col_units) * 16 + j;
+        ok[u] = uu < total && c4 < C4;
+        const long long img = ok[u] ? (p.gap_ids ? p.gap_ids[r] : r) : 0;
+        base[u] = reinterpret_cast<const float4*>(p.gap + img * p.gap_segs * C) + (ok[u] ? c4 : 0);
+      }
+      float4 a[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int sg = g; sg < p.gap_segs; sg += kWideSegGroups) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (ok[u]) add4(a[u], __ldcg(base[u] + static_cast<long long>(sg) * C4));
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) scr[u * kLk + tid] = a[u];
+      __syncthreads();
+      if (tid < 64) {
+        const int u = tid >> 4, jj = tid & 15;
+        const int uu = ub + u * gridDim.x;
+        const int r = uu / col_units, c4 = (uu % col_units) * 16 + jj;
+        if (uu < total && c4 < C4) {
+          float4 t = scr[u * kLk + jj];
+          for (int q2 = 1; q2 < kWideSegGroups; ++q2) add4(t, scr[u * kLk + q2 * 16 + jj]);
+          const float inv = p.gap_inv;
+          reinterpret_cast<float4*>(q.feats + static_cast<long long>(r) * C)[c4] =
+              make_float4(t.x * inv, t.y * inv, t.z * inv, t.w * inv);
+        }
+      }
+      __syncthreads();
+    }
+  }
+  grid_barrier(q.gsync, sync_base, gridDim.x);
+  // ---- phase 2: logits of the CTA's classes for every row. A warp owns a
+  // block of 4 rows x the CTA's <= 8 classes over a slice of the channels
+  // (lanes strided; feature loads straight from L2, all of a lane's loads in
+  // flight): 32 accumulators per lane, reduce-scattered across the lanes (31
+  // shuffles), then the slices of a block are added in fixed order.
+  STAMP(2);
+  if (nk > 0) {
+    constexpr int kRowsPerPass = 256;  // 64 row blocks: wpart holds <= 64 x 32 partials
+    for (int r0 = 0; r0 < n; r0 += kRowsPerPass) {
+      const int rn = n - r0 < kRowsPerPass ? n - r0 : kRowsPerPass;
+      const int nb = (rn + 3) >> 2;  // row blocks
+      int wpb = 1;                   // warps per row block (channel slices of >= 32)
+      while (wpb * 2 * nb <= kLk / 32 && C / (wpb * 2) >= 32) wpb *= 2;
+      const int per = (kLk / 32) / wpb;  // row blocks in flight
+      for (int rb = warp / wpb; rb < nb; rb += per) {
+        const int sub = warp % wpb;
+        const int c0 = (C * sub) / wpb, c1 = (C * (sub + 1)) / wpb;
+        float v[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) v[e] = 0.0f;
+        const int rbase = r0 + rb * 4;
+        const float* f[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) f[i] = q.feats + static_cast<long long>(rbase + i < n ? rbase + i : rbase) * C;
+#pragma unroll 4
+        for (int c = c0 + lane; c < c1; c += 32) {
+          float x[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) x[i] = rbase + i < n ? __ldcg(f[i] + c) : 0.0f;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const float w = k < nk ? w2s[k * C + c] : 0.0f;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) v[i * 8 + k] += x[i] * w;
+          }
+        }
+        // lane l ends with the full sum of accumulator l = (row i = l / 8, class k = l % 8)
+        rs_halve<32>(v, 16, lane);
+        rs_halve<16>(v, 8, lane);
+        rs_halve<8>(v, 4, lane);
+        rs_halve<4>(v, 2, lane);
+        rs_halve<2>(v, 1, lane);
+        wpart[(rb * wpb + sub) * 32 + lane] = v[0];
+      }
+      __syncthreads();
+      for (int t = tid; t < nb * 32; t += kLk) {
+        const int rb = t >> 5, l = t & 31, i = l >> 3, k = l & 7;
+        if (rb * 4 + i < rn && k < nk) {
+          float a = wpart[(rb * wpb) * 32 + l];
+          for (int sb = 1; sb < wpb; ++sb) a += wpart[(rb * wpb + sb) * 32 + l];
+          q.logits[static_cast<long long>(r0 + rb * 4 + i) * K + k0 + k] = a + __ldg(p.b2 + k0 + k);
+        }
+      }
+      __syncthreads();
+    }
+  }
+  STAMP(3);
+  grid_barrier(q.gsync, sync_base, 2 * gridDim.x);
+  if (blockIdx.x == 0 && tid == 0)  // every CTA has arrived twice: pad to the period
+    asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(q.gsync), "r"(kWideSyncPeriod - 2 * gridDim.x)
+                 : "memory");
+  STAMP(4);
+  pdl_trigger();
+  // ---- phase 3: the head of each row
+  for (int r = blockIdx.x; r < n; r += gridDim.x) {
+    for (int k = tid; k < K; k += kLk) lrow[k] = __ldcg(q.logits + static_cast<long long>(r) * K + k);
+    __syncthreads();
+    head_block(p, r, lrow, prow, hs, ws1s);
+    __syncthreads();
+  }
+  STAMP(5);
+  if (p.ex.arrive) exit_tail(p.ex, n, p.prob, p.hit, p.label);
+  STAMP(6);
+#undef STAMP
 }
 
 __global__ void gather_rows_kernel(const __nv_bfloat16* src_hi, const __nv_bfloat16* src_lo, __nv_bfloat16* dst_hi,
@@ -1231,6 +1462,39 @@ void launch_rows_fc(const float* A, long long lda, int ks, long long part_stride
   else
     launch_pdl(rows_fc_kernel<0>, dim3(grid), dim3(256), 0, s, A, lda, 0, 0, nullptr, feat, rows_fc_slice(feat), W, classes, count,
                                            max_rows, out);
+}
+
+size_t wide_lookup_smem(int classes, int C, int grid) {
+  const int kpc = (classes + grid - 1) / grid;
+  return (static_cast<size_t>(kpc) * C + 16 * static_cast<size_t>(classes) + 2 * static_cast<size_t>(classes) +
+          kWideFeatChunk) *
+         sizeof(float);
+}
+
+constexpr size_t kWideSmemMax = 200 * 1024;
+bool wide_lookup_supported(int classes, int C, int num_sms) {
+  return classes > 32 && C % 4 == 0 && C <= kWideFeatChunk && wide_lookup_smem(classes, C, num_sms) <= kWideSmemMax;
+}
+
+
+static unsigned long long* g_wide_stamps = nullptr;
+void set_wide_lookup_stamps(unsigned long long* stamps) { g_wide_stamps = stamps; }
+
+void launch_wide_lookup(const CacheHeadParams& h, float* feats, float* logits, int* gsync, int num_sms,
+                        cudaStream_t s) {
+  WideLookupParams q{};
+  q.stamps = g_wide_stamps;
+  q.h = h;
+  q.feats = feats;
+  q.logits = logits;
+  q.gsync = reinterpret_cast<unsigned*>(gsync);
+  const int grid = num_sms < static_cast<int>(kWideSyncPeriod / 2) ? num_sms : static_cast<int>(kWideSyncPeriod / 2);
+  q.kpc = (h.classes + grid - 1) / grid;
+  const size_t smem = wide_lookup_smem(h.classes, h.feat, grid);
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr))
+    cudaFuncSetAttribute(wide_lookup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kWideSmemMax);
+  launch_pdl(wide_lookup_kernel, dim3(grid), dim3(kLk), smem, s, q);
 }
 
 void launch_cache_head(const CacheHeadParams& p_in, int max_rows, cudaStream_t s) {

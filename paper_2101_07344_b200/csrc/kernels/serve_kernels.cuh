@@ -113,6 +113,19 @@ void launch_confusion(const float* probs, const int* labels, const int* base_pre
 // Pool(C) caches whose head reads the GAP partials directly (one launch per layer).
 bool fused_lookup_supported(int classes, int C, int max_rows);
 
+// Pool(C) caches with > 32 classes over tc_conv's fused GAP partials: GAP
+// features, logits, head and (h.ex.arrive) the exit in ONE persistent launch
+// of num_sms CTAs (grid barriers; needs every CTA resident: one per SM).
+// feats [max_rows][C], logits [max_rows][classes] scratch; gsync: 2 ints,
+// zero-initialised once (self-resetting).
+bool wide_lookup_supported(int classes, int C, int num_sms);
+size_t wide_lookup_smem(int classes, int C, int grid);
+void launch_wide_lookup(const CacheHeadParams& h, float* feats, float* logits, int* gsync, int num_sms,
+                        cudaStream_t s);
+// Measurement only (tests/cuda/wide_bench): CTA 0 of later wide-lookup launches
+// writes %globaltimer at its phase boundaries into stamps[0..7] (nullptr: off).
+void set_wide_lookup_stamps(unsigned long long* stamps);
+
 // Copies rows src_rows[j] of src into row j of dst (hi and lo planes).
 void launch_gather_rows(const __nv_bfloat16* src_hi, const __nv_bfloat16* src_lo, __nv_bfloat16* dst_hi,
                         __nv_bfloat16* dst_lo, long long row_elems, const int* src_rows, const int* count,

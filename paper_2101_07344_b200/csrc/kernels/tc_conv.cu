@@ -682,6 +682,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) trace_put(p, 0, 26);  // CTA entry
   // debug bits (measurement only): 1 = no TMA loads, 2 = no MMAs, 4 = no epilogue stores
   const bool dbg_noload = (p.dbg & 1) != 0, dbg_nomma = (p.dbg & 2) != 0, dbg_nostore = (p.dbg & 4) != 0;
 
@@ -716,6 +717,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  if (threadIdx.x == 0) trace_put(p, 0, 27);  // barriers + TMEM ready
   // weights do not depend on upstream kernels: warm L2 with this CTA's share
   // while the previous kernel drains (short split-K units otherwise wait on
   // first-touch HBM latency for every B box)
@@ -736,6 +738,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
   // everything above is independent of upstream kernels (programmatic launch)
   pdl_wait();
   pdl_trigger();
+  if (threadIdx.x == 0) trace_put(p, 0, 28);  // upstream complete
 
   const TileGeom g = tile_geom(p, BN);
   const int cchunks = p.C / 64;
@@ -1232,6 +1235,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
     }
   }
   __syncthreads();
+  if (threadIdx.x == 0) trace_put(p, 0, 29);  // all roles done
   if (warp == 0) {
     __syncwarp();
     tmem_dealloc(tmem_base, Cfg::kTmemCols);

@@ -460,6 +460,7 @@ static void perf_conv(const char* name, int N, int nsurv, int H, int W, int C, i
   float* dShift = dev_copy(sh);
   std::vector<int> surv;
   for (int i = 0; i < nsurv; ++i) surv.push_back((int)((long long)i * N / nsurv));
+  if (surv.empty()) surv.push_back(0);
   int* dSurv = dev_copy(surv);
   std::vector<int> cnt = {nsurv};
   int* dCnt = dev_copy(cnt);
@@ -571,6 +572,12 @@ static void perf_conv(const char* name, int N, int nsurv, int H, int W, int C, i
     for (int cta = 0; cta < 2; ++cta) {
       const unsigned long long t0 = tr[(cta * 32) * 32 + 0];
       printf("  trace CTA %d (cycles from first TMA issue): unit: tma0 tmaN | mma0 mmaN | epi0 epiN | split: fenced waited\n", cta);
+      {
+        const unsigned long long* q0 = &tr[(cta * 32) * 32];
+        auto rel0 = [&](unsigned long long v) { return v ? (long long)(v - t0) : -1LL; };
+        if (t0) printf("   prologue: entry %lld  tmem+bars ready %lld  after pdl_wait %lld  exit %lld\n", rel0(q0[26]), rel0(q0[27]),
+                       rel0(q0[28]), rel0(q0[29]));
+      }
       for (int u = 0; u < 32; ++u) {
         const unsigned long long* q = &tr[(cta * 32 + u) * 32];
         if (!q[0] && !q[4]) break;
@@ -614,6 +621,12 @@ static void perf_layers(bool trace) {
   PERF("r50 l1 3x3 64", 128, 128, 56, 56, 64, 64, 3, 1, true, false, 32, trace);
   PERF("r50 l1 1x1 64->256 res", 128, 128, 56, 56, 64, 256, 1, 1, true, true, 32, trace);
   PERF("r50 l4 3x3 512", 128, 15, 7, 7, 512, 512, 3, 1, true, false, 32, false);
+  // ResNet-50 layer3 with few survivors (the compacted step's deep tail)
+  PERF("r50 l3 1x1 1024->256 n13", 128, 13, 14, 14, 1024, 256, 1, 1, true, false, 32, trace);
+  PERF("r50 l3 3x3 256 n10", 128, 10, 14, 14, 256, 256, 3, 1, true, false, 32, trace);
+  PERF("r50 l3 1x1 256->1024 res n10", 128, 10, 14, 14, 256, 1024, 1, 1, true, true, 32, trace);
+  PERF("r50 l4 1x1 512->2048 res n1", 128, 1, 7, 7, 512, 2048, 1, 1, true, true, 32, trace);
+  PERF("r50 l4 3x3 512 n0", 128, 0, 7, 7, 512, 512, 3, 1, true, false, 32, false);
 }
 
 int main(int argc, char** argv) {
