@@ -283,8 +283,9 @@ void Engine::build_weights() {
   wide_sync_ = static_cast<int*>(dalloc(2 * sizeof(int)));
   ck(cudaMemsetAsync(wide_sync_, 0, 2 * sizeof(int), stream_), "memset");
   ws_ = static_cast<float*>(dalloc(tc_conv_ws_floats(256, num_sms_) * sizeof(float)));
-  ws_counters_ = static_cast<int*>(dalloc(2 * static_cast<size_t>(num_sms_) * sizeof(int)));
-  ck(cudaMemsetAsync(ws_counters_, 0, 2 * static_cast<size_t>(num_sms_) * sizeof(int), stream_), "memset");
+  // three counter sets (split-K launches alternate; see assign_counter_sets)
+  ws_counters_ = static_cast<int*>(dalloc(3 * 2 * static_cast<size_t>(num_sms_) * sizeof(int)));
+  ck(cudaMemsetAsync(ws_counters_, 0, 3 * 2 * static_cast<size_t>(num_sms_) * sizeof(int), stream_), "memset");
 
   // ---------------- base model
   long long max_tap_storage = 0;
@@ -735,6 +736,7 @@ void Engine::build_mlp_steps(std::vector<Step>& steps, bool shadow, bool stamps)
     prm->ks_max = 32;
     prm->ws = ws_;
     prm->ws_counters = ws_counters_;
+    split_prms_.push_back(prm);
     prm->count = cur_count;
     prm->count_static = B;
     prm->mode = 0;
@@ -924,6 +926,7 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow, bool stamps)
       }
       prm->ws = ws_;
       prm->ws_counters = ws_counters_;
+      split_prms_.push_back(prm);
       prm->surv = cur_ids;
       prm->count = cur_count;
       prm->count_static = B;
@@ -1068,6 +1071,27 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow, bool stamps)
   if (stamps) add_stamp(steps, L + 1, 0);  // after the head (charged to the last block)
 }
 
+// Split-K arrival counters without a reset arrival: the step list's split-K
+// launches cycle through counter sets so that consecutive ones (cyclically,
+// across graph replays) differ, and each launch zeroes the NEXT launch's set
+// after its upstream wait, when that set's previous user has completed. Lists
+// start on set 0; an odd count ends on set 2. A single launch keeps the
+// in-kernel reset (its next launch is itself).
+void Engine::assign_counter_sets() {
+  const size_t M = split_prms_.size();
+  if (M < 2) return;
+  std::vector<int> set(M);
+  for (size_t j = 0; j < M; ++j) set[j] = static_cast<int>(j % 2);
+  if (M % 2) set[M - 1] = 2;
+  const int len = 2 * num_sms_;
+  for (size_t j = 0; j < M; ++j) {
+    split_prms_[j]->ws_counters = ws_counters_ + static_cast<size_t>(set[j]) * len;
+    split_prms_[j]->ctr_zero = ws_counters_ + static_cast<size_t>(set[(j + 1) % M]) * len;
+    split_prms_[j]->ctr_len = len;
+  }
+  split_prms_.clear();
+}
+
 std::vector<Step>& Engine::steps_for(bool shadow) { return steps_mode(shadow ? kModeShadow : kModeCompact); }
 
 // Step lists: compact (the product), shadow (with block-boundary stamps; also
@@ -1079,8 +1103,10 @@ std::vector<Step>& Engine::steps_mode(int mode) {
     st.clear();
     const bool shadow = mode == kModeShadow, stamps = mode != kModeCompact;
     if (shadow) tap_step_end_.assign(static_cast<size_t>(model_.num_blocks) + 1, -1);
+    split_prms_.clear();
     if (model_.family == "mlp") build_mlp_steps(st, shadow, stamps);
     else build_cnn_steps(st, shadow, stamps);
+    assign_counter_sets();
     built_[mode] = true;
   }
   return st;

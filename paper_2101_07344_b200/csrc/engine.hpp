@@ -223,7 +223,10 @@ class Engine {
   // head arrival counter (both zeroed, reset in-kernel); LCB_NO_CONV_HEAD=1 off
   int* row_tiles_ = nullptr;
   int* heads_done_ = nullptr;
-  int* wide_sync_ = nullptr;  // grid barrier of the wide lookup (2 ints, self-resetting)
+  int* wide_sync_ = nullptr;
+  // split-K launches of the step list being built (assign_counter_sets)
+  std::vector<std::shared_ptr<TcConvParams>> split_prms_;
+  void assign_counter_sets();  // grid barrier of the wide lookup (2 ints, self-resetting)
   bool conv_head_ = false;  // LCB_NO_CONV_HEAD=0 opts in (measured slower: profiles/r02_fused_head_ab.txt)
   Planes im2col_buf_;
 

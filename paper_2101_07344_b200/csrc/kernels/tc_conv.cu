@@ -55,7 +55,16 @@ struct FastDiv {
     } else {
       const uint32_t l = 32 - __clz(d - 1);  // ceil(log2 d)
       const uint32_t pw = 31 + l;
-      m = static_cast<uint32_t>(((1ull << pw) + d - 1) / d);
+      if (d <= (1u << 20)) {
+        // ceil(2^pw / d) from one correctly rounded double division: exact
+        // for d <= 2^20 (a non-integer quotient < 2^32 stays >= 1/d > ulp
+        // away from the integers). The u64 division below is a ~100-
+        // instruction software routine on the kernel's startup path.
+        m = static_cast<uint32_t>(ceil(__ddiv_rn(__longlong_as_double(static_cast<long long>(1023 + pw) << 52),
+                                                 static_cast<double>(d))));
+      } else {
+        m = static_cast<uint32_t>(((1ull << pw) + d - 1) / d);
+      }
       s = pw - 32;
     }
   }
@@ -312,19 +321,6 @@ __device__ __forceinline__ void epilogue_store(const TcConvParams& p, float (&v)
   }
 }
 
-// Same, loading the residual itself (split-K reduction path).
-__device__ __forceinline__ void epilogue_store_ld(const TcConvParams& p, float (&v)[16], size_t off, int co) {
-  uint4 rh[2], rl[2];
-  if (p.res_hi) {
-    rh[0] = reinterpret_cast<const uint4*>(p.res_hi + off)[0];
-    rh[1] = reinterpret_cast<const uint4*>(p.res_hi + off)[1];
-    if (p.res_lo) {
-      rl[0] = reinterpret_cast<const uint4*>(p.res_lo + off)[0];
-      rl[1] = reinterpret_cast<const uint4*>(p.res_lo + off)[1];
-    }
-  }
-  epilogue_store(p, v, off, co, p.res_hi ? rh : nullptr, p.res_lo ? rl : nullptr);
-}
 
 // Fused global-average-pool partials of the tap this conv produces (the
 // learned cache's Pool(C) = GAP predictor input, cache.cpp:104-140 with
@@ -583,10 +579,24 @@ __device__ __noinline__ bool split_reduce(const TcConvParams& p, const TileGeom&
   for (int base = u0; base < u1; base += per_round) {
     const int uu = base + warp / wpu, sub = warp % wpu;
     const int c16 = uu / (kBM / 32), r = (uu % (kBM / 32)) * 32 + lane;
+    const int co = x.tn * BN + c16 * 16;
+    // row geometry and shift first: independent of the partials, their
+    // loads overlap the partial loads; rows outside the output have no partials
+    size_t ob = 0;
+    int img = 0;
+    bool img_ok = false, rvalid = false;
+    float4 sh[4];
+    if (uu < u1) {
+      rvalid = out_row(p, g, x, r, row_geom(p, r), ob, img, img_ok);
+      if (sub == 0 && p.shift) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) sh[q] = __ldg(reinterpret_cast<const float4*>(p.shift + co) + q);
+      }
+    }
     float v[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = 0.0f;
-    if (uu < u1) {
+    if (rvalid) {
       const int k0 = (g.ks * sub) / wpu, k1 = (g.ks * (sub + 1)) / wpu;
 #pragma unroll 6  // the partial loads of 6 k's go out together; the adds keep ascending k order
       for (int k = k0; k < k1; ++k) {
@@ -602,42 +612,58 @@ __device__ __noinline__ bool split_reduce(const TcConvParams& p, const TileGeom&
           v[4 * u + 3] += f.w;
         }
       }
-      TC_TRACE(if (warp == 0 && lane == 0 && base == u0) trace_val(p, unit, 15, clk());)
-      if (wpu > 1) {
+    }
+    TC_TRACE(if (warp == 0 && lane == 0 && base == u0) trace_val(p, unit, 15, clk());)
+    if (wpu > 1) {
+      if (uu < u1) {
 #pragma unroll
         for (int u = 0; u < 4; ++u)
           park[(warp * 4 + u) * 32 + lane] = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
       }
+      epi_bar();
     }
-    if (wpu > 1) epi_bar();
     if (uu < u1 && sub == 0) {
-      for (int w = 1; w < wpu; ++w) {
+      if (rvalid) {
+        for (int w = 1; w < wpu; ++w) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float4 f = park[((warp + w) * 4 + u) * 32 + lane];
-          v[4 * u] += f.x;
-          v[4 * u + 1] += f.y;
-          v[4 * u + 2] += f.z;
-          v[4 * u + 3] += f.w;
+          for (int u = 0; u < 4; ++u) {
+            const float4 f = park[((warp + w) * 4 + u) * 32 + lane];
+            v[4 * u] += f.x;
+            v[4 * u + 1] += f.y;
+            v[4 * u + 2] += f.z;
+            v[4 * u + 3] += f.w;
+          }
         }
-      }
-      size_t ob;
-      int img;
-      bool img_ok;
-      const int co = x.tn * BN + c16 * 16;
-      if (out_row(p, g, x, r, row_geom(p, r), ob, img, img_ok)) {
-        epilogue_store_ld(p, v, ob + co, co);
+        uint4 rh[2], rl[2];
+        if (p.res_hi) {
+          rh[0] = reinterpret_cast<const uint4*>(p.res_hi + ob + co)[0];
+          rh[1] = reinterpret_cast<const uint4*>(p.res_hi + ob + co)[1];
+          if (p.res_lo) {
+            rl[0] = reinterpret_cast<const uint4*>(p.res_lo + ob + co)[0];
+            rl[1] = reinterpret_cast<const uint4*>(p.res_lo + ob + co)[1];
+          }
+        }
+        epilogue_math(p, v, co, p.shift ? reinterpret_cast<const float*>(sh) : nullptr, p.res_hi ? rh : nullptr,
+                      p.res_lo ? rl : nullptr);
+        uint4 hi[2], lo[2];
+        split16(v, hi, lo);
+        uint4* oh = reinterpret_cast<uint4*>(p.out_hi + ob + co);
+        oh[0] = hi[0];
+        oh[1] = hi[1];
+        if (p.out_lo) {
+          uint4* ol = reinterpret_cast<uint4*>(p.out_lo + ob + co);
+          ol[0] = lo[0];
+          ol[1] = lo[1];
+        }
         TC_TRACE(if (warp == 0 && lane == 0 && base == u0) trace_val(p, unit, 12, clk());)
-      } else {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = 0.0f;
       }
-      if (p.gap_out) gap_segment(p, x, r, lane, v, co, img, img_ok);
+      if (p.gap_out) gap_segment(p, x, r, lane, v, co, img, img_ok);  // v = 0 on rows outside the output
       if (lane == 0) trace_put(p, unit, 9 + (warp < 2 ? warp : 1));
     }
     if (wpu > 1) epi_bar();  // park slots reused by the next round
   }
   if (etid == 0) trace_put(p, unit, 11);
+  if (p.ctr_zero && !p.gh.row_tiles) return false;  // the next split-K launch zeroes this counter set
   epi_bar();  // this CTA's GAP partials visible before its arrival
   if (etid == 0) {
     const bool last = atom_add_acq_rel_gpu(dep, 1) == g.ks - 1;
@@ -722,7 +748,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
   // while the previous kernel drains (short split-K units otherwise wait on
   // first-touch HBM latency for every B box)
   if (warp == 0 && p.wpre_bytes > 0) {
-    const long long chunk = ((p.wpre_bytes + gridDim.x - 1) / gridDim.x + 15) & ~15LL;
+    // (32-bit division: weight planes are < 2^31 bytes)
+    const long long chunk =
+        ((static_cast<unsigned>(p.wpre_bytes) + gridDim.x - 1) / gridDim.x + 15) & ~15LL;
     const long long off = static_cast<long long>(blockIdx.x) * chunk;
     if (off < p.wpre_bytes) {
       const long long len = p.wpre_bytes - off < chunk ? p.wpre_bytes - off : chunk;
@@ -739,6 +767,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
   pdl_wait();
   pdl_trigger();
   if (threadIdx.x == 0) trace_put(p, 0, 28);  // upstream complete
+  if (p.ctr_zero && threadIdx.x == 0)
+    for (int i = blockIdx.x; i < p.ctr_len; i += gridDim.x) p.ctr_zero[i] = 0;
 
   const TileGeom g = tile_geom(p, BN);
   const int cchunks = p.C / 64;
@@ -1149,13 +1179,15 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
           for (int i = 0; i < 16; ++i) v[0][i] = v[1][i] = 0.0f;
         }
         if (split) {
+          if (valid) {  // the reduction reads valid rows only
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int c16 = (col0 >> 4) + c32 * 2 + u;
-            float4* dst = reinterpret_cast<float4*>(wsp) + static_cast<size_t>(c16) * 4 * kBM + row;
+            for (int u = 0; u < 2; ++u) {
+              const int c16 = (col0 >> 4) + c32 * 2 + u;
+              float4* dst = reinterpret_cast<float4*>(wsp) + static_cast<size_t>(c16) * 4 * kBM + row;
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-              __stcg(dst + q * kBM, make_float4(v[u][4 * q], v[u][4 * q + 1], v[u][4 * q + 2], v[u][4 * q + 3]));
+              for (int q = 0; q < 4; ++q)
+                __stcg(dst + q * kBM, make_float4(v[u][4 * q], v[u][4 * q + 1], v[u][4 * q + 2], v[u][4 * q + 3]));
+            }
           }
           continue;
         }

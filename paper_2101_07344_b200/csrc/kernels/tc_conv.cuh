@@ -109,7 +109,10 @@ struct TcConvParams {
   int ks_max;          // mode 0: dynamic split-K upper bound (1 = off)
   int ks_min_steps;  // split-K: at least this many K-steps per split (0 = fill the grid)
   float* ws;           // mode 0 split-K workspace (fp32 partial tiles)
-  int* ws_counters;    // per output tile arrival counters (zeroed; reset by the last CTA)
+  int* ws_counters;    // per output tile arrival counters (zeroed; reset by the last CTA unless ctr_zero)
+  int* ctr_zero;       // nullable: the counter set of the NEXT split-K launch, zeroed by this launch after its
+                       // upstream wait (the previous user of that set has completed); then no reset arrival
+  int ctr_len;         // ints in ctr_zero
   const int* surv;     // survivor image list (nullptr = identity)
   const int* count;    // device-side image/row count (nullptr -> count_static)
   int count_static;
