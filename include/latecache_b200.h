@@ -253,6 +253,15 @@ int lc_run_adaptation(lc_engine* e, const float* inputs, int n_samples, const do
  * variants after lc_run_adaptation. */
 int lc_engine_variant(lc_engine* e, int k, lc_variant** out);
 
+/* Swap observer for lc_run_adaptation (replaces nothing in the reference: its
+ * single-process loop swaps `live = *pending` in place, serving.cpp:303-315).
+ * hook(ctx, t) runs on the calling thread right after a pending retrain has
+ * landed in the engine: requests at time >= t are served by the new caches,
+ * which lc_engine_variant() returns at that moment. A trainer replica uses it
+ * to broadcast each swap to the request-sharded replicas. hook == NULL clears. */
+typedef void (*lc_swap_hook)(void* ctx, double swap_time_min);
+int lc_engine_set_swap_hook(lc_engine* e, lc_swap_hook hook, void* ctx);
+
 /* Hardware-aware costs (replaces CostModel::lookup_ms, cache.hpp:46-55, and the
  * modeled LayerProfile, composer.hpp): one batch of the B host requests through
  * the graph with device timestamps at every block boundary: flags

@@ -57,6 +57,10 @@ class RetrainEventC(C.Structure):  # lc_retrain_event
     ]
 
 
+# lc_swap_hook: void (*)(void* ctx, double swap_time_min)
+SWAP_HOOK = C.CFUNCTYPE(None, C.c_void_p, C.c_double)
+
+
 def _load() -> C.CDLL:
     if not os.path.exists(LIB_PATH):
         raise ImportError(
@@ -119,6 +123,7 @@ def _load() -> C.CDLL:
         "lc_run_adaptation": (I, [P, pF, I, pD, pI, I, C.POINTER(AdaptConfig), C.POINTER(pD), pD, I, C.c_uint64, I,
                                   pI, pI, pI, pD, C.POINTER(RetrainEventC), I, pI]),
         "lc_engine_variant": (I, [P, I, C.POINTER(P)]),
+        "lc_engine_set_swap_hook": (I, [P, SWAP_HOOK, P]),
         "lc_engine_time": (I, [P, I, C.c_uint, I, pD]),
         "lc_engine_kernel_count": (I, [P, C.c_uint, I]),
         "lc_engine_profile": (I, [P, I, C.c_uint, I, pI, pI, pD, pD, pD]),
@@ -174,5 +179,5 @@ EXPORTED_SYMBOLS = [
     "lc_measure_metrics", "lc_tune_delta", "lc_train_predictor", "lc_train_selector", "lc_engine_update_variant",
     "lc_run_adaptation", "lc_engine_variant", "lc_serve_submit", "lc_serve_collect", "lc_engine_layer_times",
     "lc_model_save_binary", "lc_model_load_binary", "lc_variant_save_binary", "lc_variant_load_binary",
-    "lc_engine_read_tap",
+    "lc_engine_read_tap", "lc_engine_set_swap_hook",
 ]

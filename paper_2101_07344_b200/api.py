@@ -350,6 +350,18 @@ class Deployment:
         batch already enqueued; serving.cpp:301-315)."""
         check(lib.lc_engine_update_variant(self._h, variant._h))
 
+    def set_swap_hook(self, fn) -> None:
+        """fn(swap_time_min) after each swap run_adaptation lands (serving.cpp:303-315):
+        requests at time >= swap_time_min are served by the caches variant(k)
+        returns at that moment. None clears. (lc_engine_set_swap_hook)"""
+        from ._lib import SWAP_HOOK
+        if fn is None:
+            self._swap_cb = None
+            check(lib.lc_engine_set_swap_hook(self._h, SWAP_HOOK(), None))
+            return
+        self._swap_cb = SWAP_HOOK(lambda _ctx, t: fn(float(t)))  # kept alive with the deployment
+        check(lib.lc_engine_set_swap_hook(self._h, self._swap_cb, None))
+
     def variant(self, k: int) -> CacheVariant:
         """Copy of the k-th attached variant (probe order: ascending layer) as the engine holds it."""
         h = C.c_void_p()

@@ -594,6 +594,10 @@ int lc_run_adaptation(lc_engine* e, const float* inputs, int n_samples, const do
   });
 }
 
+int lc_engine_set_swap_hook(lc_engine* e, lc_swap_hook hook, void* ctx) {
+  return guard([&] { eng(e).set_swap_hook(hook, ctx); });
+}
+
 int lc_engine_variant(lc_engine* e, int k, lc_variant** out) {
   return guard([&] {
     need(out, "out");

@@ -124,6 +124,7 @@ void run_adaptation(Engine& en, const float* inputs, int n_samples, const double
   auto swap_in = [&]() {
     for (const CacheVariant& v : *pending) en.update_variant(v);
     pending.reset();
+    en.notify_swap(swap_time);
   };
 
   auto retrain_at = [&](double now) {  // serving.cpp:235-298

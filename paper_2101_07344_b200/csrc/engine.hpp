@@ -52,6 +52,19 @@ class Engine {
   Engine(const Engine&) = delete;
   Engine& operator=(const Engine&) = delete;
 
+  // Observer of run_adaptation's swaps (serving.cpp:303-315): called after a
+  // pending retrain has landed in the engine, with the swap time (requests at
+  // time >= t are served by the new caches). Used to replicate swaps across
+  // request-sharded replicas (shard.py).
+  using SwapHook = void (*)(void* ctx, double swap_time_min);
+  void set_swap_hook(SwapHook hook, void* ctx) {
+    swap_hook_ = hook;
+    swap_ctx_ = ctx;
+  }
+  void notify_swap(double swap_time_min) const {
+    if (swap_hook_) swap_hook_(swap_ctx_, swap_time_min);
+  }
+
   // ----- serve
   float* input_buffer() { return d_x_; }  // [max_batch][input_dim] fp32 (device)
   long long input_dim() const { return model_.input_dim(); }
@@ -224,6 +237,8 @@ class Engine {
   int* row_tiles_ = nullptr;
   int* heads_done_ = nullptr;
   int* wide_sync_ = nullptr;
+  SwapHook swap_hook_ = nullptr;
+  void* swap_ctx_ = nullptr;
   // split-K launches of the step list being built (assign_counter_sets)
   std::vector<std::shared_ptr<TcConvParams>> split_prms_;
   void assign_counter_sets();  // grid barrier of the wide lookup (2 ints, self-resetting)

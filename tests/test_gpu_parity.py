@@ -811,3 +811,70 @@ def test_adaptation_wakes_a_dead_cache_after_the_pause():
     h2 = np.array([r.hit_layer for r in res2.traces])
     assert np.all(h2[t < 4.0] == 0) and np.sum(h2[t >= 4.0] > 0) > 0
     assert np.mean(h2 == hl2) >= 0.98
+
+
+@pytest.mark.parametrize("pause_ms", [0.0, 90000.0])
+def test_adaptation_swaps_replay_on_a_second_replica(pause_ms):
+    """Cross-replica adaptation (§8f rank 3, serving.cpp:303-315): the swap hook
+    captures every swap run_adaptation lands, the payload goes through the
+    fleet broadcast encoding (pack/unpack, shard.py), and a second replica
+    (fresh Deployment) serving the same stream with serve_with_swaps matches
+    the trainer's traces (up to split-K rounding of differently composed
+    batches) and ends on byte-identical caches."""
+    from paper_2101_07344_b200.shard import (apply_swap_to_deployment, capture_swaps, pack_swaps, serve_with_swaps,
+                                             unpack_swaps)
+    model_txt, vtxt, X, labels, times, samp = _adapt_setup()
+    sel = [0, 1, 3]
+    m = lcb.load_base_model(model_txt)
+
+    def fresh():
+        vs = [lcb.load_variant(vtxt[k]) for k in sel]
+        for v in vs:
+            v.delta = 0.995
+        return lcb.Deployment(m, vs, precision="bf16x3", max_batch=256), vs
+
+    dep, vs = fresh()
+    rm = O.RefModel.load(model_txt) if os.path.exists(O.REF_SO) else None
+    orig_x = X[-120:]
+    if rm is not None:
+        otaps, oy = [], None
+        for v in vs:
+            t, oy = _ref_records(rm, orig_x, v.layer)
+            otaps.append(t)
+    else:  # records from the GPU's own shadow taps
+        pytest.skip("needs oracle/_ref for the original records")
+    cfg = lcb.AdaptationConfig(sample_rate=0.3, window_min=30.0, retrain_interval_min=15.0, epochs=3,
+                               learning_rate=0.005, retrain_pause_ms=pause_ms)
+    stream = [lcb.Request(i, float(times[i]), int(labels[samp[i]]), int(samp[i])) for i in range(len(times))]
+    swaps = capture_swaps(dep)
+    res = lcb.run_adaptation(dep, X, labels, stream, cfg, otaps, oy, seed=5, adapt_on=True)
+    dep.set_swap_hook(None)
+    assert len(swaps) >= 2 and all(len(s.blobs) == len(sel) for s in swaps)
+    assert all(a.time_min <= b.time_min for a, b in zip(swaps, swaps[1:]))
+    swaps = unpack_swaps(pack_swaps(swaps))  # the broadcast payload
+    rep, _ = fresh()
+
+    def chunks(d, xs):  # batches of at most max_batch requests
+        rs = [d.serve(xs[i:i + d.max_batch], shadow=True) for i in range(0, xs.shape[0], d.max_batch)]
+        return {"exit_layer": np.concatenate([r.exit_layer for r in rs]),
+                "served": np.concatenate([r.served for r in rs]),
+                "base_pred": np.concatenate([r.base_pred for r in rs])}
+
+    def serve(xs):
+        return chunks(rep, xs)
+
+    out = serve_with_swaps(serve, lambda s: apply_swap_to_deployment(rep, s), X[samp], times, swaps)
+    hl = np.array([t.hit_layer for t in res.traces])
+    sv = np.array([t.served_pred for t in res.traces])
+    bp = np.array([t.base_pred for t in res.traces])
+    assert np.mean(out["exit_layer"] == hl) >= 0.99, np.mean(out["exit_layer"] == hl)
+    assert np.mean(out["served"] == sv) >= 0.99
+    assert np.mean(out["base_pred"] == bp) >= 0.995
+    for k in range(len(sel)):
+        assert rep.variant(k).save() == dep.variant(k).save()
+    # the swaps matter: a frozen replica's traces differ
+    frozen, _ = fresh()
+    fz = chunks(frozen, X[samp])
+    assert np.mean(fz["exit_layer"] == hl) < np.mean(out["exit_layer"] == hl)
+    for d in (dep, rep, frozen):
+        d.close()

@@ -75,3 +75,110 @@ def test_two_rank_gloo_sharded_serve_matches_reference_traces(tmp_path):
     assert r["exit_layer"].tolist() == [int(t[5]) for t in traces]
     assert r["served"].tolist() == [int(t[4]) for t in traces]
     assert r["base_pred"].tolist() == [int(t[3]) for t in traces]
+
+
+# ------------------------------------------------------- adaptation swaps
+def test_swap_segments_follow_the_reference_swap_rule():
+    """serving.cpp:303-315: a landed swap serves every request at time >= its
+    swap time; two swaps landing before the same request both apply, in order."""
+    from paper_2101_07344_b200.shard import VariantSwap, swap_segments
+    t = [0.0, 1.0, 1.5, 2.0, 4.0, 4.0, 7.5]
+    sw = [VariantSwap(1.5), VariantSwap(1.5), VariantSwap(4.0), VariantSwap(9.0)]
+    assert swap_segments(t, sw) == [(0, 2, -1), (2, 4, 1), (4, 7, 2)]
+    assert swap_segments(t, []) == [(0, 7, -1)]
+    assert swap_segments([], sw) == []
+    with pytest.raises(ValueError):
+        swap_segments([1.0, 0.5], sw)
+
+
+def test_pack_swaps_round_trip():
+    from paper_2101_07344_b200.shard import VariantSwap, pack_swaps, unpack_swaps
+    sw = [VariantSwap(0.25, [b"abc", b""]), VariantSwap(15.0, [bytes(range(256)) * 3])]
+    back = unpack_swaps(pack_swaps(sw))
+    assert [(s.time_min, s.blobs) for s in back] == [(s.time_min, s.blobs) for s in sw]
+    with pytest.raises(ValueError):
+        unpack_swaps(pack_swaps(sw)[:-1])
+
+
+def _golden_swaps():
+    """Two retrain swaps mid-stream: the golden trained caches with other
+    thresholds (binary variants, probe order), as a trainer would broadcast."""
+    import paper_2101_07344_b200 as lcb
+    from paper_2101_07344_b200.shard import VariantSwap
+    d = os.path.join(GOLDEN, "trained")
+    texts = []
+    k = 0
+    while os.path.exists(os.path.join(d, f"variant_{k}.txt")):
+        texts.append(open(os.path.join(d, f"variant_{k}.txt")).read())
+        k += 1
+    swaps = []
+    # layer-1 cache never fires (all exit at layer 2), then neither the first nor the second
+    for t, deltas in ((12.0, (1.5, 0.0)), (25.0, (1.5, 1.5))):
+        blobs = []
+        for txt, dl in zip(texts, deltas):
+            v = lcb.load_variant(txt)
+            v.delta = dl
+            blobs.append(v.save_binary())
+        swaps.append(VariantSwap(t, blobs))
+    return swaps
+
+
+def _oracle_replica(model, caches):
+    """A CPU replica: the oracle serve over the live caches; swaps replace them."""
+    import paper_2101_07344_b200 as lcb
+    from oracle import oracle as O
+    live = {c[0]: c for c in caches}
+
+    def apply(swap):
+        for b in swap.blobs:
+            v = lcb.load_variant_binary(b)
+            pred, sel, d = O.variant_layers_from_product(v)
+            live[v.layer] = (v.layer, pred, sel, d)
+
+    def serve(xs):
+        el, sv, bp, _ = O.oracle_serve_mlp(model, [live[l] for l in sorted(live)], xs)
+        return {"exit_layer": el, "served": sv, "base_pred": bp}
+
+    return serve, apply
+
+
+def _fleet_worker(rank, world, port, out_path):
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+
+    from paper_2101_07344_b200.shard import serve_sharded_with_swaps, serve_with_swaps
+    from tests.test_oracle import _trained
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    model, caches, X, reqs, traces = _trained()
+    inputs = X[[s for _, s in reqs]]
+    times = [float(t[1]) for t in traces]
+    swaps = _golden_swaps() if rank == 0 else None  # only the trainer holds them
+    serve, apply = _oracle_replica(model, caches)
+    res = serve_sharded_with_swaps(serve, apply, inputs, times, swaps, src=0, dist=dist)
+    if rank == 0:
+        s1, a1 = _oracle_replica(model, caches)
+        single = serve_with_swaps(s1, a1, inputs, times, swaps)
+        s0, _ = _oracle_replica(model, caches)
+        frozen = s0(inputs)
+        np.savez(out_path, **{f"fleet_{k}": v for k, v in res.items()},
+                 **{f"single_{k}": v for k, v in single.items()}, **{f"frozen_{k}": v for k, v in frozen.items()})
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_gloo_swap_broadcast_matches_single_replica(tmp_path):
+    """Only rank 0 (the trainer) holds the swaps; after the broadcast every
+    rank serves its shard applying them by the reference rule, and the
+    gathered traces equal one replica serving the whole stream with the same
+    swaps (and differ from the frozen caches: the swaps matter)."""
+    import torch.multiprocessing as mp
+    out = str(tmp_path / "fleet.npz")
+    mp.spawn(_fleet_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    r = np.load(out)
+    for k in ("exit_layer", "served", "base_pred"):
+        assert np.array_equal(r[f"fleet_{k}"], r[f"single_{k}"]), k
+    assert not np.array_equal(r["fleet_exit_layer"], r["frozen_exit_layer"])
+    assert np.array_equal(r["fleet_base_pred"], r["frozen_base_pred"])  # swaps touch the caches only
