@@ -224,6 +224,7 @@ Engine::Engine(int device, const BaseModel& model, std::vector<CacheVariant> var
   halo_ = nh && nh[0] == '1';
   const char* nr = std::getenv("LCB_NO_MMA_RESIDUAL");
   mma_residual_ = !(nr && nr[0] == '1');
+  if (const char* np = std::getenv("LCB_NO_PROJ_FUSION")) proj_fusion_ = !(np[0] == '1');
   const char* nt = std::getenv("LCB_DIRECT_STORE");
   staged_store_ = !(nt && nt[0] == '1');
   build_weights();
@@ -324,6 +325,35 @@ void Engine::build_weights() {
       h2d(identity_, eye.data(), eye.size() * 2);
     }
     cnn_w_.resize(model_.ops.size());
+    // Projection shortcuts that ride their consumer's residual K-steps: a 1x1,
+    // unpadded, ReLU-free conv whose output slot is used exactly once, as the
+    // residual of a conv at the same output resolution (the ResNet downsample
+    // branch). Not with halo slabs (their producer has no projection path).
+    const size_t nops = model_.ops.size();
+    proj_into_.assign(nops, -1);
+    fused_proj_.assign(nops, -1);
+    if (proj_fusion_ && mma_residual_ && !halo_) {
+      std::vector<int> uses(static_cast<size_t>(model_.nslots), 0), producer(static_cast<size_t>(model_.nslots), -1);
+      for (size_t i = 0; i < nops; ++i) {
+        const CnnOp& o = model_.ops[i];
+        if (o.in >= 0) ++uses[static_cast<size_t>(o.in)];
+        if (o.res >= 0) ++uses[static_cast<size_t>(o.res)];
+        if (o.kind != CnnOpKind::Head) producer[static_cast<size_t>(o.out)] = static_cast<int>(i);
+      }
+      for (size_t i = 0; i < nops; ++i) {
+        const CnnOp& o = model_.ops[i];
+        if (o.kind != CnnOpKind::Conv || o.res < 0 || uses[static_cast<size_t>(o.res)] != 1) continue;
+        const int j = producer[static_cast<size_t>(o.res)];
+        if (j < 0 || j >= static_cast<int>(i)) continue;
+        const CnnOp& pj = model_.ops[static_cast<size_t>(j)];
+        if (pj.kind != CnnOpKind::Conv || pj.k != 1 || pj.pad != 0 || pj.relu || pj.res >= 0 || pj.tap >= 0 ||
+            pj.in < 0 || pj.C % 64 != 0 || pj.Cout != o.Cout || pj.Ho() != o.Ho() || pj.Wo() != o.Wo() ||
+            (pj.stride != 1 && pj.stride != 2))
+          continue;
+        proj_into_[static_cast<size_t>(j)] = static_cast<int>(i);
+        fused_proj_[i] = j;
+      }
+    }
     std::vector<long long> slot_elems(static_cast<size_t>(model_.nslots), 0);
     long long im2col_elems = 0;
     for (size_t i = 0; i < model_.ops.size(); ++i) {
@@ -361,9 +391,15 @@ void Engine::build_weights() {
                                        o.scale[static_cast<size_t>(co)]);
         dc.w = upload_planes(w);
         dc.scale = nullptr;
-        dc.shift = upload_f32(to_f32(o.shift));
+        std::vector<double> shift(o.shift);
+        if (fused_proj_[i] >= 0) {  // conv + projection accumulate together: one shift
+          const CnnOp& pj = model_.ops[static_cast<size_t>(fused_proj_[i])];
+          for (size_t c = 0; c < shift.size(); ++c) shift[c] += pj.shift[c];
+        }
+        dc.shift = upload_f32(to_f32(shift));
         cnn_w_[i] = dc;
-        slot_elems[static_cast<size_t>(o.out)] = static_cast<long long>(B) * o.Ho() * o.Wo() * o.Cout;
+        if (proj_into_[i] < 0)
+          slot_elems[static_cast<size_t>(o.out)] = static_cast<long long>(B) * o.Ho() * o.Wo() * o.Cout;
       } else if (o.kind == CnnOpKind::MaxPool) {
         slot_elems[static_cast<size_t>(o.out)] = static_cast<long long>(B) * o.Ho() * o.Wo() * o.C;
       } else if (o.kind == CnnOpKind::Head) {
@@ -377,12 +413,14 @@ void Engine::build_weights() {
       const CnnOp& o = model_.ops[i];
       if (o.in >= 0) last_use[static_cast<size_t>(o.in)] = static_cast<int>(i);
       if (o.res >= 0) last_use[static_cast<size_t>(o.res)] = static_cast<int>(i);
+      // a fused projection reads its input when its consumer runs
+      if (fused_proj_[i] >= 0) last_use[static_cast<size_t>(model_.ops[static_cast<size_t>(fused_proj_[i])].in)] = static_cast<int>(i);
     }
     slot_buf_.assign(static_cast<size_t>(model_.nslots), Planes{});
     std::multimap<long long, Planes> free_pool;
     for (size_t i = 0; i < model_.ops.size(); ++i) {
       const CnnOp& o = model_.ops[i];
-      if (o.kind != CnnOpKind::Head) {
+      if (o.kind != CnnOpKind::Head && proj_into_[i] < 0) {
         const long long need = slot_elems[static_cast<size_t>(o.out)];
         auto it = free_pool.find(need);
         if (it != free_pool.end()) {
@@ -858,8 +896,12 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow, bool stamps)
                        },
                        0, 1, static_cast<int>(cur_count - d_counts_), 0.0,
                        (x3 ? 4.0 : 2.0) * (static_cast<double>(o.H) * o.W * o.C + static_cast<double>(Ho) * Wo * o.C)});
+    } else if (o.kind == CnnOpKind::Conv && proj_into_[i] >= 0) {
+      // fused into its consumer's residual K-steps (no launch, no output buffer)
     } else if (o.kind == CnnOpKind::Conv) {
       const DevConv& dc = cnn_w_[i];
+      const int pjx = fused_proj_[i];
+      const CnnOp* pj = pjx >= 0 ? &model_.ops[static_cast<size_t>(pjx)] : nullptr;
       Planes in = slot_buf_[static_cast<size_t>(o.in)], out = slot_buf_[static_cast<size_t>(o.out)];
       // Stride 2 reads the NHWC input directly through TMA traversal strides.
       require(o.stride == 1 || o.stride == 2, "engine: only stride 1 and 2 convolutions are supported");
@@ -882,7 +924,11 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow, bool stamps)
       if (!halo && ipt > 1) {
         bool mok = encode_act_map(&prm->tmAm[0], in.hi, o.C, o.W, o.H, B, 1, abw, abh, o.stride, ipt) &&
                    (!x3 || encode_act_map(&prm->tmAm[1], in.lo, o.C, o.W, o.H, B, 1, abw, abh, o.stride, ipt));
-        if (mok && o.res >= 0 && mma_residual_) {
+        if (mok && pj) {
+          const Planes& xb = slot_buf_[static_cast<size_t>(pj->in)];
+          mok = encode_act_map(&prm->tmRm[0], xb.hi, pj->C, pj->W, pj->H, B, 1, wb, hb, pj->stride, ipt) &&
+                (!x3 || encode_act_map(&prm->tmRm[1], xb.lo, pj->C, pj->W, pj->H, B, 1, wb, hb, pj->stride, ipt));
+        } else if (mok && o.res >= 0 && mma_residual_) {
           const Planes& rb = slot_buf_[static_cast<size_t>(o.res)];
           mok = encode_act_map(&prm->tmRm[0], rb.hi, o.Cout, Wo, Ho, B, 1, wb, hb, 1, ipt) &&
                 (!x3 || encode_act_map(&prm->tmRm[1], rb.lo, o.Cout, Wo, Ho, B, 1, wb, hb, 1, ipt));
@@ -933,7 +979,21 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow, bool stamps)
       prm->mode = 0;
       prm->scale = dc.scale;
       prm->shift = dc.shift;
-      if (o.res >= 0) {
+      if (pj) {
+        // projection shortcut on the tensor core: K-steps over the block input
+        // (stride pj->stride) against the projection weights
+        require(!halo, "engine: fused projection with a halo conv");
+        const Planes& xb = slot_buf_[static_cast<size_t>(pj->in)];
+        const DevConv& pw = cnn_w_[static_cast<size_t>(pjx)];
+        bool rok = encode_act_map(&prm->tmR[0], xb.hi, pj->C, pj->W, pj->H, B, 1, wb, hb, pj->stride) &&
+                   (!x3 || encode_act_map(&prm->tmR[1], xb.lo, pj->C, pj->W, pj->H, B, 1, wb, hb, pj->stride)) &&
+                   encode_weight_map(&prm->tmP[0], pw.w.hi, pw.Kp, o.Cout, BN) &&
+                   (!x3 || encode_weight_map(&prm->tmP[1], pw.w.lo, pw.Kp, o.Cout, BN));
+        if (!rok) throw CudaFailure("engine: TMA descriptor encode failed (projection)");
+        prm->nres = pj->C / 64;
+        prm->res_proj = 1;
+        prm->res_stride = pj->stride;
+      } else if (o.res >= 0) {
         const Planes& rb = slot_buf_[static_cast<size_t>(o.res)];
         if (mma_residual_) {
           // residual add on the tensor core: BN/64 extra K-steps (residual x identity)
@@ -1026,9 +1086,11 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow, bool stamps)
                        },
                        1,
                        1, static_cast<int>(cur_count - d_counts_),
-                       2.0 * Ho * Wo * o.Cout * static_cast<double>(o.C) * o.k * o.k,
+                       2.0 * Ho * Wo * o.Cout * (static_cast<double>(o.C) * o.k * o.k + (pj ? pj->C : 0)),
                        (x3 ? 4.0 : 2.0) * (static_cast<double>(o.H) * o.W * o.C +
-                                           static_cast<double>(Ho) * Wo * o.Cout * (o.res >= 0 ? 2 : 1))});
+                                           (pj ? static_cast<double>(pj->H) * pj->W * pj->C / (pj->stride * pj->stride)
+                                               : 0.0) +
+                                           static_cast<double>(Ho) * Wo * o.Cout * (o.res >= 0 && !pj ? 2 : 1))});
     } else if (o.kind == CnnOpKind::Head) {
       Planes in = slot_buf_[static_cast<size_t>(o.in)];
       const int classes = model_.num_classes, C = o.C, HW = o.H * o.W;

@@ -224,6 +224,12 @@ class Engine {
   bool gap_fusion_ = true;  // LCB_NO_GAP_FUSION=1 disables the fused Pool(C) partials
   bool staged_store_ = true;  // LCB_DIRECT_STORE=1: per-row 16-byte stores instead of the staged coalesced epilogue
   bool mma_residual_ = true;  // LCB_NO_MMA_RESIDUAL=1: residual added in the epilogue instead of by identity K-steps
+  // Fused projection shortcuts (LCB_NO_PROJ_FUSION=1 off): a 1x1 projection
+  // conv whose only use is the residual of a later conv runs as that conv's
+  // residual K-steps (TcConvParams::res_proj). By op index:
+  bool proj_fusion_ = true;
+  std::vector<int> proj_into_;  // projection op -> the conv it is fused into (-1: runs on its own)
+  std::vector<int> fused_proj_;  // conv op -> its fused projection op (-1: none)
   __nv_bfloat16* identity_ = nullptr;
   bool fused_lookup_ = true;
   bool wide_lookup_ = true;  // LCB_NO_WIDE_LOOKUP=1: GAP bins + logits GEMM + head as three launches

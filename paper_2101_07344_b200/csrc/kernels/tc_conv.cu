@@ -735,7 +735,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
     if (p.nres) {
       tma_prefetch_desc(&p.tmR[0]);
       if (X3) tma_prefetch_desc(&p.tmR[1]);
-      tma_prefetch_desc(&p.tmE);
+      if (p.res_proj) {
+        tma_prefetch_desc(&p.tmP[0]);
+        if (X3) tma_prefetch_desc(&p.tmP[1]);
+      } else {
+        tma_prefetch_desc(&p.tmE);
+      }
     }
   }
   if (warp == 0) tmem_alloc(smem_u32(tmem_holder), Cfg::kTmemCols);
@@ -953,6 +958,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
         const int pl = lane / (nbox + 1), jb = lane % (nbox + 1);
         const int img_j = __shfl_sync(0xffffffffu, my_img, jb < nbox ? jb : 0);
         const int nk_conv = p.ntaps * cchunks;
+        // residual K-step j: A box coordinates (channel, w, h) and B box (k, n)
+        const int rs = p.res_stride > 0 ? p.res_stride : 1;
+        const int rc0 = p.res_proj ? 0 : x.tn * BN, rw = x.w0 * rs, rh = x.h0 * rs;
+        const CUtensorMap* mapE = p.res_proj ? p.tmP : &p.tmE;  // plane q: mapE[res_proj ? q : 0]
+        const int en = p.res_proj ? x.tn * BN : 0;
         int cc = x.s_begin % cchunks, tap = x.s_begin / cchunks;
         TC_TRACE(unsigned long long pw = 0;)  // cycles spent waiting for free stages
         for (int s = x.s_begin; s < x.s_end; ++s) {
@@ -971,13 +981,13 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
                 if (idx >= g.count) idx = g.count - 1;
                 const int im = image_of(p, idx);
                 if (s >= nk_conv)
-                  tma_load_5d(a0 + j * box_bytes, &mapR[q], fb, x.tn * BN + (s - nk_conv) * 64, x.w0, x.h0, im, 0);
+                  tma_load_5d(a0 + j * box_bytes, &mapR[q], fb, rc0 + (s - nk_conv) * 64, rw, rh, im, 0);
                 else
                   tma_load_5d(a0 + j * box_bytes, &mapA[q], fb, cc * 64, x.w0 * cs + p.tap_dw[tap],
                               x.h0 * cs + p.tap_dh[tap], im, p.tap_phase[tap]);
               }
               if (s >= nk_conv)
-                tma_load_2d(smem_u32(stage_b(stage, q)), &p.tmE, fb, (s - nk_conv) * 64, 0);
+                tma_load_2d(smem_u32(stage_b(stage, q)), &mapE[p.res_proj ? q : 0], fb, (s - nk_conv) * 64, en);
               else
                 tma_load_2d(smem_u32(stage_b(stage, q)), &p.tmB[q], fb, tap * p.C + cc * 64, x.tn * BN);
             }
@@ -985,12 +995,14 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
             const uint32_t a_dst = smem_u32(stage_a(stage, pl)) + jb * box_bytes;
             if (s >= nk_conv) {
               // residual K-step: A = residual channels [tn*BN + j*64, +64) at the
-              // output pixels, B = identity slice (the residual add on the tensor core)
+              // output pixels, B = identity slice (the residual add on the tensor
+              // core); fused projection: A = block-input channels [j*64, +64) at
+              // stride res_stride, B = projection weights [tn*BN, +BN) x [j*64, +64)
               const int j = s - nk_conv;
               if (jb < nbox)
-                tma_load_5d(a_dst, &mapR[pl], fb, x.tn * BN + j * 64, x.w0, x.h0, img_j, 0);
+                tma_load_5d(a_dst, &mapR[pl], fb, rc0 + j * 64, rw, rh, img_j, 0);
               else
-                tma_load_2d(smem_u32(stage_b(stage, pl)), &p.tmE, fb, j * 64, 0);
+                tma_load_2d(smem_u32(stage_b(stage, pl)), &mapE[p.res_proj ? pl : 0], fb, j * 64, en);
             } else {
               if (jb < nbox) {
                 const int wc = x.w0 * cs + p.tap_dw[tap], hc = x.h0 * cs + p.tap_dh[tap], ph = p.tap_phase[tap];
@@ -1040,7 +1052,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
           mbar_wait(full0 + 8 * stage, phase);
           tc_fence_after();
           TC_TRACE(const unsigned long long c1 = p.trace ? clk() : 0;)
-          const bool res_step = s >= nk_conv;
+          // identity K-step (residual add); a fused projection's K-steps are
+          // ordinary bf16x3 K-steps (three products, low accumulator half)
+          const bool res_step = s >= nk_conv && !p.res_proj;
+          const bool proj_step = s >= nk_conv && p.res_proj;
           // K-advance of 16 bf16 = 32 bytes = +2 in the descriptor's address
           // field; stage k's operands sit k * kStageBytes further (< 256 KB,
           // so the 14-bit address field never carries)
@@ -1050,7 +1065,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
           // LCB_DBG bit 16 keeps the per-MMA path for A/B measurements
           const bool fused_issue = !dbg_nomma && !(p.dbg & 16);
           const uint32_t eb = empty0 + 8 * stage;
-          if (fused_issue && stacked && !res_step) {
+          if (fused_issue && stacked && !res_step && !proj_step) {
             umma_kstep_x3_stacked(d_tmem, dah, dal, dbh, idesc2, idesc, s > x.s_begin ? 1u : 0u, eb);
           } else if (fused_issue && X3 && !res_step) {
             umma_kstep_x3_plain(d_tmem, dah, dal, dbh, dbl, idesc, s > x.s_begin ? 1u : 0u, eb);
@@ -1064,7 +1079,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
           for (int k = 0; k < 4; ++k) {
             if (dbg_nomma) break;
             const uint32_t first = (s > x.s_begin || k > 0) ? 1u : 0u;
-            if (stacked && !res_step) {  // [hi*hi | hi*lo] in one MMA, then lo*hi into the low half
+            if (stacked && !res_step && !proj_step) {  // [hi*hi | hi*lo] in one MMA, then lo*hi into the low half
               umma_bf16_warp(d_tmem, dah + 2 * k, dbh + 2 * k, idesc2, first);
               umma_bf16_warp(d_tmem, dal + 2 * k, dbh + 2 * k, idesc, 1u);
             } else {
@@ -1409,6 +1424,7 @@ size_t tc_conv_ws_floats(int BN, int max_ctas) { return 2ull * static_cast<size_
 
 cudaError_t tc_conv_launch(const TcConvParams& p, int BN, int num_sms, cudaStream_t stream) {
   const bool x3 = p.segs == 3;
+  if (p.res_proj && (p.halo || p.nres <= 0)) return cudaErrorInvalidValue;  // the halo producer has no projection path
   switch (BN) {
     case 64:
       return x3 ? launch_cfg<64, true>(p, num_sms, stream) : launch_cfg<64, false>(p, num_sms, stream);

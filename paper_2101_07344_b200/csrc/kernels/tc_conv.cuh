@@ -83,6 +83,15 @@ struct TcConvParams {
   // plane instead of ipt (per-box cost dominates 4x4 / 8x8 images)
   CUtensorMap tmAm[2];
   CUtensorMap tmRm[2];
+  // Fused 1x1 projection shortcut (res_proj = 1): the residual K-steps are the
+  // projection conv of the block input instead of residual x identity — A =
+  // tmR/tmRm over the block input at traversal stride res_stride, B = tmP
+  // (projection weights [Cout][Cx], BN scale folded, hi/lo planes), nres =
+  // Cx / 64; both convs accumulate in one TMEM tile and the epilogue adds the
+  // summed shift. The projection's output never exists in HBM.
+  CUtensorMap tmP[2];
+  int res_proj;
+  int res_stride;
   int multi_img;       // 1: tmAm (and tmRm when nres > 0) are valid
   int stacked;         // bf16x3: hi*hi + hi*lo as one N = 2*BN MMA (see tc_conv.cu TcCfg)
   int nres;            // residual K-steps per tile (BN/64): out = conv + residual computed by the MMA
