@@ -146,6 +146,10 @@ __device__ __forceinline__ Tile decode_tile(int t, const TcConvParams& p, const 
 
 __device__ __forceinline__ int image_of(const TcConvParams& p, int idx) { return p.surv ? p.surv[idx] : idx; }
 
+#ifndef LCB_EPI_UNROLL
+#define LCB_EPI_UNROLL 2
+#endif
+constexpr int kEpiUnroll = LCB_EPI_UNROLL;  // c32 steps of the epilogue loop unrolled together
 constexpr int kEpiWarps = 8;
 constexpr int kEpiThreads = kEpiWarps * 32;
 constexpr int kThreads = 64 + kEpiThreads;
@@ -1135,23 +1139,34 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
     bool valid_n = false, img_ok_n = false;
     int img_n = 0;
     const RowGeom rg = row_geom(p, row);
-    if (static_cast<int>(blockIdx.x) < g.total)
-      valid_n = out_row(p, g, decode_tile(blockIdx.x, p, g), row, rg, obase_n, img_n, img_ok_n);
+    // per-tile shift values live in shared memory, double-buffered with the
+    // accumulators; the NEXT tile's values are loaded into registers while
+    // this tile is processed (their L2 latency was a serial gap per tile)
+    const bool use_shs = p.shift && p.mode == 0;
+    static_assert(BN <= kEpiThreads, "one shift value per epilogue thread");
+    if (static_cast<int>(blockIdx.x) < g.total) {
+      const Tile x0 = decode_tile(blockIdx.x, p, g);
+      valid_n = out_row(p, g, x0, row, rg, obase_n, img_n, img_ok_n);
+      if (use_shs && etid < BN) shift_s[etid] = __ldg(p.shift + x0.tn * BN + etid);
+    }
     for (int t = blockIdx.x; t < g.total; t += gridDim.x, ++unit) {
       const Tile x = decode_tile(t, p, g);
       const size_t obase = obase_n;
       const bool valid = valid_n, img_ok = img_ok_n;
       const int img = img_n;
-      if (t + static_cast<int>(gridDim.x) < g.total)
-        valid_n = out_row(p, g, decode_tile(t + gridDim.x, p, g), row, rg, obase_n, img_n, img_ok_n);
-      const bool split = p.mode == 0 && g.ks > 1;
-      // this tile's shift values -> shared (one coalesced load; the buffer of
-      // tile t-2 is free: every epilogue warp passed this barrier at tile t-1)
-      float* shs = shift_s + acc * BN;
-      if (p.shift && p.mode == 0) {
-        for (int i = etid; i < BN; i += kEpiThreads) shs[i] = __ldg(p.shift + x.tn * BN + i);
-        epi_bar();
+      const bool has_next = t + static_cast<int>(gridDim.x) < g.total;
+      float nsh = 0.0f;
+      if (has_next) {
+        const Tile xn = decode_tile(t + gridDim.x, p, g);
+        valid_n = out_row(p, g, xn, row, rg, obase_n, img_n, img_ok_n);
+        if (use_shs && etid < BN) nsh = __ldg(p.shift + xn.tn * BN + etid);
       }
+      const bool split = p.mode == 0 && g.ks > 1;
+      // this tile's shift values (written at the end of the previous tile, or
+      // before the loop); the barrier also retires every warp's reads of the
+      // other buffer (tile t-1), which the end of this tile overwrites
+      float* shs = shift_s + acc * BN;
+      if (use_shs) epi_bar();
       mbar_wait(tfull0 + 8 * acc, acc_phase);
       tc_fence_after();
       if (etid == 0) trace_put(p, unit, 4);
@@ -1170,7 +1185,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
       }
       // split-K partial tile layout: [tile_mn][ks][BN/16][4 float4 groups][128 rows] (coalesced per warp)
       float* wsp = split ? p.ws + (static_cast<size_t>(x.tile_mn) * g.ks + x.ks) * kBM * BN : nullptr;
-#pragma unroll 1
+#pragma unroll kEpiUnroll
       for (int c32 = 0; c32 < kCols / 32; ++c32) {
         float v[2][16];
         tmem_ld16_nowait(t_row + c32 * 32, v[0]);
@@ -1188,6 +1203,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
         } else {
           tmem_ld_wait();
         }
+        TC_TRACE(if (etid == 0 && c32 < 2) trace_put(p, unit, 16 + 4 * c32);)
         const int cb = x.tn * BN + col0 + c32 * 32;  // first output channel of this step
         if (empty_k) {
 #pragma unroll
@@ -1248,6 +1264,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
             if (X3) st_shared_v4(wstage + 2048 + off, lo[hq]);
           }
         }
+        TC_TRACE(if (etid == 0 && c32 < 2) trace_put(p, unit, 17 + 4 * c32);)
         __syncwarp();
         {
           const int ch = lane & 3;
@@ -1262,11 +1279,13 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
             }
           }
         }
+        TC_TRACE(if (etid == 0 && c32 < 2) trace_put(p, unit, 18 + 4 * c32);)
         if (p.gap_out) {
           gap_segment(p, x, row, lane, v[0], cb, img, img_ok);  // destroys v (after staging)
           gap_segment(p, x, row, lane, v[1], cb + 16, img, img_ok);
         }
       }
+      if (use_shs && has_next && etid < BN) shift_s[(acc ^ 1) * BN + etid] = nsh;
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty0 + 8 * acc);

@@ -8,6 +8,7 @@ import sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
+by_stall = len(sys.argv) > 3 and sys.argv[3] == "stall"
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
@@ -24,5 +25,5 @@ for r in rows:
 ti = sum(d[0] for d in data)
 ts = sum(d[1] for d in data)
 print(f"instructions {ti:.0f}  stall samples {ts:.0f}")
-for d in sorted(data, reverse=True)[:top]:
+for d in sorted(data, key=lambda d: d[1] if by_stall else d[0], reverse=True)[:top]:
     print(f"{d[0]:10.0f} {100*d[0]/ti:5.1f}%  st {100*d[1]/max(ts,1):5.1f}%  {d[2]}:{d[3]:5s} {d[4]}")
