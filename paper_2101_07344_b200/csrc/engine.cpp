@@ -215,6 +215,8 @@ Engine::Engine(int device, const BaseModel& model, std::vector<CacheVariant> var
   const char* nl = std::getenv("LCB_UNFUSED_LOOKUP");
   fused_lookup_ = !(nl && nl[0] == '1');
   if (const char* nc = std::getenv("LCB_NO_CONV_HEAD")) conv_head_ = !(nc[0] == '1');
+  if (const char* cm = std::getenv("LCB_CONV_HEAD_TILE")) conv_head_post_ = !(cm[0] == '1');
+  if (const char* td = std::getenv("LCB_TC_DBG")) tc_dbg_ = std::atoi(td);
   if (const char* nw = std::getenv("LCB_NO_WIDE_LOOKUP")) wide_lookup_ = !(nw[0] == '1');
   const char* ns = std::getenv("LCB_NO_STACKED");
   stacked_ = !(ns && ns[0] == '1');
@@ -278,6 +280,8 @@ void Engine::build_weights() {
   lk_arrive_ = static_cast<int*>(dalloc(sizeof(int)));
   row_tiles_ = static_cast<int*>(dalloc(static_cast<size_t>(B) * sizeof(int)));
   ck(cudaMemsetAsync(row_tiles_, 0, static_cast<size_t>(B) * sizeof(int), stream_), "memset");
+  conv_sync_ = static_cast<unsigned*>(dalloc(sizeof(unsigned)));
+  ck(cudaMemsetAsync(conv_sync_, 0, sizeof(unsigned), stream_), "memset");
   heads_done_ = static_cast<int*>(dalloc(sizeof(int)));
   ck(cudaMemsetAsync(heads_done_, 0, sizeof(int), stream_), "memset");
   ck(cudaMemsetAsync(lk_arrive_, 0, sizeof(int), stream_), "memset");
@@ -1012,6 +1016,7 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow, bool stamps)
       prm->out_hi = out.hi;
       prm->out_lo = out.lo;
       prm->staged_store = staged_store_ ? 1 : 0;
+      prm->dbg = tc_dbg_;  // LCB_TC_DBG: measurement-only kernel bits (wrong results)
       if (o.tap >= 0 && gap_fusion_) {
         // Pool(C) cache on this conv's output: GAP partials from the epilogue.
         const int ci = cache_of_layer_[static_cast<size_t>(o.tap + 1)];
@@ -1025,13 +1030,23 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow, bool stamps)
             }
             prm->gap_out = c.gap;
             prm->gap_segs = segs;
-            if (conv_head_ && fused_lookup_ && c.width % 4 == 0) {
+            // post-phase mode runs heads with <= 32 classes (the wide ones keep
+            // their own persistent launch); per-tile mode (opt-in) also the
+            // features of wide heads
+            // (post mode stages W2, Ws1 and 8 feature rows in the pipeline ring)
+            const long long post_floats = static_cast<long long>(c.classes) * c.width + 16 * 32 + 8LL * c.width;
+            const bool post_fits = post_floats * 4 <= tc_conv_ring_bytes(BN, x3);
+            if (conv_head_ && fused_lookup_ && c.width % 4 == 0 &&
+                (conv_head_post_ ? (c.classes <= 32 && post_fits) : true)) {
               // the lookup rides the conv: every row's GAP features (and, for
               // <= 32 classes, its head and the layer's exit) come from the
-              // CTA that finishes the row's last tile
+              // conv's CTAs — after a grid barrier that follows the last tile
+              // (post mode), or from the CTA finishing the row's last tile
               const int layer = o.tap + 1;
               TcGapHead& gh = prm->gh;
               gh.row_tiles = row_tiles_;
+              gh.post = conv_head_post_ ? 1 : 0;
+              gh.gsync = conv_sync_;
               gh.inv = static_cast<float>(1.0 / (static_cast<double>(Ho) * Wo));
               if (c.classes <= 32) {
                 const ExitParams ex = exit_params(layer, shadow, cur_ids, ids + static_cast<size_t>(layer) * B,

@@ -248,7 +248,14 @@ class Engine {
   // split-K launches of the step list being built (assign_counter_sets)
   std::vector<std::shared_ptr<TcConvParams>> split_prms_;
   void assign_counter_sets();  // grid barrier of the wide lookup (2 ints, self-resetting)
-  bool conv_head_ = false;  // LCB_NO_CONV_HEAD=0 opts in (measured slower: profiles/r02_fused_head_ab.txt)
+  // Lookup (<= 32 classes) fused into the tap conv, opt-in (LCB_NO_CONV_HEAD=0):
+  // post-phase after a grid barrier (warp per row), or with LCB_CONV_HEAD_TILE=1
+  // the older per-tile row arrivals. Both measured slower than the separate
+  // head launch on R18 (profiles/r02_fused_head_ab.txt, profiles/r02c/).
+  bool conv_head_ = false;
+  bool conv_head_post_ = true;
+  int tc_dbg_ = 0;
+  unsigned* conv_sync_ = nullptr;  // grid-barrier counter of the post-phase (monotonic, zeroed once)
   Planes im2col_buf_;
 
   std::vector<Step> steps_[kModes];

@@ -896,11 +896,6 @@ constexpr unsigned kWideSyncPeriod = 512;  // >= 2 * grid
 __device__ __forceinline__ void grid_arrive(unsigned* cnt) {
   asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
 }
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 __device__ __forceinline__ void grid_barrier(unsigned* cnt, unsigned base, unsigned target) {
   __syncthreads();
   if (threadIdx.x == 0) {

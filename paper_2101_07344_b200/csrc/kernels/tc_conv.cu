@@ -146,6 +146,9 @@ __device__ __forceinline__ Tile decode_tile(int t, const TcConvParams& p, const 
 
 __device__ __forceinline__ int image_of(const TcConvParams& p, int idx) { return p.surv ? p.surv[idx] : idx; }
 
+#ifndef LCB_SMEM_SHIFT
+#define LCB_SMEM_SHIFT 1
+#endif
 #ifndef LCB_EPI_UNROLL
 #define LCB_EPI_UNROLL 2
 #endif
@@ -236,6 +239,7 @@ __device__ __forceinline__ bool out_row(const TcConvParams& p, const TileGeom& g
 // scale/shift, residual (prefetched 16-byte chunks), ReLU, hi/lo split and
 // NHWC store of 16 channels.
 // sh: the 16 shift values of these columns (shared-memory copy or global), nullable.
+template <bool kShGlobal = false>
 __device__ __forceinline__ void epilogue_math(const TcConvParams& p, float (&v)[16], int co, const float* sh,
                                               const uint4* rh, const uint4* rl) {
   if (p.scale) {
@@ -253,7 +257,7 @@ __device__ __forceinline__ void epilogue_math(const TcConvParams& p, float (&v)[
     const float4* sh4 = reinterpret_cast<const float4*>(sh);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const float4 s4 = sh4[q];
+      const float4 s4 = kShGlobal ? __ldg(sh4 + q) : sh4[q];  // global: L1-resident broadcast loads
       v[4 * q] += s4.x;
       v[4 * q + 1] += s4.y;
       v[4 * q + 2] += s4.z;
@@ -526,6 +530,154 @@ __device__ __noinline__ void gap_row_head(const TcConvParams& p, int n, int r, i
   if (sint[63]) gap_exit(h, n, etid, lane, sint);
 }
 
+// One halving step of a 32-value reduce-scatter over the lanes (lanes with
+// bit `o` keep the upper kN/2 values and add the partner's): after the steps
+// o = 16, 8, 4, 2, 1, lane l holds the full sum of value l.
+template <int kN>
+__device__ __forceinline__ void rs_half32(float (&v)[32], int o, int lane) {
+  const bool up = (lane & o) != 0;
+#pragma unroll
+  for (int e = 0; e < kN / 2; ++e) {
+    const float send = up ? v[e] : v[e + kN / 2];
+    const float keep = up ? v[e + kN / 2] : v[e];
+    v[e] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+  }
+}
+
+// Post-phase head of survivor row r by ONE warp (classes <= 32): GAP
+// features (fixed segment order) -> logits (lane-strided dots of every class,
+// reduce-scattered so lane k holds logit k) -> softmax (losses.cpp:35-46) ->
+// argmax(pr), lowest index on ties (tensor.hpp:57-63) -> selector
+// FC(C,16)+ReLU+FC(16,1) -> branch-stable sigmoid (losses.cpp:26-33) ->
+// inclusive p >= delta (cache.cpp:259-265). fs: Cout floats of warp scratch;
+// w2s / ws1s: the head weights staged in shared memory by the CTA.
+__device__ __noinline__ void row_head_warp(const TcConvParams& p, int r, int lane, float* fs, const float* w2s,
+                                           const float* ws1s) {
+  const TcGapHead& h = p.gh;
+  const int C = p.Cout, K = h.classes, C4 = C >> 2, S = p.gap_segs;
+  const int img = p.surv ? p.surv[r] : r;
+  const float4* src = reinterpret_cast<const float4*>(p.gap_out + static_cast<size_t>(img) * S * C);
+  // lane -> (float4 column j, segment group q of Q): Q = 32 / C4 groups when
+  // C < 128 (lanes would idle), each summing segments q, q + Q, ... with four
+  // independent accumulators; groups and accumulators combine in fixed order
+  const int Q = C4 < 32 ? 32 / C4 : 1;
+  for (int j0 = 0; j0 < C4; j0 += 32 / Q) {
+    const int j = j0 + (Q > 1 ? lane % C4 : lane), q = Q > 1 ? lane / C4 : 0;
+    float4 a[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) a[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (j < C4) {
+      int sg = q;
+      for (; sg + 3 * Q < S; sg += 4 * Q) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float4 t = __ldcg(src + static_cast<size_t>(sg + u * Q) * C4 + j);
+          a[u].x += t.x;
+          a[u].y += t.y;
+          a[u].z += t.z;
+          a[u].w += t.w;
+        }
+      }
+      for (; sg < S; sg += Q) {
+        const float4 t = __ldcg(src + static_cast<size_t>(sg) * C4 + j);
+        a[0].x += t.x;
+        a[0].y += t.y;
+        a[0].z += t.z;
+        a[0].w += t.w;
+      }
+    }
+    float4 t = make_float4((a[0].x + a[1].x) + (a[2].x + a[3].x), (a[0].y + a[1].y) + (a[2].y + a[3].y),
+                           (a[0].z + a[1].z) + (a[2].z + a[3].z), (a[0].w + a[1].w) + (a[2].w + a[3].w));
+    for (int o = C4; o < 32 && Q > 1; o <<= 1) {  // butterfly over the group bits
+      t.x += __shfl_xor_sync(0xffffffffu, t.x, o);
+      t.y += __shfl_xor_sync(0xffffffffu, t.y, o);
+      t.z += __shfl_xor_sync(0xffffffffu, t.z, o);
+      t.w += __shfl_xor_sync(0xffffffffu, t.w, o);
+    }
+    if (j < C4 && q == 0) {
+      t = make_float4(t.x * h.inv, t.y * h.inv, t.z * h.inv, t.w * h.inv);
+      reinterpret_cast<float4*>(fs)[j] = t;
+      if (h.feat) reinterpret_cast<float4*>(h.feat + static_cast<size_t>(r) * C)[j] = t;
+    }
+  }
+  __syncwarp();
+  float v[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) v[k] = 0.0f;
+#pragma unroll 2
+  for (int c = lane; c < C; c += 32) {
+    const float f = fs[c];
+#pragma unroll
+    for (int k = 0; k < 32; ++k)
+      if (k < K) v[k] += w2s[k * C + c] * f;
+  }
+  rs_half32<32>(v, 16, lane);
+  rs_half32<16>(v, 8, lane);
+  rs_half32<8>(v, 4, lane);
+  rs_half32<4>(v, 2, lane);
+  rs_half32<2>(v, 1, lane);
+  const bool in = lane < K;
+  const float l = in ? v[0] + __ldg(h.b2 + lane) : -FLT_MAX;
+  const float m = wmax(l);
+  const float e = in ? expf(l - m) : 0.0f;
+  const float q = e / wsum(e);
+  float bv = in ? q : -FLT_MAX;
+  int bi = in ? lane : 0x7fffffff;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > bv || (ov == bv && oi < bi)) {
+      bv = ov;
+      bi = oi;
+    }
+  }
+  // hidden unit j on lane j < 16: bs1[j] + sum_k Ws1[j][k] pr_k (k ascending)
+  float hj = 0.0f;
+  for (int k = 0; k < K; ++k) {
+    const float qk = __shfl_sync(0xffffffffu, q, k);
+    if (lane < 16) hj += ws1s[lane * K + k] * qk;
+  }
+  const float a = lane < 16 ? hj + __ldg(h.bs1 + lane) : 0.0f;
+  const float z = h.bs2 + wsum(lane < 16 ? __ldg(h.ws2 + lane) * (a > 0.0f ? a : 0.0f) : 0.0f);
+  float pz;
+  if (z >= 0.0f) {
+    pz = 1.0f / (1.0f + expf(-z));
+  } else {
+    const float ez = expf(z);
+    pz = ez / (1.0f + ez);
+  }
+  if (lane == 0) {
+    h.prob[r] = pz;
+    h.hit[r] = static_cast<double>(pz) >= h.delta ? 1 : 0;
+    h.label[r] = bi;
+  }
+}
+
+// Post-phase lookup over the layer's n rows (after the grid barrier): the
+// head weights are staged in shared memory, one warp per row across every
+// epilogue warp of the grid; each CTA then arrives once and the LAST one runs
+// the exit + compaction (gap_exit).
+__device__ __noinline__ void post_heads(const TcConvParams& p, int n, int etid, int lane, float* scratch, int* sint) {
+  const int ew = etid >> 5;
+  const int C = p.Cout, K = p.gh.classes;
+  float* w2s = scratch;                                   // [K][C]
+  float* ws1s = w2s + K * C;                              // [16][K]
+  float* fs = ws1s + 16 * 32 + static_cast<size_t>(ew) * C;  // [kEpiWarps][C]
+  const bool any = static_cast<int>(blockIdx.x) * kEpiWarps < n;
+  if (any) {
+    for (int i = etid; i < K * C / 4; i += kEpiThreads)
+      reinterpret_cast<float4*>(w2s)[i] = __ldg(reinterpret_cast<const float4*>(p.gh.W2) + i);
+    for (int i = etid; i < 16 * K; i += kEpiThreads) ws1s[i] = __ldg(p.gh.Ws1 + i);
+  }
+  epi_bar();
+  for (int r = blockIdx.x * kEpiWarps + ew; r < n; r += gridDim.x * kEpiWarps) row_head_warp(p, r, lane, fs, w2s, ws1s);
+  epi_bar();  // this CTA's rows (hit/label/prob) before its arrival
+  if (etid == 0) sint[63] = atom_add_acq_rel_gpu(p.gh.heads_done, 1) == static_cast<int>(gridDim.x) - 1 ? 1 : 0;
+  epi_bar();
+  if (sint[63]) gap_exit(p.gh, n, etid, lane, sint);
+}
+
 // After a tile's GAP partials are written by every epilogue warp: count the
 // tile against each of its survivor rows; rows completed here get their
 // features (and head) from this CTA.
@@ -667,7 +819,8 @@ __device__ __noinline__ bool split_reduce(const TcConvParams& p, const TileGeom&
     if (wpu > 1) epi_bar();  // park slots reused by the next round
   }
   if (etid == 0) trace_put(p, unit, 11);
-  if (p.ctr_zero && !p.gh.row_tiles) return false;  // the next split-K launch zeroes this counter set
+  // the next split-K launch zeroes this counter set (post-phase lookups need no per-tile completion)
+  if (p.ctr_zero && (!p.gh.row_tiles || p.gh.post)) return false;
   epi_bar();  // this CTA's GAP partials visible before its arrival
   if (etid == 0) {
     const bool last = atom_add_acq_rel_gpu(dep, 1) == g.ks - 1;
@@ -1142,7 +1295,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
     // per-tile shift values live in shared memory, double-buffered with the
     // accumulators; the NEXT tile's values are loaded into registers while
     // this tile is processed (their L2 latency was a serial gap per tile)
-    const bool use_shs = p.shift && p.mode == 0;
+    // LCB_SMEM_SHIFT=0 (default): the epilogue reads shift values straight from
+    // global memory (L1 broadcast) and warps are not re-synchronised per tile,
+    // so their math and store phases interleave instead of bursting together
+    const bool use_shs = LCB_SMEM_SHIFT && p.shift && p.mode == 0;
     static_assert(BN <= kEpiThreads, "one shift value per epilogue thread");
     if (static_cast<int>(blockIdx.x) < g.total) {
       const Tile x0 = decode_tile(blockIdx.x, p, g);
@@ -1249,7 +1405,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
               rl[1] = reinterpret_cast<const uint4*>(p.res_lo + obase + co)[1];
             }
           }
-          epilogue_math(p, v[u], co, p.shift ? shs + (co - x.tn * BN) : nullptr, r ? rh : nullptr,
+          epilogue_math<!LCB_SMEM_SHIFT>(p, v[u], co,
+                                         p.shift ? (LCB_SMEM_SHIFT ? shs + (co - x.tn * BN) : p.shift + co) : nullptr,
+                                         r ? rh : nullptr,
                         (r && X3 && p.res_lo) ? rl : nullptr);
           if (!valid) {
 #pragma unroll
@@ -1291,10 +1449,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
       if (lane == 0) mbar_arrive(tempty0 + 8 * acc);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
+      const bool per_tile = p.gh.row_tiles && !p.gh.post;
       if (split) {
-        if (split_reduce(p, g, x, BN, etid, lane, unit, epi_stage, sint + 127) && p.gh.row_tiles)
+        if (split_reduce(p, g, x, BN, etid, lane, unit, epi_stage, sint + 127) && per_tile)
           gap_complete(p, g, x, etid, lane, reinterpret_cast<float*>(epi_stage), sint);
-      } else if (p.gh.row_tiles) {
+      } else if (per_tile) {
         gap_complete(p, g, x, etid, lane, reinterpret_cast<float*>(epi_stage), sint);
       }
       if (etid == 0) trace_put(p, unit, 5);
@@ -1305,6 +1464,25 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
   if (warp == 0) {
     __syncwarp();
     tmem_dealloc(tmem_base, Cfg::kTmemCols);
+  }
+  if (p.gh.row_tiles && p.gh.post && !(p.dbg & 64)) {  // (dbg 64/32: measurement only, no post-phase / no heads)
+    // Lookup post-phase: every CTA's GAP partials are written; one grid
+    // barrier, then the survivor rows' features and heads (row-strided over
+    // the CTAs, epilogue warps), the last head's CTA runs exit + compaction.
+    // Monotonic counter: each launch adds kPostSyncPeriod in total (gridDim.x
+    // arrivals, CTA 0 pads), so its base is the counter rounded down.
+    constexpr unsigned kPostSyncPeriod = 256;  // >= grid, divides 2^32
+    if (threadIdx.x == 0) {
+      const unsigned base = ld_acquire_u32(p.gh.gsync) & ~(kPostSyncPeriod - 1u);
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.gh.gsync) : "memory");
+      while (ld_acquire_u32(p.gh.gsync) - base < gridDim.x) __nanosleep(32);
+      if (blockIdx.x == 0)
+        asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p.gh.gsync), "r"(kPostSyncPeriod - gridDim.x)
+                     : "memory");
+    }
+    __syncthreads();
+    if (warp >= 2 && !(p.dbg & 32))  // the (idle) pipeline stages are the warps' feature scratch
+      post_heads(p, g.count, threadIdx.x - 64, lane, reinterpret_cast<float*>(smem), sint);
   }
 }
 

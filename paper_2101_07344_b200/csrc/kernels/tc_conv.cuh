@@ -46,6 +46,12 @@ constexpr int kMaxTaps = 64;
 // (serve_one, serving.cpp:112-121): no separate lookup launch.
 struct TcGapHead {
   int* row_tiles;          // nullptr = off; [max_rows] per-row tile arrivals (zeroed, reset by the finisher)
+  // post = 1: no per-tile arrivals. After the CTA's last tile every CTA of the
+  // launch (all resident: persistent grid) meets at a grid barrier on gsync,
+  // then the rows' GAP features and heads are computed by CTAs in row-strided
+  // order, and the CTA finishing the last head runs the exit + compaction.
+  int post;
+  unsigned* gsync;         // monotonic grid-barrier counter (zeroed once)
   float inv;               // 1 / (Ho * Wo)
   float* feat;             // nullable: [max_rows][Cout] fp32 GAP features by row (for a separate head)
   int classes;             // 0 = features only; else <= 32: fused head + exit
