@@ -516,7 +516,9 @@ void Engine::build_weights() {
     c->logits_out = static_cast<float*>(dalloc(static_cast<size_t>(B) * C * sizeof(float)));
     if (C > 32 && c->family != 2) {
       const int feat = c->family == 1 ? c->width : c->h;
-      c->fc_scratch = static_cast<float*>(dalloc(static_cast<size_t>(rows_fc_splits(feat)) * B * C * sizeof(float)));
+      // (also the wide lookup's per-row, per-CTA softmax records: B x grid x 20 floats)
+      const size_t sc = std::max(static_cast<size_t>(rows_fc_splits(feat)) * B * C, static_cast<size_t>(B) * num_sms_ * 20);
+      c->fc_scratch = static_cast<float*>(dalloc(sc * sizeof(float)));
     }
     caches_.push_back(std::move(c));
   }

@@ -880,7 +880,7 @@ struct WideLookupParams {
   CacheHeadParams h;  // classes, feat (= C), W2, b2, Ws1, bs1, ws2, bs2, delta, count, gap, gap_segs, gap_inv, gap_ids,
                       // prob, hit, label, pr_out, logits_out, ex
   float* feats;       // [max_rows][C] scratch
-  float* logits;      // [max_rows][classes] scratch
+  float* logits;      // [max_rows][grid][kWideRec] per-row, per-CTA softmax records (scratch)
   unsigned* gsync;    // arrival counter of the grid barriers (zero-initialised once)
   int kpc;            // classes per CTA (phase 2)
   unsigned long long* stamps;  // nullable: CTA 0's %globaltimer at each phase boundary [8]
@@ -919,28 +919,43 @@ __device__ __forceinline__ void rs_halve(float (&v)[32], int o, int lane) {
 }
 
 constexpr int kWideSegGroups = kLk / 16;  // 16 float4 columns (64 channels) x 32 segment groups
-constexpr int kWideFeatChunk = 8192;      // floats of feature rows staged per phase-2 chunk
+constexpr int kWideFeatChunk = 4096;      // largest feature width (C) of a wide lookup
+constexpr int kWideScratch = 4 * kLk * 4;  // floats of phase-1 scratch (4 float4 per thread)
+constexpr int kWideRec = 20;              // record of one (row, CTA): max, argmax, sum e, 16 selector sums, pad
+
+// Group of 8 lanes (lane bits 0-2) reductions of the split softmax.
+__device__ __forceinline__ float g8_max(float v) {
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float g8_sum(float v) {
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
 
 __global__ void __launch_bounds__(kLk, 1) wide_lookup_kernel(WideLookupParams q) {
   extern __shared__ __align__(16) float wsm[];
   __shared__ HeadSmem hs;
-  __shared__ float4 red4[kLk];
   __shared__ float wpart[64 * 32];  // phase-2 partial sums [row block x slice][32]
   const CacheHeadParams& p = q.h;
 #define STAMP(i) \
   if (q.stamps && blockIdx.x == 0 && threadIdx.x == 0) q.stamps[i] = globaltimer();
   STAMP(0);
   const int C = p.feat, K = p.classes, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int G = gridDim.x;
   const int k0 = blockIdx.x * q.kpc;
   const int k1 = k0 + q.kpc < K ? k0 + q.kpc : K;
   const int nk = k1 > k0 ? k1 - k0 : 0;
-  float* w2s = wsm;                                        // [kpc][C]
-  float* ws1s = w2s + static_cast<size_t>(q.kpc) * C;       // [16][K]
-  float* lrow = ws1s + 16 * K;                              // [K] logits of the row
-  float* prow = lrow + K;                                   // [K] pr
-  float* fchunk = prow + K;                                 // [kWideFeatChunk] feature rows
+  float* w2s = wsm;                                    // [kpc][C]  the CTA's classes of W2
+  float* ws1c = w2s + static_cast<size_t>(q.kpc) * C;  // [16][8]   their selector columns
+  float* fst = ws1c + 16 * 8;                          // [kWideScratch] phase-1 scratch
   if (nk > 0) stage_floats(w2s, p.W2 + static_cast<long long>(k0) * C, nk * C, tid);
-  stage_floats(ws1s, p.Ws1, 16 * K, tid);
+  if (tid < 16 * 8) {
+    const int j = tid >> 3, k = tid & 7;
+    ws1c[tid] = k < nk ? __ldg(p.Ws1 + j * K + k0 + k) : 0.0f;
+  }
   pdl_wait();
   STAMP(1);
   const int n = *p.count;
@@ -954,7 +969,7 @@ __global__ void __launch_bounds__(kLk, 1) wide_lookup_kernel(WideLookupParams q)
     const int C4 = C >> 2;
     const int col_units = (C4 + 15) / 16, total = n * col_units;
     const int j = tid & 15, g = tid >> 4;
-    float4* scr = reinterpret_cast<float4*>(fchunk);  // [4][kLk]
+    float4* scr = reinterpret_cast<float4*>(fst);  // [4][kLk]
     for (int ub = blockIdx.x; ub < total; ub += 4 * gridDim.x) {
       const float4* base[4];
       bool ok[4];
@@ -993,60 +1008,101 @@ __global__ void __launch_bounds__(kLk, 1) wide_lookup_kernel(WideLookupParams q)
     }
   }
   grid_barrier(q.gsync, sync_base, gridDim.x);
-  // ---- phase 2: logits of the CTA's classes for every row. A warp owns a
-  // block of 4 rows x the CTA's <= 8 classes over a slice of the channels
-  // (lanes strided; feature loads straight from L2, all of a lane's loads in
-  // flight): 32 accumulators per lane, reduce-scattered across the lanes (31
-  // shuffles), then the slices of a block are added in fixed order.
+  // ---- phase 2: logits of the CTA's classes for every row, then the row's
+  // split-softmax record over those classes, by chunks of rows. A warp owns a block of 4
+  // rows x the CTA's <= 8 classes over a slice of the channels: 32
+  // accumulators per lane, reduce-scattered across the lanes (31 shuffles),
+  // slices added in fixed order. Record of (row, CTA): m = max logit, the
+  // lowest class index attaining it, S = sum e^(l - m), sel_j = sum Ws1[j][k]
+  // e^(l_k - m) — softmax + selector FC(C,16) reassociate exactly over CTAs
+  // (losses.cpp:35-46, cache.cpp:259-265).
   STAMP(2);
-  if (nk > 0) {
-    constexpr int kRowsPerPass = 256;  // 64 row blocks: wpart holds <= 64 x 32 partials
-    for (int r0 = 0; r0 < n; r0 += kRowsPerPass) {
-      const int rn = n - r0 < kRowsPerPass ? n - r0 : kRowsPerPass;
+  {
+    constexpr int R = 256;  // rows per pass (<= 64 row blocks of partial sums)
+    for (int r0 = 0; r0 < n; r0 += R) {
+      const int rn = n - r0 < R ? n - r0 : R;
       const int nb = (rn + 3) >> 2;  // row blocks
       int wpb = 1;                   // warps per row block (channel slices of >= 32)
       while (wpb * 2 * nb <= kLk / 32 && C / (wpb * 2) >= 32) wpb *= 2;
       const int per = (kLk / 32) / wpb;  // row blocks in flight
-      for (int rb = warp / wpb; rb < nb; rb += per) {
-        const int sub = warp % wpb;
-        const int c0 = (C * sub) / wpb, c1 = (C * (sub + 1)) / wpb;
-        float v[32];
+      if (nk > 0) {
+        for (int rb = warp / wpb; rb < nb; rb += per) {
+          const int sub = warp % wpb;
+          const int c0 = (C * sub) / wpb, c1 = (C * (sub + 1)) / wpb;
+          float v[32];
 #pragma unroll
-        for (int e = 0; e < 32; ++e) v[e] = 0.0f;
-        const int rbase = r0 + rb * 4;
-        const float* f[4];
+          for (int e = 0; e < 32; ++e) v[e] = 0.0f;
+          const float* f[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) f[i] = q.feats + static_cast<long long>(rbase + i < n ? rbase + i : rbase) * C;
+          for (int i = 0; i < 4; ++i)
+            f[i] = q.feats + static_cast<long long>(r0 + (rb * 4 + i < rn ? rb * 4 + i : rb * 4)) * C;
 #pragma unroll 4
-        for (int c = c0 + lane; c < c1; c += 32) {
-          float x[4];
+          for (int c = c0 + lane; c < c1; c += 32) {
+            float x[4];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) x[i] = rbase + i < n ? __ldcg(f[i] + c) : 0.0f;
+            for (int i = 0; i < 4; ++i) x[i] = __ldcg(f[i] + c);
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const float w = k < nk ? w2s[k * C + c] : 0.0f;
+            for (int k = 0; k < 8; ++k) {
+              const float w = k < nk ? w2s[k * C + c] : 0.0f;
 #pragma unroll
-            for (int i = 0; i < 4; ++i) v[i * 8 + k] += x[i] * w;
+              for (int i = 0; i < 4; ++i) v[i * 8 + k] += x[i] * w;
+            }
+          }
+          // lane l ends with the full sum of accumulator l = (row i = l / 8, class k = l % 8)
+          rs_halve<32>(v, 16, lane);
+          rs_halve<16>(v, 8, lane);
+          rs_halve<8>(v, 4, lane);
+          rs_halve<4>(v, 2, lane);
+          rs_halve<2>(v, 1, lane);
+          wpart[(rb * wpb + sub) * 32 + lane] = v[0];
+        }
+      }
+      __syncthreads();
+      // records: warp w handles row blocks w, w + 16, ...; lanes 8i..8i+7 = row i's classes
+      for (int rb = warp; rb < nb; rb += kLk / 32) {
+        const int i = lane >> 3, k = lane & 7, rr = rb * 4 + i;
+        const bool kin = k < nk;
+        float l = -FLT_MAX;
+        if (kin) {
+          float a = wpart[(rb * wpb) * 32 + lane];
+          for (int sb = 1; sb < wpb; ++sb) a += wpart[(rb * wpb + sb) * 32 + lane];
+          l = a + __ldg(p.b2 + k0 + k);
+        }
+        const float m = g8_max(l);
+        // lowest class index attaining the max (softmax is monotonic: argmax(pr) = argmax(logits))
+        int am = kin && l == m ? k : 8;
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) am = min(am, __shfl_xor_sync(0xffffffffu, am, o));
+        const float e = kin ? expf(l - m) : 0.0f;
+        const float S = g8_sum(e);
+        // 16 selector sums reduce-scattered over the 8 lanes: lane k ends with j = 2k, 2k + 1
+        float sv[16];
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) sv[jj] = ws1c[jj * 8 + k] * e;
+#pragma unroll
+        for (int o = 4, h = 8; o > 0; o >>= 1, h >>= 1) {
+          const bool up = (lane & o) != 0;
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            if (t < h) {
+              const float send = up ? sv[t] : sv[t + h];
+              const float keep = up ? sv[t + h] : sv[t];
+              sv[t] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
           }
         }
-        // lane l ends with the full sum of accumulator l = (row i = l / 8, class k = l % 8)
-        rs_halve<32>(v, 16, lane);
-        rs_halve<16>(v, 8, lane);
-        rs_halve<8>(v, 4, lane);
-        rs_halve<4>(v, 2, lane);
-        rs_halve<2>(v, 1, lane);
-        wpart[(rb * wpb + sub) * 32 + lane] = v[0];
-      }
-      __syncthreads();
-      for (int t = tid; t < nb * 32; t += kLk) {
-        const int rb = t >> 5, l = t & 31, i = l >> 3, k = l & 7;
-        if (rb * 4 + i < rn && k < nk) {
-          float a = wpart[(rb * wpb) * 32 + l];
-          for (int sb = 1; sb < wpb; ++sb) a += wpart[(rb * wpb + sb) * 32 + l];
-          q.logits[static_cast<long long>(r0 + rb * 4 + i) * K + k0 + k] = a + __ldg(p.b2 + k0 + k);
+        if (rr < rn && nk > 0) {
+          float* rec = q.logits + (static_cast<long long>(r0 + rr) * G + blockIdx.x) * kWideRec;
+          if (k == 0) {
+            rec[0] = m;
+            rec[1] = __int_as_float(k0 + am);
+            rec[2] = S;
+          }
+          rec[3 + 2 * k] = sv[0];
+          rec[4 + 2 * k] = sv[1];
         }
       }
-      __syncthreads();
+      __syncthreads();  // wpart reused by the next chunk
     }
   }
   STAMP(3);
@@ -1056,12 +1112,96 @@ __global__ void __launch_bounds__(kLk, 1) wide_lookup_kernel(WideLookupParams q)
                  : "memory");
   STAMP(4);
   pdl_trigger();
-  // ---- phase 3: the head of each row
+  // ---- phase 3: each row combines its G records (fixed CTA order):
+  // M = max m_c, label = the lowest CTA's argmax attaining M, S = sum S_c
+  // e^(m_c - M), sel_j = sum sel_c,j e^(m_c - M); then the selector head.
+  const int nwarps = kLk / 32;
   for (int r = blockIdx.x; r < n; r += gridDim.x) {
-    for (int k = tid; k < K; k += kLk) lrow[k] = __ldcg(q.logits + static_cast<long long>(r) * K + k);
+    const bool has = tid < G && (tid * q.kpc < K);  // CTAs that own classes wrote records
+    float rv[kWideRec];
+    if (has) {
+      const float4* src = reinterpret_cast<const float4*>(q.logits + (static_cast<long long>(r) * G + tid) * kWideRec);
+#pragma unroll
+      for (int u = 0; u < kWideRec / 4; ++u) {
+        const float4 t = __ldcg(src + u);
+        rv[4 * u] = t.x;
+        rv[4 * u + 1] = t.y;
+        rv[4 * u + 2] = t.z;
+        rv[4 * u + 3] = t.w;
+      }
+    } else {
+      rv[0] = -FLT_MAX;
+      rv[1] = __int_as_float(0x7fffffff);
+    }
+    // block max with the lowest CTA index on ties (CTAs own ascending class ranges)
+    float bv = rv[0];
+    int bc = has ? tid : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+      if (ov > bv || (ov == bv && oc < bc)) {
+        bv = ov;
+        bc = oc;
+      }
+    }
+    if (lane == 0) {
+      hs.bv[warp] = bv;
+      hs.bi[warp] = bc;
+    }
     __syncthreads();
-    head_block(p, r, lrow, prow, hs, ws1s);
+    float M = hs.bv[0];
+    int cm = hs.bi[0];
+    for (int w = 1; w < nwarps; ++w)
+      if (hs.bv[w] > M || (hs.bv[w] == M && hs.bi[w] < cm)) {
+        M = hs.bv[w];
+        cm = hs.bi[w];
+      }
+    const float wt = has ? expf(rv[0] - M) : 0.0f;
+    float acc[17];
+    acc[16] = has ? rv[2] * wt : 0.0f;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc[j] = has ? rv[3 + j] * wt : 0.0f;
+#pragma unroll
+    for (int j = 0; j < 17; ++j) acc[j] = warp_sum(acc[j]);
+    if (lane < 17) {
+      float v = acc[0];
+#pragma unroll
+      for (int j = 1; j < 17; ++j) v = lane == j ? acc[j] : v;
+      hs.part[warp * 17 + lane] = v;
+    }
+    if (tid == cm) hs.S = rv[1];  // the label: argmax of the CTA holding the maximum (int bits)
     __syncthreads();
+    if (warp == 0) {
+      float t = 0.0f;
+      if (lane < 17)
+        for (int w = 0; w < nwarps; ++w) t += hs.part[w * 17 + lane];
+      const float S = __shfl_sync(0xffffffffu, t, 16);
+      float h = 0.0f;
+      if (lane < 16) {
+        const float a = t / S + p.bs1[lane];
+        h = (a > 0.0f ? a : 0.0f) * p.ws2[lane];
+      }
+      float hj[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) hj[j] = __shfl_sync(0xffffffffu, h, j);
+      if (lane == 0) {
+        float z = p.bs2;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) z += hj[j];
+        float qv;
+        if (z >= 0.0f) {
+          qv = 1.0f / (1.0f + expf(-z));
+        } else {
+          const float ez = expf(z);
+          qv = ez / (1.0f + ez);
+        }
+        p.prob[r] = qv;
+        p.hit[r] = static_cast<double>(qv) >= p.delta ? 1 : 0;
+        p.label[r] = __float_as_int(hs.S);
+      }
+    }
+    __syncthreads();  // hs reused by the next row
   }
   STAMP(5);
   if (p.ex.arrive) exit_tail(p.ex, n, p.prob, p.hit, p.label);
@@ -1461,14 +1601,14 @@ void launch_rows_fc(const float* A, long long lda, int ks, long long part_stride
 
 size_t wide_lookup_smem(int classes, int C, int grid) {
   const int kpc = (classes + grid - 1) / grid;
-  return (static_cast<size_t>(kpc) * C + 16 * static_cast<size_t>(classes) + 2 * static_cast<size_t>(classes) +
-          kWideFeatChunk) *
-         sizeof(float);
+  return (static_cast<size_t>(kpc) * C + 16 * 8 + kWideScratch) * sizeof(float);
 }
 
 constexpr size_t kWideSmemMax = 200 * 1024;
 bool wide_lookup_supported(int classes, int C, int num_sms) {
-  return classes > 32 && C % 4 == 0 && C <= kWideFeatChunk && wide_lookup_smem(classes, C, num_sms) <= kWideSmemMax;
+  const int grid = num_sms < static_cast<int>(kWideSyncPeriod / 2) ? num_sms : static_cast<int>(kWideSyncPeriod / 2);
+  return classes > 32 && C % 4 == 0 && C <= kWideFeatChunk && (classes + grid - 1) / grid <= 8 &&
+         grid <= kLk && wide_lookup_smem(classes, C, num_sms) <= kWideSmemMax;
 }
 
 

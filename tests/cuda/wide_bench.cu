@@ -74,7 +74,7 @@ static void run(int B, int n, int C, int segs, int classes, int sms) {
   e.ids_out = dev_fill<int>(B, 0);
   e.count_out = dev_fill<int>(1, 0);
   float* feats = dev_fill<float>(static_cast<size_t>(B) * C, 0.0f);
-  float* logits = dev_fill<float>(static_cast<size_t>(B) * classes, 0.0f);
+  float* logits = dev_fill<float>(static_cast<size_t>(B) * sms * 20, 0.0f);  // per-row, per-CTA softmax records
   int* gsync = dev_fill<int>(2, 0);
   for (int i = 0; i < 3; ++i) launch_wide_lookup(p, feats, logits, gsync, sms, 0);
   CK(cudaDeviceSynchronize());
