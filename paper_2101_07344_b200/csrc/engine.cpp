@@ -1228,7 +1228,16 @@ void Engine::serve_mode(int B, int mode, bool use_graph) {
   if (!ge) {
     cudaGraph_t g;
     ck(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "capture");
-    for (Step& s : st) s.run(stream_);
+    try {
+      for (Step& s : st) s.run(stream_);
+    } catch (...) {
+      // a failed launch must not leave the (shared) stream capturing
+      cudaGraph_t partial = nullptr;
+      cudaStreamEndCapture(stream_, &partial);
+      if (partial) cudaGraphDestroy(partial);
+      cudaGetLastError();
+      throw;
+    }
     ck(cudaStreamEndCapture(stream_, &g), "capture end");
     ck(cudaGraphInstantiate(&ge, g, 0), "graph instantiate");
     cudaGraphDestroy(g);
