@@ -227,6 +227,7 @@ Engine::Engine(int device, const BaseModel& model, std::vector<CacheVariant> var
   const char* nr = std::getenv("LCB_NO_MMA_RESIDUAL");
   mma_residual_ = !(nr && nr[0] == '1');
   if (const char* np = std::getenv("LCB_NO_PROJ_FUSION")) proj_fusion_ = !(np[0] == '1');
+  if (const char* sp = std::getenv("LCB_NO_STEM_POOL")) stem_pool_ = !(sp[0] == '1');
   const char* nt = std::getenv("LCB_DIRECT_STORE");
   staged_store_ = !(nt && nt[0] == '1');
   build_weights();
@@ -358,6 +359,22 @@ void Engine::build_weights() {
         fused_proj_[i] = j;
       }
     }
+    // stem followed by the 3x3/s2/p1 max-pool that is its output's only use
+    stem_pool_op_ = -1;
+    if (stem_pool_) {
+      for (size_t i = 0; i + 1 < nops; ++i) {
+        const CnnOp& st = model_.ops[i];
+        const CnnOp& mp = model_.ops[i + 1];
+        if (st.kind != CnnOpKind::Stem || mp.kind != CnnOpKind::MaxPool || mp.in != st.out || mp.k != 3 ||
+            mp.stride != 2 || mp.pad != 1 || !st.relu)
+          continue;
+        int uses = 0;
+        for (const CnnOp& o : model_.ops) uses += (o.in == st.out) + (o.res == st.out);
+        const StemGeom sg = stem_geom(st.H, st.W, st.k, st.stride, st.pad);
+        if (uses == 1 && sg.Wx <= 128 && mp.Ho() == (sg.Ho - 1) / 2 + 1 && mp.Wo() == (sg.Wo - 1) / 2 + 1)
+          stem_pool_op_ = static_cast<int>(i + 1);
+      }
+    }
     std::vector<long long> slot_elems(static_cast<size_t>(model_.nslots), 0);
     long long im2col_elems = 0;
     for (size_t i = 0; i < model_.ops.size(); ++i) {
@@ -372,11 +389,28 @@ void Engine::build_weights() {
         const size_t per_out = ws.size() / static_cast<size_t>(o.Cout);
         for (size_t i = 0; i < ws.size(); ++i) ws[i] *= o.scale[i / per_out];  // fold BN scale
         stem_weights(ws.data(), o.Cout, o.C, o.k, o.stride, g, w.data());
-        dc.w = upload_planes(w);
+        if (prec_ == kPrecX3) {
+          // stacked per tap and channel group: 64 hi rows then 64 lo rows (tc_stem's N = 128 MMA)
+          std::vector<__nv_bfloat16> hi, lo, st(2 * w.size());
+          split_planes(w, hi, lo);
+          const size_t groups = w.size() / (64 * 8);  // taps x 2
+          for (size_t gi = 0; gi < groups; ++gi)
+            for (size_t r = 0; r < 64 * 8; ++r) {
+              st[gi * 1024 + r] = hi[gi * 512 + r];
+              st[gi * 1024 + 512 + r] = lo[gi * 512 + r];
+            }
+          dc.w.hi = static_cast<__nv_bfloat16*>(dalloc(st.size() * 2));
+          h2d(dc.w.hi, st.data(), st.size() * 2);
+          dc.w.lo = nullptr;
+        } else {
+          dc.w = upload_planes(w);
+        }
         dc.scale = nullptr;
         dc.shift = upload_f32(to_f32(o.shift));
         cnn_w_[i] = dc;
-        slot_elems[static_cast<size_t>(o.out)] = static_cast<long long>(B) * o.Ho() * o.Wo() * o.Cout;
+        // fused with the max-pool: the stem writes the horizontally pooled rows
+        const long long ow = stem_pool_op_ == static_cast<int>(i + 1) ? (o.Wo() - 1) / 2 + 1 : o.Wo();
+        slot_elems[static_cast<size_t>(o.out)] = static_cast<long long>(B) * o.Ho() * ow * o.Cout;
         im2col_elems = std::max(im2col_elems, static_cast<long long>(B) * 2 * g.Hx * g.Wx * 8);
       } else if (o.kind == CnnOpKind::Conv) {
         DevConv dc;
@@ -890,9 +924,25 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow, bool stamps)
       sp.relu = o.relu ? 1 : 0;
       sp.out_hi = out.hi;
       sp.out_lo = x3 ? out.lo : nullptr;
+      const bool hpool = stem_pool_op_ == static_cast<int>(i + 1);
+      if (hpool) {
+        sp.hpool = 1;
+        sp.Wp = (g.Wo - 1) / 2 + 1;
+        sp.tiles_per_img = g.Ho;  // one output row per tile
+      }
       steps.push_back({[sp, sms](cudaStream_t s) { ck(tc_stem_launch(sp, sms, s), "tc_stem"); }, 1, 1, 0,
                        2.0 * g.Ho * g.Wo * o.Cout * o.k * o.k * o.C,
-                       (x3 ? 4.0 : 2.0) * (32.0 * g.Hx * g.Wx / 2.0 + static_cast<double>(g.Ho) * g.Wo * o.Cout)});
+                       (x3 ? 4.0 : 2.0) * (32.0 * g.Hx * g.Wx / 2.0 +
+                                           static_cast<double>(g.Ho) * (hpool ? sp.Wp : g.Wo) * o.Cout)});
+    } else if (o.kind == CnnOpKind::MaxPool && stem_pool_op_ == static_cast<int>(i)) {
+      // vertical half of the stem's max-pool over the horizontally pooled rows
+      Planes in = slot_buf_[static_cast<size_t>(o.in)], out = slot_buf_[static_cast<size_t>(o.out)];
+      const int Hi = o.H, Wp = o.Wo(), Hp = o.Ho(), C = o.C;
+      steps.push_back({[in, out, Hi, Wp, Hp, C, cur_ids, cur_count, B](cudaStream_t s) {
+                         launch_stem_vpool(in.hi, in.lo, Hi, Wp, C, Hp, cur_ids, cur_count, B, out.hi, out.lo, s);
+                       },
+                       0, 1, static_cast<int>(cur_count - d_counts_), 0.0,
+                       (x3 ? 4.0 : 2.0) * (static_cast<double>(Hi) * Wp * C + static_cast<double>(Hp) * Wp * C)});
     } else if (o.kind == CnnOpKind::MaxPool) {
       Planes in = slot_buf_[static_cast<size_t>(o.in)], out = slot_buf_[static_cast<size_t>(o.out)];
       const int Ho = o.Ho(), Wo = o.Wo();

@@ -228,6 +228,10 @@ class Engine {
   // conv whose only use is the residual of a later conv runs as that conv's
   // residual K-steps (TcConvParams::res_proj). By op index:
   bool proj_fusion_ = true;
+  // Stem + 3x3/s2 max-pool: the horizontal half of the pool rides the stem's
+  // epilogue, the vertical half is a small kernel (LCB_NO_STEM_POOL=1 off).
+  bool stem_pool_ = true;
+  int stem_pool_op_ = -1;  // the max-pool op fused with the stem (-1: none)
   std::vector<int> proj_into_;  // projection op -> the conv it is fused into (-1: runs on its own)
   std::vector<int> fused_proj_;  // conv op -> its fused projection op (-1: none)
   __nv_bfloat16* identity_ = nullptr;

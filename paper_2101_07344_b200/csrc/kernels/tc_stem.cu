@@ -6,6 +6,8 @@
 //   warp 1     : MMA issuer (lane 0): k'^2 taps x {1, 3} MMAs (M128 N64 K16)
 //   warps 2..9 : epilogue (TMEM lane quadrant warp % 4, column half (warp-2)/4): folded BN, ReLU,
 //                hi/lo split, NHWC store of the valid anchors
+#include <cfloat>
+
 #include "pdl.cuh"
 #include "sm100_prims.cuh"
 #include "tc_stem.cuh"
@@ -56,11 +58,13 @@ __host__ __device__ inline StemSmem stem_smem(int x3, int kk, int Wx) {
   return s;
 }
 
-template <bool X3>
+// KK > 0: compile-time taps per dimension (the MMA issue loop fully unrolled); 0: p.kk.
+template <bool X3, int KK>
 __global__ void __launch_bounds__(320, 1) tc_stem_kernel(const __grid_constant__ StemParams p) {
+  const int kk = KK > 0 ? KK : p.kk;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const StemSmem L = stem_smem(X3 ? 1 : 0, p.kk, p.Wx);
+  const StemSmem L = stem_smem(X3 ? 1 : 0, kk, p.Wx);
   const int S = L.stages;
   uint8_t* wsm = smem;
   uint8_t* slabs = smem + L.w_bytes;
@@ -88,7 +92,9 @@ __global__ void __launch_bounds__(320, 1) tc_stem_kernel(const __grid_constant__
     fence_mbar_init();
   }
   if (threadIdx.x < kCout) shift_s[threadIdx.x] = p.shift[threadIdx.x];
-  if (warp == 0) tmem_alloc(smem_u32(tmem_holder), 2 * kCout);
+  // bf16x3: accumulators are [hi*hi | hi*lo] = 2 x 64 columns (the stacked MMA below)
+  constexpr uint32_t kAccCols = X3 ? 2 * kCout : kCout;
+  if (warp == 0) tmem_alloc(smem_u32(tmem_holder), 2 * kAccCols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -99,24 +105,22 @@ __global__ void __launch_bounds__(320, 1) tc_stem_kernel(const __grid_constant__
   const int count = *p.count;
   const int total = count * p.tiles_per_img;
   const int HWx = p.Hx * p.Wx;
-  const int npix = kBM + (p.kk - 1) * (p.Wx + 1);
+  const int npix = kBM + (kk - 1) * (p.Wx + 1);
 
   if (warp == 0) {
     {
       // ------------------------------------------------ producer (whole warp:
       // the planes x groups bulk copies of a slab go out from separate lanes)
-      const uint32_t wplane = static_cast<uint32_t>(L.taps * kTapBytes);
-      if (lane == 0) {
+      if (lane == 0) {  // resident weights (bf16x3: one stacked [tap][group][hi 64 | lo 64][8] buffer)
         mbar_expect_tx(wbar, L.w_bytes);
-        bulk_g2s(smem_u32(wsm), p.w_hi, wplane, wbar);
-        if (X3) bulk_g2s(smem_u32(wsm + wplane), p.w_lo, wplane, wbar);
+        bulk_g2s(smem_u32(wsm), p.w_hi, L.w_bytes, wbar);
       }
       const int pl = lane >> 1, grp = lane & 1;  // lane's copy: plane, channel group
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
         const int n = t / p.tiles_per_img;
-        const int m0 = (t - n * p.tiles_per_img) * kBM;
+        const int m0 = (t - n * p.tiles_per_img) * (p.hpool ? p.Wx : kBM);  // hpool: one output row per tile
         const int len = npix < HWx - m0 ? npix : HWx - m0;
         mbar_wait(empty0 + 8 * stage, phase ^ 1);
         const uint32_t fb = full0 + 8 * stage;
@@ -138,8 +142,8 @@ __global__ void __launch_bounds__(320, 1) tc_stem_kernel(const __grid_constant__
     if (lane == 0) {
       // ------------------------------------------------ MMA issuer
       constexpr uint32_t idesc = umma_idesc_bf16(kBM, kCout);
+      constexpr uint32_t idesc2 = umma_idesc_bf16(kBM, 2 * kCout);  // stacked [B_hi; B_lo]
       mbar_wait(wbar, 0);
-      const uint32_t wplane = static_cast<uint32_t>(L.taps * kTapBytes);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -148,24 +152,31 @@ __global__ void __launch_bounds__(320, 1) tc_stem_kernel(const __grid_constant__
         mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1);
         mbar_wait(full0 + 8 * stage, phase);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * kCout;
+        const uint32_t d_tmem = tmem_base + acc * kAccCols;
         const uint32_t a0 = smem_u32(slabs + stage * L.stage_bytes);
         const uint32_t b0 = smem_u32(wsm);
         // descriptors built once per tile; a tap moves the start address field
         // (bits 0-13, 16-byte units) by its row shift / weight offset
         const uint64_t da_hi = desc_kmajor_none(a0, L.group_bytes);
         const uint64_t da_lo = desc_kmajor_none(a0 + L.plane_bytes, L.group_bytes);
-        const uint64_t db_hi = desc_kmajor_none(b0, kCout * 16);
-        const uint64_t db_lo = desc_kmajor_none(b0 + wplane, kCout * 16);
+        // bf16x3 weights per tap: [group][hi 64 rows | lo 64 rows][8] (LBO =
+        // 2 KB between the channel groups): hi*[W_hi; W_lo] is ONE N = 128 MMA
+        // into [cols 0, 64) | [64, 128), then lo*W_hi (the first 64 rows) into
+        // the low half — 2 MMAs per tap instead of 3; the epilogue adds the halves
+        const uint64_t db = desc_kmajor_none(b0, (X3 ? 2 : 1) * kCout * 16);
+        constexpr uint64_t kTapStep = (X3 ? 2 : 1) * kTapBytes / 16;
         uint32_t accum = 0;
         uint64_t bo = 0;
-        for (int r = 0; r < p.kk; ++r) {
+#pragma unroll
+        for (int r = 0; r < (KK > 0 ? KK : kk); ++r) {
           uint64_t ao = static_cast<uint64_t>(r * p.Wx);
-          for (int s = 0; s < p.kk; ++s, ++ao, bo += kTapBytes / 16) {
-            umma_bf16(d_tmem, da_hi + ao, db_hi + bo, idesc, accum);
+#pragma unroll
+          for (int s = 0; s < (KK > 0 ? KK : kk); ++s, ++ao, bo += kTapStep) {
             if (X3) {
-              umma_bf16(d_tmem, da_hi + ao, db_lo + bo, idesc, 1u);
-              umma_bf16(d_tmem, da_lo + ao, db_hi + bo, idesc, 1u);
+              umma_bf16(d_tmem, da_hi + ao, db + bo, idesc2, accum);
+              umma_bf16(d_tmem, da_lo + ao, db + bo, idesc, 1u);
+            } else {
+              umma_bf16(d_tmem, da_hi + ao, db + bo, idesc, accum);
             }
             accum = 1u;
           }
@@ -191,21 +202,91 @@ __global__ void __launch_bounds__(320, 1) tc_stem_kernel(const __grid_constant__
     const int HoWx = p.Ho * p.Wx;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       const int n = t / p.tiles_per_img;
-      const int m = (t - n * p.tiles_per_img) * kBM + row;
-      const int oh = m / p.Wx, ow = m - (m / p.Wx) * p.Wx;
+      const int m = (t - n * p.tiles_per_img) * (p.hpool ? p.Wx : kBM) + row;
+      const int oh = p.hpool ? t - n * p.tiles_per_img : m / p.Wx;
+      const int ow = p.hpool ? row : m - (m / p.Wx) * p.Wx;
       const bool valid = m < HoWx && ow < p.Wo;
       mbar_wait(tfull0 + 8 * acc, acc_phase);
       tc_fence_after();
-      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * kCout;
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * kAccCols;
       float v[2][16];
 #pragma unroll
       for (int c = 0; c < 2; ++c) tmem_ld16_nowait(t_row + q * 32 + c * 16, v[c]);
-      tmem_ld_wait();
+      if (X3) {  // + the hi*lo half
+        float w[2][16];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) tmem_ld16_nowait(t_row + kCout + q * 32 + c * 16, w[c]);
+        tmem_ld_wait();
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int e = 0; e < 16; ++e) v[c][e] += w[c][e];
+      } else {
+        tmem_ld_wait();
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty0 + 8 * acc);
+      const int acc_used = acc;
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
+      if (p.hpool) {
+        // folded BN shift + ReLU in fp32; anchors past the row are -inf for the max
+        float a[32];
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            float z = v[u][e] + shift_s[q * 32 + u * 16 + e];
+            if (p.relu) z = z > 0.0f ? z : 0.0f;
+            a[u * 16 + e] = valid ? z : -FLT_MAX;
+          }
+        // left neighbour (ow - 1): the lane below, or lane 31 of the previous
+        // quad's warp through shared memory (double-buffered by accumulator)
+        float* xch = reinterpret_cast<float*>(epi) + ((acc_used * 2 + q) * 4) * 32;  // [quad][32 channels]
+        if (lane == 31)
+#pragma unroll
+          for (int c = 0; c < 32; c += 4)
+            *reinterpret_cast<float4*>(xch + quad * 32 + c) = make_float4(a[c], a[c + 1], a[c + 2], a[c + 3]);
+        asm volatile("bar.sync %0, 128;" ::"r"(2 + q) : "memory");  // the four quads of this column half
+        // lane 0's left neighbours: lane 31 of the previous row block (quad - 1)
+        const float* lxch = xch + ((quad + 3) & 3) * 32;
+        const bool even = (ow & 1) == 0 && ow < p.Wo;
+        uint4 hi[4], lo[4];
+        __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(hi);
+        __nv_bfloat162* l2 = reinterpret_cast<__nv_bfloat162*>(lo);
+#pragma unroll
+        for (int c = 0; c < 32; c += 2) {
+          float mx[2];
+#pragma unroll
+          for (int d = 0; d < 2; ++d) {
+            float left = __shfl_up_sync(0xffffffffu, a[c + d], 1);
+            if (lane == 0) left = quad == 0 ? -FLT_MAX : lxch[c + d];
+            const float right = __shfl_down_sync(0xffffffffu, a[c + d], 1);  // even lanes: always in-warp
+            // first maximum in (ow - 1, ow, ow + 1) order
+            float m = left;
+            if (a[c + d] > m) m = a[c + d];
+            if (right > m) m = right;
+            mx[d] = m;
+          }
+          const __nv_bfloat162 hh = __floats2bfloat162_rn(mx[0], mx[1]);
+          h2[c / 2] = hh;
+          const float2 hf = __bfloat1622float2(hh);
+          l2[c / 2] = __floats2bfloat162_rn(mx[0] - hf.x, mx[1] - hf.y);
+        }
+        if (even && m < HoWx) {
+          const size_t ob = ((static_cast<size_t>(n) * p.Ho + oh) * p.Wp + (ow >> 1)) * kCout + q * 32;
+          uint4* oh4 = reinterpret_cast<uint4*>(p.out_hi + ob);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) oh4[i] = hi[i];
+          if (X3 && p.out_lo) {
+            uint4* ol4 = reinterpret_cast<uint4*>(p.out_lo + ob);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) ol4[i] = lo[i];
+          }
+        }
+        continue;
+      }
       // staged, coalesced stores: 32 rows x 32 channels per step, 8 rows x 64 B per instruction
       const unsigned long long off = valid ? ((static_cast<unsigned long long>(n) * p.Ho + oh) * p.Wo + ow) * kCout : 0ull;
       const uint32_t wst = smem_u32(epi + (warp - 2) * 4096);
@@ -256,7 +337,7 @@ __global__ void __launch_bounds__(320, 1) tc_stem_kernel(const __grid_constant__
   __syncthreads();
   if (warp == 0) {
     __syncwarp();
-    tmem_dealloc(tmem_base, 2 * kCout);
+    tmem_dealloc(tmem_base, 2 * kAccCols);
   }
 }
 
@@ -306,7 +387,71 @@ __global__ void stem_s2d_kernel(const float* x, const int* count, int C, int H, 
   }
 }
 
+// Vertical 3-row max (stride 2, pad 1) over the hpool stem output, one thread
+// per (image, pooled pixel, 8 channels), 16-byte loads; hi and lo move together.
+__global__ void stem_vpool_kernel(const __nv_bfloat16* in_hi, const __nv_bfloat16* in_lo, int Hi, int Wp, int C,
+                                  int Hp, const int* ids, const int* count, __nv_bfloat16* out_hi,
+                                  __nv_bfloat16* out_lo) {
+  pdl_wait();
+  pdl_trigger();
+  const int j = blockIdx.x;
+  if (j >= *count) return;
+  const long long n = ids ? ids[j] : j;
+  const int c8n = C / 8;
+  const long long per = static_cast<long long>(Hp) * Wp * c8n;
+  for (long long i = blockIdx.y * blockDim.x + threadIdx.x; i < per; i += gridDim.y * blockDim.x) {
+    const int c8 = static_cast<int>(i % c8n);
+    const long long pix = i / c8n;
+    const int pj = static_cast<int>(pix % Wp), pi = static_cast<int>(pix / Wp);
+    uint4 vh[3], vl[3];
+    bool ok[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const int ir = 2 * pi - 1 + r;
+      ok[r] = ir >= 0 && ir < Hi;
+      const long long src = ((n * Hi + (ok[r] ? ir : 0)) * Wp + pj) * C + c8 * 8;
+      vh[r] = ok[r] ? __ldg(reinterpret_cast<const uint4*>(in_hi + src)) : make_uint4(0, 0, 0, 0);
+      vl[r] = ok[r] && in_lo ? __ldg(reinterpret_cast<const uint4*>(in_lo + src)) : make_uint4(0, 0, 0, 0);
+    }
+    float best[8];
+    uint4 bh = make_uint4(0, 0, 0, 0), bl = make_uint4(0, 0, 0, 0);
+    __nv_bfloat16* bh8 = reinterpret_cast<__nv_bfloat16*>(&bh);
+    __nv_bfloat16* bl8 = reinterpret_cast<__nv_bfloat16*>(&bl);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) best[e] = -FLT_MAX;
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      if (!ok[r]) continue;
+      const __nv_bfloat16* h8 = reinterpret_cast<const __nv_bfloat16*>(&vh[r]);
+      const __nv_bfloat16* l8 = reinterpret_cast<const __nv_bfloat16*>(&vl[r]);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float v = __bfloat162float(h8[e]) + __bfloat162float(l8[e]);
+        if (v > best[e]) {
+          best[e] = v;
+          bh8[e] = h8[e];
+          bl8[e] = l8[e];
+        }
+      }
+    }
+    const long long dst = ((n * Hp + pi) * Wp + pj) * C + c8 * 8;
+    *reinterpret_cast<uint4*>(out_hi + dst) = bh;
+    if (out_lo) *reinterpret_cast<uint4*>(out_lo + dst) = bl;
+  }
+}
+
 }  // namespace
+
+void launch_stem_vpool(const __nv_bfloat16* in_hi, const __nv_bfloat16* in_lo, int Hi, int Wp, int C, int Hp,
+                       const int* ids, const int* count, int max_rows, __nv_bfloat16* out_hi, __nv_bfloat16* out_lo,
+                       cudaStream_t s) {
+  if (max_rows <= 0) return;
+  const long long per = static_cast<long long>(Hp) * Wp * (C / 8);
+  int gy = static_cast<int>((per + 255) / 256);
+  if (gy > 128) gy = 128;
+  launch_pdl(stem_vpool_kernel, dim3(max_rows, gy), dim3(256), 0, s, in_hi, in_lo, Hi, Wp, C, Hp, ids, count, out_hi,
+             out_lo);
+}
 
 StemGeom stem_geom(int H, int W, int k, int stride, int pad) {
   StemGeom g;
@@ -359,24 +504,21 @@ void launch_stem_s2d(const float* x, const int* count, int max_n, int C, int H, 
 
 cudaError_t tc_stem_launch(const StemParams& p, int num_sms, cudaStream_t stream) {
   const bool x3 = p.x_lo != nullptr;
+  if (p.hpool && (p.Wx > kBM || p.tiles_per_img != p.Ho || p.Wp != (p.Wo - 1) / 2 + 1)) return cudaErrorInvalidValue;
   const StemSmem L = stem_smem(x3 ? 1 : 0, p.kk, p.Wx);
   if (L.stages < 2) return cudaErrorInvalidValue;
   const size_t smem = L.w_bytes + static_cast<size_t>(L.stages) * L.stage_bytes + 8 * 4096 + 256 + 256 + 1024;
   const long long tiles = static_cast<long long>(p.count_static) * p.tiles_per_img;
   if (tiles <= 0) return cudaSuccess;
   const int grid = tiles < num_sms ? static_cast<int>(tiles) : num_sms;
-  if (x3) {
-    cudaError_t e = cudaFuncSetAttribute(tc_stem_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+  auto go = [&](auto kern) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    launch_pdl(tc_stem_kernel<true>, dim3(grid), dim3(320), smem, stream, p);
-  } else {
-    cudaError_t e = cudaFuncSetAttribute(tc_stem_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    launch_pdl(tc_stem_kernel<false>, dim3(grid), dim3(320), smem, stream, p);
-  }
-  return cudaGetLastError();
+    launch_pdl(kern, dim3(grid), dim3(320), smem, stream, p);
+    return cudaGetLastError();
+  };
+  if (x3) return p.kk == 4 ? go(tc_stem_kernel<true, 4>) : p.kk == 3 ? go(tc_stem_kernel<true, 3>) : go(tc_stem_kernel<true, 0>);
+  return p.kk == 4 ? go(tc_stem_kernel<false, 4>) : p.kk == 3 ? go(tc_stem_kernel<false, 3>) : go(tc_stem_kernel<false, 0>);
 }
 
 }  // namespace lcb

@@ -23,8 +23,8 @@ namespace lcb {
 struct StemParams {
   const __nv_bfloat16* x_hi;  // [N][2][Hx*Wx][8]
   const __nv_bfloat16* x_lo;  // nullable (bf16 tier)
-  const __nv_bfloat16* w_hi;  // [taps][2][64][8]
-  const __nv_bfloat16* w_lo;  // nullable
+  const __nv_bfloat16* w_hi;  // bf16: [taps][2][64][8]; bf16x3: stacked [taps][2][hi 64 | lo 64][8]
+  const __nv_bfloat16* w_lo;  // unused (kept for the ABI of the parameter block)
   int Hx, Wx, Ho, Wo;
   int kk;                     // k' (taps per dimension over X)
   int tiles_per_img;          // ceil(Ho * Wx / 128)
@@ -33,9 +33,23 @@ struct StemParams {
   const float* scale;         // unused (BN scale is folded into the weights)
   const float* shift;         // [64]
   int relu;
-  __nv_bfloat16* out_hi;      // NHWC [N][Ho][Wo][64]
+  __nv_bfloat16* out_hi;      // NHWC [N][Ho][Wo][64] (hpool: [N][Ho][Wp][64])
   __nv_bfloat16* out_lo;      // nullable
+  // hpool = 1: the ResNet stem's 3x3/s2/p1 max-pool, horizontal half, fused
+  // into the epilogue: one output row per tile (tiles_per_img = Ho, Wx <= 128),
+  // out[n][oh][j] = max over ow in {2j-1, 2j, 2j+1} of the stem output (the
+  // vertical half is launch_stem_vpool). The full-resolution stem output never
+  // reaches HBM.
+  int hpool;
+  int Wp;                     // pooled width (Wo - 1) / 2 + 1
 };
+
+// Vertical half of the 3x3/s2/p1 max-pool over the hpool stem output:
+// out[n][i][j] = max over r in {2i-1, 2i, 2i+1} of in[n][r][j] (per channel the
+// first maximum in r order; hi and lo move together), surviving images ids.
+void launch_stem_vpool(const __nv_bfloat16* in_hi, const __nv_bfloat16* in_lo, int Hi, int Wp, int C, int Hp,
+                       const int* ids, const int* count, int max_rows, __nv_bfloat16* out_hi, __nv_bfloat16* out_lo,
+                       cudaStream_t s);
 
 // X geometry for a stem of kernel k, stride s (1 or 2), padding pad over H x W.
 struct StemGeom {
