@@ -1409,7 +1409,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
                                          p.shift ? (LCB_SMEM_SHIFT ? shs + (co - x.tn * BN) : p.shift + co) : nullptr,
                                          r ? rh : nullptr,
                         (r && X3 && p.res_lo) ? rl : nullptr);
-          if (!valid) {
+          if (!valid && p.gap_out) {  // (stores skip invalid rows; the GAP partials need zeros there)
 #pragma unroll
             for (int i = 0; i < 16; ++i) v[u][i] = 0.0f;
           }
