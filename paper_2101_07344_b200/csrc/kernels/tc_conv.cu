@@ -1111,9 +1111,13 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
         const CUtensorMap* mapR = consec ? p.tmRm : p.tmR;
         const int nbox = consec ? 1 : ipt;
         // this lane's task in every stage: plane pl, box j (j == nbox: the B box)
+        // (tiles of tiny images, up to 16 per tile with scattered ids, have up to
+        // 34 tasks: lanes take tasks lane and lane + 32)
         const int ntask = Cfg::kPlanes * (nbox + 1);
         const int pl = lane / (nbox + 1), jb = lane % (nbox + 1);
         const int img_j = __shfl_sync(0xffffffffu, my_img, jb < nbox ? jb : 0);
+        const int pl2 = (lane + 32) / (nbox + 1), jb2 = (lane + 32) % (nbox + 1);
+        const int img_j2 = __shfl_sync(0xffffffffu, my_img, jb2 < nbox && jb2 < 32 ? jb2 : 0);
         const int nk_conv = p.ntaps * cchunks;
         // residual K-step j: A box coordinates (channel, w, h) and B box (k, n)
         const int rs = p.res_stride > 0 ? p.res_stride : 1;
@@ -1129,45 +1133,31 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
           const uint32_t fb = full0 + 8 * stage;
           if (lane == 0) mbar_expect_tx(fb, dbg_noload ? 0u : static_cast<uint32_t>(Cfg::kStageBytes));
           __syncwarp();
-          if (!dbg_noload && ntask > 32 && lane == 0) {
-            // tiny images (> 15 per tile) with scattered ids: one lane walks all boxes
-            for (int q = 0; q < Cfg::kPlanes; ++q) {
-              const uint32_t a0 = smem_u32(stage_a(stage, q));
-              for (int j = 0; j < nbox; ++j) {
-                int idx = x.grp * ipt + j;
-                if (idx >= g.count) idx = g.count - 1;
-                const int im = image_of(p, idx);
-                if (s >= nk_conv)
-                  tma_load_5d(a0 + j * box_bytes, &mapR[q], fb, rc0 + (s - nk_conv) * 64, rw, rh, im, 0);
-                else
-                  tma_load_5d(a0 + j * box_bytes, &mapA[q], fb, cc * 64, x.w0 * cs + p.tap_dw[tap],
-                              x.h0 * cs + p.tap_dh[tap], im, p.tap_phase[tap]);
-              }
-              if (s >= nk_conv)
-                tma_load_2d(smem_u32(stage_b(stage, q)), &mapE[p.res_proj ? q : 0], fb, (s - nk_conv) * 64, en);
-              else
-                tma_load_2d(smem_u32(stage_b(stage, q)), &p.tmB[q], fb, tap * p.C + cc * 64, x.tn * BN);
-            }
-          } else if (!dbg_noload && ntask <= 32 && lane < ntask) {
-            const uint32_t a_dst = smem_u32(stage_a(stage, pl)) + jb * box_bytes;
+          // task (plane plx, box jbx of image imgx; jbx == nbox: the B box)
+          auto issue = [&](int plx, int jbx, int imgx) {
+            const uint32_t a_dst = smem_u32(stage_a(stage, plx)) + jbx * box_bytes;
             if (s >= nk_conv) {
               // residual K-step: A = residual channels [tn*BN + j*64, +64) at the
               // output pixels, B = identity slice (the residual add on the tensor
               // core); fused projection: A = block-input channels [j*64, +64) at
               // stride res_stride, B = projection weights [tn*BN, +BN) x [j*64, +64)
               const int j = s - nk_conv;
-              if (jb < nbox)
-                tma_load_5d(a_dst, &mapR[pl], fb, rc0 + j * 64, rw, rh, img_j, 0);
+              if (jbx < nbox)
+                tma_load_5d(a_dst, &mapR[plx], fb, rc0 + j * 64, rw, rh, imgx, 0);
               else
-                tma_load_2d(smem_u32(stage_b(stage, pl)), &mapE[p.res_proj ? pl : 0], fb, j * 64, en);
+                tma_load_2d(smem_u32(stage_b(stage, plx)), &mapE[p.res_proj ? plx : 0], fb, j * 64, en);
             } else {
-              if (jb < nbox) {
+              if (jbx < nbox) {
                 const int wc = x.w0 * cs + p.tap_dw[tap], hc = x.h0 * cs + p.tap_dh[tap], ph = p.tap_phase[tap];
-                tma_load_5d(a_dst, &mapA[pl], fb, cc * 64, wc, hc, img_j, ph);
+                tma_load_5d(a_dst, &mapA[plx], fb, cc * 64, wc, hc, imgx, ph);
               } else {
-                tma_load_2d(smem_u32(stage_b(stage, pl)), &p.tmB[pl], fb, tap * p.C + cc * 64, x.tn * BN);
+                tma_load_2d(smem_u32(stage_b(stage, plx)), &p.tmB[plx], fb, tap * p.C + cc * 64, x.tn * BN);
               }
             }
+          };
+          if (!dbg_noload) {
+            if (lane < ntask) issue(pl, jb, img_j);
+            if (lane + 32 < ntask) issue(pl2, jb2, img_j2);
           }
           if (++cc == cchunks) {
             cc = 0;
