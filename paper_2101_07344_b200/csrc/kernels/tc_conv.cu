@@ -1133,31 +1133,44 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
           const uint32_t fb = full0 + 8 * stage;
           if (lane == 0) mbar_expect_tx(fb, dbg_noload ? 0u : static_cast<uint32_t>(Cfg::kStageBytes));
           __syncwarp();
-          // task (plane plx, box jbx of image imgx; jbx == nbox: the B box)
-          auto issue = [&](int plx, int jbx, int imgx) {
-            const uint32_t a_dst = smem_u32(stage_a(stage, plx)) + jbx * box_bytes;
+          if (!dbg_noload && ntask <= 32 && lane < ntask) {
+            const uint32_t a_dst = smem_u32(stage_a(stage, pl)) + jb * box_bytes;
             if (s >= nk_conv) {
               // residual K-step: A = residual channels [tn*BN + j*64, +64) at the
               // output pixels, B = identity slice (the residual add on the tensor
               // core); fused projection: A = block-input channels [j*64, +64) at
               // stride res_stride, B = projection weights [tn*BN, +BN) x [j*64, +64)
               const int j = s - nk_conv;
-              if (jbx < nbox)
-                tma_load_5d(a_dst, &mapR[plx], fb, rc0 + j * 64, rw, rh, imgx, 0);
+              if (jb < nbox)
+                tma_load_5d(a_dst, &mapR[pl], fb, rc0 + j * 64, rw, rh, img_j, 0);
               else
-                tma_load_2d(smem_u32(stage_b(stage, plx)), &mapE[p.res_proj ? plx : 0], fb, j * 64, en);
+                tma_load_2d(smem_u32(stage_b(stage, pl)), &mapE[p.res_proj ? pl : 0], fb, j * 64, en);
             } else {
-              if (jbx < nbox) {
+              if (jb < nbox) {
                 const int wc = x.w0 * cs + p.tap_dw[tap], hc = x.h0 * cs + p.tap_dh[tap], ph = p.tap_phase[tap];
-                tma_load_5d(a_dst, &mapA[plx], fb, cc * 64, wc, hc, imgx, ph);
+                tma_load_5d(a_dst, &mapA[pl], fb, cc * 64, wc, hc, img_j, ph);
+              } else {
+                tma_load_2d(smem_u32(stage_b(stage, pl)), &p.tmB[pl], fb, tap * p.C + cc * 64, x.tn * BN);
+              }
+            }
+          } else if (!dbg_noload && ntask > 32) {
+            // tiny images (> 15 per tile) with scattered ids: tasks lane and lane + 32
+            for (int tk = lane; tk < ntask; tk += 32) {
+              const int plx = tk < 32 ? pl : pl2, jbx = tk < 32 ? jb : jb2, imgx = tk < 32 ? img_j : img_j2;
+              const uint32_t a_dst = smem_u32(stage_a(stage, plx)) + jbx * box_bytes;
+              if (s >= nk_conv) {
+                const int j = s - nk_conv;
+                if (jbx < nbox)
+                  tma_load_5d(a_dst, &mapR[plx], fb, rc0 + j * 64, rw, rh, imgx, 0);
+                else
+                  tma_load_2d(smem_u32(stage_b(stage, plx)), &mapE[p.res_proj ? plx : 0], fb, j * 64, en);
+              } else if (jbx < nbox) {
+                tma_load_5d(a_dst, &mapA[plx], fb, cc * 64, x.w0 * cs + p.tap_dw[tap], x.h0 * cs + p.tap_dh[tap], imgx,
+                            p.tap_phase[tap]);
               } else {
                 tma_load_2d(smem_u32(stage_b(stage, plx)), &p.tmB[plx], fb, tap * p.C + cc * 64, x.tn * BN);
               }
             }
-          };
-          if (!dbg_noload) {
-            if (lane < ntask) issue(pl, jb, img_j);
-            if (lane + 32 < ntask) issue(pl2, jb2, img_j2);
           }
           if (++cc == cchunks) {
             cc = 0;

@@ -3,7 +3,7 @@
 // Warp roles (320 threads, one persistent CTA per SM):
 //   warp 0     : producer (lane 0): resident weights once, then one X slab per
 //                tile (bulk copies, 2 groups x planes) into a ring of stages
-//   warp 1     : MMA issuer (lane 0): k'^2 taps x {1, 3} MMAs (M128 N64 K16)
+//   warp 1     : MMA issuer (whole warp, elect.sync): k'^2 taps x {1, 2} MMAs (M128, N 64 / stacked 128, K16)
 //   warps 2..9 : epilogue (TMEM lane quadrant warp % 4, column half (warp-2)/4): folded BN, ReLU,
 //                hi/lo split, NHWC store of the valid anchors
 #include <cfloat>
@@ -139,7 +139,8 @@ __global__ void __launch_bounds__(320, 1) tc_stem_kernel(const __grid_constant__
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // whole warp, warp-uniform operands, elect.sync issues (a single-lane
+       // loop capped the issue rate near one MMA per 130 cycles, sm100_prims.cuh)
       // ------------------------------------------------ MMA issuer
       constexpr uint32_t idesc = umma_idesc_bf16(kBM, kCout);
       constexpr uint32_t idesc2 = umma_idesc_bf16(kBM, 2 * kCout);  // stacked [B_hi; B_lo]
@@ -173,16 +174,16 @@ __global__ void __launch_bounds__(320, 1) tc_stem_kernel(const __grid_constant__
 #pragma unroll
           for (int s = 0; s < (KK > 0 ? KK : kk); ++s, ++ao, bo += kTapStep) {
             if (X3) {
-              umma_bf16(d_tmem, da_hi + ao, db + bo, idesc2, accum);
-              umma_bf16(d_tmem, da_lo + ao, db + bo, idesc, 1u);
+              umma_bf16_warp(d_tmem, da_hi + ao, db + bo, idesc2, accum);
+              umma_bf16_warp(d_tmem, da_lo + ao, db + bo, idesc, 1u);
             } else {
-              umma_bf16(d_tmem, da_hi + ao, db + bo, idesc, accum);
+              umma_bf16_warp(d_tmem, da_hi + ao, db + bo, idesc, accum);
             }
             accum = 1u;
           }
         }
-        umma_commit(empty0 + 8 * stage);
-        umma_commit(tfull0 + 8 * acc);
+        umma_commit_warp(empty0 + 8 * stage);
+        umma_commit_warp(tfull0 + 8 * acc);
         if (++stage == S) {
           stage = 0;
           phase ^= 1;

@@ -18,7 +18,7 @@ from bench import CONFIGS, build_deployment  # noqa: E402
 cfg = sys.argv[1] if len(sys.argv) > 1 else "resnet18_cifar"
 prec = sys.argv[2] if len(sys.argv) > 2 else "bf16x3"
 shadow = len(sys.argv) > 3 and sys.argv[3] == "shadow"
-B = CONFIGS[cfg][3]
+B = int(os.environ.get("LCB_PROFILE_BATCH", CONFIGS[cfg][3]))
 m, vs, dep, base, gen, _ = build_deployment(cfg, B, prec, 0)
 x = gen(B, 7).astype(np.float32)
 for _ in range(3):
