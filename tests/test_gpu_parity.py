@@ -291,12 +291,16 @@ def test_resnet18_cifar_serve_vs_oracle(shadow):
 
 
 @pytest.mark.parametrize("shadow", [True, False])
-def test_conv_head_opt_in_vs_oracle(shadow, monkeypatch):
-    """Opt-in variant (LCB_NO_CONV_HEAD=0): the tap conv's epilogue finishes
-    each row's lookup (GAP sum, head, selector, threshold) and the last head
-    runs the first-hit exit + compaction. Slower than the separate head launch
-    today (profiles/r02_fused_head_ab.txt) but kept correct."""
+@pytest.mark.parametrize("mode", ["post", "tile"])
+def test_conv_head_opt_in_vs_oracle(shadow, mode, monkeypatch):
+    """Opt-in variant (LCB_NO_CONV_HEAD=0): the tap conv finishes each row's
+    lookup (GAP sum, head, selector, threshold) — after a grid barrier that
+    follows its last tile (post) or from the CTA finishing the row's last tile
+    (tile) — and the last head runs the first-hit exit + compaction. Slower
+    than the separate head launch today (profiles/r02_fused_head_ab.txt) but
+    kept correct."""
     monkeypatch.setenv("LCB_NO_CONV_HEAD", "0")
+    monkeypatch.setenv("LCB_CONV_HEAD_TILE", "1" if mode == "tile" else "0")
     m, vs = _cnn_deployment("resnet18_cifar", 10, 21, 64)
     x = image_inputs(24, 3, 32, 32, seed=5)
     dep = lcb.Deployment(m, vs, precision="bf16x3", max_batch=32)
@@ -328,10 +332,16 @@ def test_fused_gap_matches_unfused_pool(monkeypatch):
     plain.close()
 
 
-def test_resnet50_serve_vs_oracle():
+@pytest.mark.parametrize("fusions", ["default", "unfused"])
+def test_resnet50_serve_vs_oracle(fusions, monkeypatch):
     """ImageNet shape (224x224, 1000 classes, 16 bottleneck blocks): stem,
     max-pool, 1x1/3x3/strided convs, fused GAP partials, split-K deep layers
-    and the batched 1000-class logits GEMM, against the fp64 restatement."""
+    and the 1000-class lookups, against the fp64 restatement. Both with the
+    graph-level fusions (downsample projection as residual K-steps, max-pool
+    halves in the stem epilogue) and with them off."""
+    if fusions == "unfused":
+        monkeypatch.setenv("LCB_NO_PROJ_FUSION", "1")
+        monkeypatch.setenv("LCB_NO_STEM_POOL", "1")
     m, vs = _cnn_deployment("resnet50", 1000, 31, 8, full_fraction=0.3)
     x = image_inputs(6, 3, 224, 224, seed=12)
     dep = lcb.Deployment(m, vs, precision="bf16x3", max_batch=8)
