@@ -664,14 +664,15 @@ __device__ __noinline__ void post_heads(const TcConvParams& p, int n, int etid, 
   float* w2s = scratch;                                   // [K][C]
   float* ws1s = w2s + K * C;                              // [16][K]
   float* fs = ws1s + 16 * 32 + static_cast<size_t>(ew) * C;  // [kEpiWarps][C]
-  const bool any = static_cast<int>(blockIdx.x) * kEpiWarps < n;
+  const bool any = static_cast<int>(blockIdx.x) < n;  // rows r with r % grid == this CTA
   if (any) {
     for (int i = etid; i < K * C / 4; i += kEpiThreads)
       reinterpret_cast<float4*>(w2s)[i] = __ldg(reinterpret_cast<const float4*>(p.gh.W2) + i);
     for (int i = etid; i < 16 * K; i += kEpiThreads) ws1s[i] = __ldg(p.gh.Ws1 + i);
   }
   epi_bar();
-  for (int r = blockIdx.x * kEpiWarps + ew; r < n; r += gridDim.x * kEpiWarps) row_head_warp(p, r, lane, fs, w2s, ws1s);
+  // rows spread over every CTA first (row r on CTA r % grid, warp r / grid)
+  for (int r = blockIdx.x + ew * gridDim.x; r < n; r += gridDim.x * kEpiWarps) row_head_warp(p, r, lane, fs, w2s, ws1s);
   epi_bar();  // this CTA's rows (hit/label/prob) before its arrival
   if (etid == 0) sint[63] = atom_add_acq_rel_gpu(p.gh.heads_done, 1) == static_cast<int>(gridDim.x) - 1 ? 1 : 0;
   epi_bar();
