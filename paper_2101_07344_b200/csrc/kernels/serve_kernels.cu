@@ -1444,11 +1444,10 @@ __global__ void maxpool_kernel(const __nv_bfloat16* hi, const __nv_bfloat16* lo,
   if (j >= *count) return;
   const long long n = ids[j];
   const int c8n = C / 8;
-  const long long per = static_cast<long long>(Ho) * Wo * c8n;
-  for (long long i = blockIdx.y * blockDim.x + threadIdx.x; i < per; i += gridDim.y * blockDim.x) {
-    const int c8 = static_cast<int>(i % c8n);
-    const long long pix = i / c8n;
-    const int ow = static_cast<int>(pix % Wo), oh = static_cast<int>(pix / Wo);
+  const int per = Ho * Wo * c8n;  // (32-bit index math per element)
+  for (int i = blockIdx.y * blockDim.x + threadIdx.x; i < per; i += gridDim.y * blockDim.x) {
+    const int pix = i / c8n, c8 = i - pix * c8n;
+    const int oh = pix / Wo, ow = pix - oh * Wo;
     float best[8];
     uint4 bh = make_uint4(0, 0, 0, 0), bl = make_uint4(0, 0, 0, 0);
 #pragma unroll

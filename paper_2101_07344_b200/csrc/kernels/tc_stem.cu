@@ -347,14 +347,15 @@ __global__ void stem_s2d_kernel(const float* x, const int* count, int C, int H, 
                                 int Wx, __nv_bfloat16* x_hi, __nv_bfloat16* x_lo) {
   pdl_wait();
   pdl_trigger();
-  const long long HWx = static_cast<long long>(Hx) * Wx;
-  const long long total = static_cast<long long>(*count) * 2 * HWx;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long pix = i % HWx;
-    const int grp = static_cast<int>((i / HWx) % 2);
-    const long long n = i / (2 * HWx);
-    const int I = static_cast<int>(pix / Wx), J = static_cast<int>(pix % Wx);
+  // 32-bit index math (the batch's X has < 2^31 units): 64-bit divisions per
+  // element made this kernel ALU-bound
+  const unsigned HWx = static_cast<unsigned>(Hx) * Wx;
+  const unsigned total = static_cast<unsigned>(*count) * 2u * HWx;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const unsigned ng = i / HWx, pix = i - ng * HWx;  // ng = n * 2 + grp
+    const int grp = static_cast<int>(ng & 1u);
+    const long long n = ng >> 1;
+    const int I = static_cast<int>(pix / static_cast<unsigned>(Wx)), J = static_cast<int>(pix - I * static_cast<unsigned>(Wx));
     const float* xn = x + n * C * H * W;
     float v[8];
 #pragma unroll
@@ -399,11 +400,10 @@ __global__ void stem_vpool_kernel(const __nv_bfloat16* in_hi, const __nv_bfloat1
   if (j >= *count) return;
   const long long n = ids ? ids[j] : j;
   const int c8n = C / 8;
-  const long long per = static_cast<long long>(Hp) * Wp * c8n;
-  for (long long i = blockIdx.y * blockDim.x + threadIdx.x; i < per; i += gridDim.y * blockDim.x) {
-    const int c8 = static_cast<int>(i % c8n);
-    const long long pix = i / c8n;
-    const int pj = static_cast<int>(pix % Wp), pi = static_cast<int>(pix / Wp);
+  const int per = Hp * Wp * c8n;  // (32-bit index math per element)
+  for (int i = blockIdx.y * blockDim.x + threadIdx.x; i < per; i += gridDim.y * blockDim.x) {
+    const int pix = i / c8n, c8 = i - pix * c8n;
+    const int pi = pix / Wp, pj = pix - pi * Wp;
     uint4 vh[3], vl[3];
     bool ok[3];
 #pragma unroll
