@@ -290,6 +290,38 @@ def test_resnet18_cifar_serve_vs_oracle(shadow):
     assert len(set(exit_o.tolist())) >= 3  # exits spread over several layers
 
 
+def test_ragged_batches_vs_oracle():
+    """One engine (max_batch 256) serving ragged batch sizes — 1, 7, 129 (one
+    past a 128-row tile), 256 (the maximum) — in compact and shadow mode
+    against the oracle; a request's decisions do not depend on the batch it
+    rides in (the captured graph is batch-size agnostic: every size lives in
+    device memory; only the split-K degree of the deep layers follows the
+    survivor count, so probabilities agree within the parity tolerance, not
+    bit for bit: measured ~1e-4 between a batch of 1 and of 256); sizes 0
+    and max_batch + 1 are rejected like the reference's invalid_argument."""
+    m, vs = _cnn_deployment("resnet18_cifar", 10, 21, 64)
+    dep = lcb.Deployment(m, vs, precision="bf16x3", max_batch=256)
+    deltas = {v.layer: v.delta for v in vs}
+    x = image_inputs(256, 3, 32, 32, seed=77)
+    exit_o, served_o, base_o, probs_o, gaps, _, _ = _oracle_cnn(m, vs, x, threads=os.cpu_count() or 8)
+    full = {sh: dep.serve(x, shadow=sh) for sh in (True, False)}
+    for B in (1, 7, 129, 256):
+        for shadow in (True, False):
+            res = dep.serve(x[:B], shadow=shadow)
+            compare_serve(res, exit_o[:B], served_o[:B], base_o[:B], probs_o[:B], deltas, shadow, label_gap=gaps[:B])
+            f = full[shadow]
+            ok = ~(in_band(probs_o[:B], exit_o[:B], deltas) | gaps[:B])
+            assert np.array_equal(res.exit_layer[ok], f.exit_layer[:B][ok])
+            assert np.array_equal(res.served[ok], f.served[:B][ok])
+            both = ~np.isnan(res.probs) & ~np.isnan(f.probs[:, :B])
+            assert np.array_equal(both, ~np.isnan(res.probs))
+            assert np.all(close_rel(res.probs[both], f.probs[:, :B][both]))
+    for bad in (0, 257):
+        with pytest.raises(ValueError):
+            dep.serve(np.zeros((bad, 3 * 32 * 32), np.float32), shadow=False)
+    dep.close()
+
+
 @pytest.mark.parametrize("shadow", [True, False])
 @pytest.mark.parametrize("mode", ["post", "tile"])
 def test_conv_head_opt_in_vs_oracle(shadow, mode, monkeypatch):
