@@ -227,6 +227,7 @@ Engine::Engine(int device, const BaseModel& model, std::vector<CacheVariant> var
   const char* nr = std::getenv("LCB_NO_MMA_RESIDUAL");
   mma_residual_ = !(nr && nr[0] == '1');
   if (const char* np = std::getenv("LCB_NO_PROJ_FUSION")) proj_fusion_ = !(np[0] == '1');
+  if (const char* ra = std::getenv("LCB_ORDERED_COMPACTION")) mlp_row_append_ = !(ra[0] == '1');
   if (const char* sp = std::getenv("LCB_NO_STEM_POOL")) stem_pool_ = !(sp[0] == '1');
   const char* nt = std::getenv("LCB_DIRECT_STORE");
   staged_store_ = !(nt && nt[0] == '1');
@@ -844,16 +845,27 @@ void Engine::build_mlp_steps(std::vector<Step>& steps, bool shadow, bool stamps)
       int* ids_out = ids + static_cast<size_t>(layer) * B;
       int* src_out = src + static_cast<size_t>(layer) * B;
       int* cnt_out = counts + layer;
-      const ExitParams ex = exit_params(layer, shadow, cur_ids, ids_out, src_out, cnt_out);
+      ExitParams ex = exit_params(layer, shadow, cur_ids, ids_out, src_out, cnt_out);
+      const bool row_append = !shadow && mlp_row_append_ && c.classes <= 32;
+      if (row_append) {
+        // each head CTA appends its kept row and copies the activations (no gather launch)
+        const Planes dst = mlp_cin_[static_cast<size_t>(b)];
+        ex.rows_src_hi = act.hi;
+        ex.rows_src_lo = act.lo;
+        ex.rows_dst_hi = dst.hi;
+        ex.rows_dst_lo = dst.lo;
+        ex.row_elems = f.outp;
+      }
       add_lookup_steps(steps, c, tap, B, false, false, &ex);
       if (stamps) add_stamp(steps, layer, 1);
       if (!shadow) {
         Planes dst = mlp_cin_[static_cast<size_t>(b)];
         const long long row_elems = f.outp;
-        steps.push_back({[act, dst, row_elems, src_out, cnt_out, B](cudaStream_t s) {
-                           launch_gather_rows(act.hi, act.lo, dst.hi, dst.lo, row_elems, src_out, cnt_out, B, s);
-                         },
-                         3});
+        if (!row_append)
+          steps.push_back({[act, dst, row_elems, src_out, cnt_out, B](cudaStream_t s) {
+                             launch_gather_rows(act.hi, act.lo, dst.hi, dst.lo, row_elems, src_out, cnt_out, B, s);
+                           },
+                           3});
         cur = dst;
       } else {
         cur = act;

@@ -228,6 +228,10 @@ class Engine {
   // conv whose only use is the residual of a later conv runs as that conv's
   // residual K-steps (TcConvParams::res_proj). By op index:
   bool proj_fusion_ = true;
+  // block-MLP compact mode: kept rows appended at atomic positions by their own
+  // head CTA, which also copies the activation row (LCB_ORDERED_COMPACTION=1:
+  // the last CTA's ordered scan + a gather launch)
+  bool mlp_row_append_ = true;
   // Stem + 3x3/s2 max-pool: the horizontal half of the pool rides the stem's
   // epilogue, the vertical half is a small kernel (LCB_NO_STEM_POOL=1 off).
   bool stem_pool_ = true;

@@ -783,6 +783,48 @@ __device__ void exit_tail(const ExitParams& e, int n, const float* prob, const i
   if (tid == 0) *e.count_out = base_s;
 }
 
+// First-hit exit of row r by its own CTA (serve_one, serving.cpp:112-121) with
+// atomic-position compaction of the row-compacted activations (ExitParams::
+// rows_dst_hi): a miss is appended to ids_out and its activation row copied.
+__device__ void row_exit_append(const ExitParams& e, int n, int r, const float* prob, const int* hit,
+                                const int* label) {
+  __shared__ int pos_s;
+  __syncthreads();  // the row's head results (written by thread 0)
+  if (r >= n) return;
+  if (threadIdx.x == 0) {
+    const int id = e.ids_in[r];
+    const bool h = hit[r] != 0;
+    const int lab = label[r];
+    if (e.probs_out) e.probs_out[id] = prob[r];
+    if (e.labels_out) e.labels_out[id] = lab;
+    int pos = -1;
+    if (h) {
+      if (e.exit_layer[id] == 0) {
+        e.exit_layer[id] = e.layer;
+        e.served[id] = lab;
+        e.exit_ns[id] = globaltimer();
+      }
+    } else {
+      pos = atomicAdd(e.count_out, 1);
+      e.ids_out[pos] = id;
+      if (e.src_rows_out) e.src_rows_out[pos] = r;
+    }
+    pos_s = pos;
+  }
+  __syncthreads();
+  const int pos = pos_s;
+  if (pos < 0) return;
+  const long long nv = e.row_elems / 8;  // 16-byte vectors per plane row
+  const uint4* sh = reinterpret_cast<const uint4*>(e.rows_src_hi + static_cast<long long>(r) * e.row_elems);
+  uint4* dh = reinterpret_cast<uint4*>(e.rows_dst_hi + static_cast<long long>(pos) * e.row_elems);
+  for (long long i = threadIdx.x; i < nv; i += blockDim.x) dh[i] = __ldg(sh + i);
+  if (e.rows_src_lo) {
+    const uint4* sl = reinterpret_cast<const uint4*>(e.rows_src_lo + static_cast<long long>(r) * e.row_elems);
+    uint4* dl = reinterpret_cast<uint4*>(e.rows_dst_lo + static_cast<long long>(pos) * e.row_elems);
+    for (long long i = threadIdx.x; i < nv; i += blockDim.x) dl[i] = __ldg(sl + i);
+  }
+}
+
 // ------------------------------------------------------------------ head
 // Reference lookup (cache.cpp:259-265): pr = softmax(pred(tap)),
 // p = sigmoid(sel(pr)), hit = p >= delta (inclusive); label = argmax(pr).
@@ -858,7 +900,12 @@ __global__ void __launch_bounds__(kLk) cache_head_kernel(CacheHeadParams p) {
     __syncthreads();
     head_block(p, r, logits, feat, hs, (stage_w || stage_s) ? ws1s : p.Ws1);
   }
-  if (p.ex.arrive) exit_tail(p.ex, n, p.prob, p.hit, p.label);
+  if (p.ex.arrive) {
+    if (p.ex.rows_dst_hi && !p.ex.shadow)
+      row_exit_append(p.ex, n, r, p.prob, p.hit, p.label);
+    else
+      exit_tail(p.ex, n, p.prob, p.hit, p.label);
+  }
 }
 
 // ------------------------------------------------------------ wide lookup
@@ -1514,6 +1561,8 @@ __global__ void init_batch_kernel(const int* batch, int max_batch, int* ids0, in
     *count0 = B;
     if (rows_out) *rows_out = B * rows_mult;
   }
+  // per-layer survivor counts start at zero (atomic row compaction appends to them)
+  if (blockIdx.x == 0 && threadIdx.x >= 1 && threadIdx.x <= L) count0[threadIdx.x] = 0;
 }
 
 __global__ void __launch_bounds__(256) confusion_kernel(const float* probs, const int* labels, const int* base_pred,

@@ -44,6 +44,16 @@ struct ExitParams {
   int* ids_out;
   int* src_rows_out;         // nullable
   int* count_out;
+  // Row-compacted activations (block-MLP compact mode): the row's own CTA
+  // appends a kept row at an atomic position of ids_out (count_out zeroed at
+  // batch start) and copies its activation row there — no last-CTA scan, no
+  // separate gather launch. The survivors' order then varies from run to run;
+  // no request's values do (the next layer's rows are independent).
+  const __nv_bfloat16* rows_src_hi;  // nullptr: ordered compaction by the last CTA (exit_tail)
+  const __nv_bfloat16* rows_src_lo;
+  __nv_bfloat16* rows_dst_hi;
+  __nv_bfloat16* rows_dst_lo;
+  long long row_elems;
 };
 
 // Per-row cache head inputs (one of three predictor families).
