@@ -228,6 +228,7 @@ Engine::Engine(int device, const BaseModel& model, std::vector<CacheVariant> var
   mma_residual_ = !(nr && nr[0] == '1');
   if (const char* np = std::getenv("LCB_NO_PROJ_FUSION")) proj_fusion_ = !(np[0] == '1');
   if (const char* ra = std::getenv("LCB_ORDERED_COMPACTION")) mlp_row_append_ = !(ra[0] == '1');
+  if (const char* pl = std::getenv("LCB_PREDICTOR_LAUNCH")) direct_rows_ = !(pl[0] == '1');
   if (const char* sp = std::getenv("LCB_NO_STEM_POOL")) stem_pool_ = !(sp[0] == '1');
   const char* nt = std::getenv("LCB_DIRECT_STORE");
   staged_store_ = !(nt && nt[0] == '1');
@@ -571,6 +572,10 @@ void Engine::add_lookup_steps(std::vector<Step>& steps, DevCache& c, const TapVi
   // Pool(C) with <= 32 classes: the head itself sums the conv's fused GAP partials.
   const bool head_gap = c.family == 1 && fused_gap && c.gap && fused_lookup_ &&
                         fused_lookup_supported(c.classes, c.width, max_rows);
+  // block-MLP taps (one contiguous row per request): the head reads the row and
+  // runs the Pool(w) / Conv(k,s) predictor layer itself (LCB_PREDICTOR_LAUNCH=1: separate launch)
+  const bool direct = direct_rows_ && tap.HW == 1 && !tap.data_idx && !fused_gap && (c.family == 1 || c.family == 2) &&
+                      c.D <= 8192;
   double head_bytes = 0.0;  // per surviving row, beyond the (L2-resident) head weights
   if (head_gap) {
     head_bytes = 4.0 * c.gap_segs * c.width;
@@ -616,11 +621,15 @@ void Engine::add_lookup_steps(std::vector<Step>& steps, DevCache& c, const TapVi
                                        cp->feats, s);
                      },
                      2, 1, cidx, 0.0, 4.0 * c.gap_segs * c.width + 4.0 * c.width});
+  } else if (c.family == 1 && direct) {
+    // the head pools its own row (direct row mode)
   } else if (c.family == 1) {
     steps.push_back({[cp, tap, max_rows](cudaStream_t s) {
                        launch_pool_bins(tap, max_rows, cp->win, cp->width, cp->feats, s);
                      },
                      2, 1, cidx, 0.0, tap_bytes + 4.0 * c.width});
+  } else if (c.family == 2 && direct) {
+    // the head runs the Conv(k,s) layer on its own row (direct row mode)
   } else if (c.family == 2) {
     steps.push_back({[cp, tap, max_rows](cudaStream_t s) {
                        launch_conv1d_partials(tap, max_rows, cp->D, cp->kernel, cp->stride, cp->out_dim, cp->w1,
@@ -679,8 +688,21 @@ void Engine::add_lookup_steps(std::vector<Step>& steps, DevCache& c, const TapVi
   const int rows_total = max_rows;
   const ExitParams exv = ex ? *ex : ExitParams{};
   const float gap_inv = head_gap ? static_cast<float>(1.0 / tap.HW) : 0.0f;
-  steps.push_back({[cp, tap, max_rows, rows_total, exv, head_gap, gap_inv](cudaStream_t s) {
+  steps.push_back({[cp, tap, max_rows, rows_total, exv, head_gap, gap_inv, direct](cudaStream_t s) {
                      CacheHeadParams p{};
+                     if (direct) {
+                       p.row_hi = tap.hi;
+                       p.row_lo = tap.lo;
+                       p.row_stride = tap.row_stride;
+                       p.D = static_cast<int>(cp->D);
+                       p.win = cp->win;
+                       p.pool_inv = static_cast<float>(1.0 / cp->win);
+                       p.kernel = cp->kernel;
+                       p.stride = cp->stride;
+                       p.out_dim = cp->out_dim;
+                       p.w1 = cp->w1;
+                       p.b1c = cp->b1c;
+                     }
                      p.family = cp->family;
                      p.classes = cp->classes;
                      p.feat = cp->family == 1 ? cp->width : (cp->family == 0 ? cp->h : cp->nchunks);
@@ -714,7 +736,11 @@ void Engine::add_lookup_steps(std::vector<Step>& steps, DevCache& c, const TapVi
                      p.ex = exv;
                      launch_cache_head(p, max_rows, s);
                    },
-                   2, (c.classes > 32 && c.family != 2) ? 2 : 1, cidx, 0.0, head_bytes});
+                   2, (c.classes > 32 && c.family != 2) ? 2 : 1, cidx,
+                   direct && c.family == 2 ? 2.0 * (static_cast<double>(c.out_dim) * c.kernel +
+                                                    static_cast<double>(c.out_dim) * c.classes)
+                                           : 0.0,
+                   direct ? tap_bytes : head_bytes});
 }
 
 ExitParams Engine::exit_params(int layer, bool shadow, const int* ids_in, int* ids_out, int* src_rows_out,

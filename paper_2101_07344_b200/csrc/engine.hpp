@@ -232,6 +232,7 @@ class Engine {
   // head CTA, which also copies the activation row (LCB_ORDERED_COMPACTION=1:
   // the last CTA's ordered scan + a gather launch)
   bool mlp_row_append_ = true;
+  bool direct_rows_ = true;  // block-MLP Pool / Conv caches computed inside the head (no predictor launch)
   // Stem + 3x3/s2 max-pool: the horizontal half of the pool rides the stem's
   // epilogue, the vertical half is a small kernel (LCB_NO_STEM_POOL=1 off).
   bool stem_pool_ = true;

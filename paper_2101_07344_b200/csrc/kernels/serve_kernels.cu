@@ -613,7 +613,7 @@ __host__ __device__ inline bool head_stages_weights(const CacheHeadParams& p) {
 __host__ __device__ inline bool head_stages_ws1(const CacheHeadParams& p) {
   // batch-sized launches only: with a handful of rows the copy is not hidden
   // behind the upstream kernel and the selector reads L2 directly anyway
-  return !head_stages_weights(p) && p.classes <= 1024 && p.rows_total >= 32;
+  return !head_stages_weights(p) && p.classes <= 1024 && p.rows_total >= 32 && !p.row_hi;
 }
 
 // Shared scratch of one row's head.
@@ -867,7 +867,39 @@ __global__ void __launch_bounds__(kLk) cache_head_kernel(CacheHeadParams p) {
   pdl_wait();
   pdl_trigger();
   const int n = *p.count;
-  if (r < n) {
+  if (r < n && p.row_hi) {
+    // direct row mode: x = the request's row; Pool(w) bins (AvgPool over flat
+    // windows times 1/w, network.cpp:130-138) or Conv(k,s) + ReLU
+    // (network.cpp:127-148) into feat, then the FC(.,C) logits
+    float* x = feat + (p.family == 2 ? p.out_dim : p.feat);  // [D]
+    const long long rb = static_cast<long long>(r) * p.row_stride;
+    for (int i = tid; i < p.D; i += kLk) {
+      float v = __bfloat162float(p.row_hi[rb + i]);
+      if (p.row_lo) v += __bfloat162float(p.row_lo[rb + i]);
+      x[i] = v;
+    }
+    __syncthreads();
+    int nf;
+    if (p.family == 1) {
+      nf = p.feat;
+      for (int o = tid; o < nf; o += kLk) {
+        float a = 0.0f;
+        for (int t = 0; t < p.win; ++t) a += x[o * p.win + t];
+        feat[o] = a * p.pool_inv;
+      }
+    } else {
+      nf = p.out_dim;
+      for (int o = tid; o < nf; o += kLk) {
+        float y = p.b1c;
+        for (int t = 0; t < p.kernel; ++t) y += __ldg(p.w1 + t) * x[o * p.stride + t];
+        feat[o] = y > 0.0f ? y : 0.0f;
+      }
+    }
+    __syncthreads();
+    block_logits(p.W2, p.b2, C, nf, feat, logits);
+    __syncthreads();
+    head_block(p, r, logits, feat, hs, p.Ws1);
+  } else if (r < n) {
     if (p.pre_logits) {
       for (int k = tid; k < C; k += kLk) logits[k] = fc_logit(p.pre_logits, p.pre_nz, p.pre_zstride, p.b2, r, C, k);
     } else if (p.family == 2) {
@@ -1695,7 +1727,11 @@ void launch_cache_head(const CacheHeadParams& p_in, int max_rows, cudaStream_t s
     p.pre_zstride = static_cast<long long>(max_rows) * p.classes;
     p.gap = nullptr;
   }
-  const int feat_len = (p.family == 2 || p.pre_logits) ? p.classes : (p.feat > p.classes ? p.feat : p.classes);
+  int feat_len = (p.family == 2 || p.pre_logits) ? p.classes : (p.feat > p.classes ? p.feat : p.classes);
+  if (p.row_hi) {  // direct row mode: [features][row]
+    const int nf = p.family == 2 ? p.out_dim : p.feat;
+    feat_len = (nf > p.classes ? nf : p.classes) + p.D;
+  }
   size_t smem = static_cast<size_t>(p.classes + feat_len) * sizeof(float);
   if (head_stages_weights(p)) smem += static_cast<size_t>(p.classes) * (p.feat + 16) * sizeof(float);  // W2 + Ws1
   else if (head_stages_ws1(p)) smem += static_cast<size_t>(p.classes) * 16 * sizeof(float);          // Ws1

@@ -93,6 +93,18 @@ struct CacheHeadParams {
   int pre_nz;
   long long pre_zstride;
   ExitParams ex;           // ex.arrive != nullptr: fused first-hit exit + compaction
+  // Direct row mode (block-MLP taps, one contiguous row per request): the head
+  // reads its row (hi + lo) and computes the Pool(w) bins or the Conv(k,s)
+  // layer itself — no separate predictor launch. row_hi == nullptr: off.
+  const __nv_bfloat16* row_hi;
+  const __nv_bfloat16* row_lo;
+  long long row_stride;
+  int D;                   // tap length
+  int win;                 // pool window (family 1)
+  float pool_inv;          // 1 / win
+  int kernel, stride, out_dim;  // conv (family 2)
+  const float* w1;         // conv kernel [kernel]
+  float b1c;               // conv bias
 };
 
 int rows_fc_splits(int feat);
