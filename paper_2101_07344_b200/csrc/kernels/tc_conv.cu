@@ -146,13 +146,7 @@ __device__ __forceinline__ Tile decode_tile(int t, const TcConvParams& p, const 
 
 __device__ __forceinline__ int image_of(const TcConvParams& p, int idx) { return p.surv ? p.surv[idx] : idx; }
 
-#ifndef LCB_SMEM_SHIFT
-#define LCB_SMEM_SHIFT 1
-#endif
-#ifndef LCB_EPI_UNROLL
-#define LCB_EPI_UNROLL 2
-#endif
-constexpr int kEpiUnroll = LCB_EPI_UNROLL;  // c32 steps of the epilogue loop unrolled together
+constexpr int kEpiUnroll = 2;  // 32-column epilogue steps unrolled together (BN = 128: r50 l1 64->256 227 -> 200 us)
 constexpr int kEpiWarps = 8;
 constexpr int kEpiThreads = kEpiWarps * 32;
 constexpr int kThreads = 64 + kEpiThreads;
@@ -239,7 +233,6 @@ __device__ __forceinline__ bool out_row(const TcConvParams& p, const TileGeom& g
 // scale/shift, residual (prefetched 16-byte chunks), ReLU, hi/lo split and
 // NHWC store of 16 channels.
 // sh: the 16 shift values of these columns (shared-memory copy or global), nullable.
-template <bool kShGlobal = false>
 __device__ __forceinline__ void epilogue_math(const TcConvParams& p, float (&v)[16], int co, const float* sh,
                                               const uint4* rh, const uint4* rl) {
   if (p.scale) {
@@ -257,7 +250,7 @@ __device__ __forceinline__ void epilogue_math(const TcConvParams& p, float (&v)[
     const float4* sh4 = reinterpret_cast<const float4*>(sh);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const float4 s4 = kShGlobal ? __ldg(sh4 + q) : sh4[q];  // global: L1-resident broadcast loads
+      const float4 s4 = sh4[q];
       v[4 * q] += s4.x;
       v[4 * q + 1] += s4.y;
       v[4 * q + 2] += s4.z;
@@ -1299,10 +1292,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
     // per-tile shift values live in shared memory, double-buffered with the
     // accumulators; the NEXT tile's values are loaded into registers while
     // this tile is processed (their L2 latency was a serial gap per tile)
-    // LCB_SMEM_SHIFT=0 (default): the epilogue reads shift values straight from
-    // global memory (L1 broadcast) and warps are not re-synchronised per tile,
-    // so their math and store phases interleave instead of bursting together
-    const bool use_shs = LCB_SMEM_SHIFT && p.shift && p.mode == 0;
+    // (reading them from global memory without the per-tile barrier measured slower)
+    const bool use_shs = p.shift && p.mode == 0;
     static_assert(BN <= kEpiThreads, "one shift value per epilogue thread");
     if (static_cast<int>(blockIdx.x) < g.total) {
       const Tile x0 = decode_tile(blockIdx.x, p, g);
@@ -1409,9 +1400,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
               rl[1] = reinterpret_cast<const uint4*>(p.res_lo + obase + co)[1];
             }
           }
-          epilogue_math<!LCB_SMEM_SHIFT>(p, v[u], co,
-                                         p.shift ? (LCB_SMEM_SHIFT ? shs + (co - x.tn * BN) : p.shift + co) : nullptr,
-                                         r ? rh : nullptr,
+          epilogue_math(p, v[u], co, p.shift ? shs + (co - x.tn * BN) : nullptr, r ? rh : nullptr,
                         (r && X3 && p.res_lo) ? rl : nullptr);
           if (!valid && p.gap_out) {  // (stores skip invalid rows; the GAP partials need zeros there)
 #pragma unroll
