@@ -221,6 +221,7 @@ Engine::Engine(int device, const BaseModel& model, std::vector<CacheVariant> var
   const char* ns = std::getenv("LCB_NO_STACKED");
   stacked_ = !(ns && ns[0] == '1');
   if (const char* km = std::getenv("LCB_KS_MIN_STEPS")) ks_min_steps_ = std::atoi(km);
+  if (const char* km = std::getenv("LCB_MLP_KS_MIN_STEPS")) mlp_ks_min_steps_ = std::atoi(km);
   if (const char* wp = std::getenv("LCB_NO_WPREFETCH")) wprefetch_ = !(wp[0] == '1');
   const char* nh = std::getenv("LCB_HALO");  // opt-in: not yet faster than the per-tap loads
   halo_ = nh && nh[0] == '1';
@@ -574,8 +575,9 @@ void Engine::add_lookup_steps(std::vector<Step>& steps, DevCache& c, const TapVi
                         fused_lookup_supported(c.classes, c.width, max_rows);
   // block-MLP taps (one contiguous row per request): the head reads the row and
   // runs the Pool(w) / Conv(k,s) predictor layer itself (LCB_PREDICTOR_LAUNCH=1: separate launch)
-  const bool direct = direct_rows_ && tap.HW == 1 && !tap.data_idx && !fused_gap && (c.family == 1 || c.family == 2) &&
-                      c.D <= 8192;
+  // (Pool(w) heads with > 32 classes take the batched logits GEMM over pooled features instead)
+  const bool direct = direct_rows_ && tap.HW == 1 && !tap.data_idx && !fused_gap &&
+                      ((c.family == 1 && c.classes <= 32) || c.family == 2) && c.D <= 8192;
   double head_bytes = 0.0;  // per surviving row, beyond the (L2-resident) head weights
   if (head_gap) {
     head_bytes = 4.0 * c.gap_segs * c.width;
@@ -839,6 +841,7 @@ void Engine::build_mlp_steps(std::vector<Step>& steps, bool shadow, bool stamps)
     prm->Cout = f.outp;
     prm->ksplit = 1;
     prm->ks_max = 32;
+    prm->ks_min_steps = mlp_ks_min_steps_;
     prm->ws = ws_;
     prm->ws_counters = ws_counters_;
     split_prms_.push_back(prm);

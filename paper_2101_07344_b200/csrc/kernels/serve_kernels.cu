@@ -603,12 +603,26 @@ __device__ void block_logits(const float* __restrict__ W, const float* __restric
   }
 }
 
-// Fused-GAP heads stage W2 + Ws1 in shared memory when they fit (48 KB).
-// Heads that do not stage W2 still stage the selector's first layer (16 x C)
-// before the wait when it fits (<= 64 KB): one L2 round trip off the tail.
+// Fused-GAP and direct-row heads stage W2 + Ws1 in shared memory when they
+// fit (48 KB). Heads that do not stage W2 still stage the selector's first
+// layer (16 x C) before the wait when it fits (<= 64 KB): one L2 round trip
+// off the tail.
 __host__ __device__ inline bool head_stages_ws1(const CacheHeadParams& p);
+// columns of W2 [classes][cols]: the Conv(k,s) head of a direct row reads its own conv outputs
+__host__ __device__ inline int head_w2_cols(const CacheHeadParams& p) {
+  return (p.row_hi && p.family == 2) ? p.out_dim : p.feat;
+}
 __host__ __device__ inline bool head_stages_weights(const CacheHeadParams& p) {
-  return p.gap != nullptr && p.classes * (p.feat + 16) <= 12288;
+  return (p.gap != nullptr || p.row_hi != nullptr) && !p.pre_logits && p.classes * (head_w2_cols(p) + 16) <= 12288;
+}
+// floats of the head's feature region (after the logits): direct rows hold
+// [features][row] there; launch_cache_head sizes the same extent
+__host__ __device__ inline int head_feat_len(const CacheHeadParams& p) {
+  if (p.row_hi) {
+    const int nf = head_w2_cols(p);
+    return (nf > p.classes ? nf : p.classes) + p.D;
+  }
+  return (p.family == 2 || p.pre_logits) ? p.classes : (p.feat > p.classes ? p.feat : p.classes);
 }
 __host__ __device__ inline bool head_stages_ws1(const CacheHeadParams& p) {
   // batch-sized launches only: with a handful of rows the copy is not hidden
@@ -635,7 +649,7 @@ struct HeadSmem {
 // one sweep, since sum_k Ws1[j][k] pr_k = (sum_k Ws1[j][k] e_k) / S. Two block
 // reductions instead of one per softmax/selector step.
 __device__ void head_block(const CacheHeadParams& p, int r, const float* logits, float* /*pr scratch*/, HeadSmem& hs,
-                           const float* ws1) {
+                           const float* ws1, const float* bs1, const float* ws2) {
   const int C = p.classes;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = kLk / 32;
   float bv = -FLT_MAX;
@@ -692,8 +706,8 @@ __device__ void head_block(const CacheHeadParams& p, int r, const float* logits,
     const float S = __shfl_sync(0xffffffffu, t, 16);
     float h = 0.0f;
     if (lane < 16) {
-      const float a = t / S + p.bs1[lane];
-      h = (a > 0.0f ? a : 0.0f) * p.ws2[lane];
+      const float a = t / S + bs1[lane];
+      h = (a > 0.0f ? a : 0.0f) * ws2[lane];
     }
     // z = bs2 + sum_j ws2[j] * relu(hidden_j), j ascending
     float hj[16];
@@ -786,8 +800,11 @@ __device__ void exit_tail(const ExitParams& e, int n, const float* prob, const i
 // First-hit exit of row r by its own CTA (serve_one, serving.cpp:112-121) with
 // atomic-position compaction of the row-compacted activations (ExitParams::
 // rows_dst_hi): a miss is appended to ids_out and its activation row copied.
+// held (nullable): the row's 16-byte vectors already in registers, thread t <
+// nv the hi plane's vector t, nv <= t < 2 nv the lo plane's vector t - nv (the
+// copy is then stores only: no second read of the row after the atomic).
 __device__ void row_exit_append(const ExitParams& e, int n, int r, const float* prob, const int* hit,
-                                const int* label) {
+                                const int* label, const uint4* held = nullptr, int nv_held = 0) {
   __shared__ int pos_s;
   __syncthreads();  // the row's head results (written by thread 0)
   if (r >= n) return;
@@ -814,6 +831,14 @@ __device__ void row_exit_append(const ExitParams& e, int n, int r, const float* 
   __syncthreads();
   const int pos = pos_s;
   if (pos < 0) return;
+  if (held) {
+    const int t = threadIdx.x;
+    if (t < nv_held)
+      reinterpret_cast<uint4*>(e.rows_dst_hi + static_cast<long long>(pos) * e.row_elems)[t] = *held;
+    else if (e.rows_src_lo && t < 2 * nv_held)
+      reinterpret_cast<uint4*>(e.rows_dst_lo + static_cast<long long>(pos) * e.row_elems)[t - nv_held] = *held;
+    return;
+  }
   const long long nv = e.row_elems / 8;  // 16-byte vectors per plane row
   const uint4* sh = reinterpret_cast<const uint4*>(e.rows_src_hi + static_cast<long long>(r) * e.row_elems);
   uint4* dh = reinterpret_cast<uint4*>(e.rows_dst_hi + static_cast<long long>(pos) * e.row_elems);
@@ -848,35 +873,68 @@ __global__ void __launch_bounds__(kLk) cache_head_kernel(CacheHeadParams p) {
   extern __shared__ float sm[];
   __shared__ HeadSmem hs;
   __shared__ float4 red4[kLk];
+  __shared__ float sel_s[32];  // selector: bs1[16], ws2[16]
   const int r = blockIdx.x;
   const int C = p.classes;
   float* logits = sm;    // [C]
-  float* feat = sm + C;  // [max(feat, C)]
+  float* feat = sm + C;  // [head_feat_len]
   const int tid = threadIdx.x;
-  // fused-GAP heads (<= 32 classes): the static head weights are staged in
-  // shared memory BEFORE the programmatic-launch wait, i.e. while the tap's
-  // conv is still draining (launch_cache_head sizes the region)
+  // fused-GAP and direct-row heads (<= 32 classes): the static head weights
+  // are staged in shared memory BEFORE the programmatic-launch wait, i.e.
+  // while the tap's producer is still draining (launch_cache_head sizes the region)
   const bool stage_w = head_stages_weights(p);
-  // same extent as launch_cache_head's feat_len
-  const int feat_len = (p.family == 2 || p.pre_logits) ? C : (p.feat > C ? p.feat : C);
-  float* w2s = feat + feat_len;                    // [C][feat]
+  const int w2c = head_w2_cols(p);
+  float* w2s = feat + head_feat_len(p);             // [C][w2c]
   const bool stage_s = head_stages_ws1(p);
-  float* ws1s = stage_w ? w2s + C * p.feat : w2s;  // [16][C]
-  if (stage_w) stage_floats(w2s, p.W2, C * p.feat, tid);
+  float* ws1s = stage_w ? w2s + C * w2c : w2s;  // [16][C]
+  if (stage_w) stage_floats(w2s, p.W2, C * w2c, tid);
   if (stage_w || stage_s) stage_floats(ws1s, p.Ws1, 16 * C, tid);
+  if (tid < 16) sel_s[tid] = __ldg(p.bs1 + tid);
+  else if (tid < 32) sel_s[tid] = __ldg(p.ws2 + tid - 16);
+  // direct rows in 16-byte vectors (thread t < nv: hi vector t; nv <= t < 2 nv:
+  // lo vector t - nv), kept in registers for the row append's copy
+  const int nv = p.D / 8;
+  const bool rvec = p.row_hi && (p.D & 7) == 0 && (p.row_stride & 7) == 0 &&
+                    (reinterpret_cast<uintptr_t>(p.row_hi) & 15) == 0 &&
+                    (reinterpret_cast<uintptr_t>(p.row_lo) & 15) == 0 && 2 * nv <= kLk;
   pdl_wait();
   pdl_trigger();
+  uint4 held = make_uint4(0u, 0u, 0u, 0u);
+  if (rvec) {  // issued with the count's load (rows up to max_rows are allocated; r >= n is discarded)
+    const long long rb = static_cast<long long>(r) * p.row_stride;
+    if (tid < nv)
+      held = __ldg(reinterpret_cast<const uint4*>(p.row_hi + rb) + tid);
+    else if (p.row_lo && tid < 2 * nv)
+      held = __ldg(reinterpret_cast<const uint4*>(p.row_lo + rb) + tid - nv);
+  }
   const int n = *p.count;
   if (r < n && p.row_hi) {
     // direct row mode: x = the request's row; Pool(w) bins (AvgPool over flat
     // windows times 1/w, network.cpp:130-138) or Conv(k,s) + ReLU
     // (network.cpp:127-148) into feat, then the FC(.,C) logits
     float* x = feat + (p.family == 2 ? p.out_dim : p.feat);  // [D]
-    const long long rb = static_cast<long long>(r) * p.row_stride;
-    for (int i = tid; i < p.D; i += kLk) {
-      float v = __bfloat162float(p.row_hi[rb + i]);
-      if (p.row_lo) v += __bfloat162float(p.row_lo[rb + i]);
-      x[i] = v;
+    if (rvec) {
+      // x = hi + lo (the lo plane parked in red4 first)
+      float* lo_s = reinterpret_cast<float*>(red4);
+      const __nv_bfloat16* hv = reinterpret_cast<const __nv_bfloat16*>(&held);
+      if (tid < nv) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) x[8 * tid + e] = __bfloat162float(hv[e]);
+      } else if (p.row_lo && tid < 2 * nv) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) lo_s[8 * (tid - nv) + e] = __bfloat162float(hv[e]);
+      }
+      if (p.row_lo) {
+        __syncthreads();
+        for (int i = tid; i < p.D; i += kLk) x[i] += lo_s[i];
+      }
+    } else {
+      const long long rb = static_cast<long long>(r) * p.row_stride;
+      for (int i = tid; i < p.D; i += kLk) {
+        float v = __bfloat162float(p.row_hi[rb + i]);
+        if (p.row_lo) v += __bfloat162float(p.row_lo[rb + i]);
+        x[i] = v;
+      }
     }
     __syncthreads();
     int nf;
@@ -896,9 +954,12 @@ __global__ void __launch_bounds__(kLk) cache_head_kernel(CacheHeadParams p) {
       }
     }
     __syncthreads();
-    block_logits(p.W2, p.b2, C, nf, feat, logits);
+    if (stage_w)
+      block_logits<true>(w2s, p.b2, C, nf, feat, logits);
+    else
+      block_logits(p.W2, p.b2, C, nf, feat, logits);
     __syncthreads();
-    head_block(p, r, logits, feat, hs, p.Ws1);
+    head_block(p, r, logits, feat, hs, (stage_w || stage_s) ? ws1s : p.Ws1, sel_s, sel_s + 16);
   } else if (r < n) {
     if (p.pre_logits) {
       for (int k = tid; k < C; k += kLk) logits[k] = fc_logit(p.pre_logits, p.pre_nz, p.pre_zstride, p.b2, r, C, k);
@@ -930,13 +991,17 @@ __global__ void __launch_bounds__(kLk) cache_head_kernel(CacheHeadParams p) {
         block_logits(p.W2, p.b2, C, p.feat, feat, logits);
     }
     __syncthreads();
-    head_block(p, r, logits, feat, hs, (stage_w || stage_s) ? ws1s : p.Ws1);
+    head_block(p, r, logits, feat, hs, (stage_w || stage_s) ? ws1s : p.Ws1, sel_s, sel_s + 16);
   }
   if (p.ex.arrive) {
-    if (p.ex.rows_dst_hi && !p.ex.shadow)
-      row_exit_append(p.ex, n, r, p.prob, p.hit, p.label);
-    else
+    if (p.ex.rows_dst_hi && !p.ex.shadow) {
+      // the held vectors are the whole row to copy when the tap is the compacted row itself
+      const bool use_held = rvec && p.ex.rows_src_hi == p.row_hi && p.ex.rows_src_lo == p.row_lo &&
+                            p.ex.row_elems == p.D && p.row_stride == p.ex.row_elems;
+      row_exit_append(p.ex, n, r, p.prob, p.hit, p.label, use_held ? &held : nullptr, nv);
+    } else {
       exit_tail(p.ex, n, p.prob, p.hit, p.label);
+    }
   }
 }
 
@@ -1727,13 +1792,8 @@ void launch_cache_head(const CacheHeadParams& p_in, int max_rows, cudaStream_t s
     p.pre_zstride = static_cast<long long>(max_rows) * p.classes;
     p.gap = nullptr;
   }
-  int feat_len = (p.family == 2 || p.pre_logits) ? p.classes : (p.feat > p.classes ? p.feat : p.classes);
-  if (p.row_hi) {  // direct row mode: [features][row]
-    const int nf = p.family == 2 ? p.out_dim : p.feat;
-    feat_len = (nf > p.classes ? nf : p.classes) + p.D;
-  }
-  size_t smem = static_cast<size_t>(p.classes + feat_len) * sizeof(float);
-  if (head_stages_weights(p)) smem += static_cast<size_t>(p.classes) * (p.feat + 16) * sizeof(float);  // W2 + Ws1
+  size_t smem = static_cast<size_t>(p.classes + head_feat_len(p)) * sizeof(float);
+  if (head_stages_weights(p)) smem += static_cast<size_t>(p.classes) * (head_w2_cols(p) + 16) * sizeof(float);  // W2 + Ws1
   else if (head_stages_ws1(p)) smem += static_cast<size_t>(p.classes) * 16 * sizeof(float);          // Ws1
   static std::atomic<unsigned long long> attr{0};
   if (first_on_device(attr))

@@ -183,6 +183,43 @@ def test_lookup_mlp_taps(arch):
             assert got["label"][i] == O.argmax(pr)
 
 
+@pytest.mark.parametrize("classes,widths", [(10, [64, 128, 64]), (100, [96, 100, 64])])
+def test_mlp_direct_heads_vs_oracle(classes, widths):
+    """Block-MLP serving where the heads read the request's row themselves
+    (Pool(w) / Conv(k,s) predictor inside the head, static weights staged
+    before the programmatic-launch wait, the row held in registers for the
+    compacted copy) and the FC(h) head, against the oracle's serve_one, in
+    shadow and compact mode: 10 classes (direct Pool head, 16-byte row
+    vectors), and 100 classes with a 100-wide tap (Pool(w) through the
+    batched logits GEMM, Conv(k,s) direct with the scalar row path)."""
+    m = lcb.make_base_model(48, classes, widths, 3, 13)
+    archs = ["Pool(32)", "Conv(3,1)", "FC(64)"]
+    vs = [lcb.build_variant(l + 1, 0, a, m.tap_dim(l + 1), classes, 17 + l) for l, a in enumerate(archs)]
+    for v in vs:
+        v.set_selector_out(25.0, 0.0)
+    x = mlp_inputs(96, 48, 29)
+    model = O.parse_model(m.save())
+    metas = [O.parse_variant(v.save()) for v in vs]
+
+    def oracle(ds):
+        return O.oracle_serve_mlp(model, [(mt["layer"], mt["predictor"], mt["selector"], d) for mt, d in zip(metas, ds)], x)
+
+    # thresholds at quantiles of the oracle's selector probabilities (no exits
+    # at delta 2): about a quarter of the requests exit at each cache
+    probs_all = oracle([2.0] * 3)[3]
+    ds = [float(np.quantile(probs_all[:, l], q)) for l, q in enumerate((0.75, 0.7, 0.6))]
+    for v, d in zip(vs, ds):
+        v.delta = d
+    el, sv, bp, probs = oracle(ds)
+    assert np.all(np.bincount(el, minlength=4) >= 10)  # requests exit at every cache and at the end
+    deltas = {mt["layer"]: d for mt, d in zip(metas, ds)}
+    dep = lcb.Deployment(m, vs, precision="bf16x3", max_batch=128)
+    for shadow in (True, False):
+        res = dep.serve(x, shadow=shadow)
+        compare_serve(res, el, sv, bp, probs, deltas, shadow)
+    dep.close()
+
+
 def test_inclusive_threshold_on_gpu():
     # test_cache.cpp:218-227 on the device: zeroed selector -> prob exactly 0.5
     m = lcb.make_base_model(4, 3, [4], 1, 1)
