@@ -193,7 +193,16 @@ def cpu_reference(cfg_name, steps, warmup, seed=2101):
     for _ in range(steps):
         run()
     dt = time.perf_counter() - t0
-    return {"value": sample * steps / dt, "unit": "requests/s", "cores": cores, "kind": kind, "sample": desc}
+    out = {"value": sample * steps / dt, "unit": "requests/s", "cores": cores, "kind": kind, "sample": desc}
+    if family == "mlp":
+        # the reference on one core as well (a 1024-request sample)
+        x1 = x[:1024]
+        O.ref_simulate(rm, rvs, x1[:64], threads=1)
+        t0 = time.perf_counter()
+        O.ref_simulate(rm, rvs, x1, threads=1)
+        out["single_core"] = {"value": len(x1) / (time.perf_counter() - t0), "unit": "requests/s", "cores": 1,
+                              "sample": "1024 requests of the same workload, one thread"}
+    return out
 
 
 def main():
