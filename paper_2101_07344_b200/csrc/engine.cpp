@@ -237,10 +237,17 @@ Engine::Engine(int device, const BaseModel& model, std::vector<CacheVariant> var
   ck(cudaStreamSynchronize(stream_), "build");
 }
 
+void Engine::drop_graph(int mode) {
+  if (graph_[mode]) cudaGraphExecDestroy(graph_[mode]);
+  if (graph_tmpl_[mode]) cudaGraphDestroy(graph_tmpl_[mode]);
+  graph_[mode] = nullptr;
+  graph_tmpl_[mode] = nullptr;
+  graph_init_node_[mode] = nullptr;
+}
+
 Engine::~Engine() {
   if (stream_) cudaStreamSynchronize(stream_);
-  for (auto& g : graph_)
-    if (g) cudaGraphExecDestroy(g);
+  for (int m = 0; m < kModes; ++m) drop_graph(m);
   for (void* p : allocs_) cudaFree(p);
   if (h_batch_) cudaFreeHost(h_batch_);
   if (copy_stream_) cudaStreamSynchronize(copy_stream_);
@@ -799,11 +806,10 @@ void Engine::build_mlp_steps(std::vector<Step>& steps, bool shadow, bool stamps)
   int* src = d_src_;
   int* counts = d_counts_;
   steps.push_back({[this, L](cudaStream_t s) {
-                     launch_init_batch(d_batch_, max_batch_, d_ids_, d_counts_, nullptr, 0, d_exit_, d_served_, d_base_,
-                                       d_exit_ns_, d_probs_, L, s);
-                     launch_stamp_start(d_t0_, s);
+                     launch_init_batch(cur_batch_, d_batch_, max_batch_, d_ids_, d_counts_, nullptr, 0, d_exit_,
+                                       d_served_, d_base_, d_exit_ns_, d_probs_, L, d_t0_, s);
                    },
-                   0, 2});
+                   0, 1});
   const int in_dim = static_cast<int>(model_.input_dim());
   {
     Planes in = mlp_in_;
@@ -926,11 +932,10 @@ void Engine::build_cnn_steps(std::vector<Step>& steps, bool shadow, bool stamps)
     if (o.kind == CnnOpKind::Stem) stem_mult = o.Ho() * o.Wo();
   int* stem_rows = counts + L + 1;
   steps.push_back({[this, L, stem_rows, stem_mult](cudaStream_t s) {
-                     launch_init_batch(d_batch_, max_batch_, d_ids_, d_counts_, stem_rows, stem_mult, d_exit_, d_served_,
-                                       d_base_, d_exit_ns_, d_probs_, L, s);
-                     launch_stamp_start(d_t0_, s);
+                     launch_init_batch(cur_batch_, d_batch_, max_batch_, d_ids_, d_counts_, stem_rows, stem_mult,
+                                       d_exit_, d_served_, d_base_, d_exit_ns_, d_probs_, L, d_t0_, s);
                    },
-                   0, 2});
+                   0, 1});
   int* cur_ids = ids;
   int* cur_count = counts;
   const int sms = num_sms_;
@@ -1300,7 +1305,7 @@ void Engine::serve_mode(int B, int mode, bool use_graph) {
   std::lock_guard<std::recursive_mutex> dev_lock(dev_stream(device_).mu);
   require(B > 0 && B <= max_batch_, "serve: batch size " + std::to_string(B) + " outside [1, max_batch]");
   ck(cudaSetDevice(device_), "cudaSetDevice");
-  launch_set_int(d_batch_, B, stream_);
+  cur_batch_ = B;
   std::vector<Step>& st = steps_mode(mode);
   if (!use_graph) {
     static const bool sync_steps = std::getenv("LCB_SYNC_STEPS") != nullptr;  // debug: locate a failing step
@@ -1316,6 +1321,30 @@ void Engine::serve_mode(int B, int mode, bool use_graph) {
     return;
   }
   cudaGraphExec_t& ge = graph_[mode];
+  if (ge && graph_batch_[mode] != B) {
+    // the batch size lives in the init node's arguments: update it in place
+    // (launches already enqueued keep theirs); re-capture if that fails
+    bool ok = graph_init_node_[mode] != nullptr;
+    if (ok) {
+      cudaKernelNodeParams kp{};
+      ok = cudaGraphKernelNodeGetParams(graph_init_node_[mode], &kp) == cudaSuccess && kp.kernelParams;
+      if (ok) {
+        void* args[kInitBatchArgs];
+        for (int i = 0; i < kInitBatchArgs; ++i) args[i] = kp.kernelParams[i];
+        int b = B;
+        args[0] = &b;
+        kp.kernelParams = args;
+        kp.extra = nullptr;
+        ok = cudaGraphExecKernelNodeSetParams(ge, graph_init_node_[mode], &kp) == cudaSuccess;
+      }
+    }
+    if (ok) {
+      graph_batch_[mode] = B;
+    } else {
+      cudaGetLastError();
+      drop_graph(mode);
+    }
+  }
   if (!ge) {
     cudaGraph_t g;
     ck(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "capture");
@@ -1331,7 +1360,26 @@ void Engine::serve_mode(int B, int mode, bool use_graph) {
     }
     ck(cudaStreamEndCapture(stream_, &g), "capture end");
     ck(cudaGraphInstantiate(&ge, g, 0), "graph instantiate");
-    cudaGraphDestroy(g);
+    // keep the template graph: its init node is the handle for batch-size updates
+    graph_tmpl_[mode] = g;
+    graph_batch_[mode] = B;
+    graph_init_node_[mode] = nullptr;
+    size_t nn = 0;
+    if (cudaGraphGetNodes(g, nullptr, &nn) == cudaSuccess && nn > 0) {
+      std::vector<cudaGraphNode_t> nodes(nn);
+      if (cudaGraphGetNodes(g, nodes.data(), &nn) == cudaSuccess) {
+        for (cudaGraphNode_t nd : nodes) {
+          cudaGraphNodeType ty;
+          cudaKernelNodeParams kp{};
+          if (cudaGraphNodeGetType(nd, &ty) == cudaSuccess && ty == cudaGraphNodeTypeKernel &&
+              cudaGraphKernelNodeGetParams(nd, &kp) == cudaSuccess && kp.func == init_batch_kernel_fn()) {
+            graph_init_node_[mode] = nd;
+            break;
+          }
+        }
+      }
+    }
+    cudaGetLastError();
   }
   ck(cudaGraphLaunch(ge, stream_), "graph launch");
 }
@@ -1494,7 +1542,7 @@ void Engine::read_tap_nchw(int layer, int B, float* host_out) {
   require(layer >= 1 && layer <= model_.num_blocks, "read_tap: layer out of range");
   require(B > 0 && B <= max_batch_, "read_tap: batch outside [1, max_batch]");
   ck(cudaSetDevice(device_), "cudaSetDevice");
-  launch_set_int(d_batch_, B, stream_);
+  cur_batch_ = B;
   std::vector<Step>& st = steps_for(true);
   const int end = tap_step_end_[static_cast<size_t>(layer)];
   require(end >= 0, "read_tap: no tap recorded for the layer");
@@ -1596,11 +1644,7 @@ void Engine::set_delta(int layer, double delta) {
   caches_[static_cast<size_t>(ci)]->delta = delta;
   variants_[static_cast<size_t>(ci)].delta = delta;
   // Graphs bake kernel parameters: re-capture on next serve.
-  for (auto& g : graph_)
-    if (g) {
-      cudaGraphExecDestroy(g);
-      g = nullptr;
-    }
+  for (int m = 0; m < kModes; ++m) drop_graph(m);
 }
 
 namespace {
@@ -1659,11 +1703,7 @@ void Engine::update_variant(const CacheVariant& nv) {
   c.delta = nv.delta;
   cur = nv;
   ck(cudaStreamSynchronize(stream_), "update_variant: upload");
-  for (auto& g : graph_)
-    if (g) {
-      cudaGraphExecDestroy(g);
-      g = nullptr;
-    }
+  for (int m = 0; m < kModes; ++m) drop_graph(m);
 }
 
 void Engine::read_taps(int layer, int B, double* host_out) {
@@ -1726,11 +1766,7 @@ void Engine::set_selector_out(int layer, double gain, double bias) {
   h2d(c.ws2, w.data(), w.size() * sizeof(float));
   ck(cudaStreamSynchronize(stream_), "selector upload");
   c.bs2 = static_cast<float>(bias);
-  for (auto& g : graph_)
-    if (g) {
-      cudaGraphExecDestroy(g);
-      g = nullptr;
-    }
+  for (int m = 0; m < kModes; ++m) drop_graph(m);
   c.lookup_steps.clear();
 }
 
@@ -1738,7 +1774,7 @@ std::vector<StepProfile> Engine::profile(int B, bool shadow) {
   std::lock_guard<std::recursive_mutex> dev_lock(dev_stream(device_).mu);
   require(B > 0 && B <= max_batch_, "profile: batch outside [1, max_batch]");
   ck(cudaSetDevice(device_), "cudaSetDevice");
-  launch_set_int(d_batch_, B, stream_);
+  cur_batch_ = B;
   std::vector<Step>& st = steps_for(shadow);
   std::vector<cudaEvent_t> ev(st.size() + 1);
   for (auto& e : ev) ck(cudaEventCreate(&e), "event");

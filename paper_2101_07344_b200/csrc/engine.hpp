@@ -272,6 +272,11 @@ class Engine {
   std::vector<int> tap_step_end_;  // shadow step list: index one past the op producing tap l (by layer)
   bool built_[kModes] = {false, false, false};
   cudaGraphExec_t graph_[kModes] = {nullptr, nullptr, nullptr};
+  cudaGraph_t graph_tmpl_[kModes] = {nullptr, nullptr, nullptr};          // captured template (owns the init node)
+  cudaGraphNode_t graph_init_node_[kModes] = {nullptr, nullptr, nullptr};  // batch-init node: B is its argument 0
+  int graph_batch_[kModes] = {0, 0, 0};                                     // B the executable graph holds
+  int cur_batch_ = 0;  // batch size of the serve being issued (the init step's argument)
+  void drop_graph(int mode);
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
   struct Slot {
     float* d_in = nullptr;  // staged input [max_batch][input_dim]

@@ -800,11 +800,11 @@ __device__ void exit_tail(const ExitParams& e, int n, const float* prob, const i
 // First-hit exit of row r by its own CTA (serve_one, serving.cpp:112-121) with
 // atomic-position compaction of the row-compacted activations (ExitParams::
 // rows_dst_hi): a miss is appended to ids_out and its activation row copied.
-// held (nullable): the row's 16-byte vectors already in registers, thread t <
+// use_held: the row's 16-byte vectors already in registers (held), thread t <
 // nv the hi plane's vector t, nv <= t < 2 nv the lo plane's vector t - nv (the
 // copy is then stores only: no second read of the row after the atomic).
 __device__ void row_exit_append(const ExitParams& e, int n, int r, const float* prob, const int* hit,
-                                const int* label, const uint4* held = nullptr, int nv_held = 0) {
+                                const int* label, bool use_held = false, uint4 held = uint4{}, int nv_held = 0) {
   __shared__ int pos_s;
   __syncthreads();  // the row's head results (written by thread 0)
   if (r >= n) return;
@@ -831,12 +831,12 @@ __device__ void row_exit_append(const ExitParams& e, int n, int r, const float* 
   __syncthreads();
   const int pos = pos_s;
   if (pos < 0) return;
-  if (held) {
+  if (use_held) {
     const int t = threadIdx.x;
     if (t < nv_held)
-      reinterpret_cast<uint4*>(e.rows_dst_hi + static_cast<long long>(pos) * e.row_elems)[t] = *held;
+      reinterpret_cast<uint4*>(e.rows_dst_hi + static_cast<long long>(pos) * e.row_elems)[t] = held;
     else if (e.rows_src_lo && t < 2 * nv_held)
-      reinterpret_cast<uint4*>(e.rows_dst_lo + static_cast<long long>(pos) * e.row_elems)[t - nv_held] = *held;
+      reinterpret_cast<uint4*>(e.rows_dst_lo + static_cast<long long>(pos) * e.row_elems)[t - nv_held] = held;
     return;
   }
   const long long nv = e.row_elems / 8;  // 16-byte vectors per plane row
@@ -889,8 +889,10 @@ __global__ void __launch_bounds__(kLk) cache_head_kernel(CacheHeadParams p) {
   float* ws1s = stage_w ? w2s + C * w2c : w2s;  // [16][C]
   if (stage_w) stage_floats(w2s, p.W2, C * w2c, tid);
   if (stage_w || stage_s) stage_floats(ws1s, p.Ws1, 16 * C, tid);
-  if (tid < 16) sel_s[tid] = __ldg(p.bs1 + tid);
-  else if (tid < 32) sel_s[tid] = __ldg(p.ws2 + tid - 16);
+  if (p.row_hi) {  // (direct rows: the whole head reads shared memory after the wait)
+    if (tid < 16) sel_s[tid] = __ldg(p.bs1 + tid);
+    else if (tid < 32) sel_s[tid] = __ldg(p.ws2 + tid - 16);
+  }
   // direct rows in 16-byte vectors (thread t < nv: hi vector t; nv <= t < 2 nv:
   // lo vector t - nv), kept in registers for the row append's copy
   const int nv = p.D / 8;
@@ -916,13 +918,15 @@ __global__ void __launch_bounds__(kLk) cache_head_kernel(CacheHeadParams p) {
     if (rvec) {
       // x = hi + lo (the lo plane parked in red4 first)
       float* lo_s = reinterpret_cast<float*>(red4);
-      const __nv_bfloat16* hv = reinterpret_cast<const __nv_bfloat16*>(&held);
-      if (tid < nv) {
+      // bf16 -> fp32 is the 16-bit pattern shifted up (no address taken: held stays in registers)
+      const uint32_t hw[4] = {held.x, held.y, held.z, held.w};
+      float* dst = tid < nv ? x + 8 * tid : lo_s + 8 * (tid - nv);
+      if (tid < nv || (p.row_lo && tid < 2 * nv)) {
 #pragma unroll
-        for (int e = 0; e < 8; ++e) x[8 * tid + e] = __bfloat162float(hv[e]);
-      } else if (p.row_lo && tid < 2 * nv) {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) lo_s[8 * (tid - nv) + e] = __bfloat162float(hv[e]);
+        for (int e = 0; e < 4; ++e) {
+          dst[2 * e] = __uint_as_float(hw[e] << 16);
+          dst[2 * e + 1] = __uint_as_float(hw[e] & 0xffff0000u);
+        }
       }
       if (p.row_lo) {
         __syncthreads();
@@ -959,7 +963,7 @@ __global__ void __launch_bounds__(kLk) cache_head_kernel(CacheHeadParams p) {
     else
       block_logits(p.W2, p.b2, C, nf, feat, logits);
     __syncthreads();
-    head_block(p, r, logits, feat, hs, (stage_w || stage_s) ? ws1s : p.Ws1, sel_s, sel_s + 16);
+    head_block(p, r, logits, feat, hs, stage_w ? ws1s : p.Ws1, sel_s, sel_s + 16);
   } else if (r < n) {
     if (p.pre_logits) {
       for (int k = tid; k < C; k += kLk) logits[k] = fc_logit(p.pre_logits, p.pre_nz, p.pre_zstride, p.b2, r, C, k);
@@ -991,14 +995,14 @@ __global__ void __launch_bounds__(kLk) cache_head_kernel(CacheHeadParams p) {
         block_logits(p.W2, p.b2, C, p.feat, feat, logits);
     }
     __syncthreads();
-    head_block(p, r, logits, feat, hs, (stage_w || stage_s) ? ws1s : p.Ws1, sel_s, sel_s + 16);
+    head_block(p, r, logits, feat, hs, (stage_w || stage_s) ? ws1s : p.Ws1, p.bs1, p.ws2);
   }
   if (p.ex.arrive) {
     if (p.ex.rows_dst_hi && !p.ex.shadow) {
       // the held vectors are the whole row to copy when the tap is the compacted row itself
       const bool use_held = rvec && p.ex.rows_src_hi == p.row_hi && p.ex.rows_src_lo == p.row_lo &&
                             p.ex.row_elems == p.D && p.row_stride == p.ex.row_elems;
-      row_exit_append(p.ex, n, r, p.prob, p.hit, p.label, use_held ? &held : nullptr, nv);
+      row_exit_append(p.ex, n, r, p.prob, p.hit, p.label, use_held, held, nv);
     } else {
       exit_tail(p.ex, n, p.prob, p.hit, p.label);
     }
@@ -1640,12 +1644,15 @@ __global__ void stamp_kernel(unsigned long long* t0) {
   pdl_wait();
   pdl_trigger(); *t0 = globaltimer(); }
 
-__global__ void init_batch_kernel(const int* batch, int max_batch, int* ids0, int* count0, int* rows_out, int rows_mult,
-                                  int* exit_layer, int* served, int* base_pred, unsigned long long* exit_ns,
-                                  float* probs, int L) {
+// B is a kernel argument: a captured graph's node is updated in place when
+// the batch size changes (Engine::serve_mode), so no separate launch writes
+// it; batch_out keeps a device copy for later kernels (confusion counts).
+__global__ void init_batch_kernel(int B, int* batch_out, int max_batch, int* ids0, int* count0, int* rows_out,
+                                  int rows_mult, int* exit_layer, int* served, int* base_pred,
+                                  unsigned long long* exit_ns, float* probs, int L, unsigned long long* t0) {
   pdl_wait();
   pdl_trigger();
-  const int B = *batch;
+  if (t0 && blockIdx.x == 0 && threadIdx.x == 0) *t0 = globaltimer();  // batch start (latency origin)
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < max_batch; i += gridDim.x * blockDim.x) {
     ids0[i] = i;
     exit_layer[i] = 0;
@@ -1656,6 +1663,7 @@ __global__ void init_batch_kernel(const int* batch, int max_batch, int* ids0, in
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     *count0 = B;
+    if (batch_out) *batch_out = B;
     if (rows_out) *rows_out = B * rows_mult;
   }
   // per-layer survivor counts start at zero (atomic row compaction appends to them)
@@ -1904,12 +1912,14 @@ void launch_set_int(int* p, int v, cudaStream_t s) { launch_pdl(set_int_kernel, 
 
 void launch_stamp_start(unsigned long long* t0, cudaStream_t s) { launch_pdl(stamp_kernel, dim3(1), dim3(1), 0, s, t0); }
 
-void launch_init_batch(const int* batch, int max_batch, int* ids0, int* count0, int* rows_out, int rows_mult,
+void launch_init_batch(int B, int* batch_out, int max_batch, int* ids0, int* count0, int* rows_out, int rows_mult,
                        int* exit_layer, int* served, int* base_pred, unsigned long long* exit_ns, float* probs, int L,
-                       cudaStream_t s) {
+                       unsigned long long* t0, cudaStream_t s) {
   const int blocks = (max_batch + 255) / 256 > 0 ? (max_batch + 255) / 256 : 1;
-  launch_pdl(init_batch_kernel, dim3(blocks), dim3(256), 0, s, batch, max_batch, ids0, count0, rows_out, rows_mult, exit_layer, served,
-                                           base_pred, exit_ns, probs, L);
+  launch_pdl(init_batch_kernel, dim3(blocks), dim3(256), 0, s, B, batch_out, max_batch, ids0, count0, rows_out,
+             rows_mult, exit_layer, served, base_pred, exit_ns, probs, L, t0);
 }
+
+const void* init_batch_kernel_fn() { return reinterpret_cast<const void*>(&init_batch_kernel); }
 
 }  // namespace lcb

@@ -193,10 +193,14 @@ void launch_stamp_start(unsigned long long* t0, cudaStream_t s);
 // *p = v as a stream-ordered kernel (the value travels in the launch parameters,
 // so back-to-back submissions never race on a host staging word).
 void launch_set_int(int* p, int v, cudaStream_t s);
-// Batch prologue: B = *batch; ids0 = identity, count0 = B, rows_out = B *
-// rows_mult (stem GEMM rows, nullable), outputs reset, probs [L][max_batch] = NaN.
-void launch_init_batch(const int* batch, int max_batch, int* ids0, int* count0, int* rows_out, int rows_mult,
+// Batch prologue: ids0 = identity, count0 = B (and *batch_out), rows_out = B *
+// rows_mult (stem GEMM rows, nullable), outputs reset, probs [L][max_batch] =
+// NaN, *t0 = %globaltimer (batch start, nullable).
+void launch_init_batch(int B, int* batch_out, int max_batch, int* ids0, int* count0, int* rows_out, int rows_mult,
                        int* exit_layer, int* served, int* base_pred, unsigned long long* exit_ns, float* probs, int L,
-                       cudaStream_t s);
+                       unsigned long long* t0, cudaStream_t s);
+// host stub of the batch-init kernel (locates its node in a captured graph) and its argument count
+const void* init_batch_kernel_fn();
+constexpr int kInitBatchArgs = 14;
 
 }  // namespace lcb
