@@ -608,12 +608,17 @@ __device__ void block_logits(const float* __restrict__ W, const float* __restric
 // layer (16 x C) before the wait when it fits (<= 64 KB): one L2 round trip
 // off the tail.
 __host__ __device__ inline bool head_stages_ws1(const CacheHeadParams& p);
+#ifndef LCB_FC_NO_STAGE
+#define LCB_FC_NO_STAGE 0
+#endif
 // columns of W2 [classes][cols]: the Conv(k,s) head of a direct row reads its own conv outputs
 __host__ __device__ inline int head_w2_cols(const CacheHeadParams& p) {
   return (p.row_hi && p.family == 2) ? p.out_dim : p.feat;
 }
 __host__ __device__ inline bool head_stages_weights(const CacheHeadParams& p) {
-  return (p.gap != nullptr || p.row_hi != nullptr) && !p.pre_logits && p.classes * (head_w2_cols(p) + 16) <= 12288;
+  // (FC(h) heads: batch-sized launches only, whose copy overlaps the hidden-layer GEMM)
+  return (p.gap != nullptr || p.row_hi != nullptr || (p.family == 0 && p.rows_total >= 32 && !LCB_FC_NO_STAGE)) &&
+         !p.pre_logits && p.classes * (head_w2_cols(p) + 16) <= 12288;
 }
 // floats of the head's feature region (after the logits): direct rows hold
 // [features][row] there; launch_cache_head sizes the same extent
@@ -982,9 +987,22 @@ __global__ void __launch_bounds__(kLk) cache_head_kernel(CacheHeadParams p) {
       } else if (p.family == 1) {
         for (int o = tid; o < p.feat; o += kLk) feat[o] = __ldg(p.feats + static_cast<long long>(r) * p.feat + o);
       } else {
+        // hidden = relu(b1 + sum of the split-K partials, ascending split):
+        // 8 splits' loads issued before the adds (a runtime-bounded loop
+        // would wait on each load in turn)
         for (int j = tid; j < p.feat; j += kLk) {
           float a = p.b1[j];
-          for (int s = 0; s < p.ks; ++s) a += __ldg(p.feats + (static_cast<long long>(s) * p.rows_total + r) * p.hp + j);
+          for (int s0 = 0; s0 < p.ks; s0 += 8) {
+            float t[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int sp = s0 + u < p.ks ? s0 + u : p.ks - 1;
+              t[u] = __ldg(p.feats + (static_cast<long long>(sp) * p.rows_total + r) * p.hp + j);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              if (s0 + u < p.ks) a += t[u];
+          }
           feat[j] = a > 0.0f ? a : 0.0f;
         }
       }
@@ -1382,9 +1400,46 @@ __global__ void split_rows_kernel(const float* x, int in_dim, int dp, const int*
   const int j = blockIdx.x;
   if (j >= *count) return;
   const long long src = ids ? ids[j] : j;
+  const float* xr = x + src * in_dim;
+  const long long ob = static_cast<long long>(j) * dp;
+  if ((in_dim & 3) == 0 && (dp & 3) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+    // 16-byte loads, kSplitVec per thread issued before any use (the row is
+    // usually cold in HBM: one round trip per batch of loads, not per element)
+    constexpr int kSplitVec = 4;
+    const int n4 = dp >> 2, in4 = in_dim >> 2;
+    for (int base = 0; base < n4; base += kSplitVec * blockDim.x) {
+      float4 v[kSplitVec];
+#pragma unroll
+      for (int u = 0; u < kSplitVec; ++u) {
+        const int i4 = base + u * blockDim.x + threadIdx.x;
+        v[u] = i4 < in4 ? __ldg(reinterpret_cast<const float4*>(xr) + i4) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < kSplitVec; ++u) {
+        const int i4 = base + u * blockDim.x + threadIdx.x;
+        if (i4 < n4) {
+          const float f[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+          __nv_bfloat16 h[4], l[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            h[e] = __float2bfloat16_rn(f[e]);
+            l[e] = __float2bfloat16_rn(f[e] - __bfloat162float(h[e]));
+          }
+          uint2 hp, lp;
+          hp.x = (static_cast<uint32_t>(__bfloat16_as_ushort(h[1])) << 16) | __bfloat16_as_ushort(h[0]);
+          hp.y = (static_cast<uint32_t>(__bfloat16_as_ushort(h[3])) << 16) | __bfloat16_as_ushort(h[2]);
+          lp.x = (static_cast<uint32_t>(__bfloat16_as_ushort(l[1])) << 16) | __bfloat16_as_ushort(l[0]);
+          lp.y = (static_cast<uint32_t>(__bfloat16_as_ushort(l[3])) << 16) | __bfloat16_as_ushort(l[2]);
+          *reinterpret_cast<uint2*>(hi + ob + 4 * i4) = hp;
+          if (lo) *reinterpret_cast<uint2*>(lo + ob + 4 * i4) = lp;
+        }
+      }
+    }
+    return;
+  }
   for (int i = threadIdx.x; i < dp; i += blockDim.x) {
-    const float v = i < in_dim ? x[src * in_dim + i] : 0.0f;
-    split_store(v, hi, lo, static_cast<long long>(j) * dp + i);
+    const float v = i < in_dim ? xr[i] : 0.0f;
+    split_store(v, hi, lo, ob + i);
   }
 }
 
