@@ -703,19 +703,10 @@ __device__ __noinline__ bool split_reduce(const TcConvParams& p, const TileGeom&
                                           int lane, int unit, uint8_t* scratch, int* last_flag) {
   int* arr = p.ws_counters + 2 * x.tile_mn;
   int* dep = arr + 1;
-  epi_bar();  // this CTA's partial tile stores before the arrival (acq_rel, cumulative)
-  if (etid == 0) {
-    trace_put(p, unit, 6);
-    atom_add_acq_rel_gpu(arr, 1);
-    while (ld_acquire_gpu(arr) < g.ks) __nanosleep(64);
-    trace_put(p, unit, 7);
-  }
-  epi_bar();
   const int nu = (BN / 16) * (kBM / 32);
   const int u0 = static_cast<int>((static_cast<long long>(nu) * x.ks) / g.ks);
   const int u1 = static_cast<int>((static_cast<long long>(nu) * (x.ks + 1)) / g.ks);
   const float* tile_ws = p.ws + static_cast<size_t>(x.tile_mn) * g.ks * kBM * BN;
-  if (etid == 0) trace_put(p, unit, 8);
   // wpu warps share a unit (32 rows x 16 columns): warp `sub` sums the
   // partials k in [sub*ks/wpu, (sub+1)*ks/wpu) (all its loads in flight at
   // once), parks the sum in shared memory, and the unit's first warp adds the
@@ -726,23 +717,53 @@ __device__ __noinline__ bool split_reduce(const TcConvParams& p, const TileGeom&
   while (nunits > 0 && wpu * 2 * nunits <= kEpiWarps) wpu *= 2;  // (a CTA may own no unit: nu < ks)
   const int per_round = kEpiWarps / wpu;
   float4* park = reinterpret_cast<float4*>(scratch);  // [warp][4][32] float4
+  // Row geometry (survivor-list load) and BN shift of a round's unit: they do
+  // not depend on the partials, so the first round's are fetched between this
+  // CTA's arrival and its wait for the others (traced ~3k cycles after the wait otherwise)
+  struct RowUnit {
+    size_t ob;
+    int img;
+    bool img_ok, rvalid;
+    float4 sh[4];
+  };
+  auto row_unit = [&](int base, RowUnit& ru) {
+    const int uu = base + warp / wpu, sub = warp % wpu;
+    const int r = (uu % (kBM / 32)) * 32 + lane;
+    const int co = x.tn * BN + (uu / (kBM / 32)) * 16;
+    ru.ob = 0;
+    ru.img = 0;
+    ru.img_ok = false;
+    ru.rvalid = false;
+    if (uu < u1) {
+      ru.rvalid = out_row(p, g, x, r, row_geom(p, r), ru.ob, ru.img, ru.img_ok);
+      if (sub == 0 && p.shift) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) ru.sh[q] = __ldg(reinterpret_cast<const float4*>(p.shift + co) + q);
+      }
+    }
+  };
+  epi_bar();  // this CTA's partial tile stores before the arrival (acq_rel, cumulative)
+  if (etid == 0) {
+    trace_put(p, unit, 6);
+    atom_add_acq_rel_gpu(arr, 1);
+  }
+  RowUnit ru;
+  row_unit(u0, ru);  // while the tile's other CTAs arrive
+  if (etid == 0) {
+    while (ld_acquire_gpu(arr) < g.ks) __nanosleep(64);
+    trace_put(p, unit, 7);
+  }
+  epi_bar();
+  if (etid == 0) trace_put(p, unit, 8);
   for (int base = u0; base < u1; base += per_round) {
     const int uu = base + warp / wpu, sub = warp % wpu;
     const int c16 = uu / (kBM / 32), r = (uu % (kBM / 32)) * 32 + lane;
     const int co = x.tn * BN + c16 * 16;
-    // row geometry and shift first: independent of the partials, their
-    // loads overlap the partial loads; rows outside the output have no partials
-    size_t ob = 0;
-    int img = 0;
-    bool img_ok = false, rvalid = false;
-    float4 sh[4];
-    if (uu < u1) {
-      rvalid = out_row(p, g, x, r, row_geom(p, r), ob, img, img_ok);
-      if (sub == 0 && p.shift) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) sh[q] = __ldg(reinterpret_cast<const float4*>(p.shift + co) + q);
-      }
-    }
+    if (base != u0) row_unit(base, ru);
+    const size_t ob = ru.ob;
+    const int img = ru.img;
+    const bool img_ok = ru.img_ok, rvalid = ru.rvalid;
+    const float4* sh = ru.sh;
     float v[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = 0.0f;
