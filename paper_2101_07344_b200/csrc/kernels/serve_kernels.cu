@@ -1027,6 +1027,292 @@ __global__ void __launch_bounds__(kLk) cache_head_kernel(CacheHeadParams p) {
   }
 }
 
+// ------------------------------------------------------- warp-per-row head
+// The same lookup (cache.cpp:259-265) for heads with <= 32 classes whose
+// features come from the request's own row (block-MLP Pool(w) / Conv(k,s)),
+// from FC(h) split-K partials or from pooled bins: one WARP per row, 8 rows
+// per CTA, no block barriers after the staging. W2 is staged transposed
+// ([feature][class]) so lane k accumulates class k from shared memory
+// without bank conflicts; softmax, argmax (lowest index on ties), the
+// selector FC(C,16)+ReLU+FC(16,1) and the branch-stable sigmoid are warp
+// reductions. The block-per-row kernel above costs a 512-thread CTA per row:
+// latency-bound at a few hundred rows and ~50x slower per row at 16K rows.
+constexpr int kWhWarps = 8;
+
+__host__ __device__ inline int warp_head_nf(const CacheHeadParams& p) {
+  return (p.row_hi && p.family == 2) ? p.out_dim : p.feat;
+}
+__host__ __device__ inline int warp_head_dx(const CacheHeadParams& p) { return p.row_hi ? ((p.D + 3) & ~3) : 0; }
+// floats of shared memory: W2 [C][nf + 1] (odd row pitch: lane k reading
+// W2[k][o] hits bank (k (nf + 1) + o) mod 32, distinct over the classes),
+// Ws1 [16][C], bs1|ws2 [32], b2 [32], per warp x [dx] + feat [nf]
+__host__ __device__ inline size_t warp_head_smem_floats(const CacheHeadParams& p) {
+  const size_t nf = static_cast<size_t>(warp_head_nf(p)), C = static_cast<size_t>(p.classes);
+  return (nf + 1) * C + 16 * C + 64 + static_cast<size_t>(kWhWarps) * (static_cast<size_t>(warp_head_dx(p)) + nf);
+}
+
+__global__ void __launch_bounds__(kWhWarps * 32) warp_head_kernel(CacheHeadParams p) {
+  extern __shared__ __align__(16) float whs[];
+  const int C = p.classes, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool direct = p.row_hi != nullptr;
+  const int nf = warp_head_nf(p), dx = warp_head_dx(p);
+  const int pw = nf + 1;       // W2 row pitch in shared memory
+  float* w2s = whs;            // [C][nf + 1]
+  float* ws1 = w2s + pw * C;   // [16][C]
+  float* sel = ws1 + 16 * C;   // bs1[16], ws2[16]
+  float* b2s = sel + 32;       // [C]
+  float* x = b2s + 32 + warp * (dx + nf);  // this warp's row [dx]
+  float* feat = x + dx;                    // and features [nf]
+  // static head weights, before the programmatic-launch wait
+  // 16-byte loads of W2's rows, 4 per thread in flight per round (W2 rows are
+  // 16-byte aligned when nf % 4 == 0), scattered into the padded rows
+  if ((nf & 3) == 0 && (reinterpret_cast<uintptr_t>(p.W2) & 15) == 0) {
+    const int n4 = nf * C / 4;
+    for (int b0 = 0; b0 < n4; b0 += 4 * kWhWarps * 32) {
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i4 = b0 + u * kWhWarps * 32 + tid;
+        v[u] = i4 < n4 ? __ldg(reinterpret_cast<const float4*>(p.W2) + i4) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i4 = b0 + u * kWhWarps * 32 + tid;
+        if (i4 < n4) {
+          const int k = (4 * i4) / nf, o = 4 * i4 - k * nf;
+          float* d = w2s + k * pw + o;
+          d[0] = v[u].x;
+          d[1] = v[u].y;
+          d[2] = v[u].z;
+          d[3] = v[u].w;
+        }
+      }
+    }
+  } else {
+    for (int i = tid; i < nf * C; i += blockDim.x) {
+      const int k = i / nf, o = i - k * nf;
+      w2s[k * pw + o] = __ldg(p.W2 + i);
+    }
+  }
+  for (int i = tid; i < 16 * C; i += blockDim.x) ws1[i] = __ldg(p.Ws1 + i);
+  if (tid < 16)
+    sel[tid] = __ldg(p.bs1 + tid);
+  else if (tid < 32)
+    sel[tid] = __ldg(p.ws2 + tid - 16);
+  else if (tid < 32 + C)
+    b2s[tid - 32] = __ldg(p.b2 + tid - 32);
+  pdl_wait();
+  pdl_trigger();
+  const int n = *p.count;
+  __syncthreads();
+  const int r = blockIdx.x * kWhWarps + warp;
+  // direct rows as 16-byte vectors (lane j holds vectors j, j + 32, ...), kept for the row append's copy
+  const int nv = direct ? p.D / 8 : 0;
+  const bool rvec = direct && (p.D & 7) == 0 && (p.row_stride & 7) == 0 &&
+                    (reinterpret_cast<uintptr_t>(p.row_hi) & 15) == 0 &&
+                    (reinterpret_cast<uintptr_t>(p.row_lo) & 15) == 0 && nv <= 32 * 4;
+  uint4 hv[4], lv[4];
+  float q = 0.0f;
+  int hit = 0, am = 0;
+  if (r < n) {
+    if (direct) {
+      const long long rb = static_cast<long long>(r) * p.row_stride;
+      if (rvec) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int vi = lane + 32 * j;
+          hv[j] = lv[j] = make_uint4(0u, 0u, 0u, 0u);
+          if (vi < nv) {
+            hv[j] = __ldg(reinterpret_cast<const uint4*>(p.row_hi + rb) + vi);
+            if (p.row_lo) lv[j] = __ldg(reinterpret_cast<const uint4*>(p.row_lo + rb) + vi);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int vi = lane + 32 * j;
+          if (vi < nv) {
+            const uint32_t hw[4] = {hv[j].x, hv[j].y, hv[j].z, hv[j].w};
+            const uint32_t lw[4] = {lv[j].x, lv[j].y, lv[j].z, lv[j].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              // bf16 -> fp32: the pattern shifted up; x = hi + lo as the reference-width value
+              float a = __uint_as_float(hw[e] << 16), b = __uint_as_float(hw[e] & 0xffff0000u);
+              if (p.row_lo) {
+                a += __uint_as_float(lw[e] << 16);
+                b += __uint_as_float(lw[e] & 0xffff0000u);
+              }
+              x[8 * vi + 2 * e] = a;
+              x[8 * vi + 2 * e + 1] = b;
+            }
+          }
+        }
+      } else {
+        for (int i = lane; i < p.D; i += 32) {
+          float v = __bfloat162float(p.row_hi[rb + i]);
+          if (p.row_lo) v += __bfloat162float(p.row_lo[rb + i]);
+          x[i] = v;
+        }
+      }
+      __syncwarp();
+      if (p.family == 1) {  // Pool(w): AvgPool over flat windows times 1/w (network.cpp:130-138)
+        for (int o = lane; o < nf; o += 32) {
+          float a = 0.0f;
+          for (int t = 0; t < p.win; ++t) a += x[o * p.win + t];
+          feat[o] = a * p.pool_inv;
+        }
+      } else {  // Conv(k,s) + ReLU (network.cpp:127-148)
+        for (int o = lane; o < nf; o += 32) {
+          float y = p.b1c;
+          for (int t = 0; t < p.kernel; ++t) y += __ldg(p.w1 + t) * x[o * p.stride + t];
+          feat[o] = y > 0.0f ? y : 0.0f;
+        }
+      }
+    } else if (p.family == 1) {  // pooled bins [rows][feat]
+      for (int o = lane; o < nf; o += 32) feat[o] = __ldg(p.feats + static_cast<long long>(r) * nf + o);
+    } else {  // FC(h): hidden = relu(b1 + sum of the split-K partials, ascending split)
+      // 4 hidden units per lane x 4 splits per round: 16 loads in flight
+      for (int j0 = lane; j0 < nf; j0 += 4 * 32) {
+        float a[4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) a[v] = j0 + 32 * v < nf ? p.b1[j0 + 32 * v] : 0.0f;
+        for (int s0 = 0; s0 < p.ks; s0 += 4) {
+          float t[4][4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int sp = s0 + u < p.ks ? s0 + u : p.ks - 1;
+            const float* src = p.feats + (static_cast<long long>(sp) * p.rows_total + r) * p.hp;
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              const int j = j0 + 32 * v < nf ? j0 + 32 * v : j0;
+              t[u][v] = __ldg(src + j);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (s0 + u < p.ks) {
+#pragma unroll
+              for (int v = 0; v < 4; ++v) a[v] += t[u][v];
+            }
+        }
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+          if (j0 + 32 * v < nf) feat[j0 + 32 * v] = a[v] > 0.0f ? a[v] : 0.0f;
+      }
+    }
+    __syncwarp();
+    // logits: lane k < C owns class k (4 chains over the features)
+    float l = -FLT_MAX;
+    if (lane < C) {
+      float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
+      int o = 0;
+      const float* wr = w2s + lane * pw;
+      for (; o + 3 < nf; o += 4) {
+        a0 += wr[o] * feat[o];
+        a1 += wr[o + 1] * feat[o + 1];
+        a2 += wr[o + 2] * feat[o + 2];
+        a3 += wr[o + 3] * feat[o + 3];
+      }
+      for (; o < nf; ++o) a0 += wr[o] * feat[o];
+      l = ((a0 + a1) + (a2 + a3)) + b2s[lane];
+    }
+    // argmax(pr) = argmax(logits), lowest index on ties (tensor.hpp:57-63)
+    float m = l;
+    am = lane < C ? lane : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, m, o);
+      const int oa = __shfl_xor_sync(0xffffffffu, am, o);
+      if (ov > m || (ov == m && oa < am)) {
+        m = ov;
+        am = oa;
+      }
+    }
+    // softmax (losses.cpp:35-46) and the selector: sum_k Ws1[j][k] pr_k = (sum_k Ws1[j][k] e_k) / S
+    const float e = lane < C ? expf(l - m) : 0.0f;
+    const float S = warp_sum(e);
+    float t = 0.0f;
+    for (int k = 0; k < C; ++k) {
+      const float ek = __shfl_sync(0xffffffffu, e, k);
+      if (lane < 16) t += ws1[lane * C + k] * ek;
+    }
+    float h = 0.0f;
+    if (lane < 16) {
+      const float a = t / S + sel[lane];
+      h = (a > 0.0f ? a : 0.0f) * sel[16 + lane];
+    }
+    float hj[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) hj[j] = __shfl_sync(0xffffffffu, h, j);
+    if (lane == 0) {
+      float z = p.bs2;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) z += hj[j];
+      if (z >= 0.0f) {  // branch-stable sigmoid (losses.cpp:26-33)
+        q = 1.0f / (1.0f + expf(-z));
+      } else {
+        const float ez = expf(z);
+        q = ez / (1.0f + ez);
+      }
+      hit = static_cast<double>(q) >= p.delta ? 1 : 0;  // inclusive threshold
+      p.prob[r] = q;
+      p.hit[r] = hit;
+      p.label[r] = am;
+    }
+    if (p.pr_out && lane < C) p.pr_out[static_cast<long long>(r) * C + lane] = e / S;
+    if (p.logits_out && lane < C) p.logits_out[static_cast<long long>(r) * C + lane] = l;
+  }
+  if (!p.ex.arrive) return;
+  const ExitParams& ex = p.ex;
+  if (!(ex.rows_dst_hi && !ex.shadow)) {
+    exit_tail(ex, n, p.prob, p.hit, p.label);  // ordered compaction by the last CTA (every thread)
+    return;
+  }
+  // block-MLP compact mode: the row's warp records a first hit or appends the
+  // miss at an atomic position and copies its activations (serving.cpp:112-121)
+  if (r >= n) return;
+  int pos = -1;
+  if (lane == 0) {
+    const int id = ex.ids_in[r];
+    if (ex.probs_out) ex.probs_out[id] = q;
+    if (ex.labels_out) ex.labels_out[id] = am;
+    if (hit) {
+      if (ex.exit_layer[id] == 0) {
+        ex.exit_layer[id] = ex.layer;
+        ex.served[id] = am;
+        ex.exit_ns[id] = globaltimer();
+      }
+    } else {
+      pos = atomicAdd(ex.count_out, 1);
+      ex.ids_out[pos] = id;
+      if (ex.src_rows_out) ex.src_rows_out[pos] = r;
+    }
+  }
+  pos = __shfl_sync(0xffffffffu, pos, 0);
+  if (pos < 0) return;
+  const bool held = rvec && ex.rows_src_hi == p.row_hi && ex.rows_src_lo == p.row_lo && ex.row_elems == p.D &&
+                    p.row_stride == ex.row_elems;
+  if (held) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int vi = lane + 32 * j;
+      if (vi < nv) {
+        reinterpret_cast<uint4*>(ex.rows_dst_hi + static_cast<long long>(pos) * ex.row_elems)[vi] = hv[j];
+        if (ex.rows_src_lo) reinterpret_cast<uint4*>(ex.rows_dst_lo + static_cast<long long>(pos) * ex.row_elems)[vi] = lv[j];
+      }
+    }
+    return;
+  }
+  const long long nvr = ex.row_elems / 8;
+  const uint4* sh = reinterpret_cast<const uint4*>(ex.rows_src_hi + static_cast<long long>(r) * ex.row_elems);
+  uint4* dh = reinterpret_cast<uint4*>(ex.rows_dst_hi + static_cast<long long>(pos) * ex.row_elems);
+  for (long long i = lane; i < nvr; i += 32) dh[i] = __ldg(sh + i);
+  if (ex.rows_src_lo) {
+    const uint4* sl = reinterpret_cast<const uint4*>(ex.rows_src_lo + static_cast<long long>(r) * ex.row_elems);
+    uint4* dl = reinterpret_cast<uint4*>(ex.rows_dst_lo + static_cast<long long>(pos) * ex.row_elems);
+    for (long long i = lane; i < nvr; i += 32) dl[i] = __ldg(sl + i);
+  }
+}
+
 // ------------------------------------------------------------ wide lookup
 // Pool(C) caches with many classes (ImageNet heads: C up to 2048, 1000
 // classes) in ONE persistent launch instead of three (GAP bins, logits GEMM,
@@ -1840,9 +2126,36 @@ void launch_wide_lookup(const CacheHeadParams& h, float* feats, float* logits, i
   launch_pdl(wide_lookup_kernel, dim3(grid), dim3(kLk), smem, s, q);
 }
 
+// Warp-per-row head eligibility: <= 32 classes, features from the row, FC(h)
+// partials or pooled bins (not the fused GAP partials, not the Conv(k,s)
+// chunk partials), shared memory within bounds; LCB_BLOCK_HEADS=1 keeps the
+// block-per-row kernel (A/B).
+static bool warp_head_ok(const CacheHeadParams& p, int max_rows) {
+  const char* env = std::getenv("LCB_BLOCK_HEADS");  // (read per launch build: tests switch it)
+  const int mode = env ? std::atoi(env) : 0;
+  if (mode == 1 || p.classes > 32 || p.gap || p.pre_logits) return false;
+  const bool direct = p.row_hi != nullptr;
+  if (!direct && p.family == 2) return false;
+  if (direct && p.family == 0) return false;
+  // a warp per row has a longer per-row latency than 16 warps per row: it wins
+  // once there are more rows than a CTA-per-row launch keeps resident (C1:
+  // b256 202 vs 217 us/step, b16384 2329 vs 658 us/step; LCB_BLOCK_HEADS=2 forces it)
+  if (max_rows < 1024 && mode != 2) return false;
+  if (direct && p.D > 8192) return false;
+  return warp_head_smem_floats(p) * sizeof(float) <= 160 * 1024;
+}
+
 void launch_cache_head(const CacheHeadParams& p_in, int max_rows, cudaStream_t s) {
   if (max_rows <= 0) return;
   CacheHeadParams p = p_in;
+  if (warp_head_ok(p, max_rows)) {
+    static std::atomic<unsigned long long> wattr{0};
+    if (first_on_device(wattr))
+      cudaFuncSetAttribute(warp_head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    launch_pdl(warp_head_kernel, dim3((max_rows + kWhWarps - 1) / kWhWarps), dim3(kWhWarps * 32),
+               warp_head_smem_floats(p) * sizeof(float), s, p);
+    return;
+  }
   if (p.classes > 32 && p.family != 2 && p.fc_scratch) {
     // Many classes: one batched split-K logits GEMM, then the per-row head.
     if (p.family == 1)

@@ -183,15 +183,20 @@ def test_lookup_mlp_taps(arch):
             assert got["label"][i] == O.argmax(pr)
 
 
+@pytest.mark.parametrize("heads", ["auto", "warp"])
 @pytest.mark.parametrize("classes,widths", [(10, [64, 128, 64]), (100, [96, 100, 64])])
-def test_mlp_direct_heads_vs_oracle(classes, widths):
+def test_mlp_direct_heads_vs_oracle(classes, widths, heads, monkeypatch):
     """Block-MLP serving where the heads read the request's row themselves
     (Pool(w) / Conv(k,s) predictor inside the head, static weights staged
     before the programmatic-launch wait, the row held in registers for the
     compacted copy) and the FC(h) head, against the oracle's serve_one, in
     shadow and compact mode: 10 classes (direct Pool head, 16-byte row
     vectors), and 100 classes with a 100-wide tap (Pool(w) through the
-    batched logits GEMM, Conv(k,s) direct with the scalar row path)."""
+    batched logits GEMM, Conv(k,s) direct with the scalar row path). heads =
+    "warp" forces the warp-per-row head kernel (LCB_BLOCK_HEADS=2), which the
+    engine otherwise picks only for batch capacities >= 1024."""
+    if heads == "warp":
+        monkeypatch.setenv("LCB_BLOCK_HEADS", "2")
     m = lcb.make_base_model(48, classes, widths, 3, 13)
     archs = ["Pool(32)", "Conv(3,1)", "FC(64)"]
     vs = [lcb.build_variant(l + 1, 0, a, m.tap_dim(l + 1), classes, 17 + l) for l, a in enumerate(archs)]
