@@ -1200,20 +1200,28 @@ __global__ void __launch_bounds__(kWhWarps * 32) warp_head_kernel(CacheHeadParam
       }
     }
     __syncwarp();
-    // logits: lane k < C owns class k (4 chains over the features)
+    // logits: lane = (class k, slice g), G = 32 / C slices of the features
+    // (every lane busy for C <= 16), 2 chains per lane; the slices' sums are
+    // gathered into lane k in ascending g (fixed order)
     float l = -FLT_MAX;
-    if (lane < C) {
-      float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
-      int o = 0;
-      const float* wr = w2s + lane * pw;
-      for (; o + 3 < nf; o += 4) {
-        a0 += wr[o] * feat[o];
-        a1 += wr[o + 1] * feat[o + 1];
-        a2 += wr[o + 2] * feat[o + 2];
-        a3 += wr[o + 3] * feat[o + 3];
+    {
+      const int G = 32 / C;
+      const int k = lane % C, g = lane / C;
+      float a0 = 0.0f, a1 = 0.0f;
+      if (g < G) {
+        const int o0 = (nf * g) / G, o1 = (nf * (g + 1)) / G;
+        const float* wr = w2s + k * pw;
+        int o = o0;
+        for (; o + 1 < o1; o += 2) {
+          a0 += wr[o] * feat[o];
+          a1 += wr[o + 1] * feat[o + 1];
+        }
+        if (o < o1) a0 += wr[o] * feat[o];
       }
-      for (; o < nf; ++o) a0 += wr[o] * feat[o];
-      l = ((a0 + a1) + (a2 + a3)) + b2s[lane];
+      float part = a0 + a1;
+      float sum = part;
+      for (int gg = 1; gg < G; ++gg) sum += __shfl_sync(0xffffffffu, part, lane + gg * C < 32 ? lane + gg * C : lane);
+      if (lane < C) l = sum + b2s[lane];
     }
     // argmax(pr) = argmax(logits), lowest index on ties (tensor.hpp:57-63)
     float m = l;
