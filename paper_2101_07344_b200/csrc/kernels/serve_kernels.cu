@@ -2147,8 +2147,8 @@ static bool warp_head_ok(const CacheHeadParams& p, int max_rows) {
   if (direct && p.family == 0) return false;
   // a warp per row has a longer per-row latency than 16 warps per row: it wins
   // once there are more rows than a CTA-per-row launch keeps resident (C1:
-  // b256 202 vs 217 us/step, b16384 2329 vs 658 us/step; LCB_BLOCK_HEADS=2 forces it)
-  if (max_rows < 1024 && mode != 2) return false;
+  // b256 202 vs 204 us/step, b512 226 vs 214, b16384 2329 vs 533; LCB_BLOCK_HEADS=2 forces it)
+  if (max_rows < 512 && mode != 2) return false;
   if (direct && p.D > 8192) return false;
   return warp_head_smem_floats(p) * sizeof(float) <= 160 * 1024;
 }

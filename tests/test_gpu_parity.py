@@ -194,7 +194,7 @@ def test_mlp_direct_heads_vs_oracle(classes, widths, heads, monkeypatch):
     vectors), and 100 classes with a 100-wide tap (Pool(w) through the
     batched logits GEMM, Conv(k,s) direct with the scalar row path). heads =
     "warp" forces the warp-per-row head kernel (LCB_BLOCK_HEADS=2), which the
-    engine otherwise picks only for batch capacities >= 1024."""
+    engine otherwise picks only for batch capacities >= 512."""
     if heads == "warp":
         monkeypatch.setenv("LCB_BLOCK_HEADS", "2")
     m = lcb.make_base_model(48, classes, widths, 3, 13)
