@@ -1167,6 +1167,28 @@ __global__ void __launch_bounds__(kWhWarps * 32) warp_head_kernel(CacheHeadParam
           feat[o] = y > 0.0f ? y : 0.0f;
         }
       }
+    } else if (p.gap) {  // Pool(C) = GAP from the conv's fused partials gap[image][segs][C], C % 4 == 0
+      const long long img = p.gap_ids ? p.gap_ids[r] : r;
+      const float4* s4 = reinterpret_cast<const float4*>(p.gap + img * p.gap_segs * nf);
+      const int C4 = nf >> 2;
+      for (int j = lane; j < C4; j += 32) {
+        float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
+        int sg = 0;
+        for (; sg + 4 <= p.gap_segs; sg += 4) {
+          add4(a0, __ldg(s4 + static_cast<long long>(sg) * C4 + j));
+          add4(a1, __ldg(s4 + static_cast<long long>(sg + 1) * C4 + j));
+          add4(a2, __ldg(s4 + static_cast<long long>(sg + 2) * C4 + j));
+          add4(a3, __ldg(s4 + static_cast<long long>(sg + 3) * C4 + j));
+        }
+        for (; sg < p.gap_segs; ++sg) add4(a0, __ldg(s4 + static_cast<long long>(sg) * C4 + j));
+        add4(a0, a1);
+        add4(a2, a3);
+        add4(a0, a2);
+        feat[4 * j] = a0.x * p.gap_inv;
+        feat[4 * j + 1] = a0.y * p.gap_inv;
+        feat[4 * j + 2] = a0.z * p.gap_inv;
+        feat[4 * j + 3] = a0.w * p.gap_inv;
+      }
     } else if (p.family == 1) {  // pooled bins [rows][feat]
       for (int o = lane; o < nf; o += 32) feat[o] = __ldg(p.feats + static_cast<long long>(r) * nf + o);
     } else {  // FC(h): hidden = relu(b1 + sum of the split-K partials, ascending split)
@@ -2141,14 +2163,16 @@ void launch_wide_lookup(const CacheHeadParams& h, float* feats, float* logits, i
 static bool warp_head_ok(const CacheHeadParams& p, int max_rows) {
   const char* env = std::getenv("LCB_BLOCK_HEADS");  // (read per launch build: tests switch it)
   const int mode = env ? std::atoi(env) : 0;
-  if (mode == 1 || p.classes > 32 || p.gap || p.pre_logits) return false;
+  if (mode == 1 || p.classes > 32 || p.pre_logits) return false;
+  if (p.gap && (p.family != 1 || (p.feat & 3) != 0)) return false;
   const bool direct = p.row_hi != nullptr;
   if (!direct && p.family == 2) return false;
   if (direct && p.family == 0) return false;
   // a warp per row has a longer per-row latency than 16 warps per row: it wins
   // once there are more rows than a CTA-per-row launch keeps resident (C1:
   // b256 202 vs 204 us/step, b512 226 vs 214, b16384 2329 vs 533; LCB_BLOCK_HEADS=2 forces it)
-  if (max_rows < 512 && mode != 2) return false;
+  // (fused-GAP heads read a few KB per row: the warp wins at any batch — R18 b256 355.8K -> 360.7K req/s)
+  if (max_rows < 512 && !p.gap && mode != 2) return false;
   if (direct && p.D > 8192) return false;
   return warp_head_smem_floats(p) * sizeof(float) <= 160 * 1024;
 }
