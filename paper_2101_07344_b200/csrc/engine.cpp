@@ -222,6 +222,7 @@ Engine::Engine(int device, const BaseModel& model, std::vector<CacheVariant> var
   stacked_ = !(ns && ns[0] == '1');
   if (const char* km = std::getenv("LCB_KS_MIN_STEPS")) ks_min_steps_ = std::atoi(km);
   if (const char* km = std::getenv("LCB_MLP_KS_MIN_STEPS")) mlp_ks_min_steps_ = std::atoi(km);
+  if (const char* u = std::getenv("LCB_UNORDERED_IDS")) unordered_ids_ = std::atoi(u) != 0;
   if (const char* wp = std::getenv("LCB_NO_WPREFETCH")) wprefetch_ = !(wp[0] == '1');
   const char* nh = std::getenv("LCB_HALO");  // opt-in: not yet faster than the per-tap loads
   halo_ = nh && nh[0] == '1';
@@ -767,6 +768,7 @@ ExitParams Engine::exit_params(int layer, bool shadow, const int* ids_in, int* i
   e.ids_out = ids_out;
   e.src_rows_out = src_rows_out;
   e.count_out = count_out;
+  e.unordered = (!shadow && unordered_ids_) ? 1 : 0;
   return e;
 }
 

@@ -1293,6 +1293,39 @@ __global__ void __launch_bounds__(kWhWarps * 32) warp_head_kernel(CacheHeadParam
   }
   if (!p.ex.arrive) return;
   const ExitParams& ex = p.ex;
+  if (!ex.rows_dst_hi && ex.unordered && !ex.shadow) {
+    // first-hit records per row; the CTA's misses take one atomic for their positions
+    __shared__ int miss_s[kWhWarps], base_s;
+    const bool miss = r < n && !__shfl_sync(0xffffffffu, hit, 0);
+    int id = 0;
+    if (lane == 0) {
+      if (r < n) {
+        id = ex.ids_in[r];
+        if (ex.probs_out) ex.probs_out[id] = q;
+        if (ex.labels_out) ex.labels_out[id] = am;
+        if (hit && ex.exit_layer[id] == 0) {
+          ex.exit_layer[id] = ex.layer;
+          ex.served[id] = am;
+          ex.exit_ns[id] = globaltimer();
+        }
+      }
+      miss_s[warp] = miss ? 1 : 0;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int tot = 0;
+      for (int w = 0; w < kWhWarps; ++w) tot += miss_s[w];
+      base_s = tot ? atomicAdd(ex.count_out, tot) : 0;
+    }
+    __syncthreads();
+    if (miss && lane == 0) {
+      int pos = base_s;
+      for (int w = 0; w < warp; ++w) pos += miss_s[w];
+      ex.ids_out[pos] = id;
+      if (ex.src_rows_out) ex.src_rows_out[pos] = r;
+    }
+    return;
+  }
   if (!(ex.rows_dst_hi && !ex.shadow)) {
     exit_tail(ex, n, p.prob, p.hit, p.label);  // ordered compaction by the last CTA (every thread)
     return;

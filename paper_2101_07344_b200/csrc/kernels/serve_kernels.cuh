@@ -54,6 +54,10 @@ struct ExitParams {
   __nv_bfloat16* rows_dst_hi;
   __nv_bfloat16* rows_dst_lo;
   long long row_elems;
+  // compact mode without row copies (CNN taps): 1 = the warp-per-row head
+  // appends misses at atomic positions (one atomic per CTA) instead of the
+  // last CTA's ordered scan; survivors' order then varies, no request's values do
+  int unordered;
 };
 
 // Per-row cache head inputs (one of three predictor families).
