@@ -223,6 +223,7 @@ Engine::Engine(int device, const BaseModel& model, std::vector<CacheVariant> var
   if (const char* km = std::getenv("LCB_KS_MIN_STEPS")) ks_min_steps_ = std::atoi(km);
   if (const char* km = std::getenv("LCB_MLP_KS_MIN_STEPS")) mlp_ks_min_steps_ = std::atoi(km);
   if (const char* u = std::getenv("LCB_UNORDERED_IDS")) unordered_ids_ = std::atoi(u) != 0;
+  if (const char* u = std::getenv("LCB_SCAN_COMPACTION")) scan_compaction_ = std::atoi(u) != 0;
   if (const char* wp = std::getenv("LCB_NO_WPREFETCH")) wprefetch_ = !(wp[0] == '1');
   const char* nh = std::getenv("LCB_HALO");  // opt-in: not yet faster than the per-tap loads
   halo_ = nh && nh[0] == '1';
@@ -276,7 +277,10 @@ void Engine::build_weights() {
   ck(cudaMallocHost(&h_batch_, sizeof(int)), "cudaMallocHost");
   d_ids_ = static_cast<int*>(dalloc(static_cast<size_t>(L + 1) * B * sizeof(int)));
   d_src_ = static_cast<int*>(dalloc(static_cast<size_t>(L + 1) * B * sizeof(int)));
-  d_counts_ = static_cast<int*>(dalloc(static_cast<size_t>(L + 2) * sizeof(int)));
+  d_counts_ = static_cast<int*>(dalloc(static_cast<size_t>(L + 4) * sizeof(int)));  // [L + 2] = serve epoch
+  ck(cudaMemsetAsync(d_counts_, 0, static_cast<size_t>(L + 4) * sizeof(int), stream_), "memset");
+  d_scan_ = static_cast<unsigned long long*>(dalloc(static_cast<size_t>(L + 1) * kScanMaxCtas * 8));
+  ck(cudaMemsetAsync(d_scan_, 0, static_cast<size_t>(L + 1) * kScanMaxCtas * 8, stream_), "memset");
   d_exit_ = static_cast<int*>(dalloc(static_cast<size_t>(B) * sizeof(int)));
   d_served_ = static_cast<int*>(dalloc(static_cast<size_t>(B) * sizeof(int)));
   d_base_ = static_cast<int*>(dalloc(static_cast<size_t>(B) * sizeof(int)));
@@ -769,6 +773,10 @@ ExitParams Engine::exit_params(int layer, bool shadow, const int* ids_in, int* i
   e.src_rows_out = src_rows_out;
   e.count_out = count_out;
   e.unordered = (!shadow && unordered_ids_) ? 1 : 0;
+  if (scan_compaction_) {
+    e.scan_agg = d_scan_ + static_cast<size_t>(layer) * kScanMaxCtas;
+    e.epoch = d_counts_ + model_.num_blocks + 2;
+  }
   return e;
 }
 

@@ -244,7 +244,9 @@ class Engine {
   bool wide_lookup_ = true;  // LCB_NO_WIDE_LOOKUP=1: GAP bins + logits GEMM + head as three launches
   bool stacked_ = true;
   int ks_min_steps_ = 0;
-  bool unordered_ids_ = false;  // CNN compact mode: atomic survivor appends in the warp heads (LCB_UNORDERED_IDS)
+  bool unordered_ids_ = false;
+  bool scan_compaction_ = true;  // warp heads: ordered compaction by look-back scan (LCB_SCAN_COMPACTION=0: last-CTA scan)
+  unsigned long long* d_scan_ = nullptr;  // [L + 1][kScanMaxCtas] look-back records  // CNN compact mode: atomic survivor appends in the warp heads (LCB_UNORDERED_IDS)
   int mlp_ks_min_steps_ = 8;  // block-MLP layers: K-steps per split at least (LCB_MLP_KS_MIN_STEPS; C1 sweep 0/2/4/8/12/16/24: 8 best)
   bool wprefetch_ = true;  // LCB_NO_WPREFETCH=1: no L2 prefetch of conv weights before the PDL wait  // LCB_KS_MIN_STEPS: split-K floor of K-steps per split (CNN convs)  // LCB_NO_STACKED=1: three MMAs per bf16x3 K16 group everywhere
   bool halo_ = false;  // LCB_HALO=1: stride-1 convs load one padded-row halo slab per channel chunk  // LCB_UNFUSED_LOOKUP=1: gap_bins + head + exit_compact as three launches

@@ -1293,6 +1293,56 @@ __global__ void __launch_bounds__(kWhWarps * 32) warp_head_kernel(CacheHeadParam
   }
   if (!p.ex.arrive) return;
   const ExitParams& ex = p.ex;
+  if (!ex.rows_dst_hi && ex.scan_agg && !ex.unordered && !ex.shadow && gridDim.x <= kScanMaxCtas) {
+    // ordered compaction in one pass: this CTA's rows are positions
+    // [prefix, prefix + misses) where prefix = the misses of CTAs 0..b-1
+    // (all co-resident: the grid is at most 2 CTAs per SM)
+    __shared__ int miss_s[kWhWarps], red_s[kWhWarps], tot_s;
+    const bool miss = r < n && !__shfl_sync(0xffffffffu, hit, 0);
+    int id = 0;
+    if (lane == 0) {
+      if (r < n) {
+        id = ex.ids_in[r];
+        if (ex.probs_out) ex.probs_out[id] = q;
+        if (ex.labels_out) ex.labels_out[id] = am;
+        if (hit && ex.exit_layer[id] == 0) {
+          ex.exit_layer[id] = ex.layer;
+          ex.served[id] = am;
+          ex.exit_ns[id] = globaltimer();
+        }
+      }
+      miss_s[warp] = miss ? 1 : 0;
+    }
+    __syncthreads();
+    const unsigned long long ep = static_cast<unsigned long long>(static_cast<unsigned>(*ex.epoch)) << 32;
+    if (tid == 0) {
+      int tot = 0;
+      for (int w = 0; w < kWhWarps; ++w) tot += miss_s[w];
+      tot_s = tot;
+      st_release_u64(ex.scan_agg + blockIdx.x, ep | static_cast<unsigned long long>(tot + 1));
+    }
+    int acc = 0;
+    for (int j = tid; j < static_cast<int>(blockIdx.x); j += blockDim.x) {
+      unsigned long long v;
+      do {
+        v = ld_acquire_u64(ex.scan_agg + j);
+      } while ((v & 0xffffffff00000000ull) != ep);
+      acc += static_cast<int>(v & 0xffffffffull) - 1;
+    }
+    acc = __reduce_add_sync(0xffffffffu, acc);
+    if (lane == 0) red_s[warp] = acc;
+    __syncthreads();
+    int prefix = 0;
+    for (int w = 0; w < kWhWarps; ++w) prefix += red_s[w];
+    if (miss && lane == 0) {
+      int pos = prefix;
+      for (int w = 0; w < warp; ++w) pos += miss_s[w];
+      ex.ids_out[pos] = id;
+      if (ex.src_rows_out) ex.src_rows_out[pos] = r;
+    }
+    if (blockIdx.x == gridDim.x - 1 && tid == 0) *ex.count_out = prefix + tot_s;
+    return;
+  }
   if (!ex.rows_dst_hi && ex.unordered && !ex.shadow) {
     // first-hit records per row; the CTA's misses take one atomic for their positions
     __shared__ int miss_s[kWhWarps], base_s;
@@ -2070,8 +2120,10 @@ __global__ void init_batch_kernel(int B, int* batch_out, int max_batch, int* ids
     if (batch_out) *batch_out = B;
     if (rows_out) *rows_out = B * rows_mult;
   }
-  // per-layer survivor counts start at zero (atomic row compaction appends to them)
+  // per-layer survivor counts start at zero (atomic row compaction appends to them);
+  // count0[L + 2] is the serve epoch that tags the heads' look-back scan records
   if (blockIdx.x == 0 && threadIdx.x >= 1 && threadIdx.x <= L) count0[threadIdx.x] = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) count0[L + 2] += 1;
 }
 
 __global__ void __launch_bounds__(256) confusion_kernel(const float* probs, const int* labels, const int* base_pred,
@@ -2214,6 +2266,8 @@ void launch_cache_head(const CacheHeadParams& p_in, int max_rows, cudaStream_t s
   if (max_rows <= 0) return;
   CacheHeadParams p = p_in;
   if (warp_head_ok(p, max_rows)) {
+    // the look-back scan needs every CTA of the grid resident: <= 2 per SM by shared memory
+    if (warp_head_smem_floats(p) * sizeof(float) > 100 * 1024) p.ex.scan_agg = nullptr;
     static std::atomic<unsigned long long> wattr{0};
     if (first_on_device(wattr))
       cudaFuncSetAttribute(warp_head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);

@@ -58,7 +58,14 @@ struct ExitParams {
   // appends misses at atomic positions (one atomic per CTA) instead of the
   // last CTA's ordered scan; survivors' order then varies, no request's values do
   int unordered;
+  // compact mode without row copies, warp heads: ordered compaction by a
+  // single-pass look-back scan (each CTA publishes its miss count tagged with
+  // the serve's epoch, then sums its predecessors') instead of the last CTA's
+  // scan; nullable. scan_agg: [head grid] per cache layer (grid <= kScanMaxCtas)
+  unsigned long long* scan_agg;
+  const int* epoch;
 };
+constexpr int kScanMaxCtas = 296;  // = 2 CTAs per SM: every CTA of the head grid co-resident
 
 // Per-row cache head inputs (one of three predictor families).
 struct CacheHeadParams {
