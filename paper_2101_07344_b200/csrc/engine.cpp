@@ -114,6 +114,15 @@ struct DevCache {
   // the tap conv also finishes the lookup: features only (conv_feat, the head
   // runs separately on them) or the whole head + exit (conv_head)
   bool conv_feat = false, conv_head = false;
+  // block-MLP FC(h) caches: the hidden layer rides the next block's GEMM
+  // ([W_next; W1] concatenated along N, one launch over the tap's rows); the
+  // next block's output for those rows lands in `spec` and the head's
+  // compaction copies the survivors' rows on (Engine::mlp_fuse_hidden_)
+  bool fused = false;
+  Planes fw;             // [next.outp + hp][next.inp]
+  float* fb = nullptr;   // [next.outp + hp]: next block's bias, zeros
+  int fn1 = 0, fBN = 64;
+  Planes spec;           // [max_batch][next.outp]
   // lookup-only step list
   std::vector<Step> lookup_steps;
 };
@@ -223,6 +232,7 @@ Engine::Engine(int device, const BaseModel& model, std::vector<CacheVariant> var
   if (const char* km = std::getenv("LCB_KS_MIN_STEPS")) ks_min_steps_ = std::atoi(km);
   if (const char* km = std::getenv("LCB_MLP_KS_MIN_STEPS")) mlp_ks_min_steps_ = std::atoi(km);
   if (const char* u = std::getenv("LCB_UNORDERED_IDS")) unordered_ids_ = std::atoi(u) != 0;
+  if (const char* u = std::getenv("LCB_MLP_FUSE_HIDDEN")) mlp_fuse_hidden_ = std::atoi(u) != 0;
   if (const char* u = std::getenv("LCB_SCAN_COMPACTION")) scan_compaction_ = std::atoi(u) != 0;
   if (const char* wp = std::getenv("LCB_NO_WPREFETCH")) wprefetch_ = !(wp[0] == '1');
   const char* nh = std::getenv("LCB_HALO");  // opt-in: not yet faster than the per-tap loads
@@ -572,11 +582,39 @@ void Engine::build_weights() {
     caches_.push_back(std::move(c));
   }
   lk_tap_ = alloc_planes(static_cast<size_t>(B) * round_up(max_tap_storage, 64));
+  if (model_.family == "mlp" && mlp_fuse_hidden_) {
+    for (auto& cp : caches_) {
+      DevCache& c = *cp;
+      if (c.family != 0 || c.layer >= model_.num_blocks) continue;
+      const DevFC& nf = mlp_fc_[static_cast<size_t>(c.layer)];  // the next block's FC
+      if (nf.inp != c.Dk) continue;
+      const int n1 = nf.outp, nt = n1 + c.hp;
+      int bn = tc_conv_pick_bn(nt, prec_ == kPrecX3 ? 3 : 1);
+      if (n1 % bn != 0 || c.hp % bn != 0) bn = 64;
+      c.fw = alloc_planes(static_cast<size_t>(nt) * nf.inp, false);
+      const size_t e1 = static_cast<size_t>(n1) * nf.inp, e2 = static_cast<size_t>(c.hp) * c.Dk;
+      ck(cudaMemcpyAsync(c.fw.hi, nf.w.hi, e1 * 2, cudaMemcpyDeviceToDevice, stream_), "fused W");
+      ck(cudaMemcpyAsync(c.fw.hi + e1, c.W1.hi, e2 * 2, cudaMemcpyDeviceToDevice, stream_), "fused W");
+      if (c.fw.lo) {
+        ck(cudaMemcpyAsync(c.fw.lo, nf.w.lo, e1 * 2, cudaMemcpyDeviceToDevice, stream_), "fused W");
+        ck(cudaMemcpyAsync(c.fw.lo + e1, c.W1.lo, e2 * 2, cudaMemcpyDeviceToDevice, stream_), "fused W");
+      }
+      c.fb = static_cast<float*>(dalloc(static_cast<size_t>(nt) * sizeof(float)));
+      ck(cudaMemsetAsync(c.fb, 0, static_cast<size_t>(nt) * sizeof(float), stream_), "fused b");
+      ck(cudaMemcpyAsync(c.fb, nf.b, static_cast<size_t>(n1) * sizeof(float), cudaMemcpyDeviceToDevice, stream_),
+         "fused b");
+      c.spec = alloc_planes(static_cast<size_t>(B) * n1, false);
+      c.fn1 = n1;
+      c.fBN = bn;
+      c.ks = 1;  // the hidden layer's partials: one split (K = the tap width)
+      c.fused = true;
+    }
+  }
 }
 
 // ------------------------------------------------------------------ lookups
 void Engine::add_lookup_steps(std::vector<Step>& steps, DevCache& c, const TapView& tap, int max_rows,
-                              bool stage_gather, bool fused_gap, const ExitParams* ex) {
+                              bool stage_gather, bool fused_gap, const ExitParams* ex, bool hidden_done) {
   DevCache* cp = &c;
   const long long L2 = model_.num_blocks + 2;
   const int cidx = (tap.count >= d_counts_ && tap.count < d_counts_ + L2) ? static_cast<int>(tap.count - d_counts_) : -1;
@@ -652,6 +690,8 @@ void Engine::add_lookup_steps(std::vector<Step>& steps, DevCache& c, const TapVi
                      },
                      2, 1, cidx, 2.0 * (static_cast<double>(c.out_dim) * c.kernel + static_cast<double>(c.out_dim) * c.classes),
                      tap_bytes});
+  } else if (hidden_done) {
+    // FC(h) whose hidden layer the next block's GEMM already produced (fused serve)
   } else {
     // FC(h): hidden = W1 . tap as a split-K tensor-core GEMM over the rows.
     const __nv_bfloat16* a_hi = tap.hi;
@@ -832,17 +872,18 @@ void Engine::build_mlp_steps(std::vector<Step>& steps, bool shadow, bool stamps)
   Planes cur = mlp_in_;
   int* cur_ids = ids;
   int* cur_count = counts;
-  for (int b = 0; b < L; ++b) {
-    const DevFC& f = mlp_fc_[static_cast<size_t>(b)];
-    Planes act = mlp_act_[static_cast<size_t>(b)];
+  // one plain tcgen05 GEMM over the rows: Cout columns of W (K = inp) from A;
+  // with fuse != nullptr the columns >= fuse->fn1 are the FC(h) cache's hidden
+  // layer (fp32 partials into its feats), the rest the block's output
+  auto gemm_step = [&](const Planes& A, int inp, const Planes& W, int cout, int BN, const float* bias,
+                       const Planes& out, int out_ld, DevCache* fuse, double flops, double bytes) {
     auto prm = std::make_shared<TcConvParams>();
     std::memset(prm.get(), 0, sizeof(TcConvParams));
-    const int BN = tc_conv_pick_bn(f.outp, x3 ? 3 : 1);
-    bool ok = encode_act_map(&prm->tmA[0], cur.hi, f.inp, B, 1, 1, 1, 128, 1) &&
-              encode_weight_map(&prm->tmB[0], f.w.hi, f.inp, f.outp, BN);
+    bool ok = encode_act_map(&prm->tmA[0], A.hi, inp, B, 1, 1, 1, 128, 1) &&
+              encode_weight_map(&prm->tmB[0], W.hi, inp, cout, BN);
     if (x3)
-      ok = ok && encode_act_map(&prm->tmA[1], cur.lo, f.inp, B, 1, 1, 1, 128, 1) &&
-           encode_weight_map(&prm->tmB[1], f.w.lo, f.inp, f.outp, BN);
+      ok = ok && encode_act_map(&prm->tmA[1], A.lo, inp, B, 1, 1, 1, 128, 1) &&
+           encode_weight_map(&prm->tmB[1], W.lo, inp, cout, BN);
     if (!ok) throw CudaFailure("engine: TMA descriptor encode failed (mlp)");
     prm->plain = 1;
     prm->Ho = 1;
@@ -851,34 +892,64 @@ void Engine::build_mlp_steps(std::vector<Step>& steps, bool shadow, bool stamps)
     prm->wb = 128;
     prm->ipt = 1;
     prm->tiles_h = 1;
-    prm->C = f.inp;
+    prm->C = inp;
     prm->ntaps = 1;
     prm->segs = x3 ? 3 : 1;
-    prm->Cout = f.outp;
+    prm->Cout = cout;
     prm->ksplit = 1;
-    prm->ks_max = 32;
-    prm->ks_min_steps = mlp_ks_min_steps_;
-    prm->ws = ws_;
-    prm->ws_counters = ws_counters_;
-    split_prms_.push_back(prm);
+    if (fuse) {
+      prm->ks_max = 1;  // (K = one tap: 1-8 steps)
+      prm->mix_n1 = fuse->fn1;
+      prm->mix_ld = fuse->hp;
+      prm->out_ld = out_ld;
+      prm->out_f32 = fuse->feats;
+      prm->rows_total = B;
+    } else {
+      prm->ks_max = 32;
+      prm->ks_min_steps = mlp_ks_min_steps_;
+      prm->ws = ws_;
+      prm->ws_counters = ws_counters_;
+      split_prms_.push_back(prm);
+    }
     prm->count = cur_count;
     prm->count_static = B;
     prm->mode = 0;
-    prm->shift = f.b;
+    prm->shift = bias;
     prm->relu = 1;
-    prm->out_hi = act.hi;
-    prm->out_lo = act.lo;
+    prm->out_hi = out.hi;
+    prm->out_lo = out.lo;
     prm->staged_store = staged_store_ ? 1 : 0;
     const int sms = num_sms_;
     steps.push_back({[prm, BN, sms](cudaStream_t s) { ck(tc_conv_launch(*prm, BN, sms, s), "tc_conv (mlp)"); }, 1, 1,
-                     static_cast<int>(cur_count - d_counts_), 2.0 * f.in * f.out,
-                     (x3 ? 4.0 : 2.0) * (static_cast<double>(f.inp) + f.outp)});
+                     static_cast<int>(cur_count - d_counts_), flops, bytes});
+  };
+  std::vector<char> gemm_done(static_cast<size_t>(L), 0);
+  for (int b = 0; b < L; ++b) {
+    const DevFC& f = mlp_fc_[static_cast<size_t>(b)];
+    Planes act = mlp_act_[static_cast<size_t>(b)];
     const int layer = b + 1;
-    if (shadow) tap_step_end_[static_cast<size_t>(layer)] = static_cast<int>(steps.size());
+    if (!gemm_done[static_cast<size_t>(b)]) {
+      gemm_step(cur, f.inp, f.w, f.outp, tc_conv_pick_bn(f.outp, x3 ? 3 : 1), f.b, act, 0, nullptr,
+                2.0 * f.in * f.out, (x3 ? 4.0 : 2.0) * (static_cast<double>(f.inp) + f.outp));
+      if (shadow) tap_step_end_[static_cast<size_t>(layer)] = static_cast<int>(steps.size());
+    }
     if (stamps) add_stamp(steps, layer, 0);
     const int ci = cache_of_layer_[static_cast<size_t>(layer)];
     if (ci >= 0) {
       DevCache& c = *caches_[static_cast<size_t>(ci)];
+      const bool fuse = c.fused && b + 1 < L;
+      const Planes next_act = fuse ? mlp_act_[static_cast<size_t>(b + 1)] : Planes{};
+      if (fuse) {
+        // the next block's FC and this cache's hidden layer in one GEMM over the
+        // tap's rows: the next block's rows for requests that exit here are
+        // computed and dropped by the compaction below
+        const DevFC& nf = mlp_fc_[static_cast<size_t>(b + 1)];
+        gemm_step(act, nf.inp, c.fw, c.fn1 + c.hp, c.fBN, c.fb, shadow ? next_act : c.spec, c.fn1, &c,
+                  2.0 * nf.in * nf.out + 2.0 * static_cast<double>(c.D) * c.h,
+                  (x3 ? 4.0 : 2.0) * (static_cast<double>(nf.inp) + nf.outp) + 4.0 * c.hp);
+        gemm_done[static_cast<size_t>(b + 1)] = 1;
+        if (shadow) tap_step_end_[static_cast<size_t>(layer + 1)] = static_cast<int>(steps.size());
+      }
       TapView tap;
       tap.hi = act.hi;
       tap.lo = act.lo;
@@ -892,26 +963,27 @@ void Engine::build_mlp_steps(std::vector<Step>& steps, bool shadow, bool stamps)
       int* cnt_out = counts + layer;
       ExitParams ex = exit_params(layer, shadow, cur_ids, ids_out, src_out, cnt_out);
       const bool row_append = !shadow && mlp_row_append_ && c.classes <= 32;
+      // the rows that continue: this tap's (compacted into cin) or, fused, the next block's output
+      const Planes csrc = fuse ? c.spec : act;
+      const Planes cdst = fuse ? next_act : mlp_cin_[static_cast<size_t>(b)];
+      const long long crow = fuse ? c.fn1 : f.outp;
       if (row_append) {
-        // each head CTA appends its kept row and copies the activations (no gather launch)
-        const Planes dst = mlp_cin_[static_cast<size_t>(b)];
-        ex.rows_src_hi = act.hi;
-        ex.rows_src_lo = act.lo;
-        ex.rows_dst_hi = dst.hi;
-        ex.rows_dst_lo = dst.lo;
-        ex.row_elems = f.outp;
+        // each head appends its kept row and copies the activations (no gather launch)
+        ex.rows_src_hi = csrc.hi;
+        ex.rows_src_lo = csrc.lo;
+        ex.rows_dst_hi = cdst.hi;
+        ex.rows_dst_lo = cdst.lo;
+        ex.row_elems = crow;
       }
-      add_lookup_steps(steps, c, tap, B, false, false, &ex);
+      add_lookup_steps(steps, c, tap, B, false, false, &ex, fuse);
       if (stamps) add_stamp(steps, layer, 1);
       if (!shadow) {
-        Planes dst = mlp_cin_[static_cast<size_t>(b)];
-        const long long row_elems = f.outp;
         if (!row_append)
-          steps.push_back({[act, dst, row_elems, src_out, cnt_out, B](cudaStream_t s) {
-                             launch_gather_rows(act.hi, act.lo, dst.hi, dst.lo, row_elems, src_out, cnt_out, B, s);
+          steps.push_back({[csrc, cdst, crow, src_out, cnt_out, B](cudaStream_t s) {
+                             launch_gather_rows(csrc.hi, csrc.lo, cdst.hi, cdst.lo, crow, src_out, cnt_out, B, s);
                            },
                            3});
-        cur = dst;
+        cur = cdst;
       } else {
         cur = act;
       }
@@ -1694,6 +1766,11 @@ void Engine::update_variant(const CacheVariant& nv) {
     split_planes(w, hi, lo);
     h2d(c.W1.hi, hi.data(), w.size() * 2);
     if (c.W1.lo) h2d(c.W1.lo, lo.data(), w.size() * 2);
+    if (c.fused) {  // the concatenated copy the serve GEMM reads
+      const size_t e1 = static_cast<size_t>(c.fn1) * c.Dk;
+      ck(cudaMemcpyAsync(c.fw.hi + e1, c.W1.hi, w.size() * 2, cudaMemcpyDeviceToDevice, stream_), "fused W");
+      if (c.fw.lo) ck(cudaMemcpyAsync(c.fw.lo + e1, c.W1.lo, w.size() * 2, cudaMemcpyDeviceToDevice, stream_), "fused W");
+    }
     put_f32(c.b1, PW[0].b, stream_);
     put_f32(c.W2, PW[2].w, stream_);
     put_f32(c.b2, PW[2].b, stream_);

@@ -157,7 +157,7 @@ class Engine {
   std::vector<Step>& steps_mode(int mode);
   void serve_mode(int B, int mode, bool use_graph);
   void add_lookup_steps(std::vector<Step>& steps, DevCache& c, const TapView& tap, int max_rows, bool stage_gather,
-                        bool fused_gap = false, const ExitParams* ex = nullptr);
+                        bool fused_gap = false, const ExitParams* ex = nullptr, bool hidden_done = false);
   ExitParams exit_params(int layer, bool shadow, const int* ids_in, int* ids_out, int* src_rows_out, int* count_out);
   void add_stamp(std::vector<Step>& steps, int layer, int which);
   std::vector<Step>& steps_for(bool shadow);
@@ -244,6 +244,7 @@ class Engine {
   bool wide_lookup_ = true;  // LCB_NO_WIDE_LOOKUP=1: GAP bins + logits GEMM + head as three launches
   bool stacked_ = true;
   int ks_min_steps_ = 0;
+  bool mlp_fuse_hidden_ = true;  // block-MLP FC(h) hidden layer fused into the next block's GEMM (LCB_MLP_FUSE_HIDDEN)
   bool unordered_ids_ = false;
   bool scan_compaction_ = true;  // warp heads: ordered compaction by look-back scan (LCB_SCAN_COMPACTION=0: last-CTA scan)
   unsigned long long* d_scan_ = nullptr;  // [L + 1][kScanMaxCtas] look-back records  // CNN compact mode: atomic survivor appends in the warp heads (LCB_UNORDERED_IDS)

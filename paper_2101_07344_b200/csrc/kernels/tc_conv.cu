@@ -206,7 +206,7 @@ __device__ __forceinline__ bool out_row(const TcConvParams& p, const TileGeom& g
                                         const RowGeom& rg, size_t& obase, int& img, bool& img_ok) {
   if (p.plain) {
     const int grow = x.w0 + row;
-    obase = static_cast<size_t>(grow) * p.Cout;
+    obase = static_cast<size_t>(grow) * (p.out_ld > 0 ? p.out_ld : p.Cout);
     img = grow;
     img_ok = grow < g.count;
     return img_ok;
@@ -1394,9 +1394,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const __grid_const
           }
           continue;
         }
-        if (p.mode == 1) {
+        if (p.mode == 1 || (p.mix_n1 > 0 && x.tn * BN >= p.mix_n1)) {
           if (valid) {
-            float* dst = p.out_f32 + (static_cast<size_t>(x.ks) * p.rows_total + x.w0 + row) * p.Cout + cb;
+            const int f32_ld = p.mix_n1 > 0 ? p.mix_ld : p.Cout;
+            float* dst = p.out_f32 + (static_cast<size_t>(x.ks) * p.rows_total + x.w0 + row) * f32_ld + (cb - p.mix_n1);
 #pragma unroll
             for (int u = 0; u < 2; ++u)
 #pragma unroll

@@ -123,6 +123,13 @@ struct TcConvParams {
   int ksplit;          // mode 1: static split-K factor
   int ks_max;          // mode 0: dynamic split-K upper bound (1 = off)
   int ks_min_steps;  // split-K: at least this many K-steps per split (0 = fill the grid)
+  // plain mode, two outputs from one GEMM over shared rows (block-MLP: the next
+  // block's FC and an FC(h) cache's hidden layer): output columns >= mix_n1 (a
+  // multiple of BN) are written as fp32 to out_f32 [rows][mix_ld] at column
+  // (c - mix_n1), like mode 1; columns < mix_n1 take the mode-0 epilogue with
+  // output rows of out_ld elements. 0 = off.
+  int mix_n1, mix_ld;
+  int out_ld;        // plain mode-0 output row stride in elements (0 = Cout)
   float* ws;           // mode 0 split-K workspace (fp32 partial tiles)
   int* ws_counters;    // per output tile arrival counters (zeroed; reset by the last CTA unless ctr_zero)
   int* ctr_zero;       // nullable: the counter set of the NEXT split-K launch, zeroed by this launch after its
