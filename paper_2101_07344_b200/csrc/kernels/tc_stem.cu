@@ -1,12 +1,18 @@
 // tcgen05 stem convolution over the space-to-depth image X (see tc_stem.cuh).
 //
-// Warp roles (320 threads, one persistent CTA per SM):
+// Warp roles (one persistent CTA per SM; 2 + 8 * SETS warps):
 //   warp 0     : producer (lane 0): resident weights once, then one X slab per
 //                tile (bulk copies, 2 groups x planes) into a ring of stages
 //   warp 1     : MMA issuer (whole warp, elect.sync): k'^2 taps x {1, 2} MMAs (M128, N 64 / stacked 128, K16)
-//   warps 2..9 : epilogue (TMEM lane quadrant warp % 4, column half (warp-2)/4): folded BN, ReLU,
-//                hi/lo split, NHWC store of the valid anchors
+//   warps 2..  : epilogue (TMEM lane quadrant warp % 4, column half ((warp-2)/4) % 2): folded BN, ReLU,
+//                hi/lo split, NHWC store of the valid anchors. SETS = 2: two sets of
+//                8 warps, set s drains TMEM accumulator s (the CTA's tiles 2i + s), so
+//                one set's dependent chain (TMEM load -> exchange barrier -> shuffles
+//                -> stores) overlaps the other's — with one set the epilogue's
+//                latency, not the tensor pipe (44 % busy), set the stem's tile rate
 #include <cfloat>
+#include <cstdlib>
+#include <type_traits>
 
 #include "pdl.cuh"
 #include "sm100_prims.cuh"
@@ -40,10 +46,12 @@ __device__ __forceinline__ uint64_t desc_kmajor_none(uint32_t saddr, uint32_t lb
 
 struct StemSmem {
   int planes, taps, npix_alloc, stages;
-  uint32_t w_bytes, stage_bytes, group_bytes, plane_bytes;
+  uint32_t w_bytes, stage_bytes, group_bytes, plane_bytes, epi_bytes;
 };
 
-__host__ __device__ inline StemSmem stem_smem(int x3, int kk, int Wx) {
+// epilogue scratch: 4 KB store staging per epilogue warp (direct stores), or
+// the hpool path's left-neighbour exchange (4 buffers x 2 halves x 4 quads x 32 floats)
+__host__ __device__ inline StemSmem stem_smem(int x3, int kk, int Wx, int hpool, int sets) {
   StemSmem s;
   s.planes = x3 ? 2 : 1;
   s.taps = kk * kk;
@@ -53,24 +61,25 @@ __host__ __device__ inline StemSmem stem_smem(int x3, int kk, int Wx) {
   s.plane_bytes = 2 * s.group_bytes;
   s.stage_bytes = s.planes * s.plane_bytes;
   s.w_bytes = static_cast<uint32_t>(s.planes * s.taps * kTapBytes);
-  int st = static_cast<int>((220u * 1024u - 34u * 1024u - s.w_bytes) / s.stage_bytes);
+  s.epi_bytes = hpool ? 4096u : static_cast<uint32_t>(sets) * 8u * 4096u;
+  int st = static_cast<int>((220u * 1024u - 2u * 1024u - s.epi_bytes - s.w_bytes) / s.stage_bytes);
   s.stages = st > 8 ? 8 : st;
   return s;
 }
 
 // KK > 0: compile-time taps per dimension (the MMA issue loop fully unrolled); 0: p.kk.
-template <bool X3, int KK>
-__global__ void __launch_bounds__(320, 1) tc_stem_kernel(const __grid_constant__ StemParams p) {
+template <bool X3, int KK, int SETS>
+__global__ void __launch_bounds__(64 + 256 * SETS, 1) tc_stem_kernel(const __grid_constant__ StemParams p) {
   const int kk = KK > 0 ? KK : p.kk;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const StemSmem L = stem_smem(X3 ? 1 : 0, kk, p.Wx);
+  const StemSmem L = stem_smem(X3 ? 1 : 0, kk, p.Wx, p.hpool, SETS);
   const int S = L.stages;
   uint8_t* wsm = smem;
   uint8_t* slabs = smem + L.w_bytes;
-  uint8_t* epi = slabs + S * L.stage_bytes;  // 8 warps x 4 KB staging, then 64 floats of shift
-  float* shift_s = reinterpret_cast<float*>(epi + 8 * 4096);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(epi + 8 * 4096 + 256);
+  uint8_t* epi = slabs + S * L.stage_bytes;  // epilogue scratch, then 64 floats of shift
+  float* shift_s = reinterpret_cast<float*>(epi + L.epi_bytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(epi + L.epi_bytes + 256);
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * 8 + 5);
   const uint32_t full0 = smem_u32(bars);
   const uint32_t empty0 = smem_u32(bars + 8);
@@ -193,15 +202,18 @@ __global__ void __launch_bounds__(320, 1) tc_stem_kernel(const __grid_constant__
       }
     }
   } else {
-    // ------------------------------------------------ epilogue (8 warps: TMEM lane quadrant warp % 4,
-    // column half (warp - 2) / 4)
+    // ------------------------------------------------ epilogue (8 warps per set: TMEM lane quadrant
+    // warp % 4, column half ((warp - 2) / 4) % 2; set (warp - 2) / 8 drains accumulator `set`
+    // when SETS = 2, both accumulators in turn when SETS = 1)
     const int quad = warp & 3;
-    const int q = (warp - 2) >> 2;
+    const int q = ((warp - 2) >> 2) & 1;
+    const int set = (warp - 2) >> 3;
     const int row = quad * 32 + lane;
-    int acc = 0;
+    int acc = SETS == 2 ? set : 0;
     uint32_t acc_phase = 0;
+    int iter = 0;
     const int HoWx = p.Ho * p.Wx;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    for (int t = blockIdx.x + set * gridDim.x; t < total; t += SETS * gridDim.x, ++iter) {
       const int n = t / p.tiles_per_img;
       const int m = (t - n * p.tiles_per_img) * (p.hpool ? p.Wx : kBM) + row;
       const int oh = p.hpool ? t - n * p.tiles_per_img : m / p.Wx;
@@ -228,9 +240,15 @@ __global__ void __launch_bounds__(320, 1) tc_stem_kernel(const __grid_constant__
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty0 + 8 * acc);
-      const int acc_used = acc;
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
+      // exchange buffer: alternates between consecutive tiles of the same warps
+      // (a fast warp's next write must not land on a slow warp's pending read)
+      const int xbuf = SETS == 2 ? set * 2 + (iter & 1) : acc;
+      if (SETS == 2) {
+        acc_phase ^= 1;
+      } else {
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
       if (p.hpool) {
         // folded BN shift + ReLU in fp32; anchors past the row are -inf for the max
         float a[32];
@@ -244,12 +262,12 @@ __global__ void __launch_bounds__(320, 1) tc_stem_kernel(const __grid_constant__
           }
         // left neighbour (ow - 1): the lane below, or lane 31 of the previous
         // quad's warp through shared memory (double-buffered by accumulator)
-        float* xch = reinterpret_cast<float*>(epi) + ((acc_used * 2 + q) * 4) * 32;  // [quad][32 channels]
+        float* xch = reinterpret_cast<float*>(epi) + ((xbuf * 2 + q) * 4) * 32;  // [quad][32 channels]
         if (lane == 31)
 #pragma unroll
           for (int c = 0; c < 32; c += 4)
             *reinterpret_cast<float4*>(xch + quad * 32 + c) = make_float4(a[c], a[c + 1], a[c + 2], a[c + 3]);
-        asm volatile("bar.sync %0, 128;" ::"r"(2 + q) : "memory");  // the four quads of this column half
+        asm volatile("bar.sync %0, 128;" ::"r"(2 + 2 * set + q) : "memory");  // the four quads of this column half
         // lane 0's left neighbours: lane 31 of the previous row block (quad - 1)
         const float* lxch = xch + ((quad + 3) & 3) * 32;
         const bool even = (ow & 1) == 0 && ow < p.Wo;
@@ -506,20 +524,34 @@ void launch_stem_s2d(const float* x, const int* count, int max_n, int C, int H, 
 cudaError_t tc_stem_launch(const StemParams& p, int num_sms, cudaStream_t stream) {
   const bool x3 = p.x_lo != nullptr;
   if (p.hpool && (p.Wx > kBM || p.tiles_per_img != p.Ho || p.Wp != (p.Wo - 1) / 2 + 1)) return cudaErrorInvalidValue;
-  const StemSmem L = stem_smem(x3 ? 1 : 0, p.kk, p.Wx);
+  // LCB_STEM_EPI_SETS=1: one set of 8 epilogue warps (the round-2 layout, kept for A/B)
+  static const int sets = [] {
+    const char* e = std::getenv("LCB_STEM_EPI_SETS");
+    return e && std::atoi(e) == 1 ? 1 : 2;
+  }();
+  const StemSmem L = stem_smem(x3 ? 1 : 0, p.kk, p.Wx, p.hpool, sets);
   if (L.stages < 2) return cudaErrorInvalidValue;
-  const size_t smem = L.w_bytes + static_cast<size_t>(L.stages) * L.stage_bytes + 8 * 4096 + 256 + 256 + 1024;
+  const size_t smem = L.w_bytes + static_cast<size_t>(L.stages) * L.stage_bytes + L.epi_bytes + 256 + 256 + 1024;
   const long long tiles = static_cast<long long>(p.count_static) * p.tiles_per_img;
   if (tiles <= 0) return cudaSuccess;
   const int grid = tiles < num_sms ? static_cast<int>(tiles) : num_sms;
   auto go = [&](auto kern) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    launch_pdl(kern, dim3(grid), dim3(320), smem, stream, p);
+    launch_pdl(kern, dim3(grid), dim3(64 + 256 * sets), smem, stream, p);
     return cudaGetLastError();
   };
-  if (x3) return p.kk == 4 ? go(tc_stem_kernel<true, 4>) : p.kk == 3 ? go(tc_stem_kernel<true, 3>) : go(tc_stem_kernel<true, 0>);
-  return p.kk == 4 ? go(tc_stem_kernel<false, 4>) : p.kk == 3 ? go(tc_stem_kernel<false, 3>) : go(tc_stem_kernel<false, 0>);
+  auto pick = [&](auto x3c, auto setsc) {
+    constexpr bool X = decltype(x3c)::value;
+    constexpr int E = decltype(setsc)::value;
+    return p.kk == 4 ? go(tc_stem_kernel<X, 4, E>) : p.kk == 3 ? go(tc_stem_kernel<X, 3, E>) : go(tc_stem_kernel<X, 0, E>);
+  };
+  using T = std::true_type;
+  using F = std::false_type;
+  using One = std::integral_constant<int, 1>;
+  using Two = std::integral_constant<int, 2>;
+  if (x3) return sets == 2 ? pick(T{}, Two{}) : pick(T{}, One{});
+  return sets == 2 ? pick(F{}, Two{}) : pick(F{}, One{});
 }
 
 }  // namespace lcb
