@@ -631,7 +631,10 @@ __host__ __device__ inline int head_feat_len(const CacheHeadParams& p) {
 }
 __host__ __device__ inline bool head_stages_ws1(const CacheHeadParams& p) {
   // batch-sized launches only: with a handful of rows the copy is not hidden
-  // behind the upstream kernel and the selector reads L2 directly anyway
+  // behind the upstream kernel and the selector reads L2 directly anyway.
+  // rows_total is the engine's capacity (max_batch), fixed when the graph is
+  // captured — not the live count: an engine built for >= 32 rows stages even
+  // when it serves one request (the batch-1 saving needs max_batch < 32)
   return !head_stages_weights(p) && p.classes <= 1024 && p.rows_total >= 32 && !p.row_hi;
 }
 
