@@ -26,6 +26,10 @@ constexpr int kBM = 128;
 constexpr int kCout = 64;
 constexpr int kTapBytes = 2 * kCout * 16;  // [2 groups][64 rows][16 B]
 
+__device__ __forceinline__ float4 u4_as_f4(uint4 u) {
+  return make_float4(__uint_as_float(u.x), __uint_as_float(u.y), __uint_as_float(u.z), __uint_as_float(u.w));
+}
+
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar)
@@ -251,15 +255,24 @@ __global__ void __launch_bounds__(64 + 256 * SETS, 1) tc_stem_kernel(const __gri
       }
       if (p.hpool) {
         // folded BN shift + ReLU in fp32; anchors past the row are -inf for the max
+        // (shared operands through explicit 16-byte ld.shared: the aligned smem
+        // base is an integer round trip, so plain pointers compile to generic
+        // loads, and the MIO queue — shared by 16 epilogue warps' shuffles — is
+        // the epilogue's throttle)
         float a[32];
+        const uint32_t sh_addr = smem_u32(shift_s + q * 32);
 #pragma unroll
-        for (int u = 0; u < 2; ++u)
+        for (int u4 = 0; u4 < 8; ++u4) {
+          const float4 s4 = u4_as_f4(ld_shared_v4(sh_addr + u4 * 16));
+          const float sv[4] = {s4.x, s4.y, s4.z, s4.w};
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            float z = v[u][e] + shift_s[q * 32 + u * 16 + e];
+          for (int k = 0; k < 4; ++k) {
+            const int i = u4 * 4 + k;
+            float z = v[i >> 4][i & 15] + sv[k];
             if (p.relu) z = z > 0.0f ? z : 0.0f;
-            a[u * 16 + e] = valid ? z : -FLT_MAX;
+            a[i] = valid ? z : -FLT_MAX;
           }
+        }
         // left neighbour (ow - 1): the lane below, or lane 31 of the previous
         // quad's warp through shared memory (double-buffered by accumulator)
         float* xch = reinterpret_cast<float*>(epi) + ((xbuf * 2 + q) * 4) * 32;  // [quad][32 channels]
@@ -269,18 +282,25 @@ __global__ void __launch_bounds__(64 + 256 * SETS, 1) tc_stem_kernel(const __gri
             *reinterpret_cast<float4*>(xch + quad * 32 + c) = make_float4(a[c], a[c + 1], a[c + 2], a[c + 3]);
         asm volatile("bar.sync %0, 128;" ::"r"(2 + 2 * set + q) : "memory");  // the four quads of this column half
         // lane 0's left neighbours: lane 31 of the previous row block (quad - 1)
-        const float* lxch = xch + ((quad + 3) & 3) * 32;
+        const uint32_t lx_addr = smem_u32(xch + ((quad + 3) & 3) * 32);
         const bool even = (ow & 1) == 0 && ow < p.Wo;
         uint4 hi[4], lo[4];
         __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(hi);
         __nv_bfloat162* l2 = reinterpret_cast<__nv_bfloat162*>(lo);
 #pragma unroll
         for (int c = 0; c < 32; c += 2) {
+          float lv[2] = {-FLT_MAX, -FLT_MAX};
+          if (lane == 0 && quad != 0) {  // 8 bytes of lane 31's row per channel pair
+            uint32_t x0, x1;
+            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(x0), "=r"(x1) : "r"(lx_addr + c * 4));
+            lv[0] = __uint_as_float(x0);
+            lv[1] = __uint_as_float(x1);
+          }
           float mx[2];
 #pragma unroll
           for (int d = 0; d < 2; ++d) {
             float left = __shfl_up_sync(0xffffffffu, a[c + d], 1);
-            if (lane == 0) left = quad == 0 ? -FLT_MAX : lxch[c + d];
+            if (lane == 0) left = lv[d];
             const float right = __shfl_down_sync(0xffffffffu, a[c + d], 1);  // even lanes: always in-warp
             // first maximum in (ow - 1, ow, ow + 1) order
             float m = left;
