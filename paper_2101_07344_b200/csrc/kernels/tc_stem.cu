@@ -283,45 +283,55 @@ __global__ void __launch_bounds__(64 + 256 * SETS, 1) tc_stem_kernel(const __gri
         asm volatile("bar.sync %0, 128;" ::"r"(2 + 2 * set + q) : "memory");  // the four quads of this column half
         // lane 0's left neighbours: lane 31 of the previous row block (quad - 1)
         const uint32_t lx_addr = smem_u32(xch + ((quad + 3) & 3) * 32);
-        const bool even = (ow & 1) == 0 && ow < p.Wo;
-        uint4 hi[4], lo[4];
+        // lane pairs (ow, ow + 1), ow even, share the pooled pixel ow: the even lane
+        // writes its channels [0, 16), the odd lane [16, 32) — 48 shuffles per lane
+        // instead of 64 (one exchange inside the pair, the left neighbour's two halves)
+        const int odd = lane & 1;
+        const int pw = ow - odd;  // the pooled anchor (even)
+        const int src_l = (odd ? lane - 2 : lane - 1) & 31;
+        uint4 hi[2], lo[2];
         __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(hi);
         __nv_bfloat162* l2 = reinterpret_cast<__nv_bfloat162*>(lo);
 #pragma unroll
-        for (int c = 0; c < 32; c += 2) {
+        for (int k = 0; k < 16; k += 2) {
           float lv[2] = {-FLT_MAX, -FLT_MAX};
-          if (lane == 0 && quad != 0) {  // 8 bytes of lane 31's row per channel pair
+          if (lane < 2 && quad != 0) {  // lane 31 of the previous row block, this lane's half
             uint32_t x0, x1;
-            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(x0), "=r"(x1) : "r"(lx_addr + c * 4));
+            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(x0), "=r"(x1) : "r"(lx_addr + (odd * 16 + k) * 4));
             lv[0] = __uint_as_float(x0);
             lv[1] = __uint_as_float(x1);
           }
           float mx[2];
 #pragma unroll
           for (int d = 0; d < 2; ++d) {
-            float left = __shfl_up_sync(0xffffffffu, a[c + d], 1);
-            if (lane == 0) left = lv[d];
-            const float right = __shfl_down_sync(0xffffffffu, a[c + d], 1);  // even lanes: always in-warp
-            // first maximum in (ow - 1, ow, ow + 1) order
+            const int c = k + d;
+            const float mine = odd ? a[16 + c] : a[c];
+            // even lane: a[ow + 1][c]; odd lane: a[ow - 1][16 + c]
+            const float pair = __shfl_xor_sync(0xffffffffu, odd ? a[c] : a[16 + c], 1);
+            const float l0 = __shfl_sync(0xffffffffu, a[c], src_l);
+            const float l1 = __shfl_sync(0xffffffffu, a[16 + c], src_l);
+            const float left = lane < 2 ? lv[d] : (odd ? l1 : l0);
+            // first maximum in (pw - 1, pw, pw + 1) order
+            const float mid = odd ? pair : mine, right = odd ? mine : pair;
             float m = left;
-            if (a[c + d] > m) m = a[c + d];
+            if (mid > m) m = mid;
             if (right > m) m = right;
             mx[d] = m;
           }
           const __nv_bfloat162 hh = __floats2bfloat162_rn(mx[0], mx[1]);
-          h2[c / 2] = hh;
+          h2[k / 2] = hh;
           const float2 hf = __bfloat1622float2(hh);
-          l2[c / 2] = __floats2bfloat162_rn(mx[0] - hf.x, mx[1] - hf.y);
+          l2[k / 2] = __floats2bfloat162_rn(mx[0] - hf.x, mx[1] - hf.y);
         }
-        if (even && m < HoWx) {
-          const size_t ob = ((static_cast<size_t>(n) * p.Ho + oh) * p.Wp + (ow >> 1)) * kCout + q * 32;
+        if (pw < p.Wo && m - odd < HoWx) {
+          const size_t ob = ((static_cast<size_t>(n) * p.Ho + oh) * p.Wp + (pw >> 1)) * kCout + q * 32 + odd * 16;
           uint4* oh4 = reinterpret_cast<uint4*>(p.out_hi + ob);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) oh4[i] = hi[i];
+          oh4[0] = hi[0];
+          oh4[1] = hi[1];
           if (X3 && p.out_lo) {
             uint4* ol4 = reinterpret_cast<uint4*>(p.out_lo + ob);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) ol4[i] = lo[i];
+            ol4[0] = lo[0];
+            ol4[1] = lo[1];
           }
         }
         continue;
